@@ -1,0 +1,78 @@
+"""Seeded synthetic input generators shared by the oracle side and the GPU side.
+
+This module holds NO arithmetic of the method (no GEMM, reduction, math
+function or hash): it only turns (seed, index) into bits.  Both sides of every
+parity test receive the SAME arrays from here, so nothing either side computes
+can leak into the other's inputs.
+
+Generator: SplitMix64, counter based -- element i of stream `seed` is
+splitmix64(seed + (i+1) * 0x9E3779B97F4A7C15).  Floats are drawn on a 24-bit
+grid, u = (x >> 40) * 2^-23 - 1 in [-1, 1), so every draw is exact in binary32.
+Integers in [0, n) use Lemire's multiply-shift on the top 32 bits.
+
+Workload recipes are stated next to each helper.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+_GOLDEN = np.uint64(0x9E3779B97F4A7C15)
+_M1 = np.uint64(0xBF58476D1CE4E5B9)
+_M2 = np.uint64(0x94D049BB133111EB)
+
+
+def splitmix64(seed: int, n: int, offset: int = 0) -> np.ndarray:
+    """n consecutive SplitMix64 outputs of stream `seed`, starting at counter `offset`."""
+    with np.errstate(over="ignore"):
+        i = np.arange(offset + 1, offset + n + 1, dtype=np.uint64)
+        z = np.uint64(seed & 0xFFFFFFFFFFFFFFFF) + i * _GOLDEN
+        z = (z ^ (z >> np.uint64(30))) * _M1
+        z = (z ^ (z >> np.uint64(27))) * _M2
+        z = z ^ (z >> np.uint64(31))
+    return z
+
+
+def uniform(seed: int, shape, scale: float = 1.0) -> np.ndarray:
+    """float32 U[-1, 1) on a 24-bit grid (exact), optionally times `scale`
+    (the product is rounded to binary32 once, here, before either side sees it)."""
+    shape = (shape,) if isinstance(shape, int) else tuple(shape)
+    n = int(np.prod(shape)) if shape else 1
+    k = (splitmix64(seed, n) >> np.uint64(40)).astype(np.float64)
+    x = (k * (2.0 ** -23) - 1.0).astype(np.float32)
+    if scale != 1.0:
+        x = (x.astype(np.float64) * scale).astype(np.float32)
+    return x.reshape(shape)
+
+
+def integers(seed: int, n: int, hi: int) -> np.ndarray:
+    """int32 uniform in [0, hi) by Lemire multiply-shift of the top 32 bits."""
+    top = (splitmix64(seed, n) >> np.uint64(32)).astype(np.uint64)
+    return ((top * np.uint64(hi)) >> np.uint64(32)).astype(np.int32)
+
+
+def small_ints(seed: int, shape, lo: int = -8, hi: int = 8) -> np.ndarray:
+    """float32 integers in [lo, hi) -- for GEMMs whose every partial sum is exact."""
+    shape = (shape,) if isinstance(shape, int) else tuple(shape)
+    n = int(np.prod(shape))
+    return (integers(seed, n, hi - lo).astype(np.int64) + lo).astype(np.float32).reshape(shape)
+
+
+def seed_for(*labels) -> int:
+    """Stable 64-bit stream id from labels (FNV-1a over their text)."""
+    h = 0xCBF29CE484222325
+    for ch in "/".join(str(x) for x in labels).encode():
+        h ^= ch
+        h = (h * 0x100000001B3) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+# ----------------------------------------------------------------- recipes
+def gemm_inputs(n_or_mnk, tag: str = "gemm"):
+    """Config 1/2: A, B ~ U[-1,1) (24-bit grid).  Returns (A[M,K], B[K,N])."""
+    if isinstance(n_or_mnk, int):
+        M = N = K = n_or_mnk
+    else:
+        M, N, K = n_or_mnk
+    A = uniform(seed_for(tag, "A", M, N, K), (M, K))
+    B = uniform(seed_for(tag, "B", M, N, K), (K, N))
+    return A, B
