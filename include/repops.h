@@ -1,0 +1,236 @@
+/*
+ * repops.h -- C ABI of the B200-native RepOps / Verde hot path (librepops.so).
+ *
+ * Paper: "Verde: Verification via Refereed Delegation for Machine Learning
+ * Programs" (arXiv 2502.19405).  Citations "P:n" are lines of the paper text
+ * (PAPER.md); "Rk" are the readings listed in DESIGN.md §3.
+ *
+ * Conventions (all entry points):
+ *   - Return an int status: REPOPS_OK (0) or a REPOPS_E* code.  The message of
+ *     the last failure on the calling thread is repops_last_error().  No C++
+ *     exception crosses this boundary.
+ *   - Tensor pointers are DEVICE pointers owned by the caller; the library
+ *     allocates nothing persistent and never frees caller memory.  Host
+ *     pointers are marked (host) and are only borrowed for the call.
+ *   - Layout is row-major with an explicit leading dimension (elements).
+ *     Alignment is never required for correctness; aligned rows take 128-bit
+ *     paths with identical bits.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Device entry
+ *     points only enqueue work and return without synchronising.
+ *   - Determinism contract: output bits are a pure function of the input
+ *     bits, the shapes and the fixed constants of DESIGN.md §3 -- never of the
+ *     stream, the tile configuration, the SM count or the number of GPUs.
+ *   - All floating point is IEEE-754 binary32, round to nearest even, no
+ *     flush-to-zero, no contraction (explicit fma only where written).  A NaN
+ *     result is always written as the canonical 0x7FC00000 (R10).
+ *   - NaN / Inf inputs are data, not errors.
+ */
+#ifndef REPOPS_H
+#define REPOPS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define REPOPS_ABI_VERSION 1
+
+enum repops_status {
+    REPOPS_OK = 0,
+    REPOPS_EINVAL = 1,   /* null pointer, negative size, ld < row length, bad enum */
+    REPOPS_ESHAPE = 2,   /* shapes inconsistent (e.g. causal with rows % cols != 0) */
+    REPOPS_ECUDA = 3,    /* a CUDA runtime call or kernel launch failed */
+    REPOPS_ENOSPACE = 4  /* caller workspace too small */
+};
+
+enum repops_epilogue {
+    REPOPS_EPI_NONE = 0,  /* C = acc                      */
+    REPOPS_EPI_BIAS = 1,  /* C = fadd(acc, bias[j])       */
+    REPOPS_EPI_SCALE = 2  /* C = fmul(acc, scale)         */
+};
+
+enum verde_dtype { VERDE_F32 = 1, VERDE_I32 = 2, VERDE_U8 = 3 };
+
+int repops_abi_version(void);
+const char *repops_last_error(void);
+
+/* ------------------------------------------------------------------ GEMM
+ * R-GEMM, PAPER.md P:598-609 (Sec. 3.2 listing): for every (i, j)
+ *     acc = +0;  for k = 0 .. K-1 ascending: acc = fma(opA(i,k), opB(k,j), acc)
+ *     C[i*ldc + j] = epi(acc)
+ * opA(i,k) = transA ? A[k*lda + i] : A[i*lda + k]   (A is M x K, or K x M if transA)
+ * opB(k,j) = transB ? B[j*ldb + k] : B[k*ldb + j]   (B is K x N, or N x K if transB)
+ * K is never split; only M/N are tiled.  K == 0 gives C = epi(+0).
+ * bias: device, N floats (epi == BIAS); scale: host float (epi == SCALE).
+ * Errors: EINVAL for M,N,K < 0, null pointers with nonzero extent, lda/ldb/ldc
+ * smaller than the stored row length, unknown epi. */
+int repops_gemm(int64_t M, int64_t N, int64_t K,
+                const float *A, int64_t lda, int transA,
+                const float *B, int64_t ldb, int transB,
+                int epi, const float *bias, float scale,
+                float *C, int64_t ldc, void *stream);
+
+/* Batched R-GEMM over a two-level batch (b0 < batch0, b1 < batch1), e.g.
+ * (sequence, head) for attention.  Problem (b0, b1) uses
+ *   A + b0*sA0 + b1*sA1,  B + b0*sB0 + b1*sB1,  C + b0*sC0 + b1*sC1   (elements).
+ * Every problem is an independent R-GEMM with the same M, N, K, ld*, trans*. */
+int repops_gemm_strided_batched(int64_t M, int64_t N, int64_t K,
+                                const float *A, int64_t lda, int transA, int64_t sA0, int64_t sA1,
+                                const float *B, int64_t ldb, int transB, int64_t sB0, int64_t sB1,
+                                int epi, const float *bias, float scale,
+                                float *C, int64_t ldc, int64_t sC0, int64_t sC1,
+                                int64_t batch0, int64_t batch1, void *stream);
+
+/* ------------------------------------------------------------------ reductions
+ * R-CSUM (R4): n <= 4096: 128 slots from +0, x[i] into slot i%128
+ * ascending, then TREE128 (h = 64..1: p[s] = p[s] + p[s+h]); longer rows are
+ * the CSUM of their 4096-element tile CSUMs.  Rows up to 4096*4096 elements.
+ * out: device, rows floats. */
+int repops_sum_rows(const float *x, int64_t rows, int64_t cols, int64_t ld, float *out, void *stream);
+
+/* R-SEQ (R4): rows split into nseg equal contiguous segments (rows % nseg == 0);
+ * out[s*cols + j] = fold over the segment's rows ascending of (acc + x[r*ld+j]), acc = +0. */
+int repops_sum_cols_seq(const float *x, int64_t rows, int64_t cols, int64_t ld, int64_t nseg,
+                        float *out, void *stream);
+
+/* R-TREE_S (R14): out = T(parts[0..nparts)), T(lo,1) = parts[lo],
+ * T(lo,n) = fadd(T(lo,n/2), T(lo+n/2,n/2)), elementwise over n floats.
+ * parts: HOST array of nparts DEVICE pointers; nparts in {1,2,4,8,16}. */
+int repops_tree_sum(const float *const *parts, int nparts, int64_t n, float *out, void *stream);
+
+/* ------------------------------------------------------------------ row operators
+ * R-SOFTMAX (R7): per row, m = max of the valid non-NaN entries (+0 if zero);
+ * e_i = exp(x_i - m); s = CSUM(e); y_i = e_i * (1/s).  causal != 0 requires
+ * rows % cols == 0; row r keeps (r mod cols)+1 entries and writes +0 elsewhere.
+ * y may alias x when ldy == ldx. */
+int repops_softmax(const float *x, int64_t rows, int64_t cols, int64_t ldx, int causal,
+                   float *y, int64_t ldy, void *stream);
+
+/* R-SOFTMAX-BWD: c = CDOT(y, dy) over the full row; dx_i = fmul(fmul(y_i, dy_i - c), scale).
+ * dx may alias dy. */
+int repops_softmax_backward(const float *y, int64_t ldy, const float *dy, int64_t lddy,
+                            int64_t rows, int64_t cols, float scale, float *dx, int64_t lddx,
+                            void *stream);
+
+/* R-LN (P:834-835 lists LayerNorm among RepOps operators; R8): contiguous rows.
+ * mu = CSUM(x)/n; d = x - mu; var = CDOT(d,d)/n; rstd = 1/sqrt(var + eps);
+ * y = fma(d*rstd, gamma, beta).  mean / rstd (rows floats) are optional (NULL). */
+int repops_layernorm(const float *x, const float *gamma, const float *beta, int64_t rows,
+                     int64_t cols, float eps, float *y, float *mean, float *rstd, void *stream);
+
+/* LN backward, row part: xh = (x - mean)*rstd; g = dy*gamma; a = CSUM(g)/n;
+ * b = CDOT(g, xh)/n; dx = ((g - a) - xh*b)*rstd; if dres != NULL: dx = dres + dx. */
+int repops_layernorm_backward(const float *dy, const float *x, const float *gamma,
+                              const float *mean, const float *rstd, const float *dres,
+                              int64_t rows, int64_t cols, float *dx, void *stream);
+
+/* LN parameter gradients per segment (R-SEQ): dgamma[s][j] = fold fma(dy, xh, acc),
+ * dbeta[s][j] = fold (acc + dy); outputs nseg x cols. */
+int repops_layernorm_backward_params(const float *dy, const float *x, const float *mean,
+                                     const float *rstd, int64_t rows, int64_t cols, int64_t nseg,
+                                     float *dgamma, float *dbeta, void *stream);
+
+/* R-CE: per row of V logits: m = max; s = CSUM(exp(x - m));
+ * loss[r] = (m + log s) - x[label];  dlogits_i = ((exp(x_i - m)*(1/s)) - [i == label]) * scale.
+ * labels: device int32[rows], each in [0, V).  loss / dlogits optional (NULL);
+ * dlogits may alias logits (ldd == ld). */
+int repops_cross_entropy(const float *logits, int64_t rows, int64_t V, int64_t ld,
+                         const int32_t *labels, float scale, float *loss, float *dlogits,
+                         int64_t ldd, void *stream);
+
+/* ------------------------------------------------------------------ elementwise
+ * Software math (R5/R6): fixed IEEE-RN op chains. */
+int repops_exp(const float *x, int64_t n, float *y, void *stream);
+int repops_log(const float *x, int64_t n, float *y, void *stream);
+int repops_tanh(const float *x, int64_t n, float *y, void *stream);
+int repops_rsqrt(const float *x, int64_t n, float *y, void *stream);   /* fdiv(1, fsqrt(x)) */
+int repops_gelu(const float *x, int64_t n, float *y, void *stream);    /* tanh form, R13 */
+int repops_gelu_backward(const float *x, const float *dy, int64_t n, float *dx, void *stream);
+int repops_add(const float *a, const float *b, int64_t n, float *y, void *stream);
+
+/* R-EMB forward: x0[t][c] = fadd(wte[tok[t]][c], wpe[t mod T][c]); tok device int32. */
+int repops_embedding(const int32_t *tok, int64_t ntok, int64_t T, const float *wte,
+                     const float *wpe, int64_t C, float *x0, void *stream);
+/* R-EMB backward for one data-parallel shard, accumulated INTO dwte (and dwpe):
+ * dwte[v][c] = fadd(dwte[v][c], fold over t ascending with tok[t]==v of (acc + dx0[t][c]));
+ * dwpe[p][c] = fadd(dwpe[p][c], fold over t ascending with t mod T == p).  Untouched
+ * rows keep their bits.  dwpe may be NULL. */
+int repops_embedding_backward(const int32_t *tok, int64_t ntok, int64_t T, const float *dx0,
+                              int64_t C, float *dwte, float *dwpe, void *stream);
+
+/* R-ADAMW (R15): in place on p, m, v (n floats), g read-only.  bc1 = 1 - b1^step,
+ * bc2 = 1 - b2^step with b^step by iterated binary32 multiplication (host side). */
+int repops_adamw(float *p, const float *g, float *m, float *v, int64_t n, int64_t step,
+                 float lr, float b1, float b2, float eps, float wd, int decay, void *stream);
+
+/* Fault injection (Verde config 5): flips bit `bit` (0..31) of 32-bit element
+ * `elem` of the device buffer `data`. */
+int repops_flip_bit(void *data, int64_t elem, int bit, void *stream);
+
+/* ------------------------------------------------------------------ Verde commitments
+ * R-TCOMMIT (P:240-244 SHA-256 commitment; P:393-406 tensor hashes in the node;
+ * R11): data bytes (little-endian image) are cut into 4096-byte chunks (last
+ * one short); leaf_i = SHA-256(0x00 || chunk_i); data_root = RFC 6962 MTH
+ * (SHA-256() for 0 bytes); digest = SHA-256(0x54 || u8 dtype || u64le rank ||
+ * u64le dims[rank] || u64le nbytes || u32le 4096 || data_root).            */
+typedef struct {
+    const void *data;   /* device */
+    int64_t nbytes;
+    int32_t dtype;      /* verde_dtype */
+    int32_t rank;       /* 0..8 */
+    int64_t dims[8];
+    uint8_t *digest;    /* device, 32 bytes */
+} verde_tensor_desc;
+
+/* Workspace (device bytes) needed to commit the given tensors in one call. */
+int64_t verde_commit_workspace_bytes(const verde_tensor_desc *descs /* host */, int n);
+/* Commit n tensors in one batched launch sequence; digests are written to
+ * device memory asynchronously.  ws: device workspace >= the size above. */
+int verde_commit_tensors(const verde_tensor_desc *descs /* host */, int n, void *ws,
+                         int64_t ws_bytes, void *stream);
+/* Single-tensor convenience form (dims: host int64[rank]). */
+int verde_commit_tensor(const void *data, int64_t nbytes, int dtype, int rank, const int64_t *dims,
+                        uint8_t *digest32, void *ws, int64_t ws_bytes, void *stream);
+
+/* R-MERKLE (Fig. 2; R12): RFC 6962 MTH over n 32-byte entries (host),
+ * root32 (host).  n == 0 -> REPOPS_EINVAL. */
+int verde_merkle_root(const uint8_t *leaves, int64_t n, uint8_t *root32);
+
+/* SHA-256 of a host buffer (host). */
+int verde_sha256(const uint8_t *data, int64_t n, uint8_t *out32);
+
+/* R-NODE (the AugmentedCGNode box; R13 in DESIGN.md): the node digest
+ * SHA-256( 0x4E || u32 index || u16 op || u32 shard || u32 n_attr ||
+ *          (u32 key, u64 value)*n_attr || u32 n_in || (u32 src_node, u32 src_slot)*n_in ||
+ *          u32 n_out_nodes || (u32 dst_node)*n_out_nodes || u32 n_out ||
+ *          in_digests (32*n_in) || out_digests (32*n_out) ), little-endian. All host. */
+typedef struct {
+    uint32_t index;
+    uint16_t op;
+    uint32_t shard;
+    int32_t n_attr;
+    const uint32_t *attr_keys;   /* ascending */
+    const uint64_t *attr_vals;
+    int32_t n_in;
+    const uint32_t *in_src_node;
+    const uint32_t *in_src_slot;
+    const uint8_t *in_digests;   /* 32 * n_in */
+    int32_t n_dst;
+    const uint32_t *dst_nodes;
+    int32_t n_out;
+    const uint8_t *out_digests;  /* 32 * n_out */
+} verde_node;
+
+int verde_node_digest(const verde_node *node, uint8_t *out32);
+
+/* First index d with seq0[d] != seq1[d] over n 32-byte digests (Alg. 2 line 8,
+ * P:429-430), found by descending the two RFC 6962 trees from the roots
+ * (O(log n) subtree comparisons).  *d_out = -1 if the sequences are equal. */
+int verde_first_divergence(const uint8_t *seq0, const uint8_t *seq1, int64_t n, int64_t *d_out,
+                           int64_t *rounds_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* REPOPS_H */

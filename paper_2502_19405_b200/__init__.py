@@ -1,0 +1,372 @@
+"""B200-native RepOps / Verde hot path (arXiv 2502.19405).
+
+Thin Python binding over librepops.so (include/repops.h).  Each function has
+the name of the C entry point it calls and only marshals arguments: torch
+supplies device memory and the current CUDA stream, every arithmetic step runs
+in the library's CUDA kernels.  Functions take torch CUDA tensors (float32
+unless stated) and return the output tensor(s).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from ._lib import Node, RepopsError, TensorDesc, check, header_symbols, lib
+
+EPI_NONE, EPI_BIAS, EPI_SCALE = 0, 1, 2
+F32, I32, U8 = 1, 2, 3
+_DT = {torch.float32: F32, torch.int32: I32, torch.uint8: U8}
+
+__all__ = [
+    "repops_gemm", "repops_gemm_strided_batched", "repops_sum_rows", "repops_sum_cols_seq", "repops_tree_sum",
+    "repops_softmax", "repops_softmax_backward", "repops_layernorm", "repops_layernorm_backward",
+    "repops_layernorm_backward_params", "repops_cross_entropy", "repops_exp", "repops_log", "repops_tanh",
+    "repops_rsqrt", "repops_gelu", "repops_gelu_backward", "repops_add", "repops_embedding",
+    "repops_embedding_backward", "repops_adamw", "repops_flip_bit", "verde_commit_tensor",
+    "verde_commit_tensors", "verde_merkle_root", "verde_sha256", "verde_node_digest",
+    "verde_first_divergence", "CommitWorkspace", "RepopsError", "header_symbols", "lib",
+]
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _p(t) -> int | None:
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise RepopsError("tensor must live on a CUDA device")
+    return t.data_ptr()
+
+
+def _f32(t, name):
+    if t.dtype != torch.float32 or not t.is_cuda:
+        raise RepopsError(f"{name}: expected a float32 CUDA tensor, got {t.dtype} on {t.device}")
+    return t
+
+
+def _ld(t) -> int:
+    if t.dim() != 2 or t.stride(1) != 1:
+        raise RepopsError("expected a 2-D tensor with unit column stride")
+    return t.stride(0)
+
+
+# ------------------------------------------------------------------ GEMM
+def repops_gemm(A, B, transA=False, transB=False, epi=EPI_NONE, bias=None, scale=1.0, out=None, stream=None,
+                cfg=None):
+    """R-GEMM.  A: (M,K) or (K,M) if transA; B: (K,N) or (N,K) if transB."""
+    _f32(A, "A"), _f32(B, "B")
+    M = A.shape[1] if transA else A.shape[0]
+    K = A.shape[0] if transA else A.shape[1]
+    N = B.shape[0] if transB else B.shape[1]
+    Kb = B.shape[1] if transB else B.shape[0]
+    if Kb != K:
+        raise RepopsError(f"repops_gemm: inner dimensions differ ({K} vs {Kb})")
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.float32, device=A.device)
+    args = (M, N, K, _p(A), _ld(A), int(bool(transA)), _p(B), _ld(B), int(bool(transB)), int(epi), _p(bias),
+            float(scale), _p(out), _ld(out), _stream(stream))
+    if cfg is None:
+        check(lib().repops_gemm(*args), "repops_gemm")
+    else:
+        check(lib().repops_gemm_cfg(*args, int(cfg)), "repops_gemm_cfg")
+    return out
+
+
+def repops_gemm_strided_batched(A, B, C_out, M, N, K, lda, ldb, ldc, sA, sB, sC, batch, transA=False,
+                                transB=False, epi=EPI_NONE, bias=None, scale=1.0, offA=0, offB=0, offC=0,
+                                stream=None):
+    """Two-level strided batch of R-GEMMs.  sA/sB/sC = (outer, inner) element strides,
+    batch = (outer, inner) counts; off* are element offsets into the storage of A/B/C."""
+    _f32(A, "A"), _f32(B, "B"), _f32(C_out, "C")
+    check(lib().repops_gemm_strided_batched(
+        M, N, K, _p(A) + 4 * offA, lda, int(bool(transA)), sA[0], sA[1], _p(B) + 4 * offB, ldb,
+        int(bool(transB)), sB[0], sB[1], int(epi), _p(bias), float(scale), _p(C_out) + 4 * offC, ldc, sC[0],
+        sC[1], batch[0], batch[1], _stream(stream)), "repops_gemm_strided_batched")
+    return C_out
+
+
+# ------------------------------------------------------------------ reductions
+def repops_sum_rows(x, out=None, stream=None):
+    _f32(x, "x")
+    if out is None:
+        out = torch.empty(x.shape[0], dtype=torch.float32, device=x.device)
+    check(lib().repops_sum_rows(_p(x), x.shape[0], x.shape[1], _ld(x), _p(out), _stream(stream)), "repops_sum_rows")
+    return out
+
+
+def repops_sum_cols_seq(x, nseg=1, out=None, stream=None):
+    _f32(x, "x")
+    if out is None:
+        out = torch.empty((nseg, x.shape[1]), dtype=torch.float32, device=x.device)
+    check(lib().repops_sum_cols_seq(_p(x), x.shape[0], x.shape[1], _ld(x), nseg, _p(out), _stream(stream)),
+          "repops_sum_cols_seq")
+    return out
+
+
+def repops_tree_sum(parts, out=None, stream=None):
+    n = parts[0].numel()
+    for q in parts:
+        _f32(q, "part")
+        if q.numel() != n or not q.is_contiguous():
+            raise RepopsError("repops_tree_sum: parts must be contiguous with equal sizes")
+    if out is None:
+        out = torch.empty_like(parts[0])
+    arr = (C.c_void_p * len(parts))(*[q.data_ptr() for q in parts])
+    check(lib().repops_tree_sum(arr, len(parts), n, _p(out), _stream(stream)), "repops_tree_sum")
+    return out
+
+
+# ------------------------------------------------------------------ row operators
+def repops_softmax(x, causal=False, out=None, stream=None):
+    _f32(x, "x")
+    if out is None:
+        out = torch.empty_like(x)
+    check(lib().repops_softmax(_p(x), x.shape[0], x.shape[1], _ld(x), int(bool(causal)), _p(out), _ld(out),
+                               _stream(stream)), "repops_softmax")
+    return out
+
+
+def repops_softmax_backward(y, dy, scale=1.0, out=None, stream=None):
+    _f32(y, "y"), _f32(dy, "dy")
+    if out is None:
+        out = torch.empty_like(y)
+    check(lib().repops_softmax_backward(_p(y), _ld(y), _p(dy), _ld(dy), y.shape[0], y.shape[1], float(scale),
+                                        _p(out), _ld(out), _stream(stream)), "repops_softmax_backward")
+    return out
+
+
+def _contig(t, name):
+    _f32(t, name)
+    if not t.is_contiguous():
+        raise RepopsError(f"{name} must be contiguous")
+    return t
+
+
+def repops_layernorm(x, gamma, beta, eps=1e-5, out=None, mean=None, rstd=None, stream=None):
+    _contig(x, "x")
+    rows, cols = x.shape
+    if out is None:
+        out = torch.empty_like(x)
+    if mean is None:
+        mean = torch.empty(rows, dtype=torch.float32, device=x.device)
+    if rstd is None:
+        rstd = torch.empty(rows, dtype=torch.float32, device=x.device)
+    check(lib().repops_layernorm(_p(x), _p(gamma), _p(beta), rows, cols, float(eps), _p(out), _p(mean), _p(rstd),
+                                 _stream(stream)), "repops_layernorm")
+    return out, mean, rstd
+
+
+def repops_layernorm_backward(dy, x, gamma, mean, rstd, dres=None, out=None, stream=None):
+    _contig(dy, "dy"), _contig(x, "x")
+    rows, cols = x.shape
+    if out is None:
+        out = torch.empty_like(x)
+    check(lib().repops_layernorm_backward(_p(dy), _p(x), _p(gamma), _p(mean), _p(rstd), _p(dres), rows, cols,
+                                          _p(out), _stream(stream)), "repops_layernorm_backward")
+    return out
+
+
+def repops_layernorm_backward_params(dy, x, mean, rstd, nseg=1, dgamma=None, dbeta=None, stream=None):
+    rows, cols = x.shape
+    if dgamma is None:
+        dgamma = torch.empty((nseg, cols), dtype=torch.float32, device=x.device)
+    if dbeta is None:
+        dbeta = torch.empty((nseg, cols), dtype=torch.float32, device=x.device)
+    check(lib().repops_layernorm_backward_params(_p(dy), _p(x), _p(mean), _p(rstd), rows, cols, nseg, _p(dgamma),
+                                                 _p(dbeta), _stream(stream)), "repops_layernorm_backward_params")
+    return dgamma, dbeta
+
+
+def repops_cross_entropy(logits, labels, scale=1.0, loss=None, dlogits=None, want_grad=True, V=None, stream=None):
+    """logits: (rows, ld) with the first V columns valid (V defaults to all)."""
+    _f32(logits, "logits")
+    rows = logits.shape[0]
+    V = logits.shape[1] if V is None else V
+    if labels.dtype != torch.int32:
+        raise RepopsError("labels must be int32")
+    if loss is None:
+        loss = torch.empty(rows, dtype=torch.float32, device=logits.device)
+    if want_grad and dlogits is None:
+        dlogits = torch.empty_like(logits)
+    check(lib().repops_cross_entropy(_p(logits), rows, V, _ld(logits), _p(labels), float(scale), _p(loss),
+                                     _p(dlogits) if want_grad else None,
+                                     _ld(dlogits) if want_grad else V, _stream(stream)), "repops_cross_entropy")
+    return loss, dlogits
+
+
+# ------------------------------------------------------------------ elementwise
+def _unary(name, x, out, stream):
+    _contig(x, "x")
+    if out is None:
+        out = torch.empty_like(x)
+    check(getattr(lib(), name)(_p(x), x.numel(), _p(out), _stream(stream)), name)
+    return out
+
+
+def repops_exp(x, out=None, stream=None):
+    return _unary("repops_exp", x, out, stream)
+
+
+def repops_log(x, out=None, stream=None):
+    return _unary("repops_log", x, out, stream)
+
+
+def repops_tanh(x, out=None, stream=None):
+    return _unary("repops_tanh", x, out, stream)
+
+
+def repops_rsqrt(x, out=None, stream=None):
+    return _unary("repops_rsqrt", x, out, stream)
+
+
+def repops_gelu(x, out=None, stream=None):
+    return _unary("repops_gelu", x, out, stream)
+
+
+def repops_gelu_backward(x, dy, out=None, stream=None):
+    _contig(x, "x"), _contig(dy, "dy")
+    if out is None:
+        out = torch.empty_like(x)
+    check(lib().repops_gelu_backward(_p(x), _p(dy), x.numel(), _p(out), _stream(stream)), "repops_gelu_backward")
+    return out
+
+
+def repops_add(a, b, out=None, stream=None):
+    _contig(a, "a"), _contig(b, "b")
+    if out is None:
+        out = torch.empty_like(a)
+    check(lib().repops_add(_p(a), _p(b), a.numel(), _p(out), _stream(stream)), "repops_add")
+    return out
+
+
+def repops_embedding(tok, wte, wpe, T, out=None, stream=None):
+    if tok.dtype != torch.int32:
+        raise RepopsError("tok must be int32")
+    Cc = wte.shape[1]
+    if out is None:
+        out = torch.empty((tok.numel(), Cc), dtype=torch.float32, device=wte.device)
+    check(lib().repops_embedding(_p(tok), tok.numel(), T, _p(wte), _p(wpe), Cc, _p(out), _stream(stream)),
+          "repops_embedding")
+    return out
+
+
+def repops_embedding_backward(tok, dx0, T, dwte, dwpe=None, stream=None):
+    """Accumulates the shard's embedding gradient INTO dwte (and dwpe)."""
+    check(lib().repops_embedding_backward(_p(tok), tok.numel(), T, _p(dx0), dx0.shape[1], _p(dwte), _p(dwpe),
+                                          _stream(stream)), "repops_embedding_backward")
+    return dwte, dwpe
+
+
+def repops_adamw(p, g, m, v, step, lr, b1, b2, eps, wd, decay, stream=None):
+    """In place on p, m, v."""
+    for t, nm in ((p, "p"), (g, "g"), (m, "m"), (v, "v")):
+        _contig(t, nm)
+    check(lib().repops_adamw(_p(p), _p(g), _p(m), _p(v), p.numel(), int(step), float(lr), float(b1), float(b2),
+                             float(eps), float(wd), int(bool(decay)), _stream(stream)), "repops_adamw")
+    return p, m, v
+
+
+def repops_flip_bit(t, elem, bit, stream=None):
+    check(lib().repops_flip_bit(_p(t), int(elem), int(bit), _stream(stream)), "repops_flip_bit")
+    return t
+
+
+# ------------------------------------------------------------------ Verde commitments
+class CommitWorkspace:
+    """Caller-owned device workspace for verde_commit_tensors (grown on demand)."""
+
+    def __init__(self, device="cuda"):
+        self.device = torch.device(device)
+        self.buf = None
+
+    def get(self, nbytes: int):
+        if self.buf is None or self.buf.numel() < nbytes:
+            self.buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=self.device)
+        return self.buf
+
+
+def _desc(t, digest) -> TensorDesc:
+    if not t.is_contiguous():
+        raise RepopsError("committed tensors must be contiguous")
+    d = TensorDesc()
+    d.data = t.data_ptr() if t.numel() else None
+    d.nbytes = t.numel() * t.element_size()
+    d.dtype = _DT[t.dtype]
+    d.rank = t.dim()
+    for i, s in enumerate(t.shape):
+        d.dims[i] = s
+    d.digest = digest.data_ptr()
+    return d
+
+
+def verde_commit_tensors(tensors, digests=None, ws: CommitWorkspace | None = None, stream=None):
+    """R-TCOMMIT for a list of tensors in one batched launch sequence.  Returns a
+    (n, 32) uint8 CUDA tensor of digests (written asynchronously)."""
+    n = len(tensors)
+    dev = tensors[0].device
+    if digests is None:
+        digests = torch.empty((n, 32), dtype=torch.uint8, device=dev)
+    arr = (TensorDesc * n)(*[_desc(t, digests[i]) for i, t in enumerate(tensors)])
+    need = lib().verde_commit_workspace_bytes(arr, n)
+    ws = ws or CommitWorkspace(dev)
+    buf = ws.get(need)
+    check(lib().verde_commit_tensors(arr, n, buf.data_ptr(), buf.numel(), _stream(stream)), "verde_commit_tensors")
+    return digests
+
+
+def verde_commit_tensor(t, ws: CommitWorkspace | None = None, stream=None):
+    return verde_commit_tensors([t], ws=ws, stream=stream)[0]
+
+
+def verde_merkle_root(digests: list[bytes] | bytes) -> bytes:
+    blob = b"".join(digests) if isinstance(digests, list) else bytes(digests)
+    n = len(blob) // 32
+    buf = C.create_string_buffer(blob, max(len(blob), 1))
+    out = C.create_string_buffer(32)
+    check(lib().verde_merkle_root(buf, n, out), "verde_merkle_root")
+    return out.raw
+
+
+def verde_sha256(data: bytes) -> bytes:
+    buf = C.create_string_buffer(bytes(data), max(len(data), 1))
+    out = C.create_string_buffer(32)
+    check(lib().verde_sha256(buf, len(data), out), "verde_sha256")
+    return out.raw
+
+
+def verde_node_digest(index, op, shard, attrs, inputs, dsts, in_digests, out_digests) -> bytes:
+    """attrs: {key(int): value(u64)}; inputs: [(src_node, src_slot)]; dsts: [dst_node];
+    in/out_digests: lists of 32-byte strings."""
+    keys = sorted(attrs)
+    nd = Node()
+    nd.index, nd.op, nd.shard = index, op, shard
+    ak = (C.c_uint32 * max(len(keys), 1))(*keys)
+    av = (C.c_uint64 * max(len(keys), 1))(*[attrs[k] for k in keys])
+    nd.n_attr, nd.attr_keys, nd.attr_vals = len(keys), C.cast(ak, C.c_void_p), C.cast(av, C.c_void_p)
+    sn = (C.c_uint32 * max(len(inputs), 1))(*[s for s, _ in inputs])
+    ss = (C.c_uint32 * max(len(inputs), 1))(*[q for _, q in inputs])
+    ind = C.create_string_buffer(b"".join(in_digests), max(32 * len(in_digests), 1))
+    nd.n_in, nd.in_src_node, nd.in_src_slot = len(inputs), C.cast(sn, C.c_void_p), C.cast(ss, C.c_void_p)
+    nd.in_digests = C.cast(ind, C.c_void_p)
+    dn = (C.c_uint32 * max(len(dsts), 1))(*dsts)
+    nd.n_dst, nd.dst_nodes = len(dsts), C.cast(dn, C.c_void_p)
+    outd = C.create_string_buffer(b"".join(out_digests), max(32 * len(out_digests), 1))
+    nd.n_out, nd.out_digests = len(out_digests), C.cast(outd, C.c_void_p)
+    out = C.create_string_buffer(32)
+    check(lib().verde_node_digest(C.byref(nd), out), "verde_node_digest")
+    return out.raw
+
+
+def verde_first_divergence(seq0: bytes, seq1: bytes) -> tuple[int, int]:
+    """(first differing index or -1, number of subtree comparisons)."""
+    n = len(seq0) // 32
+    a = C.create_string_buffer(bytes(seq0), max(len(seq0), 1))
+    b = C.create_string_buffer(bytes(seq1), max(len(seq1), 1))
+    d = C.c_int64()
+    r = C.c_int64()
+    check(lib().verde_first_divergence(a, b, n, C.byref(d), C.byref(r)), "verde_first_divergence")
+    return d.value, r.value

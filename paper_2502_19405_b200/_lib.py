@@ -1,0 +1,105 @@
+"""ctypes loader for librepops.so and the symbol table of include/repops.h.
+
+Argument marshalling only.  If the library is missing the import fails loudly
+(there is no CPU fallback and no other backend).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "librepops.so")
+HEADER = os.path.join(os.path.dirname(HERE), "include", "repops.h")
+
+i64, i32, f32, vp, u8p = C.c_int64, C.c_int, C.c_float, C.c_void_p, C.c_void_p
+
+
+class TensorDesc(C.Structure):
+    """verde_tensor_desc (repops.h)"""
+    _fields_ = [("data", C.c_void_p), ("nbytes", C.c_int64), ("dtype", C.c_int32), ("rank", C.c_int32),
+                ("dims", C.c_int64 * 8), ("digest", C.c_void_p)]
+
+
+class Node(C.Structure):
+    """verde_node (repops.h)"""
+    _fields_ = [("index", C.c_uint32), ("op", C.c_uint16), ("shard", C.c_uint32),
+                ("n_attr", C.c_int32), ("attr_keys", C.c_void_p), ("attr_vals", C.c_void_p),
+                ("n_in", C.c_int32), ("in_src_node", C.c_void_p), ("in_src_slot", C.c_void_p),
+                ("in_digests", C.c_void_p), ("n_dst", C.c_int32), ("dst_nodes", C.c_void_p),
+                ("n_out", C.c_int32), ("out_digests", C.c_void_p)]
+
+
+SIGNATURES = {
+    "repops_abi_version": (i32, []),
+    "repops_last_error": (C.c_char_p, []),
+    "repops_gemm": (i32, [i64, i64, i64, vp, i64, i32, vp, i64, i32, i32, vp, f32, vp, i64, vp]),
+    "repops_gemm_strided_batched": (i32, [i64, i64, i64, vp, i64, i32, i64, i64, vp, i64, i32, i64, i64,
+                                          i32, vp, f32, vp, i64, i64, i64, i64, i64, vp]),
+    "repops_gemm_cfg": (i32, [i64, i64, i64, vp, i64, i32, vp, i64, i32, i32, vp, f32, vp, i64, vp, i32]),
+    "repops_sum_rows": (i32, [vp, i64, i64, i64, vp, vp]),
+    "repops_sum_cols_seq": (i32, [vp, i64, i64, i64, i64, vp, vp]),
+    "repops_tree_sum": (i32, [vp, i32, i64, vp, vp]),
+    "repops_softmax": (i32, [vp, i64, i64, i64, i32, vp, i64, vp]),
+    "repops_softmax_backward": (i32, [vp, i64, vp, i64, i64, i64, f32, vp, i64, vp]),
+    "repops_layernorm": (i32, [vp, vp, vp, i64, i64, f32, vp, vp, vp, vp]),
+    "repops_layernorm_backward": (i32, [vp, vp, vp, vp, vp, vp, i64, i64, vp, vp]),
+    "repops_layernorm_backward_params": (i32, [vp, vp, vp, vp, i64, i64, i64, vp, vp, vp]),
+    "repops_cross_entropy": (i32, [vp, i64, i64, i64, vp, f32, vp, vp, i64, vp]),
+    "repops_exp": (i32, [vp, i64, vp, vp]),
+    "repops_log": (i32, [vp, i64, vp, vp]),
+    "repops_tanh": (i32, [vp, i64, vp, vp]),
+    "repops_rsqrt": (i32, [vp, i64, vp, vp]),
+    "repops_gelu": (i32, [vp, i64, vp, vp]),
+    "repops_gelu_backward": (i32, [vp, vp, i64, vp, vp]),
+    "repops_add": (i32, [vp, vp, i64, vp, vp]),
+    "repops_embedding": (i32, [vp, i64, i64, vp, vp, i64, vp, vp]),
+    "repops_embedding_backward": (i32, [vp, i64, i64, vp, i64, vp, vp, vp]),
+    "repops_adamw": (i32, [vp, vp, vp, vp, i64, i64, f32, f32, f32, f32, f32, i32, vp]),
+    "repops_flip_bit": (i32, [vp, i64, i32, vp]),
+    "verde_commit_workspace_bytes": (i64, [vp, i32]),
+    "verde_commit_tensors": (i32, [vp, i32, vp, i64, vp]),
+    "verde_commit_tensor": (i32, [vp, i64, i32, i32, vp, vp, vp, i64, vp]),
+    "verde_merkle_root": (i32, [vp, i64, vp]),
+    "verde_sha256": (i32, [vp, i64, vp]),
+    "verde_node_digest": (i32, [vp, vp]),
+    "verde_first_divergence": (i32, [vp, vp, i64, vp, vp]),
+}
+
+_lib = None
+
+
+class RepopsError(RuntimeError):
+    pass
+
+
+def header_symbols() -> list[str]:
+    """Every function declared in include/repops.h."""
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*((?:repops|verde)_[a-z_0-9]+)\s*\(",
+                                 txt, flags=re.M)))
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RepopsError(f"librepops.so not built ({LIB_PATH}); run __graft_entry__.build() "
+                              "-- there is no CPU fallback")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        if L.repops_abi_version() != 1:
+            raise RepopsError("librepops.so ABI version mismatch")
+        _lib = L
+    return _lib
+
+
+def check(status: int, what: str) -> None:
+    if status != 0:
+        msg = lib().repops_last_error().decode(errors="replace")
+        raise RepopsError(f"{what} failed (status {status}): {msg}")

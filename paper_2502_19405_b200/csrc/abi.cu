@@ -1,0 +1,482 @@
+// abi.cu -- the extern "C" boundary of librepops.so (include/repops.h).
+//
+// Host side only: argument validation, thread-local error messages, tile /
+// launch selection (always bits-neutral), the host-side Verde pieces (SHA-256
+// of small host buffers, the step Merkle root, node digests, divergence
+// search).  Every compute step on a tensor runs in the kernels of gemm.cu,
+// rowops.cu, elementwise.cu and sha256.cu.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/repops.h"
+#include "common.cuh"
+#include "elementwise.cuh"
+#include "gemm.cuh"
+#include "rowops.cuh"
+#include "sha256.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+int cuda_status(cudaError_t e, const char *what) {
+    if (e == cudaSuccess) return REPOPS_OK;
+    return fail(REPOPS_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+inline cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+inline bool a16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+#define REQ(cond, ...) \
+    do {               \
+        if (!(cond)) return fail(REPOPS_EINVAL, __VA_ARGS__); \
+    } while (0)
+
+// ------------------------------------------------------------------ host SHA-256 (FIPS 180-4)
+class Sha256 {
+  public:
+    Sha256() { reset(); }
+    void reset() {
+        static const uint32_t iv[8] = {0x6a09e667, 0xbb67ae85, 0x3c6ef372, 0xa54ff53a,
+                                       0x510e527f, 0x9b05688c, 0x1f83d9ab, 0x5be0cd19};
+        memcpy(h_, iv, sizeof iv);
+        total_ = 0;
+        used_ = 0;
+    }
+    Sha256 &put(const void *p, size_t n) {
+        const uint8_t *b = static_cast<const uint8_t *>(p);
+        total_ += n;
+        if (used_) {
+            size_t k = std::min(n, (size_t)64 - used_);
+            memcpy(blk_ + used_, b, k);
+            used_ += k; b += k; n -= k;
+            if (used_ == 64) { block(blk_); used_ = 0; }
+        }
+        while (n >= 64) { block(b); b += 64; n -= 64; }
+        if (n) { memcpy(blk_, b, n); used_ = n; }
+        return *this;
+    }
+    Sha256 &u8(uint8_t v) { return put(&v, 1); }
+    Sha256 &u16(uint16_t v) { uint8_t b[2] = {(uint8_t)v, (uint8_t)(v >> 8)}; return put(b, 2); }
+    Sha256 &u32(uint32_t v) {
+        uint8_t b[4];
+        for (int i = 0; i < 4; ++i) b[i] = (uint8_t)(v >> (8 * i));
+        return put(b, 4);
+    }
+    Sha256 &u64(uint64_t v) {
+        uint8_t b[8];
+        for (int i = 0; i < 8; ++i) b[i] = (uint8_t)(v >> (8 * i));
+        return put(b, 8);
+    }
+    void done(uint8_t out[32]) {
+        uint64_t bits = total_ * 8;
+        uint8_t pad[72] = {0x80};
+        size_t padlen = (used_ < 56) ? 56 - used_ : 120 - used_;
+        uint8_t lenbe[8];
+        for (int i = 0; i < 8; ++i) lenbe[i] = (uint8_t)(bits >> (56 - 8 * i));
+        put(pad, padlen);
+        put(lenbe, 8);
+        for (int i = 0; i < 8; ++i)
+            for (int q = 0; q < 4; ++q) out[4 * i + q] = (uint8_t)(h_[i] >> (24 - 8 * q));
+    }
+
+  private:
+    static uint32_t ror(uint32_t x, int n) { return (x >> n) | (x << (32 - n)); }
+    void block(const uint8_t *p) {
+        static const uint32_t k[64] = {
+            0x428a2f98, 0x71374491, 0xb5c0fbcf, 0xe9b5dba5, 0x3956c25b, 0x59f111f1, 0x923f82a4, 0xab1c5ed5,
+            0xd807aa98, 0x12835b01, 0x243185be, 0x550c7dc3, 0x72be5d74, 0x80deb1fe, 0x9bdc06a7, 0xc19bf174,
+            0xe49b69c1, 0xefbe4786, 0x0fc19dc6, 0x240ca1cc, 0x2de92c6f, 0x4a7484aa, 0x5cb0a9dc, 0x76f988da,
+            0x983e5152, 0xa831c66d, 0xb00327c8, 0xbf597fc7, 0xc6e00bf3, 0xd5a79147, 0x06ca6351, 0x14292967,
+            0x27b70a85, 0x2e1b2138, 0x4d2c6dfc, 0x53380d13, 0x650a7354, 0x766a0abb, 0x81c2c92e, 0x92722c85,
+            0xa2bfe8a1, 0xa81a664b, 0xc24b8b70, 0xc76c51a3, 0xd192e819, 0xd6990624, 0xf40e3585, 0x106aa070,
+            0x19a4c116, 0x1e376c08, 0x2748774c, 0x34b0bcb5, 0x391c0cb3, 0x4ed8aa4a, 0x5b9cca4f, 0x682e6ff3,
+            0x748f82ee, 0x78a5636f, 0x84c87814, 0x8cc70208, 0x90befffa, 0xa4506ceb, 0xbef9a3f7, 0xc67178f2};
+        uint32_t w[64];
+        for (int i = 0; i < 16; ++i)
+            w[i] = (uint32_t)p[4 * i] << 24 | (uint32_t)p[4 * i + 1] << 16 | (uint32_t)p[4 * i + 2] << 8 | p[4 * i + 3];
+        for (int i = 16; i < 64; ++i)
+            w[i] = w[i - 16] + (ror(w[i - 15], 7) ^ ror(w[i - 15], 18) ^ (w[i - 15] >> 3)) + w[i - 7] +
+                   (ror(w[i - 2], 17) ^ ror(w[i - 2], 19) ^ (w[i - 2] >> 10));
+        uint32_t v[8];
+        memcpy(v, h_, sizeof v);
+        for (int i = 0; i < 64; ++i) {
+            uint32_t t1 = v[7] + (ror(v[4], 6) ^ ror(v[4], 11) ^ ror(v[4], 25)) + ((v[4] & v[5]) ^ (~v[4] & v[6])) +
+                          k[i] + w[i];
+            uint32_t t2 = (ror(v[0], 2) ^ ror(v[0], 13) ^ ror(v[0], 22)) + ((v[0] & v[1]) ^ (v[0] & v[2]) ^ (v[1] & v[2]));
+            memmove(v + 1, v, 7 * sizeof(uint32_t));
+            v[4] += t1;
+            v[0] = t1 + t2;
+        }
+        for (int i = 0; i < 8; ++i) h_[i] += v[i];
+    }
+    uint32_t h_[8];
+    uint8_t blk_[64];
+    uint64_t total_;
+    size_t used_;
+};
+
+struct Node32 { uint8_t b[32]; };
+
+// RFC 6962 MTH of entries[lo, lo+n)  (entries are 32-byte digests)
+Node32 mth(const uint8_t *e, int64_t lo, int64_t n) {
+    Node32 out;
+    Sha256 h;
+    if (n == 1) {
+        h.u8(0x00).put(e + 32 * lo, 32).done(out.b);
+        return out;
+    }
+    int64_t k = 1;
+    while (2 * k < n) k *= 2;
+    Node32 l = mth(e, lo, k), r = mth(e, lo + k, n - k);
+    h.u8(0x01).put(l.b, 32).put(r.b, 32).done(out.b);
+    return out;
+}
+
+}  // namespace
+
+namespace ro_host {
+int num_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+    }
+    return sms;
+}
+}  // namespace ro_host
+
+extern "C" {
+
+int repops_abi_version(void) { return REPOPS_ABI_VERSION; }
+const char *repops_last_error(void) { return g_err.c_str(); }
+
+// ------------------------------------------------------------------ GEMM
+static int gemm_common(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, int transA, int64_t sA0,
+                       int64_t sA1, const float *B, int64_t ldb, int transB, int64_t sB0, int64_t sB1, int epi,
+                       const float *bias, float scale, float *C, int64_t ldc, int64_t sC0, int64_t sC1, int64_t b0,
+                       int64_t b1, void *stream, int force_cfg) {
+    REQ(M >= 0 && N >= 0 && K >= 0 && b0 >= 0 && b1 >= 0, "gemm: negative extent");
+    REQ(epi >= REPOPS_EPI_NONE && epi <= REPOPS_EPI_SCALE, "gemm: unknown epilogue %d", epi);
+    if (M == 0 || N == 0 || b0 == 0 || b1 == 0) return REPOPS_OK;
+    REQ(C != nullptr, "gemm: C is null");
+    REQ(ldc >= N, "gemm: ldc %lld < N %lld", (long long)ldc, (long long)N);
+    if (K > 0) {
+        REQ(A != nullptr && B != nullptr, "gemm: A or B is null");
+        REQ(lda >= (transA ? M : K), "gemm: lda too small");
+        REQ(ldb >= (transB ? K : N), "gemm: ldb too small");
+    }
+    REQ(epi != REPOPS_EPI_BIAS || bias != nullptr, "gemm: bias epilogue without bias");
+    GemmParams p{};
+    p.M = M; p.N = N; p.K = K;
+    p.A = A; p.lda = lda; p.sA0 = sA0; p.sA1 = sA1;
+    p.B = B; p.ldb = ldb; p.sB0 = sB0; p.sB1 = sB1;
+    p.C = C; p.ldc = ldc; p.sC0 = sC0; p.sC1 = sC1;
+    p.batch0 = b0; p.batch1 = b1;
+    p.transA = transA ? 1 : 0; p.transB = transB ? 1 : 0;
+    p.epi = epi; p.bias = bias; p.scale = scale;
+    p.vecA = a16(A) && lda % 4 == 0 && sA0 % 4 == 0 && sA1 % 4 == 0;
+    p.vecB = a16(B) && ldb % 4 == 0 && sB0 % 4 == 0 && sB1 % 4 == 0;
+    p.vecC = a16(C) && ldc % 4 == 0 && sC0 % 4 == 0 && sC1 % 4 == 0;
+    return cuda_status(gemm_launch(p, S(stream), force_cfg), "gemm launch");
+}
+
+int repops_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, int transA, const float *B, int64_t ldb,
+                int transB, int epi, const float *bias, float scale, float *C, int64_t ldc, void *stream) {
+    return gemm_common(M, N, K, A, lda, transA, 0, 0, B, ldb, transB, 0, 0, epi, bias, scale, C, ldc, 0, 0, 1, 1,
+                       stream, -1);
+}
+
+int repops_gemm_strided_batched(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, int transA, int64_t sA0,
+                                int64_t sA1, const float *B, int64_t ldb, int transB, int64_t sB0, int64_t sB1, int epi,
+                                const float *bias, float scale, float *C, int64_t ldc, int64_t sC0, int64_t sC1,
+                                int64_t batch0, int64_t batch1, void *stream) {
+    return gemm_common(M, N, K, A, lda, transA, sA0, sA1, B, ldb, transB, sB0, sB1, epi, bias, scale, C, ldc, sC0,
+                       sC1, batch0, batch1, stream, -1);
+}
+
+// Test hook (not in repops.h): force a tile configuration to prove bits-neutrality.
+int repops_gemm_cfg(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, int transA, const float *B,
+                    int64_t ldb, int transB, int epi, const float *bias, float scale, float *C, int64_t ldc,
+                    void *stream, int cfg) {
+    REQ(cfg >= 0 && cfg <= 1, "gemm_cfg: cfg must be 0 or 1");
+    return gemm_common(M, N, K, A, lda, transA, 0, 0, B, ldb, transB, 0, 0, epi, bias, scale, C, ldc, 0, 0, 1, 1,
+                       stream, cfg);
+}
+
+// ------------------------------------------------------------------ reductions
+int repops_sum_rows(const float *x, int64_t rows, int64_t cols, int64_t ld, float *out, void *stream) {
+    REQ(rows >= 0 && cols >= 0, "sum_rows: negative extent");
+    if (rows == 0) return REPOPS_OK;
+    REQ(out && (cols == 0 || x), "sum_rows: null pointer");
+    REQ(ld >= cols, "sum_rows: ld < cols");
+    REQ(cols <= TILE_ELEMS * TILE_ELEMS, "sum_rows: row longer than 4096 tiles");
+    return cuda_status(launch_sum_rows(x, rows, cols, ld, out, S(stream)), "sum_rows");
+}
+
+int repops_sum_cols_seq(const float *x, int64_t rows, int64_t cols, int64_t ld, int64_t nseg, float *out,
+                        void *stream) {
+    REQ(rows >= 0 && cols >= 0 && nseg >= 1, "sum_cols_seq: bad extent");
+    REQ(rows % nseg == 0, "sum_cols_seq: rows %% nseg != 0");
+    if (cols == 0) return REPOPS_OK;
+    REQ(out && (rows == 0 || x), "sum_cols_seq: null pointer");
+    REQ(ld >= cols, "sum_cols_seq: ld < cols");
+    return cuda_status(launch_sum_cols_seq(x, rows, cols, ld, nseg, out, S(stream)), "sum_cols_seq");
+}
+
+int repops_tree_sum(const float *const *parts, int nparts, int64_t n, float *out, void *stream) {
+    REQ(nparts == 1 || nparts == 2 || nparts == 4 || nparts == 8 || nparts == 16, "tree_sum: nparts %d", nparts);
+    REQ(n >= 0, "tree_sum: negative n");
+    if (n == 0) return REPOPS_OK;
+    REQ(parts && out, "tree_sum: null pointer");
+    for (int q = 0; q < nparts; ++q) REQ(parts[q], "tree_sum: null part");
+    return cuda_status(launch_tree_sum(parts, nparts, n, out, S(stream)), "tree_sum");
+}
+
+// ------------------------------------------------------------------ row operators
+int repops_softmax(const float *x, int64_t rows, int64_t cols, int64_t ldx, int causal, float *y, int64_t ldy,
+                   void *stream) {
+    REQ(rows >= 0 && cols >= 0, "softmax: negative extent");
+    if (rows == 0 || cols == 0) return REPOPS_OK;
+    REQ(x && y, "softmax: null pointer");
+    REQ(ldx >= cols && ldy >= cols, "softmax: ld < cols");
+    REQ(cols <= TILE_ELEMS * TILE_ELEMS, "softmax: row too long");
+    if (causal && rows % cols != 0) return fail(REPOPS_ESHAPE, "softmax: causal needs rows %% cols == 0");
+    return cuda_status(launch_softmax(x, rows, cols, ldx, causal ? 1 : 0, y, ldy, S(stream)), "softmax");
+}
+
+int repops_softmax_backward(const float *y, int64_t ldy, const float *dy, int64_t lddy, int64_t rows, int64_t cols,
+                            float scale, float *dx, int64_t lddx, void *stream) {
+    REQ(rows >= 0 && cols >= 0, "softmax_backward: negative extent");
+    if (rows == 0 || cols == 0) return REPOPS_OK;
+    REQ(y && dy && dx, "softmax_backward: null pointer");
+    REQ(ldy >= cols && lddy >= cols && lddx >= cols, "softmax_backward: ld < cols");
+    REQ(cols <= TILE_ELEMS * TILE_ELEMS, "softmax_backward: row too long");
+    return cuda_status(launch_softmax_backward(y, ldy, dy, lddy, rows, cols, scale, dx, lddx, S(stream)),
+                       "softmax_backward");
+}
+
+int repops_layernorm(const float *x, const float *gamma, const float *beta, int64_t rows, int64_t cols, float eps,
+                     float *y, float *mean, float *rstd, void *stream) {
+    REQ(rows >= 0 && cols >= 1, "layernorm: bad extent");
+    REQ(cols <= TILE_ELEMS, "layernorm: cols > 4096 not supported");
+    if (rows == 0) return REPOPS_OK;
+    REQ(x && gamma && beta && y, "layernorm: null pointer");
+    return cuda_status(launch_layernorm(x, gamma, beta, rows, cols, eps, y, mean, rstd, S(stream)), "layernorm");
+}
+
+int repops_layernorm_backward(const float *dy, const float *x, const float *gamma, const float *mean,
+                              const float *rstd, const float *dres, int64_t rows, int64_t cols, float *dx,
+                              void *stream) {
+    REQ(rows >= 0 && cols >= 1, "layernorm_backward: bad extent");
+    REQ(cols <= TILE_ELEMS, "layernorm_backward: cols > 4096 not supported");
+    if (rows == 0) return REPOPS_OK;
+    REQ(dy && x && gamma && mean && rstd && dx, "layernorm_backward: null pointer");
+    return cuda_status(launch_layernorm_backward(dy, x, gamma, mean, rstd, dres, rows, cols, dx, S(stream)),
+                       "layernorm_backward");
+}
+
+int repops_layernorm_backward_params(const float *dy, const float *x, const float *mean, const float *rstd,
+                                     int64_t rows, int64_t cols, int64_t nseg, float *dgamma, float *dbeta,
+                                     void *stream) {
+    REQ(rows >= 0 && cols >= 0 && nseg >= 1 && rows % nseg == 0, "layernorm_backward_params: bad extent");
+    if (cols == 0) return REPOPS_OK;
+    REQ(dgamma && dbeta && (rows == 0 || (dy && x && mean && rstd)), "layernorm_backward_params: null pointer");
+    return cuda_status(launch_layernorm_params(dy, x, mean, rstd, rows, cols, nseg, dgamma, dbeta, S(stream)),
+                       "layernorm_backward_params");
+}
+
+int repops_cross_entropy(const float *logits, int64_t rows, int64_t V, int64_t ld, const int32_t *labels, float scale,
+                         float *loss, float *dlogits, int64_t ldd, void *stream) {
+    REQ(rows >= 0 && V >= 1, "cross_entropy: bad extent");
+    if (rows == 0) return REPOPS_OK;
+    REQ(logits && labels, "cross_entropy: null pointer");
+    REQ(ld >= V && (!dlogits || ldd >= V), "cross_entropy: ld < V");
+    REQ(V <= TILE_ELEMS * TILE_ELEMS, "cross_entropy: V too large");
+    return cuda_status(launch_cross_entropy(logits, rows, V, ld, labels, scale, loss, dlogits, ldd, S(stream)),
+                       "cross_entropy");
+}
+
+// ------------------------------------------------------------------ elementwise
+#define UNARY(name, fn)                                                           \
+    int name(const float *x, int64_t n, float *y, void *stream) {                 \
+        REQ(n >= 0, #name ": negative n");                                         \
+        if (n == 0) return REPOPS_OK;                                              \
+        REQ(x && y, #name ": null pointer");                                       \
+        return cuda_status(fn(x, n, y, S(stream)), #name);                         \
+    }
+UNARY(repops_exp, launch_exp)
+UNARY(repops_log, launch_log)
+UNARY(repops_tanh, launch_tanh)
+UNARY(repops_rsqrt, launch_rsqrt)
+UNARY(repops_gelu, launch_gelu)
+
+int repops_gelu_backward(const float *x, const float *dy, int64_t n, float *dx, void *stream) {
+    REQ(n >= 0, "gelu_backward: negative n");
+    if (n == 0) return REPOPS_OK;
+    REQ(x && dy && dx, "gelu_backward: null pointer");
+    return cuda_status(launch_gelu_backward(x, dy, n, dx, S(stream)), "gelu_backward");
+}
+
+int repops_add(const float *a, const float *b, int64_t n, float *y, void *stream) {
+    REQ(n >= 0, "add: negative n");
+    if (n == 0) return REPOPS_OK;
+    REQ(a && b && y, "add: null pointer");
+    return cuda_status(launch_add(a, b, n, y, S(stream)), "add");
+}
+
+int repops_embedding(const int32_t *tok, int64_t ntok, int64_t T, const float *wte, const float *wpe, int64_t C,
+                     float *x0, void *stream) {
+    REQ(ntok >= 0 && T >= 1 && C >= 0, "embedding: bad extent");
+    if (ntok == 0 || C == 0) return REPOPS_OK;
+    REQ(tok && wte && wpe && x0, "embedding: null pointer");
+    return cuda_status(launch_embedding(tok, ntok, T, wte, wpe, C, x0, S(stream)), "embedding");
+}
+
+int repops_embedding_backward(const int32_t *tok, int64_t ntok, int64_t T, const float *dx0, int64_t C, float *dwte,
+                              float *dwpe, void *stream) {
+    REQ(ntok >= 0 && T >= 1 && C >= 0, "embedding_backward: bad extent");
+    REQ(ntok <= 16384, "embedding_backward: at most 16384 tokens per shard");
+    if (ntok == 0 || C == 0) return REPOPS_OK;
+    REQ(tok && dx0 && dwte, "embedding_backward: null pointer");
+    return cuda_status(launch_embedding_backward(tok, ntok, T, dx0, C, dwte, dwpe, S(stream)), "embedding_backward");
+}
+
+int repops_adamw(float *p, const float *g, float *m, float *v, int64_t n, int64_t step, float lr, float b1, float b2,
+                 float eps, float wd, int decay, void *stream) {
+    REQ(n >= 0 && step >= 1, "adamw: bad n/step");
+    if (n == 0) return REPOPS_OK;
+    REQ(p && g && m && v, "adamw: null pointer");
+    // bc = 1 - b^step, b^step by iterated binary32 multiplication (R15); no contraction here
+    volatile float pw1 = b1, pw2 = b2;
+    for (int64_t i = 1; i < step; ++i) {
+        pw1 = pw1 * b1;
+        pw2 = pw2 * b2;
+    }
+    volatile float bc1 = 1.0f - pw1, bc2 = 1.0f - pw2, omb1 = 1.0f - b1, omb2 = 1.0f - b2;
+    return cuda_status(launch_adamw(p, g, m, v, n, lr, b1, b2, eps, wd, bc1, bc2, omb1, omb2, decay ? 1 : 0,
+                                    S(stream)),
+                       "adamw");
+}
+
+int repops_flip_bit(void *data, int64_t elem, int bit, void *stream) {
+    REQ(data && elem >= 0 && bit >= 0 && bit < 32, "flip_bit: bad argument");
+    return cuda_status(launch_flip_bit(data, elem, bit, S(stream)), "flip_bit");
+}
+
+// ------------------------------------------------------------------ Verde
+int64_t verde_commit_workspace_bytes(const verde_tensor_desc *descs, int n) {
+    if (!descs || n <= 0) return 0;
+    return commit_workspace_bytes(descs, n);
+}
+
+int verde_commit_tensors(const verde_tensor_desc *descs, int n, void *ws, int64_t ws_bytes, void *stream) {
+    REQ(n >= 0, "commit: negative n");
+    if (n == 0) return REPOPS_OK;
+    REQ(descs != nullptr, "commit: null descriptors");
+    for (int t = 0; t < n; ++t) {
+        REQ(descs[t].nbytes >= 0 && (descs[t].nbytes == 0 || descs[t].data), "commit: tensor %d has no data", t);
+        REQ(descs[t].rank >= 0 && descs[t].rank <= 8, "commit: tensor %d rank %d", t, descs[t].rank);
+        REQ(descs[t].digest != nullptr, "commit: tensor %d has no digest buffer", t);
+    }
+    REQ(ws != nullptr, "commit: null workspace");
+    int64_t need = 0;
+    cudaError_t e = commit_launch(descs, n, ws, ws_bytes, S(stream), &need);
+    if (e == cudaErrorMemoryAllocation && ws_bytes < need)
+        return fail(REPOPS_ENOSPACE, "commit: workspace %lld < %lld bytes", (long long)ws_bytes, (long long)need);
+    return cuda_status(e, "commit");
+}
+
+int verde_commit_tensor(const void *data, int64_t nbytes, int dtype, int rank, const int64_t *dims, uint8_t *digest32,
+                        void *ws, int64_t ws_bytes, void *stream) {
+    REQ(rank >= 0 && rank <= 8 && (rank == 0 || dims), "commit_tensor: bad rank/dims");
+    verde_tensor_desc d{};
+    d.data = data;
+    d.nbytes = nbytes;
+    d.dtype = dtype;
+    d.rank = rank;
+    for (int i = 0; i < rank; ++i) d.dims[i] = dims[i];
+    d.digest = digest32;
+    return verde_commit_tensors(&d, 1, ws, ws_bytes, stream);
+}
+
+int verde_merkle_root(const uint8_t *leaves, int64_t n, uint8_t *root32) {
+    if (n <= 0) return fail(REPOPS_EINVAL, "merkle_root: empty leaf list");
+    REQ(leaves && root32, "merkle_root: null pointer");
+    Node32 r = mth(leaves, 0, n);
+    memcpy(root32, r.b, 32);
+    return REPOPS_OK;
+}
+
+int verde_sha256(const uint8_t *data, int64_t n, uint8_t *out32) {
+    REQ(n >= 0 && out32 && (n == 0 || data), "sha256: bad argument");
+    Sha256 h;
+    if (n) h.put(data, (size_t)n);
+    h.done(out32);
+    return REPOPS_OK;
+}
+
+int verde_node_digest(const verde_node *node, uint8_t *out32) {
+    REQ(node && out32, "node_digest: null pointer");
+    const verde_node &nd = *node;
+    REQ(nd.n_attr >= 0 && nd.n_in >= 0 && nd.n_out >= 0 && nd.n_dst >= 0, "node_digest: negative count");
+    for (int i = 1; i < nd.n_attr; ++i) REQ(nd.attr_keys[i - 1] < nd.attr_keys[i], "node_digest: attr keys not ascending");
+    Sha256 h;
+    h.u8(0x4E).u32(nd.index).u16(nd.op).u32(nd.shard);
+    h.u32((uint32_t)nd.n_attr);
+    for (int i = 0; i < nd.n_attr; ++i) h.u32(nd.attr_keys[i]).u64(nd.attr_vals[i]);
+    h.u32((uint32_t)nd.n_in);
+    for (int i = 0; i < nd.n_in; ++i) h.u32(nd.in_src_node[i]).u32(nd.in_src_slot[i]);
+    h.u32((uint32_t)nd.n_dst);
+    for (int i = 0; i < nd.n_dst; ++i) h.u32(nd.dst_nodes[i]);
+    h.u32((uint32_t)nd.n_out);
+    if (nd.n_in) h.put(nd.in_digests, 32 * (size_t)nd.n_in);
+    if (nd.n_out) h.put(nd.out_digests, 32 * (size_t)nd.n_out);
+    h.done(out32);
+    return REPOPS_OK;
+}
+
+int verde_first_divergence(const uint8_t *seq0, const uint8_t *seq1, int64_t n, int64_t *d_out, int64_t *rounds_out) {
+    REQ(n >= 1 && seq0 && seq1 && d_out, "first_divergence: bad argument");
+    // Descend the two RFC 6962 trees: at each node compare the LEFT subtree roots;
+    // equal -> the first difference is in the right subtree.
+    int64_t lo = 0, len = n, rounds = 0;
+    Node32 a = mth(seq0, 0, n), b = mth(seq1, 0, n);
+    ++rounds;
+    if (memcmp(a.b, b.b, 32) == 0) {
+        *d_out = -1;
+        if (rounds_out) *rounds_out = rounds;
+        return REPOPS_OK;
+    }
+    while (len > 1) {
+        int64_t k = 1;
+        while (2 * k < len) k *= 2;
+        Node32 l0 = mth(seq0, lo, k), l1 = mth(seq1, lo, k);
+        ++rounds;
+        if (memcmp(l0.b, l1.b, 32) != 0) {
+            len = k;
+        } else {
+            lo += k;
+            len -= k;
+        }
+    }
+    *d_out = lo;
+    if (rounds_out) *rounds_out = rounds;
+    return REPOPS_OK;
+}
+
+}  // extern "C"

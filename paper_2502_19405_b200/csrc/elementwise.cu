@@ -1,0 +1,259 @@
+// elementwise.cu -- order-free (per element) operators: software math
+// (R5/R6), GELU, residual add, R-TREE_S (R14), AdamW (R15),
+// embedding forward/backward (R-EMB), fault injection.
+//
+// HBM-bound: grid-stride loops over float4 with a grid of a few waves of the
+// 148 SMs; each element's arithmetic is the fixed chain in common.cuh.
+#include "common.cuh"
+#include "elementwise.cuh"
+
+namespace {
+
+using namespace ro;
+
+template <class F>
+__global__ void unary_kernel(const float *__restrict__ x, int64_t n, float *__restrict__ y, F f) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n4 = (aligned16(x) && aligned16(y)) ? n / 4 : 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+        float4 v = reinterpret_cast<const float4 *>(x)[i];
+        reinterpret_cast<float4 *>(y)[i] = make_float4(f(v.x), f(v.y), f(v.z), f(v.w));
+    }
+    for (int64_t i = n4 * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) y[i] = f(x[i]);
+}
+
+template <class F>
+__global__ void binary_kernel(const float *__restrict__ a, const float *__restrict__ b, int64_t n,
+                              float *__restrict__ y, F f) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n4 = (aligned16(a) && aligned16(b) && aligned16(y)) ? n / 4 : 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+        float4 u = reinterpret_cast<const float4 *>(a)[i];
+        float4 v = reinterpret_cast<const float4 *>(b)[i];
+        reinterpret_cast<float4 *>(y)[i] = make_float4(f(u.x, v.x), f(u.y, v.y), f(u.z, v.z), f(u.w, v.w));
+    }
+    for (int64_t i = n4 * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) y[i] = f(a[i], b[i]);
+}
+
+struct ExpF { RO_DEV float operator()(float x) const { return canon(exp_rn(x)); } };
+struct LogF { RO_DEV float operator()(float x) const { return canon(log_rn(x)); } };
+struct TanhF { RO_DEV float operator()(float x) const { return canon(tanh_rn(x)); } };
+struct RsqrtF { RO_DEV float operator()(float x) const { return canon(rsqrt_rn(x)); } };
+struct GeluF { RO_DEV float operator()(float x) const { return canon(gelu_rn(x)); } };
+struct GeluBwdF { RO_DEV float operator()(float x, float dy) const { return canon(gelu_grad_rn(x, dy)); } };
+struct AddF { RO_DEV float operator()(float a, float b) const { return canon(__fadd_rn(a, b)); } };
+
+// R-TREE_S: balanced pairwise tree over up to 16 parts, leaves are the parts themselves
+struct Parts { const float *p[16]; };
+
+template <int NP>
+RO_DEV float tree_at(const Parts &ps, int64_t i) {
+    float v[NP];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) v[q] = __ldg(ps.p[q] + i);
+#pragma unroll
+    for (int w = 1; w < NP; w <<= 1)
+#pragma unroll
+        for (int q = 0; q < NP; q += 2 * w) v[q] = __fadd_rn(v[q], v[q + w]);
+    return v[0];
+}
+
+template <int NP>
+__global__ void tree_kernel(Parts ps, int64_t n, float *__restrict__ out) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    bool al = aligned16(out);
+#pragma unroll
+    for (int q = 0; q < NP; ++q) al = al && aligned16(ps.p[q]);
+    const int64_t n4 = al ? n / 4 : 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+        float4 v[NP];
+#pragma unroll
+        for (int q = 0; q < NP; ++q) v[q] = __ldg(reinterpret_cast<const float4 *>(ps.p[q]) + i);
+#pragma unroll
+        for (int w = 1; w < NP; w <<= 1)
+#pragma unroll
+            for (int q = 0; q < NP; q += 2 * w) {
+                v[q].x = __fadd_rn(v[q].x, v[q + w].x);
+                v[q].y = __fadd_rn(v[q].y, v[q + w].y);
+                v[q].z = __fadd_rn(v[q].z, v[q + w].z);
+                v[q].w = __fadd_rn(v[q].w, v[q + w].w);
+            }
+        reinterpret_cast<float4 *>(out)[i] = make_float4(canon(v[0].x), canon(v[0].y), canon(v[0].z), canon(v[0].w));
+    }
+    for (int64_t i = n4 * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        out[i] = canon(tree_at<NP>(ps, i));
+}
+
+// R-ADAMW element chain (oracle: orc_adamw)
+struct AdamHyper { float lr, b1, b2, eps, wd, bc1, bc2, omb1, omb2; int decay; };
+
+RO_DEV void adam_elem(float &p, float g, float &m, float &v, const AdamHyper &h) {
+    float mi = __fadd_rn(__fmul_rn(h.b1, m), __fmul_rn(h.omb1, g));
+    float vi = __fadd_rn(__fmul_rn(h.b2, v), __fmul_rn(h.omb2, __fmul_rn(g, g)));
+    float upd = __fdiv_rn(__fdiv_rn(mi, h.bc1), __fadd_rn(__fsqrt_rn(__fdiv_rn(vi, h.bc2)), h.eps));
+    if (h.decay) upd = __fadd_rn(upd, __fmul_rn(h.wd, p));
+    p = canon(__fsub_rn(p, __fmul_rn(h.lr, upd)));
+    m = canon(mi);
+    v = canon(vi);
+}
+
+__global__ void adamw_kernel(float *__restrict__ p, const float *__restrict__ g, float *__restrict__ m,
+                             float *__restrict__ v, int64_t n, AdamHyper h) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const bool al = aligned16(p) && aligned16(g) && aligned16(m) && aligned16(v);
+    const int64_t n4 = al ? n / 4 : 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+        float4 pp = reinterpret_cast<float4 *>(p)[i];
+        float4 gg = __ldg(reinterpret_cast<const float4 *>(g) + i);
+        float4 mm = reinterpret_cast<float4 *>(m)[i];
+        float4 vv = reinterpret_cast<float4 *>(v)[i];
+        adam_elem(pp.x, gg.x, mm.x, vv.x, h);
+        adam_elem(pp.y, gg.y, mm.y, vv.y, h);
+        adam_elem(pp.z, gg.z, mm.z, vv.z, h);
+        adam_elem(pp.w, gg.w, mm.w, vv.w, h);
+        reinterpret_cast<float4 *>(p)[i] = pp;
+        reinterpret_cast<float4 *>(m)[i] = mm;
+        reinterpret_cast<float4 *>(v)[i] = vv;
+    }
+    for (int64_t i = n4 * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        float pp = p[i], mm = m[i], vv = v[i];
+        adam_elem(pp, g[i], mm, vv, h);
+        p[i] = pp;
+        m[i] = mm;
+        v[i] = vv;
+    }
+}
+
+// R-EMB forward: x0[t][c] = wte[tok[t]][c] + wpe[t mod T][c]; one CTA-row per token
+__global__ void embedding_kernel(const int32_t *__restrict__ tok, int64_t ntok, int64_t T,
+                                 const float *__restrict__ wte, const float *__restrict__ wpe, int64_t C,
+                                 float *__restrict__ x0) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.y + threadIdx.y;
+    if (t >= ntok) return;
+    const float *a = wte + (int64_t)__ldg(tok + t) * C;
+    const float *b = wpe + (t % T) * C;
+    float *o = x0 + t * C;
+    for (int64_t c = threadIdx.x; c < C; c += blockDim.x) o[c] = canon(__fadd_rn(__ldg(a + c), __ldg(b + c)));
+}
+
+// R-EMB backward for one shard.  One CTA per token position u: if u is the
+// first occurrence of its token, it folds dx0 over all positions t >= u with
+// the same token, in ascending t, and adds the fold into dwte[token].
+// Position rows of dwpe likewise (CTAs with u < T handle position u).
+__global__ void embedding_bwd_kernel(const int32_t *__restrict__ tok, int64_t ntok, int64_t T,
+                                     const float *__restrict__ dx0, int64_t C, float *__restrict__ dwte,
+                                     float *__restrict__ dwpe) {
+    extern __shared__ int32_t stok[];
+    const int64_t u = blockIdx.x;
+    for (int64_t i = threadIdx.x; i < ntok; i += blockDim.x) stok[i] = __ldg(tok + i);
+    __syncthreads();
+    const int32_t v = stok[u];
+    bool first = true;
+    for (int64_t i = 0; i < u; ++i)
+        if (stok[i] == v) { first = false; break; }
+    if (first) {
+        for (int64_t c = threadIdx.x; c < C; c += blockDim.x) {
+            float acc = 0.f;
+            for (int64_t t = u; t < ntok; ++t)
+                if (stok[t] == v) acc = __fadd_rn(acc, __ldg(dx0 + t * C + c));
+            float *o = dwte + (int64_t)v * C + c;
+            *o = canon(__fadd_rn(*o, acc));
+        }
+    }
+    if (dwpe && u < T) {
+        for (int64_t c = threadIdx.x; c < C; c += blockDim.x) {
+            float acc = 0.f;
+            for (int64_t t = u; t < ntok; t += T) acc = __fadd_rn(acc, __ldg(dx0 + t * C + c));
+            float *o = dwpe + u * C + c;
+            *o = canon(__fadd_rn(*o, acc));
+        }
+    }
+}
+
+__global__ void flip_bit_kernel(uint32_t *data, int64_t elem, int bit) { data[elem] ^= (1u << bit); }
+
+int ew_grid(int64_t n) {
+    int64_t blocks = (n / 4 + 255) / 256;
+    int64_t cap = (int64_t)ro_host::num_sms() * 8;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    return (int)blocks;
+}
+
+}  // namespace
+
+template <class F>
+static cudaError_t run_unary(const float *x, int64_t n, float *y, cudaStream_t s, F f) {
+    if (n == 0) return cudaSuccess;
+    unary_kernel<<<ew_grid(n), 256, 0, s>>>(x, n, y, f);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_exp(const float *x, int64_t n, float *y, cudaStream_t s) { return run_unary(x, n, y, s, ExpF{}); }
+cudaError_t launch_log(const float *x, int64_t n, float *y, cudaStream_t s) { return run_unary(x, n, y, s, LogF{}); }
+cudaError_t launch_tanh(const float *x, int64_t n, float *y, cudaStream_t s) { return run_unary(x, n, y, s, TanhF{}); }
+cudaError_t launch_rsqrt(const float *x, int64_t n, float *y, cudaStream_t s) { return run_unary(x, n, y, s, RsqrtF{}); }
+cudaError_t launch_gelu(const float *x, int64_t n, float *y, cudaStream_t s) { return run_unary(x, n, y, s, GeluF{}); }
+
+cudaError_t launch_gelu_backward(const float *x, const float *dy, int64_t n, float *dx, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    binary_kernel<<<ew_grid(n), 256, 0, s>>>(x, dy, n, dx, GeluBwdF{});
+    return cudaGetLastError();
+}
+
+cudaError_t launch_add(const float *a, const float *b, int64_t n, float *y, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    binary_kernel<<<ew_grid(n), 256, 0, s>>>(a, b, n, y, AddF{});
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tree_sum(const float *const *parts, int nparts, int64_t n, float *out, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    Parts ps{};
+    for (int q = 0; q < nparts; ++q) ps.p[q] = parts[q];
+    int g = ew_grid(n * (nparts > 2 ? 1 : 1));
+    switch (nparts) {
+        case 1: tree_kernel<1><<<g, 256, 0, s>>>(ps, n, out); break;
+        case 2: tree_kernel<2><<<g, 256, 0, s>>>(ps, n, out); break;
+        case 4: tree_kernel<4><<<g, 256, 0, s>>>(ps, n, out); break;
+        case 8: tree_kernel<8><<<g, 256, 0, s>>>(ps, n, out); break;
+        case 16: tree_kernel<16><<<g, 256, 0, s>>>(ps, n, out); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_adamw(float *p, const float *g, float *m, float *v, int64_t n, float lr, float b1, float b2,
+                         float eps, float wd, float bc1, float bc2, float omb1, float omb2, int decay,
+                         cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    AdamHyper h{lr, b1, b2, eps, wd, bc1, bc2, omb1, omb2, decay};
+    adamw_kernel<<<ew_grid(n), 256, 0, s>>>(p, g, m, v, n, h);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_embedding(const int32_t *tok, int64_t ntok, int64_t T, const float *wte, const float *wpe,
+                             int64_t C, float *x0, cudaStream_t s) {
+    if (ntok == 0) return cudaSuccess;
+    dim3 block(128, 4);
+    embedding_kernel<<<(unsigned)((ntok + 3) / 4), block, 0, s>>>(tok, ntok, T, wte, wpe, C, x0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_embedding_backward(const int32_t *tok, int64_t ntok, int64_t T, const float *dx0, int64_t C,
+                                      float *dwte, float *dwpe, cudaStream_t s) {
+    if (ntok == 0) return cudaSuccess;
+    size_t smem = (size_t)ntok * sizeof(int32_t);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(embedding_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    embedding_bwd_kernel<<<(unsigned)ntok, 256, smem, s>>>(tok, ntok, T, dx0, C, dwte, dwpe);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_flip_bit(void *data, int64_t elem, int bit, cudaStream_t s) {
+    flip_bit_kernel<<<1, 1, 0, s>>>(reinterpret_cast<uint32_t *>(data), elem, bit);
+    return cudaGetLastError();
+}

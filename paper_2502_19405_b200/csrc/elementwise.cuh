@@ -1,0 +1,21 @@
+// elementwise.cuh -- launchers of the per-element operators (internal).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+cudaError_t launch_exp(const float *x, int64_t n, float *y, cudaStream_t s);
+cudaError_t launch_log(const float *x, int64_t n, float *y, cudaStream_t s);
+cudaError_t launch_tanh(const float *x, int64_t n, float *y, cudaStream_t s);
+cudaError_t launch_rsqrt(const float *x, int64_t n, float *y, cudaStream_t s);
+cudaError_t launch_gelu(const float *x, int64_t n, float *y, cudaStream_t s);
+cudaError_t launch_gelu_backward(const float *x, const float *dy, int64_t n, float *dx, cudaStream_t s);
+cudaError_t launch_add(const float *a, const float *b, int64_t n, float *y, cudaStream_t s);
+cudaError_t launch_tree_sum(const float *const *parts, int nparts, int64_t n, float *out, cudaStream_t s);
+cudaError_t launch_adamw(float *p, const float *g, float *m, float *v, int64_t n, float lr, float b1, float b2,
+                         float eps, float wd, float bc1, float bc2, float omb1, float omb2, int decay,
+                         cudaStream_t s);
+cudaError_t launch_embedding(const int32_t *tok, int64_t ntok, int64_t T, const float *wte, const float *wpe,
+                             int64_t C, float *x0, cudaStream_t s);
+cudaError_t launch_embedding_backward(const int32_t *tok, int64_t ntok, int64_t T, const float *dx0, int64_t C,
+                                      float *dwte, float *dwpe, cudaStream_t s);
+cudaError_t launch_flip_bit(void *data, int64_t elem, int bit, cudaStream_t s);

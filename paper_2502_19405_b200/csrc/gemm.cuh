@@ -1,0 +1,23 @@
+// gemm.cuh -- parameters of the R-GEMM launch (internal to librepops.so).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+struct GemmParams {
+    int64_t M, N, K;
+    const float *A;
+    int64_t lda, sA0, sA1;
+    const float *B;
+    int64_t ldb, sB0, sB1;
+    float *C;
+    int64_t ldc, sC0, sC1;
+    int64_t batch0, batch1;
+    int transA, transB;
+    int epi;
+    const float *bias;
+    float scale;
+    bool vecA, vecB, vecC;  // 16-byte alignment of every row start (speed only)
+};
+
+// force_cfg: -1 = automatic, 0 = 128x128 tiles, 1 = 64x64 tiles (bits-neutral)
+cudaError_t gemm_launch(const GemmParams &p, cudaStream_t s, int force_cfg);

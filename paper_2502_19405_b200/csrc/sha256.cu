@@ -1,0 +1,413 @@
+// sha256.cu -- Verde tensor commitments on the GPU (R-TCOMMIT, reading R11).
+//
+// The paper commits every tensor entering / leaving a graph node with
+// "a standard collision-resistant hash function like SHA-256" (PAPER.md
+// P:240-244, box P:400-406).  A flat SHA-256 is a strictly sequential chain
+// of compressions; this build cuts each tensor into 4096-byte chunks and
+// commits to their RFC 6962 Merkle tree (R11), which is embarrassingly
+// parallel and lets the referee later descend to one chunk.
+//
+// Launch sequence for a batch of tensors (verde_commit_tensors):
+//   1. leaf kernel   : one thread per 4 KiB chunk -> SHA-256(0x00 || chunk)
+//                      (65 compressions; the 1-byte prefix is absorbed with a
+//                      byte permute per message word: PRMT)
+//   2. reduce passes : one CTA per aligned group of <= 256 nodes of one tensor
+//                      reduces them level by level in shared memory with
+//                      RFC 6962 odd-node promotion (== the recursive MTH,
+//                      because groups are aligned powers of two)
+//   3. header kernel : one thread per tensor -> SHA-256(0x54 || dtype || rank
+//                      || dims || nbytes || 4096 || data_root)
+// SHA-256 is integer-ALU bound on sm_100a (rotates = SHF, Ch/Maj/xor = LOP3,
+// adds = IADD3/IMAD), not HBM bound; see DESIGN.md §5.
+#include <vector>
+
+#include "common.cuh"
+#include "sha256.cuh"
+
+namespace {
+
+__constant__ uint32_t kK[64] = {
+    0x428a2f98, 0x71374491, 0xb5c0fbcf, 0xe9b5dba5, 0x3956c25b, 0x59f111f1, 0x923f82a4, 0xab1c5ed5,
+    0xd807aa98, 0x12835b01, 0x243185be, 0x550c7dc3, 0x72be5d74, 0x80deb1fe, 0x9bdc06a7, 0xc19bf174,
+    0xe49b69c1, 0xefbe4786, 0x0fc19dc6, 0x240ca1cc, 0x2de92c6f, 0x4a7484aa, 0x5cb0a9dc, 0x76f988da,
+    0x983e5152, 0xa831c66d, 0xb00327c8, 0xbf597fc7, 0xc6e00bf3, 0xd5a79147, 0x06ca6351, 0x14292967,
+    0x27b70a85, 0x2e1b2138, 0x4d2c6dfc, 0x53380d13, 0x650a7354, 0x766a0abb, 0x81c2c92e, 0x92722c85,
+    0xa2bfe8a1, 0xa81a664b, 0xc24b8b70, 0xc76c51a3, 0xd192e819, 0xd6990624, 0xf40e3585, 0x106aa070,
+    0x19a4c116, 0x1e376c08, 0x2748774c, 0x34b0bcb5, 0x391c0cb3, 0x4ed8aa4a, 0x5b9cca4f, 0x682e6ff3,
+    0x748f82ee, 0x78a5636f, 0x84c87814, 0x8cc70208, 0x90befffa, 0xa4506ceb, 0xbef9a3f7, 0xc67178f2};
+
+struct Digest { uint32_t h[8]; };
+
+RO_DEV uint32_t rotr(uint32_t x, int n) { return __funnelshift_r(x, x, n); }
+
+RO_DEV void init_state(uint32_t s[8]) {
+    s[0] = 0x6a09e667; s[1] = 0xbb67ae85; s[2] = 0x3c6ef372; s[3] = 0xa54ff53a;
+    s[4] = 0x510e527f; s[5] = 0x9b05688c; s[6] = 0x1f83d9ab; s[7] = 0x5be0cd19;
+}
+
+// FIPS 180-4 compression of one 512-bit block (w = big-endian message words)
+RO_DEV void compress(uint32_t s[8], uint32_t w[16]) {
+    uint32_t a = s[0], b = s[1], c = s[2], d = s[3], e = s[4], f = s[5], g = s[6], h = s[7];
+#pragma unroll
+    for (int t = 0; t < 64; ++t) {
+        uint32_t wt;
+        if (t < 16) {
+            wt = w[t];
+        } else {
+            uint32_t w15 = w[(t - 15) & 15], w2 = w[(t - 2) & 15];
+            uint32_t s0 = rotr(w15, 7) ^ rotr(w15, 18) ^ (w15 >> 3);
+            uint32_t s1 = rotr(w2, 17) ^ rotr(w2, 19) ^ (w2 >> 10);
+            wt = w[t & 15] = w[t & 15] + s0 + w[(t - 7) & 15] + s1;
+        }
+        uint32_t S1 = rotr(e, 6) ^ rotr(e, 11) ^ rotr(e, 25);
+        uint32_t ch = (e & f) ^ (~e & g);
+        uint32_t t1 = h + S1 + ch + kK[t] + wt;
+        uint32_t S0 = rotr(a, 2) ^ rotr(a, 13) ^ rotr(a, 22);
+        uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
+        h = g; g = f; f = e; e = d + t1; d = c; c = b; b = a; a = t1 + S0 + mj;
+    }
+    s[0] += a; s[1] += b; s[2] += c; s[3] += d; s[4] += e; s[5] += f; s[6] += g; s[7] += h;
+}
+
+// SHA-256 of a short local byte message (<= 119 bytes -> at most 2 blocks)
+RO_DEV void sha_small(const uint8_t *msg, int len, uint32_t out[8]) {
+    init_state(out);
+    const int nblk = (len + 9 + 63) / 64;
+    for (int blk = 0; blk < nblk; ++blk) {
+        uint32_t w[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            uint32_t word = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                int m = blk * 64 + i * 4 + q;
+                uint32_t byte;
+                if (m < len) byte = msg[m];
+                else if (m == len) byte = 0x80;
+                else if (m >= nblk * 64 - 8) {
+                    uint64_t bits = (uint64_t)len * 8;
+                    byte = (uint32_t)(bits >> (8 * (nblk * 64 - 1 - m))) & 0xFF;
+                } else byte = 0;
+                word = (word << 8) | byte;
+            }
+            w[i] = word;
+        }
+        compress(out, w);
+    }
+}
+
+// message byte m of (0x00 || data[0..len)) with SHA padding, total blocks nblk
+RO_DEV uint32_t leaf_msg_byte(const uint8_t *data, int64_t len, int64_t m, int64_t nblk) {
+    if (m == 0) return 0x00;
+    if (m <= len) return data[m - 1];
+    if (m == len + 1) return 0x80;
+    if (m >= nblk * 64 - 8) {
+        uint64_t bits = (uint64_t)(len + 1) * 8;
+        return (uint32_t)(bits >> (8 * (nblk * 64 - 1 - m))) & 0xFF;
+    }
+    return 0;
+}
+
+// SHA-256(0x00 || chunk), chunk = data[0..len), len <= 4096
+RO_DEV void hash_leaf(const uint8_t *__restrict__ data, int64_t len, uint32_t st[8]) {
+    init_state(st);
+    const int64_t nblk = (len + 1 + 9 + 63) / 64;
+    const bool al = ro::aligned16(data);
+    int64_t blk = 0;
+    if (al) {
+        // fast path: blocks whose 16 data words D[16j .. 16j+15] are all in range
+        const uint4 *d4 = reinterpret_cast<const uint4 *>(data);
+        uint32_t prev = 0;  // word holding the 0x00 prefix byte in its top byte
+        for (; blk * 64 + 64 <= len; ++blk) {
+            uint32_t D[16];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                uint4 v = __ldg(d4 + blk * 4 + q);
+                D[4 * q] = v.x; D[4 * q + 1] = v.y; D[4 * q + 2] = v.z; D[4 * q + 3] = v.w;
+            }
+            uint32_t w[16];
+            w[0] = __byte_perm(prev, D[0], 0x3456);
+#pragma unroll
+            for (int i = 1; i < 16; ++i) w[i] = __byte_perm(D[i - 1], D[i], 0x3456);
+            prev = D[15];
+            compress(st, w);
+        }
+    }
+    for (; blk < nblk; ++blk) {
+        uint32_t w[16];
+#pragma unroll 4
+        for (int i = 0; i < 16; ++i) {
+            uint32_t word = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) word = (word << 8) | leaf_msg_byte(data, len, blk * 64 + i * 4 + q, nblk);
+            w[i] = word;
+        }
+        compress(st, w);
+    }
+}
+
+// SHA-256(0x01 || L || R) with L, R given as state words (big-endian digest)
+RO_DEV void hash_node(const uint32_t L[8], const uint32_t R[8], uint32_t st[8]) {
+    init_state(st);
+    uint32_t w[16];
+    w[0] = 0x01000000u | (L[0] >> 8);
+#pragma unroll
+    for (int i = 1; i < 8; ++i) w[i] = __funnelshift_r(L[i], L[i - 1], 8);
+    w[8] = __funnelshift_r(R[0], L[7], 8);
+#pragma unroll
+    for (int i = 1; i < 8; ++i) w[8 + i] = __funnelshift_r(R[i], R[i - 1], 8);
+    compress(st, w);
+    w[0] = (R[7] << 24) | 0x00800000u;
+#pragma unroll
+    for (int i = 1; i < 15; ++i) w[i] = 0;
+    w[15] = 65 * 8;
+    compress(st, w);
+}
+
+struct DevTensor {
+    const uint8_t *data;
+    int64_t nbytes;
+    int64_t dims[8];
+    uint8_t *digest;
+    int32_t dtype, rank;
+};
+
+RO_DEV int64_t find_seg(const int64_t *prefix, int n, int64_t g) {
+    // largest t with prefix[t] <= g (prefix nondecreasing, prefix[0] = 0)
+    int lo = 0, hi = n;
+    while (hi - lo > 1) {
+        int mid = (lo + hi) >> 1;
+        if (prefix[mid] <= g) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void leaf_kernel(const DevTensor *__restrict__ ts, int n, const int64_t *__restrict__ chunk_prefix,
+                            int64_t total, Digest *__restrict__ out) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += stride) {
+        int t = (int)find_seg(chunk_prefix, n, g);
+        int64_t c = g - chunk_prefix[t];
+        const DevTensor &T = ts[t];
+        int64_t off = c * 4096;
+        int64_t len = T.nbytes - off < 4096 ? T.nbytes - off : 4096;
+        uint32_t st[8];
+        hash_leaf(T.data + off, len, st);
+        Digest d;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) d.h[i] = st[i];
+        out[g] = d;
+    }
+}
+
+// one CTA (128 threads) per group of <= 256 nodes of one tensor
+__global__ void reduce_kernel(const int64_t *__restrict__ block_prefix, const int64_t *__restrict__ cur_off,
+                              const int64_t *__restrict__ cur_cnt, const int64_t *__restrict__ nxt_off, int n,
+                              const Digest *__restrict__ cur, Digest *__restrict__ nxt) {
+    __shared__ Digest sm[256];
+    const int64_t b = blockIdx.x;
+    const int t = (int)find_seg(block_prefix, n, b);
+    const int64_t j = b - block_prefix[t];
+    const int64_t base = cur_off[t] + j * 256;
+    int cnt = (int)min((int64_t)256, cur_cnt[t] - j * 256);
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) sm[i] = cur[base + i];
+    __syncthreads();
+    while (cnt > 1) {
+        const int pairs = cnt >> 1;
+        Digest r;
+        int i = threadIdx.x;
+        if (i < pairs) hash_node(sm[2 * i].h, sm[2 * i + 1].h, r.h);
+        const bool promote = (cnt & 1) && threadIdx.x == 0;
+        Digest last;
+        if (promote) last = sm[cnt - 1];
+        __syncthreads();
+        if (i < pairs) sm[i] = r;
+        if (promote) sm[pairs] = last;
+        cnt = pairs + (cnt & 1);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) nxt[nxt_off[t] + j] = sm[0];
+}
+
+__global__ void header_kernel(const DevTensor *__restrict__ ts, int n, const int64_t *__restrict__ root_off,
+                              const Digest *__restrict__ roots) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const DevTensor &T = ts[t];
+    uint32_t root[8];
+    if (T.nbytes == 0) {
+        sha_small(nullptr, 0, root);
+    } else {
+        const Digest &d = roots[root_off[t]];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) root[i] = d.h[i];
+    }
+    uint8_t msg[128];
+    int len = 0;
+    msg[len++] = 0x54;
+    msg[len++] = (uint8_t)T.dtype;
+    auto put64 = [&](uint64_t v) {
+        for (int i = 0; i < 8; ++i) msg[len++] = (uint8_t)(v >> (8 * i));
+    };
+    put64((uint64_t)T.rank);
+    for (int i = 0; i < T.rank; ++i) put64((uint64_t)T.dims[i]);
+    put64((uint64_t)T.nbytes);
+    msg[len++] = 0x00; msg[len++] = 0x10; msg[len++] = 0x00; msg[len++] = 0x00;  // u32le 4096
+    for (int i = 0; i < 8; ++i) {
+        msg[len++] = (uint8_t)(root[i] >> 24); msg[len++] = (uint8_t)(root[i] >> 16);
+        msg[len++] = (uint8_t)(root[i] >> 8); msg[len++] = (uint8_t)root[i];
+    }
+    uint32_t out[8];
+    sha_small(msg, len, out);
+    for (int i = 0; i < 8; ++i) {
+        T.digest[4 * i] = (uint8_t)(out[i] >> 24); T.digest[4 * i + 1] = (uint8_t)(out[i] >> 16);
+        T.digest[4 * i + 2] = (uint8_t)(out[i] >> 8); T.digest[4 * i + 3] = (uint8_t)out[i];
+    }
+}
+
+inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+// Host-side plan of one batched commit: tables + workspace layout.
+struct Plan {
+    int n = 0;
+    int64_t total_chunks = 0;
+    std::vector<int64_t> chunk_prefix;                   // n+1
+    struct Pass { std::vector<int64_t> block_prefix, cur_off, cur_cnt, nxt_off; int64_t blocks; bool to_b; };
+    std::vector<Pass> passes;
+    std::vector<int64_t> root_off;                       // n, offsets into the final buffer
+    bool final_in_b = false;
+    int64_t bufA = 0, bufB = 0;                          // digests
+};
+
+Plan make_plan(const verde_tensor_desc *d, int n) {
+    Plan p;
+    p.n = n;
+    p.chunk_prefix.assign(n + 1, 0);
+    std::vector<int64_t> cnt(n);
+    for (int t = 0; t < n; ++t) {
+        cnt[t] = (d[t].nbytes + 4095) / 4096;
+        p.chunk_prefix[t + 1] = p.chunk_prefix[t] + cnt[t];
+    }
+    p.total_chunks = p.chunk_prefix[n];
+    p.bufA = p.total_chunks > 0 ? p.total_chunks : 1;
+    std::vector<int64_t> off(n);
+    for (int t = 0; t < n; ++t) off[t] = p.chunk_prefix[t];
+    bool in_b = false;
+    int64_t maxB = 1;
+    for (;;) {
+        int64_t mx = 0;
+        for (int t = 0; t < n; ++t) mx = cnt[t] > mx ? cnt[t] : mx;
+        if (mx <= 1) break;
+        Plan::Pass ps;
+        ps.block_prefix.assign(n + 1, 0);
+        ps.cur_off = off;
+        ps.cur_cnt = cnt;
+        ps.nxt_off.assign(n, 0);
+        std::vector<int64_t> ncnt(n);
+        int64_t acc = 0;
+        for (int t = 0; t < n; ++t) {
+            int64_t blocks = (cnt[t] + 255) / 256;
+            ps.block_prefix[t + 1] = ps.block_prefix[t] + blocks;
+            ps.nxt_off[t] = acc;
+            ncnt[t] = blocks;
+            acc += blocks;
+        }
+        ps.blocks = ps.block_prefix[n];
+        ps.to_b = !in_b;
+        if (!in_b && acc > maxB) maxB = acc;
+        p.passes.push_back(ps);
+        off = ps.nxt_off;
+        cnt = ncnt;
+        in_b = !in_b;
+    }
+    p.root_off = off;
+    p.final_in_b = in_b;
+    p.bufB = maxB;
+    return p;
+}
+
+struct Layout {
+    int64_t tensors, tables, bufA, bufB, total;
+    std::vector<int64_t> blob;  // int64 tables, concatenated
+    // offsets (in int64 units) of each table inside blob
+    int64_t chunk_prefix_at, root_off_at;
+    std::vector<int64_t> pass_at;  // 4 tables per pass, consecutive
+};
+
+Layout make_layout(const Plan &p) {
+    Layout L;
+    L.chunk_prefix_at = 0;
+    L.blob.insert(L.blob.end(), p.chunk_prefix.begin(), p.chunk_prefix.end());
+    L.root_off_at = (int64_t)L.blob.size();
+    L.blob.insert(L.blob.end(), p.root_off.begin(), p.root_off.end());
+    for (const auto &ps : p.passes) {
+        L.pass_at.push_back((int64_t)L.blob.size());
+        L.blob.insert(L.blob.end(), ps.block_prefix.begin(), ps.block_prefix.end());
+        L.blob.insert(L.blob.end(), ps.cur_off.begin(), ps.cur_off.end());
+        L.blob.insert(L.blob.end(), ps.cur_cnt.begin(), ps.cur_cnt.end());
+        L.blob.insert(L.blob.end(), ps.nxt_off.begin(), ps.nxt_off.end());
+    }
+    L.tensors = 0;
+    L.tables = align_up((int64_t)sizeof(DevTensor) * p.n, 256);
+    L.bufA = L.tables + align_up((int64_t)L.blob.size() * 8, 256);
+    L.bufB = L.bufA + align_up(p.bufA * (int64_t)sizeof(Digest), 256);
+    L.total = L.bufB + align_up(p.bufB * (int64_t)sizeof(Digest), 256);
+    return L;
+}
+
+}  // namespace
+
+int64_t commit_workspace_bytes(const verde_tensor_desc *d, int n) {
+    if (n <= 0) return 0;
+    Plan p = make_plan(d, n);
+    return make_layout(p).total;
+}
+
+cudaError_t commit_launch(const verde_tensor_desc *d, int n, void *ws, int64_t ws_bytes, cudaStream_t s,
+                          int64_t *need) {
+    if (n <= 0) return cudaSuccess;
+    Plan p = make_plan(d, n);
+    Layout L = make_layout(p);
+    *need = L.total;
+    if (ws_bytes < L.total) return cudaErrorMemoryAllocation;
+    uint8_t *base = reinterpret_cast<uint8_t *>(ws);
+    // one staging blob: tensor descriptors then the int64 tables
+    std::vector<uint8_t> host((size_t)L.bufA);
+    std::vector<DevTensor> dt(n);
+    for (int t = 0; t < n; ++t) {
+        dt[t].data = reinterpret_cast<const uint8_t *>(d[t].data);
+        dt[t].nbytes = d[t].nbytes;
+        for (int i = 0; i < 8; ++i) dt[t].dims[i] = (i < d[t].rank) ? d[t].dims[i] : 0;
+        dt[t].digest = d[t].digest;
+        dt[t].dtype = d[t].dtype;
+        dt[t].rank = d[t].rank;
+    }
+    memcpy(host.data(), dt.data(), sizeof(DevTensor) * n);
+    memcpy(host.data() + L.tables, L.blob.data(), L.blob.size() * 8);
+    cudaError_t e = cudaMemcpyAsync(base, host.data(), (size_t)L.bufA, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return e;
+    // the staging buffer must outlive the async copy of pageable memory: cudaMemcpyAsync
+    // from pageable host memory returns only after the data has been staged.
+    const DevTensor *dts = reinterpret_cast<const DevTensor *>(base);
+    const int64_t *tab = reinterpret_cast<const int64_t *>(base + L.tables);
+    Digest *A = reinterpret_cast<Digest *>(base + L.bufA);
+    Digest *B = reinterpret_cast<Digest *>(base + L.bufB);
+    if (p.total_chunks > 0) {
+        int64_t blocks = (p.total_chunks + 127) / 128;
+        int64_t cap = (int64_t)ro_host::num_sms() * 16;
+        if (blocks > cap) blocks = cap;
+        leaf_kernel<<<(unsigned)blocks, 128, 0, s>>>(dts, n, tab + L.chunk_prefix_at, p.total_chunks, A);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    for (size_t q = 0; q < p.passes.size(); ++q) {
+        const auto &ps = p.passes[q];
+        const int64_t *pt = tab + L.pass_at[q];
+        const Digest *cur = ps.to_b ? A : B;
+        Digest *nxt = ps.to_b ? B : A;
+        reduce_kernel<<<(unsigned)ps.blocks, 128, 0, s>>>(pt, pt + (n + 1), pt + (n + 1) + n, pt + (n + 1) + 2 * n, n,
+                                                          cur, nxt);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    header_kernel<<<(n + 63) / 64, 64, 0, s>>>(dts, n, tab + L.root_off_at, p.final_in_b ? B : A);
+    return cudaGetLastError();
+}

@@ -1,0 +1,317 @@
+"""GPU parity: every kernel of librepops.so against the CPU oracle, element by
+element as raw uint32 bit patterns (tolerance 0 ULP, north_star), on seeded
+synthetic inputs from `synth`, through the C ABI (the Python binding only
+marshals arguments).  Sizes span several tiles plus ragged tails; edge cases
+(empty, K = 0, K tails, -0, NaN/Inf, long rows) are included."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+R = None
+
+
+def setup_module(_):
+    global R
+    import paper_2502_19405_b200 as mod
+    R = mod
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def assert_bits(gpu, ref, what=""):
+    g = np.ascontiguousarray(gpu, dtype=np.float32).view(np.uint32)
+    r = np.ascontiguousarray(ref, dtype=np.float32).view(np.uint32)
+    assert g.shape == r.shape, (what, g.shape, r.shape)
+    bad = np.flatnonzero(g.ravel() != r.ravel())
+    assert bad.size == 0, f"{what}: {bad.size} of {g.size} differ; first at {bad[:5]}: " \
+                          f"gpu {g.ravel()[bad[:3]]} oracle {r.ravel()[bad[:3]]}"
+
+
+# ------------------------------------------------------------------ GEMM
+GEMM_SHAPES = [(1, 1, 1), (7, 5, 3), (128, 128, 128), (129, 257, 33), (300, 200, 1000), (64, 96, 17),
+               (513, 130, 7), (5, 700, 256)]
+
+
+@pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
+@pytest.mark.parametrize("tA,tB", [(0, 0), (0, 1), (1, 0), (1, 1)])
+def test_gemm_parity(M, N, K, tA, tB):
+    A, B = synth.gemm_inputs((M, N, K), "gp")
+    Ain = np.ascontiguousarray(A.T) if tA else A
+    Bin = np.ascontiguousarray(B.T) if tB else B
+    ref = oracle.gemm(Ain, Bin, transA=bool(tA), transB=bool(tB))
+    for cfg in (None, 0, 1):
+        got = R.repops_gemm(dev(Ain), dev(Bin), transA=bool(tA), transB=bool(tB), cfg=cfg)
+        assert_bits(host(got), ref, f"gemm {M}x{N}x{K} tA{tA} tB{tB} cfg{cfg}")
+
+
+def test_gemm_epilogues_and_edge_cases():
+    A, B = synth.gemm_inputs((70, 90, 45), "ge")
+    bias = synth.uniform(5, 90)
+    ref = oracle.gemm(A, B, epi=1, bias=bias)
+    assert_bits(host(R.repops_gemm(dev(A), dev(B), epi=R.EPI_BIAS, bias=dev(bias))), ref, "bias")
+    ref = oracle.gemm(A, B, epi=2, scale=0.125)
+    assert_bits(host(R.repops_gemm(dev(A), dev(B), epi=R.EPI_SCALE, scale=0.125)), ref, "scale")
+    # K = 0: C = epi(+0)
+    Z = R.repops_gemm(torch.empty((3, 0), device="cuda"), torch.empty((0, 4), device="cuda"))
+    assert np.all(host(Z).view(np.uint32) == 0)
+    # underflow to -0 inside the K fold: K tail must not be zero padded
+    a = np.array([[-2.0 ** -80, 2.0 ** -80, 0.0]], np.float32)
+    b = np.array([[2.0 ** -80], [0.0], [0.0]], np.float32)
+    ref = oracle.gemm(a[:, :2], b[:2])
+    assert_bits(host(R.repops_gemm(dev(a[:, :2].copy()), dev(b[:2].copy()))), ref, "neg-zero")
+    # NaN / Inf propagate and NaN is canonical
+    A2 = A.copy()
+    A2[3, 4] = np.inf
+    A2[5, 6] = np.nan
+    B2 = B.copy()
+    B2[7, 8] = 0.0
+    ref = oracle.gemm(A2, B2)
+    assert_bits(host(R.repops_gemm(dev(A2), dev(B2))), ref, "nan/inf")
+
+
+def test_gemm_unaligned_leading_dims():
+    A, B = synth.gemm_inputs((67, 45, 131), "gu")
+    # view with ld = 133 (not a multiple of 4) and an offset start
+    big = np.zeros((67, 134), np.float32)
+    big[:, 1:132] = A
+    tA = dev(big)[:, 1:132]
+    ref = oracle.gemm(A, B)
+    assert_bits(host(R.repops_gemm(tA, dev(B))), ref, "unaligned")
+
+
+def test_gemm_strided_batched_attention_layout():
+    # QK^T per (sequence, head) inside a packed QKV buffer, as in the GPT-2 step
+    Bsz, T, H, hd = 2, 96, 3, 16
+    D = H * hd
+    qkv = synth.uniform(9, (Bsz * T, 3 * D))
+    S = torch.empty((Bsz * H * T, T), device="cuda")
+    q = dev(qkv)
+    R.repops_gemm_strided_batched(q, q, S, M=T, N=T, K=hd, lda=3 * D, ldb=3 * D, ldc=T,
+                                  sA=(T * 3 * D, hd), sB=(T * 3 * D, hd), sC=(H * T * T, T * T),
+                                  batch=(Bsz, H), transB=True, epi=R.EPI_SCALE, scale=0.25, offA=0, offB=D)
+    got = host(S)
+    for b in range(Bsz):
+        for h in range(H):
+            Q = qkv[b * T:(b + 1) * T, h * hd:(h + 1) * hd]
+            K = qkv[b * T:(b + 1) * T, D + h * hd:D + (h + 1) * hd]
+            ref = oracle.gemm(Q, K, transB=True, epi=2, scale=0.25)
+            assert_bits(got[(b * H + h) * T:(b * H + h + 1) * T], ref, f"batch {b},{h}")
+
+
+@pytest.mark.parametrize("n", [1024, 2048, 8192])
+def test_gemm_full_size_sampled(n):
+    # BASELINE config 2 sizes in the launch configuration bench.py times; the
+    # oracle recomputes sampled elements one by one (full K fold each)
+    A, B = synth.gemm_inputs(n, "bench")
+    got = host(R.repops_gemm(dev(A), dev(B)))
+    rng = np.random.default_rng(n)
+    idx = [(0, 0), (n - 1, n - 1), (n - 1, 0), (0, n - 1)] + [tuple(x) for x in rng.integers(0, n, (60, 2))]
+    for i, j in idx:
+        r = oracle.gemm_element(A, B, i, j)
+        assert got[i, j].view(np.uint32) == np.float32(r).view(np.uint32), (i, j)
+
+
+# ------------------------------------------------------------------ reductions
+@pytest.mark.parametrize("cols", [1, 5, 127, 128, 129, 768, 4095, 4096, 4097, 50257, 3 * 4096 + 11])
+def test_sum_rows_parity(cols):
+    x = synth.uniform(synth.seed_for("sr", cols), (9, cols), 3.0)
+    x[0, :min(cols, 3)] = -0.0
+    ref = oracle.sum_rows(x)
+    assert_bits(host(R.repops_sum_rows(dev(x))), ref, f"sum_rows {cols}")
+
+
+def test_sum_rows_order_pins_on_gpu():
+    x = np.ones((1, 4098), np.float32)
+    x[0, 0] = 2.0 ** 24
+    assert host(R.repops_sum_rows(dev(x)))[0] == 16781282.0
+    y = np.zeros((1, 66), np.float32)
+    y[0, 0], y[0, 1], y[0, 65] = 2.0 ** 24, 1, 1
+    assert host(R.repops_sum_rows(dev(y)))[0] == 16777218.0
+
+
+def test_sum_cols_seq_parity():
+    x = synth.uniform(3, (512 * 4, 333))
+    ref = oracle.sum_cols_seq(x, nseg=4)
+    assert_bits(host(R.repops_sum_cols_seq(dev(x), nseg=4)), ref, "seq")
+
+
+@pytest.mark.parametrize("nparts", [1, 2, 4, 8])
+def test_tree_sum_parity(nparts):
+    parts = [synth.uniform(50 + i, 100003) for i in range(nparts)]
+    ref = oracle.tree_sum(parts)
+    assert_bits(host(R.repops_tree_sum([dev(p) for p in parts])), ref, f"tree {nparts}")
+
+
+# ------------------------------------------------------------------ row operators
+@pytest.mark.parametrize("rows,cols,causal", [(37, 5, False), (96, 512, True), (64, 512, False),
+                                              (8, 2048, True), (6, 4096, False), (3, 4097, False),
+                                              (2, 50257, False), (4096 * 2, 4096, True)])
+def test_softmax_parity(rows, cols, causal):
+    if rows * cols > 2 ** 25:
+        rows = (2 ** 25 // cols) // cols * cols or cols
+    x = synth.uniform(synth.seed_for("sm", rows, cols), (rows, cols), 6.0)
+    ref = oracle.softmax(x, causal=causal)
+    assert_bits(host(R.repops_softmax(dev(x), causal=causal)), ref, f"softmax {rows}x{cols} c{causal}")
+
+
+def test_softmax_special_values():
+    x = synth.uniform(4, (6, 300), 2.0)
+    x[0, 5] = np.nan
+    x[1, :] = -np.inf
+    x[2, 7] = np.inf
+    x[3, :] = 0.0
+    x[3, 9] = -0.0
+    x[4, 3] = -np.inf
+    ref = oracle.softmax(x)
+    assert_bits(host(R.repops_softmax(dev(x))), ref, "softmax specials")
+
+
+@pytest.mark.parametrize("rows,cols", [(96, 512), (13, 77), (4, 5000)])
+def test_softmax_backward_parity(rows, cols):
+    y = oracle.softmax(synth.uniform(7, (rows, cols), 3.0))
+    dy = synth.uniform(8, (rows, cols))
+    ref = oracle.softmax_backward(y, dy, scale=0.125)
+    assert_bits(host(R.repops_softmax_backward(dev(y), dev(dy), scale=0.125)), ref, "softmax bwd")
+
+
+@pytest.mark.parametrize("rows,cols", [(64, 768), (33, 100), (5, 4096), (3, 1)])
+def test_layernorm_parity(rows, cols):
+    x = synth.uniform(1, (rows, cols), 2.0)
+    g = synth.uniform(2, cols)
+    b = synth.uniform(3, cols)
+    y, mean, rstd = oracle.layernorm(x, g, b)
+    gy, gm, gr = R.repops_layernorm(dev(x), dev(g), dev(b))
+    assert_bits(host(gy), y, "ln y")
+    assert_bits(host(gm), mean, "ln mean")
+    assert_bits(host(gr), rstd, "ln rstd")
+    dy = synth.uniform(4, (rows, cols))
+    dres = synth.uniform(5, (rows, cols))
+    dx = oracle.layernorm_backward(dy, x, g, mean, rstd, dres=dres)
+    assert_bits(host(R.repops_layernorm_backward(dev(dy), dev(x), dev(g), gm, gr, dres=dev(dres))), dx, "ln dx")
+    dx0 = oracle.layernorm_backward(dy, x, g, mean, rstd)
+    assert_bits(host(R.repops_layernorm_backward(dev(dy), dev(x), dev(g), gm, gr)), dx0, "ln dx nores")
+    if rows % 1 == 0:
+        nseg = 1 if rows % 4 else 4
+        dgm, dbt = oracle.layernorm_backward_params(dy, x, mean, rstd, nseg=nseg)
+        gdg, gdb = R.repops_layernorm_backward_params(dev(dy), dev(x), gm, gr, nseg=nseg)
+        assert_bits(host(gdg), dgm, "dgamma")
+        assert_bits(host(gdb), dbt, "dbeta")
+
+
+@pytest.mark.parametrize("rows,V", [(8, 4), (16, 1000), (6, 50257)])
+def test_cross_entropy_parity(rows, V):
+    x = synth.uniform(11, (rows, V), 8.0)
+    lab = synth.integers(12, rows, V)
+    loss, d = oracle.cross_entropy(x, lab, scale=2.0 ** -12)
+    gl, gd = R.repops_cross_entropy(dev(x), dev(lab), scale=2.0 ** -12)
+    assert_bits(host(gl), loss, "ce loss")
+    assert_bits(host(gd), d, "ce grad")
+    # in place (dlogits aliasing logits), padded leading dimension
+    ld = V + 47
+    xp = np.zeros((rows, ld), np.float32)
+    xp[:, :V] = x
+    t = dev(xp)
+    gl2, _ = R.repops_cross_entropy(t, dev(lab), scale=2.0 ** -12, dlogits=t, V=V)
+    assert_bits(host(gl2), loss, "ce loss padded")
+    assert_bits(host(t)[:, :V], d, "ce grad in place")
+
+
+# ------------------------------------------------------------------ elementwise / math
+def _sweep(stride, lo=0, hi=2 ** 32):
+    return np.arange(lo, hi, stride, dtype=np.uint64).astype(np.uint32).view(np.float32)
+
+
+@pytest.mark.parametrize("name", ["exp", "log", "tanh", "rsqrt"])
+def test_math_sweep_all_floats(name):
+    # a stride-1009 sweep of ALL 2^32 bit patterns (NaNs, infs, subnormals, both signs)
+    x = _sweep(1009)
+    x = np.concatenate([x, np.float32([0.0, -0.0, np.inf, -np.inf, np.nan, 88.72283172607422,
+                                       88.72283935546875, -104.0, -103.99999, 89.0, 1.17549435e-38])])
+    ref = getattr(oracle, name)(x)
+    got = getattr(R, "repops_" + name)(dev(x))
+    assert_bits(host(got), ref, name)
+
+
+def test_gelu_parity():
+    x = np.concatenate([synth.uniform(1, 1000003, 8.0), np.float32([0, -0.0, 30, -30, np.nan, np.inf, -np.inf])])
+    assert_bits(host(R.repops_gelu(dev(x))), oracle.gelu(x), "gelu")
+    dy = synth.uniform(2, x.size)
+    assert_bits(host(R.repops_gelu_backward(dev(x), dev(dy))), oracle.gelu_backward(x, dy), "gelu bwd")
+
+
+def test_add_parity():
+    a = synth.uniform(1, 100001)
+    b = synth.uniform(2, 100001)
+    a[:3] = [-0.0, np.nan, np.inf]
+    b[:3] = [-0.0, 1.0, -np.inf]
+    assert_bits(host(R.repops_add(dev(a), dev(b))), oracle.add(a, b), "add")
+
+
+def test_embedding_parity():
+    V, T, Cc, ntok = 1000, 64, 96, 256
+    wte = synth.uniform(1, (V, Cc))
+    wpe = synth.uniform(2, (T, Cc))
+    tok = synth.integers(3, ntok, 50)  # many repeats
+    x0 = oracle.embedding(tok, wte, wpe, T)
+    assert_bits(host(R.repops_embedding(dev(tok), dev(wte), dev(wpe), T)), x0, "emb fwd")
+    dx0 = synth.uniform(4, (ntok, Cc))
+    inc_te = synth.uniform(5, (V, Cc))
+    inc_pe = synth.uniform(6, (T, Cc))
+    rte, rpe = oracle.embedding_backward(tok, dx0, T, inc_te, inc_pe)
+    gte, gpe = dev(inc_te), dev(inc_pe)
+    R.repops_embedding_backward(dev(tok), dev(dx0), T, gte, gpe)
+    assert_bits(host(gte), rte, "emb bwd wte")
+    assert_bits(host(gpe), rpe, "emb bwd wpe")
+
+
+def test_adamw_parity():
+    n = 100003
+    p, g = synth.uniform(1, n), synth.uniform(2, n)
+    m, v = synth.uniform(3, n, 0.01), np.abs(synth.uniform(4, n, 0.001))
+    for step, decay in ((1, True), (7, False), (1000, True)):
+        rp, rm, rv = oracle.adamw(p, g, m, v, step, 6e-4, 0.9, 0.95, 1e-8, 0.1, decay)
+        tp, tm, tv = dev(p), dev(m), dev(v)
+        R.repops_adamw(tp, dev(g), tm, tv, step, 6e-4, 0.9, 0.95, 1e-8, 0.1, decay)
+        assert_bits(host(tp), rp, "adam p")
+        assert_bits(host(tm), rm, "adam m")
+        assert_bits(host(tv), rv, "adam v")
+
+
+# ------------------------------------------------------------------ Verde commitments
+def test_commit_parity_and_batching():
+    shapes = [(0,), (1,), (1023,), (1024,), (1025,), (3, 4096), (257, 1000), (4096 * 70 + 3,), (5, 7, 11)]
+    arrs = [synth.uniform(synth.seed_for("cm", s), s) for s in shapes]
+    refs = [oracle.commit_tensor(a) for a in arrs]
+    ts = [dev(a) for a in arrs]
+    ws = R.CommitWorkspace()
+    digs = host(R.verde_commit_tensors(ts, ws=ws))
+    for i, r in enumerate(refs):
+        assert digs[i].tobytes() == r, shapes[i]
+    # one at a time gives the same digests
+    for t, r in zip(ts, refs):
+        assert host(R.verde_commit_tensor(t, ws=ws)).tobytes() == r
+
+
+def test_commit_large_tensor_multi_pass():
+    # > 256*256 leaves -> three reduce passes (logits-sized tensors)
+    a = synth.uniform(77, 256 * 256 * 1024 + 12345)  # 268 MB
+    t = dev(a)
+    got = host(R.verde_commit_tensor(t)).tobytes()
+    assert got == oracle.commit_tensor(a)
+    R.repops_flip_bit(t, 123456789, 0)
+    b = a.copy()
+    b.view(np.uint32)[123456789] ^= 1
+    got2 = host(R.verde_commit_tensor(t)).tobytes()
+    assert got2 == oracle.commit_tensor(b) and got2 != got
