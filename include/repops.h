@@ -54,6 +54,9 @@ enum verde_dtype { VERDE_F32 = 1, VERDE_I32 = 2, VERDE_U8 = 3 };
 
 int repops_abi_version(void);
 const char *repops_last_error(void);
+/* Number of kernels this library has enqueued in this process (all threads).
+ * bench.py reports the difference across its timed region as gpu_launches. */
+int64_t repops_launch_count(void);
 
 /* ------------------------------------------------------------------ GEMM
  * R-GEMM, PAPER.md P:598-609 (Sec. 3.2 listing): for every (i, j)
@@ -181,7 +184,18 @@ typedef struct {
     int32_t rank;       /* 0..8 */
     int64_t dims[8];
     uint8_t *digest;    /* device, 32 bytes */
+    int32_t mode;       /* 0 = tensor digest; 1 = data_root only (MTH over chunks, no header) */
+    int32_t reserved;
 } verde_tensor_desc;
+
+/* Digest of a tensor whose byte image was committed as k equal, contiguous
+ * slabs (one per GPU, mode = 1): each slab must hold 2^j whole 4096-byte
+ * chunks, so every slab root is an aligned RFC 6962 subtree and the tensor's
+ * data_root is the plain binary tree SHA-256(0x01 || L || R) over the k slab
+ * roots (k a power of two).  Identical to committing the whole tensor.
+ * subroots, dims, out32: host.  EINVAL if the slab geometry is not aligned. */
+int verde_digest_from_subroots(const uint8_t *subroots, int64_t k, int dtype, int rank, const int64_t *dims,
+                               int64_t nbytes, uint8_t *out32);
 
 /* Workspace (device bytes) needed to commit the given tensors in one call. */
 int64_t verde_commit_workspace_bytes(const verde_tensor_desc *descs /* host */, int n);

@@ -134,6 +134,7 @@ def gemm_element(A, B, i, j, transA=False, transB=False, epi=0, bias=None, scale
     K = A.shape[0] if transA else A.shape[1]
     lda = A.shape[1]
     ldb = B.shape[1]
+    i, j = int(i), int(j)
     a_off = i if transA else i * lda
     b_off = j * ldb if transB else j
     out = np.empty((1, 1), dtype=np.float32)

@@ -25,7 +25,8 @@ __all__ = [
     "repops_rsqrt", "repops_gelu", "repops_gelu_backward", "repops_add", "repops_embedding",
     "repops_embedding_backward", "repops_adamw", "repops_flip_bit", "verde_commit_tensor",
     "verde_commit_tensors", "verde_merkle_root", "verde_sha256", "verde_node_digest",
-    "verde_first_divergence", "CommitWorkspace", "RepopsError", "header_symbols", "lib",
+    "verde_first_divergence", "verde_digest_from_subroots", "launch_count", "CommitWorkspace", "RepopsError",
+    "header_symbols", "lib",
 ]
 
 
@@ -289,7 +290,7 @@ class CommitWorkspace:
         return self.buf
 
 
-def _desc(t, digest) -> TensorDesc:
+def _desc(t, digest, mode=0) -> TensorDesc:
     if not t.is_contiguous():
         raise RepopsError("committed tensors must be contiguous")
     d = TensorDesc()
@@ -300,17 +301,19 @@ def _desc(t, digest) -> TensorDesc:
     for i, s in enumerate(t.shape):
         d.dims[i] = s
     d.digest = digest.data_ptr()
+    d.mode = mode
     return d
 
 
-def verde_commit_tensors(tensors, digests=None, ws: CommitWorkspace | None = None, stream=None):
+def verde_commit_tensors(tensors, digests=None, ws: CommitWorkspace | None = None, stream=None, mode=0):
     """R-TCOMMIT for a list of tensors in one batched launch sequence.  Returns a
-    (n, 32) uint8 CUDA tensor of digests (written asynchronously)."""
+    (n, 32) uint8 CUDA tensor of digests (written asynchronously).  mode=1
+    returns data roots (slab subtree roots) instead of digests."""
     n = len(tensors)
     dev = tensors[0].device
     if digests is None:
         digests = torch.empty((n, 32), dtype=torch.uint8, device=dev)
-    arr = (TensorDesc * n)(*[_desc(t, digests[i]) for i, t in enumerate(tensors)])
+    arr = (TensorDesc * n)(*[_desc(t, digests[i], mode) for i, t in enumerate(tensors)])
     need = lib().verde_commit_workspace_bytes(arr, n)
     ws = ws or CommitWorkspace(dev)
     buf = ws.get(need)
@@ -320,6 +323,22 @@ def verde_commit_tensors(tensors, digests=None, ws: CommitWorkspace | None = Non
 
 def verde_commit_tensor(t, ws: CommitWorkspace | None = None, stream=None):
     return verde_commit_tensors([t], ws=ws, stream=stream)[0]
+
+
+def verde_digest_from_subroots(subroots: bytes, dtype: int, shape, nbytes: int) -> bytes:
+    """Digest of a tensor committed as k = len(subroots)/32 aligned slabs (mode=1)."""
+    k = len(subroots) // 32
+    dims = (C.c_int64 * max(len(shape), 1))(*shape)
+    buf = C.create_string_buffer(bytes(subroots), max(len(subroots), 1))
+    out = C.create_string_buffer(32)
+    check(lib().verde_digest_from_subroots(buf, k, int(dtype), len(shape), dims, int(nbytes), out),
+          "verde_digest_from_subroots")
+    return out.raw
+
+
+def launch_count() -> int:
+    """Kernels enqueued by librepops.so in this process so far."""
+    return lib().repops_launch_count()
 
 
 def verde_merkle_root(digests: list[bytes] | bytes) -> bytes:

@@ -19,7 +19,7 @@ i64, i32, f32, vp, u8p = C.c_int64, C.c_int, C.c_float, C.c_void_p, C.c_void_p
 class TensorDesc(C.Structure):
     """verde_tensor_desc (repops.h)"""
     _fields_ = [("data", C.c_void_p), ("nbytes", C.c_int64), ("dtype", C.c_int32), ("rank", C.c_int32),
-                ("dims", C.c_int64 * 8), ("digest", C.c_void_p)]
+                ("dims", C.c_int64 * 8), ("digest", C.c_void_p), ("mode", C.c_int32), ("reserved", C.c_int32)]
 
 
 class Node(C.Structure):
@@ -34,6 +34,7 @@ class Node(C.Structure):
 SIGNATURES = {
     "repops_abi_version": (i32, []),
     "repops_last_error": (C.c_char_p, []),
+    "repops_launch_count": (i64, []),
     "repops_gemm": (i32, [i64, i64, i64, vp, i64, i32, vp, i64, i32, i32, vp, f32, vp, i64, vp]),
     "repops_gemm_strided_batched": (i32, [i64, i64, i64, vp, i64, i32, i64, i64, vp, i64, i32, i64, i64,
                                           i32, vp, f32, vp, i64, i64, i64, i64, i64, vp]),
@@ -62,6 +63,7 @@ SIGNATURES = {
     "verde_commit_tensors": (i32, [vp, i32, vp, i64, vp]),
     "verde_commit_tensor": (i32, [vp, i64, i32, i32, vp, vp, vp, i64, vp]),
     "verde_merkle_root": (i32, [vp, i64, vp]),
+    "verde_digest_from_subroots": (i32, [vp, i64, i32, i32, vp, i64, vp]),
     "verde_sha256": (i32, [vp, i64, vp]),
     "verde_node_digest": (i32, [vp, vp]),
     "verde_first_divergence": (i32, [vp, vp, i64, vp, vp]),

@@ -5,6 +5,7 @@
 // of small host buffers, the step Merkle root, node digests, divergence
 // search).  Every compute step on a tensor runs in the kernels of gemm.cu,
 // rowops.cu, elementwise.cu and sha256.cu.
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -32,8 +33,15 @@ int fail(int code, const char *fmt, ...) {
     return code;
 }
 
+std::atomic<int64_t> g_launches{0};
+
+// every launcher behind cuda_status() enqueues exactly one kernel on success
+// (verde_commit_tensors adds its extra kernels itself)
 int cuda_status(cudaError_t e, const char *what) {
-    if (e == cudaSuccess) return REPOPS_OK;
+    if (e == cudaSuccess) {
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return REPOPS_OK;
+    }
     return fail(REPOPS_ECUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
@@ -163,6 +171,7 @@ int num_sms() {
 extern "C" {
 
 int repops_abi_version(void) { return REPOPS_ABI_VERSION; }
+int64_t repops_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 const char *repops_last_error(void) { return g_err.c_str(); }
 
 // ------------------------------------------------------------------ GEMM
@@ -395,9 +404,11 @@ int verde_commit_tensors(const verde_tensor_desc *descs, int n, void *ws, int64_
     }
     REQ(ws != nullptr, "commit: null workspace");
     int64_t need = 0;
-    cudaError_t e = commit_launch(descs, n, ws, ws_bytes, S(stream), &need);
+    int nk = 0;
+    cudaError_t e = commit_launch(descs, n, ws, ws_bytes, S(stream), &need, &nk);
     if (e == cudaErrorMemoryAllocation && ws_bytes < need)
         return fail(REPOPS_ENOSPACE, "commit: workspace %lld < %lld bytes", (long long)ws_bytes, (long long)need);
+    if (e == cudaSuccess) g_launches.fetch_add(nk - 1, std::memory_order_relaxed);
     return cuda_status(e, "commit");
 }
 
@@ -412,6 +423,30 @@ int verde_commit_tensor(const void *data, int64_t nbytes, int dtype, int rank, c
     for (int i = 0; i < rank; ++i) d.dims[i] = dims[i];
     d.digest = digest32;
     return verde_commit_tensors(&d, 1, ws, ws_bytes, stream);
+}
+
+int verde_digest_from_subroots(const uint8_t *subroots, int64_t k, int dtype, int rank, const int64_t *dims,
+                               int64_t nbytes, uint8_t *out32) {
+    REQ(subroots && out32 && k >= 1 && (k & (k - 1)) == 0, "digest_from_subroots: k must be a power of two");
+    REQ(rank >= 0 && rank <= 8 && (rank == 0 || dims), "digest_from_subroots: bad rank");
+    REQ(nbytes > 0 && nbytes % (k * 4096) == 0, "digest_from_subroots: slabs must be whole 4096-byte chunks");
+    int64_t chunks = nbytes / k / 4096;
+    REQ((chunks & (chunks - 1)) == 0, "digest_from_subroots: slab chunk count must be a power of two");
+    std::vector<Node32> level((size_t)k);
+    for (int64_t i = 0; i < k; ++i) memcpy(level[i].b, subroots + 32 * i, 32);
+    while (level.size() > 1) {
+        std::vector<Node32> nxt(level.size() / 2);
+        for (size_t i = 0; i < nxt.size(); ++i) {
+            Sha256 h;
+            h.u8(0x01).put(level[2 * i].b, 32).put(level[2 * i + 1].b, 32).done(nxt[i].b);
+        }
+        level.swap(nxt);
+    }
+    Sha256 h;
+    h.u8(0x54).u8((uint8_t)dtype).u64((uint64_t)rank);
+    for (int i = 0; i < rank; ++i) h.u64((uint64_t)dims[i]);
+    h.u64((uint64_t)nbytes).u32(4096).put(level[0].b, 32).done(out32);
+    return REPOPS_OK;
 }
 
 int verde_merkle_root(const uint8_t *leaves, int64_t n, uint8_t *root32) {

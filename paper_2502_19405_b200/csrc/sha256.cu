@@ -169,7 +169,7 @@ struct DevTensor {
     int64_t nbytes;
     int64_t dims[8];
     uint8_t *digest;
-    int32_t dtype, rank;
+    int32_t dtype, rank, mode;
 };
 
 RO_DEV int64_t find_seg(const int64_t *prefix, int n, int64_t g) {
@@ -258,7 +258,11 @@ __global__ void header_kernel(const DevTensor *__restrict__ ts, int n, const int
         msg[len++] = (uint8_t)(root[i] >> 8); msg[len++] = (uint8_t)root[i];
     }
     uint32_t out[8];
-    sha_small(msg, len, out);
+    if (T.mode == 1) {
+        for (int i = 0; i < 8; ++i) out[i] = root[i];  // data_root only (slab of a sharded tensor)
+    } else {
+        sha_small(msg, len, out);
+    }
     for (int i = 0; i < 8; ++i) {
         T.digest[4 * i] = (uint8_t)(out[i] >> 24); T.digest[4 * i + 1] = (uint8_t)(out[i] >> 16);
         T.digest[4 * i + 2] = (uint8_t)(out[i] >> 8); T.digest[4 * i + 3] = (uint8_t)out[i];
@@ -364,7 +368,7 @@ int64_t commit_workspace_bytes(const verde_tensor_desc *d, int n) {
 }
 
 cudaError_t commit_launch(const verde_tensor_desc *d, int n, void *ws, int64_t ws_bytes, cudaStream_t s,
-                          int64_t *need) {
+                          int64_t *need, int *nkernels) {
     if (n <= 0) return cudaSuccess;
     Plan p = make_plan(d, n);
     Layout L = make_layout(p);
@@ -381,6 +385,7 @@ cudaError_t commit_launch(const verde_tensor_desc *d, int n, void *ws, int64_t w
         dt[t].digest = d[t].digest;
         dt[t].dtype = d[t].dtype;
         dt[t].rank = d[t].rank;
+        dt[t].mode = d[t].mode;
     }
     memcpy(host.data(), dt.data(), sizeof(DevTensor) * n);
     memcpy(host.data() + L.tables, L.blob.data(), L.blob.size() * 8);
@@ -408,6 +413,7 @@ cudaError_t commit_launch(const verde_tensor_desc *d, int n, void *ws, int64_t w
                                                           cur, nxt);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
+    *nkernels = (p.total_chunks > 0 ? 1 : 0) + (int)p.passes.size() + 1;
     header_kernel<<<(n + 63) / 64, 64, 0, s>>>(dts, n, tab + L.root_off_at, p.final_in_b ? B : A);
     return cudaGetLastError();
 }

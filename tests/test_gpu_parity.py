@@ -155,8 +155,9 @@ def test_tree_sum_parity(nparts):
 
 
 # ------------------------------------------------------------------ row operators
-@pytest.mark.parametrize("rows,cols,causal", [(37, 5, False), (96, 512, True), (64, 512, False),
-                                              (8, 2048, True), (6, 4096, False), (3, 4097, False),
+@pytest.mark.parametrize("rows,cols,causal", [(37, 5, False), (2 * 512, 512, True), (64, 512, False),
+                                              (2048, 2048, True), (6, 4096, False), (3, 4097, False),
+                                              (3 * 5000, 5000, True),
                                               (2, 50257, False), (4096 * 2, 4096, True)])
 def test_softmax_parity(rows, cols, causal):
     if rows * cols > 2 ** 25:
@@ -310,8 +311,8 @@ def test_commit_large_tensor_multi_pass():
     t = dev(a)
     got = host(R.verde_commit_tensor(t)).tobytes()
     assert got == oracle.commit_tensor(a)
-    R.repops_flip_bit(t, 123456789, 0)
+    R.repops_flip_bit(t, 12345678, 0)
     b = a.copy()
-    b.view(np.uint32)[123456789] ^= 1
+    b.view(np.uint32)[12345678] ^= 1
     got2 = host(R.verde_commit_tensor(t)).tobytes()
     assert got2 == oracle.commit_tensor(b) and got2 != got

@@ -1,4 +1,6 @@
 """Quick device timing of the main kernels (CUDA events, not a bench number)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import sys, time
 import torch
 import paper_2502_19405_b200 as R
