@@ -222,7 +222,7 @@ int repops_gemm_strided_batched(int64_t M, int64_t N, int64_t K, const float *A,
 int repops_gemm_cfg(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, int transA, const float *B,
                     int64_t ldb, int transB, int epi, const float *bias, float scale, float *C, int64_t ldc,
                     void *stream, int cfg) {
-    REQ(cfg >= 0 && cfg <= 1, "gemm_cfg: cfg must be 0 or 1");
+    REQ(cfg >= 0 && cfg < gemm_num_cfgs(), "gemm_cfg: unknown tile configuration %d", cfg);
     return gemm_common(M, N, K, A, lda, transA, 0, 0, B, ldb, transB, 0, 0, epi, bias, scale, C, ldc, 0, 0, 1, 1,
                        stream, cfg);
 }

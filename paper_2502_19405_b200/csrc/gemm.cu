@@ -73,7 +73,7 @@ RO_DEV void tile_async(float *dst, const float *__restrict__ src, int64_t ld, in
     }
 }
 
-template <int BM, int BN, int BK, int TM, int TN, bool TA, bool TB>
+template <int BM, int BN, int BK, int TM, int TN, bool TA, bool TB, int KGO = 0>
 struct Cfg {
     static constexpr int TX = BN / TN;          // threads along n
     static constexpr int TY = BM / TM;          // threads along m
@@ -85,12 +85,12 @@ struct Cfg {
     static constexpr int B_WORDS = TB ? BN * SKP : BK * BN;
     static constexpr int STAGE_WORDS = A_WORDS + B_WORDS;
     // k-group width for k-contiguous operands (LDS.64 when both are k-contiguous)
-    static constexpr int KG = (!TA && TB) ? 2 : 4;
+    static constexpr int KG = KGO ? KGO : ((!TA && TB) ? 2 : 4);
 };
 
-template <int BM, int BN, int BK, int TM, int TN, int STAGES, bool TA, bool TB, bool VEC>
-__global__ void __launch_bounds__((BM / TM) * (BN / TN), 2) gemm_kernel(GemmParams p) {
-    using CF = Cfg<BM, BN, BK, TM, TN, TA, TB>;
+template <int BM, int BN, int BK, int TM, int TN, int STAGES, int MINB, int KGO, bool TA, bool TB, bool VEC>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB) gemm_kernel(GemmParams p) {
+    using CF = Cfg<BM, BN, BK, TM, TN, TA, TB, KGO>;
     constexpr int THREADS = CF::THREADS;
     constexpr int TX = CF::TX, TY = CF::TY, SKP = CF::SKP, KG = CF::KG;
     extern __shared__ __align__(16) float smem[];
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), 2) gemm_kernel(GemmPara
         if (kmax == BK) {
 #pragma unroll
             for (int kg = 0; kg < BK; kg += KG) {
-                float ak[TA ? 1 : TM][KG], bk[TB ? 1 : TN][KG];
+                float ak[TA ? 1 : TM][KG], bk[TB ? TN : 1][KG];
                 if (!TA) {
 #pragma unroll
                     for (int i = 0; i < TM; ++i) {
@@ -278,11 +278,11 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), 2) gemm_kernel(GemmPara
     }
 }
 
-template <int BM, int BN, int BK, int TM, int TN, int STAGES, bool TA, bool TB, bool VEC>
+template <int BM, int BN, int BK, int TM, int TN, int STAGES, int MINB, int KGO, bool TA, bool TB, bool VEC>
 cudaError_t launch_one(const GemmParams &p, cudaStream_t s) {
-    using CF = Cfg<BM, BN, BK, TM, TN, TA, TB>;
+    using CF = Cfg<BM, BN, BK, TM, TN, TA, TB, KGO>;
     const size_t smem = (size_t)STAGES * CF::STAGE_WORDS * sizeof(float);
-    auto kern = gemm_kernel<BM, BN, BK, TM, TN, STAGES, TA, TB, VEC>;
+    auto kern = gemm_kernel<BM, BN, BK, TM, TN, STAGES, MINB, KGO, TA, TB, VEC>;
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -295,13 +295,13 @@ cudaError_t launch_one(const GemmParams &p, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-template <int BM, int BN, int BK, int TM, int TN, int STAGES>
+template <int BM, int BN, int BK, int TM, int TN, int STAGES, int MINB, int KGO = 0>
 cudaError_t launch_cfg(const GemmParams &p, cudaStream_t s) {
     const bool vec = p.vecA && p.vecB;
-#define RO_GEMM_CASE(TA_, TB_)                                                             \
-    if ((bool)p.transA == TA_ && (bool)p.transB == TB_)                                    \
-        return vec ? launch_one<BM, BN, BK, TM, TN, STAGES, TA_, TB_, true>(p, s)          \
-                   : launch_one<BM, BN, BK, TM, TN, STAGES, TA_, TB_, false>(p, s);
+#define RO_GEMM_CASE(TA_, TB_)                                                                        \
+    if ((bool)p.transA == TA_ && (bool)p.transB == TB_)                                               \
+        return vec ? launch_one<BM, BN, BK, TM, TN, STAGES, MINB, KGO, TA_, TB_, true>(p, s)          \
+                   : launch_one<BM, BN, BK, TM, TN, STAGES, MINB, KGO, TA_, TB_, false>(p, s);
     RO_GEMM_CASE(false, false)
     RO_GEMM_CASE(false, true)
     RO_GEMM_CASE(true, false)
@@ -312,8 +312,12 @@ cudaError_t launch_cfg(const GemmParams &p, cudaStream_t s) {
 
 }  // namespace
 
-// Tile-config choice (bits-neutral): 128 x 128 tiles when there are enough of
-// them to fill the 148 SMs twice, else 64 x 64.
+// Tile configurations (all bits-neutral: only the M/N tiling differs).
+//   0: 128 x 128, 8 x 8 per thread, 3 stages, 2 CTAs/SM   (large problems)
+//   1:  64 x  64, 8 x 4 per thread, 3 stages              (small M*N)
+//   2..5: tuning variants (selected by the benchmarks / tools/gemm_tune.py)
+int gemm_num_cfgs() { return 6; }
+
 cudaError_t gemm_launch(const GemmParams &p, cudaStream_t s, int force_cfg) {
     if (p.M == 0 || p.N == 0 || p.batch0 * p.batch1 == 0) return cudaSuccess;
     if (p.batch0 * p.batch1 > 65535) return cudaErrorInvalidValue;
@@ -322,6 +326,13 @@ cudaError_t gemm_launch(const GemmParams &p, cudaStream_t s, int force_cfg) {
         int64_t tiles128 = ((p.M + 127) / 128) * ((p.N + 127) / 128) * p.batch0 * p.batch1;
         cfg = (tiles128 >= 2 * 148) ? 0 : 1;
     }
-    if (cfg == 0) return launch_cfg<128, 128, 16, 8, 8, 3>(p, s);
-    return launch_cfg<64, 64, 16, 8, 4, 3>(p, s);
+    switch (cfg) {
+        case 0: return launch_cfg<128, 128, 16, 8, 8, 3, 2>(p, s);
+        case 1: return launch_cfg<64, 64, 16, 8, 4, 3, 2>(p, s);
+        case 2: return launch_cfg<128, 128, 16, 8, 8, 4, 1>(p, s);
+        case 3: return launch_cfg<128, 256, 16, 8, 16, 3, 1>(p, s);
+        case 4: return launch_cfg<256, 128, 16, 16, 8, 3, 1>(p, s);
+        case 5: return launch_cfg<128, 128, 16, 8, 8, 3, 2, 2>(p, s);
+        default: return cudaErrorInvalidValue;
+    }
 }

@@ -19,5 +19,6 @@ struct GemmParams {
     bool vecA, vecB, vecC;  // 16-byte alignment of every row start (speed only)
 };
 
-// force_cfg: -1 = automatic, 0 = 128x128 tiles, 1 = 64x64 tiles (bits-neutral)
+// force_cfg: -1 = automatic, else one of gemm_num_cfgs() tile configurations (bits-neutral)
 cudaError_t gemm_launch(const GemmParams &p, cudaStream_t s, int force_cfg);
+int gemm_num_cfgs();
