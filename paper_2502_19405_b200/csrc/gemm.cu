@@ -9,19 +9,26 @@
 // Tensor cores are deliberately not used: their internal accumulation order is
 // not IEEE-sequential (north_star).
 //
-// Kernel (v2).  CTA tile BM x BN (128 x 128, 256 threads, 8 x 8 outputs per
-// thread; or 64 x 64, 128 threads, 8 x 4), BK = 16, STAGES-deep cp.async ring
-// (global -> shared without registers; src-size zero-fill at the M/N/K edges).
-// Operand tiles keep their global orientation in shared memory:
-//   "mn-contiguous" (A^T stored K x M, or B stored K x N): [BK][BM] rows, the
-//      thread reads its 4 consecutive rows/cols at one k with one LDS.128;
-//   "k-contiguous"  (A stored M x K, or B^T stored N x K): [BM][BK+4] rows, the
-//      thread owns rows ty + TY*i and reads KG consecutive k of each row with
-//      one LDS.64/.128 (row stride 20 words -> the 4 / 8 rows a warp touches
-//      fall in disjoint bank groups).
-// Warps are 8 (n) x 4 (m) lanes so one LDS instruction touches <= 128 bytes.
-// CTAs are rasterised in groups of GROUP_M row tiles so the A and B panels of
-// concurrently running CTAs are shared through L2.
+// Kernel (v3).
+//  * FFMA2: the micro-kernel issues __ffma2_rn (SASS FFMA2: two binary32 FMAs
+//    per lane, each exactly __fmaf_rn, with the A value broadcast from a
+//    scalar register).  Accumulators are float2 pairs along n.  Half the FMA
+//    instructions of a scalar-FFMA kernel, which is what the v2 profile was
+//    limited by (issue / register-bank dispatch stalls).
+//  * CTA tile BM x BN (128 x 128, 256 threads, 8 x 8 outputs per thread;
+//    or 64 x 64, 128 threads, 8 x 4), BK = 16, STAGES-deep ring in shared
+//    memory.  A tiles arrive by cp.async in their global orientation:
+//      A^T stored K x M  -> [BK][BM]: 4 consecutive rows at one k = one LDS.128
+//      A   stored M x K  -> [BM][BK+4]: rows ty + TY*i, 4 consecutive k of a
+//                           row = one LDS.128 (row stride 20 words: the rows a
+//                           warp touches fall in disjoint bank groups)
+//    B tiles are always [BK][BN] (n contiguous) so B pairs are natural float2:
+//      B stored K x N    -> cp.async;
+//      B^T stored N x K  -> register-staged 4-k loads, transposed on the
+//                           store into shared memory (conflict-free: a warp
+//                           writes 32 consecutive n of one k row).
+//  * Warps are 8 (n) x 4 (m) lanes so one LDS touches <= 128 bytes.
+//  * CTAs are rasterised in groups of GROUP_M row tiles (L2 reuse of panels).
 #include "common.cuh"
 #include "gemm.cuh"
 
@@ -73,26 +80,63 @@ RO_DEV void tile_async(float *dst, const float *__restrict__ src, int64_t ld, in
     }
 }
 
-template <int BM, int BN, int BK, int TM, int TN, bool TA, bool TB, int KGO = 0>
+// B^T stored N x K (k contiguous): each thread loads 4 consecutive k of rows
+// n = (tid % BN) (+ BN*... for more chunks) into registers ...
+template <int BN, int BK, int THREADS>
+struct BtStage {
+    static constexpr int CHUNKS = BN * BK / 4 / THREADS;  // float4 chunks per thread
+    float v[CHUNKS][4];
+};
+
+template <int BN, int BK, int THREADS, bool VEC>
+RO_DEV void bt_load(BtStage<BN, BK, THREADS> &st, const float *__restrict__ src, int64_t ld, int64_t nvalid,
+                    int64_t kvalid, int tid) {
+#pragma unroll
+    for (int q = 0; q < BtStage<BN, BK, THREADS>::CHUNKS; ++q) {
+        const int c = tid + q * THREADS;
+        const int n = c % BN;           // consecutive threads -> consecutive n
+        const int kq = (c / BN) * 4;
+        const float *s = src + (int64_t)n * ld + kq;
+        if (VEC && n < nvalid && kq + 4 <= kvalid) {
+            float4 x = __ldg(reinterpret_cast<const float4 *>(s));
+            st.v[q][0] = x.x; st.v[q][1] = x.y; st.v[q][2] = x.z; st.v[q][3] = x.w;
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) st.v[q][e] = (n < nvalid && kq + e < kvalid) ? __ldg(s + e) : 0.f;
+        }
+    }
+}
+
+template <int BN, int BK, int THREADS>
+RO_DEV void bt_store(float *Bs, const BtStage<BN, BK, THREADS> &st, int tid) {
+#pragma unroll
+    for (int q = 0; q < BtStage<BN, BK, THREADS>::CHUNKS; ++q) {
+        const int c = tid + q * THREADS;
+        const int n = c % BN;
+        const int kq = (c / BN) * 4;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) Bs[(kq + e) * BN + n] = st.v[q][e];
+    }
+}
+
+template <int BM, int BN, int BK, int TM, int TN, bool TA>
 struct Cfg {
     static constexpr int TX = BN / TN;          // threads along n
     static constexpr int TY = BM / TM;          // threads along m
     static constexpr int THREADS = TX * TY;
     static constexpr int WX = TX / 8;           // warps along n (8 lanes each)
-    static constexpr int SKP = BK + 4;          // k-contiguous row stride (words)
-    // shared-memory stage layout
+    static constexpr int SKP = BK + 4;          // k-contiguous A row stride (words)
     static constexpr int A_WORDS = TA ? BK * BM : BM * SKP;
-    static constexpr int B_WORDS = TB ? BN * SKP : BK * BN;
+    static constexpr int B_WORDS = BK * BN;
     static constexpr int STAGE_WORDS = A_WORDS + B_WORDS;
-    // k-group width for k-contiguous operands (LDS.64 when both are k-contiguous)
-    static constexpr int KG = KGO ? KGO : ((!TA && TB) ? 2 : 4);
+    static constexpr int NP = TN / 2;           // accumulator pairs per row
 };
 
-template <int BM, int BN, int BK, int TM, int TN, int STAGES, int MINB, int KGO, bool TA, bool TB, bool VEC>
+template <int BM, int BN, int BK, int TM, int TN, int STAGES, int MINB, bool TA, bool TB, bool VEC>
 __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB) gemm_kernel(GemmParams p) {
-    using CF = Cfg<BM, BN, BK, TM, TN, TA, TB, KGO>;
+    using CF = Cfg<BM, BN, BK, TM, TN, TA>;
     constexpr int THREADS = CF::THREADS;
-    constexpr int TX = CF::TX, TY = CF::TY, SKP = CF::SKP, KG = CF::KG;
+    constexpr int TX = CF::TX, TY = CF::TY, SKP = CF::SKP, NP = CF::NP;
     extern __shared__ __align__(16) float smem[];
 
     const int tid = threadIdx.x;
@@ -107,9 +151,8 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB) gemm_kernel(GemmP
     const int64_t g = t / per_group;
     const int64_t first_m = g * GROUP_M;
     const int64_t gsz = min((int64_t)GROUP_M, tiles_m - first_m);
-    const int64_t tm_ = first_m + (t % per_group) % gsz;
-    const int64_t tn_ = (t % per_group) / gsz;
-    const int64_t m0 = tm_ * BM, n0 = tn_ * BN;
+    const int64_t m0 = (first_m + (t % per_group) % gsz) * BM;
+    const int64_t n0 = ((t % per_group) / gsz) * BN;
 
     const int64_t b0 = blockIdx.y / p.batch1, b1 = blockIdx.y % p.batch1;
     const float *__restrict__ A = p.A + b0 * p.sA0 + b1 * p.sA1;
@@ -117,82 +160,69 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB) gemm_kernel(GemmP
     float *__restrict__ Cp = p.C + b0 * p.sC0 + b1 * p.sC1;
     const int64_t M = p.M, N = p.N, K = p.K;
 
-    auto load_stage = [&](int slot, int64_t kt) {
+    auto load_a = [&](int slot, int64_t kt) {
         float *As = smem + slot * CF::STAGE_WORDS;
-        float *Bs = As + CF::A_WORDS;
         const int64_t k0 = kt * BK;
         if (TA)  // A stored K x M: tile rows = k, contiguous m
             tile_async<BK, BM, BM, THREADS, VEC>(As, A + k0 * p.lda + m0, p.lda, K - k0, M - m0, tid);
         else     // A stored M x K: tile rows = m, contiguous k
             tile_async<BM, BK, SKP, THREADS, VEC>(As, A + m0 * p.lda + k0, p.lda, M - m0, K - k0, tid);
-        if (TB)  // B stored N x K
-            tile_async<BN, BK, SKP, THREADS, VEC>(Bs, B + n0 * p.ldb + k0, p.ldb, N - n0, K - k0, tid);
-        else     // B stored K x N
+        if (!TB) {  // B stored K x N -> [BK][BN] directly
+            float *Bs = As + CF::A_WORDS;
             tile_async<BK, BN, BN, THREADS, VEC>(Bs, B + k0 * p.ldb + n0, p.ldb, K - k0, N - n0, tid);
+        }
     };
+    BtStage<BN, BK, THREADS> bst;  // register stage for B^T (TB only)
+    auto load_bt = [&](int64_t kt) {
+        const int64_t k0 = kt * BK;
+        bt_load<BN, BK, THREADS, VEC>(bst, B + n0 * p.ldb + k0, p.ldb, N - n0, K - k0, tid);
+    };
+    auto store_bt = [&](int slot) { bt_store<BN, BK, THREADS>(smem + slot * CF::STAGE_WORDS + CF::A_WORDS, bst, tid); };
 
-    float acc[TM][TN];
+    float2 acc[TM][NP];
 #pragma unroll
     for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;  // +0 (R2)
+        for (int j = 0; j < NP; ++j) acc[i][j] = make_float2(0.f, 0.f);  // +0 (R2)
 
     const int64_t ktiles = (K + BK - 1) / BK;
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
-        if (s < ktiles) load_stage(s, s);
+        if (s < ktiles) {
+            load_a(s, s);
+            if (TB) { load_bt(s); store_bt(s); }
+        }
         cp_commit();
     }
 
-    // fragment address helpers
-    // mn-contiguous A: rows (i/4)*(BM/(TM/4)) + ty*4 + i%4 ; k-contiguous A: rows ty + TY*i
-    // mn-contiguous B: cols (j/4)*(BN/(TN/4)) + tx*4 + j%4 ; k-contiguous B: cols tx + TX*j
     for (int64_t kt = 0; kt < ktiles; ++kt) {
         cp_wait<STAGES - 2>();
         __syncthreads();
-        {
-            const int64_t nk = kt + STAGES - 1;
-            if (nk < ktiles) load_stage((int)(nk % STAGES), nk);
-            cp_commit();
+        const int64_t nk = kt + STAGES - 1;
+        const bool pref = nk < ktiles;
+        if (pref) {
+            load_a((int)(nk % STAGES), nk);
+            if (TB) load_bt(nk);
         }
+        cp_commit();
         const float *As = smem + (int)(kt % STAGES) * CF::STAGE_WORDS;
         const float *Bs = As + CF::A_WORDS;
         const int kmax = (int)min((int64_t)BK, K - kt * BK);
         if (kmax == BK) {
 #pragma unroll
-            for (int kg = 0; kg < BK; kg += KG) {
-                float ak[TA ? 1 : TM][KG], bk[TB ? TN : 1][KG];
+            for (int kg = 0; kg < BK; kg += 4) {
+                float ak[TA ? 1 : TM][4];
                 if (!TA) {
 #pragma unroll
                     for (int i = 0; i < TM; ++i) {
-                        const float *src = As + (ty + TY * i) * SKP + kg;
-                        if (KG == 4) {
-                            float4 v = *reinterpret_cast<const float4 *>(src);
-                            ak[i][0] = v.x; ak[i][KG > 1 ? 1 : 0] = v.y;
-                            ak[i][KG > 2 ? 2 : 0] = v.z; ak[i][KG > 3 ? 3 : 0] = v.w;
-                        } else {
-                            float2 v = *reinterpret_cast<const float2 *>(src);
-                            ak[i][0] = v.x; ak[i][KG > 1 ? 1 : 0] = v.y;
-                        }
-                    }
-                }
-                if (TB) {
-#pragma unroll
-                    for (int j = 0; j < TN; ++j) {
-                        const float *src = Bs + (tx + TX * j) * SKP + kg;
-                        if (KG == 4) {
-                            float4 v = *reinterpret_cast<const float4 *>(src);
-                            bk[j][0] = v.x; bk[j][KG > 1 ? 1 : 0] = v.y;
-                            bk[j][KG > 2 ? 2 : 0] = v.z; bk[j][KG > 3 ? 3 : 0] = v.w;
-                        } else {
-                            float2 v = *reinterpret_cast<const float2 *>(src);
-                            bk[j][0] = v.x; bk[j][KG > 1 ? 1 : 0] = v.y;
-                        }
+                        float4 v = *reinterpret_cast<const float4 *>(As + (ty + TY * i) * SKP + kg);
+                        ak[i][0] = v.x; ak[i][1] = v.y; ak[i][2] = v.z; ak[i][3] = v.w;
                     }
                 }
 #pragma unroll
-                for (int kk = 0; kk < KG; ++kk) {
-                    float a[TM], b[TN];
+                for (int kk = 0; kk < 4; ++kk) {
+                    float a[TM];
+                    float2 b[NP];
                     if (TA) {
 #pragma unroll
                         for (int h = 0; h < TM / 4; ++h) {
@@ -203,38 +233,39 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB) gemm_kernel(GemmP
 #pragma unroll
                         for (int i = 0; i < TM; ++i) a[i] = ak[i][kk];
                     }
-                    if (!TB) {
 #pragma unroll
-                        for (int h = 0; h < TN / 4; ++h) {
-                            float4 v = *reinterpret_cast<const float4 *>(Bs + (kg + kk) * BN + h * (BN / (TN / 4)) + tx * 4);
-                            b[h * 4] = v.x; b[h * 4 + 1] = v.y; b[h * 4 + 2] = v.z; b[h * 4 + 3] = v.w;
-                        }
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < TN; ++j) b[j] = bk[j][kk];
+                    for (int h = 0; h < TN / 4; ++h) {
+                        float4 v = *reinterpret_cast<const float4 *>(Bs + (kg + kk) * BN + h * (BN / (TN / 4)) + tx * 4);
+                        b[2 * h] = make_float2(v.x, v.y);
+                        b[2 * h + 1] = make_float2(v.z, v.w);
                     }
 #pragma unroll
                     for (int i = 0; i < TM; ++i)
 #pragma unroll
-                        for (int j = 0; j < TN; ++j) acc[i][j] = __fmaf_rn(a[i], b[j], acc[i][j]);
+                        for (int j = 0; j < NP; ++j) acc[i][j] = __ffma2_rn(make_float2(a[i], a[i]), b[j], acc[i][j]);
                 }
             }
         } else {
             // ragged last K tile: the real k only, ascending (no zero padding)
             for (int k = 0; k < kmax; ++k) {
-                float a[TM], b[TN];
+                float a[TM];
+                float2 b[NP];
 #pragma unroll
                 for (int i = 0; i < TM; ++i)
                     a[i] = TA ? As[k * BM + (i / 4) * (BM / (TM / 4)) + ty * 4 + (i % 4)] : As[(ty + TY * i) * SKP + k];
 #pragma unroll
-                for (int j = 0; j < TN; ++j)
-                    b[j] = TB ? Bs[(tx + TX * j) * SKP + k] : Bs[k * BN + (j / 4) * (BN / (TN / 4)) + tx * 4 + (j % 4)];
+                for (int h = 0; h < TN / 4; ++h) {
+                    const float *src = Bs + k * BN + h * (BN / (TN / 4)) + tx * 4;
+                    b[2 * h] = make_float2(src[0], src[1]);
+                    b[2 * h + 1] = make_float2(src[2], src[3]);
+                }
 #pragma unroll
                 for (int i = 0; i < TM; ++i)
 #pragma unroll
-                    for (int j = 0; j < TN; ++j) acc[i][j] = __fmaf_rn(a[i], b[j], acc[i][j]);
+                    for (int j = 0; j < NP; ++j) acc[i][j] = __ffma2_rn(make_float2(a[i], a[i]), b[j], acc[i][j]);
             }
         }
+        if (TB && pref) store_bt((int)(nk % STAGES));  // slot (kt-1) % STAGES: free since this iteration's barrier
     }
     cp_wait<0>();
 
@@ -244,45 +275,33 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB) gemm_kernel(GemmP
         const int64_t m = m0 + (TA ? (i / 4) * (BM / (TM / 4)) + ty * 4 + (i % 4) : ty + TY * i);
         if (m >= M) continue;
         float *crow = Cp + m * p.ldc;
-        if (!TB) {
 #pragma unroll
-            for (int h = 0; h < TN / 4; ++h) {
-                const int64_t n = n0 + h * (BN / (TN / 4)) + tx * 4;
-                float v[4];
+        for (int h = 0; h < TN / 4; ++h) {
+            const int64_t n = n0 + h * (BN / (TN / 4)) + tx * 4;
+            float v[4] = {acc[i][2 * h].x, acc[i][2 * h].y, acc[i][2 * h + 1].x, acc[i][2 * h + 1].y};
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    float x = acc[i][h * 4 + c];
-                    if (p.epi == 1) x = (n + c < N) ? __fadd_rn(x, __ldg(p.bias + n + c)) : x;
-                    else if (p.epi == 2) x = __fmul_rn(x, p.scale);
-                    v[c] = canon(x);
-                }
-                if (p.vecC && n + 4 <= N) {
-                    *reinterpret_cast<float4 *>(crow + n) = make_float4(v[0], v[1], v[2], v[3]);
-                } else {
-#pragma unroll
-                    for (int c = 0; c < 4; ++c)
-                        if (n + c < N) crow[n + c] = v[c];
-                }
-            }
-        } else {
-#pragma unroll
-            for (int j = 0; j < TN; ++j) {
-                const int64_t n = n0 + tx + TX * j;
-                if (n >= N) continue;
-                float x = acc[i][j];
-                if (p.epi == 1) x = __fadd_rn(x, __ldg(p.bias + n));
+            for (int c = 0; c < 4; ++c) {
+                float x = v[c];
+                if (p.epi == 1) x = (n + c < N) ? __fadd_rn(x, __ldg(p.bias + n + c)) : x;
                 else if (p.epi == 2) x = __fmul_rn(x, p.scale);
-                crow[n] = canon(x);
+                v[c] = canon(x);
+            }
+            if (p.vecC && n + 4 <= N) {
+                *reinterpret_cast<float4 *>(crow + n) = make_float4(v[0], v[1], v[2], v[3]);
+            } else {
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    if (n + c < N) crow[n + c] = v[c];
             }
         }
     }
 }
 
-template <int BM, int BN, int BK, int TM, int TN, int STAGES, int MINB, int KGO, bool TA, bool TB, bool VEC>
+template <int BM, int BN, int BK, int TM, int TN, int STAGES, int MINB, bool TA, bool TB, bool VEC>
 cudaError_t launch_one(const GemmParams &p, cudaStream_t s) {
-    using CF = Cfg<BM, BN, BK, TM, TN, TA, TB, KGO>;
+    using CF = Cfg<BM, BN, BK, TM, TN, TA>;
     const size_t smem = (size_t)STAGES * CF::STAGE_WORDS * sizeof(float);
-    auto kern = gemm_kernel<BM, BN, BK, TM, TN, STAGES, MINB, KGO, TA, TB, VEC>;
+    auto kern = gemm_kernel<BM, BN, BK, TM, TN, STAGES, MINB, TA, TB, VEC>;
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -295,13 +314,13 @@ cudaError_t launch_one(const GemmParams &p, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-template <int BM, int BN, int BK, int TM, int TN, int STAGES, int MINB, int KGO = 0>
+template <int BM, int BN, int BK, int TM, int TN, int STAGES, int MINB>
 cudaError_t launch_cfg(const GemmParams &p, cudaStream_t s) {
     const bool vec = p.vecA && p.vecB;
-#define RO_GEMM_CASE(TA_, TB_)                                                                        \
-    if ((bool)p.transA == TA_ && (bool)p.transB == TB_)                                               \
-        return vec ? launch_one<BM, BN, BK, TM, TN, STAGES, MINB, KGO, TA_, TB_, true>(p, s)          \
-                   : launch_one<BM, BN, BK, TM, TN, STAGES, MINB, KGO, TA_, TB_, false>(p, s);
+#define RO_GEMM_CASE(TA_, TB_)                                                                   \
+    if ((bool)p.transA == TA_ && (bool)p.transB == TB_)                                          \
+        return vec ? launch_one<BM, BN, BK, TM, TN, STAGES, MINB, TA_, TB_, true>(p, s)          \
+                   : launch_one<BM, BN, BK, TM, TN, STAGES, MINB, TA_, TB_, false>(p, s);
     RO_GEMM_CASE(false, false)
     RO_GEMM_CASE(false, true)
     RO_GEMM_CASE(true, false)
@@ -315,8 +334,8 @@ cudaError_t launch_cfg(const GemmParams &p, cudaStream_t s) {
 // Tile configurations (all bits-neutral: only the M/N tiling differs).
 //   0: 128 x 128, 8 x 8 per thread, 3 stages, 2 CTAs/SM   (large problems)
 //   1:  64 x  64, 8 x 4 per thread, 3 stages              (small M*N)
-//   2..5: tuning variants (selected by the benchmarks / tools/gemm_tune.py)
-int gemm_num_cfgs() { return 6; }
+//   2..4: tuning variants (tools/gemm_tune.py)
+int gemm_num_cfgs() { return 5; }
 
 cudaError_t gemm_launch(const GemmParams &p, cudaStream_t s, int force_cfg) {
     if (p.M == 0 || p.N == 0 || p.batch0 * p.batch1 == 0) return cudaSuccess;
@@ -332,7 +351,6 @@ cudaError_t gemm_launch(const GemmParams &p, cudaStream_t s, int force_cfg) {
         case 2: return launch_cfg<128, 128, 16, 8, 8, 4, 1>(p, s);
         case 3: return launch_cfg<128, 256, 16, 8, 16, 3, 1>(p, s);
         case 4: return launch_cfg<256, 128, 16, 16, 8, 3, 1>(p, s);
-        case 5: return launch_cfg<128, 128, 16, 8, 8, 3, 2, 2>(p, s);
         default: return cudaErrorInvalidValue;
     }
 }
