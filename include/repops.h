@@ -93,9 +93,10 @@ int repops_gemm_strided_batched(int64_t M, int64_t N, int64_t K,
 int repops_sum_rows(const float *x, int64_t rows, int64_t cols, int64_t ld, float *out, void *stream);
 
 /* R-SEQ (R4): rows split into nseg equal contiguous segments (rows % nseg == 0);
- * out[s*cols + j] = fold over the segment's rows ascending of (acc + x[r*ld+j]), acc = +0. */
+ * out[s*ldo + j] = fold over the segment's rows ascending of (acc + x[r*ld+j]), acc = +0
+ * (ldo >= cols: e.g. the flat per-shard gradient length, to write each shard's row in place). */
 int repops_sum_cols_seq(const float *x, int64_t rows, int64_t cols, int64_t ld, int64_t nseg,
-                        float *out, void *stream);
+                        float *out, int64_t ldo, void *stream);
 
 /* R-TREE_S (R14): out = T(parts[0..nparts)), T(lo,1) = parts[lo],
  * T(lo,n) = fadd(T(lo,n/2), T(lo+n/2,n/2)), elementwise over n floats.
@@ -128,11 +129,11 @@ int repops_layernorm_backward(const float *dy, const float *x, const float *gamm
                               const float *mean, const float *rstd, const float *dres,
                               int64_t rows, int64_t cols, float *dx, void *stream);
 
-/* LN parameter gradients per segment (R-SEQ): dgamma[s][j] = fold fma(dy, xh, acc),
- * dbeta[s][j] = fold (acc + dy); outputs nseg x cols. */
+/* LN parameter gradients per segment (R-SEQ): dgamma[s*ldo + j] = fold fma(dy, xh, acc),
+ * dbeta[s*ldo + j] = fold (acc + dy), xh = (x - mean)*rstd recomputed as in the forward. */
 int repops_layernorm_backward_params(const float *dy, const float *x, const float *mean,
                                      const float *rstd, int64_t rows, int64_t cols, int64_t nseg,
-                                     float *dgamma, float *dbeta, void *stream);
+                                     float *dgamma, float *dbeta, int64_t ldo, void *stream);
 
 /* R-CE: per row of V logits: m = max; s = CSUM(exp(x - m));
  * loss[r] = (m + log s) - x[label];  dlogits_i = ((exp(x_i - m)*(1/s)) - [i == label]) * scale.
@@ -203,6 +204,19 @@ int64_t verde_commit_workspace_bytes(const verde_tensor_desc *descs /* host */, 
  * device memory asynchronously.  ws: device workspace >= the size above. */
 int verde_commit_tensors(const verde_tensor_desc *descs /* host */, int n, void *ws,
                          int64_t ws_bytes, void *stream);
+/* Reusable commit of a fixed set of tensors (static shapes and addresses, as
+ * in a training step that re-uses its buffers).  create() builds the plan and
+ * uploads its tables into `ws` with one synchronous copy; every run() then
+ * only enqueues the leaf / reduce / header kernels on `stream` (no host
+ * traffic, capturable in a CUDA graph).  `ws` (>= verde_commit_workspace_bytes)
+ * is owned by the caller and must outlive the plan; runs of one plan must not
+ * overlap.  destroy() frees the host-side plan object. */
+typedef struct verde_commit_plan verde_commit_plan;
+int verde_commit_plan_create(const verde_tensor_desc *descs /* host */, int n, void *ws, int64_t ws_bytes,
+                             verde_commit_plan **plan);
+int verde_commit_plan_run(const verde_commit_plan *plan, void *stream);
+void verde_commit_plan_destroy(verde_commit_plan *plan);
+
 /* Single-tensor convenience form (dims: host int64[rank]). */
 int verde_commit_tensor(const void *data, int64_t nbytes, int dtype, int rank, const int64_t *dims,
                         uint8_t *digest32, void *ws, int64_t ws_bytes, void *stream);

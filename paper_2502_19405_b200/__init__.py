@@ -25,7 +25,8 @@ __all__ = [
     "repops_rsqrt", "repops_gelu", "repops_gelu_backward", "repops_add", "repops_embedding",
     "repops_embedding_backward", "repops_adamw", "repops_flip_bit", "verde_commit_tensor",
     "verde_commit_tensors", "verde_merkle_root", "verde_sha256", "verde_node_digest",
-    "verde_first_divergence", "verde_digest_from_subroots", "launch_count", "CommitWorkspace", "RepopsError",
+    "verde_first_divergence", "verde_digest_from_subroots", "launch_count", "CommitWorkspace", "CommitPlan",
+    "RepopsError",
     "header_symbols", "lib",
 ]
 
@@ -99,11 +100,13 @@ def repops_sum_rows(x, out=None, stream=None):
     return out
 
 
-def repops_sum_cols_seq(x, nseg=1, out=None, stream=None):
+def repops_sum_cols_seq(x, nseg=1, out=None, ldo=None, stream=None):
+    """R-SEQ column folds per segment; out[s*ldo + j] (out may be a flat buffer view)."""
     _f32(x, "x")
     if out is None:
         out = torch.empty((nseg, x.shape[1]), dtype=torch.float32, device=x.device)
-    check(lib().repops_sum_cols_seq(_p(x), x.shape[0], x.shape[1], _ld(x), nseg, _p(out), _stream(stream)),
+    ldo = x.shape[1] if ldo is None else ldo
+    check(lib().repops_sum_cols_seq(_p(x), x.shape[0], x.shape[1], _ld(x), nseg, _p(out), ldo, _stream(stream)),
           "repops_sum_cols_seq")
     return out
 
@@ -171,14 +174,15 @@ def repops_layernorm_backward(dy, x, gamma, mean, rstd, dres=None, out=None, str
     return out
 
 
-def repops_layernorm_backward_params(dy, x, mean, rstd, nseg=1, dgamma=None, dbeta=None, stream=None):
+def repops_layernorm_backward_params(dy, x, mean, rstd, nseg=1, dgamma=None, dbeta=None, ldo=None, stream=None):
     rows, cols = x.shape
+    ldo = cols if ldo is None else ldo
     if dgamma is None:
         dgamma = torch.empty((nseg, cols), dtype=torch.float32, device=x.device)
     if dbeta is None:
         dbeta = torch.empty((nseg, cols), dtype=torch.float32, device=x.device)
     check(lib().repops_layernorm_backward_params(_p(dy), _p(x), _p(mean), _p(rstd), rows, cols, nseg, _p(dgamma),
-                                                 _p(dbeta), _stream(stream)), "repops_layernorm_backward_params")
+                                                 _p(dbeta), ldo, _stream(stream)), "repops_layernorm_backward_params")
     return dgamma, dbeta
 
 
@@ -319,6 +323,37 @@ def verde_commit_tensors(tensors, digests=None, ws: CommitWorkspace | None = Non
     buf = ws.get(need)
     check(lib().verde_commit_tensors(arr, n, buf.data_ptr(), buf.numel(), _stream(stream)), "verde_commit_tensors")
     return digests
+
+
+class CommitPlan:
+    """verde_commit_plan_*: a prepared commit of a fixed list of tensors into
+    fixed digest slots; run() only enqueues kernels."""
+
+    def __init__(self, tensors, digests, modes=None, device=None):
+        n = len(tensors)
+        self.n = n
+        modes = modes or [0] * n
+        self._keep = (list(tensors), digests)
+        arr = (TensorDesc * n)(*[_desc(t, digests[i], modes[i]) for i, t in enumerate(tensors)])
+        need = lib().verde_commit_workspace_bytes(arr, n)
+        dev = device or tensors[0].device
+        self.ws = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
+        self.nbytes = sum(t.numel() * t.element_size() for t in tensors)
+        h = C.c_void_p()
+        check(lib().verde_commit_plan_create(arr, n, self.ws.data_ptr(), self.ws.numel(), C.byref(h)),
+              "verde_commit_plan_create")
+        self.h = h
+
+    def run(self, stream=None):
+        check(lib().verde_commit_plan_run(self.h, _stream(stream)), "verde_commit_plan_run")
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().verde_commit_plan_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
 
 
 def verde_commit_tensor(t, ws: CommitWorkspace | None = None, stream=None):

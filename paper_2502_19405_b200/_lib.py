@@ -40,13 +40,13 @@ SIGNATURES = {
                                           i32, vp, f32, vp, i64, i64, i64, i64, i64, vp]),
     "repops_gemm_cfg": (i32, [i64, i64, i64, vp, i64, i32, vp, i64, i32, i32, vp, f32, vp, i64, vp, i32]),
     "repops_sum_rows": (i32, [vp, i64, i64, i64, vp, vp]),
-    "repops_sum_cols_seq": (i32, [vp, i64, i64, i64, i64, vp, vp]),
+    "repops_sum_cols_seq": (i32, [vp, i64, i64, i64, i64, vp, i64, vp]),
     "repops_tree_sum": (i32, [vp, i32, i64, vp, vp]),
     "repops_softmax": (i32, [vp, i64, i64, i64, i32, vp, i64, vp]),
     "repops_softmax_backward": (i32, [vp, i64, vp, i64, i64, i64, f32, vp, i64, vp]),
     "repops_layernorm": (i32, [vp, vp, vp, i64, i64, f32, vp, vp, vp, vp]),
     "repops_layernorm_backward": (i32, [vp, vp, vp, vp, vp, vp, i64, i64, vp, vp]),
-    "repops_layernorm_backward_params": (i32, [vp, vp, vp, vp, i64, i64, i64, vp, vp, vp]),
+    "repops_layernorm_backward_params": (i32, [vp, vp, vp, vp, i64, i64, i64, vp, vp, i64, vp]),
     "repops_cross_entropy": (i32, [vp, i64, i64, i64, vp, f32, vp, vp, i64, vp]),
     "repops_exp": (i32, [vp, i64, vp, vp]),
     "repops_log": (i32, [vp, i64, vp, vp]),
@@ -62,6 +62,9 @@ SIGNATURES = {
     "verde_commit_workspace_bytes": (i64, [vp, i32]),
     "verde_commit_tensors": (i32, [vp, i32, vp, i64, vp]),
     "verde_commit_tensor": (i32, [vp, i64, i32, i32, vp, vp, vp, i64, vp]),
+    "verde_commit_plan_create": (i32, [vp, i32, vp, i64, vp]),
+    "verde_commit_plan_run": (i32, [vp, vp]),
+    "verde_commit_plan_destroy": (None, [vp]),
     "verde_merkle_root": (i32, [vp, i64, vp]),
     "verde_digest_from_subroots": (i32, [vp, i64, i32, i32, vp, i64, vp]),
     "verde_sha256": (i32, [vp, i64, vp]),

@@ -238,13 +238,13 @@ int repops_sum_rows(const float *x, int64_t rows, int64_t cols, int64_t ld, floa
 }
 
 int repops_sum_cols_seq(const float *x, int64_t rows, int64_t cols, int64_t ld, int64_t nseg, float *out,
-                        void *stream) {
+                        int64_t ldo, void *stream) {
     REQ(rows >= 0 && cols >= 0 && nseg >= 1, "sum_cols_seq: bad extent");
     REQ(rows % nseg == 0, "sum_cols_seq: rows %% nseg != 0");
     if (cols == 0) return REPOPS_OK;
     REQ(out && (rows == 0 || x), "sum_cols_seq: null pointer");
-    REQ(ld >= cols, "sum_cols_seq: ld < cols");
-    return cuda_status(launch_sum_cols_seq(x, rows, cols, ld, nseg, out, S(stream)), "sum_cols_seq");
+    REQ(ld >= cols && ldo >= cols, "sum_cols_seq: ld/ldo < cols");
+    return cuda_status(launch_sum_cols_seq(x, rows, cols, ld, nseg, out, ldo, S(stream)), "sum_cols_seq");
 }
 
 int repops_tree_sum(const float *const *parts, int nparts, int64_t n, float *out, void *stream) {
@@ -301,11 +301,12 @@ int repops_layernorm_backward(const float *dy, const float *x, const float *gamm
 
 int repops_layernorm_backward_params(const float *dy, const float *x, const float *mean, const float *rstd,
                                      int64_t rows, int64_t cols, int64_t nseg, float *dgamma, float *dbeta,
-                                     void *stream) {
+                                     int64_t ldo, void *stream) {
     REQ(rows >= 0 && cols >= 0 && nseg >= 1 && rows % nseg == 0, "layernorm_backward_params: bad extent");
     if (cols == 0) return REPOPS_OK;
     REQ(dgamma && dbeta && (rows == 0 || (dy && x && mean && rstd)), "layernorm_backward_params: null pointer");
-    return cuda_status(launch_layernorm_params(dy, x, mean, rstd, rows, cols, nseg, dgamma, dbeta, S(stream)),
+    REQ(ldo >= cols, "layernorm_backward_params: ldo < cols");
+    return cuda_status(launch_layernorm_params(dy, x, mean, rstd, rows, cols, nseg, dgamma, dbeta, ldo, S(stream)),
                        "layernorm_backward_params");
 }
 
@@ -410,6 +411,36 @@ int verde_commit_tensors(const verde_tensor_desc *descs, int n, void *ws, int64_
         return fail(REPOPS_ENOSPACE, "commit: workspace %lld < %lld bytes", (long long)ws_bytes, (long long)need);
     if (e == cudaSuccess) g_launches.fetch_add(nk - 1, std::memory_order_relaxed);
     return cuda_status(e, "commit");
+}
+
+int verde_commit_plan_create(const verde_tensor_desc *descs, int n, void *ws, int64_t ws_bytes,
+                             verde_commit_plan **plan) {
+    REQ(n >= 1 && descs && ws && plan, "commit_plan_create: bad argument");
+    for (int t = 0; t < n; ++t) {
+        REQ(descs[t].nbytes >= 0 && (descs[t].nbytes == 0 || descs[t].data), "commit_plan: tensor %d has no data", t);
+        REQ(descs[t].rank >= 0 && descs[t].rank <= 8, "commit_plan: tensor %d rank %d", t, descs[t].rank);
+        REQ(descs[t].digest != nullptr, "commit_plan: tensor %d has no digest buffer", t);
+    }
+    int64_t need = 0;
+    void *out = nullptr;
+    cudaError_t e = commit_plan_create(descs, n, ws, ws_bytes, &out, &need);
+    if (e == cudaErrorMemoryAllocation && ws_bytes < need)
+        return fail(REPOPS_ENOSPACE, "commit_plan: workspace %lld < %lld bytes", (long long)ws_bytes, (long long)need);
+    if (e != cudaSuccess) return fail(REPOPS_ECUDA, "commit_plan_create: %s", cudaGetErrorString(e));
+    *plan = reinterpret_cast<verde_commit_plan *>(out);
+    return REPOPS_OK;
+}
+
+int verde_commit_plan_run(const verde_commit_plan *plan, void *stream) {
+    REQ(plan, "commit_plan_run: null plan");
+    int nk = 0;
+    cudaError_t e = commit_plan_run(plan, S(stream), &nk);
+    if (e == cudaSuccess) g_launches.fetch_add(nk - 1, std::memory_order_relaxed);
+    return cuda_status(e, "commit_plan_run");
+}
+
+void verde_commit_plan_destroy(verde_commit_plan *plan) {
+    if (plan) commit_plan_destroy(plan);
 }
 
 int verde_commit_tensor(const void *data, int64_t nbytes, int dtype, int rank, const int64_t *dims, uint8_t *digest32,

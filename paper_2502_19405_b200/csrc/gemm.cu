@@ -342,8 +342,14 @@ cudaError_t gemm_launch(const GemmParams &p, cudaStream_t s, int force_cfg) {
     if (p.batch0 * p.batch1 > 65535) return cudaErrorInvalidValue;
     int cfg = force_cfg;
     if (cfg < 0) {
-        int64_t tiles128 = ((p.M + 127) / 128) * ((p.N + 127) / 128) * p.batch0 * p.batch1;
-        cfg = (tiles128 >= 2 * 148) ? 0 : 1;
+        // measured on B200 (tools/gemm_tune.py): 128x256 / 256x128 tiles when there
+        // are >= 4 waves of them, 128x128 when >= 2 waves, else 64x64
+        const int64_t nb = p.batch0 * p.batch1;
+        const int64_t tiles_big = ((p.M + 127) / 128) * ((p.N + 255) / 256) * nb;
+        const int64_t tiles128 = ((p.M + 127) / 128) * ((p.N + 127) / 128) * nb;
+        if (tiles_big >= 4 * 148) cfg = (!p.transA && p.transB) ? 4 : 3;
+        else if (tiles128 >= 2 * 148) cfg = 0;
+        else cfg = 1;
     }
     switch (cfg) {
         case 0: return launch_cfg<128, 128, 16, 8, 8, 3, 2>(p, s);

@@ -114,7 +114,7 @@ __global__ void sum_rows_cta(const float *__restrict__ x, int64_t rows, int64_t 
 
 // ------------------------------------------------------------------ R-SEQ column folds
 __global__ void sum_cols_seq_kernel(const float *__restrict__ x, int64_t rows, int64_t cols, int64_t ld,
-                                    int64_t nseg, float *__restrict__ out) {
+                                    int64_t nseg, float *__restrict__ out, int64_t ldo) {
     int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int64_t s = blockIdx.y;
     if (j >= cols) return;
@@ -129,7 +129,7 @@ __global__ void sum_cols_seq_kernel(const float *__restrict__ x, int64_t rows, i
         acc = __fadd_rn(acc, v2); acc = __fadd_rn(acc, v3);
     }
     for (; t < per; ++t) acc = __fadd_rn(acc, __ldg(p + t * ld));
-    out[s * cols + j] = canon(acc);
+    out[s * ldo + j] = canon(acc);
 }
 
 // ------------------------------------------------------------------ softmax
@@ -362,7 +362,7 @@ __global__ void layernorm_bwd_warp(const float *__restrict__ dy, const float *__
 __global__ void layernorm_params_kernel(const float *__restrict__ dy, const float *__restrict__ x,
                                         const float *__restrict__ mean, const float *__restrict__ rstd,
                                         int64_t rows, int64_t cols, int64_t nseg, float *__restrict__ dgamma,
-                                        float *__restrict__ dbeta) {
+                                        float *__restrict__ dbeta, int64_t ldo) {
     int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int64_t s = blockIdx.y;
     if (j >= cols) return;
@@ -374,8 +374,8 @@ __global__ void layernorm_params_kernel(const float *__restrict__ dy, const floa
         ag = __fmaf_rn(d, xh, ag);
         ab = __fadd_rn(ab, d);
     }
-    dgamma[s * cols + j] = canon(ag);
-    dbeta[s * cols + j] = canon(ab);
+    dgamma[s * ldo + j] = canon(ag);
+    dbeta[s * ldo + j] = canon(ab);
 }
 
 // ------------------------------------------------------------------ cross entropy (CTA per row)
@@ -439,10 +439,10 @@ cudaError_t launch_sum_rows(const float *x, int64_t rows, int64_t cols, int64_t 
 }
 
 cudaError_t launch_sum_cols_seq(const float *x, int64_t rows, int64_t cols, int64_t ld, int64_t nseg, float *out,
-                                cudaStream_t s) {
+                                int64_t ldo, cudaStream_t s) {
     if (cols == 0 || nseg == 0) return cudaSuccess;
     dim3 grid((unsigned)((cols + 127) / 128), (unsigned)nseg);
-    sum_cols_seq_kernel<<<grid, 128, 0, s>>>(x, rows, cols, ld, nseg, out);
+    sum_cols_seq_kernel<<<grid, 128, 0, s>>>(x, rows, cols, ld, nseg, out, ldo);
     return cudaGetLastError();
 }
 
@@ -487,10 +487,11 @@ cudaError_t launch_layernorm_backward(const float *dy, const float *x, const flo
 }
 
 cudaError_t launch_layernorm_params(const float *dy, const float *x, const float *mean, const float *rstd,
-                                    int64_t rows, int64_t cols, int64_t nseg, float *dg, float *db, cudaStream_t s) {
+                                    int64_t rows, int64_t cols, int64_t nseg, float *dg, float *db, int64_t ldo,
+                                    cudaStream_t s) {
     if (cols == 0 || nseg == 0) return cudaSuccess;
     dim3 grid((unsigned)((cols + 127) / 128), (unsigned)nseg);
-    layernorm_params_kernel<<<grid, 128, 0, s>>>(dy, x, mean, rstd, rows, cols, nseg, dg, db);
+    layernorm_params_kernel<<<grid, 128, 0, s>>>(dy, x, mean, rstd, rows, cols, nseg, dg, db, ldo);
     return cudaGetLastError();
 }
 

@@ -19,6 +19,8 @@
 //                      || dims || nbytes || 4096 || data_root)
 // SHA-256 is integer-ALU bound on sm_100a (rotates = SHF, Ch/Maj/xor = LOP3,
 // adds = IADD3/IMAD), not HBM bound; see DESIGN.md §5.
+#include <cstring>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -367,15 +369,16 @@ int64_t commit_workspace_bytes(const verde_tensor_desc *d, int n) {
     return make_layout(p).total;
 }
 
-cudaError_t commit_launch(const verde_tensor_desc *d, int n, void *ws, int64_t ws_bytes, cudaStream_t s,
-                          int64_t *need, int *nkernels) {
-    if (n <= 0) return cudaSuccess;
-    Plan p = make_plan(d, n);
-    Layout L = make_layout(p);
-    *need = L.total;
-    if (ws_bytes < L.total) return cudaErrorMemoryAllocation;
-    uint8_t *base = reinterpret_cast<uint8_t *>(ws);
-    // one staging blob: tensor descriptors then the int64 tables
+// A prepared commit: host plan + workspace layout; the tables already live in
+// the device workspace, so running it only launches kernels.
+struct CommitPlanImpl {
+    Plan p;
+    Layout L;
+    uint8_t *base;
+    int n;
+};
+
+static std::vector<uint8_t> stage_tables(const verde_tensor_desc *d, int n, const Layout &L) {
     std::vector<uint8_t> host((size_t)L.bufA);
     std::vector<DevTensor> dt(n);
     for (int t = 0; t < n; ++t) {
@@ -389,10 +392,11 @@ cudaError_t commit_launch(const verde_tensor_desc *d, int n, void *ws, int64_t w
     }
     memcpy(host.data(), dt.data(), sizeof(DevTensor) * n);
     memcpy(host.data() + L.tables, L.blob.data(), L.blob.size() * 8);
-    cudaError_t e = cudaMemcpyAsync(base, host.data(), (size_t)L.bufA, cudaMemcpyHostToDevice, s);
-    if (e != cudaSuccess) return e;
-    // the staging buffer must outlive the async copy of pageable memory: cudaMemcpyAsync
-    // from pageable host memory returns only after the data has been staged.
+    return host;
+}
+
+static cudaError_t run_kernels(const Plan &p, const Layout &L, uint8_t *base, int n, cudaStream_t s, int *nkernels) {
+    cudaError_t e;
     const DevTensor *dts = reinterpret_cast<const DevTensor *>(base);
     const int64_t *tab = reinterpret_cast<const int64_t *>(base + L.tables);
     Digest *A = reinterpret_cast<Digest *>(base + L.bufA);
@@ -417,3 +421,39 @@ cudaError_t commit_launch(const verde_tensor_desc *d, int n, void *ws, int64_t w
     header_kernel<<<(n + 63) / 64, 64, 0, s>>>(dts, n, tab + L.root_off_at, p.final_in_b ? B : A);
     return cudaGetLastError();
 }
+
+cudaError_t commit_launch(const verde_tensor_desc *d, int n, void *ws, int64_t ws_bytes, cudaStream_t s,
+                          int64_t *need, int *nkernels) {
+    *nkernels = 0;
+    if (n <= 0) return cudaSuccess;
+    Plan p = make_plan(d, n);
+    Layout L = make_layout(p);
+    *need = L.total;
+    if (ws_bytes < L.total) return cudaErrorMemoryAllocation;
+    uint8_t *base = reinterpret_cast<uint8_t *>(ws);
+    std::vector<uint8_t> host = stage_tables(d, n, L);
+    // pageable source: returns once the bytes are staged, so `host` may be freed after
+    cudaError_t e = cudaMemcpyAsync(base, host.data(), (size_t)L.bufA, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return e;
+    return run_kernels(p, L, base, n, s, nkernels);
+}
+
+cudaError_t commit_plan_create(const verde_tensor_desc *d, int n, void *ws, int64_t ws_bytes, void **out,
+                               int64_t *need) {
+    Plan p = make_plan(d, n);
+    Layout L = make_layout(p);
+    *need = L.total;
+    if (ws_bytes < L.total) return cudaErrorMemoryAllocation;
+    std::vector<uint8_t> host = stage_tables(d, n, L);
+    cudaError_t e = cudaMemcpy(ws, host.data(), (size_t)L.bufA, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return e;
+    *out = new CommitPlanImpl{std::move(p), std::move(L), reinterpret_cast<uint8_t *>(ws), n};
+    return cudaSuccess;
+}
+
+cudaError_t commit_plan_run(const void *plan, cudaStream_t s, int *nkernels) {
+    const CommitPlanImpl *c = reinterpret_cast<const CommitPlanImpl *>(plan);
+    return run_kernels(c->p, c->L, c->base, c->n, s, nkernels);
+}
+
+void commit_plan_destroy(void *plan) { delete reinterpret_cast<CommitPlanImpl *>(plan); }

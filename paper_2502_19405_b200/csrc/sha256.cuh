@@ -9,3 +9,7 @@ int64_t commit_workspace_bytes(const verde_tensor_desc *d, int n);
 // returns cudaErrorMemoryAllocation (and *need) if ws_bytes is too small
 cudaError_t commit_launch(const verde_tensor_desc *d, int n, void *ws, int64_t ws_bytes, cudaStream_t s,
                           int64_t *need, int *nkernels);
+cudaError_t commit_plan_create(const verde_tensor_desc *d, int n, void *ws, int64_t ws_bytes, void **out,
+                               int64_t *need);
+cudaError_t commit_plan_run(const void *plan, cudaStream_t s, int *nkernels);
+void commit_plan_destroy(void *plan);

@@ -76,3 +76,33 @@ def gemm_inputs(n_or_mnk, tag: str = "gemm"):
     A = uniform(seed_for(tag, "A", M, N, K), (M, K))
     B = uniform(seed_for(tag, "B", M, N, K), (K, N))
     return A, B
+
+
+# ----------------------------------------------------------------- GPT-2 (BASELINE config 3)
+def gpt2_param_specs(n_layer, d, ffn, vocab, n_pos):
+    """(name, shape, kind) in the canonical GPT-2 order.  kind: 'w' (2-D weight,
+    U[-a, a) with a = 0.02*sqrt(3), i.e. std 0.02), 'g' (LN gain = 1), 'b' (zeros)."""
+    specs = [("wte", (vocab, d), "w"), ("wpe", (n_pos, d), "w")]
+    for l in range(n_layer):
+        p = f"h{l}."
+        specs += [(p + "ln1.g", (d,), "g"), (p + "ln1.b", (d,), "b"),
+                  (p + "attn.w", (d, 3 * d), "w"), (p + "attn.b", (3 * d,), "b"),
+                  (p + "proj.w", (d, d), "w"), (p + "proj.b", (d,), "b"),
+                  (p + "ln2.g", (d,), "g"), (p + "ln2.b", (d,), "b"),
+                  (p + "fc.w", (d, ffn), "w"), (p + "fc.b", (ffn,), "b"),
+                  (p + "fc2.w", (ffn, d), "w"), (p + "fc2.b", (d,), "b")]
+    specs += [("lnf.g", (d,), "g"), ("lnf.b", (d,), "b")]
+    return specs
+
+
+def gpt2_param(name, shape, kind, seed=0):
+    if kind == "w":
+        return uniform(seed_for("gpt2", seed, name), shape, 0.034641016151377546)
+    if kind == "g":
+        return np.ones(shape, np.float32)
+    return np.zeros(shape, np.float32)
+
+
+def gpt2_tokens(vocab, seq, shard, step=0, seed=0):
+    """seq+1 tokens of one shard (one sequence); input = [:-1], target = [1:]."""
+    return integers(seed_for("gpt2-tokens", seed, step, shard), seq + 1, vocab)
