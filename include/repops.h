@@ -156,9 +156,10 @@ int repops_add(const float *a, const float *b, int64_t n, float *y, void *stream
 /* R-EMB forward: x0[t][c] = fadd(wte[tok[t]][c], wpe[t mod T][c]); tok device int32. */
 int repops_embedding(const int32_t *tok, int64_t ntok, int64_t T, const float *wte,
                      const float *wpe, int64_t C, float *x0, void *stream);
-/* R-EMB backward for one data-parallel shard, accumulated INTO dwte (and dwpe):
+/* R-EMB backward for one data-parallel shard.  dwte is accumulated INTO (it holds
+ * the tied lm-head gradient of the shard), dwpe is overwritten:
  * dwte[v][c] = fadd(dwte[v][c], fold over t ascending with tok[t]==v of (acc + dx0[t][c]));
- * dwpe[p][c] = fadd(dwpe[p][c], fold over t ascending with t mod T == p).  Untouched
+ * dwpe[p][c] = fold over t ascending with t mod T == p (p < min(ntok, T)).  Untouched
  * rows keep their bits.  dwpe may be NULL. */
 int repops_embedding_backward(const int32_t *tok, int64_t ntok, int64_t T, const float *dx0,
                               int64_t C, float *dwte, float *dwpe, void *stream);

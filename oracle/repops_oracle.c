@@ -423,10 +423,11 @@ void orc_cross_entropy(const float *logits, i64 rows, i64 V, i64 ld, const int32
 /* ======================================================================
  * R-EMB: token + position embedding.
  *   fwd: x0[t][c] = wte[tok_t][c] + wpe[t mod T][c]
- *   bwd (one shard = rows [r0, r0+nrows)), accumulated INTO dwte / dwpe:
+ *   bwd (one shard): dwte is accumulated INTO (it holds the shard's tied
+ *   lm-head gradient), dwpe is written:
  *     for each vocab row v used by the shard:
  *        dwte[v][c] = dwte[v][c] + fold_{t ascending, tok_t == v} (acc + dx0[t][c])
- *     for each position p:  dwpe[p][c] = dwpe[p][c] + fold_{t ascending, t mod T == p} ...
+ *     for each position p < min(ntok, T):  dwpe[p][c] = fold_{t ascending, t mod T == p} ...
  * (the fold is the one-hot GEMM's ascending-token order, reading R4)
  * ==================================================================== */
 void orc_embedding(const int32_t *tok, i64 ntok, i64 T, const float *wte, const float *wpe, i64 C, float *x0) {
@@ -456,7 +457,7 @@ void orc_embedding_backward(const int32_t *tok, i64 ntok, i64 T, const float *dx
             for (i64 c = 0; c < C; ++c) {
                 float acc = 0.0f;
                 for (i64 u = p; u < ntok; u += T) acc = acc + dx0[u * C + c];
-                dwpe[p * C + c] = canon(dwpe[p * C + c] + acc);
+                dwpe[p * C + c] = canon(acc);
             }
     }
 }

@@ -164,8 +164,7 @@ __global__ void embedding_bwd_kernel(const int32_t *__restrict__ tok, int64_t nt
         for (int64_t c = threadIdx.x; c < C; c += blockDim.x) {
             float acc = 0.f;
             for (int64_t t = u; t < ntok; t += T) acc = __fadd_rn(acc, __ldg(dx0 + t * C + c));
-            float *o = dwpe + u * C + c;
-            *o = canon(__fadd_rn(*o, acc));
+            dwpe[u * C + c] = canon(acc);  // overwritten (position rows have no other producer)
         }
     }
 }

@@ -169,7 +169,7 @@ def test_embedding_backward_pins():
     tok = np.array([3, 1, 3, 3, 0, 1, 7, 3] * 2, np.int32)
     dx0 = synth.small_ints(4, (16, 5))
     dwte, dwpe = oracle.embedding_backward(tok, dx0, T, np.zeros((10, 5), np.float32),
-                                           np.zeros((T, 5), np.float32))
+                                           np.full((T, 5), 7.0, np.float32))  # dwpe is overwritten
     ref = np.zeros((10, 5), np.int64)
     np.add.at(ref, tok, dx0.astype(np.int64))
     assert np.array_equal(dwte, ref.astype(np.float32))
