@@ -253,6 +253,16 @@ typedef struct {
 
 int verde_node_digest(const verde_node *node, uint8_t *out32);
 
+/* Batched R-NODE + R-MERKLE for a whole step (all host).  Node i's digest is
+ * SHA-256( blob[offs[i] .. offs[i+1]) || table[slots[j]] for j in [soffs[i], soffs[i+1]) )
+ * where blob holds the static part of each node's serialisation above (0x4E ..
+ * u32 n_out) and the slots name its input then output tensor digests in
+ * `table` (n_slots x 32 bytes).  out: n x 32 node digests; root32 (nullable):
+ * RFC 6962 MTH over them -- the step checkpoint (Fig. 2). */
+int verde_node_digests(int64_t n, const uint8_t *blob, const int64_t *offs, const int64_t *slots,
+                       const int64_t *soffs, const uint8_t *table, int64_t n_slots, uint8_t *out,
+                       uint8_t *root32);
+
 /* First index d with seq0[d] != seq1[d] over n 32-byte digests (Alg. 2 line 8,
  * P:429-430), found by descending the two RFC 6962 trees from the roots
  * (O(log n) subtree comparisons).  *d_out = -1 if the sequences are equal. */

@@ -69,6 +69,7 @@ SIGNATURES = {
     "verde_digest_from_subroots": (i32, [vp, i64, i32, i32, vp, i64, vp]),
     "verde_sha256": (i32, [vp, i64, vp]),
     "verde_node_digest": (i32, [vp, vp]),
+    "verde_node_digests": (i32, [i64, vp, vp, vp, vp, vp, i64, vp, vp]),
     "verde_first_divergence": (i32, [vp, vp, i64, vp, vp]),
 }
 

@@ -516,6 +516,27 @@ int verde_node_digest(const verde_node *node, uint8_t *out32) {
     return REPOPS_OK;
 }
 
+int verde_node_digests(int64_t n, const uint8_t *blob, const int64_t *offs, const int64_t *slots, const int64_t *soffs,
+                       const uint8_t *table, int64_t n_slots, uint8_t *out, uint8_t *root32) {
+    REQ(n >= 1 && blob && offs && slots && soffs && table && out, "node_digests: bad argument");
+    for (int64_t i = 0; i < n; ++i) {
+        REQ(offs[i] <= offs[i + 1] && soffs[i] <= soffs[i + 1], "node_digests: offsets not monotone at %lld",
+            (long long)i);
+        Sha256 h;
+        h.put(blob + offs[i], (size_t)(offs[i + 1] - offs[i]));
+        for (int64_t j = soffs[i]; j < soffs[i + 1]; ++j) {
+            REQ(slots[j] >= 0 && slots[j] < n_slots, "node_digests: slot out of range");
+            h.put(table + 32 * slots[j], 32);
+        }
+        h.done(out + 32 * i);
+    }
+    if (root32) {
+        Node32 r = mth(out, 0, n);
+        memcpy(root32, r.b, 32);
+    }
+    return REPOPS_OK;
+}
+
 int verde_first_divergence(const uint8_t *seq0, const uint8_t *seq1, int64_t n, int64_t *d_out, int64_t *rounds_out) {
     REQ(n >= 1 && seq0 && seq1 && d_out, "first_divergence: bad argument");
     // Descend the two RFC 6962 trees: at each node compare the LEFT subtree roots;

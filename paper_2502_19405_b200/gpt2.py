@@ -1,0 +1,722 @@
+"""GPT-2 (124M) training step on RepOps with Verde commitments (BASELINE config 3 + 5).
+
+One step = forward + backward + canonical data-parallel gradient combine +
+AdamW ("forward pass, backward pass, parameter updates and
+an optimizer state update"), every operator a RepOps kernel of librepops.so,
+every operator output committed (R-TCOMMIT) and every graph node hashed into
+the step's Merkle root (the checkpoint commitment, Fig. 2).
+
+Data parallelism (reading R14): the global batch is S = 8 fixed shards of one
+sequence each.  Rank r of G owns shards [r*S/G, (r+1)*S/G).  Per-shard weight
+gradients are R-GEMMs with K = the shard's tokens; the shards' gradients are
+combined by the balanced tree R-TREE_S (aligned local subtree, NCCL all-gather
+of the G partials -- data movement only --, then the top levels on every
+rank).  The result is bit-identical for G in {1, 2, 4, 8}.
+
+Node graph (reading R13): the extended computational graph of Fig. 1
+(P:367-391), topologically ordered as
+  [PARAM_IN x n_params] [for s in 0..S-1: TOKENS_IN, forward nodes, backward nodes]
+  [TREE_SUM x n_params] [ADAMW x n_params]
+Per-shard nodes are G-independent even though the kernels batch all local
+shards into one launch: M-batching of a GEMM and row-batching of a row op are
+bits-neutral.  Every node's inputs / outputs are tensors whose digests live
+in a device digest table; the host builds the node digests and the step root
+with one native call (verde_node_digests_root) after one D2H copy of the table.
+
+Python here only sequences C-ABI calls and owns buffers (torch memory).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import struct
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+import synth
+
+from . import (EPI_BIAS, EPI_SCALE, CommitPlan, repops_add, repops_cross_entropy, repops_embedding,
+               repops_embedding_backward, repops_gelu, repops_gelu_backward, repops_gemm,
+               repops_gemm_strided_batched, repops_layernorm, repops_layernorm_backward,
+               repops_layernorm_backward_params, repops_softmax, repops_softmax_backward, repops_sum_cols_seq,
+               repops_adamw, repops_tree_sum)
+from ._lib import check, lib
+from .dist import all_gather_rows, dp_tree_combine, gather_shard_digests, shard_block
+
+# node operator codes (u16)
+OP = dict(PARAM_IN=1, TOKENS_IN=2, EMBED=3, LAYERNORM=4, LINEAR=5, ATTN_SCORES=6, SOFTMAX=7, ATTN_PV=8,
+          RESIDUAL=9, GELU=10, LM_HEAD=11, CROSS_ENTROPY=12,
+          LM_DGRAD=20, LM_WGRAD=21, LN_BWD=22, LN_PARAM_GRAD=23, LINEAR_DGRAD=24, LINEAR_WGRAD=25,
+          BIAS_GRAD=26, GELU_BWD=27, ATTN_DP=28, SOFTMAX_BWD=29, ATTN_DQKV=30, EMBED_BWD=31,
+          TREE_SUM=40, ADAMW=41)
+# attribute keys
+AK = dict(layer=1, eps=2, scale=3, causal=4, lr=5, beta1=6, beta2=7, adam_eps=8, wd=9, step=10, decay=11,
+          which=12)
+
+
+def f32bits(x: float) -> int:
+    return int(np.float32(x).view(np.uint32))
+
+
+@dataclass
+class GPT2Config:
+    n_layer: int = 12
+    d: int = 768
+    n_head: int = 12
+    ffn: int = 3072
+    vocab: int = 50257
+    n_pos: int = 1024
+    seq: int = 512
+    shards: int = 8
+    ln_eps: float = 1e-5
+    lr: float = 6e-4
+    beta1: float = 0.9
+    beta2: float = 0.95
+    adam_eps: float = 1e-8
+    wd: float = 0.1
+    seed: int = 0
+
+    @property
+    def hd(self):
+        return self.d // self.n_head
+
+    @property
+    def vocab_ld(self):
+        return (self.vocab + 63) // 64 * 64
+
+    @staticmethod
+    def tiny():
+        return GPT2Config(n_layer=2, d=64, n_head=4, ffn=256, vocab=512, n_pos=64, seq=32, shards=8)
+
+
+@dataclass
+class TensorRef:
+    name: str
+    view: torch.Tensor
+    slot: int               # digest-table slot
+    producer: int = -1      # node index
+    pslot: int = 0          # output position within the producer
+
+
+@dataclass
+class NodeRec:
+    index: int
+    op: int
+    shard: int              # 0xFFFFFFFF for replicated nodes
+    attrs: dict
+    inputs: list            # TensorRef indices
+    outputs: list
+    name: str = ""
+    dsts: list = field(default_factory=list)
+
+
+REPLICATED = 0xFFFFFFFF
+
+
+class GPT2Step:
+    """Static program of one training step for the shards owned by this rank."""
+
+    def __init__(self, cfg: GPT2Config, rank: int = 0, world: int = 1, device="cuda", pg=None,
+                 structure_only=False):
+        """structure_only: build the node graph / slot layout on the 'meta' device
+        (no memory, no kernels) -- used by the CPU tests of the host logic."""
+        assert cfg.shards % world == 0
+        self.cfg, self.rank, self.world, self.pg = cfg, rank, world, pg
+        self.structure_only = structure_only
+        self.dev = torch.device("meta" if structure_only else device)
+        self.s0, self.S_loc = shard_block(rank, world, cfg.shards)
+        self.step_no = 0
+        c = cfg
+        self.M = self.S_loc * c.seq
+        self._init_params()
+        self._alloc()
+        self._build_program()
+
+    # ------------------------------------------------------------------ parameters
+    def _init_params(self):
+        c = self.cfg
+        self.specs = synth.gpt2_param_specs(c.n_layer, c.d, c.ffn, c.vocab, c.n_pos)
+        self.off, off = {}, 0
+        for name, shape, kind in self.specs:
+            n = int(np.prod(shape))
+            self.off[name] = (off, shape, kind)
+            off += n
+        self.P = off
+        if self.structure_only:
+            self.params = torch.empty(self.P, device=self.dev)
+            self.m = torch.empty(self.P, device=self.dev)
+            self.v = torch.empty(self.P, device=self.dev)
+            return
+        host = np.empty(self.P, np.float32)
+        for name, shape, kind in self.specs:
+            o, _, _ = self.off[name]
+            host[o:o + int(np.prod(shape))] = synth.gpt2_param(name, shape, kind, c.seed).ravel()
+        self.params = torch.from_numpy(host).to(self.dev)
+        self.m = torch.zeros(self.P, device=self.dev)
+        self.v = torch.zeros(self.P, device=self.dev)
+
+    def pview(self, buf, name):
+        o, shape, _ = self.off[name]
+        return buf[o:o + int(np.prod(shape))].view(*shape)
+
+    # ------------------------------------------------------------------ buffers
+    def _alloc(self):
+        c, M, dev = self.cfg, self.M, self.dev
+        E = lambda *s: torch.empty(*s, dtype=torch.float32, device=dev)  # noqa: E731
+        L, d, T, H = c.n_layer, c.d, c.seq, c.n_head
+        self.tok = torch.empty((self.S_loc, T + 1), dtype=torch.int32, device=dev)
+        self.x = [E(M, d) for _ in range(L + 1)]
+        a = self.act = []
+        for _ in range(L):
+            a.append(dict(ln1=E(M, d), mu1=E(M), rs1=E(M), qkv=E(M, 3 * d), S=E(self.S_loc * H * T, T),
+                          P=E(self.S_loc * H * T, T), att=E(M, d), proj=E(M, d), xmid=E(M, d), ln2=E(M, d),
+                          mu2=E(M), rs2=E(M), fc=E(M, c.ffn), gelu=E(M, c.ffn), fc2=E(M, d)))
+        self.lnf, self.muf, self.rsf = E(M, d), E(M), E(M)
+        self.logits = torch.zeros(M, c.vocab_ld, device=dev)   # padding columns stay 0 (committed bytes)
+        self.dlogits = torch.zeros(M, c.vocab_ld, device=dev)
+        self.loss_tok = E(M)
+        self.dlnf = E(M, d)
+        g = self.grad_act = []
+        for _ in range(L):
+            g.append(dict(dgelu=E(M, c.ffn), dfc=E(M, c.ffn), dln2=E(M, d), dxmid=E(M, d), datt=E(M, d),
+                          dP=E(self.S_loc * H * T, T), dS=E(self.S_loc * H * T, T), dqkv=E(M, 3 * d),
+                          dln1=E(M, d)))
+        self.dx = [E(M, d) for _ in range(L + 1)]  # dx[l] = gradient w.r.t. x[l]
+        self.glocal = torch.zeros(self.S_loc, self.P, device=dev)  # per-shard gradients (rows)
+        self.grad = E(self.P)
+        self.shard_loss = E(self.S_loc)
+
+    # ------------------------------------------------------------------ program construction
+    def _build_program(self):
+        c = self.cfg
+        self.tensors: list[TensorRef] = []
+        self.nodes: list[NodeRec] = []
+        self.phases = []          # list of (name, [launch closures], [tensor ids to commit])
+        self._cur = None
+        # digest slots: replicated region first, then S shard regions of equal size
+        self.rep_slots = 0
+        self.shard_slots = 0
+
+        # pass 1 (count shard slots) uses a dry build of one shard's tensor list;
+        # simpler: assign slots lazily per region, then fix the shard stride afterwards.
+        self._rep_ids, self._shard_ids = [], {s: [] for s in range(c.shards)}
+
+        def T_(name, view, shard):
+            tid = len(self.tensors)
+            self.tensors.append(TensorRef(name, view, -1))
+            (self._rep_ids if shard == REPLICATED else self._shard_ids[shard]).append(tid)
+            return tid
+
+        self._T = T_
+        self._deferred = []
+        # ---- replicated input nodes: parameters with their optimizer state
+        self.phase("inputs")
+        self.param_in = {}
+        for name, shape, kind in self.specs:
+            ids = [T_(f"param/{name}", self.pview(self.params, name), REPLICATED),
+                   T_(f"m/{name}", self.pview(self.m, name), REPLICATED),
+                   T_(f"v/{name}", self.pview(self.v, name), REPLICATED)]
+            self.node(OP["PARAM_IN"], REPLICATED, {}, [], ids, f"in/{name}")
+            self.param_in[name] = ids
+        # ---- per shard (global ids); only local shards get launches, but every
+        # shard's structure is recorded so the node list is the global one
+        self.shard_nodes = {}
+        for s in range(c.shards):
+            self._build_shard(s)
+        # ---- tree + AdamW (replicated)
+        self._build_tree_and_adam()
+        self._finalize()
+
+    def phase(self, name):
+        self._cur = (name, [], [])
+        self.phases.append(self._cur)
+
+    def launch(self, fn):
+        self._cur[1].append(fn)
+
+    def node(self, op, shard, attrs, inputs, outputs, name="", defer=False):
+        idx = len(self.nodes)
+        self.nodes.append(NodeRec(idx, op, shard, attrs, inputs, outputs, name))
+        for q, t in enumerate(outputs):
+            self.tensors[t].producer = idx
+            self.tensors[t].pslot = q
+            if shard == REPLICATED or self._is_local(shard):
+                (self._deferred if defer else self._cur[2]).append(t)
+        return idx
+
+    def _is_local(self, s):
+        return self.s0 <= s < self.s0 + self.S_loc
+
+    # per-shard slab helpers (views only exist for local shards)
+    def _slab(self, buf, s, rows_per_shard):
+        sl = s - self.s0
+        return buf[sl * rows_per_shard:(sl + 1) * rows_per_shard]
+
+    def _build_shard(self, s):
+        c = self.cfg
+        L, d, T, H, hd = c.n_layer, c.d, c.seq, c.n_head, c.hd
+        local = self._is_local(s)
+        first_local = local and s == self.s0
+        T_ = self._T
+        P_ = self.param_in
+        dummy = torch.empty(0, device=self.dev)
+
+        def V(buf, rows):  # view of this shard's slab (or an empty placeholder for remote shards)
+            return self._slab(buf, s, rows) if local else dummy
+
+        def attrs(**kw):
+            out = {}
+            for k, v in kw.items():
+                out[AK[k]] = f32bits(v) if isinstance(v, float) else int(v)
+            return out
+
+        Mloc, S_loc = self.M, self.S_loc
+        sl = s - self.s0
+        # ---------------- forward
+        self.phase(f"s{s}/tokens")
+        t_tok = T_(f"s{s}/tokens", self.tok[sl] if local else dummy, s)
+        self.node(OP["TOKENS_IN"], s, {}, [], [t_tok], f"s{s}/tokens")
+
+        if first_local:
+            self.launch(lambda: repops_embedding(self.tok_in_flat, self.pview(self.params, "wte"),
+                                                 self.pview(self.params, "wpe"), c.seq, out=self.x[0]))
+        t_x = T_(f"s{s}/x0", V(self.x[0], T), s)
+        self.node(OP["EMBED"], s, {}, [t_tok, P_["wte"][0], P_["wpe"][0]], [t_x], f"s{s}/embed")
+
+        for l in range(L):
+            a = self.act[l]
+            p = f"h{l}."
+            W = lambda n: self.pview(self.params, p + n)  # noqa: E731
+            if first_local:
+                def fwd(l=l, a=a, W=W):
+                    repops_layernorm(self.x[l], W("ln1.g"), W("ln1.b"), c.ln_eps, out=a["ln1"], mean=a["mu1"],
+                                     rstd=a["rs1"])
+                    repops_gemm(a["ln1"], W("attn.w"), epi=EPI_BIAS, bias=W("attn.b"), out=a["qkv"])
+                    # scores S = (Q K^T) * 1/sqrt(hd), batched over (local shard, head)
+                    repops_gemm_strided_batched(a["qkv"], a["qkv"], a["S"], M=T, N=T, K=hd, lda=3 * d, ldb=3 * d,
+                                                ldc=T, sA=(T * 3 * d, hd), sB=(T * 3 * d, hd),
+                                                sC=(H * T * T, T * T), batch=(S_loc, H), transB=True,
+                                                epi=EPI_SCALE, scale=1.0 / np.sqrt(hd), offB=d)
+                    repops_softmax(a["S"], causal=True, out=a["P"])
+                    repops_gemm_strided_batched(a["P"], a["qkv"], a["att"], M=T, N=hd, K=T, lda=T, ldb=3 * d,
+                                                ldc=d, sA=(H * T * T, T * T), sB=(T * 3 * d, hd), sC=(T * d, hd),
+                                                batch=(S_loc, H), offB=2 * d)
+                    repops_gemm(a["att"], W("proj.w"), epi=EPI_BIAS, bias=W("proj.b"), out=a["proj"])
+                    repops_add(self.x[l], a["proj"], out=a["xmid"])
+                    repops_layernorm(a["xmid"], W("ln2.g"), W("ln2.b"), c.ln_eps, out=a["ln2"], mean=a["mu2"],
+                                     rstd=a["rs2"])
+                    repops_gemm(a["ln2"], W("fc.w"), epi=EPI_BIAS, bias=W("fc.b"), out=a["fc"])
+                    repops_gelu(a["fc"], out=a["gelu"])
+                    repops_gemm(a["gelu"], W("fc2.w"), epi=EPI_BIAS, bias=W("fc2.b"), out=a["fc2"])
+                    repops_add(a["xmid"], a["fc2"], out=self.x[l + 1])
+                self.launch(fwd)
+            pre = f"s{s}/h{l}/"
+            t_ln1 = T_(pre + "ln1", V(a["ln1"], T), s)
+            t_mu1 = T_(pre + "mu1", V(a["mu1"], T), s)
+            t_rs1 = T_(pre + "rs1", V(a["rs1"], T), s)
+            self.node(OP["LAYERNORM"], s, attrs(layer=l, eps=c.ln_eps, which=1),
+                      [t_x, P_[p + "ln1.g"][0], P_[p + "ln1.b"][0]], [t_ln1, t_mu1, t_rs1], pre + "ln1")
+            t_qkv = T_(pre + "qkv", V(a["qkv"], T), s)
+            self.node(OP["LINEAR"], s, attrs(layer=l, which=1), [t_ln1, P_[p + "attn.w"][0], P_[p + "attn.b"][0]],
+                      [t_qkv], pre + "qkv")
+            t_S = T_(pre + "scores", V(a["S"], H * T), s)
+            self.node(OP["ATTN_SCORES"], s, attrs(layer=l, scale=float(1.0 / np.sqrt(hd))), [t_qkv], [t_S],
+                      pre + "scores")
+            t_P = T_(pre + "probs", V(a["P"], H * T), s)
+            self.node(OP["SOFTMAX"], s, attrs(layer=l, causal=1), [t_S], [t_P], pre + "softmax")
+            t_att = T_(pre + "att", V(a["att"], T), s)
+            self.node(OP["ATTN_PV"], s, attrs(layer=l), [t_P, t_qkv], [t_att], pre + "pv")
+            t_proj = T_(pre + "proj", V(a["proj"], T), s)
+            self.node(OP["LINEAR"], s, attrs(layer=l, which=2), [t_att, P_[p + "proj.w"][0], P_[p + "proj.b"][0]],
+                      [t_proj], pre + "proj")
+            t_xmid = T_(pre + "xmid", V(a["xmid"], T), s)
+            self.node(OP["RESIDUAL"], s, attrs(layer=l, which=1), [t_x, t_proj], [t_xmid], pre + "res1")
+            t_ln2 = T_(pre + "ln2", V(a["ln2"], T), s)
+            t_mu2 = T_(pre + "mu2", V(a["mu2"], T), s)
+            t_rs2 = T_(pre + "rs2", V(a["rs2"], T), s)
+            self.node(OP["LAYERNORM"], s, attrs(layer=l, eps=c.ln_eps, which=2),
+                      [t_xmid, P_[p + "ln2.g"][0], P_[p + "ln2.b"][0]], [t_ln2, t_mu2, t_rs2], pre + "ln2")
+            t_fc = T_(pre + "fc", V(a["fc"], T), s)
+            self.node(OP["LINEAR"], s, attrs(layer=l, which=3), [t_ln2, P_[p + "fc.w"][0], P_[p + "fc.b"][0]],
+                      [t_fc], pre + "fc")
+            t_gelu = T_(pre + "gelu", V(a["gelu"], T), s)
+            self.node(OP["GELU"], s, attrs(layer=l), [t_fc], [t_gelu], pre + "gelu")
+            t_fc2 = T_(pre + "fc2", V(a["fc2"], T), s)
+            self.node(OP["LINEAR"], s, attrs(layer=l, which=4), [t_gelu, P_[p + "fc2.w"][0], P_[p + "fc2.b"][0]],
+                      [t_fc2], pre + "fc2")
+            t_xn = T_(f"s{s}/x{l + 1}", V(self.x[l + 1], T), s)
+            self.node(OP["RESIDUAL"], s, attrs(layer=l, which=2), [t_xmid, t_fc2], [t_xn], pre + "res2")
+            a["_ids"] = a.get("_ids", {})
+            a["_ids"][s] = dict(ln1=t_ln1, mu1=t_mu1, rs1=t_rs1, qkv=t_qkv, P=t_P, att=t_att, xmid=t_xmid,
+                                ln2=t_ln2, mu2=t_mu2, rs2=t_rs2, fc=t_fc, gelu=t_gelu, x=t_x)
+            t_x = t_xn
+            self.phase(f"s{s}/fwd{l + 1}")
+        # ---------------- head
+        if first_local:
+            def head():
+                repops_layernorm(self.x[L], self.pview(self.params, "lnf.g"), self.pview(self.params, "lnf.b"),
+                                 c.ln_eps, out=self.lnf, mean=self.muf, rstd=self.rsf)
+                wte = self.pview(self.params, "wte")
+                repops_gemm(self.lnf, wte, transB=True, out=self.logits[:, :c.vocab])
+                repops_cross_entropy(self.logits, self.targets_flat, scale=1.0 / (c.shards * c.seq),
+                                     loss=self.loss_tok, dlogits=self.dlogits, V=c.vocab)
+            self.launch(head)
+        pre = f"s{s}/head/"
+        t_lnf = T_(pre + "lnf", V(self.lnf, T), s)
+        t_muf = T_(pre + "muf", V(self.muf, T), s)
+        t_rsf = T_(pre + "rsf", V(self.rsf, T), s)
+        self.node(OP["LAYERNORM"], s, attrs(layer=L, eps=c.ln_eps, which=3),
+                  [t_x, P_["lnf.g"][0], P_["lnf.b"][0]], [t_lnf, t_muf, t_rsf], pre + "lnf")
+        t_logits = T_(pre + "logits", V(self.logits, T), s)
+        self.node(OP["LM_HEAD"], s, {}, [t_lnf, P_["wte"][0]], [t_logits], pre + "lm_head")
+        t_loss = T_(pre + "loss", V(self.loss_tok, T), s)
+        t_dlog = T_(pre + "dlogits", V(self.dlogits, T), s)
+        self.node(OP["CROSS_ENTROPY"], s, attrs(scale=float(1.0 / (c.shards * c.seq))), [t_logits, t_tok],
+                  [t_loss, t_dlog], pre + "ce")
+        # ---------------- backward: head
+        self.phase(f"s{s}/bwd_head")
+        gl = self.glocal
+        G_ = lambda n: self._gslice(s, n)  # noqa: E731  this shard's gradient slice of parameter n
+        if first_local:
+            def head_bwd():
+                wte = self.pview(self.params, "wte")
+                repops_gemm(self.dlogits[:, :c.vocab], wte, out=self.dlnf)
+                o = self.off["wte"][0]
+                repops_gemm_strided_batched(self.dlogits, self.lnf, gl, M=c.vocab, N=d, K=T, lda=c.vocab_ld, ldb=d,
+                                            ldc=d, sA=(T * c.vocab_ld, 0), sB=(T * d, 0), sC=(self.P, 0),
+                                            batch=(S_loc, 1), transA=True, offC=o)
+                repops_layernorm_backward(self.dlnf, self.x[L], self.pview(self.params, "lnf.g"), self.muf, self.rsf,
+                                          out=self.dx[L])
+                repops_layernorm_backward_params(self.dlnf, self.x[L], self.muf, self.rsf, nseg=S_loc,
+                                                 dgamma=gl[:, self.off["lnf.g"][0]:],
+                                                 dbeta=gl[:, self.off["lnf.b"][0]:], ldo=self.P)
+            self.launch(head_bwd)
+        t_dlnf = T_(pre + "dlnf", V(self.dlnf, T), s)
+        self.node(OP["LM_DGRAD"], s, {}, [t_dlog, P_["wte"][0]], [t_dlnf], pre + "lm_dgrad")
+        t_gwte_lm = T_(f"s{s}/grad/wte_lm", G_("wte"), s)
+        self.node(OP["LM_WGRAD"], s, {}, [t_dlog, t_lnf], [t_gwte_lm], pre + "lm_wgrad")
+        t_dx = T_(f"s{s}/dx{L}", V(self.dx[L], T), s)
+        self.node(OP["LN_BWD"], s, attrs(layer=L, which=3), [t_dlnf, t_x, P_["lnf.g"][0], t_muf, t_rsf], [t_dx],
+                  pre + "lnf_bwd")
+        self.final_grad = getattr(self, "final_grad", {})
+        fg = self.final_grad.setdefault(s, {})
+        fg["lnf.g"] = T_(f"s{s}/grad/lnf.g", G_("lnf.g"), s)
+        fg["lnf.b"] = T_(f"s{s}/grad/lnf.b", G_("lnf.b"), s)
+        self.node(OP["LN_PARAM_GRAD"], s, attrs(layer=L, which=3), [t_dlnf, t_x, t_muf, t_rsf],
+                  [fg["lnf.g"], fg["lnf.b"]], pre + "lnf_params")
+        # ---------------- backward: layers
+        for l in reversed(range(L)):
+            a, g = self.act[l], self.grad_act[l]
+            ids = a["_ids"][s]
+            p = f"h{l}."
+            W = lambda n, p=p: self.pview(self.params, p + n)  # noqa: E731
+            self.phase(f"s{s}/bwd{l}")
+            if first_local:
+                def bwd(l=l, a=a, g=g, W=W, p=p):
+                    dout = self.dx[l + 1]
+                    o = lambda n: self.off[p + n][0]  # noqa: E731
+                    # FC2
+                    repops_gemm(dout, W("fc2.w"), transB=True, out=g["dgelu"])
+                    repops_gemm_strided_batched(a["gelu"], dout, gl, M=c.ffn, N=d, K=T, lda=c.ffn, ldb=d, ldc=d,
+                                                sA=(T * c.ffn, 0), sB=(T * d, 0), sC=(self.P, 0), batch=(S_loc, 1),
+                                                transA=True, offC=o("fc2.w"))
+                    repops_sum_cols_seq(dout, nseg=S_loc, out=gl[:, o("fc2.b"):], ldo=self.P)
+                    repops_gelu_backward(a["fc"], g["dgelu"], out=g["dfc"])
+                    # FC
+                    repops_gemm(g["dfc"], W("fc.w"), transB=True, out=g["dln2"])
+                    repops_gemm_strided_batched(a["ln2"], g["dfc"], gl, M=d, N=c.ffn, K=T, lda=d, ldb=c.ffn,
+                                                ldc=c.ffn, sA=(T * d, 0), sB=(T * c.ffn, 0), sC=(self.P, 0),
+                                                batch=(S_loc, 1), transA=True, offC=o("fc.w"))
+                    repops_sum_cols_seq(g["dfc"], nseg=S_loc, out=gl[:, o("fc.b"):], ldo=self.P)
+                    # LN2 (+ residual gradient)
+                    repops_layernorm_backward(g["dln2"], a["xmid"], W("ln2.g"), a["mu2"], a["rs2"], dres=dout,
+                                              out=g["dxmid"])
+                    repops_layernorm_backward_params(g["dln2"], a["xmid"], a["mu2"], a["rs2"], nseg=S_loc,
+                                                     dgamma=gl[:, o("ln2.g"):], dbeta=gl[:, o("ln2.b"):], ldo=self.P)
+                    # proj
+                    repops_gemm(g["dxmid"], W("proj.w"), transB=True, out=g["datt"])
+                    repops_gemm_strided_batched(a["att"], g["dxmid"], gl, M=d, N=d, K=T, lda=d, ldb=d, ldc=d,
+                                                sA=(T * d, 0), sB=(T * d, 0), sC=(self.P, 0), batch=(S_loc, 1),
+                                                transA=True, offC=o("proj.w"))
+                    repops_sum_cols_seq(g["dxmid"], nseg=S_loc, out=gl[:, o("proj.b"):], ldo=self.P)
+                    # attention
+                    repops_gemm_strided_batched(g["datt"], a["qkv"], g["dP"], M=T, N=T, K=hd, lda=d, ldb=3 * d,
+                                                ldc=T, sA=(T * d, hd), sB=(T * 3 * d, hd), sC=(H * T * T, T * T),
+                                                batch=(S_loc, H), transB=True, offB=2 * d)
+                    repops_softmax_backward(a["P"], g["dP"], scale=1.0 / np.sqrt(hd), out=g["dS"])
+                    # dV = P^T dO ; dQ = dS K ; dK = dS^T Q   (into the packed dqkv)
+                    repops_gemm_strided_batched(a["P"], g["datt"], g["dqkv"], M=T, N=hd, K=T, lda=T, ldb=d,
+                                                ldc=3 * d, sA=(H * T * T, T * T), sB=(T * d, hd),
+                                                sC=(T * 3 * d, hd), batch=(S_loc, H), transA=True, offC=2 * d)
+                    repops_gemm_strided_batched(g["dS"], a["qkv"], g["dqkv"], M=T, N=hd, K=T, lda=T, ldb=3 * d,
+                                                ldc=3 * d, sA=(H * T * T, T * T), sB=(T * 3 * d, hd),
+                                                sC=(T * 3 * d, hd), batch=(S_loc, H), offB=d)
+                    repops_gemm_strided_batched(g["dS"], a["qkv"], g["dqkv"], M=T, N=hd, K=T, lda=T, ldb=3 * d,
+                                                ldc=3 * d, sA=(H * T * T, T * T), sB=(T * 3 * d, hd),
+                                                sC=(T * 3 * d, hd), batch=(S_loc, H), transA=True, offC=d)
+                    # QKV
+                    repops_gemm(g["dqkv"], W("attn.w"), transB=True, out=g["dln1"])
+                    repops_gemm_strided_batched(a["ln1"], g["dqkv"], gl, M=d, N=3 * d, K=T, lda=d, ldb=3 * d,
+                                                ldc=3 * d, sA=(T * d, 0), sB=(T * 3 * d, 0), sC=(self.P, 0),
+                                                batch=(S_loc, 1), transA=True, offC=o("attn.w"))
+                    repops_sum_cols_seq(g["dqkv"], nseg=S_loc, out=gl[:, o("attn.b"):], ldo=self.P)
+                    repops_layernorm_backward(g["dln1"], self.x[l], W("ln1.g"), a["mu1"], a["rs1"], dres=g["dxmid"],
+                                              out=self.dx[l])
+                    repops_layernorm_backward_params(g["dln1"], self.x[l], a["mu1"], a["rs1"], nseg=S_loc,
+                                                     dgamma=gl[:, o("ln1.g"):], dbeta=gl[:, o("ln1.b"):], ldo=self.P)
+                self.launch(bwd)
+            pre = f"s{s}/h{l}/"
+            t_dout = t_dx
+            t_dgelu = T_(pre + "dgelu", V(g["dgelu"], T), s)
+            self.node(OP["LINEAR_DGRAD"], s, attrs(layer=l, which=4), [t_dout, P_[p + "fc2.w"][0]], [t_dgelu],
+                      pre + "fc2_dgrad")
+            fg[p + "fc2.w"] = T_(f"s{s}/grad/{p}fc2.w", G_(p + "fc2.w"), s)
+            self.node(OP["LINEAR_WGRAD"], s, attrs(layer=l, which=4), [ids["gelu"], t_dout], [fg[p + "fc2.w"]],
+                      pre + "fc2_wgrad")
+            fg[p + "fc2.b"] = T_(f"s{s}/grad/{p}fc2.b", G_(p + "fc2.b"), s)
+            self.node(OP["BIAS_GRAD"], s, attrs(layer=l, which=4), [t_dout], [fg[p + "fc2.b"]], pre + "fc2_bgrad")
+            t_dfc = T_(pre + "dfc", V(g["dfc"], T), s)
+            self.node(OP["GELU_BWD"], s, attrs(layer=l), [ids["fc"], t_dgelu], [t_dfc], pre + "gelu_bwd")
+            t_dln2 = T_(pre + "dln2", V(g["dln2"], T), s)
+            self.node(OP["LINEAR_DGRAD"], s, attrs(layer=l, which=3), [t_dfc, P_[p + "fc.w"][0]], [t_dln2],
+                      pre + "fc_dgrad")
+            fg[p + "fc.w"] = T_(f"s{s}/grad/{p}fc.w", G_(p + "fc.w"), s)
+            self.node(OP["LINEAR_WGRAD"], s, attrs(layer=l, which=3), [ids["ln2"], t_dfc], [fg[p + "fc.w"]],
+                      pre + "fc_wgrad")
+            fg[p + "fc.b"] = T_(f"s{s}/grad/{p}fc.b", G_(p + "fc.b"), s)
+            self.node(OP["BIAS_GRAD"], s, attrs(layer=l, which=3), [t_dfc], [fg[p + "fc.b"]], pre + "fc_bgrad")
+            t_dxmid = T_(pre + "dxmid", V(g["dxmid"], T), s)
+            self.node(OP["LN_BWD"], s, attrs(layer=l, which=2),
+                      [t_dln2, ids["xmid"], P_[p + "ln2.g"][0], ids["mu2"], ids["rs2"], t_dout], [t_dxmid],
+                      pre + "ln2_bwd")
+            fg[p + "ln2.g"] = T_(f"s{s}/grad/{p}ln2.g", G_(p + "ln2.g"), s)
+            fg[p + "ln2.b"] = T_(f"s{s}/grad/{p}ln2.b", G_(p + "ln2.b"), s)
+            self.node(OP["LN_PARAM_GRAD"], s, attrs(layer=l, which=2), [t_dln2, ids["xmid"], ids["mu2"], ids["rs2"]],
+                      [fg[p + "ln2.g"], fg[p + "ln2.b"]], pre + "ln2_params")
+            t_datt = T_(pre + "datt", V(g["datt"], T), s)
+            self.node(OP["LINEAR_DGRAD"], s, attrs(layer=l, which=2), [t_dxmid, P_[p + "proj.w"][0]], [t_datt],
+                      pre + "proj_dgrad")
+            fg[p + "proj.w"] = T_(f"s{s}/grad/{p}proj.w", G_(p + "proj.w"), s)
+            self.node(OP["LINEAR_WGRAD"], s, attrs(layer=l, which=2), [ids["att"], t_dxmid], [fg[p + "proj.w"]],
+                      pre + "proj_wgrad")
+            fg[p + "proj.b"] = T_(f"s{s}/grad/{p}proj.b", G_(p + "proj.b"), s)
+            self.node(OP["BIAS_GRAD"], s, attrs(layer=l, which=2), [t_dxmid], [fg[p + "proj.b"]], pre + "proj_bgrad")
+            t_dP = T_(pre + "dP", V(g["dP"], H * T), s)
+            self.node(OP["ATTN_DP"], s, attrs(layer=l), [t_datt, ids["qkv"]], [t_dP], pre + "attn_dp")
+            t_dS = T_(pre + "dS", V(g["dS"], H * T), s)
+            self.node(OP["SOFTMAX_BWD"], s, attrs(layer=l, scale=float(1.0 / np.sqrt(hd))), [ids["P"], t_dP], [t_dS],
+                      pre + "softmax_bwd")
+            t_dqkv = T_(pre + "dqkv", V(g["dqkv"], T), s)
+            self.node(OP["ATTN_DQKV"], s, attrs(layer=l), [t_dS, ids["P"], t_datt, ids["qkv"]], [t_dqkv],
+                      pre + "attn_dqkv")
+            t_dln1 = T_(pre + "dln1", V(g["dln1"], T), s)
+            self.node(OP["LINEAR_DGRAD"], s, attrs(layer=l, which=1), [t_dqkv, P_[p + "attn.w"][0]], [t_dln1],
+                      pre + "qkv_dgrad")
+            fg[p + "attn.w"] = T_(f"s{s}/grad/{p}attn.w", G_(p + "attn.w"), s)
+            self.node(OP["LINEAR_WGRAD"], s, attrs(layer=l, which=1), [ids["ln1"], t_dqkv], [fg[p + "attn.w"]],
+                      pre + "qkv_wgrad")
+            fg[p + "attn.b"] = T_(f"s{s}/grad/{p}attn.b", G_(p + "attn.b"), s)
+            self.node(OP["BIAS_GRAD"], s, attrs(layer=l, which=1), [t_dqkv], [fg[p + "attn.b"]], pre + "qkv_bgrad")
+            t_dx = T_(f"s{s}/dx{l}", V(self.dx[l], T), s)
+            self.node(OP["LN_BWD"], s, attrs(layer=l, which=1),
+                      [t_dln1, ids["x"], P_[p + "ln1.g"][0], ids["mu1"], ids["rs1"], t_dxmid], [t_dx],
+                      pre + "ln1_bwd")
+            fg[p + "ln1.g"] = T_(f"s{s}/grad/{p}ln1.g", G_(p + "ln1.g"), s)
+            fg[p + "ln1.b"] = T_(f"s{s}/grad/{p}ln1.b", G_(p + "ln1.b"), s)
+            self.node(OP["LN_PARAM_GRAD"], s, attrs(layer=l, which=1), [t_dln1, ids["x"], ids["mu1"], ids["rs1"]],
+                      [fg[p + "ln1.g"], fg[p + "ln1.b"]], pre + "ln1_params")
+        # ---------------- embedding backward (accumulates IN PLACE into the tied lm-head
+        # gradient, so it runs -- and is committed -- in a global phase after every
+        # shard's LM_WGRAD output has been committed; the node keeps its place in
+        # the shard's node order)
+        fg["wte"] = T_(f"s{s}/grad/wte", G_("wte"), s)
+        fg["wpe"] = T_(f"s{s}/grad/wpe", G_("wpe"), s)
+        self.node(OP["EMBED_BWD"], s, {}, [t_tok, t_dx, t_gwte_lm], [fg["wte"], fg["wpe"]], f"s{s}/embed_bwd",
+                  defer=True)
+
+    def _gslice(self, s, name):
+        if not self._is_local(s):
+            return torch.empty(0, device=self.dev)
+        o, shape, _ = self.off[name]
+        return self.glocal[s - self.s0, o:o + int(np.prod(shape))].view(*shape)
+
+    def _build_tree_and_adam(self):
+        c = self.cfg
+        self.phase("embed_bwd")
+
+        def emb_bwd():
+            for q in range(self.S_loc):
+                repops_embedding_backward(self.tok_in[q], self.dx[0][q * c.seq:(q + 1) * c.seq], c.seq,
+                                          self._gslice(self.s0 + q, "wte"), self._gslice(self.s0 + q, "wpe"))
+        self.launch(emb_bwd)
+        self._cur[2].extend(self._deferred)
+        self.phase("tree")
+
+        def tree():
+            parts = [self.glocal[q] for q in range(self.S_loc)]
+            dp_tree_combine(parts, self.world, lambda ps, out: repops_tree_sum(ps, out=out), self.pg, out=self.grad)
+        self.launch(tree)
+        T_ = self._T
+        self.grad_out = {}
+        for name, shape, kind in self.specs:
+            t = T_(f"grad/{name}", self.pview(self.grad, name), REPLICATED)
+            ins = [self.final_grad[s][name] for s in range(c.shards)]
+            self.node(OP["TREE_SUM"], REPLICATED, {}, ins, [t], f"tree/{name}")
+            self.grad_out[name] = t
+        self.phase("adamw")
+
+        def adam():
+            for name, shape, kind in self.specs:
+                decay = len(shape) == 2
+                repops_adamw(self.pview(self.params, name), self.pview(self.grad, name), self.pview(self.m, name),
+                             self.pview(self.v, name), self.step_no + 1, c.lr, c.beta1, c.beta2, c.adam_eps, c.wd,
+                             decay)
+        self.launch(adam)
+        self.adam_out = {}
+        for name, shape, kind in self.specs:
+            p_, m_, v_ = self.param_in[name]
+            outs = [T_(f"param'/{name}", self.pview(self.params, name), REPLICATED),
+                    T_(f"m'/{name}", self.pview(self.m, name), REPLICATED),
+                    T_(f"v'/{name}", self.pview(self.v, name), REPLICATED)]
+            attrs = {AK["lr"]: f32bits(c.lr), AK["beta1"]: f32bits(c.beta1), AK["beta2"]: f32bits(c.beta2),
+                     AK["adam_eps"]: f32bits(c.adam_eps), AK["wd"]: f32bits(c.wd),
+                     AK["decay"]: int(len(shape) == 2)}
+            self.node(OP["ADAMW"], REPLICATED, attrs, [p_, self.grad_out[name], m_, v_], outs, f"adamw/{name}")
+            self.adam_out[name] = outs
+
+    # ------------------------------------------------------------------ finalisation
+    def _finalize(self):
+        c = self.cfg
+        # digest slots: replicated ids first, then shard regions with a common stride
+        for i, t in enumerate(self._rep_ids):
+            self.tensors[t].slot = i
+        n_rep = len(self._rep_ids)
+        per = len(self._shard_ids[0])
+        assert all(len(v) == per for v in self._shard_ids.values())
+        self.rep_slots, self.shard_slots = n_rep, per
+        for s in range(c.shards):
+            for i, t in enumerate(self._shard_ids[s]):
+                self.tensors[t].slot = n_rep + s * per + i
+        self.n_slots = n_rep + c.shards * per
+        self.digests = torch.zeros((self.n_slots, 32), dtype=torch.uint8, device=self.dev)
+        pin = (lambda t: t) if self.structure_only else (lambda t: t.pin_memory())
+        self.digests_host = pin(torch.zeros((self.n_slots, 32), dtype=torch.uint8))
+        # consumers (output node pointers of the box)
+        for nd in self.nodes:
+            for t in nd.inputs:
+                src = self.tensors[t].producer
+                if nd.index not in self.nodes[src].dsts:
+                    self.nodes[src].dsts.append(nd.index)
+        # token arrays used by the batched launches (staged from the host with the batch)
+        self.tok_in = torch.empty((self.S_loc, c.seq), dtype=torch.int32, device=self.dev)
+        self.tok_in_flat = self.tok_in.view(-1)
+        self.targets = torch.empty((self.S_loc, c.seq), dtype=torch.int32, device=self.dev)
+        self.targets_flat = self.targets.view(-1)
+        self.tok_host = pin(torch.empty((self.S_loc, c.seq + 1), dtype=torch.int32))
+        self.tin_host = pin(torch.empty((self.S_loc, c.seq), dtype=torch.int32))
+        self.tgt_host = pin(torch.empty((self.S_loc, c.seq), dtype=torch.int32))
+        # one commit plan per phase (tensors produced in that phase, local or replicated)
+        self.plans = []
+        for name, fns, tids in self.phases:
+            views = [self.tensors[t].view for t in tids]
+            if views and not self.structure_only:
+                self.plans.append(CommitPlan(views, [self.digests[self.tensors[t].slot] for t in tids]))
+            else:
+                self.plans.append(None)
+        self.commit_bytes = sum(p.nbytes for p in self.plans if p is not None)
+        self._build_node_blob()
+
+    def _build_node_blob(self):
+        """Static serialisation of every node except its tensor digests (R13)."""
+        blob, offs, slots, soffs = bytearray(), [0], [], [0]
+        for nd in self.nodes:
+            keys = sorted(nd.attrs)
+            b = bytearray(b"\x4e")
+            b += struct.pack("<IHI", nd.index, nd.op, nd.shard)
+            b += struct.pack("<I", len(keys))
+            for k in keys:
+                b += struct.pack("<IQ", k, nd.attrs[k])
+            b += struct.pack("<I", len(nd.inputs))
+            for t in nd.inputs:
+                b += struct.pack("<II", self.tensors[t].producer, self.tensors[t].pslot)
+            b += struct.pack("<I", len(nd.dsts))
+            for q in nd.dsts:
+                b += struct.pack("<I", q)
+            b += struct.pack("<I", len(nd.outputs))
+            blob += b
+            offs.append(len(blob))
+            slots += [self.tensors[t].slot for t in nd.inputs] + [self.tensors[t].slot for t in nd.outputs]
+            soffs.append(len(slots))
+        self.node_blob = np.frombuffer(bytes(blob), np.uint8).copy()
+        self.node_offs = np.asarray(offs, np.int64)
+        self.node_slots = np.asarray(slots, np.int64)
+        self.node_soffs = np.asarray(soffs, np.int64)
+
+    # ------------------------------------------------------------------ running
+    def set_tokens(self, step: int | None = None, host_tokens=None):
+        """Load this rank's shards' tokens (synthetic recipe, or given host int32 [S_loc, T+1])."""
+        c = self.cfg
+        if host_tokens is None:
+            st = self.step_no if step is None else step
+            host_tokens = np.stack([synth.gpt2_tokens(c.vocab, c.seq, self.s0 + q, st, c.seed)
+                                    for q in range(self.S_loc)])
+        h = np.ascontiguousarray(host_tokens, dtype=np.int32)
+        self.tok_host.numpy()[...] = h
+        self.tin_host.numpy()[...] = h[:, :c.seq]
+        self.tgt_host.numpy()[...] = h[:, 1:]
+        self.tok.copy_(self.tok_host, non_blocking=True)     # H2D: the step's input batch
+        self.tok_in.copy_(self.tin_host, non_blocking=True)
+        self.targets.copy_(self.tgt_host, non_blocking=True)
+
+    @property
+    def h2d_bytes(self):
+        return 3 * self.tok_host.numel() * 4
+
+    def run(self, commit=True, inject=None):
+        """Enqueue one full training step.  inject = (phase_name, fn) runs fn after that
+        phase's kernels (fault injection for the dispute demo)."""
+        for (name, fns, _), plan in zip(self.phases, self.plans):
+            for fn in fns:
+                fn()
+            if inject is not None and inject[0] == name:
+                inject[1]()
+            if commit and plan is not None:
+                plan.run()
+        self.step_no += 1
+
+    def gather_digests(self):
+        """C2: all-gather the per-shard digest regions; copy the table to the host."""
+        gather_shard_digests(self.digests, self.rep_slots, self.shard_slots, self.s0, self.S_loc, self.world, self.pg)
+        self.digests_host.copy_(self.digests, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return self.digests_host.numpy()
+
+    def step_root(self, table=None):
+        """Node digests (R-NODE) and the step's Merkle root (R-MERKLE), host native code."""
+        table = self.gather_digests() if table is None else table
+        n = len(self.nodes)
+        out = np.empty((n, 32), np.uint8)
+        root = np.empty(32, np.uint8)
+        P = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        check(lib().verde_node_digests(n, P(self.node_blob), P(self.node_offs), P(self.node_slots),
+                                       P(self.node_soffs), P(np.ascontiguousarray(table)), self.n_slots, P(out),
+                                       P(root)), "verde_node_digests")
+        return root.tobytes(), out
+
+    def loss(self):
+        """Step loss (reported metric): R-SEQ per shard, R-TREE_S over shards, x 1/(S T)."""
+        from . import repops_sum_cols_seq as seq
+        seq(self.loss_tok.view(-1, 1), nseg=self.S_loc, out=self.shard_loss.view(-1, 1))
+        allv = all_gather_rows(self.shard_loss, self.world, self.pg).reshape(-1)
+        tot = repops_tree_sum([allv[q:q + 1] for q in range(self.cfg.shards)])
+        return float(np.float32(tot.item()) * np.float32(1.0 / (self.cfg.shards * self.cfg.seq)))
+
+    def flops_per_step(self):
+        """Algorithmic matmul flops of one full step (all shards): fwd 2*M*N*K, bwd 2x fwd."""
+        c = self.cfg
+        Ntok = c.shards * c.seq
+        lin = 2 * Ntok * (c.d * 3 * c.d + c.d * c.d + 2 * c.d * c.ffn) * c.n_layer
+        attn = 2 * 2 * c.shards * c.n_head * c.seq * c.seq * c.hd * c.n_layer
+        head = 2 * Ntok * c.d * c.vocab
+        return 3 * (lin + attn + head)
