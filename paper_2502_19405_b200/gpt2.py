@@ -287,7 +287,7 @@ class GPT2Step:
         for l in range(L):
             a = self.act[l]
             p = f"h{l}."
-            W = lambda n: self.pview(self.params, p + n)  # noqa: E731
+            W = lambda n, p=p: self.pview(self.params, p + n)  # noqa: E731  (bind this layer's prefix)
             if first_local:
                 def fwd(l=l, a=a, W=W):
                     repops_layernorm(self.x[l], W("ln1.g"), W("ln1.b"), c.ln_eps, out=a["ln1"], mean=a["mu1"],
