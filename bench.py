@@ -1,20 +1,23 @@
-"""bench.py -- RepOps / Verde hot path on B200 (see DESIGN.md §7 "Measurement").
+"""bench.py -- RepOps / Verde hot path on B200 (DESIGN.md §7 "Measurement").
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl repops|reference] [--workload gemm]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl repops|reference] [--workload gpt2|gemm]
     python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \
         --master-port P bench.py --gpus N --steps K --warmup W
 
-Workload "gemm" (BASELINE.json configs[1]: reproducible FP32 GEMM sweep, square
-1024..8192, M-sharded over N GPUs, 0-ULP vs the oracle).  One step = the whole
-hot path of that config over one batch of synthetic inputs:
-  for n in (1024, 2048, 4096, 8192):
-      C_r = R-GEMM(A[rows_r], B)            (rank r owns n/N rows, full K)
-      root_r = Verde data-root commit of C_r (SHA-256 leaves + RFC 6962 levels)
-  all_gather(root_r) -> tensor digest of C   (identical at every N)
-value = sum of 2 n^3 over the sweep / max-over-ranks device time per step.
+Default workload "gpt2" (BASELINE.json configs[2] + [4]): one GPT-2 small (124M)
+training step, batch 8 x seq 512, as S = 8 data-parallel shards spread over the
+N GPUs: forward, backward, canonical R-TREE_S gradient combine (NCCL all-gather
+of partials for N > 1), AdamW, a Verde commitment (SHA-256 / RFC 6962) of every
+operator output, the node digests and the step's Merkle root.  This is one pass
+of every §8(a) row.  value = algorithmic matmul TFLOP of the step / step time;
+ms_per_step is the GPT-2 step time (the metric's second half).
 
-Prints ONE JSON line (rank 0).  The oracle (CPU, test infrastructure) is only
-executed by the cpu_baseline leg (rank 0, N = 1) and by --impl reference.
+The GEMM sweep of configs[1] (square 1024..8192, M-sharded) runs in the same
+invocation and is reported under "gemm_sweep"; --workload gemm makes it the
+headline line instead.
+
+Prints ONE JSON line (rank 0).  The oracle (CPU test infrastructure) is only
+run by the cpu_baseline leg (rank 0, N = 1) and by --impl reference.
 """
 from __future__ import annotations
 
@@ -41,12 +44,19 @@ def fp32_peak_tflops(mhz: float, sms: int = 148) -> float:
     return sms * 128 * 2 * mhz * 1e6 / 1e12
 
 
+def measured_hbm_gbs() -> float:
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return 6650.0  # B200_PROFILING.md fallback
+
+
 # ---------------------------------------------------------------------- clocks
 class ClockSampler:
     """NVML sampling of SM clock + throttle reasons while the timed region runs."""
 
     REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
-               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle"}
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, index: int):
         self.samples, self.reasons, self.max_mhz = [], set(), None
@@ -66,7 +76,7 @@ class ClockSampler:
                 self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
                 r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 for bit, name in self.REASONS.items():
-                    if r & bit and name != "gpu_idle":
+                    if r & bit:
                         self.reasons.add(name)
             except Exception:
                 pass
@@ -96,8 +106,8 @@ def dist_init():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
     if world > 1:
-        torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return rank, world, local
 
@@ -114,7 +124,7 @@ def max_over_ranks(x: float, world: int) -> float:
     import torch
     import torch.distributed as dist
     t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)  # timing scalar only (not the data path)
     return float(t.item())
 
 
@@ -124,6 +134,7 @@ class GemmSweep:
 
     def __init__(self, rank, world, device):
         import torch
+
         import paper_2502_19405_b200 as R
         import synth
         self.R, self.torch = R, torch
@@ -135,77 +146,77 @@ class GemmSweep:
             Ar = np.ascontiguousarray(A[rank * rows:(rank + 1) * rows])
             hA = torch.from_numpy(Ar).pin_memory()
             hB = torch.from_numpy(B).pin_memory()
-            dA = hA.to(device)
-            dB = hB.to(device)
-            dC = torch.empty((rows, n), dtype=torch.float32, device=device)
-            self.items.append(dict(n=n, rows=rows, hA=hA, hB=hB, A=dA, B=dB, C=dC))
+            self.items.append(dict(n=n, rows=rows, hA=hA, hB=hB, A=hA.to(device), B=hB.to(device),
+                                   C=torch.empty((rows, n), dtype=torch.float32, device=device)))
         self.roots = torch.empty((len(SIZES), 32), dtype=torch.uint8, device=device)
-        self.ws = R.CommitWorkspace(device)
-        self.stream = torch.cuda.current_stream()
-        self.gemm_ms = []  # per-launch device times of the dominant kernel
-        self.gemm_flops = 0
+        self.plan = R.CommitPlan([it["C"] for it in self.items], self.roots, modes=[1] * len(SIZES))
+        self.flops = SWEEP_FLOPS
 
-    def step(self, time_gemm=False):
-        R, torch = self.R, self.torch
+    def step(self):
         for it in self.items:
-            if time_gemm:
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(self.stream)
-            R.repops_gemm(it["A"], it["B"], out=it["C"])
-            if time_gemm:
-                e1.record(self.stream)
-                self.gemm_ms.append((e0, e1, 2 * it["rows"] * it["n"] * it["n"]))
-        R.verde_commit_tensors([it["C"] for it in self.items], digests=self.roots, ws=self.ws, mode=1)
+            self.R.repops_gemm(it["A"], it["B"], out=it["C"])
+        self.plan.run()
 
     def e2e_step(self):
-        """Same step through the public API from pinned HOST buffers: H2D of the
-        inputs, the step, D2H of the committed result (the slab roots)."""
         for it in self.items:
             it["A"].copy_(it["hA"], non_blocking=True)
             it["B"].copy_(it["hB"], non_blocking=True)
         self.step()
-        return self.roots.to("cpu", non_blocking=False)
+        return self.roots.to("cpu")
 
     @property
     def h2d_bytes(self):
         return sum(it["hA"].numel() * 4 + it["hB"].numel() * 4 for it in self.items)
 
-    @property
-    def d2h_bytes(self):
-        return self.roots.numel()
+    d2h_bytes = len(SIZES) * 32
 
     def digests(self):
         """Tensor digests of the full C matrices (identical at every world size)."""
-        torch = self.torch
-        roots = self.roots
-        if self.world > 1:
-            import torch.distributed as dist
-            parts = [torch.empty_like(roots) for _ in range(self.world)]
-            dist.all_gather(parts, roots)
-        else:
-            parts = [roots]
+        from paper_2502_19405_b200.dist import all_gather_rows
+        parts = all_gather_rows(self.roots, self.world).cpu().numpy()
         out = []
         for q, it in enumerate(self.items):
-            sub = b"".join(bytes(p[q].cpu().numpy().tobytes()) for p in parts)
             n = it["n"]
+            sub = b"".join(parts[r, q].tobytes() for r in range(self.world))
             out.append(self.R.verde_digest_from_subroots(sub, self.R.F32, (n, n), n * n * 4).hex())
         return out
 
-    def kernel_times(self):
-        ms = sum(e0.elapsed_time(e1) for e0, e1, _ in self.gemm_ms)
-        flops = sum(f for _, _, f in self.gemm_ms)
-        return ms, flops, len(self.gemm_ms)
+
+# ---------------------------------------------------------------------- GPT-2 workload
+class GPT2Train:
+    def __init__(self, rank, world, device, pg=None):
+        from paper_2502_19405_b200.gpt2 import GPT2Config, GPT2Step
+        self.st = GPT2Step(GPT2Config(), rank=rank, world=world, device=device, pg=pg)
+        self.st.set_tokens(0)
+        self.flops = self.st.flops_per_step()
+        self.root = None
+
+    def step(self):
+        self.st.run()
+        self.root, _ = self.st.step_root()   # C2 gather + D2H of the digest table + node digests + root
+
+    def e2e_step(self):
+        self.st.set_tokens(self.st.step_no)    # H2D of this step's batch from pinned host memory
+        self.step()
+        return self.st.loss(), self.root       # D2H of the loss (root already on the host)
+
+    @property
+    def h2d_bytes(self):
+        return self.st.h2d_bytes
+
+    @property
+    def d2h_bytes(self):
+        return self.st.n_slots * 32 + 4
 
 
 # ---------------------------------------------------------------------- oracle legs
-def cpu_sample_gemm(seconds_target=10.0):
-    """Time the oracle (as it stands) on a bounded sample of the workload: the first
-    r rows of each GEMM in the sweep (full K fold per element), r chosen for ~10 s."""
+def oracle_sample_gemm(seconds_target=10.0):
+    """The oracle (as it stands) on a bounded sample of the GEMM sweep: the first r
+    rows of each GEMM (full K fold per element), r chosen for ~10 s on one core."""
     import oracle
     import synth
     oracle.lib()
     flops, t_total, rows_done = 0, 0.0, {}
-    # calibrate on the 1024 problem
     A, B = synth.gemm_inputs(1024, "bench")
     t0 = time.perf_counter()
     oracle.gemm(A[:2], B)
@@ -213,14 +224,37 @@ def cpu_sample_gemm(seconds_target=10.0):
     for n in SIZES:
         A, B = synth.gemm_inputs(n, "bench")
         est_row = per_row_1024 * (n / 1024) ** 2 * (1.6 if n >= 4096 else 1.0)
-        r = max(1, int(seconds_target / len(SIZES) / est_row))
-        r = min(r, n)
+        r = min(n, max(1, int(seconds_target / len(SIZES) / est_row)))
         t0 = time.perf_counter()
         oracle.gemm(A[:r], B)
         t_total += time.perf_counter() - t0
         flops += 2 * r * n * n
         rows_done[n] = r
-    return flops / t_total / 1e12, t_total, rows_done
+    return flops / t_total / 1e12, t_total, f"first rows {rows_done} of each sweep GEMM (full K fold)"
+
+
+def oracle_sample_gpt2(rows=8):
+    """The oracle on a bounded sample of the GPT-2 step: `rows` token rows of shard 0
+    through layer 0's four linear GEMMs (full K folds) and the LM head (K = 768 over
+    all 50257 vocabulary columns), with their LayerNorm / GELU / softmax row work."""
+    import oracle
+    import synth
+    oracle.lib()
+    d, F, V, T = 768, 3072, 50257, 512
+    W = {n: synth.gpt2_param(n, s, k) for n, s, k in synth.gpt2_param_specs(1, d, F, V, 1024)}
+    x = synth.uniform(11, (rows, d), 1.0)
+    t0 = time.perf_counter()
+    ln, _, _ = oracle.layernorm(x, W["h0.ln1.g"], W["h0.ln1.b"])
+    qkv = oracle.gemm(ln, W["h0.attn.w"], epi=1, bias=W["h0.attn.b"])
+    oracle.softmax(qkv[:, :T].copy(), causal=False)
+    proj = oracle.gemm(qkv[:, :d].copy(), W["h0.proj.w"], epi=1, bias=W["h0.proj.b"])
+    fc = oracle.gemm(proj, W["h0.fc.w"], epi=1, bias=W["h0.fc.b"])
+    g = oracle.gelu(fc)
+    fc2 = oracle.gemm(g, W["h0.fc2.w"], epi=1, bias=W["h0.fc2.b"])
+    oracle.gemm(fc2, W["wte"], transB=True)
+    dt = time.perf_counter() - t0
+    flops = 2 * rows * (d * 3 * d + d * d + 2 * d * F + d * V)
+    return flops / dt / 1e12, dt, f"{rows} token rows through layer 0's linears + LM head (fp32 canonical order)"
 
 
 def run_reference(args, rank, world):
@@ -229,144 +263,186 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     import oracle
-    import synth
     oracle.lib()
-    inputs = [synth.gemm_inputs(n, "bench") for n in SIZES]
-    rows = {1024: 16, 2048: 4, 4096: 1, 8192: 1}
-
-    def ref_step():
-        f = 0
-        for (A, B), n in zip(inputs, SIZES):
-            r = rows[n]
-            C = oracle.gemm(A[:r], B)
-            oracle.data_root(C)
-            f += 2 * r * n * n
-        return f
-
+    if args.workload == "gemm":
+        fn = lambda: oracle_sample_gemm(2.0)  # noqa: E731
+        cfg = {"workload": "gemm-sweep 1024-8192 (oracle sample)"}
+    else:
+        fn = lambda: oracle_sample_gpt2(2)  # noqa: E731
+        cfg = {"workload": "gpt2-124m train step B=8 T=512 (oracle sample)"}
     for _ in range(args.warmup):
-        ref_step()
-    t0 = time.perf_counter()
-    flops = 0
+        fn()
+    vals, secs, sample = [], 0.0, ""
     for _ in range(args.steps):
-        flops += ref_step()
-    dt = time.perf_counter() - t0
-    value = flops / dt / 1e12
-    sample = f"rows {rows} of each n^3 GEMM (full K fold per element) + RFC 6962 data root of those rows"
+        v, s, sample = fn()
+        vals.append(v)
+        secs += s
+    value = statistics.median(vals)
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "config": {"workload": "gemm-sweep 1024-8192 (oracle sample)", "sizes": list(SIZES)},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": cfg,
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
 
-# ---------------------------------------------------------------------- main
+# ---------------------------------------------------------------------- timing
+def timed(wl, steps, world, local):
+    """W warm-up done by the caller; K steps bracketed by barrier + sync, CUDA events
+    on the launching stream, kernel families timed live (KernelTimer)."""
+    import torch
+
+    import paper_2502_19405_b200 as R
+    stream = torch.cuda.current_stream()
+    timer = R.KernelTimer()
+    l0 = R.launch_count()
+    with ClockSampler(local) as clk:
+        barrier(world)
+        torch.cuda.synchronize()
+        R.set_timer(timer)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(steps):
+            wl.step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        R.set_timer(None)
+        barrier(world)
+    launches = (R.launch_count() - l0) // steps
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / steps, world)
+    return ms, timer.totals(), launches, clk.summary()
+
+
+def e2e(wl, steps, world):
+    import torch
+    for _ in range(2):
+        wl.e2e_step()
+    barrier(world)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        wl.e2e_step()
+    torch.cuda.synchronize()
+    return max_over_ranks((time.perf_counter() - t0) / steps, world)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="repops", choices=["repops", "reference"])
-    ap.add_argument("--workload", default="gemm", choices=["gemm"])
+    ap.add_argument("--workload", default="gpt2", choices=["gpt2", "gemm"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-
-    rank, world, local = (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
-                          int(os.environ.get("LOCAL_RANK", "0")))
+    rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
 
     import torch
     rank, world, local = dist_init()
-    torch.cuda.set_device(local)
     device = torch.device("cuda", local)
-    import paper_2502_19405_b200 as R
-
-    wl = GemmSweep(rank, world, device)
-    for _ in range(args.warmup):
-        wl.step()
-    torch.cuda.synchronize()
-
-    # ---- timed region: K steps, device time via CUDA events, max over ranks
-    stream = torch.cuda.current_stream()
-    l0 = R.launch_count()
-    with ClockSampler(local) as clk:
-        barrier(world)
+    hbm = measured_hbm_gbs()
+    out = {"metric": METRIC}
+    results = {}
+    order = [args.workload] + ([] if args.no_sweep else [w for w in ("gemm",) if w != args.workload])
+    for wname in order:
+        wl = GPT2Train(rank, world, device) if wname == "gpt2" else GemmSweep(rank, world, device)
+        for _ in range(args.warmup):
+            wl.step()
         torch.cuda.synchronize()
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record(stream)
-        for _ in range(args.steps):
-            wl.step(time_gemm=True)
-        ev1.record(stream)
-        torch.cuda.synchronize()
-        barrier(world)
-    launches = (R.launch_count() - l0) // args.steps
-    ms = ev0.elapsed_time(ev1) / args.steps
-    ms = max_over_ranks(ms, world)
-    value = SWEEP_FLOPS / (ms * 1e-3) / 1e12
+        ms, tot, launches, clk = timed(wl, args.steps, world, local)
+        e2e_s = e2e(wl, args.steps, world)
+        gemm_ms, gemm_flops, gemm_n = tot.get("gemm", (0.0, 0, 0))
+        gemm_ms = max_over_ranks(gemm_ms, world)
+        peak = fp32_peak_tflops(clk["sm_max_mhz"] or 1965.0)
+        achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms else 0.0   # per GPU
+        res = dict(ms=ms, value=wl.flops / (ms * 1e-3) / 1e12, launches=launches, clk=clk, e2e_s=e2e_s,
+                   e2e_value=wl.flops / e2e_s / 1e12, gemm=(achieved, peak, gemm_ms / args.steps, gemm_n // args.steps),
+                   h2d=wl.h2d_bytes, d2h=wl.d2h_bytes)
+        if "commit" in tot:
+            c_ms, c_bytes, c_n = tot["commit"]
+            res["commit"] = dict(gbs=c_bytes / (c_ms * 1e-3) / 1e9, ms_per_step=c_ms / args.steps,
+                                 gb_per_step=c_bytes / args.steps / 1e9, plans_per_step=c_n // args.steps)
+        if wname == "gpt2":
+            res["root"] = wl.root.hex()
+            res["loss"] = wl.st.loss()
+        else:
+            res["digests"] = wl.digests()
+        results[wname] = res
+        del wl
+        torch.cuda.empty_cache()
 
-    gemm_ms, gemm_flops, nl = wl.kernel_times()
-    gemm_ms = max_over_ranks(gemm_ms, world)
-    achieved = gemm_flops * world / (gemm_ms * 1e-3) / 1e12  # all ranks' GEMM flops over the (max) GEMM time
-    achieved_per_gpu = achieved / world
-
-    # ---- e2e through the public API from pinned host buffers
-    for _ in range(2):
-        wl.e2e_step()
-    barrier(world)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        wl.e2e_step()
-    torch.cuda.synchronize()
-    e2e_s = max_over_ranks((time.perf_counter() - t0) / args.steps, world)
-    e2e_value = SWEEP_FLOPS / e2e_s / 1e12
-
-    digests = wl.digests()
-    c = clk.summary()
-    peak_max = fp32_peak_tflops(c["sm_max_mhz"] or 1965.0)
-    out = {
-        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "gemm-sweep: R-GEMM square n=1024,2048,4096,8192 + Verde commit of every output",
-                   "sizes": list(SIZES), "sharding": f"M-split over {world} GPU(s), full K per rank",
-                   "l2": "step working set 1.07 GB > 126 MB L2 (no explicit flush)",
-                   "inputs": "A,B ~ U[-1,1) on a 24-bit grid (synth.gemm_inputs, SplitMix64)"},
-        "roofline": {"bound": "alu", "kernel": "repops_gemm (FP32 FFMA, sequential K)",
-                     "achieved": achieved_per_gpu, "peak": peak_max, "unit": "TFLOP/s",
-                     "frac": achieved_per_gpu / peak_max,
-                     "peak_note": "148 SM x 128 FP32 lanes x 2 x sm_max_mhz (guide unit counts); "
-                                  "frac at the median observed clock: %.3f" % (
-                                      achieved_per_gpu / fp32_peak_tflops(c["sm_mhz"]) if c["sm_mhz"] else -1),
-                     "traffic": None, "launches_timed": nl},
-        "clocks": c,
-        "gpu_launches": launches,
-        "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": wl.h2d_bytes,
-                "d2h_bytes_per_step": wl.d2h_bytes,
-                "note": "pinned host A,B -> device, step, committed roots -> host (wall clock, max over ranks)"},
-        "digests": digests,
-    }
+    head = results[args.workload]
+    achieved, peak, gemm_ms_step, gemm_launches = head["gemm"]
+    clk = head["clk"]
+    out.update({
+        "value": head["value"], "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": head["ms"], "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+    })
+    if args.workload == "gpt2":
+        out["config"] = {"workload": "gpt2-124m train step B=8 T=512 (S=8 DP shards) + Verde commit of every "
+                                     "operator output + node digests + step Merkle root",
+                         "global_batch": 8, "seq_len": 512, "parallelism": f"dp{world} (canonical R-TREE_S)",
+                         "l2": "per-step working set ~17 GB >> 126 MB L2 (no explicit flush)",
+                         "inputs": "synthetic tokens + U(std 0.02) weights (synth.gpt2_*)",
+                         "flops_per_step": GPT2_FLOPS_NOTE}
+        out["gpt2_step_ms"] = head["ms"]
+        out["loss"] = head["loss"]
+        out["step_root"] = head["root"]
+    else:
+        out["config"] = {"workload": "gemm-sweep: R-GEMM square n=1024..8192 + Verde commit of every output",
+                         "sizes": list(SIZES), "sharding": f"M-split over {world} GPU(s), full K per rank",
+                         "l2": "step working set 1.07 GB > 126 MB L2 (no explicit flush)"}
+        out["digests"] = head["digests"]
+    out["roofline"] = {"bound": "alu", "kernel": "repops_gemm (FP32 FFMA2 on CUDA cores, sequential K)",
+                       "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else 0,
+                       "peak_note": "148 SM x 128 FP32 lanes x 2 x sm_max_mhz (unit counts of the guides); frac at "
+                                    "the median observed clock: %.3f" % (
+                                        achieved / fp32_peak_tflops(clk["sm_mhz"]) if clk["sm_mhz"] else -1),
+                       "gemm_ms_per_step": gemm_ms_step, "gemm_launches_per_step": gemm_launches,
+                       "traffic": None}
+    if "commit" in head:
+        cm = head["commit"]
+        cm["hbm_frac"] = cm["gbs"] / hbm
+        cm["hbm_peak_gbs"] = hbm
+        out["commit"] = cm
+    out["clocks"] = clk
+    out["gpu_launches"] = head["launches"]
+    out["e2e"] = {"value": head["e2e_value"], "unit": "TFLOP/s", "h2d_bytes_per_step": head["h2d"],
+                  "d2h_bytes_per_step": head["d2h"],
+                  "note": "wall clock per step through the public API: H2D of the batch from pinned host memory, "
+                          "the step, D2H of the committed result (max over ranks)"}
+    for other, res in results.items():
+        if other != args.workload:
+            out[other + "_sweep" if other == "gemm" else other] = {
+                "value": res["value"], "unit": "TFLOP/s", "ms_per_step": res["ms"],
+                "gemm_roofline_frac": res["gemm"][0] / res["gemm"][1], "digests": res.get("digests"),
+                "commit": res.get("commit")}
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         try:
-            out["roofline"]["traffic"] = json.load(open(tp)).get("repops_gemm_8192")
+            out["roofline"]["traffic"] = json.load(open(tp)).get(args.workload)
         except Exception:
             pass
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, secs, rows = cpu_sample_gemm()
+        v, secs, sample = oracle_sample_gpt2() if args.workload == "gpt2" else oracle_sample_gemm()
         out["cpu_baseline"] = {"value": v, "unit": "TFLOP/s", "cores": 1, "kind": "oracle",
-                               "sample": f"first rows {rows} of each sweep GEMM, {secs:.1f} s on 1 host core"}
+                               "sample": f"{sample}; {secs:.1f} s on 1 host core"}
     if rank == 0:
         print(json.dumps(out))
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
 
+
+GPT2_FLOPS_NOTE = "3 x (2 M N K over every fwd matmul: 12 x [QKV, proj, FC, FC2] + full (unmasked) QK^T, PV + LM head)"
 
 if __name__ == "__main__":
     main()

@@ -27,7 +27,7 @@ __all__ = [
     "verde_commit_tensors", "verde_merkle_root", "verde_sha256", "verde_node_digest",
     "verde_first_divergence", "verde_digest_from_subroots", "launch_count", "CommitWorkspace", "CommitPlan",
     "RepopsError",
-    "header_symbols", "lib",
+    "header_symbols", "lib", "KernelTimer", "set_timer",
 ]
 
 
@@ -56,6 +56,39 @@ def _ld(t) -> int:
     return t.stride(0)
 
 
+# ------------------------------------------------------------------ live kernel timing (bench.py)
+class KernelTimer:
+    """Optional CUDA-event bracketing of library launches on their stream, so a
+    benchmark can report a kernel family's device time inside its timed region.
+    Enabled with set_timer(KernelTimer()); costs two event records per launch."""
+
+    def __init__(self):
+        self.ev = {}  # kind -> list of (start, end, work)
+
+    def begin(self, stream=None):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream if stream is not None else torch.cuda.current_stream())
+        return e
+
+    def end(self, kind, e0, work, stream=None):
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record(stream if stream is not None else torch.cuda.current_stream())
+        self.ev.setdefault(kind, []).append((e0, e1, work))
+
+    def totals(self):
+        """kind -> (device ms, work units, launches); call after synchronising."""
+        return {k: (sum(a.elapsed_time(b) for a, b, _ in v), sum(w for _, _, w in v), len(v))
+                for k, v in self.ev.items()}
+
+
+_TIMER = None
+
+
+def set_timer(t):
+    global _TIMER
+    _TIMER = t
+
+
 # ------------------------------------------------------------------ GEMM
 def repops_gemm(A, B, transA=False, transB=False, epi=EPI_NONE, bias=None, scale=1.0, out=None, stream=None,
                 cfg=None):
@@ -71,10 +104,13 @@ def repops_gemm(A, B, transA=False, transB=False, epi=EPI_NONE, bias=None, scale
         out = torch.empty((M, N), dtype=torch.float32, device=A.device)
     args = (M, N, K, _p(A), _ld(A), int(bool(transA)), _p(B), _ld(B), int(bool(transB)), int(epi), _p(bias),
             float(scale), _p(out), _ld(out), _stream(stream))
+    t0 = _TIMER.begin(stream) if _TIMER else None
     if cfg is None:
         check(lib().repops_gemm(*args), "repops_gemm")
     else:
         check(lib().repops_gemm_cfg(*args, int(cfg)), "repops_gemm_cfg")
+    if t0 is not None:
+        _TIMER.end("gemm", t0, 2 * M * N * K, stream)
     return out
 
 
@@ -84,10 +120,13 @@ def repops_gemm_strided_batched(A, B, C_out, M, N, K, lda, ldb, ldc, sA, sB, sC,
     """Two-level strided batch of R-GEMMs.  sA/sB/sC = (outer, inner) element strides,
     batch = (outer, inner) counts; off* are element offsets into the storage of A/B/C."""
     _f32(A, "A"), _f32(B, "B"), _f32(C_out, "C")
+    t0 = _TIMER.begin(stream) if _TIMER else None
     check(lib().repops_gemm_strided_batched(
         M, N, K, _p(A) + 4 * offA, lda, int(bool(transA)), sA[0], sA[1], _p(B) + 4 * offB, ldb,
         int(bool(transB)), sB[0], sB[1], int(epi), _p(bias), float(scale), _p(C_out) + 4 * offC, ldc, sC[0],
         sC[1], batch[0], batch[1], _stream(stream)), "repops_gemm_strided_batched")
+    if t0 is not None:
+        _TIMER.end("gemm", t0, 2 * M * N * K * batch[0] * batch[1], stream)
     return C_out
 
 
@@ -345,7 +384,10 @@ class CommitPlan:
         self.h = h
 
     def run(self, stream=None):
+        t0 = _TIMER.begin(stream) if _TIMER else None
         check(lib().verde_commit_plan_run(self.h, _stream(stream)), "verde_commit_plan_run")
+        if t0 is not None:
+            _TIMER.end("commit", t0, self.nbytes, stream)
 
     def __del__(self):
         try:
