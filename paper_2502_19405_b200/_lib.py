@@ -99,6 +99,7 @@ def lib() -> C.CDLL:
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
+        _hooks(L)
         if L.repops_abi_version() != 1:
             raise RepopsError("librepops.so ABI version mismatch")
         _lib = L
@@ -109,3 +110,9 @@ def check(status: int, what: str) -> None:
     if status != 0:
         msg = lib().repops_last_error().decode(errors="replace")
         raise RepopsError(f"{what} failed (status {status}): {msg}")
+
+
+# tuning / test hooks exported by the library but not part of include/repops.h
+def _hooks(L):
+    L.repops_gemm_force_cfg.restype = i32
+    L.repops_gemm_force_cfg.argtypes = [i32]

@@ -34,6 +34,7 @@ int fail(int code, const char *fmt, ...) {
 }
 
 std::atomic<int64_t> g_launches{0};
+std::atomic<int> g_force_cfg{-1};  // tuning override of the GEMM tile choice (bits-neutral)
 
 // every launcher behind cuda_status() enqueues exactly one kernel on success
 // (verde_commit_tensors adds its extra kernels itself)
@@ -201,6 +202,7 @@ static int gemm_common(int64_t M, int64_t N, int64_t K, const float *A, int64_t 
     p.vecA = a16(A) && lda % 4 == 0 && sA0 % 4 == 0 && sA1 % 4 == 0;
     p.vecB = a16(B) && ldb % 4 == 0 && sB0 % 4 == 0 && sB1 % 4 == 0;
     p.vecC = a16(C) && ldc % 4 == 0 && sC0 % 4 == 0 && sC1 % 4 == 0;
+    if (force_cfg < 0) force_cfg = g_force_cfg.load(std::memory_order_relaxed);
     return cuda_status(gemm_launch(p, S(stream), force_cfg), "gemm launch");
 }
 
@@ -216,6 +218,14 @@ int repops_gemm_strided_batched(int64_t M, int64_t N, int64_t K, const float *A,
                                 int64_t batch0, int64_t batch1, void *stream) {
     return gemm_common(M, N, K, A, lda, transA, sA0, sA1, B, ldb, transB, sB0, sB1, epi, bias, scale, C, ldc, sC0,
                        sC1, batch0, batch1, stream, -1);
+}
+
+// Tuning hook (not in repops.h): process-wide override of the automatic tile
+// choice (-1 = automatic).  Bits never depend on it.
+int repops_gemm_force_cfg(int cfg) {
+    REQ(cfg >= -1 && cfg < gemm_num_cfgs(), "gemm_force_cfg: unknown configuration %d", cfg);
+    g_force_cfg.store(cfg);
+    return REPOPS_OK;
 }
 
 // Test hook (not in repops.h): force a tile configuration to prove bits-neutrality.

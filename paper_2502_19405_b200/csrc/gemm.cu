@@ -335,7 +335,7 @@ cudaError_t launch_cfg(const GemmParams &p, cudaStream_t s) {
 //   0: 128 x 128, 8 x 8 per thread, 3 stages, 2 CTAs/SM   (large problems)
 //   1:  64 x  64, 8 x 4 per thread, 3 stages              (small M*N)
 //   2..4: tuning variants (tools/gemm_tune.py)
-int gemm_num_cfgs() { return 5; }
+int gemm_num_cfgs() { return 7; }
 
 cudaError_t gemm_launch(const GemmParams &p, cudaStream_t s, int force_cfg) {
     if (p.M == 0 || p.N == 0 || p.batch0 * p.batch1 == 0) return cudaSuccess;
@@ -357,6 +357,8 @@ cudaError_t gemm_launch(const GemmParams &p, cudaStream_t s, int force_cfg) {
         case 2: return launch_cfg<128, 128, 16, 8, 8, 4, 1>(p, s);
         case 3: return launch_cfg<128, 256, 16, 8, 16, 3, 1>(p, s);
         case 4: return launch_cfg<256, 128, 16, 16, 8, 3, 1>(p, s);
+        case 5: return launch_cfg<128, 64, 16, 8, 8, 3, 3>(p, s);
+        case 6: return launch_cfg<64, 128, 16, 8, 8, 3, 3>(p, s);
         default: return cudaErrorInvalidValue;
     }
 }

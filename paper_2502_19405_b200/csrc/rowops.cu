@@ -113,23 +113,44 @@ __global__ void sum_rows_cta(const float *__restrict__ x, int64_t rows, int64_t 
 }
 
 // ------------------------------------------------------------------ R-SEQ column folds
-__global__ void sum_cols_seq_kernel(const float *__restrict__ x, int64_t rows, int64_t cols, int64_t ld,
-                                    int64_t nseg, float *__restrict__ out, int64_t ldo) {
-    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    int64_t s = blockIdx.y;
-    if (j >= cols) return;
-    int64_t per = rows / nseg;
-    const float *p = x + s * per * ld + j;
+// A column fold is one sequential chain per (segment, column) -- the canonical
+// order leaves no parallelism inside it -- so the kernel hides the load latency
+// instead: a CTA owns FC = 32 columns of one segment; all 8 warps stream
+// FR-row chunks of the [rows x 32] panel into shared memory with coalesced
+// 128-byte row reads (double buffered), and warp 0's 32 lanes run the 32 folds
+// out of shared memory (lane = column: conflict-free).
+constexpr int FC = 32, FR = 64;
+
+__global__ void __launch_bounds__(256) sum_cols_seq_kernel(const float *__restrict__ x, int64_t rows, int64_t cols,
+                                                           int64_t ld, int64_t nseg, float *__restrict__ out,
+                                                           int64_t ldo) {
+    __shared__ float tile[2][FR][FC];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t j0 = (int64_t)blockIdx.x * FC;
+    const int64_t s = blockIdx.y;
+    const int64_t per = rows / nseg;
+    const float *base = x + s * per * ld;
+    const int64_t jl = j0 + lane;
+    const int64_t nch = (per + FR - 1) / FR;
+    auto load = [&](int buf, int64_t c) {
+        for (int r = w; r < FR; r += 8) {
+            const int64_t t = c * FR + r;
+            tile[buf][r][lane] = (t < per && jl < cols) ? __ldg(base + t * ld + jl) : 0.f;
+        }
+    };
     float acc = 0.f;
-    int64_t t = 0;
-    for (; t + 4 <= per; t += 4) {  // loads batched, adds stay in ascending order
-        float v0 = __ldg(p + (t + 0) * ld), v1 = __ldg(p + (t + 1) * ld);
-        float v2 = __ldg(p + (t + 2) * ld), v3 = __ldg(p + (t + 3) * ld);
-        acc = __fadd_rn(acc, v0); acc = __fadd_rn(acc, v1);
-        acc = __fadd_rn(acc, v2); acc = __fadd_rn(acc, v3);
+    if (nch > 0) load(0, 0);
+    __syncthreads();
+    for (int64_t c = 0; c < nch; ++c) {
+        if (c + 1 < nch) load((int)((c + 1) & 1), c + 1);
+        if (w == 0) {
+            const int n = (int)min((int64_t)FR, per - c * FR);
+            const float(*tb)[FC] = tile[c & 1];
+            for (int r = 0; r < n; ++r) acc = __fadd_rn(acc, tb[r][lane]);  // ascending rows
+        }
+        __syncthreads();
     }
-    for (; t < per; ++t) acc = __fadd_rn(acc, __ldg(p + t * ld));
-    out[s * ldo + j] = canon(acc);
+    if (w == 0 && jl < cols) out[s * ldo + jl] = canon(acc);
 }
 
 // ------------------------------------------------------------------ softmax
@@ -363,19 +384,44 @@ __global__ void layernorm_params_kernel(const float *__restrict__ dy, const floa
                                         const float *__restrict__ mean, const float *__restrict__ rstd,
                                         int64_t rows, int64_t cols, int64_t nseg, float *__restrict__ dgamma,
                                         float *__restrict__ dbeta, int64_t ldo) {
-    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    int64_t s = blockIdx.y;
-    if (j >= cols) return;
-    int64_t per = rows / nseg;
+    // same panel-streaming structure as sum_cols_seq_kernel; the folded value
+    // xh = (x - mean[t]) * rstd[t] is recomputed exactly as in the forward
+    __shared__ float tdy[2][FR][FC], txh[2][FR][FC];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t j0 = (int64_t)blockIdx.x * FC;
+    const int64_t s = blockIdx.y;
+    const int64_t per = rows / nseg;
+    const int64_t jl = j0 + lane;
+    const int64_t nch = (per + FR - 1) / FR;
+    auto load = [&](int buf, int64_t c) {
+        for (int r = w; r < FR; r += 8) {
+            const int64_t t = s * per + c * FR + r;
+            const bool ok = (c * FR + r < per) && jl < cols;
+            tdy[buf][r][lane] = ok ? __ldg(dy + t * cols + jl) : 0.f;
+            txh[buf][r][lane] =
+                ok ? __fmul_rn(__fsub_rn(__ldg(x + t * cols + jl), __ldg(mean + t)), __ldg(rstd + t)) : 0.f;
+        }
+    };
     float ag = 0.f, ab = 0.f;
-    for (int64_t t = s * per; t < (s + 1) * per; ++t) {
-        float d = __ldg(dy + t * cols + j);
-        float xh = __fmul_rn(__fsub_rn(__ldg(x + t * cols + j), __ldg(mean + t)), __ldg(rstd + t));
-        ag = __fmaf_rn(d, xh, ag);
-        ab = __fadd_rn(ab, d);
+    if (nch > 0) load(0, 0);
+    __syncthreads();
+    for (int64_t c = 0; c < nch; ++c) {
+        if (c + 1 < nch) load((int)((c + 1) & 1), c + 1);
+        if (w == 0) {
+            const int n = (int)min((int64_t)FR, per - c * FR);
+            const int b = (int)(c & 1);
+            for (int r = 0; r < n; ++r) {  // ascending rows of the segment
+                const float d = tdy[b][r][lane];
+                ag = __fmaf_rn(d, txh[b][r][lane], ag);
+                ab = __fadd_rn(ab, d);
+            }
+        }
+        __syncthreads();
     }
-    dgamma[s * ldo + j] = canon(ag);
-    dbeta[s * ldo + j] = canon(ab);
+    if (w == 0 && jl < cols) {
+        dgamma[s * ldo + jl] = canon(ag);
+        dbeta[s * ldo + jl] = canon(ab);
+    }
 }
 
 // ------------------------------------------------------------------ cross entropy (CTA per row)
@@ -441,8 +487,8 @@ cudaError_t launch_sum_rows(const float *x, int64_t rows, int64_t cols, int64_t 
 cudaError_t launch_sum_cols_seq(const float *x, int64_t rows, int64_t cols, int64_t ld, int64_t nseg, float *out,
                                 int64_t ldo, cudaStream_t s) {
     if (cols == 0 || nseg == 0) return cudaSuccess;
-    dim3 grid((unsigned)((cols + 127) / 128), (unsigned)nseg);
-    sum_cols_seq_kernel<<<grid, 128, 0, s>>>(x, rows, cols, ld, nseg, out, ldo);
+    dim3 grid((unsigned)((cols + FC - 1) / FC), (unsigned)nseg);
+    sum_cols_seq_kernel<<<grid, 256, 0, s>>>(x, rows, cols, ld, nseg, out, ldo);
     return cudaGetLastError();
 }
 
@@ -490,8 +536,8 @@ cudaError_t launch_layernorm_params(const float *dy, const float *x, const float
                                     int64_t rows, int64_t cols, int64_t nseg, float *dg, float *db, int64_t ldo,
                                     cudaStream_t s) {
     if (cols == 0 || nseg == 0) return cudaSuccess;
-    dim3 grid((unsigned)((cols + 127) / 128), (unsigned)nseg);
-    layernorm_params_kernel<<<grid, 128, 0, s>>>(dy, x, mean, rstd, rows, cols, nseg, dg, db, ldo);
+    dim3 grid((unsigned)((cols + FC - 1) / FC), (unsigned)nseg);
+    layernorm_params_kernel<<<grid, 256, 0, s>>>(dy, x, mean, rstd, rows, cols, nseg, dg, db, ldo);
     return cudaGetLastError();
 }
 

@@ -616,15 +616,27 @@ class GPT2Step:
         self.tok_host = pin(torch.empty((self.S_loc, c.seq + 1), dtype=torch.int32))
         self.tin_host = pin(torch.empty((self.S_loc, c.seq), dtype=torch.int32))
         self.tgt_host = pin(torch.empty((self.S_loc, c.seq), dtype=torch.int32))
-        # one commit plan per phase (tensors produced in that phase, local or replicated)
+        # Commit plans.  A tensor must be hashed before anything modifies it in
+        # place; the only in-place writers are the embedding backward (the tied
+        # lm-head gradient) and AdamW (parameters / moments).  So the step needs
+        # three batched commits: the inputs | every shard's forward + backward
+        # outputs | embedding-backward, tree and AdamW outputs.  Few, large
+        # batches keep the SHA-256 leaf kernel's grid full.
+        group = lambda name: 0 if name == "inputs" else (1 if name.startswith("s") else 2)  # noqa: E731
+        gtids, glast = {}, {}
+        for i, (name, fns, tids) in enumerate(self.phases):
+            g = group(name)
+            gtids.setdefault(g, []).extend(tids)
+            glast[g] = i
+        self.plan_after = {}
         self.plans = []
-        for name, fns, tids in self.phases:
-            views = [self.tensors[t].view for t in tids]
-            if views and not self.structure_only:
-                self.plans.append(CommitPlan(views, [self.digests[self.tensors[t].slot] for t in tids]))
-            else:
-                self.plans.append(None)
-        self.commit_bytes = sum(p.nbytes for p in self.plans if p is not None)
+        for g, tids in sorted(gtids.items()):
+            if tids and not self.structure_only:
+                plan = CommitPlan([self.tensors[t].view for t in tids],
+                                  [self.digests[self.tensors[t].slot] for t in tids])
+                self.plans.append(plan)
+                self.plan_after[glast[g]] = plan
+        self.commit_bytes = sum(p.nbytes for p in self.plans)
         self._build_node_blob()
 
     def _build_node_blob(self):
@@ -676,11 +688,12 @@ class GPT2Step:
     def run(self, commit=True, inject=None):
         """Enqueue one full training step.  inject = (phase_name, fn) runs fn after that
         phase's kernels (fault injection for the dispute demo)."""
-        for (name, fns, _), plan in zip(self.phases, self.plans):
+        for i, (name, fns, _) in enumerate(self.phases):
             for fn in fns:
                 fn()
             if inject is not None and inject[0] == name:
                 inject[1]()
+            plan = self.plan_after.get(i)
             if commit and plan is not None:
                 plan.run()
         self.step_no += 1
