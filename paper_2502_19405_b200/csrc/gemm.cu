@@ -342,14 +342,23 @@ cudaError_t gemm_launch(const GemmParams &p, cudaStream_t s, int force_cfg) {
     if (p.batch0 * p.batch1 > 65535) return cudaErrorInvalidValue;
     int cfg = force_cfg;
     if (cfg < 0) {
-        // measured on B200 (tools/gemm_tune.py): 128x256 / 256x128 tiles when there
-        // are >= 4 waves of them, 128x128 when >= 2 waves, else 64x64
+        // Wave-quantisation cost model (bits-neutral choice): time ~ waves x tile
+        // area / sustained rate, rates measured on B200 with tools/gemm_tune.py and
+        // tools/gpt2_gemm_tune.py (TFLOP/s on large, full-wave problems).
+        struct C { int id, bm, bn, occ; double rate; };
+        static const C cand[] = {{3, 128, 256, 1, 53.0}, {4, 256, 128, 1, 50.0}, {0, 128, 128, 2, 50.0},
+                                 {6, 64, 128, 3, 49.0}, {5, 128, 64, 3, 47.5}, {1, 64, 64, 2, 44.0}};
         const int64_t nb = p.batch0 * p.batch1;
-        const int64_t tiles_big = ((p.M + 127) / 128) * ((p.N + 255) / 256) * nb;
-        const int64_t tiles128 = ((p.M + 127) / 128) * ((p.N + 127) / 128) * nb;
-        if (tiles_big >= 4 * 148) cfg = (!p.transA && p.transB) ? 4 : 3;
-        else if (tiles128 >= 2 * 148) cfg = 0;
-        else cfg = 1;
+        const int sms = ro_host::num_sms();
+        double best = 1e300;
+        for (const C &c : cand) {
+            if (c.id == 4 && !(!p.transA && p.transB)) continue;  // 256x128 only wins for NT
+            const int64_t tiles = ((p.M + c.bm - 1) / c.bm) * ((p.N + c.bn - 1) / c.bn) * nb;
+            const int64_t slots = (int64_t)sms * c.occ;
+            const int64_t waves = (tiles + slots - 1) / slots;
+            const double t = (double)waves * c.bm * c.bn * c.occ / c.rate;
+            if (t < best * 0.97) { best = t; cfg = c.id; }
+        }
     }
     switch (cfg) {
         case 0: return launch_cfg<128, 128, 16, 8, 8, 3, 2>(p, s);

@@ -108,6 +108,7 @@ class NodeRec:
     inputs: list            # TensorRef indices
     outputs: list
     name: str = ""
+    label: str | None = None  # launch label of the op that produces the outputs
     dsts: list = field(default_factory=list)
 
 
@@ -126,6 +127,7 @@ class GPT2Step:
         self.structure_only = structure_only
         self.dev = torch.device("meta" if structure_only else device)
         self.s0, self.S_loc = shard_block(rank, world, cfg.shards)
+        self._fault = None
         self.step_no = 0
         c = cfg
         self.M = self.S_loc * c.seq
@@ -235,9 +237,16 @@ class GPT2Step:
     def launch(self, fn):
         self._cur[1].append(fn)
 
-    def node(self, op, shard, attrs, inputs, outputs, name="", defer=False):
+    def _hook(self, label):
+        """Fault-injection point after the launch of op `label` (config 5 dispute demo)."""
+        if self._fault is not None and self._fault[0] == label:
+            self._fault[1]()
+
+    def node(self, op, shard, attrs, inputs, outputs, name="", defer=False, label=None):
         idx = len(self.nodes)
-        self.nodes.append(NodeRec(idx, op, shard, attrs, inputs, outputs, name))
+        if label is None and shard != REPLICATED:
+            label = name.split("/", 1)[1]  # "s3/h1/qkv" -> "h1/qkv" (the batched launch's hook label)
+        self.nodes.append(NodeRec(idx, op, shard, attrs, inputs, outputs, name, label=label))
         for q, t in enumerate(outputs):
             self.tensors[t].producer = idx
             self.tensors[t].pslot = q
@@ -292,24 +301,36 @@ class GPT2Step:
                 def fwd(l=l, a=a, W=W):
                     repops_layernorm(self.x[l], W("ln1.g"), W("ln1.b"), c.ln_eps, out=a["ln1"], mean=a["mu1"],
                                      rstd=a["rs1"])
+                    self._hook(f"h{l}/ln1")
                     repops_gemm(a["ln1"], W("attn.w"), epi=EPI_BIAS, bias=W("attn.b"), out=a["qkv"])
+                    self._hook(f"h{l}/qkv")
                     # scores S = (Q K^T) * 1/sqrt(hd), batched over (local shard, head)
                     repops_gemm_strided_batched(a["qkv"], a["qkv"], a["S"], M=T, N=T, K=hd, lda=3 * d, ldb=3 * d,
                                                 ldc=T, sA=(T * 3 * d, hd), sB=(T * 3 * d, hd),
                                                 sC=(H * T * T, T * T), batch=(S_loc, H), transB=True,
                                                 epi=EPI_SCALE, scale=1.0 / np.sqrt(hd), offB=d)
+                    self._hook(f"h{l}/scores")
                     repops_softmax(a["S"], causal=True, out=a["P"])
+                    self._hook(f"h{l}/softmax")
                     repops_gemm_strided_batched(a["P"], a["qkv"], a["att"], M=T, N=hd, K=T, lda=T, ldb=3 * d,
                                                 ldc=d, sA=(H * T * T, T * T), sB=(T * 3 * d, hd), sC=(T * d, hd),
                                                 batch=(S_loc, H), offB=2 * d)
+                    self._hook(f"h{l}/pv")
                     repops_gemm(a["att"], W("proj.w"), epi=EPI_BIAS, bias=W("proj.b"), out=a["proj"])
+                    self._hook(f"h{l}/proj")
                     repops_add(self.x[l], a["proj"], out=a["xmid"])
+                    self._hook(f"h{l}/res1")
                     repops_layernorm(a["xmid"], W("ln2.g"), W("ln2.b"), c.ln_eps, out=a["ln2"], mean=a["mu2"],
                                      rstd=a["rs2"])
+                    self._hook(f"h{l}/ln2")
                     repops_gemm(a["ln2"], W("fc.w"), epi=EPI_BIAS, bias=W("fc.b"), out=a["fc"])
+                    self._hook(f"h{l}/fc")
                     repops_gelu(a["fc"], out=a["gelu"])
+                    self._hook(f"h{l}/gelu")
                     repops_gemm(a["gelu"], W("fc2.w"), epi=EPI_BIAS, bias=W("fc2.b"), out=a["fc2"])
+                    self._hook(f"h{l}/fc2")
                     repops_add(a["xmid"], a["fc2"], out=self.x[l + 1])
+                    self._hook(f"h{l}/res2")
                 self.launch(fwd)
             pre = f"s{s}/h{l}/"
             t_ln1 = T_(pre + "ln1", V(a["ln1"], T), s)
@@ -357,10 +378,13 @@ class GPT2Step:
             def head():
                 repops_layernorm(self.x[L], self.pview(self.params, "lnf.g"), self.pview(self.params, "lnf.b"),
                                  c.ln_eps, out=self.lnf, mean=self.muf, rstd=self.rsf)
+                self._hook("head/lnf")
                 wte = self.pview(self.params, "wte")
                 repops_gemm(self.lnf, wte, transB=True, out=self.logits[:, :c.vocab])
+                self._hook("head/lm_head")
                 repops_cross_entropy(self.logits, self.targets_flat, scale=1.0 / (c.shards * c.seq),
                                      loss=self.loss_tok, dlogits=self.dlogits, V=c.vocab)
+                self._hook("head/ce")
             self.launch(head)
         pre = f"s{s}/head/"
         t_lnf = T_(pre + "lnf", V(self.lnf, T), s)
@@ -382,15 +406,19 @@ class GPT2Step:
             def head_bwd():
                 wte = self.pview(self.params, "wte")
                 repops_gemm(self.dlogits[:, :c.vocab], wte, out=self.dlnf)
+                self._hook("head/lm_dgrad")
                 o = self.off["wte"][0]
                 repops_gemm_strided_batched(self.dlogits, self.lnf, gl, M=c.vocab, N=d, K=T, lda=c.vocab_ld, ldb=d,
                                             ldc=d, sA=(T * c.vocab_ld, 0), sB=(T * d, 0), sC=(self.P, 0),
                                             batch=(S_loc, 1), transA=True, offC=o)
+                self._hook("head/lm_wgrad")
                 repops_layernorm_backward(self.dlnf, self.x[L], self.pview(self.params, "lnf.g"), self.muf, self.rsf,
                                           out=self.dx[L])
+                self._hook("head/lnf_bwd")
                 repops_layernorm_backward_params(self.dlnf, self.x[L], self.muf, self.rsf, nseg=S_loc,
                                                  dgamma=gl[:, self.off["lnf.g"][0]:],
                                                  dbeta=gl[:, self.off["lnf.b"][0]:], ldo=self.P)
+                self._hook("head/lnf_params")
             self.launch(head_bwd)
         t_dlnf = T_(pre + "dlnf", V(self.dlnf, T), s)
         self.node(OP["LM_DGRAD"], s, {}, [t_dlog, P_["wte"][0]], [t_dlnf], pre + "lm_dgrad")
@@ -418,33 +446,47 @@ class GPT2Step:
                     o = lambda n: self.off[p + n][0]  # noqa: E731
                     # FC2
                     repops_gemm(dout, W("fc2.w"), transB=True, out=g["dgelu"])
+                    self._hook(f"h{l}/fc2_dgrad")
                     repops_gemm_strided_batched(a["gelu"], dout, gl, M=c.ffn, N=d, K=T, lda=c.ffn, ldb=d, ldc=d,
                                                 sA=(T * c.ffn, 0), sB=(T * d, 0), sC=(self.P, 0), batch=(S_loc, 1),
                                                 transA=True, offC=o("fc2.w"))
+                    self._hook(f"h{l}/fc2_wgrad")
                     repops_sum_cols_seq(dout, nseg=S_loc, out=gl[:, o("fc2.b"):], ldo=self.P)
+                    self._hook(f"h{l}/fc2_bgrad")
                     repops_gelu_backward(a["fc"], g["dgelu"], out=g["dfc"])
+                    self._hook(f"h{l}/gelu_bwd")
                     # FC
                     repops_gemm(g["dfc"], W("fc.w"), transB=True, out=g["dln2"])
+                    self._hook(f"h{l}/fc_dgrad")
                     repops_gemm_strided_batched(a["ln2"], g["dfc"], gl, M=d, N=c.ffn, K=T, lda=d, ldb=c.ffn,
                                                 ldc=c.ffn, sA=(T * d, 0), sB=(T * c.ffn, 0), sC=(self.P, 0),
                                                 batch=(S_loc, 1), transA=True, offC=o("fc.w"))
+                    self._hook(f"h{l}/fc_wgrad")
                     repops_sum_cols_seq(g["dfc"], nseg=S_loc, out=gl[:, o("fc.b"):], ldo=self.P)
+                    self._hook(f"h{l}/fc_bgrad")
                     # LN2 (+ residual gradient)
                     repops_layernorm_backward(g["dln2"], a["xmid"], W("ln2.g"), a["mu2"], a["rs2"], dres=dout,
                                               out=g["dxmid"])
+                    self._hook(f"h{l}/ln2_bwd")
                     repops_layernorm_backward_params(g["dln2"], a["xmid"], a["mu2"], a["rs2"], nseg=S_loc,
                                                      dgamma=gl[:, o("ln2.g"):], dbeta=gl[:, o("ln2.b"):], ldo=self.P)
+                    self._hook(f"h{l}/ln2_params")
                     # proj
                     repops_gemm(g["dxmid"], W("proj.w"), transB=True, out=g["datt"])
+                    self._hook(f"h{l}/proj_dgrad")
                     repops_gemm_strided_batched(a["att"], g["dxmid"], gl, M=d, N=d, K=T, lda=d, ldb=d, ldc=d,
                                                 sA=(T * d, 0), sB=(T * d, 0), sC=(self.P, 0), batch=(S_loc, 1),
                                                 transA=True, offC=o("proj.w"))
+                    self._hook(f"h{l}/proj_wgrad")
                     repops_sum_cols_seq(g["dxmid"], nseg=S_loc, out=gl[:, o("proj.b"):], ldo=self.P)
+                    self._hook(f"h{l}/proj_bgrad")
                     # attention
                     repops_gemm_strided_batched(g["datt"], a["qkv"], g["dP"], M=T, N=T, K=hd, lda=d, ldb=3 * d,
                                                 ldc=T, sA=(T * d, hd), sB=(T * 3 * d, hd), sC=(H * T * T, T * T),
                                                 batch=(S_loc, H), transB=True, offB=2 * d)
+                    self._hook(f"h{l}/attn_dp")
                     repops_softmax_backward(a["P"], g["dP"], scale=1.0 / np.sqrt(hd), out=g["dS"])
+                    self._hook(f"h{l}/softmax_bwd")
                     # dV = P^T dO ; dQ = dS K ; dK = dS^T Q   (into the packed dqkv)
                     repops_gemm_strided_batched(a["P"], g["datt"], g["dqkv"], M=T, N=hd, K=T, lda=T, ldb=d,
                                                 ldc=3 * d, sA=(H * T * T, T * T), sB=(T * d, hd),
@@ -455,16 +497,22 @@ class GPT2Step:
                     repops_gemm_strided_batched(g["dS"], a["qkv"], g["dqkv"], M=T, N=hd, K=T, lda=T, ldb=3 * d,
                                                 ldc=3 * d, sA=(H * T * T, T * T), sB=(T * 3 * d, hd),
                                                 sC=(T * 3 * d, hd), batch=(S_loc, H), transA=True, offC=d)
+                    self._hook(f"h{l}/attn_dqkv")
                     # QKV
                     repops_gemm(g["dqkv"], W("attn.w"), transB=True, out=g["dln1"])
+                    self._hook(f"h{l}/qkv_dgrad")
                     repops_gemm_strided_batched(a["ln1"], g["dqkv"], gl, M=d, N=3 * d, K=T, lda=d, ldb=3 * d,
                                                 ldc=3 * d, sA=(T * d, 0), sB=(T * 3 * d, 0), sC=(self.P, 0),
                                                 batch=(S_loc, 1), transA=True, offC=o("attn.w"))
+                    self._hook(f"h{l}/qkv_wgrad")
                     repops_sum_cols_seq(g["dqkv"], nseg=S_loc, out=gl[:, o("attn.b"):], ldo=self.P)
+                    self._hook(f"h{l}/qkv_bgrad")
                     repops_layernorm_backward(g["dln1"], self.x[l], W("ln1.g"), a["mu1"], a["rs1"], dres=g["dxmid"],
                                               out=self.dx[l])
+                    self._hook(f"h{l}/ln1_bwd")
                     repops_layernorm_backward_params(g["dln1"], self.x[l], a["mu1"], a["rs1"], nseg=S_loc,
                                                      dgamma=gl[:, o("ln1.g"):], dbeta=gl[:, o("ln1.b"):], ldo=self.P)
+                    self._hook(f"h{l}/ln1_params")
                 self.launch(bwd)
             pre = f"s{s}/h{l}/"
             t_dout = t_dx
@@ -685,9 +733,20 @@ class GPT2Step:
     def h2d_bytes(self):
         return 3 * self.tok_host.numel() * 4
 
+    def inject_fault(self, node_index, out_slot=0, elem=0, bit=0):
+        """Arm a 1-bit flip of element `elem` of output `out_slot` of node `node_index`,
+        applied right after the launch that produces it (so it propagates downstream).
+        Used to build a dishonest trainer for the Verde dispute (config 5)."""
+        from . import repops_flip_bit
+        nd = self.nodes[node_index]
+        if nd.label is None or not self._is_local(nd.shard):
+            raise ValueError("fault injection needs a local per-shard node with a launch hook")
+        view = self.tensors[nd.outputs[out_slot]].view
+        self._fault = (nd.label, lambda: repops_flip_bit(view, elem, bit))
+
     def run(self, commit=True, inject=None):
         """Enqueue one full training step.  inject = (phase_name, fn) runs fn after that
-        phase's kernels (fault injection for the dispute demo)."""
+        phase's kernels (coarse fault injection; see inject_fault for per-op points)."""
         for i, (name, fns, _) in enumerate(self.phases):
             for fn in fns:
                 fn()
