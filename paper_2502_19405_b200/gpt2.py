@@ -212,6 +212,7 @@ class GPT2Step:
 
         self._T = T_
         self._deferred = []
+        self._label_phase, self._tensor_phase = {}, {}
         # ---- replicated input nodes: parameters with their optimizer state
         self.phase("inputs")
         self.param_in = {}
@@ -247,6 +248,17 @@ class GPT2Step:
         if label is None and shard != REPLICATED:
             label = name.split("/", 1)[1]  # "s3/h1/qkv" -> "h1/qkv" (the batched launch's hook label)
         self.nodes.append(NodeRec(idx, op, shard, attrs, inputs, outputs, name, label=label))
+        # phase in which the producing launch is enqueued: the first local shard's
+        # phase for batched per-shard launches, else the current phase
+        ph = len(self.phases) - 1
+        if shard != REPLICATED and self._is_local(shard):
+            if shard == self.s0:
+                self._label_phase[label] = ph
+            else:
+                ph = self._label_phase.get(label, ph)
+        self._tensor_phase.update({t: ph for t in outputs})
+        if defer:
+            self._tensor_phase.update({t: None for t in outputs})
         for q, t in enumerate(outputs):
             self.tensors[t].producer = idx
             self.tensors[t].pslot = q
@@ -664,27 +676,34 @@ class GPT2Step:
         self.tok_host = pin(torch.empty((self.S_loc, c.seq + 1), dtype=torch.int32))
         self.tin_host = pin(torch.empty((self.S_loc, c.seq), dtype=torch.int32))
         self.tgt_host = pin(torch.empty((self.S_loc, c.seq), dtype=torch.int32))
-        # Commit plans.  A tensor must be hashed before anything modifies it in
-        # place; the only in-place writers are the embedding backward (the tied
-        # lm-head gradient) and AdamW (parameters / moments).  So the step needs
-        # three batched commits: the inputs | every shard's forward + backward
-        # outputs | embedding-backward, tree and AdamW outputs.  Few, large
-        # batches keep the SHA-256 leaf kernel's grid full.
-        group = lambda name: 0 if name == "inputs" else (1 if name.startswith("s") else 2)  # noqa: E731
-        gtids, glast = {}, {}
-        for i, (name, fns, tids) in enumerate(self.phases):
-            g = group(name)
-            gtids.setdefault(g, []).extend(tids)
-            glast[g] = i
+        # Commit plans, one per phase whose launches produce local tensors (all
+        # local shards of a batched launch together).  They run on a side stream,
+        # each after an event recorded when its phase's kernels are enqueued, so
+        # SHA-256 (integer ALU pipe) overlaps the next phases' GEMMs (FMA pipe).
+        # A tensor must be hashed before anything modifies it in place; the only
+        # in-place writers are the embedding backward (the tied lm-head gradient)
+        # and AdamW (parameters / moments) -- run() makes those phases wait for
+        # the side stream.
+        deferred_phase = next(i for i, p in enumerate(self.phases) if p[0] == "embed_bwd")
+        per_phase = {}
+        for name, fns, tids in self.phases:
+            for t in tids:
+                ph = self._tensor_phase.get(t)
+                ph = deferred_phase if ph is None else ph
+                per_phase.setdefault(ph, []).append(t)
         self.plan_after = {}
         self.plans = []
-        for g, tids in sorted(gtids.items()):
+        for ph, tids in sorted(per_phase.items()):
             if tids and not self.structure_only:
                 plan = CommitPlan([self.tensors[t].view for t in tids],
                                   [self.digests[self.tensors[t].slot] for t in tids])
                 self.plans.append(plan)
-                self.plan_after[glast[g]] = plan
+                self.plan_after[ph] = plan
         self.commit_bytes = sum(p.nbytes for p in self.plans)
+        self._wait_side_before = {deferred_phase, next(i for i, p in enumerate(self.phases) if p[0] == "adamw")}
+        if not self.structure_only:
+            self.side = torch.cuda.Stream(device=self.dev)
+            self.overlap_commits = True
         self._build_node_blob()
 
     def _build_node_blob(self):
@@ -747,14 +766,26 @@ class GPT2Step:
     def run(self, commit=True, inject=None):
         """Enqueue one full training step.  inject = (phase_name, fn) runs fn after that
         phase's kernels (coarse fault injection; see inject_fault for per-op points)."""
+        main = torch.cuda.current_stream()
+        side = self.side if self.overlap_commits else main
+        if side is not main:
+            side.wait_stream(main)  # the step's inputs (tokens, checkpoint) are ready
         for i, (name, fns, _) in enumerate(self.phases):
+            if commit and side is not main and i in self._wait_side_before:
+                main.wait_stream(side)  # in-place writers wait until their inputs are hashed
             for fn in fns:
                 fn()
             if inject is not None and inject[0] == name:
                 inject[1]()
             plan = self.plan_after.get(i)
             if commit and plan is not None:
-                plan.run()
+                if side is main:
+                    plan.run()
+                else:
+                    side.wait_stream(main)
+                    plan.run(stream=side)
+        if side is not main:
+            main.wait_stream(side)
         self.step_no += 1
 
     def gather_digests(self):
