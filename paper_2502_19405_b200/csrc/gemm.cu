@@ -80,6 +80,21 @@ RO_DEV void tile_async(float *dst, const float *__restrict__ src, int64_t ld, in
     }
 }
 
+// Interior fast path of tile_async: every chunk in range, 16-byte aligned rows,
+// 32-bit offset arithmetic (ld < 2^23), no predicates.
+template <int R, int L, int SLD, int THREADS>
+RO_DEV void tile_async_full(float *dst, const float *__restrict__ src, int ld, int tid) {
+    constexpr int CPR = L / 4;
+    constexpr int TOTAL = R * CPR;
+#pragma unroll
+    for (int q = 0; q < TOTAL / THREADS; ++q) {
+        const int c = tid + q * THREADS;
+        const int r = c / CPR;
+        const int l = (c % CPR) * 4;
+        cp_async16(dst + r * SLD + l, src + (r * ld + l), 16);
+    }
+}
+
 // B^T stored N x K (k contiguous): each thread loads 4 consecutive k of rows
 // n = (tid % BN) (+ BN*... for more chunks) into registers ...
 template <int BN, int BK, int THREADS>
@@ -132,8 +147,9 @@ struct Cfg {
     static constexpr int NP = TN / 2;           // accumulator pairs per row
 };
 
-template <int BM, int BN, int BK, int TM, int TN, int STAGES, int MINB, bool TA, bool TB, bool VEC>
+template <int BM, int BN, int BK, int TM, int TN, int STAGES, int MINB, int KG0, bool TA, bool TB, int LD>
 __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB) gemm_kernel(GemmParams p) {
+    constexpr int KG = (LD == 2) ? 4 : KG0;  // full tiles have the registers for LDS.128 A fragments
     using CF = Cfg<BM, BN, BK, TM, TN, TA>;
     constexpr int THREADS = CF::THREADS;
     constexpr int TX = CF::TX, TY = CF::TY, SKP = CF::SKP, NP = CF::NP;
@@ -160,9 +176,17 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB) gemm_kernel(GemmP
     float *__restrict__ Cp = p.C + b0 * p.sC0 + b1 * p.sC1;
     const int64_t M = p.M, N = p.N, K = p.K;
 
+    // LD == 2: the launcher proved every tile full and aligned -> predicate-free loads
+    constexpr bool VEC = LD >= 1;
     auto load_a = [&](int slot, int64_t kt) {
         float *As = smem + slot * CF::STAGE_WORDS;
         const int64_t k0 = kt * BK;
+        if constexpr (LD == 2) {
+            if (TA) tile_async_full<BK, BM, BM, THREADS>(As, A + k0 * p.lda + m0, (int)p.lda, tid);
+            else tile_async_full<BM, BK, SKP, THREADS>(As, A + m0 * p.lda + k0, (int)p.lda, tid);
+            if (!TB) tile_async_full<BK, BN, BN, THREADS>(As + CF::A_WORDS, B + k0 * p.ldb + n0, (int)p.ldb, tid);
+            return;
+        }
         if (TA)  // A stored K x M: tile rows = k, contiguous m
             tile_async<BK, BM, BM, THREADS, VEC>(As, A + k0 * p.lda + m0, p.lda, K - k0, M - m0, tid);
         else     // A stored M x K: tile rows = m, contiguous k
@@ -195,32 +219,41 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB) gemm_kernel(GemmP
         cp_commit();
     }
 
+    int cur_slot = 0, nxt_slot = STAGES - 1;  // ring positions of tile kt and kt + STAGES - 1
     for (int64_t kt = 0; kt < ktiles; ++kt) {
         cp_wait<STAGES - 2>();
         __syncthreads();
         const int64_t nk = kt + STAGES - 1;
         const bool pref = nk < ktiles;
         if (pref) {
-            load_a((int)(nk % STAGES), nk);
+            load_a(nxt_slot, nk);
             if (TB) load_bt(nk);
         }
         cp_commit();
-        const float *As = smem + (int)(kt % STAGES) * CF::STAGE_WORDS;
+        const int slot_now = cur_slot, slot_pref = nxt_slot;
+        cur_slot = (cur_slot + 1 == STAGES) ? 0 : cur_slot + 1;
+        nxt_slot = (nxt_slot + 1 == STAGES) ? 0 : nxt_slot + 1;
+        const float *As = smem + slot_now * CF::STAGE_WORDS;
         const float *Bs = As + CF::A_WORDS;
         const int kmax = (int)min((int64_t)BK, K - kt * BK);
         if (kmax == BK) {
 #pragma unroll
-            for (int kg = 0; kg < BK; kg += 4) {
-                float ak[TA ? 1 : TM][4];
+            for (int kg = 0; kg < BK; kg += KG) {
+                float ak[TA ? 1 : TM][KG];
                 if (!TA) {
 #pragma unroll
                     for (int i = 0; i < TM; ++i) {
-                        float4 v = *reinterpret_cast<const float4 *>(As + (ty + TY * i) * SKP + kg);
-                        ak[i][0] = v.x; ak[i][1] = v.y; ak[i][2] = v.z; ak[i][3] = v.w;
+                        if constexpr (KG == 4) {
+                            float4 v = *reinterpret_cast<const float4 *>(As + (ty + TY * i) * SKP + kg);
+                            ak[i][0] = v.x; ak[i][1] = v.y; ak[i][2] = v.z; ak[i][3] = v.w;
+                        } else {
+                            float2 v = *reinterpret_cast<const float2 *>(As + (ty + TY * i) * SKP + kg);
+                            ak[i][0] = v.x; ak[i][1] = v.y;
+                        }
                     }
                 }
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk) {
+                for (int kk = 0; kk < KG; ++kk) {
                     float a[TM];
                     float2 b[NP];
                     if (TA) {
@@ -265,7 +298,7 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB) gemm_kernel(GemmP
                     for (int j = 0; j < NP; ++j) acc[i][j] = __ffma2_rn(make_float2(a[i], a[i]), b[j], acc[i][j]);
             }
         }
-        if (TB && pref) store_bt((int)(nk % STAGES));  // slot (kt-1) % STAGES: free since this iteration's barrier
+        if (TB && pref) store_bt(slot_pref);  // slot of tile kt-1: free since this iteration's barrier
     }
     cp_wait<0>();
 
@@ -297,11 +330,11 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB) gemm_kernel(GemmP
     }
 }
 
-template <int BM, int BN, int BK, int TM, int TN, int STAGES, int MINB, bool TA, bool TB, bool VEC>
+template <int BM, int BN, int BK, int TM, int TN, int STAGES, int MINB, int KG, bool TA, bool TB, int LD>
 cudaError_t launch_one(const GemmParams &p, cudaStream_t s) {
     using CF = Cfg<BM, BN, BK, TM, TN, TA>;
     const size_t smem = (size_t)STAGES * CF::STAGE_WORDS * sizeof(float);
-    auto kern = gemm_kernel<BM, BN, BK, TM, TN, STAGES, MINB, TA, TB, VEC>;
+    auto kern = gemm_kernel<BM, BN, BK, TM, TN, STAGES, MINB, KG, TA, TB, LD>;
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -314,13 +347,16 @@ cudaError_t launch_one(const GemmParams &p, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-template <int BM, int BN, int BK, int TM, int TN, int STAGES, int MINB>
+template <int BM, int BN, int BK, int TM, int TN, int STAGES, int MINB, int KG = 4>
 cudaError_t launch_cfg(const GemmParams &p, cudaStream_t s) {
     const bool vec = p.vecA && p.vecB;
+    const bool full = vec && p.M % BM == 0 && p.N % BN == 0 && p.K % BK == 0 && p.lda < (1 << 23) &&
+                      p.ldb < (1 << 23);
 #define RO_GEMM_CASE(TA_, TB_)                                                                   \
     if ((bool)p.transA == TA_ && (bool)p.transB == TB_)                                          \
-        return vec ? launch_one<BM, BN, BK, TM, TN, STAGES, MINB, TA_, TB_, true>(p, s)          \
-                   : launch_one<BM, BN, BK, TM, TN, STAGES, MINB, TA_, TB_, false>(p, s);
+        return full ? launch_one<BM, BN, BK, TM, TN, STAGES, MINB, KG, TA_, TB_, 2>(p, s)        \
+                    : vec ? launch_one<BM, BN, BK, TM, TN, STAGES, MINB, KG, TA_, TB_, 1>(p, s)  \
+                          : launch_one<BM, BN, BK, TM, TN, STAGES, MINB, KG, TA_, TB_, 0>(p, s);
     RO_GEMM_CASE(false, false)
     RO_GEMM_CASE(false, true)
     RO_GEMM_CASE(true, false)
@@ -361,11 +397,11 @@ cudaError_t gemm_launch(const GemmParams &p, cudaStream_t s, int force_cfg) {
         }
     }
     switch (cfg) {
-        case 0: return launch_cfg<128, 128, 16, 8, 8, 3, 2>(p, s);
+        case 0: return launch_cfg<128, 128, 16, 8, 8, 3, 2, 2>(p, s);
         case 1: return launch_cfg<64, 64, 16, 8, 4, 3, 2>(p, s);
         case 2: return launch_cfg<128, 128, 16, 8, 8, 4, 1>(p, s);
-        case 3: return launch_cfg<128, 256, 16, 8, 16, 3, 1>(p, s);
-        case 4: return launch_cfg<256, 128, 16, 16, 8, 3, 1>(p, s);
+        case 3: return launch_cfg<128, 256, 16, 8, 16, 3, 1, 2>(p, s);
+        case 4: return launch_cfg<256, 128, 16, 16, 8, 3, 1, 2>(p, s);
         case 5: return launch_cfg<128, 64, 16, 8, 8, 3, 3>(p, s);
         case 6: return launch_cfg<64, 128, 16, 8, 8, 3, 3>(p, s);
         default: return cudaErrorInvalidValue;
