@@ -169,6 +169,10 @@ int repops_embedding_backward(const int32_t *tok, int64_t ntok, int64_t T, const
 int repops_adamw(float *p, const float *g, float *m, float *v, int64_t n, int64_t step,
                  float lr, float b1, float b2, float eps, float wd, int decay, void *stream);
 
+/* Transpose (data movement only, bit-exact): y[j*ldy + i] = x[i*ldx + j] for a
+ * rows x cols x.  Used to give backward GEMMs an n-contiguous weight operand. */
+int repops_transpose(const float *x, int64_t rows, int64_t cols, int64_t ldx, float *y, int64_t ldy, void *stream);
+
 /* Fault injection (Verde config 5): flips bit `bit` (0..31) of 32-bit element
  * `elem` of the device buffer `data`. */
 int repops_flip_bit(void *data, int64_t elem, int bit, void *stream);

@@ -314,6 +314,16 @@ def repops_adamw(p, g, m, v, step, lr, b1, b2, eps, wd, decay, stream=None):
     return p, m, v
 
 
+def repops_transpose(x, out=None, stream=None):
+    """out = x^T (bit-exact data movement)."""
+    _f32(x, "x")
+    rows, cols = x.shape
+    if out is None:
+        out = torch.empty((cols, rows), dtype=torch.float32, device=x.device)
+    check(lib().repops_transpose(_p(x), rows, cols, _ld(x), _p(out), _ld(out), _stream(stream)), "repops_transpose")
+    return out
+
+
 def repops_flip_bit(t, elem, bit, stream=None):
     check(lib().repops_flip_bit(_p(t), int(elem), int(bit), _stream(stream)), "repops_flip_bit")
     return t

@@ -59,6 +59,7 @@ SIGNATURES = {
     "repops_embedding_backward": (i32, [vp, i64, i64, vp, i64, vp, vp, vp]),
     "repops_adamw": (i32, [vp, vp, vp, vp, i64, i64, f32, f32, f32, f32, f32, i32, vp]),
     "repops_flip_bit": (i32, [vp, i64, i32, vp]),
+    "repops_transpose": (i32, [vp, i64, i64, i64, vp, i64, vp]),
     "verde_commit_workspace_bytes": (i64, [vp, i32]),
     "verde_commit_tensors": (i32, [vp, i32, vp, i64, vp]),
     "verde_commit_tensor": (i32, [vp, i64, i32, i32, vp, vp, vp, i64, vp]),

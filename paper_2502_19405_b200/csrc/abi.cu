@@ -393,6 +393,13 @@ int repops_adamw(float *p, const float *g, float *m, float *v, int64_t n, int64_
                        "adamw");
 }
 
+int repops_transpose(const float *x, int64_t rows, int64_t cols, int64_t ldx, float *y, int64_t ldy, void *stream) {
+    REQ(rows >= 0 && cols >= 0, "transpose: negative extent");
+    if (rows == 0 || cols == 0) return REPOPS_OK;
+    REQ(x && y && ldx >= cols && ldy >= rows, "transpose: bad pointer or leading dimension");
+    return cuda_status(launch_transpose(x, rows, cols, ldx, y, ldy, S(stream)), "transpose");
+}
+
 int repops_flip_bit(void *data, int64_t elem, int bit, void *stream) {
     REQ(data && elem >= 0 && bit >= 0 && bit < 32, "flip_bit: bad argument");
     return cuda_status(launch_flip_bit(data, elem, bit, S(stream)), "flip_bit");

@@ -256,3 +256,29 @@ cudaError_t launch_flip_bit(void *data, int64_t elem, int bit, cudaStream_t s) {
     flip_bit_kernel<<<1, 1, 0, s>>>(reinterpret_cast<uint32_t *>(data), elem, bit);
     return cudaGetLastError();
 }
+
+// ------------------------------------------------------------------ transpose (data movement only)
+namespace {
+__global__ void transpose_kernel(const float *__restrict__ x, int64_t rows, int64_t cols, int64_t ldx,
+                                 float *__restrict__ y, int64_t ldy) {
+    __shared__ float t[32][33];
+    const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
+    for (int i = threadIdx.y; i < 32; i += 8) {
+        const int64_t r = r0 + i, c = c0 + threadIdx.x;
+        if (r < rows && c < cols) t[i][threadIdx.x] = __ldg(x + r * ldx + c);
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += 8) {
+        const int64_t c = c0 + i, r = r0 + threadIdx.x;
+        if (r < rows && c < cols) y[c * ldy + r] = t[threadIdx.x][i];
+    }
+}
+}  // namespace
+
+cudaError_t launch_transpose(const float *x, int64_t rows, int64_t cols, int64_t ldx, float *y, int64_t ldy,
+                             cudaStream_t s) {
+    if (rows == 0 || cols == 0) return cudaSuccess;
+    dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+    transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(x, rows, cols, ldx, y, ldy);
+    return cudaGetLastError();
+}

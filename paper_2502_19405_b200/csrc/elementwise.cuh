@@ -19,3 +19,5 @@ cudaError_t launch_embedding(const int32_t *tok, int64_t ntok, int64_t T, const 
 cudaError_t launch_embedding_backward(const int32_t *tok, int64_t ntok, int64_t T, const float *dx0, int64_t C,
                                       float *dwte, float *dwpe, cudaStream_t s);
 cudaError_t launch_flip_bit(void *data, int64_t elem, int bit, cudaStream_t s);
+cudaError_t launch_transpose(const float *x, int64_t rows, int64_t cols, int64_t ldx, float *y, int64_t ldy,
+                             cudaStream_t s);

@@ -382,8 +382,8 @@ cudaError_t gemm_launch(const GemmParams &p, cudaStream_t s, int force_cfg) {
         // area / sustained rate, rates measured on B200 with tools/gemm_tune.py and
         // tools/gpt2_gemm_tune.py (TFLOP/s on large, full-wave problems).
         struct C { int id, bm, bn, occ; double rate; };
-        static const C cand[] = {{3, 128, 256, 1, 53.0}, {4, 256, 128, 1, 50.0}, {0, 128, 128, 2, 50.0},
-                                 {6, 64, 128, 3, 49.0}, {5, 128, 64, 3, 47.5}, {1, 64, 64, 2, 44.0}};
+        static const C cand[] = {{6, 64, 128, 3, 55.0}, {3, 128, 256, 1, 55.0}, {5, 128, 64, 3, 53.0},
+                                 {4, 256, 128, 1, 49.0}, {1, 64, 64, 2, 48.0}};
         const int64_t nb = p.batch0 * p.batch1;
         const int sms = ro_host::num_sms();
         double best = 1e300;

@@ -188,6 +188,10 @@ class GPT2Step:
         self.glocal = torch.zeros(self.S_loc, self.P, device=dev)  # per-shard gradients (rows)
         self.grad = E(self.P)
         self.shard_loss = E(self.S_loc)
+        # transposed copies of the 2-D weights (refreshed every step, data movement
+        # only): every dgrad GEMM and the LM head then read an n-contiguous B
+        self.wT = {name: E(*shape[::-1]) for name, shape, kind in self.specs
+                   if len(shape) == 2 and name != "wpe"}
 
     # ------------------------------------------------------------------ program construction
     def _build_program(self):
@@ -215,6 +219,12 @@ class GPT2Step:
         self._label_phase, self._tensor_phase = {}, {}
         # ---- replicated input nodes: parameters with their optimizer state
         self.phase("inputs")
+        if not self.structure_only:
+            def transposes():
+                from . import repops_transpose
+                for name, t in self.wT.items():
+                    repops_transpose(self.pview(self.params, name), out=t)
+            self.launch(transposes)
         self.param_in = {}
         for name, shape, kind in self.specs:
             ids = [T_(f"param/{name}", self.pview(self.params, name), REPLICATED),
@@ -392,7 +402,7 @@ class GPT2Step:
                                  c.ln_eps, out=self.lnf, mean=self.muf, rstd=self.rsf)
                 self._hook("head/lnf")
                 wte = self.pview(self.params, "wte")
-                repops_gemm(self.lnf, wte, transB=True, out=self.logits[:, :c.vocab])
+                repops_gemm(self.lnf, self.wT["wte"], out=self.logits[:, :c.vocab])
                 self._hook("head/lm_head")
                 repops_cross_entropy(self.logits, self.targets_flat, scale=1.0 / (c.shards * c.seq),
                                      loss=self.loss_tok, dlogits=self.dlogits, V=c.vocab)
@@ -457,7 +467,7 @@ class GPT2Step:
                     dout = self.dx[l + 1]
                     o = lambda n: self.off[p + n][0]  # noqa: E731
                     # FC2
-                    repops_gemm(dout, W("fc2.w"), transB=True, out=g["dgelu"])
+                    repops_gemm(dout, self.wT[p + "fc2.w"], out=g["dgelu"])
                     self._hook(f"h{l}/fc2_dgrad")
                     repops_gemm_strided_batched(a["gelu"], dout, gl, M=c.ffn, N=d, K=T, lda=c.ffn, ldb=d, ldc=d,
                                                 sA=(T * c.ffn, 0), sB=(T * d, 0), sC=(self.P, 0), batch=(S_loc, 1),
@@ -468,7 +478,7 @@ class GPT2Step:
                     repops_gelu_backward(a["fc"], g["dgelu"], out=g["dfc"])
                     self._hook(f"h{l}/gelu_bwd")
                     # FC
-                    repops_gemm(g["dfc"], W("fc.w"), transB=True, out=g["dln2"])
+                    repops_gemm(g["dfc"], self.wT[p + "fc.w"], out=g["dln2"])
                     self._hook(f"h{l}/fc_dgrad")
                     repops_gemm_strided_batched(a["ln2"], g["dfc"], gl, M=d, N=c.ffn, K=T, lda=d, ldb=c.ffn,
                                                 ldc=c.ffn, sA=(T * d, 0), sB=(T * c.ffn, 0), sC=(self.P, 0),
@@ -484,7 +494,7 @@ class GPT2Step:
                                                      dgamma=gl[:, o("ln2.g"):], dbeta=gl[:, o("ln2.b"):], ldo=self.P)
                     self._hook(f"h{l}/ln2_params")
                     # proj
-                    repops_gemm(g["dxmid"], W("proj.w"), transB=True, out=g["datt"])
+                    repops_gemm(g["dxmid"], self.wT[p + "proj.w"], out=g["datt"])
                     self._hook(f"h{l}/proj_dgrad")
                     repops_gemm_strided_batched(a["att"], g["dxmid"], gl, M=d, N=d, K=T, lda=d, ldb=d, ldc=d,
                                                 sA=(T * d, 0), sB=(T * d, 0), sC=(self.P, 0), batch=(S_loc, 1),
@@ -511,7 +521,7 @@ class GPT2Step:
                                                 sC=(T * 3 * d, hd), batch=(S_loc, H), transA=True, offC=d)
                     self._hook(f"h{l}/attn_dqkv")
                     # QKV
-                    repops_gemm(g["dqkv"], W("attn.w"), transB=True, out=g["dln1"])
+                    repops_gemm(g["dqkv"], self.wT[p + "attn.w"], out=g["dln1"])
                     self._hook(f"h{l}/qkv_dgrad")
                     repops_gemm_strided_batched(a["ln1"], g["dqkv"], gl, M=d, N=3 * d, K=T, lda=d, ldb=3 * d,
                                                 ldc=3 * d, sA=(T * d, 0), sB=(T * 3 * d, 0), sC=(self.P, 0),
