@@ -184,15 +184,17 @@ class GemmSweep:
 
 # ---------------------------------------------------------------------- GPT-2 workload
 class GPT2Train:
-    def __init__(self, rank, world, device, pg=None):
+    def __init__(self, rank, world, device, pg=None, commit=True, overlap=True):
         from paper_2502_19405_b200.gpt2 import GPT2Config, GPT2Step
         self.st = GPT2Step(GPT2Config(), rank=rank, world=world, device=device, pg=pg)
+        self.st.overlap_commits = overlap
+        self.commit = commit
         self.st.set_tokens(0)
         self.flops = self.st.flops_per_step()
         self.root = None
 
     def step(self):
-        self.st.run()
+        self.st.run(commit=self.commit)
         self.root, _ = self.st.step_root()   # C2 gather + D2H of the digest table + node digests + root
 
     def e2e_step(self):
@@ -233,7 +235,7 @@ def oracle_sample_gemm(seconds_target=10.0):
     return flops / t_total / 1e12, t_total, f"first rows {rows_done} of each sweep GEMM (full K fold)"
 
 
-def oracle_sample_gpt2(rows=8):
+def oracle_sample_gpt2(rows=128):
     """The oracle on a bounded sample of the GPT-2 step: `rows` token rows of shard 0
     through layer 0's four linear GEMMs (full K folds) and the LM head (K = 768 over
     all 50257 vocabulary columns), with their LayerNorm / GELU / softmax row work."""
@@ -337,6 +339,8 @@ def main():
     ap.add_argument("--workload", default="gpt2", choices=["gpt2", "gemm"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-commit", action="store_true", help="diagnostic: skip the Verde commitments")
+    ap.add_argument("--no-overlap", action="store_true", help="diagnostic: commits on the main stream")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
@@ -352,7 +356,8 @@ def main():
     results = {}
     order = [args.workload] + ([] if args.no_sweep else [w for w in ("gemm",) if w != args.workload])
     for wname in order:
-        wl = GPT2Train(rank, world, device) if wname == "gpt2" else GemmSweep(rank, world, device)
+        wl = (GPT2Train(rank, world, device, commit=not args.no_commit, overlap=not args.no_overlap)
+              if wname == "gpt2" else GemmSweep(rank, world, device))
         for _ in range(args.warmup):
             wl.step()
         torch.cuda.synchronize()
