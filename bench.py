@@ -195,7 +195,7 @@ class GPT2Train:
 
     def step(self):
         self.st.run(commit=self.commit)
-        self.root, _ = self.st.step_root()   # C2 gather + D2H of the digest table + node digests + root
+        self.root = self.st.device_root()    # C2 gather + node digests + step root on the GPU; 32 B D2H
 
     def e2e_step(self):
         self.st.set_tokens(self.st.step_no)    # H2D of this step's batch from pinned host memory
@@ -208,7 +208,7 @@ class GPT2Train:
 
     @property
     def d2h_bytes(self):
-        return self.st.n_slots * 32 + 4
+        return 32 + 4  # step root + loss
 
 
 # ---------------------------------------------------------------------- oracle legs

@@ -267,6 +267,21 @@ int verde_node_digests(int64_t n, const uint8_t *blob, const int64_t *offs, cons
                        const int64_t *soffs, const uint8_t *table, int64_t n_slots, uint8_t *out,
                        uint8_t *root32);
 
+/* The same step root computed on the DEVICE from device-resident inputs, as a
+ * reusable plan: blob/offs/slots/soffs are the static node serialisations and
+ * slot lists above (device copies), table the device digest table that the
+ * commit plans fill.  run() enqueues: one thread per node hashing its
+ * serialisation + gathered digests; RFC 6962 leaves; aligned 256-group reduce
+ * passes; writes node_out (n x 32, nullable) and root_out (32 bytes, device).
+ * ws >= verde_root_plan_workspace_bytes(n) is caller-owned and outlives the plan. */
+typedef struct verde_root_plan verde_root_plan;
+int64_t verde_root_plan_workspace_bytes(int64_t n);
+int verde_root_plan_create(int64_t n, const uint8_t *blob, const int64_t *offs, const int64_t *slots,
+                           const int64_t *soffs, const uint8_t *table, uint8_t *node_out, uint8_t *root_out,
+                           void *ws, int64_t ws_bytes, verde_root_plan **plan);
+int verde_root_plan_run(const verde_root_plan *plan, void *stream);
+void verde_root_plan_destroy(verde_root_plan *plan);
+
 /* First index d with seq0[d] != seq1[d] over n 32-byte digests (Alg. 2 line 8,
  * P:429-430), found by descending the two RFC 6962 trees from the roots
  * (O(log n) subtree comparisons).  *d_out = -1 if the sequences are equal. */

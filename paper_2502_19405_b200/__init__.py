@@ -408,6 +408,42 @@ class CommitPlan:
             pass
 
 
+class RootPlan:
+    """verde_root_plan_*: node digests + RFC 6962 step root on the device.
+    blob/offs/slots/soffs: host numpy arrays of the static node serialisation
+    (copied to the device once); table: device uint8 [n_slots, 32]."""
+
+    def __init__(self, blob, offs, slots, soffs, table, with_nodes=True):
+        dev = table.device
+        n = len(offs) - 1
+        self.n = n
+        self.blob = torch.from_numpy(blob).to(dev)
+        self.offs = torch.from_numpy(offs).to(dev)
+        self.slots = torch.from_numpy(slots).to(dev)
+        self.soffs = torch.from_numpy(soffs).to(dev)
+        self.table = table
+        self.nodes = torch.zeros((n, 32), dtype=torch.uint8, device=dev) if with_nodes else None
+        self.root = torch.zeros(32, dtype=torch.uint8, device=dev)
+        self.ws = torch.empty(max(lib().verde_root_plan_workspace_bytes(n), 256), dtype=torch.uint8, device=dev)
+        h = C.c_void_p()
+        check(lib().verde_root_plan_create(n, self.blob.data_ptr(), self.offs.data_ptr(), self.slots.data_ptr(),
+                                           self.soffs.data_ptr(), table.data_ptr(),
+                                           self.nodes.data_ptr() if with_nodes else None, self.root.data_ptr(),
+                                           self.ws.data_ptr(), self.ws.numel(), C.byref(h)), "verde_root_plan_create")
+        self.h = h
+
+    def run(self, stream=None):
+        check(lib().verde_root_plan_run(self.h, _stream(stream)), "verde_root_plan_run")
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().verde_root_plan_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
 def verde_commit_tensor(t, ws: CommitWorkspace | None = None, stream=None):
     return verde_commit_tensors([t], ws=ws, stream=stream)[0]
 

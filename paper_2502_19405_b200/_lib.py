@@ -72,6 +72,10 @@ SIGNATURES = {
     "verde_node_digest": (i32, [vp, vp]),
     "verde_node_digests": (i32, [i64, vp, vp, vp, vp, vp, i64, vp, vp]),
     "verde_first_divergence": (i32, [vp, vp, i64, vp, vp]),
+    "verde_root_plan_workspace_bytes": (i64, [i64]),
+    "verde_root_plan_create": (i32, [i64, vp, vp, vp, vp, vp, vp, vp, vp, i64, vp]),
+    "verde_root_plan_run": (i32, [vp, vp]),
+    "verde_root_plan_destroy": (None, [vp]),
 }
 
 _lib = None

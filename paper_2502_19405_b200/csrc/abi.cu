@@ -554,6 +554,34 @@ int verde_node_digests(int64_t n, const uint8_t *blob, const int64_t *offs, cons
     return REPOPS_OK;
 }
 
+int64_t verde_root_plan_workspace_bytes(int64_t n) { return n >= 1 ? root_plan_workspace(n) : 0; }
+
+int verde_root_plan_create(int64_t n, const uint8_t *blob, const int64_t *offs, const int64_t *slots,
+                           const int64_t *soffs, const uint8_t *table, uint8_t *node_out, uint8_t *root_out,
+                           void *ws, int64_t ws_bytes, verde_root_plan **plan) {
+    REQ(n >= 1 && blob && offs && slots && soffs && table && root_out && ws && plan, "root_plan_create: bad argument");
+    void *out = nullptr;
+    cudaError_t e = root_plan_create(n, blob, offs, slots, soffs, table, node_out, root_out, ws, ws_bytes, &out);
+    if (e == cudaErrorMemoryAllocation)
+        return fail(REPOPS_ENOSPACE, "root_plan: workspace %lld < %lld", (long long)ws_bytes,
+                    (long long)root_plan_workspace(n));
+    if (e != cudaSuccess) return fail(REPOPS_ECUDA, "root_plan_create: %s", cudaGetErrorString(e));
+    *plan = reinterpret_cast<verde_root_plan *>(out);
+    return REPOPS_OK;
+}
+
+int verde_root_plan_run(const verde_root_plan *plan, void *stream) {
+    REQ(plan, "root_plan_run: null plan");
+    int nk = 0;
+    cudaError_t e = root_plan_run(plan, S(stream), &nk);
+    if (e == cudaSuccess) g_launches.fetch_add(nk - 1, std::memory_order_relaxed);
+    return cuda_status(e, "root_plan_run");
+}
+
+void verde_root_plan_destroy(verde_root_plan *plan) {
+    if (plan) root_plan_destroy(plan);
+}
+
 int verde_first_divergence(const uint8_t *seq0, const uint8_t *seq1, int64_t n, int64_t *d_out, int64_t *rounds_out) {
     REQ(n >= 1 && seq0 && seq1 && d_out, "first_divergence: bad argument");
     // Descend the two RFC 6962 trees: at each node compare the LEFT subtree roots;

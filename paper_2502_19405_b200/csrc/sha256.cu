@@ -457,3 +457,154 @@ cudaError_t commit_plan_run(const void *plan, cudaStream_t s, int *nkernels) {
 }
 
 void commit_plan_destroy(void *plan) { delete reinterpret_cast<CommitPlanImpl *>(plan); }
+
+// ---------------------------------------------------------------------------------
+// Step root on the device (R-NODE + R-MERKLE): node digests from the static node
+// serialisations and the device digest table, then the RFC 6962 root over them.
+namespace {
+
+// SHA-256 of blob[a, b) || table[32*slots[j]] for j in [sa, sb) -- streamed in 64-byte blocks
+__global__ void node_digest_kernel(const uint8_t *__restrict__ blob, const int64_t *__restrict__ offs,
+                                   const int64_t *__restrict__ slots, const int64_t *__restrict__ soffs,
+                                   const uint8_t *__restrict__ table, int64_t n, Digest *__restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t pa = offs[i], pb = offs[i + 1], sa = soffs[i], sb = soffs[i + 1];
+    const int64_t len = (pb - pa) + 32 * (sb - sa);
+    auto byte_at = [&](int64_t m) -> uint32_t {
+        if (m < pb - pa) return blob[pa + m];
+        const int64_t q = m - (pb - pa);
+        return table[32 * slots[sa + q / 32] + (q % 32)];
+    };
+    uint32_t st[8];
+    init_state(st);
+    const int64_t nblk = (len + 9 + 63) / 64;
+    for (int64_t blk = 0; blk < nblk; ++blk) {
+        uint32_t w[16];
+        for (int j = 0; j < 16; ++j) {
+            uint32_t word = 0;
+            for (int q = 0; q < 4; ++q) {
+                const int64_t m = blk * 64 + j * 4 + q;
+                uint32_t b;
+                if (m < len) b = byte_at(m);
+                else if (m == len) b = 0x80;
+                else if (m >= nblk * 64 - 8) b = (uint32_t)(((uint64_t)len * 8) >> (8 * (nblk * 64 - 1 - m))) & 0xFF;
+                else b = 0;
+                word = (word << 8) | b;
+            }
+            w[j] = word;
+        }
+        compress(st, w);
+    }
+    Digest d;
+    for (int j = 0; j < 8; ++j) d.h[j] = st[j];
+    out[i] = d;
+}
+
+// RFC 6962 leaf hash of 32-byte entries: SHA-256(0x00 || entry), entry as state words
+__global__ void entry_leaf_kernel(const Digest *__restrict__ e, int64_t n, Digest *__restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t *h = e[i].h;
+    uint32_t w[16];
+    w[0] = h[0] >> 8;
+    for (int j = 1; j < 8; ++j) w[j] = __funnelshift_r(h[j], h[j - 1], 8);
+    w[8] = (h[7] << 24) | 0x00800000u;
+    for (int j = 9; j < 15; ++j) w[j] = 0;
+    w[15] = 33 * 8;
+    uint32_t st[8];
+    init_state(st);
+    compress(st, w);
+    Digest d;
+    for (int j = 0; j < 8; ++j) d.h[j] = st[j];
+    out[i] = d;
+}
+
+__global__ void digest_bytes_kernel(const Digest *__restrict__ in, int64_t n, uint8_t *__restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n * 8) return;
+    const uint32_t v = in[i / 8].h[i % 8];
+    uint8_t *o = out + 4 * i;
+    o[0] = (uint8_t)(v >> 24); o[1] = (uint8_t)(v >> 16); o[2] = (uint8_t)(v >> 8); o[3] = (uint8_t)v;
+}
+
+}  // namespace
+
+struct RootPlanImpl {
+    int64_t n;
+    const uint8_t *blob;
+    const int64_t *offs, *slots, *soffs;
+    const uint8_t *table;
+    uint8_t *node_out, *root_out;
+    // workspace: node digests (as words) | leaf digests A | level buffer B | pass tables
+    Digest *nodes, *A, *B;
+    std::vector<int64_t> pass_blocks;  // reduce passes: number of CTAs each
+    std::vector<int64_t *> pass_tab;   // per pass: 4 int64 tables of length 2,1,1,1 (one "tensor")
+    std::vector<bool> pass_to_b;
+    bool final_in_b;
+};
+
+int64_t root_plan_workspace(int64_t n) {
+    int64_t passes = 0, c = n;
+    while (c > 1) { c = (c + 255) / 256; ++passes; }
+    return align_up(n * 32, 256) * 2 + align_up(((n + 255) / 256 + 1) * 32, 256) + 256 * (passes + 1);
+}
+
+cudaError_t root_plan_create(int64_t n, const uint8_t *blob, const int64_t *offs, const int64_t *slots,
+                             const int64_t *soffs, const uint8_t *table, uint8_t *node_out, uint8_t *root_out,
+                             void *ws, int64_t ws_bytes, void **out) {
+    if (ws_bytes < root_plan_workspace(n)) return cudaErrorMemoryAllocation;
+    RootPlanImpl *p = new RootPlanImpl{};
+    p->n = n; p->blob = blob; p->offs = offs; p->slots = slots; p->soffs = soffs; p->table = table;
+    p->node_out = node_out; p->root_out = root_out;
+    uint8_t *base = reinterpret_cast<uint8_t *>(ws);
+    p->nodes = reinterpret_cast<Digest *>(base);
+    p->A = reinterpret_cast<Digest *>(base + align_up(n * 32, 256));
+    p->B = reinterpret_cast<Digest *>(base + 2 * align_up(n * 32, 256));
+    uint8_t *tabs = base + 2 * align_up(n * 32, 256) + align_up(((n + 255) / 256 + 1) * 32, 256);
+    // passes over a single "tensor" of n leaves: ping-pong A -> B -> A ...
+    int64_t cnt = n;
+    bool in_b = false;
+    std::vector<int64_t> host;
+    while (cnt > 1) {
+        const int64_t blocks = (cnt + 255) / 256;
+        int64_t t[5] = {0, blocks, 0, cnt, 0};  // block_prefix[2], cur_off, cur_cnt, nxt_off
+        int64_t *dst = reinterpret_cast<int64_t *>(tabs + 256 * p->pass_tab.size());
+        cudaError_t e = cudaMemcpy(dst, t, sizeof t, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) { delete p; return e; }
+        p->pass_tab.push_back(dst);
+        p->pass_blocks.push_back(blocks);
+        p->pass_to_b.push_back(!in_b);
+        in_b = !in_b;
+        cnt = blocks;
+    }
+    p->final_in_b = in_b;
+    *out = p;
+    return cudaSuccess;
+}
+
+cudaError_t root_plan_run(const void *plan, cudaStream_t s, int *nkernels) {
+    const RootPlanImpl *p = reinterpret_cast<const RootPlanImpl *>(plan);
+    const int64_t n = p->n;
+    const unsigned g = (unsigned)((n + 127) / 128);
+    node_digest_kernel<<<g, 128, 0, s>>>(p->blob, p->offs, p->slots, p->soffs, p->table, n, p->nodes);
+    entry_leaf_kernel<<<g, 128, 0, s>>>(p->nodes, n, p->A);
+    int nk = 2;
+    for (size_t q = 0; q < p->pass_tab.size(); ++q) {
+        const int64_t *t = p->pass_tab[q];
+        const Digest *cur = p->pass_to_b[q] ? p->A : p->B;
+        Digest *nxt = p->pass_to_b[q] ? p->B : p->A;
+        reduce_kernel<<<(unsigned)p->pass_blocks[q], 128, 0, s>>>(t, t + 2, t + 3, t + 4, 1, cur, nxt);
+        ++nk;
+    }
+    const Digest *root = (n == 1) ? p->A : (p->final_in_b ? p->B : p->A);
+    if (p->node_out) {
+        digest_bytes_kernel<<<(unsigned)((n * 8 + 255) / 256), 256, 0, s>>>(p->nodes, n, p->node_out);
+        ++nk;
+    }
+    digest_bytes_kernel<<<1, 32, 0, s>>>(root, 1, p->root_out);
+    *nkernels = nk + 1;
+    return cudaGetLastError();
+}
+
+void root_plan_destroy(void *plan) { delete reinterpret_cast<RootPlanImpl *>(plan); }

@@ -12,4 +12,10 @@ cudaError_t commit_launch(const verde_tensor_desc *d, int n, void *ws, int64_t w
 cudaError_t commit_plan_create(const verde_tensor_desc *d, int n, void *ws, int64_t ws_bytes, void **out,
                                int64_t *need);
 cudaError_t commit_plan_run(const void *plan, cudaStream_t s, int *nkernels);
+int64_t root_plan_workspace(int64_t n);
+cudaError_t root_plan_create(int64_t n, const uint8_t *blob, const int64_t *offs, const int64_t *slots,
+                             const int64_t *soffs, const uint8_t *table, uint8_t *node_out, uint8_t *root_out,
+                             void *ws, int64_t ws_bytes, void **out);
+cudaError_t root_plan_run(const void *plan, cudaStream_t s, int *nkernels);
+void root_plan_destroy(void *plan);
 void commit_plan_destroy(void *plan);

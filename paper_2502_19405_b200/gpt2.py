@@ -715,6 +715,11 @@ class GPT2Step:
             self.side = torch.cuda.Stream(device=self.dev)
             self.overlap_commits = True
         self._build_node_blob()
+        if not self.structure_only:
+            from . import RootPlan
+            self.root_plan = RootPlan(self.node_blob, self.node_offs, self.node_slots, self.node_soffs,
+                                      self.digests, with_nodes=True)
+            self.root_host = torch.zeros(32, dtype=torch.uint8).pin_memory()
 
     def _build_node_blob(self):
         """Static serialisation of every node except its tensor digests (R13)."""
@@ -804,6 +809,16 @@ class GPT2Step:
         self.digests_host.copy_(self.digests, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         return self.digests_host.numpy()
+
+    def device_root(self, sync=True):
+        """Step root computed on the GPU (verde_root_plan): C2 gather of the shard digest
+        regions (N > 1), node digests, RFC 6962 root; only 32 bytes come back."""
+        gather_shard_digests(self.digests, self.rep_slots, self.shard_slots, self.s0, self.S_loc, self.world, self.pg)
+        self.root_plan.run()
+        self.root_host.copy_(self.root_plan.root, non_blocking=True)
+        if sync:
+            torch.cuda.current_stream().synchronize()
+        return bytes(self.root_host.numpy())
 
     def step_root(self, table=None):
         """Node digests (R-NODE) and the step's Merkle root (R-MERKLE), host native code."""

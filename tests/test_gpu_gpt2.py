@@ -88,6 +88,12 @@ def test_tiny_step_root_recomputed_independently(tiny_run):
     assert root == mth(digs)
 
 
+def test_device_root_equals_host_root(tiny_run):
+    cfg, st, root, nd, ref, W = tiny_run
+    assert st.device_root() == root
+    assert st.root_plan.nodes.cpu().numpy().tobytes() == np.asarray(nd).tobytes()
+
+
 def test_tiny_step_replay_is_bit_identical(tiny_run):
     from paper_2502_19405_b200.gpt2 import GPT2Step
     cfg, st, root, nd, ref, W = tiny_run
