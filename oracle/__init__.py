@@ -80,6 +80,9 @@ def lib():
                 "orc_commit_tensor": (None, [vp, i64, i32, i32, vp, vp]),
                 "orc_data_root": (None, [vp, i64, vp]),
                 "orc_mth": (None, [vp, vp, i64, vp]),
+                "orc_rmsnorm": (None, [vp, vp, i64, i64, f32, vp, vp]),
+                "orc_swiglu": (None, [vp, vp, i64, vp]),
+                "orc_rope": (None, [vp, i64, i64, i64, i64, vp, vp, vp, i64]),
             }
             for name, (res, args) in sig.items():
                 fn = getattr(L, name)
@@ -265,6 +268,36 @@ def layernorm_backward_params(dy, x, mean, rstd, nseg=1):
     db = np.empty((nseg, c), np.float32)
     lib().orc_layernorm_backward_params(_p(dy), _p(x), _p(mean), _p(rstd), r, c, nseg, _p(dg), _p(db))
     return dg, db
+
+
+def rmsnorm(x, w, eps=1e-5):
+    """R-RMSNORM (orc_rmsnorm).  Returns (y, rstd)."""
+    x = _f32(x)
+    w = _f32(w)
+    r, c = x.shape
+    y = np.empty_like(x)
+    rs = np.empty(r, np.float32)
+    lib().orc_rmsnorm(_p(x), _p(w), r, c, float(eps), _p(y), _p(rs))
+    return y, rs
+
+
+def swiglu(g, u):
+    """R-SWIGLU: silu(g) * u elementwise (orc_swiglu)."""
+    g = _f32(g)
+    u = _f32(u)
+    h = np.empty_like(g)
+    lib().orc_swiglu(_p(g), _p(u), g.size, _p(h))
+    return h
+
+
+def rope(x, cos, sin, nhead, hd):
+    """R-ROPE on x [ntok, nhead*hd] (rows = tokens) with tables [ntok, hd/2]."""
+    x = _f32(x)
+    cos = _f32(cos)
+    sin = _f32(sin)
+    y = np.empty_like(x)
+    lib().orc_rope(_p(x), x.shape[0], nhead, hd, x.shape[1], _p(cos), _p(sin), _p(y), x.shape[1])
+    return y
 
 
 def cross_entropy(logits, labels, scale=1.0, want_grad=True):

@@ -393,6 +393,47 @@ void orc_layernorm_backward_params(const float *dy, const float *x, const float 
 }
 
 /* ======================================================================
+ * Llama operators (BASELINE config 4; readings R20-R22 in DESIGN.md).
+ * R-RMSNORM: ms = CDOT(x,x)/n;  rstd = 1/sqrt(ms + eps);  y_i = (x_i * rstd) * w_i
+ * R-SWIGLU:  h_i = silu(g_i) * u_i,  silu(g) = g / (1 + exp(-g))   (-g: sign flip, exact)
+ * R-ROPE:    rotate-half form with cos/sin tables given as inputs [T, hd/2]:
+ *            y_i     = x_i * c_i - x_{i+h} * s_i,   y_{i+h} = x_{i+h} * c_i + x_i * s_i
+ *            for each token t, head, i < h = hd/2 (t indexes the table rows)
+ * ==================================================================== */
+void orc_rmsnorm(const float *x, const float *w, i64 rows, i64 cols, float eps, float *y, float *rstd) {
+    float n = (float)cols;
+    for (i64 r = 0; r < rows; ++r) {
+        const float *xr = x + r * cols;
+        float ms = orc_cdot(xr, xr, cols) / n;
+        float rs = 1.0f / sqrtf(ms + eps);
+        for (i64 i = 0; i < cols; ++i) y[r * cols + i] = canon((xr[i] * rs) * w[i]);
+        if (rstd) rstd[r] = canon(rs);
+    }
+}
+
+static float silu(float g) { return g / (1.0f + orc_exp(-g)); }
+
+void orc_swiglu(const float *g, const float *u, i64 n, float *h) {
+    for (i64 i = 0; i < n; ++i) h[i] = canon(silu(g[i]) * u[i]);
+}
+
+void orc_rope(const float *x, i64 ntok, i64 nhead, i64 hd, i64 ld, const float *cosv, const float *sinv,
+              float *y, i64 ldy) {
+    i64 h = hd / 2;
+    for (i64 t = 0; t < ntok; ++t)
+        for (i64 q = 0; q < nhead; ++q) {
+            const float *xi = x + t * ld + q * hd;
+            float *yo = y + t * ldy + q * hd;
+            for (i64 i = 0; i < h; ++i) {
+                float c = cosv[t * h + i], s = sinv[t * h + i];
+                float a = xi[i], b = xi[i + h];
+                yo[i] = canon((a * c) - (b * s));
+                yo[i + h] = canon((b * c) + (a * s));
+            }
+        }
+}
+
+/* ======================================================================
  * R-CE: cross entropy over a row of V logits (leading dimension ld).
  *   m = max;  s = CSUM(exp(x_i - m));  loss = (m + log s) - x_label
  *   dlogit_i = ((exp(x_i - m) * (1/s)) - [i == label]) * scale
