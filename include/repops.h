@@ -169,6 +169,29 @@ int repops_embedding_backward(const int32_t *tok, int64_t ntok, int64_t T, const
 int repops_adamw(float *p, const float *g, float *m, float *v, int64_t n, int64_t step,
                  float lr, float b1, float b2, float eps, float wd, int decay, void *stream);
 
+/* ------------------------------------------------------------------ Llama operators (config 4)
+ * R-RMSNORM (R20): ms = CDOT(x,x)/n; rstd = fdiv(1, fsqrt(ms + eps)); y = fmul(fmul(x, rstd), w).
+ * Contiguous rows, cols <= 4096; rstd (rows floats) optional. */
+int repops_rmsnorm(const float *x, const float *w, int64_t rows, int64_t cols, float eps, float *y, float *rstd,
+                   void *stream);
+/* R-SWIGLU (R21): h = fmul(fdiv(g, fadd(1, exp(-g))), u), exp = R-EXP, -g an exact sign flip. */
+int repops_swiglu(const float *g, const float *u, int64_t n, float *h, void *stream);
+/* R-ROPE (R22), rotate-half form with cos/sin tables [ntok, hd/2] given as inputs:
+ * y_i = x_i c_i - x_{i+h} s_i,  y_{i+h} = x_{i+h} c_i + x_i s_i  per (token, head), h = hd/2.
+ * x, y: [ntok, ld/ldy] rows holding nhead*hd values; y may alias x. */
+int repops_rope(const float *x, int64_t ntok, int64_t nhead, int64_t hd, int64_t ld, const float *cos_t,
+                const float *sin_t, float *y, int64_t ldy, void *stream);
+/* out[t][c] = table[idx[t]][c] (exact gather; token embedding without positions). */
+int repops_gather_rows(const float *table, const int32_t *idx, int64_t n, int64_t C, float *out, void *stream);
+/* Synthetic-input generator (not part of the method): out[i] = the SplitMix64
+ * uniform of synth.uniform(seed) (24-bit grid in [-1,1), times `scale` rounded
+ * once); lets multi-GB weights be generated on the device bit-identically. */
+int repops_fill_uniform(float *out, int64_t n, uint64_t seed, double scale, void *stream);
+
+/* Strided 2-D copy (data movement only): dst[r*ldd + c] = src[r*lds + c], r < rows, c < cols.
+ * Used to place all-gathered tensor-parallel column blocks into one activation. */
+int repops_copy2d(const float *src, int64_t rows, int64_t cols, int64_t lds, float *dst, int64_t ldd, void *stream);
+
 /* Transpose (data movement only, bit-exact): y[j*ldy + i] = x[i*ldx + j] for a
  * rows x cols x.  Used to give backward GEMMs an n-contiguous weight operand. */
 int repops_transpose(const float *x, int64_t rows, int64_t cols, int64_t ldx, float *y, int64_t ldy, void *stream);

@@ -314,6 +314,61 @@ def repops_adamw(p, g, m, v, step, lr, b1, b2, eps, wd, decay, stream=None):
     return p, m, v
 
 
+def repops_rmsnorm(x, w, eps=1e-5, out=None, rstd=None, stream=None):
+    """R-RMSNORM (contiguous rows, cols <= 4096).  Returns (y, rstd)."""
+    _contig(x, "x")
+    rows, cols = x.shape
+    if out is None:
+        out = torch.empty_like(x)
+    if rstd is None:
+        rstd = torch.empty(rows, dtype=torch.float32, device=x.device)
+    check(lib().repops_rmsnorm(_p(x), _p(w), rows, cols, float(eps), _p(out), _p(rstd), _stream(stream)),
+          "repops_rmsnorm")
+    return out, rstd
+
+
+def repops_swiglu(g, u, out=None, stream=None):
+    _contig(g, "g"), _contig(u, "u")
+    if out is None:
+        out = torch.empty_like(g)
+    check(lib().repops_swiglu(_p(g), _p(u), g.numel(), _p(out), _stream(stream)), "repops_swiglu")
+    return out
+
+
+def repops_rope(x, cos_t, sin_t, nhead, hd, out=None, stream=None):
+    """R-ROPE on x [ntok, >= nhead*hd] (row stride = ld) with tables [ntok, hd/2]."""
+    _f32(x, "x")
+    if out is None:
+        out = torch.empty_like(x)
+    check(lib().repops_rope(_p(x), x.shape[0], nhead, hd, _ld(x), _p(cos_t), _p(sin_t), _p(out), _ld(out),
+                            _stream(stream)), "repops_rope")
+    return out
+
+
+def repops_gather_rows(table, idx, out=None, stream=None):
+    if idx.dtype != torch.int32:
+        raise RepopsError("idx must be int32")
+    n, Cc = idx.numel(), table.shape[1]
+    if out is None:
+        out = torch.empty((n, Cc), dtype=torch.float32, device=table.device)
+    check(lib().repops_gather_rows(_p(table), _p(idx), n, Cc, _p(out), _stream(stream)), "repops_gather_rows")
+    return out
+
+
+def repops_fill_uniform(out, seed, scale=1.0, stream=None):
+    """Device twin of synth.uniform(seed, shape, scale) (input generation only)."""
+    check(lib().repops_fill_uniform(_p(out), out.numel(), int(seed) & 0xFFFFFFFFFFFFFFFF, float(scale),
+                                    _stream(stream)), "repops_fill_uniform")
+    return out
+
+
+def repops_copy2d(src, dst, stream=None):
+    """dst[:, :] = src (both 2-D views with unit column stride; data movement only)."""
+    rows, cols = src.shape
+    check(lib().repops_copy2d(_p(src), rows, cols, _ld(src), _p(dst), _ld(dst), _stream(stream)), "repops_copy2d")
+    return dst
+
+
 def repops_transpose(x, out=None, stream=None):
     """out = x^T (bit-exact data movement)."""
     _f32(x, "x")

@@ -60,6 +60,12 @@ SIGNATURES = {
     "repops_adamw": (i32, [vp, vp, vp, vp, i64, i64, f32, f32, f32, f32, f32, i32, vp]),
     "repops_flip_bit": (i32, [vp, i64, i32, vp]),
     "repops_transpose": (i32, [vp, i64, i64, i64, vp, i64, vp]),
+    "repops_rmsnorm": (i32, [vp, vp, i64, i64, f32, vp, vp, vp]),
+    "repops_copy2d": (i32, [vp, i64, i64, i64, vp, i64, vp]),
+    "repops_swiglu": (i32, [vp, vp, i64, vp, vp]),
+    "repops_rope": (i32, [vp, i64, i64, i64, i64, vp, vp, vp, i64, vp]),
+    "repops_gather_rows": (i32, [vp, vp, i64, i64, vp, vp]),
+    "repops_fill_uniform": (i32, [vp, i64, C.c_uint64, C.c_double, vp]),
     "verde_commit_workspace_bytes": (i64, [vp, i32]),
     "verde_commit_tensors": (i32, [vp, i32, vp, i64, vp]),
     "verde_commit_tensor": (i32, [vp, i64, i32, i32, vp, vp, vp, i64, vp]),

@@ -393,6 +393,49 @@ int repops_adamw(float *p, const float *g, float *m, float *v, int64_t n, int64_
                        "adamw");
 }
 
+int repops_rmsnorm(const float *x, const float *w, int64_t rows, int64_t cols, float eps, float *y, float *rstd,
+                   void *stream) {
+    REQ(rows >= 0 && cols >= 1 && cols <= TILE_ELEMS, "rmsnorm: need 1 <= cols <= 4096");
+    if (rows == 0) return REPOPS_OK;
+    REQ(x && w && y, "rmsnorm: null pointer");
+    return cuda_status(launch_rmsnorm(x, w, rows, cols, eps, y, rstd, S(stream)), "rmsnorm");
+}
+
+int repops_swiglu(const float *g, const float *u, int64_t n, float *h, void *stream) {
+    REQ(n >= 0, "swiglu: negative n");
+    if (n == 0) return REPOPS_OK;
+    REQ(g && u && h, "swiglu: null pointer");
+    return cuda_status(launch_swiglu(g, u, n, h, S(stream)), "swiglu");
+}
+
+int repops_rope(const float *x, int64_t ntok, int64_t nhead, int64_t hd, int64_t ld, const float *cos_t,
+                const float *sin_t, float *y, int64_t ldy, void *stream) {
+    REQ(ntok >= 0 && nhead >= 0 && hd >= 2 && hd % 2 == 0, "rope: bad shape");
+    if (ntok == 0 || nhead == 0) return REPOPS_OK;
+    REQ(x && cos_t && sin_t && y && ld >= nhead * hd && ldy >= nhead * hd, "rope: bad pointer / ld");
+    return cuda_status(launch_rope(x, ntok, nhead, hd, ld, cos_t, sin_t, y, ldy, S(stream)), "rope");
+}
+
+int repops_gather_rows(const float *table, const int32_t *idx, int64_t n, int64_t C, float *out, void *stream) {
+    REQ(n >= 0 && C >= 0, "gather_rows: negative extent");
+    if (n == 0 || C == 0) return REPOPS_OK;
+    REQ(table && idx && out, "gather_rows: null pointer");
+    return cuda_status(launch_gather_rows(table, idx, n, C, out, S(stream)), "gather_rows");
+}
+
+int repops_fill_uniform(float *out, int64_t n, uint64_t seed, double scale, void *stream) {
+    REQ(n >= 0 && (n == 0 || out), "fill_uniform: bad argument");
+    if (n == 0) return REPOPS_OK;
+    return cuda_status(launch_fill_uniform(out, n, seed, scale, S(stream)), "fill_uniform");
+}
+
+int repops_copy2d(const float *src, int64_t rows, int64_t cols, int64_t lds, float *dst, int64_t ldd, void *stream) {
+    REQ(rows >= 0 && cols >= 0, "copy2d: negative extent");
+    if (rows == 0 || cols == 0) return REPOPS_OK;
+    REQ(src && dst && lds >= cols && ldd >= cols, "copy2d: bad pointer / ld");
+    return cuda_status(launch_copy2d(src, rows, cols, lds, dst, ldd, S(stream)), "copy2d");
+}
+
 int repops_transpose(const float *x, int64_t rows, int64_t cols, int64_t ldx, float *y, int64_t ldy, void *stream) {
     REQ(rows >= 0 && cols >= 0, "transpose: negative extent");
     if (rows == 0 || cols == 0) return REPOPS_OK;

@@ -275,6 +275,99 @@ __global__ void transpose_kernel(const float *__restrict__ x, int64_t rows, int6
 }
 }  // namespace
 
+// ------------------------------------------------------------------ Llama operators (config 4)
+namespace {
+struct SwiGluF {
+    // R-SWIGLU: silu(g) * u, silu(g) = g / (1 + exp(-g)); -g is an exact sign flip
+    RO_DEV float operator()(float g, float u) const {
+        float e = ro::exp_rn(__uint_as_float(__float_as_uint(g) ^ 0x80000000u));
+        return ro::canon(__fmul_rn(__fdiv_rn(g, __fadd_rn(1.0f, e)), u));
+    }
+};
+
+// R-ROPE, rotate-half form, one thread per (token, head, i < hd/2)
+__global__ void rope_kernel(const float *__restrict__ x, int64_t ntok, int64_t nhead, int64_t hd, int64_t ld,
+                            const float *__restrict__ cosv, const float *__restrict__ sinv, float *__restrict__ y,
+                            int64_t ldy) {
+    const int64_t h = hd / 2;
+    const int64_t total = ntok * nhead * h;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = idx % h, q = (idx / h) % nhead, t = idx / (h * nhead);
+        const float c = __ldg(cosv + t * h + i), s = __ldg(sinv + t * h + i);
+        const float a = __ldg(x + t * ld + q * hd + i), b = __ldg(x + t * ld + q * hd + i + h);
+        y[t * ldy + q * hd + i] = ro::canon(__fsub_rn(__fmul_rn(a, c), __fmul_rn(b, s)));
+        y[t * ldy + q * hd + i + h] = ro::canon(__fadd_rn(__fmul_rn(b, c), __fmul_rn(a, s)));
+    }
+}
+
+__global__ void gather_rows_kernel(const float *__restrict__ table, const int32_t *__restrict__ idx, int64_t n,
+                                   int64_t C, float *__restrict__ out) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.y + threadIdx.y;
+    if (t >= n) return;
+    const float *src = table + (int64_t)__ldg(idx + t) * C;
+    for (int64_t c = threadIdx.x; c < C; c += blockDim.x) out[t * C + c] = __ldg(src + c);
+}
+
+// synthetic-input generator, bit-identical to synth.uniform: element i of stream
+// `seed` = ((splitmix64(seed + (i+1)*golden) >> 40) * 2^-23 - 1) [* scale, rounded once]
+__global__ void fill_uniform_kernel(float *__restrict__ out, int64_t n, uint64_t seed, double scale, int use_scale) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t z = seed + (uint64_t)(i + 1) * 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z = z ^ (z >> 31);
+        const double u = (double)(z >> 40) * (1.0 / 8388608.0) - 1.0;  // exact
+        const float f = (float)u;                                       // exact (24-bit grid)
+        out[i] = use_scale ? (float)((double)f * scale) : f;
+    }
+}
+}  // namespace
+
+namespace {
+__global__ void copy2d_kernel(const float *__restrict__ src, int64_t rows, int64_t cols, int64_t lds,
+                              float *__restrict__ dst, int64_t ldd) {
+    const int64_t r = blockIdx.y;
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += (int64_t)gridDim.x * blockDim.x)
+        dst[r * ldd + c] = src[r * lds + c];
+}
+}  // namespace
+
+cudaError_t launch_copy2d(const float *src, int64_t rows, int64_t cols, int64_t lds, float *dst, int64_t ldd,
+                          cudaStream_t s) {
+    if (rows == 0 || cols == 0) return cudaSuccess;
+    dim3 grid((unsigned)min((cols + 255) / 256, (int64_t)64), (unsigned)rows);
+    copy2d_kernel<<<grid, 256, 0, s>>>(src, rows, cols, lds, dst, ldd);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_swiglu(const float *g, const float *u, int64_t n, float *h, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    binary_kernel<<<ew_grid(n), 256, 0, s>>>(g, u, n, h, SwiGluF{});
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rope(const float *x, int64_t ntok, int64_t nhead, int64_t hd, int64_t ld, const float *c,
+                        const float *sn, float *y, int64_t ldy, cudaStream_t s) {
+    const int64_t total = ntok * nhead * (hd / 2);
+    if (total == 0) return cudaSuccess;
+    rope_kernel<<<ew_grid(4 * total), 256, 0, s>>>(x, ntok, nhead, hd, ld, c, sn, y, ldy);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather_rows(const float *table, const int32_t *idx, int64_t n, int64_t C, float *out,
+                               cudaStream_t s) {
+    if (n == 0 || C == 0) return cudaSuccess;
+    gather_rows_kernel<<<(unsigned)((n + 3) / 4), dim3(128, 4), 0, s>>>(table, idx, n, C, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fill_uniform(float *out, int64_t n, uint64_t seed, double scale, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    fill_uniform_kernel<<<ew_grid(4 * n), 256, 0, s>>>(out, n, seed, scale, scale != 1.0);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_transpose(const float *x, int64_t rows, int64_t cols, int64_t ldx, float *y, int64_t ldy,
                              cudaStream_t s) {
     if (rows == 0 || cols == 0) return cudaSuccess;

@@ -19,5 +19,13 @@ cudaError_t launch_embedding(const int32_t *tok, int64_t ntok, int64_t T, const 
 cudaError_t launch_embedding_backward(const int32_t *tok, int64_t ntok, int64_t T, const float *dx0, int64_t C,
                                       float *dwte, float *dwpe, cudaStream_t s);
 cudaError_t launch_flip_bit(void *data, int64_t elem, int bit, cudaStream_t s);
+cudaError_t launch_copy2d(const float *src, int64_t rows, int64_t cols, int64_t lds, float *dst, int64_t ldd,
+                          cudaStream_t s);
+cudaError_t launch_swiglu(const float *g, const float *u, int64_t n, float *h, cudaStream_t s);
+cudaError_t launch_rope(const float *x, int64_t ntok, int64_t nhead, int64_t hd, int64_t ld, const float *c,
+                        const float *sn, float *y, int64_t ldy, cudaStream_t s);
+cudaError_t launch_gather_rows(const float *table, const int32_t *idx, int64_t n, int64_t C, float *out,
+                               cudaStream_t s);
+cudaError_t launch_fill_uniform(float *out, int64_t n, uint64_t seed, double scale, cudaStream_t s);
 cudaError_t launch_transpose(const float *x, int64_t rows, int64_t cols, int64_t ldx, float *y, int64_t ldy,
                              cudaStream_t s);

@@ -323,6 +323,34 @@ __global__ void layernorm_warp(const float *__restrict__ x, const float *__restr
     }
 }
 
+// R-RMSNORM (cols <= 4096): ms = CDOT(x,x)/n; rstd = 1/sqrt(ms+eps); y = (x*rstd)*w
+__global__ void rmsnorm_warp(const float *__restrict__ x, const float *__restrict__ w, int64_t rows, int64_t cols,
+                             float eps, float *__restrict__ y, float *__restrict__ rstd) {
+    int lane = threadIdx.x & 31;
+    int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (r >= rows) return;
+    const float *xr = x + r * cols;
+    float *yr = y + r * cols;
+    const bool al = al16(xr) && al16(w) && al16(yr);
+    const float ms = __fdiv_rn(warp_cdot_tile(xr, xr, cols, lane, al), (float)cols);
+    const float rs = rsqrt_rn(__fadd_rn(ms, eps));
+    for (int64_t b = 0; b < cols; b += 128) {
+        int64_t i = b + 4 * lane;
+        float4 v = ld4(xr, i, cols, al);
+        float4 g = ld4(w, i, cols, al);
+        float o[4] = {canon(__fmul_rn(__fmul_rn(v.x, rs), g.x)), canon(__fmul_rn(__fmul_rn(v.y, rs), g.y)),
+                      canon(__fmul_rn(__fmul_rn(v.z, rs), g.z)), canon(__fmul_rn(__fmul_rn(v.w, rs), g.w))};
+        if (al && i + 3 < cols) {
+            *reinterpret_cast<float4 *>(yr + i) = make_float4(o[0], o[1], o[2], o[3]);
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (i + q < cols) yr[i + q] = o[q];
+        }
+    }
+    if (lane == 0 && rstd) rstd[r] = canon(rs);
+}
+
 __global__ void layernorm_bwd_warp(const float *__restrict__ dy, const float *__restrict__ x,
                                    const float *__restrict__ gamma, const float *__restrict__ mean,
                                    const float *__restrict__ rstd, const float *__restrict__ dres, int64_t rows,
@@ -538,6 +566,13 @@ cudaError_t launch_layernorm_params(const float *dy, const float *x, const float
     if (cols == 0 || nseg == 0) return cudaSuccess;
     dim3 grid((unsigned)((cols + FC - 1) / FC), (unsigned)nseg);
     layernorm_params_kernel<<<grid, 256, 0, s>>>(dy, x, mean, rstd, rows, cols, nseg, dg, db, ldo);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rmsnorm(const float *x, const float *w, int64_t rows, int64_t cols, float eps, float *y,
+                           float *rstd, cudaStream_t s) {
+    if (rows == 0) return cudaSuccess;
+    rmsnorm_warp<<<rows_grid(rows, 8), 256, 0, s>>>(x, w, rows, cols, eps, y, rstd);
     return cudaGetLastError();
 }
 

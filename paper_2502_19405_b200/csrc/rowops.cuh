@@ -20,5 +20,7 @@ cudaError_t launch_layernorm_backward(const float *dy, const float *x, const flo
 cudaError_t launch_layernorm_params(const float *dy, const float *x, const float *mean, const float *rstd,
                                     int64_t rows, int64_t cols, int64_t nseg, float *dg, float *db, int64_t ldo,
                                     cudaStream_t s);
+cudaError_t launch_rmsnorm(const float *x, const float *w, int64_t rows, int64_t cols, float eps, float *y,
+                           float *rstd, cudaStream_t s);
 cudaError_t launch_cross_entropy(const float *logits, int64_t rows, int64_t V, int64_t ld, const int32_t *labels,
                                  float scale, float *loss, float *dlogits, int64_t ldd, cudaStream_t s);

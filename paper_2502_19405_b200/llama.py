@@ -1,0 +1,437 @@
+"""Llama-3-8B-shaped FP32 prefill forward, tensor-parallel N-split (BASELINE config 4).
+
+RepOps forward of a Llama-3 decoder (RMSNorm, GQA attention with RoPE, SwiGLU
+MLP, untied LM head) over T prompt tokens, with every operator output
+committed and the pass's node graph hashed into a Merkle root (Verde, Fig. 2).
+
+Tensor parallelism without reordering any reduction (PAPER.md P:585-587 and
+the future-work note on model parallelism): every weight matrix is
+split along its OUTPUT (N) dimension into NB = 8 column blocks; block b is
+computed by rank b // (NB/G) with the full K.  Activations that a block's GEMM
+needs in full (attention output, SwiGLU output, the O / down projections'
+results) are all-gathered (data movement only) and placed by repops_copy2d.
+Megatron's row-parallel K split + all-reduce is never used: it would change
+the K order.  Nodes are defined per column block (G-independent), so the
+pass's root is bit-identical for G in {1, 2, 4, 8}.
+
+Node order (R13 analogue): params | tokens, RoPE tables, embedding | per layer:
+attn RMSNorm, for each block (QKV, RoPE, scores, softmax, PV), for each block
+O-proj, residual, MLP RMSNorm, for each block (gate, up, SwiGLU), for each block
+down, residual | final RMSNorm, for each block LM head.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import struct
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+import synth
+
+from . import (EPI_SCALE, CommitPlan, RootPlan, repops_add, repops_copy2d, repops_fill_uniform, repops_gather_rows,
+               repops_gemm_strided_batched, repops_rmsnorm, repops_rope, repops_softmax, repops_swiglu,
+               verde_commit_tensors)
+from ._lib import check, lib
+from .dist import all_gather_rows, gather_shard_digests, shard_block
+
+OP = dict(PARAM_IN=1, TOKENS_IN=2, TABLES_IN=3, EMBED=4, RMSNORM=5, QKV=6, ROPE=7, SCORES=8, SOFTMAX=9, PV=10,
+          OPROJ=11, RESIDUAL=12, GATE=13, UP=14, SWIGLU=15, DOWN=16, LMHEAD=17)
+REPLICATED = 0xFFFFFFFF
+
+
+@dataclass
+class LlamaConfig:
+    n_layer: int = 32
+    d: int = 4096
+    n_head: int = 32
+    n_kv: int = 8
+    hd: int = 128
+    ffn: int = 14336
+    vocab: int = 128256
+    seq: int = 2048
+    eps: float = 1e-5
+    theta: float = 500000.0
+    nb: int = 8          # tensor-parallel column blocks (one KV head each)
+    seed: int = 0
+
+    @staticmethod
+    def tiny():
+        return LlamaConfig(n_layer=2, d=128, n_head=16, n_kv=8, hd=8, ffn=256, vocab=512, seq=64)
+
+    @property
+    def qh(self):  # query heads per block
+        return self.n_head // self.nb
+
+    def check(self):
+        assert self.n_kv == self.nb and self.n_head % self.nb == 0
+        assert self.d % self.nb == 0 and self.ffn % self.nb == 0 and self.vocab % self.nb == 0
+
+
+@dataclass
+class TRef:
+    name: str
+    view: torch.Tensor
+    slot: int = -1
+    producer: int = -1
+    pslot: int = 0
+
+
+@dataclass
+class NRec:
+    index: int
+    op: int
+    block: int
+    attrs: dict
+    inputs: list
+    outputs: list
+    name: str = ""
+    dsts: list = field(default_factory=list)
+
+
+class LlamaPrefill:
+    def __init__(self, cfg: LlamaConfig, rank=0, world=1, device="cuda", pg=None, structure_only=False):
+        cfg.check()
+        self.cfg, self.rank, self.world, self.pg = cfg, rank, world, pg
+        self.structure_only = structure_only
+        self.dev = torch.device("meta" if structure_only else device)
+        self.b0, self.nbl = shard_block(rank, world, cfg.nb)
+        c = cfg
+        self.Wb = (c.qh + 2) * c.hd        # fused per-block QKV width (qh q heads, 1 k, 1 v)
+        self.Fb, self.Db, self.Vb = c.ffn // c.nb, c.d // c.nb, c.vocab // c.nb
+        self.specs = synth.llama_param_specs(c.n_layer, c.d, c.n_head, c.n_kv, c.hd, c.ffn, c.vocab)
+        self._alloc()
+        self._build()
+
+    # ------------------------------------------------------------------ weights
+    def _alloc(self):
+        c, dev, nbl, T = self.cfg, self.dev, self.nbl, self.cfg.seq
+        E = lambda *s: torch.empty(*s, dtype=torch.float32, device=dev)  # noqa: E731
+        L, d, hd, qh = c.n_layer, c.d, c.hd, c.qh
+        self.tok = torch.empty(T, dtype=torch.int32, device=dev)
+        cos, sin = synth.rope_tables(T, hd, c.theta)
+        self.cos = torch.from_numpy(cos).to(dev) if not self.structure_only else E(T, hd // 2)
+        self.sin = torch.from_numpy(sin).to(dev) if not self.structure_only else E(T, hd // 2)
+        # local weights in block layout
+        self.w = []
+        for _ in range(L):
+            self.w.append(dict(attn_norm=E(d), wqkv=E(nbl, d, self.Wb), wo=E(nbl, c.n_head * hd, self.Db),
+                               mlp_norm=E(d), wg=E(nbl, d, self.Fb), wu=E(nbl, d, self.Fb),
+                               wd=E(nbl, c.ffn, self.Db)))
+        self.tok_emb = E(c.vocab, d)
+        self.norm = E(d)
+        self.wlm = E(nbl, d, self.Vb)
+        # activations
+        self.x = [E(T, d) for _ in range(L + 1)]
+        self.act = []
+        for _ in range(L):
+            self.act.append(dict(xn=E(T, d), rs1=E(T), qkv=E(nbl, T, self.Wb), qk=E(nbl, T, (qh + 1) * hd),
+                                 S=E(nbl, qh * T, T), P=E(nbl, qh * T, T), o=E(nbl, T, qh * hd),
+                                 o_all=E(T, c.n_head * hd), op=E(nbl, T, self.Db), attn=E(T, d), h=E(T, d),
+                                 hn=E(T, d), rs2=E(T), g=E(nbl, T, self.Fb), u=E(nbl, T, self.Fb),
+                                 a=E(nbl, T, self.Fb), a_all=E(T, c.ffn), dn=E(nbl, T, self.Db), mlp=E(T, d)))
+        self.xf, self.rsf = E(T, d), E(T)
+        self.logits = E(nbl, T, self.Vb)
+
+    def load_weights(self):
+        """Generate every parameter on the device (SplitMix64, identical to synth.llama_param),
+        commit the full tensors (the model checkpoint), keep this rank's column blocks."""
+        c = self.cfg
+        self.param_digest = {}
+        d, hd, qh = c.d, c.hd, c.qh
+        for name, shape, kind in self.specs:
+            full = torch.empty(shape, dtype=torch.float32, device=self.dev)
+            if kind == "w":
+                repops_fill_uniform(full, synth.llama_param_seed(name, c.seed), synth.LLAMA_WSCALE)
+            else:
+                full.fill_(1.0)
+            slot = self.tensors[self._pin[name]].slot
+            verde_commit_tensors([full], digests=self.digests[slot:slot + 1])  # into the digest table, once
+            self._place(name, full)
+            del full
+        torch.cuda.synchronize()
+
+    def _place(self, name, full):
+        c, hd, qh = self.cfg, self.cfg.hd, self.cfg.qh
+        if name == "tok_emb":
+            self.tok_emb.copy_(full)
+            return
+        if name == "norm":
+            self.norm.copy_(full)
+            return
+        if name == "lm_head":
+            for j in range(self.nbl):
+                b = self.b0 + j
+                repops_copy2d(full[:, b * self.Vb:(b + 1) * self.Vb], self.wlm[j])
+            return
+        l, kind = name[1:].split(".", 1)
+        w = self.w[int(l)]
+        if kind in ("attn_norm", "mlp_norm"):
+            w[kind].copy_(full)
+            return
+        for j in range(self.nbl):
+            b = self.b0 + j
+            if kind == "wq":
+                repops_copy2d(full[:, b * qh * hd:(b + 1) * qh * hd], w["wqkv"][j][:, :qh * hd])
+            elif kind == "wk":
+                repops_copy2d(full[:, b * hd:(b + 1) * hd], w["wqkv"][j][:, qh * hd:(qh + 1) * hd])
+            elif kind == "wv":
+                repops_copy2d(full[:, b * hd:(b + 1) * hd], w["wqkv"][j][:, (qh + 1) * hd:])
+            elif kind == "wo":
+                repops_copy2d(full[:, b * self.Db:(b + 1) * self.Db], w["wo"][j])
+            elif kind == "w_gate":
+                repops_copy2d(full[:, b * self.Fb:(b + 1) * self.Fb], w["wg"][j])
+            elif kind == "w_up":
+                repops_copy2d(full[:, b * self.Fb:(b + 1) * self.Fb], w["wu"][j])
+            elif kind == "w_down":
+                repops_copy2d(full[:, b * self.Db:(b + 1) * self.Db], w["wd"][j])
+
+    # ------------------------------------------------------------------ program
+    def _T(self, name, view, block):
+        tid = len(self.tensors)
+        self.tensors.append(TRef(name, view))
+        (self._rep if block == REPLICATED else self._blk[block]).append(tid)
+        return tid
+
+    def _node(self, op, block, attrs, inputs, outputs, name):
+        idx = len(self.nodes)
+        self.nodes.append(NRec(idx, op, block, attrs, inputs, outputs, name))
+        for q, t in enumerate(outputs):
+            self.tensors[t].producer, self.tensors[t].pslot = idx, q
+            if block == REPLICATED or self._local(block):
+                self._cur[2].append(t)
+        return idx
+
+    def _local(self, b):
+        return self.b0 <= b < self.b0 + self.nbl
+
+    def _phase(self, name):
+        self._cur = (name, [], [])
+        self.phases.append(self._cur)
+
+    def _build(self):
+        c = self.cfg
+        L, T, d, hd, qh, nb, nbl = c.n_layer, c.seq, c.d, c.hd, c.qh, c.nb, self.nbl
+        self.tensors, self.nodes, self.phases = [], [], []
+        self._rep, self._blk = [], {b: [] for b in range(nb)}
+        dummy = torch.empty(0, device=self.dev)
+        T_, N_ = self._T, self._node
+        bv = lambda buf, b: buf[b - self.b0] if self._local(b) else dummy  # noqa: E731
+        self._phase("inputs")
+        pin = {}
+        for name, shape, kind in self.specs:
+            pin[name] = T_("param/" + name, dummy, REPLICATED)   # digest computed at load time
+            N_(OP["PARAM_IN"], REPLICATED, {}, [], [pin[name]], "in/" + name)
+        t_tok = T_("tokens", self.tok, REPLICATED)
+        N_(OP["TOKENS_IN"], REPLICATED, {}, [], [t_tok], "tokens")
+        t_cos, t_sin = T_("rope/cos", self.cos, REPLICATED), T_("rope/sin", self.sin, REPLICATED)
+        N_(OP["TABLES_IN"], REPLICATED, {1: struct.unpack("<Q", struct.pack("<d", c.theta))[0]}, [],
+           [t_cos, t_sin], "rope_tables")
+        self._launch(lambda: repops_gather_rows(self.tok_emb, self.tok, out=self.x[0]))
+        t_x = T_("x0", self.x[0], REPLICATED)
+        N_(OP["EMBED"], REPLICATED, {}, [t_tok, pin["tok_emb"]], [t_x], "embed")
+        scale = float(np.float32(1.0 / np.sqrt(hd)))
+        for l in range(L):
+            a, w, p = self.act[l], self.w[l], f"l{l}."
+            self._phase(f"layer{l}")
+            self._launch(lambda l=l, a=a, w=w: self._attn(l, a, w, scale))
+            t_xn = T_(f"l{l}/xn", a["xn"], REPLICATED)
+            t_rs1 = T_(f"l{l}/rs1", a["rs1"], REPLICATED)
+            N_(OP["RMSNORM"], REPLICATED, {1: l, 2: 1}, [t_x, pin[p + "attn_norm"]], [t_xn, t_rs1], f"l{l}/attn_norm")
+            t_o = []
+            for b in range(nb):
+                q = f"l{l}/b{b}/"
+                wins = [pin[p + "wq"], pin[p + "wk"], pin[p + "wv"]]
+                t_qkv = T_(q + "qkv", bv(a["qkv"], b), b)
+                N_(OP["QKV"], b, {1: l}, [t_xn] + wins, [t_qkv], q + "qkv")
+                t_qk = T_(q + "qk_rope", bv(a["qk"], b), b)
+                N_(OP["ROPE"], b, {1: l}, [t_qkv, t_cos, t_sin], [t_qk], q + "rope")
+                t_S = T_(q + "scores", bv(a["S"], b), b)
+                N_(OP["SCORES"], b, {1: l, 3: int(np.float32(scale).view(np.uint32))}, [t_qk], [t_S], q + "scores")
+                t_P = T_(q + "probs", bv(a["P"], b), b)
+                N_(OP["SOFTMAX"], b, {1: l, 4: 1}, [t_S], [t_P], q + "softmax")
+                t_ob = T_(q + "attn_out", bv(a["o"], b), b)
+                N_(OP["PV"], b, {1: l}, [t_P, t_qkv], [t_ob], q + "pv")
+                t_o.append(t_ob)
+            t_op = []
+            for b in range(nb):
+                q = f"l{l}/b{b}/"
+                t = T_(q + "oproj", bv(a["op"], b), b)
+                N_(OP["OPROJ"], b, {1: l}, t_o + [pin[p + "wo"]], [t], q + "oproj")
+                t_op.append(t)
+            t_h = T_(f"l{l}/h", a["h"], REPLICATED)
+            N_(OP["RESIDUAL"], REPLICATED, {1: l, 2: 1}, [t_x] + t_op, [t_h], f"l{l}/res1")
+            self._phase(f"layer{l}/mlp")
+            self._launch(lambda l=l, a=a, w=w: self._mlp(l, a, w))
+            t_hn = T_(f"l{l}/hn", a["hn"], REPLICATED)
+            t_rs2 = T_(f"l{l}/rs2", a["rs2"], REPLICATED)
+            N_(OP["RMSNORM"], REPLICATED, {1: l, 2: 2}, [t_h, pin[p + "mlp_norm"]], [t_hn, t_rs2], f"l{l}/mlp_norm")
+            t_a = []
+            for b in range(nb):
+                q = f"l{l}/b{b}/"
+                t_g = T_(q + "gate", bv(a["g"], b), b)
+                N_(OP["GATE"], b, {1: l}, [t_hn, pin[p + "w_gate"]], [t_g], q + "gate")
+                t_u = T_(q + "up", bv(a["u"], b), b)
+                N_(OP["UP"], b, {1: l}, [t_hn, pin[p + "w_up"]], [t_u], q + "up")
+                t_s = T_(q + "swiglu", bv(a["a"], b), b)
+                N_(OP["SWIGLU"], b, {1: l}, [t_g, t_u], [t_s], q + "swiglu")
+                t_a.append(t_s)
+            t_dn = []
+            for b in range(nb):
+                q = f"l{l}/b{b}/"
+                t = T_(q + "down", bv(a["dn"], b), b)
+                N_(OP["DOWN"], b, {1: l}, t_a + [pin[p + "w_down"]], [t], q + "down")
+                t_dn.append(t)
+            t_x = T_(f"x{l + 1}", self.x[l + 1], REPLICATED)
+            N_(OP["RESIDUAL"], REPLICATED, {1: l, 2: 2}, [t_h] + t_dn, [t_x], f"l{l}/res2")
+        self._phase("head")
+        self._launch(self._head)
+        t_xf = T_("xf", self.xf, REPLICATED)
+        t_rsf = T_("rsf", self.rsf, REPLICATED)
+        N_(OP["RMSNORM"], REPLICATED, {1: L, 2: 3}, [t_x, pin["norm"]], [t_xf, t_rsf], "final_norm")
+        for b in range(nb):
+            t = T_(f"b{b}/logits", bv(self.logits, b), b)
+            N_(OP["LMHEAD"], b, {}, [t_xf, pin["lm_head"]], [t], f"b{b}/lm_head")
+        self._pin = pin
+        self._finalize()
+
+    def _launch(self, fn):
+        self._cur[1].append(fn)
+
+    # ---- launches (this rank's blocks, batched)
+    def _gather_blocks(self, local, full, width):
+        """all-gather [nbl, T, width] block results and place block b at full[:, b*width:(b+1)*width]."""
+        allb = all_gather_rows(local, self.world, self.pg).reshape(self.cfg.nb, self.cfg.seq, width)
+        for b in range(self.cfg.nb):
+            repops_copy2d(allb[b], full[:, b * width:(b + 1) * width])
+
+    def _attn(self, l, a, w, scale):
+        c = self.cfg
+        T, d, hd, qh, nbl, Wb = c.seq, c.d, c.hd, c.qh, self.nbl, self.Wb
+        repops_rmsnorm(self.x[l], w["attn_norm"], c.eps, out=a["xn"], rstd=a["rs1"])
+        repops_gemm_strided_batched(a["xn"], w["wqkv"], a["qkv"], M=T, N=Wb, K=d, lda=d, ldb=Wb, ldc=Wb,
+                                    sA=(0, 0), sB=(d * Wb, 0), sC=(T * Wb, 0), batch=(nbl, 1))
+        for j in range(nbl):
+            repops_rope(a["qkv"][j][:, :(qh + 1) * hd], self.cos, self.sin, qh + 1, hd, out=a["qk"][j])
+        W2 = (qh + 1) * hd
+        repops_gemm_strided_batched(a["qk"], a["qk"], a["S"], M=T, N=T, K=hd, lda=W2, ldb=W2, ldc=T,
+                                    sA=(T * W2, hd), sB=(T * W2, 0), sC=(qh * T * T, T * T), batch=(nbl, qh),
+                                    transB=True, epi=EPI_SCALE, scale=scale, offB=qh * hd)
+        repops_softmax(a["S"].view(-1, T), causal=True, out=a["P"].view(-1, T))
+        repops_gemm_strided_batched(a["P"], a["qkv"], a["o"], M=T, N=hd, K=T, lda=T, ldb=Wb, ldc=qh * hd,
+                                    sA=(qh * T * T, T * T), sB=(T * Wb, 0), sC=(T * qh * hd, hd), batch=(nbl, qh),
+                                    offB=(qh + 1) * hd)
+        self._gather_blocks(a["o"], a["o_all"], qh * hd)
+        HD = c.n_head * hd
+        repops_gemm_strided_batched(a["o_all"], w["wo"], a["op"], M=T, N=self.Db, K=HD, lda=HD, ldb=self.Db,
+                                    ldc=self.Db, sA=(0, 0), sB=(HD * self.Db, 0), sC=(T * self.Db, 0),
+                                    batch=(nbl, 1))
+        self._gather_blocks(a["op"], a["attn"], self.Db)
+        repops_add(self.x[l], a["attn"], out=a["h"])
+
+    def _mlp(self, l, a, w):
+        c = self.cfg
+        T, d, nbl, Fb = c.seq, c.d, self.nbl, self.Fb
+        repops_rmsnorm(a["h"], w["mlp_norm"], c.eps, out=a["hn"], rstd=a["rs2"])
+        for wk, out in (("wg", "g"), ("wu", "u")):
+            repops_gemm_strided_batched(a["hn"], w[wk], a[out], M=T, N=Fb, K=d, lda=d, ldb=Fb, ldc=Fb, sA=(0, 0),
+                                        sB=(d * Fb, 0), sC=(T * Fb, 0), batch=(nbl, 1))
+        repops_swiglu(a["g"], a["u"], out=a["a"])
+        self._gather_blocks(a["a"], a["a_all"], Fb)
+        repops_gemm_strided_batched(a["a_all"], w["wd"], a["dn"], M=T, N=self.Db, K=c.ffn, lda=c.ffn, ldb=self.Db,
+                                    ldc=self.Db, sA=(0, 0), sB=(c.ffn * self.Db, 0), sC=(T * self.Db, 0),
+                                    batch=(nbl, 1))
+        self._gather_blocks(a["dn"], a["mlp"], self.Db)
+        repops_add(a["h"], a["mlp"], out=self.x[l + 1])
+
+    def _head(self):
+        c = self.cfg
+        T, d = c.seq, c.d
+        repops_rmsnorm(self.x[c.n_layer], self.norm, c.eps, out=self.xf, rstd=self.rsf)
+        repops_gemm_strided_batched(self.xf, self.wlm, self.logits, M=T, N=self.Vb, K=d, lda=d, ldb=self.Vb,
+                                    ldc=self.Vb, sA=(0, 0), sB=(d * self.Vb, 0), sC=(T * self.Vb, 0),
+                                    batch=(self.nbl, 1))
+
+    # ------------------------------------------------------------------ finalisation / running
+    def _finalize(self):
+        c = self.cfg
+        for i, t in enumerate(self._rep):
+            self.tensors[t].slot = i
+        per = len(self._blk[0])
+        assert all(len(v) == per for v in self._blk.values())
+        self.rep_slots, self.blk_slots = len(self._rep), per
+        for b in range(c.nb):
+            for i, t in enumerate(self._blk[b]):
+                self.tensors[t].slot = self.rep_slots + b * per + i
+        self.n_slots = self.rep_slots + c.nb * per
+        for nd in self.nodes:
+            for t in nd.inputs:
+                src = self.tensors[t].producer
+                if nd.index not in self.nodes[src].dsts:
+                    self.nodes[src].dsts.append(nd.index)
+        blob, offs, slots, soffs = bytearray(), [0], [], [0]
+        for nd in self.nodes:
+            keys = sorted(nd.attrs)
+            b = bytearray(b"\x4e") + struct.pack("<IHI", nd.index, nd.op, nd.block) + struct.pack("<I", len(keys))
+            for k in keys:
+                b += struct.pack("<IQ", k, nd.attrs[k])
+            b += struct.pack("<I", len(nd.inputs))
+            for t in nd.inputs:
+                b += struct.pack("<II", self.tensors[t].producer, self.tensors[t].pslot)
+            b += struct.pack("<I", len(nd.dsts)) + b"".join(struct.pack("<I", q) for q in nd.dsts)
+            b += struct.pack("<I", len(nd.outputs))
+            blob += b
+            offs.append(len(blob))
+            slots += [self.tensors[t].slot for t in nd.inputs + nd.outputs]
+            soffs.append(len(slots))
+        self.node_blob = np.frombuffer(bytes(blob), np.uint8).copy()
+        self.node_offs = np.asarray(offs, np.int64)
+        self.node_slots = np.asarray(slots, np.int64)
+        self.node_soffs = np.asarray(soffs, np.int64)
+        if self.structure_only:
+            return
+        self.digests = torch.zeros((self.n_slots, 32), dtype=torch.uint8, device=self.dev)
+        self.plans = []
+        for name, fns, tids in self.phases:
+            tids = [t for t in tids if self.tensors[t].view.numel() > 0 or t == -1]
+            tids = [t for t in tids if not self.tensors[t].name.startswith("param/")]
+            self.plans.append(CommitPlan([self.tensors[t].view for t in tids],
+                                         [self.digests[self.tensors[t].slot] for t in tids]) if tids else None)
+        self.root_plan = RootPlan(self.node_blob, self.node_offs, self.node_slots, self.node_soffs, self.digests)
+        self.root_host = torch.zeros(32, dtype=torch.uint8).pin_memory()
+        self.side = torch.cuda.Stream(device=self.dev)
+        self.commit_bytes = sum(p.nbytes for p in self.plans if p is not None)
+
+    def set_tokens(self, host_tokens=None):
+        c = self.cfg
+        if host_tokens is None:
+            host_tokens = synth.llama_tokens(c.vocab, c.seq, c.seed)
+        self.tok.copy_(torch.as_tensor(np.ascontiguousarray(host_tokens, dtype=np.int32)))
+
+    def run(self, commit=True):
+        """One prefill pass; commits of each phase run on a side stream (overlap)."""
+        main = torch.cuda.current_stream()
+        side = self.side   # parameter digests were written into the table at load time
+        side.wait_stream(main)
+        for (name, fns, _), plan in zip(self.phases, self.plans):
+            for fn in fns:
+                fn()
+            if commit and plan is not None:
+                side.wait_stream(main)
+                plan.run(stream=side)
+        main.wait_stream(side)
+
+    def device_root(self):
+        gather_shard_digests(self.digests, self.rep_slots, self.blk_slots, self.b0, self.nbl, self.world, self.pg)
+        self.root_plan.run()
+        self.root_host.copy_(self.root_plan.root, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return bytes(self.root_host.numpy())
+
+    def flops(self):
+        c = self.cfg
+        T, d, hd = c.seq, c.d, c.hd
+        lin = 2 * T * d * (c.n_head * hd + 2 * c.n_kv * hd) + 2 * T * c.n_head * hd * d + 3 * 2 * T * d * c.ffn
+        attn = 2 * 2 * c.n_head * T * T * hd
+        return c.n_layer * (lin + attn) + 2 * T * d * c.vocab

@@ -106,3 +106,40 @@ def gpt2_param(name, shape, kind, seed=0):
 def gpt2_tokens(vocab, seq, shard, step=0, seed=0):
     """seq+1 tokens of one shard (one sequence); input = [:-1], target = [1:]."""
     return integers(seed_for("gpt2-tokens", seed, step, shard), seq + 1, vocab)
+
+
+# ----------------------------------------------------------------- Llama-3-8B-shaped prefill (config 4)
+def llama_param_specs(n_layer, d, n_head, n_kv, hd, ffn, vocab):
+    """(name, shape, kind) in canonical order; weights stored [in, out] (y = x W)."""
+    specs = [("tok_emb", (vocab, d), "w")]
+    for l in range(n_layer):
+        p = f"l{l}."
+        specs += [(p + "attn_norm", (d,), "g"), (p + "wq", (d, n_head * hd), "w"), (p + "wk", (d, n_kv * hd), "w"),
+                  (p + "wv", (d, n_kv * hd), "w"), (p + "wo", (n_head * hd, d), "w"), (p + "mlp_norm", (d,), "g"),
+                  (p + "w_gate", (d, ffn), "w"), (p + "w_up", (d, ffn), "w"), (p + "w_down", (ffn, d), "w")]
+    specs += [("norm", (d,), "g"), ("lm_head", (d, vocab), "w")]
+    return specs
+
+
+def llama_param_seed(name, seed=0):
+    return seed_for("llama", seed, name)
+
+
+LLAMA_WSCALE = 0.034641016151377546  # U[-a, a), std 0.02
+
+
+def llama_param(name, shape, kind, seed=0):
+    if kind == "w":
+        return uniform(llama_param_seed(name, seed), shape, LLAMA_WSCALE)
+    return np.ones(shape, np.float32)
+
+
+def llama_tokens(vocab, seq, seed=0):
+    return integers(seed_for("llama-tokens", seed), seq, vocab)
+
+
+def rope_tables(seq, hd, theta=500000.0):
+    """cos/sin tables [seq, hd/2] (float64 angles rounded once to binary32): input data."""
+    inv = theta ** (-np.arange(0, hd, 2, dtype=np.float64) / hd)
+    ang = np.arange(seq, dtype=np.float64)[:, None] * inv[None, :]
+    return np.cos(ang).astype(np.float32), np.sin(ang).astype(np.float32)

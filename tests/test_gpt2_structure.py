@@ -62,6 +62,20 @@ def test_graph_is_topological_and_single_producer(ref_graph):
         assert [st.nodes[st.tensors[t].producer].shard for t in nd.inputs] == list(range(8))
 
 
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_llama_tp_graph_identical_for_every_degree(world):
+    from paper_2502_19405_b200.llama import LlamaConfig, LlamaPrefill
+    ref = LlamaPrefill(LlamaConfig(), structure_only=True)
+    assert len(ref.nodes) == 2991
+    for rank in range(world):
+        st = LlamaPrefill(LlamaConfig(), rank=rank, world=world, structure_only=True)
+        assert np.array_equal(st.node_blob, ref.node_blob) and np.array_equal(st.node_slots, ref.node_slots)
+    # 8,030,261,248 parameters (Llama-3-8B)
+    import synth as S
+    specs = S.llama_param_specs(32, 4096, 32, 8, 128, 14336, 128256)
+    assert sum(int(np.prod(s)) for _, s, _ in specs) == 8_030_261_248
+
+
 def test_shard_block_rules():
     assert D.shard_block(3, 4, 8) == (6, 2)
     with pytest.raises(ValueError):
