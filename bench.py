@@ -211,6 +211,31 @@ class GPT2Train:
         return 32 + 4  # step root + loss
 
 
+class LlamaPrefillBench:
+    """BASELINE config 4: Llama-3-8B-shaped FP32 prefill, 2048 tokens, TP N-split over the
+    N GPUs (8 column blocks), every operator output committed, pass root on the GPU."""
+
+    def __init__(self, rank, world, device, pg=None):
+        from paper_2502_19405_b200.llama import LlamaConfig, LlamaPrefill
+        self.st = LlamaPrefill(LlamaConfig(), rank=rank, world=world, device=device, pg=pg)
+        self.st.load_weights()
+        self.st.set_tokens()
+        self.flops = self.st.flops()
+        self.root = None
+
+    def step(self):
+        self.st.run()
+        self.root = self.st.device_root()
+
+    def e2e_step(self):
+        self.st.set_tokens()
+        self.step()
+        return self.root
+
+    h2d_bytes = 2048 * 4
+    d2h_bytes = 32
+
+
 # ---------------------------------------------------------------------- oracle legs
 def oracle_sample_gemm(seconds_target=10.0):
     """The oracle (as it stands) on a bounded sample of the GEMM sweep: the first r
@@ -354,29 +379,37 @@ def main():
     hbm = measured_hbm_gbs()
     out = {"metric": METRIC}
     results = {}
-    order = [args.workload] + ([] if args.no_sweep else [w for w in ("gemm",) if w != args.workload])
+    order = [args.workload] + ([] if args.no_sweep else [w for w in ("gemm", "llama") if w != args.workload])
     for wname in order:
-        wl = (GPT2Train(rank, world, device, commit=not args.no_commit, overlap=not args.no_overlap)
-              if wname == "gpt2" else GemmSweep(rank, world, device))
-        for _ in range(args.warmup):
+        if wname == "gpt2":
+            wl = GPT2Train(rank, world, device, commit=not args.no_commit, overlap=not args.no_overlap)
+        elif wname == "gemm":
+            wl = GemmSweep(rank, world, device)
+        else:
+            wl = LlamaPrefillBench(rank, world, device)
+        head_wl = wname == args.workload
+        steps = args.steps if head_wl else max(2, min(args.steps, 3))
+        for _ in range(args.warmup if head_wl else 1):
             wl.step()
         torch.cuda.synchronize()
-        ms, tot, launches, clk = timed(wl, args.steps, world, local)
-        e2e_s = e2e(wl, args.steps, world)
+        ms, tot, launches, clk = timed(wl, steps, world, local)
+        e2e_s = e2e(wl, steps, world) if head_wl else ms * 1e-3
         gemm_ms, gemm_flops, gemm_n = tot.get("gemm", (0.0, 0, 0))
         gemm_ms = max_over_ranks(gemm_ms, world)
         peak = fp32_peak_tflops(clk["sm_max_mhz"] or 1965.0)
         achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms else 0.0   # per GPU
         res = dict(ms=ms, value=wl.flops / (ms * 1e-3) / 1e12, launches=launches, clk=clk, e2e_s=e2e_s,
-                   e2e_value=wl.flops / e2e_s / 1e12, gemm=(achieved, peak, gemm_ms / args.steps, gemm_n // args.steps),
+                   e2e_value=wl.flops / e2e_s / 1e12, gemm=(achieved, peak, gemm_ms / steps, gemm_n // steps),
                    h2d=wl.h2d_bytes, d2h=wl.d2h_bytes)
         if "commit" in tot:
             c_ms, c_bytes, c_n = tot["commit"]
-            res["commit"] = dict(gbs=c_bytes / (c_ms * 1e-3) / 1e9, ms_per_step=c_ms / args.steps,
-                                 gb_per_step=c_bytes / args.steps / 1e9, plans_per_step=c_n // args.steps)
+            res["commit"] = dict(gbs=c_bytes / (c_ms * 1e-3) / 1e9, ms_per_step=c_ms / steps,
+                                 gb_per_step=c_bytes / steps / 1e9, plans_per_step=c_n // steps)
         if wname == "gpt2":
             res["root"] = wl.root.hex()
             res["loss"] = wl.st.loss()
+        elif wname == "llama":
+            res["root"] = wl.root.hex()
         else:
             res["digests"] = wl.digests()
         results[wname] = res
@@ -426,10 +459,14 @@ def main():
                           "the step, D2H of the committed result (max over ranks)"}
     for other, res in results.items():
         if other != args.workload:
-            out[other + "_sweep" if other == "gemm" else other] = {
-                "value": res["value"], "unit": "TFLOP/s", "ms_per_step": res["ms"],
-                "gemm_roofline_frac": res["gemm"][0] / res["gemm"][1], "digests": res.get("digests"),
-                "commit": res.get("commit")}
+            key = {"gemm": "gemm_sweep", "llama": "llama_prefill", "gpt2": "gpt2_step"}[other]
+            out[key] = {"value": res["value"], "unit": "TFLOP/s", "ms_per_step": res["ms"],
+                        "gemm_tflops": res["gemm"][0], "gemm_roofline_frac": res["gemm"][0] / res["gemm"][1],
+                        "digests": res.get("digests"), "root": res.get("root"), "commit": res.get("commit"),
+                        "config": {"gemm": "square n=1024..8192, M-split, each output committed",
+                                   "llama": "Llama-3-8B-shaped FP32 prefill, 2048 tokens, 32 layers, TP N-split "
+                                            f"over {world} GPU(s) (8 column blocks), every output committed",
+                                   "gpt2": "GPT-2 124M train step"}[other]}
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         try:
