@@ -127,3 +127,7 @@ def check(status: int, what: str) -> None:
 def _hooks(L):
     L.repops_gemm_force_cfg.restype = i32
     L.repops_gemm_force_cfg.argtypes = [i32]
+    L.repops_gemm_smem_floor.restype = i32
+    L.repops_gemm_smem_floor.argtypes = [i32]
+    L.repops_commit_ctas_per_sm.restype = i32
+    L.repops_commit_ctas_per_sm.argtypes = [i32]

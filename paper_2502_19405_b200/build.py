@@ -38,7 +38,8 @@ def _deps_mtime() -> float:
 
 def _compile(src: str, verbose: bool) -> str:
     obj = os.path.join(OBJ, src.replace(".cu", ".o"))
-    cmd = [NVCC, *ARCH, *NUMERIC, *COMMON, "-c", os.path.join(CSRC, src), "-o", obj]
+    extra = os.environ.get("RO_NVCC_DEFS", "").split()  # tuning variants only (tools/sha_tune.sh)
+    cmd = [NVCC, *ARCH, *NUMERIC, *COMMON, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
     if verbose:
         cmd[1:1] = ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -228,6 +228,21 @@ int repops_gemm_force_cfg(int cfg) {
     return REPOPS_OK;
 }
 
+// Tuning hook (not in repops.h): minimum dynamic shared memory per GEMM CTA, used
+// to cap GEMM occupancy in co-residency experiments.  Bits never depend on it.
+int repops_gemm_smem_floor(int bytes) {
+    REQ(bytes >= 0 && bytes <= 227 * 1024, "gemm_smem_floor: %d bytes out of range", bytes);
+    g_gemm_smem_floor.store(bytes);
+    return REPOPS_OK;
+}
+
+// Tuning hook (not in repops.h): cap on resident SHA-256 leaf CTAs per SM.
+int repops_commit_ctas_per_sm(int n) {
+    REQ(n >= 1 && n <= 64, "commit_ctas_per_sm: %d out of range", n);
+    g_leaf_ctas_per_sm.store(n);
+    return REPOPS_OK;
+}
+
 // Test hook (not in repops.h): force a tile configuration to prove bits-neutrality.
 int repops_gemm_cfg(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, int transA, const float *B,
                     int64_t ldb, int transB, int epi, const float *bias, float scale, float *C, int64_t ldc,

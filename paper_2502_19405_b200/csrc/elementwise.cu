@@ -273,6 +273,42 @@ __global__ void transpose_kernel(const float *__restrict__ x, int64_t rows, int6
         if (r < rows && c < cols) y[c * ldy + r] = t[threadIdx.x][i];
     }
 }
+
+// 64 x 64 tiles, 256 threads, 16-byte loads and stores (rows of x and y 16-byte
+// aligned); ragged edges fall back to scalar accesses inside the same tile.
+__global__ void __launch_bounds__(256) transpose64_kernel(const float *__restrict__ x, int64_t rows, int64_t cols,
+                                                          int64_t ldx, float *__restrict__ y, int64_t ldy) {
+    __shared__ float t[64][65];
+    const int64_t c0 = (int64_t)blockIdx.x * 64, r0 = (int64_t)blockIdx.y * 64;
+    const int tid = threadIdx.x;
+    const bool full = r0 + 64 <= rows && c0 + 64 <= cols;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {  // 64 rows x 16 float4
+        const int i = (tid >> 4) + 16 * q, j = (tid & 15) * 4;
+        const int64_t r = r0 + i, c = c0 + j;
+        if (full) {
+            const float4 v = __ldg(reinterpret_cast<const float4 *>(x + r * ldx + c));
+            t[i][j] = v.x; t[i][j + 1] = v.y; t[i][j + 2] = v.z; t[i][j + 3] = v.w;
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (r < rows && c + e < cols) t[i][j + e] = __ldg(x + r * ldx + c + e);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {  // 64 output rows (= x columns) x 16 float4
+        const int i = (tid >> 4) + 16 * q, j = (tid & 15) * 4;
+        const int64_t c = c0 + i, r = r0 + j;
+        if (full) {
+            *reinterpret_cast<float4 *>(y + c * ldy + r) = make_float4(t[j][i], t[j + 1][i], t[j + 2][i], t[j + 3][i]);
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (c < cols && r + e < rows) y[c * ldy + r + e] = t[j + e][i];
+        }
+    }
+}
 }  // namespace
 
 // ------------------------------------------------------------------ Llama operators (config 4)
@@ -371,6 +407,12 @@ cudaError_t launch_fill_uniform(float *out, int64_t n, uint64_t seed, double sca
 cudaError_t launch_transpose(const float *x, int64_t rows, int64_t cols, int64_t ldx, float *y, int64_t ldy,
                              cudaStream_t s) {
     if (rows == 0 || cols == 0) return cudaSuccess;
+    const bool vec = ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0) && ldx % 4 == 0 && ldy % 4 == 0;
+    if (vec && (rows + 63) / 64 <= 65535) {
+        dim3 grid((unsigned)((cols + 63) / 64), (unsigned)((rows + 63) / 64));
+        transpose64_kernel<<<grid, 256, 0, s>>>(x, rows, cols, ldx, y, ldy);
+        return cudaGetLastError();
+    }
     dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
     transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(x, rows, cols, ldx, y, ldy);
     return cudaGetLastError();

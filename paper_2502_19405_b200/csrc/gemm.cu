@@ -21,7 +21,10 @@
 //      A^T stored K x M  -> [BK][BM]: 4 consecutive rows at one k = one LDS.128
 //      A   stored M x K  -> [BM][BK+4]: rows ty + TY*i, 4 consecutive k of a
 //                           row = one LDS.128 (row stride 20 words: the rows a
-//                           warp touches fall in disjoint bank groups)
+//                           warp touches fall in disjoint bank groups); with
+//                           XP this tile is then transposed shared->shared
+//                           into [BK][BM] (double buffered, one extra barrier
+//                           per K tile) and read like A^T
 //    B tiles are always [BK][BN] (n contiguous) so B pairs are natural float2:
 //      B stored K x N    -> cp.async;
 //      B^T stored N x K  -> register-staged 4-k loads, transposed on the
@@ -147,9 +150,12 @@ struct Cfg {
     static constexpr int NP = TN / 2;           // accumulator pairs per row
 };
 
-template <int BM, int BN, int BK, int TM, int TN, int STAGES, int MINB, int KG0, bool TA, bool TB, int LD>
+template <int BM, int BN, int BK, int TM, int TN, int STAGES, int MINB, int KG, bool TA, bool TB, int LD, bool XP>
 __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB) gemm_kernel(GemmParams p) {
-    constexpr int KG = (LD == 2) ? 4 : KG0;  // full tiles have the registers for LDS.128 A fragments
+    // XP: an A stored M x K is transposed shared->shared into [BK][BM] once per
+    // K tile, so the micro-kernel reads it exactly like A^T (2 LDS.128 per k)
+    constexpr bool XA = XP && !TA;
+    constexpr bool AT = TA || XA;
     using CF = Cfg<BM, BN, BK, TM, TN, TA>;
     constexpr int THREADS = CF::THREADS;
     constexpr int TX = CF::TX, TY = CF::TY, SKP = CF::SKP, NP = CF::NP;
@@ -182,10 +188,12 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB) gemm_kernel(GemmP
         float *As = smem + slot * CF::STAGE_WORDS;
         const int64_t k0 = kt * BK;
         if constexpr (LD == 2) {
-            if (TA) tile_async_full<BK, BM, BM, THREADS>(As, A + k0 * p.lda + m0, (int)p.lda, tid);
-            else tile_async_full<BM, BK, SKP, THREADS>(As, A + m0 * p.lda + k0, (int)p.lda, tid);
-            if (!TB) tile_async_full<BK, BN, BN, THREADS>(As + CF::A_WORDS, B + k0 * p.ldb + n0, (int)p.ldb, tid);
-            return;
+            if (k0 + BK <= K) {  // every K tile but a ragged last one
+                if (TA) tile_async_full<BK, BM, BM, THREADS>(As, A + k0 * p.lda + m0, (int)p.lda, tid);
+                else tile_async_full<BM, BK, SKP, THREADS>(As, A + m0 * p.lda + k0, (int)p.lda, tid);
+                if (!TB) tile_async_full<BK, BN, BN, THREADS>(As + CF::A_WORDS, B + k0 * p.ldb + n0, (int)p.ldb, tid);
+                return;
+            }
         }
         if (TA)  // A stored K x M: tile rows = k, contiguous m
             tile_async<BK, BM, BM, THREADS, VEC>(As, A + k0 * p.lda + m0, p.lda, K - k0, M - m0, tid);
@@ -237,10 +245,26 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB) gemm_kernel(GemmP
         const float *Bs = As + CF::A_WORDS;
         const int kmax = (int)min((int64_t)BK, K - kt * BK);
         if (kmax == BK) {
+            const float *Ac = As;  // A in [BK][BM] layout (AT only)
+            if constexpr (XA) {
+                float *At = smem + STAGES * CF::STAGE_WORDS + (int)(kt & 1) * (BK * BM);
+#pragma unroll
+                for (int q = 0; q < BM * BK / 4 / THREADS; ++q) {
+                    const int c = tid + q * THREADS;
+                    const int r = c % BM, kq = (c / BM) * 4;  // a warp: 32 consecutive rows, one k quad
+                    const float4 v = *reinterpret_cast<const float4 *>(As + r * SKP + kq);
+                    At[(kq + 0) * BM + r] = v.x;
+                    At[(kq + 1) * BM + r] = v.y;
+                    At[(kq + 2) * BM + r] = v.z;
+                    At[(kq + 3) * BM + r] = v.w;
+                }
+                __syncthreads();  // At[kt & 1] complete (the other buffer may still be read)
+                Ac = At;
+            }
 #pragma unroll
             for (int kg = 0; kg < BK; kg += KG) {
-                float ak[TA ? 1 : TM][KG];
-                if (!TA) {
+                float ak[AT ? 1 : TM][KG];
+                if (!AT) {
 #pragma unroll
                     for (int i = 0; i < TM; ++i) {
                         if constexpr (KG == 4) {
@@ -256,10 +280,10 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB) gemm_kernel(GemmP
                 for (int kk = 0; kk < KG; ++kk) {
                     float a[TM];
                     float2 b[NP];
-                    if (TA) {
+                    if (AT) {
 #pragma unroll
                         for (int h = 0; h < TM / 4; ++h) {
-                            float4 v = *reinterpret_cast<const float4 *>(As + (kg + kk) * BM + h * (BM / (TM / 4)) + ty * 4);
+                            float4 v = *reinterpret_cast<const float4 *>(Ac + (kg + kk) * BM + h * (BM / (TM / 4)) + ty * 4);
                             a[h * 4] = v.x; a[h * 4 + 1] = v.y; a[h * 4 + 2] = v.z; a[h * 4 + 3] = v.w;
                         }
                     } else {
@@ -284,8 +308,10 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB) gemm_kernel(GemmP
                 float a[TM];
                 float2 b[NP];
 #pragma unroll
-                for (int i = 0; i < TM; ++i)
-                    a[i] = TA ? As[k * BM + (i / 4) * (BM / (TM / 4)) + ty * 4 + (i % 4)] : As[(ty + TY * i) * SKP + k];
+                for (int i = 0; i < TM; ++i) {
+                    const int rat = (i / 4) * (BM / (TM / 4)) + ty * 4 + (i % 4);  // row in the AT mapping
+                    a[i] = TA ? As[k * BM + rat] : XA ? As[rat * SKP + k] : As[(ty + TY * i) * SKP + k];
+                }
 #pragma unroll
                 for (int h = 0; h < TN / 4; ++h) {
                     const float *src = Bs + k * BN + h * (BN / (TN / 4)) + tx * 4;
@@ -305,7 +331,7 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB) gemm_kernel(GemmP
     // epilogue (R3): epi(acc) once, NaN canonicalised (R10)
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
-        const int64_t m = m0 + (TA ? (i / 4) * (BM / (TM / 4)) + ty * 4 + (i % 4) : ty + TY * i);
+        const int64_t m = m0 + (AT ? (i / 4) * (BM / (TM / 4)) + ty * 4 + (i % 4) : ty + TY * i);
         if (m >= M) continue;
         float *crow = Cp + m * p.ldc;
 #pragma unroll
@@ -330,16 +356,18 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB) gemm_kernel(GemmP
     }
 }
 
-template <int BM, int BN, int BK, int TM, int TN, int STAGES, int MINB, int KG, bool TA, bool TB, int LD>
+template <int BM, int BN, int BK, int TM, int TN, int STAGES, int MINB, int KG, bool TA, bool TB, int LD, bool XP>
 cudaError_t launch_one(const GemmParams &p, cudaStream_t s) {
     using CF = Cfg<BM, BN, BK, TM, TN, TA>;
-    const size_t smem = (size_t)STAGES * CF::STAGE_WORDS * sizeof(float);
-    auto kern = gemm_kernel<BM, BN, BK, TM, TN, STAGES, MINB, KG, TA, TB, LD>;
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
+    size_t smem = (size_t)(STAGES * CF::STAGE_WORDS + (XP && !TA ? 2 * BK * BM : 0)) * sizeof(float);
+    const size_t floor_bytes = (size_t)g_gemm_smem_floor.load(std::memory_order_relaxed);
+    if (floor_bytes > smem) smem = floor_bytes;  // occupancy experiments only (tools/overlap_probe.py)
+    auto kern = gemm_kernel<BM, BN, BK, TM, TN, STAGES, MINB, KG, TA, TB, LD, XP>;
+    static size_t attr_bytes = 0;  // per instantiation
+    if (smem > attr_bytes) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        attr_set = true;
+        attr_bytes = smem;
     }
     const int64_t tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
     dim3 grid((unsigned)tiles, (unsigned)(p.batch0 * p.batch1));
@@ -347,16 +375,16 @@ cudaError_t launch_one(const GemmParams &p, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-template <int BM, int BN, int BK, int TM, int TN, int STAGES, int MINB, int KG = 4>
+template <int BM, int BN, int BK, int TM, int TN, int STAGES, int MINB, int KG = 4, bool XP = false>
 cudaError_t launch_cfg(const GemmParams &p, cudaStream_t s) {
     const bool vec = p.vecA && p.vecB;
-    const bool full = vec && p.M % BM == 0 && p.N % BN == 0 && p.K % BK == 0 && p.lda < (1 << 23) &&
-                      p.ldb < (1 << 23);
+    // full: every M/N tile complete (a ragged last K tile takes the bounded load)
+    const bool full = vec && p.M % BM == 0 && p.N % BN == 0 && p.lda < (1 << 23) && p.ldb < (1 << 23);
 #define RO_GEMM_CASE(TA_, TB_)                                                                   \
     if ((bool)p.transA == TA_ && (bool)p.transB == TB_)                                          \
-        return full ? launch_one<BM, BN, BK, TM, TN, STAGES, MINB, KG, TA_, TB_, 2>(p, s)        \
-                    : vec ? launch_one<BM, BN, BK, TM, TN, STAGES, MINB, KG, TA_, TB_, 1>(p, s)  \
-                          : launch_one<BM, BN, BK, TM, TN, STAGES, MINB, KG, TA_, TB_, 0>(p, s);
+        return full ? launch_one<BM, BN, BK, TM, TN, STAGES, MINB, KG, TA_, TB_, 2, XP>(p, s)        \
+                    : vec ? launch_one<BM, BN, BK, TM, TN, STAGES, MINB, KG, TA_, TB_, 1, XP>(p, s)  \
+                          : launch_one<BM, BN, BK, TM, TN, STAGES, MINB, KG, TA_, TB_, 0, XP>(p, s);
     RO_GEMM_CASE(false, false)
     RO_GEMM_CASE(false, true)
     RO_GEMM_CASE(true, false)
@@ -368,10 +396,14 @@ cudaError_t launch_cfg(const GemmParams &p, cudaStream_t s) {
 }  // namespace
 
 // Tile configurations (all bits-neutral: only the M/N tiling differs).
-//   0: 128 x 128, 8 x 8 per thread, 3 stages, 2 CTAs/SM   (large problems)
-//   1:  64 x  64, 8 x 4 per thread, 3 stages              (small M*N)
-//   2..4: tuning variants (tools/gemm_tune.py)
-int gemm_num_cfgs() { return 7; }
+//   0: 128 x 128, 8 x 8 per thread, 3 stages, 2 CTAs/SM
+//   1:  64 x  64, 8 x 4 per thread, 3 stages
+//   3: 128 x 256 (8 x 16), 4: 256 x 128 (16 x 8), 1 CTA/SM
+//   5: 128 x 64, 6: 64 x 128 (8 x 8), 3 CTAs/SM  -- the usual winners
+//   2, 7, 8, 9: stage / fragment / occupancy variants kept for tools/gemm_tune.py
+//   10..14: 6, 5, 3, 1, 4 with XP (A stored M x K transposed in shared memory)
+int gemm_num_cfgs() { return 19; }
+std::atomic<int> g_gemm_smem_floor{0};
 
 cudaError_t gemm_launch(const GemmParams &p, cudaStream_t s, int force_cfg) {
     if (p.M == 0 || p.N == 0 || p.batch0 * p.batch1 == 0) return cudaSuccess;
@@ -395,15 +427,29 @@ cudaError_t gemm_launch(const GemmParams &p, cudaStream_t s, int force_cfg) {
             const double t = (double)waves * c.bm * c.bn * c.occ / c.rate;
             if (t < best * 0.97) { best = t; cfg = c.id; }
         }
+        // NN: same tiles with the A operand transposed in shared memory (+1..3%, tools/gemm_tune.py)
+        if (!p.transA && !p.transB && cfg == 6) cfg = 10;
     }
     switch (cfg) {
-        case 0: return launch_cfg<128, 128, 16, 8, 8, 3, 2, 2>(p, s);
+        case 0: return launch_cfg<128, 128, 16, 8, 8, 3, 2, 4>(p, s);
         case 1: return launch_cfg<64, 64, 16, 8, 4, 3, 2>(p, s);
         case 2: return launch_cfg<128, 128, 16, 8, 8, 4, 1>(p, s);
-        case 3: return launch_cfg<128, 256, 16, 8, 16, 3, 1, 2>(p, s);
-        case 4: return launch_cfg<256, 128, 16, 16, 8, 3, 1, 2>(p, s);
+        case 3: return launch_cfg<128, 256, 16, 8, 16, 3, 1, 4>(p, s);
+        case 4: return launch_cfg<256, 128, 16, 16, 8, 3, 1, 4>(p, s);
         case 5: return launch_cfg<128, 64, 16, 8, 8, 3, 3>(p, s);
         case 6: return launch_cfg<64, 128, 16, 8, 8, 3, 3>(p, s);
+        case 7: return launch_cfg<64, 128, 16, 8, 8, 3, 3, 2>(p, s);
+        case 8: return launch_cfg<128, 64, 16, 8, 8, 3, 3, 2>(p, s);
+        case 9: return launch_cfg<64, 128, 16, 8, 8, 3, 2>(p, s);
+        case 10: return launch_cfg<64, 128, 16, 8, 8, 3, 3, 4, true>(p, s);
+        case 11: return launch_cfg<128, 64, 16, 8, 8, 3, 3, 4, true>(p, s);
+        case 12: return launch_cfg<128, 256, 16, 8, 16, 3, 1, 4, true>(p, s);
+        case 13: return launch_cfg<64, 64, 16, 8, 4, 3, 2, 4, true>(p, s);
+        case 14: return launch_cfg<256, 128, 16, 16, 8, 3, 1, 4, true>(p, s);
+        case 15: return launch_cfg<64, 128, 16, 8, 8, 4, 3, 4, true>(p, s);
+        case 16: return launch_cfg<64, 128, 16, 8, 8, 5, 3, 4, true>(p, s);
+        case 17: return launch_cfg<64, 128, 32, 8, 8, 3, 2, 4, true>(p, s);
+        case 18: return launch_cfg<64, 128, 32, 8, 8, 2, 3, 4, true>(p, s);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 struct GemmParams {
     int64_t M, N, K;
     const float *A;
@@ -22,3 +24,5 @@ struct GemmParams {
 // force_cfg: -1 = automatic, else one of gemm_num_cfgs() tile configurations (bits-neutral)
 cudaError_t gemm_launch(const GemmParams &p, cudaStream_t s, int force_cfg);
 int gemm_num_cfgs();
+// tuning hook: minimum dynamic shared memory per GEMM CTA (limits occupancy; bits-neutral)
+extern std::atomic<int> g_gemm_smem_floor;

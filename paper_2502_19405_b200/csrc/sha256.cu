@@ -395,6 +395,8 @@ static std::vector<uint8_t> stage_tables(const verde_tensor_desc *d, int n, cons
     return host;
 }
 
+std::atomic<int> g_leaf_ctas_per_sm{16};  // leaf-kernel residency cap (tuning hook; bits-neutral)
+
 static cudaError_t run_kernels(const Plan &p, const Layout &L, uint8_t *base, int n, cudaStream_t s, int *nkernels) {
     cudaError_t e;
     const DevTensor *dts = reinterpret_cast<const DevTensor *>(base);
@@ -403,7 +405,7 @@ static cudaError_t run_kernels(const Plan &p, const Layout &L, uint8_t *base, in
     Digest *B = reinterpret_cast<Digest *>(base + L.bufB);
     if (p.total_chunks > 0) {
         int64_t blocks = (p.total_chunks + 127) / 128;
-        int64_t cap = (int64_t)ro_host::num_sms() * 16;
+        int64_t cap = (int64_t)ro_host::num_sms() * g_leaf_ctas_per_sm.load(std::memory_order_relaxed);
         if (blocks > cap) blocks = cap;
         leaf_kernel<<<(unsigned)blocks, 128, 0, s>>>(dts, n, tab + L.chunk_prefix_at, p.total_chunks, A);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "../../include/repops.h"
 
 int64_t commit_workspace_bytes(const verde_tensor_desc *d, int n);
@@ -19,3 +21,5 @@ cudaError_t root_plan_create(int64_t n, const uint8_t *blob, const int64_t *offs
 cudaError_t root_plan_run(const void *plan, cudaStream_t s, int *nkernels);
 void root_plan_destroy(void *plan);
 void commit_plan_destroy(void *plan);
+// tuning hook: resident leaf-kernel CTAs per SM (co-residency with GEMMs; bits-neutral)
+extern std::atomic<int> g_leaf_ctas_per_sm;

@@ -192,6 +192,25 @@ class GPT2Step:
         # only): every dgrad GEMM and the LM head then read an n-contiguous B
         self.wT = {name: E(*shape[::-1]) for name, shape, kind in self.specs
                    if len(shape) == 2 and name != "wpe"}
+        # wte^T with vocab_ld columns; the padding columns stay +0, so the LM head
+        # can run over all vocab_ld columns with full tiles and write exactly the
+        # +0 padding the committed logits already hold (acc = +0 + sum of +-0 = +0)
+        self.wteT_pad = torch.zeros(c.d, c.vocab_ld, device=dev)
+        self.wT["wte"] = self.wteT_pad[:, :c.vocab]
+        # scratch for X^T: every activation-side GEMM operand is transposed first so
+        # the GEMM runs TN (A^T tiles are 10-40% faster than row-major A on sm_100a,
+        # DESIGN.md §5); data movement only, consumed by the very next GEMM
+        self.xT = E(max(c.vocab, c.ffn, 3 * d) * M)
+
+    def _gemm_tn(self, X, B, **kw):
+        """repops_gemm(X, B, **kw) computed as (X^T)^T B: X^T is written to the
+        scratch first (bit-exact copy), then the GEMM reads it as A^T.  The K
+        order of every output element is unchanged (R2)."""
+        from . import repops_transpose
+        rows, cols = X.shape
+        xt = self.xT[:rows * cols].view(cols, rows)
+        repops_transpose(X, out=xt)
+        return repops_gemm(xt, B, transA=True, **kw)
 
     # ------------------------------------------------------------------ program construction
     def _build_program(self):
@@ -324,7 +343,7 @@ class GPT2Step:
                     repops_layernorm(self.x[l], W("ln1.g"), W("ln1.b"), c.ln_eps, out=a["ln1"], mean=a["mu1"],
                                      rstd=a["rs1"])
                     self._hook(f"h{l}/ln1")
-                    repops_gemm(a["ln1"], W("attn.w"), epi=EPI_BIAS, bias=W("attn.b"), out=a["qkv"])
+                    self._gemm_tn(a["ln1"], W("attn.w"), epi=EPI_BIAS, bias=W("attn.b"), out=a["qkv"])
                     self._hook(f"h{l}/qkv")
                     # scores S = (Q K^T) * 1/sqrt(hd), batched over (local shard, head)
                     repops_gemm_strided_batched(a["qkv"], a["qkv"], a["S"], M=T, N=T, K=hd, lda=3 * d, ldb=3 * d,
@@ -338,18 +357,18 @@ class GPT2Step:
                                                 ldc=d, sA=(H * T * T, T * T), sB=(T * 3 * d, hd), sC=(T * d, hd),
                                                 batch=(S_loc, H), offB=2 * d)
                     self._hook(f"h{l}/pv")
-                    repops_gemm(a["att"], W("proj.w"), epi=EPI_BIAS, bias=W("proj.b"), out=a["proj"])
+                    self._gemm_tn(a["att"], W("proj.w"), epi=EPI_BIAS, bias=W("proj.b"), out=a["proj"])
                     self._hook(f"h{l}/proj")
                     repops_add(self.x[l], a["proj"], out=a["xmid"])
                     self._hook(f"h{l}/res1")
                     repops_layernorm(a["xmid"], W("ln2.g"), W("ln2.b"), c.ln_eps, out=a["ln2"], mean=a["mu2"],
                                      rstd=a["rs2"])
                     self._hook(f"h{l}/ln2")
-                    repops_gemm(a["ln2"], W("fc.w"), epi=EPI_BIAS, bias=W("fc.b"), out=a["fc"])
+                    self._gemm_tn(a["ln2"], W("fc.w"), epi=EPI_BIAS, bias=W("fc.b"), out=a["fc"])
                     self._hook(f"h{l}/fc")
                     repops_gelu(a["fc"], out=a["gelu"])
                     self._hook(f"h{l}/gelu")
-                    repops_gemm(a["gelu"], W("fc2.w"), epi=EPI_BIAS, bias=W("fc2.b"), out=a["fc2"])
+                    self._gemm_tn(a["gelu"], W("fc2.w"), epi=EPI_BIAS, bias=W("fc2.b"), out=a["fc2"])
                     self._hook(f"h{l}/fc2")
                     repops_add(a["xmid"], a["fc2"], out=self.x[l + 1])
                     self._hook(f"h{l}/res2")
@@ -402,7 +421,7 @@ class GPT2Step:
                                  c.ln_eps, out=self.lnf, mean=self.muf, rstd=self.rsf)
                 self._hook("head/lnf")
                 wte = self.pview(self.params, "wte")
-                repops_gemm(self.lnf, self.wT["wte"], out=self.logits[:, :c.vocab])
+                self._gemm_tn(self.lnf, self.wteT_pad, out=self.logits)
                 self._hook("head/lm_head")
                 repops_cross_entropy(self.logits, self.targets_flat, scale=1.0 / (c.shards * c.seq),
                                      loss=self.loss_tok, dlogits=self.dlogits, V=c.vocab)
@@ -427,7 +446,7 @@ class GPT2Step:
         if first_local:
             def head_bwd():
                 wte = self.pview(self.params, "wte")
-                repops_gemm(self.dlogits[:, :c.vocab], wte, out=self.dlnf)
+                self._gemm_tn(self.dlogits[:, :c.vocab], wte, out=self.dlnf)
                 self._hook("head/lm_dgrad")
                 o = self.off["wte"][0]
                 repops_gemm_strided_batched(self.dlogits, self.lnf, gl, M=c.vocab, N=d, K=T, lda=c.vocab_ld, ldb=d,
@@ -467,7 +486,7 @@ class GPT2Step:
                     dout = self.dx[l + 1]
                     o = lambda n: self.off[p + n][0]  # noqa: E731
                     # FC2
-                    repops_gemm(dout, self.wT[p + "fc2.w"], out=g["dgelu"])
+                    self._gemm_tn(dout, self.wT[p + "fc2.w"], out=g["dgelu"])
                     self._hook(f"h{l}/fc2_dgrad")
                     repops_gemm_strided_batched(a["gelu"], dout, gl, M=c.ffn, N=d, K=T, lda=c.ffn, ldb=d, ldc=d,
                                                 sA=(T * c.ffn, 0), sB=(T * d, 0), sC=(self.P, 0), batch=(S_loc, 1),
@@ -478,7 +497,7 @@ class GPT2Step:
                     repops_gelu_backward(a["fc"], g["dgelu"], out=g["dfc"])
                     self._hook(f"h{l}/gelu_bwd")
                     # FC
-                    repops_gemm(g["dfc"], self.wT[p + "fc.w"], out=g["dln2"])
+                    self._gemm_tn(g["dfc"], self.wT[p + "fc.w"], out=g["dln2"])
                     self._hook(f"h{l}/fc_dgrad")
                     repops_gemm_strided_batched(a["ln2"], g["dfc"], gl, M=d, N=c.ffn, K=T, lda=d, ldb=c.ffn,
                                                 ldc=c.ffn, sA=(T * d, 0), sB=(T * c.ffn, 0), sC=(self.P, 0),
@@ -494,7 +513,7 @@ class GPT2Step:
                                                      dgamma=gl[:, o("ln2.g"):], dbeta=gl[:, o("ln2.b"):], ldo=self.P)
                     self._hook(f"h{l}/ln2_params")
                     # proj
-                    repops_gemm(g["dxmid"], self.wT[p + "proj.w"], out=g["datt"])
+                    self._gemm_tn(g["dxmid"], self.wT[p + "proj.w"], out=g["datt"])
                     self._hook(f"h{l}/proj_dgrad")
                     repops_gemm_strided_batched(a["att"], g["dxmid"], gl, M=d, N=d, K=T, lda=d, ldb=d, ldc=d,
                                                 sA=(T * d, 0), sB=(T * d, 0), sC=(self.P, 0), batch=(S_loc, 1),
@@ -521,7 +540,7 @@ class GPT2Step:
                                                 sC=(T * 3 * d, hd), batch=(S_loc, H), transA=True, offC=d)
                     self._hook(f"h{l}/attn_dqkv")
                     # QKV
-                    repops_gemm(g["dqkv"], self.wT[p + "attn.w"], out=g["dln1"])
+                    self._gemm_tn(g["dqkv"], self.wT[p + "attn.w"], out=g["dln1"])
                     self._hook(f"h{l}/qkv_dgrad")
                     repops_gemm_strided_batched(a["ln1"], g["dqkv"], gl, M=d, N=3 * d, K=T, lda=d, ldb=3 * d,
                                                 ldc=3 * d, sA=(T * d, 0), sB=(T * 3 * d, 0), sC=(self.P, 0),

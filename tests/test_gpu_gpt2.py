@@ -28,10 +28,16 @@ def mth(entries):
     return H(b"\x01" + mth(entries[:k]) + mth(entries[k:]))
 
 
-@pytest.fixture(scope="module")
-def tiny_run():
+@pytest.fixture(scope="module", params=["tiny", "tiny_vocab500"])
+def tiny_run(request):
+    import dataclasses
+
     from paper_2502_19405_b200.gpt2 import GPT2Config, GPT2Step
     cfg = GPT2Config.tiny()
+    if request.param == "tiny_vocab500":
+        # ragged vocabulary (vocab_ld = 512 > 500) as in GPT-2's 50257: exercises the
+        # LM head over the zero-padded wte^T and the dgrad with a ragged K tail
+        cfg = dataclasses.replace(cfg, vocab=500)
     st = GPT2Step(cfg)
     st.set_tokens(0)
     st.run()

@@ -56,6 +56,21 @@ def test_gemm_parity(M, N, K, tA, tB):
         assert_bits(host(got), ref, f"gemm {M}x{N}x{K} tA{tA} tB{tB} cfg{cfg}")
 
 
+@pytest.mark.parametrize("K", [7, 16, 1005])
+@pytest.mark.parametrize("tA,tB", [(0, 0), (0, 1), (1, 0), (1, 1)])
+def test_gemm_full_tiles_ragged_k_every_cfg(K, tA, tB):
+    # M, N multiples of every tile shape -> the predicate-free full-tile loads,
+    # with a ragged last K tile taking the bounded path (no zero padding, R2)
+    M, N = 256, 512
+    A, B = synth.gemm_inputs((M, N, K), "gk")
+    Ain = np.ascontiguousarray(A.T) if tA else A
+    Bin = np.ascontiguousarray(B.T) if tB else B
+    ref = oracle.gemm(Ain, Bin, transA=bool(tA), transB=bool(tB))
+    for cfg in range(10):
+        got = R.repops_gemm(dev(Ain), dev(Bin), transA=bool(tA), transB=bool(tB), cfg=cfg)
+        assert_bits(host(got), ref, f"gemm {M}x{N}x{K} tA{tA} tB{tB} cfg{cfg}")
+
+
 def test_gemm_epilogues_and_edge_cases():
     A, B = synth.gemm_inputs((70, 90, 45), "ge")
     bias = synth.uniform(5, 90)
@@ -288,6 +303,20 @@ def test_adamw_parity():
         assert_bits(host(tp), rp, "adam p")
         assert_bits(host(tm), rm, "adam m")
         assert_bits(host(tv), rv, "adam v")
+
+
+@pytest.mark.parametrize("rows,cols", [(1, 1), (64, 64), (130, 67), (256, 1000), (4096, 77)])
+def test_transpose_exact(rows, cols):
+    # data movement only: y = x^T bit for bit, contiguous (16-byte path) and strided views
+    x = synth.uniform(31, (rows, cols + 5))
+    xs = np.ascontiguousarray(x[:, :cols])
+    got = R.repops_transpose(dev(xs))
+    assert np.array_equal(host(got).view(np.uint32), xs.T.view(np.uint32))
+    big = torch.zeros((cols, rows + 8), device="cuda")
+    R.repops_transpose(dev(x)[:, 1:cols + 1], out=big[:, 3:rows + 3])  # misaligned views: scalar path
+    b = host(big)
+    assert np.array_equal(b[:, 3:rows + 3].view(np.uint32), x[:, 1:cols + 1].T.view(np.uint32))
+    assert np.all(b[:, :3] == 0) and np.all(b[:, rows + 3:] == 0)
 
 
 # ------------------------------------------------------------------ Verde commitments

@@ -27,15 +27,17 @@ shapes = [(8192, 8192, 8192), (4096, 4096, 4096), (4096, 2304, 768), (768, 2304,
 if len(sys.argv) > 1:
     shapes = [tuple(int(x) for x in s.split("x")) for s in sys.argv[1].split(",")]
 ncfg = int(os.environ.get("NCFG", "6"))
+cfgs = [int(x) for x in os.environ["CFGS"].split(",")] if "CFGS" in os.environ else list(range(ncfg))
+layouts = [tuple(int(c) for c in x) for x in os.environ.get("LAYOUTS", "00,01,10").split(",")]
 torch.manual_seed(0)
 for (M, N, K) in shapes:
-    for ta, tb in ((0, 0), (0, 1), (1, 0)):
+    for ta, tb in layouts:
         A = (torch.rand((K, M) if ta else (M, K), device="cuda") * 2 - 1)
         B = (torch.rand((N, K) if tb else (K, N), device="cuda") * 2 - 1)
         C0 = torch.empty(M, N, device="cuda")
         R.repops_gemm(A, B, transA=bool(ta), transB=bool(tb), out=C0, cfg=0)
         res = []
-        for cfg in range(ncfg):
+        for cfg in cfgs:
             C = torch.empty(M, N, device="cuda")
             ms = t_ms(lambda: R.repops_gemm(A, B, transA=bool(ta), transB=bool(tb), out=C, cfg=cfg))
             same = torch.equal(C.view(torch.int32), C0.view(torch.int32))

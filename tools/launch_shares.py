@@ -12,7 +12,7 @@ step = ts[len(ts) - len(ts) // nsteps:]
 tot, cnt = collections.defaultdict(float), collections.Counter()
 for k, v in step:
     k = k.replace('(anonymous namespace)::', '').replace('<unnamed>::', '')
-    m = re.search(r'gemm_kernel<(\d+), (\d+), \d+, \d+, \d+, \d+, \d+, (\w+), (\w+)', k)
+    m = re.search(r'gemm_kernel<(\d+), (\d+)(?:, \d+)+, (true|false|0|1), (true|false|0|1)', k)
     if m:
         k = 'gemm_kernel %sx%s %s%s' % (m.group(1), m.group(2), 'T' if m.group(3) in ('true', '1') else 'N',
                                         'T' if m.group(4) in ('true', '1') else 'N')
