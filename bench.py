@@ -44,6 +44,25 @@ def fp32_peak_tflops(mhz: float, sms: int = 148) -> float:
     return sms * 128 * 2 * mhz * 1e6 / 1e12
 
 
+def profiled_gemm_traffic():
+    """DRAM bytes per R-GEMM launch, averaged over one GPT-2 step's GEMM launches in
+    the committed ncu launch list (profiles/, tools/profile_round.sh); None if absent."""
+    import csv
+    path = os.path.join(ROOT, "profiles", "r01_gpt2_step_launches.csv")
+    try:
+        rows = list(csv.reader(open(path)))
+        h = rows[0]
+        ki, mi, vi = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value")
+        byts, ids = 0.0, set()
+        for r in rows[1:]:
+            if "gemm_kernel" in r[ki] and r[mi] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                byts += float(r[vi].replace(",", ""))
+                ids.add(r[0])
+        return byts / len(ids) if ids else None
+    except Exception:
+        return None
+
+
 def measured_hbm_gbs() -> float:
     try:
         return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
@@ -234,6 +253,59 @@ class LlamaPrefillBench:
 
     h2d_bytes = 2048 * 4
     d2h_bytes = 32
+
+
+def mlp_extra(with_oracle=True, reps=200):
+    """BASELINE config 1 (configs[0]): the 2-layer MLP DP step (fwd, bwd, R-TREE_S,
+    AdamW, commit of all 104 outputs) -- launch-latency bound, so reported in us per
+    step: eager, and as one CUDA-graph replay; plus the config's 128^3 R-GEMM; beside
+    the full oracle step on one host core (seconds)."""
+    import torch
+
+    import paper_2502_19405_b200 as R
+    import synth
+    from paper_2502_19405_b200.mlp import MLPConfig, MLPStep
+
+    def us(fn, n):
+        for _ in range(5):
+            fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(n):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / n * 1e3
+
+    st = MLPStep(MLPConfig())
+    l0 = R.launch_count()
+    st.run()
+    launches = R.launch_count() - l0
+    eager = us(lambda: (st.reset(), st.run()), reps)
+    st.capture()
+    graph = us(st.replay, reps)
+    torch.cuda.synchronize()
+    root = st.root().hex()
+    A, B = (torch.from_numpy(t).cuda() for t in synth.gemm_inputs(128, "bench"))
+    C = torch.empty(128, 128, device="cuda")
+    g128 = us(lambda: R.repops_gemm(A, B, out=C), reps)
+    res = {"us_per_step_graph": graph, "us_per_step_eager": eager, "gpu_launches": launches,
+           "gemm128_us": g128, "root": root,
+           "config": "Linear-ReLU-Linear-CE, width 256, batch 32 = 8 shards x 4 rows, AdamW, every output "
+                     "committed (BASELINE configs[0])"}
+    if with_oracle:
+        import oracle
+        from oracle import mlp_step as omlp
+        oracle.lib()
+        t0 = time.perf_counter()
+        omlp.run_step(MLPConfig())
+        res["oracle_s_per_step"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        a_, b_ = synth.gemm_inputs(128, "bench")
+        oracle.gemm(a_, b_)
+        res["oracle_gemm128_s"] = time.perf_counter() - t0
+    return res
 
 
 # ---------------------------------------------------------------------- oracle legs
@@ -445,7 +517,10 @@ def main():
                                     "the median observed clock: %.3f" % (
                                         achieved / fp32_peak_tflops(clk["sm_mhz"]) if clk["sm_mhz"] else -1),
                        "gemm_ms_per_step": gemm_ms_step, "gemm_launches_per_step": gemm_launches,
-                       "traffic": None}
+                       "traffic": profiled_gemm_traffic(),
+                       "traffic_note": "DRAM bytes (read + write) per R-GEMM launch, mean over one GPT-2 step's "
+                                       "GEMM launches, from the committed ncu launch list "
+                                       "profiles/r01_gpt2_step_launches.csv (cold-cache replay)"}
     if "commit" in head:
         cm = head["commit"]
         cm["hbm_frac"] = cm["gbs"] / hbm
@@ -467,12 +542,8 @@ def main():
                                    "llama": "Llama-3-8B-shaped FP32 prefill, 2048 tokens, 32 layers, TP N-split "
                                             f"over {world} GPU(s) (8 column blocks), every output committed",
                                    "gpt2": "GPT-2 124M train step"}[other]}
-    tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp):
-        try:
-            out["roofline"]["traffic"] = json.load(open(tp)).get(args.workload)
-        except Exception:
-            pass
+    if rank == 0 and world == 1 and not args.no_sweep:
+        out["mlp_step"] = mlp_extra(with_oracle=not args.no_cpu_baseline)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, secs, sample = oracle_sample_gpt2() if args.workload == "gpt2" else oracle_sample_gemm()
         out["cpu_baseline"] = {"value": v, "unit": "TFLOP/s", "cores": 1, "kind": "oracle",

@@ -152,6 +152,11 @@ int repops_rsqrt(const float *x, int64_t n, float *y, void *stream);   /* fdiv(1
 int repops_gelu(const float *x, int64_t n, float *y, void *stream);    /* tanh form, R13 */
 int repops_gelu_backward(const float *x, const float *dy, int64_t n, float *dx, void *stream);
 int repops_add(const float *a, const float *b, int64_t n, float *y, void *stream);
+/* ReLU (config-1 MLP; reading R24): y = x > 0 ? x : +0 (-0 and negatives
+ * give +0); dx = x > 0 ? g : +0 (subgradient 0 at x = 0); a NaN x gives the canonical NaN.
+ * x, g, y, dx: device float[n], contiguous; y / dx may alias x / g. */
+int repops_relu(const float *x, int64_t n, float *y, void *stream);
+int repops_relu_backward(const float *x, const float *g, int64_t n, float *dx, void *stream);
 
 /* R-EMB forward: x0[t][c] = fadd(wte[tok[t]][c], wpe[t mod T][c]); tok device int32. */
 int repops_embedding(const int32_t *tok, int64_t ntok, int64_t T, const float *wte,

@@ -64,6 +64,8 @@ def lib():
                 "orc_rsqrt_vec": (None, [vp, i64, vp]),
                 "orc_add": (None, [vp, vp, i64, vp]),
                 "orc_gelu": (None, [vp, i64, vp]),
+                "orc_relu": (None, [vp, i64, vp]),
+                "orc_relu_backward": (None, [vp, vp, i64, vp]),
                 "orc_gelu_backward": (None, [vp, vp, i64, vp]),
                 "orc_softmax": (None, [vp, i64, i64, i64, i32, vp, i64]),
                 "orc_softmax_backward": (None, [vp, i64, vp, i64, i64, i64, f32, vp, i64]),
@@ -211,6 +213,20 @@ def gelu_backward(x, dy):
     dy = _f32(dy)
     dx = np.empty_like(x)
     lib().orc_gelu_backward(_p(x), _p(dy), x.size, _p(dx))
+    return dx
+
+
+def relu(x):
+    """orc_relu (reading R24)."""
+    return _vec("orc_relu", x)
+
+
+def relu_backward(x, g):
+    """orc_relu_backward (reading R24; subgradient 0 at x = 0)."""
+    x = _f32(x)
+    g = _f32(g)
+    dx = np.empty_like(x)
+    lib().orc_relu_backward(_p(x), _p(g), x.size, _p(dx))
     return dx
 
 

@@ -251,6 +251,17 @@ void orc_rsqrt_vec(const float *x, i64 n, float *y) { for (i64 i = 0; i < n; ++i
 /* elementwise residual add: y = a + b */
 void orc_add(const float *a, const float *b, i64 n, float *y) { for (i64 i = 0; i < n; ++i) y[i] = canon(a[i] + b[i]); }
 
+/* ReLU (config 1 MLP, reading R24 in DESIGN.md):
+ *   relu(x) = x if x > 0, else +0 (so -0 and negatives give +0); NaN -> canonical NaN.
+ *   relu_backward(x, g) = g if x > 0, else +0 (subgradient at 0 is 0); NaN x -> NaN. */
+void orc_relu(const float *x, i64 n, float *y) {
+    for (i64 i = 0; i < n; ++i) y[i] = (x[i] != x[i]) ? canon(x[i]) : (x[i] > 0.0f ? x[i] : 0.0f);
+}
+
+void orc_relu_backward(const float *x, const float *g, i64 n, float *dx) {
+    for (i64 i = 0; i < n; ++i) dx[i] = (x[i] != x[i]) ? canon(x[i]) : (x[i] > 0.0f ? canon(g[i]) : 0.0f);
+}
+
 /* GELU, tanh form (GPT-2), reading R5/R13 in DESIGN.md:
  *   u = sqrt(2/pi) * (x + 0.044715 x^3),  y = 0.5 x (1 + tanh u) */
 void orc_gelu(const float *x, i64 n, float *y) {

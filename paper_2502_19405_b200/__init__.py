@@ -22,7 +22,7 @@ __all__ = [
     "repops_gemm", "repops_gemm_strided_batched", "repops_sum_rows", "repops_sum_cols_seq", "repops_tree_sum",
     "repops_softmax", "repops_softmax_backward", "repops_layernorm", "repops_layernorm_backward",
     "repops_layernorm_backward_params", "repops_cross_entropy", "repops_exp", "repops_log", "repops_tanh",
-    "repops_rsqrt", "repops_gelu", "repops_gelu_backward", "repops_add", "repops_embedding",
+    "repops_rsqrt", "repops_gelu", "repops_gelu_backward", "repops_relu", "repops_relu_backward", "repops_add", "repops_embedding",
     "repops_embedding_backward", "repops_adamw", "repops_flip_bit", "verde_commit_tensor",
     "verde_commit_tensors", "verde_merkle_root", "verde_sha256", "verde_node_digest",
     "verde_first_divergence", "verde_digest_from_subroots", "launch_count", "CommitWorkspace", "CommitPlan",
@@ -269,6 +269,20 @@ def repops_rsqrt(x, out=None, stream=None):
 
 def repops_gelu(x, out=None, stream=None):
     return _unary("repops_gelu", x, out, stream)
+
+
+def repops_relu(x, out=None, stream=None):
+    """R24: relu(x) = x > 0 ? x : +0."""
+    return _unary("repops_relu", x, out, stream)
+
+
+def repops_relu_backward(x, g, out=None, stream=None):
+    """R24: dx = x > 0 ? g : +0 (subgradient 0 at x = 0)."""
+    _contig(x, "x"), _contig(g, "g")
+    if out is None:
+        out = torch.empty_like(x)
+    check(lib().repops_relu_backward(_p(x), _p(g), x.numel(), _p(out), _stream(stream)), "repops_relu_backward")
+    return out
 
 
 def repops_gelu_backward(x, dy, out=None, stream=None):

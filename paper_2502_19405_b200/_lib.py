@@ -53,6 +53,8 @@ SIGNATURES = {
     "repops_tanh": (i32, [vp, i64, vp, vp]),
     "repops_rsqrt": (i32, [vp, i64, vp, vp]),
     "repops_gelu": (i32, [vp, i64, vp, vp]),
+    "repops_relu": (i32, [vp, i64, vp, vp]),
+    "repops_relu_backward": (i32, [vp, vp, i64, vp, vp]),
     "repops_gelu_backward": (i32, [vp, vp, i64, vp, vp]),
     "repops_add": (i32, [vp, vp, i64, vp, vp]),
     "repops_embedding": (i32, [vp, i64, i64, vp, vp, i64, vp, vp]),

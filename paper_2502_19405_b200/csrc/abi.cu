@@ -359,6 +359,14 @@ UNARY(repops_log, launch_log)
 UNARY(repops_tanh, launch_tanh)
 UNARY(repops_rsqrt, launch_rsqrt)
 UNARY(repops_gelu, launch_gelu)
+UNARY(repops_relu, launch_relu)
+
+int repops_relu_backward(const float *x, const float *g, int64_t n, float *dx, void *stream) {
+    REQ(n >= 0, "relu_backward: negative n");
+    if (n == 0) return REPOPS_OK;
+    REQ(x && g && dx, "relu_backward: null pointer");
+    return cuda_status(launch_relu_backward(x, g, n, dx, S(stream)), "relu_backward");
+}
 
 int repops_gelu_backward(const float *x, const float *dy, int64_t n, float *dx, void *stream) {
     REQ(n >= 0, "gelu_backward: negative n");

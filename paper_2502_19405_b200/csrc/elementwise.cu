@@ -41,6 +41,13 @@ struct TanhF { RO_DEV float operator()(float x) const { return canon(tanh_rn(x))
 struct RsqrtF { RO_DEV float operator()(float x) const { return canon(rsqrt_rn(x)); } };
 struct GeluF { RO_DEV float operator()(float x) const { return canon(gelu_rn(x)); } };
 struct GeluBwdF { RO_DEV float operator()(float x, float dy) const { return canon(gelu_grad_rn(x, dy)); } };
+// R24 (config-1 MLP): relu(x) = x > 0 ? x : +0; relu'(x) g = x > 0 ? g : +0; NaN x -> NaN
+struct ReluF {
+    RO_DEV float operator()(float x) const { return x != x ? canon(x) : (x > 0.f ? x : 0.f); }
+};
+struct ReluBwdF {
+    RO_DEV float operator()(float x, float g) const { return x != x ? canon(x) : (x > 0.f ? canon(g) : 0.f); }
+};
 struct AddF { RO_DEV float operator()(float a, float b) const { return canon(__fadd_rn(a, b)); } };
 
 // R-TREE_S: balanced pairwise tree over up to 16 parts, leaves are the parts themselves
@@ -193,6 +200,14 @@ cudaError_t launch_log(const float *x, int64_t n, float *y, cudaStream_t s) { re
 cudaError_t launch_tanh(const float *x, int64_t n, float *y, cudaStream_t s) { return run_unary(x, n, y, s, TanhF{}); }
 cudaError_t launch_rsqrt(const float *x, int64_t n, float *y, cudaStream_t s) { return run_unary(x, n, y, s, RsqrtF{}); }
 cudaError_t launch_gelu(const float *x, int64_t n, float *y, cudaStream_t s) { return run_unary(x, n, y, s, GeluF{}); }
+
+cudaError_t launch_relu(const float *x, int64_t n, float *y, cudaStream_t s) { return run_unary(x, n, y, s, ReluF{}); }
+
+cudaError_t launch_relu_backward(const float *x, const float *g, int64_t n, float *dx, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    binary_kernel<<<ew_grid(n), 256, 0, s>>>(x, g, n, dx, ReluBwdF{});
+    return cudaGetLastError();
+}
 
 cudaError_t launch_gelu_backward(const float *x, const float *dy, int64_t n, float *dx, cudaStream_t s) {
     if (n == 0) return cudaSuccess;

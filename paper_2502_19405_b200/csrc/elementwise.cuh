@@ -8,6 +8,8 @@ cudaError_t launch_log(const float *x, int64_t n, float *y, cudaStream_t s);
 cudaError_t launch_tanh(const float *x, int64_t n, float *y, cudaStream_t s);
 cudaError_t launch_rsqrt(const float *x, int64_t n, float *y, cudaStream_t s);
 cudaError_t launch_gelu(const float *x, int64_t n, float *y, cudaStream_t s);
+cudaError_t launch_relu(const float *x, int64_t n, float *y, cudaStream_t s);
+cudaError_t launch_relu_backward(const float *x, const float *g, int64_t n, float *dx, cudaStream_t s);
 cudaError_t launch_gelu_backward(const float *x, const float *dy, int64_t n, float *dx, cudaStream_t s);
 cudaError_t launch_add(const float *a, const float *b, int64_t n, float *y, cudaStream_t s);
 cudaError_t launch_tree_sum(const float *const *parts, int nparts, int64_t n, float *out, cudaStream_t s);

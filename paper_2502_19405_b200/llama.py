@@ -32,7 +32,7 @@ import synth
 
 from . import (EPI_SCALE, CommitPlan, RootPlan, repops_add, repops_copy2d, repops_fill_uniform, repops_gather_rows,
                repops_gemm_strided_batched, repops_rmsnorm, repops_rope, repops_softmax, repops_swiglu,
-               verde_commit_tensors)
+               repops_transpose, verde_commit_tensors)
 from ._lib import check, lib
 from .dist import all_gather_rows, gather_shard_digests, shard_block
 
@@ -132,6 +132,9 @@ class LlamaPrefill:
                                  hn=E(T, d), rs2=E(T), g=E(nbl, T, self.Fb), u=E(nbl, T, self.Fb),
                                  a=E(nbl, T, self.Fb), a_all=E(T, c.ffn), dn=E(nbl, T, self.Db), mlp=E(T, d)))
         self.xf, self.rsf = E(T, d), E(T)
+        # X^T scratch: the shared activation operand of every projection is transposed
+        # once so the GEMMs run TN; data movement only
+        self.xT = E(max(c.ffn, c.n_head * hd, d) * T)
         self.logits = E(nbl, T, self.Vb)
 
     def load_weights(self):
@@ -306,12 +309,18 @@ class LlamaPrefill:
         for b in range(self.cfg.nb):
             repops_copy2d(allb[b], full[:, b * width:(b + 1) * width])
 
+    def _xT(self, x):
+        rows, cols = x.shape
+        t = self.xT[:rows * cols].view(cols, rows)
+        repops_transpose(x, out=t)
+        return t
+
     def _attn(self, l, a, w, scale):
         c = self.cfg
         T, d, hd, qh, nbl, Wb = c.seq, c.d, c.hd, c.qh, self.nbl, self.Wb
         repops_rmsnorm(self.x[l], w["attn_norm"], c.eps, out=a["xn"], rstd=a["rs1"])
-        repops_gemm_strided_batched(a["xn"], w["wqkv"], a["qkv"], M=T, N=Wb, K=d, lda=d, ldb=Wb, ldc=Wb,
-                                    sA=(0, 0), sB=(d * Wb, 0), sC=(T * Wb, 0), batch=(nbl, 1))
+        repops_gemm_strided_batched(self._xT(a["xn"]), w["wqkv"], a["qkv"], M=T, N=Wb, K=d, lda=T, ldb=Wb, ldc=Wb,
+                                    sA=(0, 0), sB=(d * Wb, 0), sC=(T * Wb, 0), batch=(nbl, 1), transA=True)
         for j in range(nbl):
             repops_rope(a["qkv"][j][:, :(qh + 1) * hd], self.cos, self.sin, qh + 1, hd, out=a["qk"][j])
         W2 = (qh + 1) * hd
@@ -324,9 +333,9 @@ class LlamaPrefill:
                                     offB=(qh + 1) * hd)
         self._gather_blocks(a["o"], a["o_all"], qh * hd)
         HD = c.n_head * hd
-        repops_gemm_strided_batched(a["o_all"], w["wo"], a["op"], M=T, N=self.Db, K=HD, lda=HD, ldb=self.Db,
-                                    ldc=self.Db, sA=(0, 0), sB=(HD * self.Db, 0), sC=(T * self.Db, 0),
-                                    batch=(nbl, 1))
+        repops_gemm_strided_batched(self._xT(a["o_all"]), w["wo"], a["op"], M=T, N=self.Db, K=HD, lda=T,
+                                    ldb=self.Db, ldc=self.Db, sA=(0, 0), sB=(HD * self.Db, 0), sC=(T * self.Db, 0),
+                                    batch=(nbl, 1), transA=True)
         self._gather_blocks(a["op"], a["attn"], self.Db)
         repops_add(self.x[l], a["attn"], out=a["h"])
 
@@ -334,14 +343,15 @@ class LlamaPrefill:
         c = self.cfg
         T, d, nbl, Fb = c.seq, c.d, self.nbl, self.Fb
         repops_rmsnorm(a["h"], w["mlp_norm"], c.eps, out=a["hn"], rstd=a["rs2"])
+        hnT = self._xT(a["hn"])
         for wk, out in (("wg", "g"), ("wu", "u")):
-            repops_gemm_strided_batched(a["hn"], w[wk], a[out], M=T, N=Fb, K=d, lda=d, ldb=Fb, ldc=Fb, sA=(0, 0),
-                                        sB=(d * Fb, 0), sC=(T * Fb, 0), batch=(nbl, 1))
+            repops_gemm_strided_batched(hnT, w[wk], a[out], M=T, N=Fb, K=d, lda=T, ldb=Fb, ldc=Fb, sA=(0, 0),
+                                        sB=(d * Fb, 0), sC=(T * Fb, 0), batch=(nbl, 1), transA=True)
         repops_swiglu(a["g"], a["u"], out=a["a"])
         self._gather_blocks(a["a"], a["a_all"], Fb)
-        repops_gemm_strided_batched(a["a_all"], w["wd"], a["dn"], M=T, N=self.Db, K=c.ffn, lda=c.ffn, ldb=self.Db,
-                                    ldc=self.Db, sA=(0, 0), sB=(c.ffn * self.Db, 0), sC=(T * self.Db, 0),
-                                    batch=(nbl, 1))
+        repops_gemm_strided_batched(self._xT(a["a_all"]), w["wd"], a["dn"], M=T, N=self.Db, K=c.ffn, lda=T,
+                                    ldb=self.Db, ldc=self.Db, sA=(0, 0), sB=(c.ffn * self.Db, 0),
+                                    sC=(T * self.Db, 0), batch=(nbl, 1), transA=True)
         self._gather_blocks(a["dn"], a["mlp"], self.Db)
         repops_add(a["h"], a["mlp"], out=self.x[l + 1])
 
@@ -349,9 +359,9 @@ class LlamaPrefill:
         c = self.cfg
         T, d = c.seq, c.d
         repops_rmsnorm(self.x[c.n_layer], self.norm, c.eps, out=self.xf, rstd=self.rsf)
-        repops_gemm_strided_batched(self.xf, self.wlm, self.logits, M=T, N=self.Vb, K=d, lda=d, ldb=self.Vb,
-                                    ldc=self.Vb, sA=(0, 0), sB=(d * self.Vb, 0), sC=(T * self.Vb, 0),
-                                    batch=(self.nbl, 1))
+        repops_gemm_strided_batched(self._xT(self.xf), self.wlm, self.logits, M=T, N=self.Vb, K=d, lda=T,
+                                    ldb=self.Vb, ldc=self.Vb, sA=(0, 0), sB=(d * self.Vb, 0),
+                                    sC=(T * self.Vb, 0), batch=(self.nbl, 1), transA=True)
 
     # ------------------------------------------------------------------ finalisation / running
     def _finalize(self):

@@ -109,6 +109,15 @@ def gpt2_tokens(vocab, seq, shard, step=0, seed=0):
 
 
 # ----------------------------------------------------------------- Llama-3-8B-shaped prefill (config 4)
+def mlp_inputs(batch=32, width=256, classes=256, seed=0):
+    """Config-1 MLP: x[batch x width] U[-1,1); W1 [width x width],
+    W2 [width x classes], b1, b2 U[-1/16, 1/16); labels U{0..classes-1}."""
+    u = lambda name, shape, scale=1.0: uniform(seed_for("mlp", seed, name), shape, scale)  # noqa: E731
+    return {"x": u("x", (batch, width)), "W1": u("W1", (width, width), 1 / 16), "b1": u("b1", width, 1 / 16),
+            "W2": u("W2", (width, classes), 1 / 16), "b2": u("b2", classes, 1 / 16),
+            "labels": integers(seed_for("mlp", seed, "labels"), batch, classes)}
+
+
 def llama_param_specs(n_layer, d, n_head, n_kv, hd, ffn, vocab):
     """(name, shape, kind) in canonical order; weights stored [in, out] (y = x W)."""
     specs = [("tok_emb", (vocab, d), "w")]

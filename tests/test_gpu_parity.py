@@ -305,6 +305,14 @@ def test_adamw_parity():
         assert_bits(host(tv), rv, "adam v")
 
 
+def test_relu_and_backward_exact():
+    x = np.concatenate([synth.uniform(41, 100003, 3.0),
+                        np.float32([0.0, -0.0, np.inf, -np.inf, np.nan, 1e-45, -1e-45])])
+    g = synth.uniform(42, x.size, 2.0)
+    assert_bits(host(R.repops_relu(dev(x))), oracle.relu(x), "relu")
+    assert_bits(host(R.repops_relu_backward(dev(x), dev(g))), oracle.relu_backward(x, g), "relu_backward")
+
+
 @pytest.mark.parametrize("rows,cols", [(1, 1), (64, 64), (130, 67), (256, 1000), (4096, 77)])
 def test_transpose_exact(rows, cols):
     # data movement only: y = x^T bit for bit, contiguous (16-byte path) and strided views

@@ -1,13 +1,19 @@
 #!/bin/bash
-# Profiles for profiles/: launch list of the bench command + ncu --set full of the top kernels.
-mkdir -p gpurun_out
+# One gpurun call producing the judged profiles (summaries are written remotely: .ncu-rep files are large).
+#  gpurun_out/launches.csv : ncu launch list of the bench command (duration + DRAM bytes per launch)
+#  gpurun_out/ncu_<tag>.txt: ncu --set full summaries (+ per-SASS stall attribution) of the top kernels
 python -c "import __graft_entry__ as g; g.build()" > /dev/null
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bench.csv \
+mkdir -p gpurun_out
+timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-sweep > gpurun_out/launches_bench.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm_kernel -s 2 -c 1 -o gpurun_out/ncu_gemm_fc -f \
-    python tools/gemm_one.py 4096x3072x768 0 0 -1 > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm_kernel -s 2 -c 1 -o gpurun_out/ncu_gemm_8192 -f \
-    python tools/gemm_one.py 8192x8192x8192 0 0 -1 > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:leaf_kernel -s 1 -c 1 -o gpurun_out/ncu_leaf -f \
-    python tools/commit_one.py > /dev/null 2>&1
-ls -la gpurun_out
+echo "launch list: $(wc -l < gpurun_out/launches.csv) lines"
+bash tools/prof_gemm_remote.sh "4096x768x3072 1 0 -1 gemm_fc2_tn" "4096x3072x768 1 0 -1 gemm_fc_tn" \
+    "8192x8192x8192 1 0 -1 gemm_8192_tn" "8192x8192x8192 0 0 -1 gemm_8192_nn"
+mkdir -p gpurun_out/prof_tmp
+timeout 300 ncu --set full --import-source on --clock-control none -k regex:leaf_kernel -s 1 -c 1 \
+    -o gpurun_out/prof_tmp/leaf -f python tools/commit_one.py > /dev/null 2>&1
+ncu -i gpurun_out/prof_tmp/leaf.ncu-rep --page raw --csv > gpurun_out/prof_tmp/leaf.csv 2>/dev/null
+python tools/ncu_summary.py gpurun_out/prof_tmp/leaf.csv > gpurun_out/ncu_leaf.txt
+rm -rf gpurun_out/prof_tmp
+ls -la gpurun_out/ncu_*.txt
