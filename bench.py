@@ -213,13 +213,19 @@ class GPT2Train:
         self.root = None
 
     def step(self):
-        self.st.run(commit=self.commit)
-        self.root = self.st.device_root()    # C2 gather + node digests + step root on the GPU; 32 B D2H
+        # the tail commits + root of step n run beside step n+1's forward (no host sync)
+        self.st.run(commit=self.commit, join=False)
+        self.st.device_root(sync=False)       # C2 gather + node digests + step root on the GPU; 32 B D2H
+
+    def join(self):
+        self.st.join()
+        self.root = self.st.root_bytes()
 
     def e2e_step(self):
         self.st.set_tokens(self.st.step_no)    # H2D of this step's batch from pinned host memory
-        self.step()
-        return self.st.loss(), self.root       # D2H of the loss (root already on the host)
+        self.st.run(commit=self.commit)
+        self.root = self.st.device_root()      # 32 B D2H
+        return self.st.loss(), self.root       # D2H of the loss
 
     @property
     def h2d_bytes(self):
@@ -405,6 +411,8 @@ def timed(wl, steps, world, local):
         ev0.record(stream)
         for _ in range(steps):
             wl.step()
+        if hasattr(wl, "join"):
+            wl.join()                         # side-stream work of the last step is inside the region
         ev1.record(stream)
         torch.cuda.synchronize()
         R.set_timer(None)

@@ -730,9 +730,18 @@ class GPT2Step:
                 self.plan_after[ph] = plan
         self.commit_bytes = sum(p.nbytes for p in self.plans)
         self._wait_side_before = {deferred_phase, next(i for i, p in enumerate(self.phases) if p[0] == "adamw")}
+        # Commits of the "tree" / "adamw" phases hash buffers (grad, p, m, v) that the
+        # next step rewrites only after a _wait_side_before phase, so with join=False
+        # they (and the root plan) may run beside the next step's forward; every
+        # other commit must finish before the next step rewrites its activations.
+        self._tail_from = next(i for i, p in enumerate(self.phases) if p[0] == "tree")
+        self._last_act_plan = max(i for i in self.plan_after if i < self._tail_from) if self.plan_after else -1
+        self._joined = True
         if not self.structure_only:
             self.side = torch.cuda.Stream(device=self.dev)
             self.overlap_commits = True
+            self._ev_act = torch.cuda.Event()
+            self._ev_root = torch.cuda.Event()
         self._build_node_blob()
         if not self.structure_only:
             from . import RootPlan
@@ -797,9 +806,12 @@ class GPT2Step:
         view = self.tensors[nd.outputs[out_slot]].view
         self._fault = (nd.label, lambda: repops_flip_bit(view, elem, bit))
 
-    def run(self, commit=True, inject=None):
+    def run(self, commit=True, inject=None, join=True):
         """Enqueue one full training step.  inject = (phase_name, fn) runs fn after that
-        phase's kernels (coarse fault injection; see inject_fault for per-op points)."""
+        phase's kernels (coarse fault injection; see inject_fault for per-op points).
+        join=False: the main stream only waits for the activation commits, so the
+        tail commits (tree / AdamW outputs) overlap the next step; device_root() then
+        runs on the side stream and join() waits for everything."""
         main = torch.cuda.current_stream()
         side = self.side if self.overlap_commits else main
         if side is not main:
@@ -818,9 +830,21 @@ class GPT2Step:
                 else:
                     side.wait_stream(main)
                     plan.run(stream=side)
+                    if i == self._last_act_plan:
+                        self._ev_act.record(side)
         if side is not main:
-            main.wait_stream(side)
+            if join or not commit:
+                main.wait_stream(side)
+            else:
+                main.wait_event(self._ev_act)
+        self._joined = side is main or join or not commit
         self.step_no += 1
+
+    def join(self):
+        """Make the current stream wait for every enqueued commit / root launch."""
+        if not self.structure_only and self.overlap_commits:
+            torch.cuda.current_stream().wait_stream(self.side)
+        self._joined = True
 
     def gather_digests(self):
         """C2: all-gather the per-shard digest regions; copy the table to the host."""
@@ -831,12 +855,23 @@ class GPT2Step:
 
     def device_root(self, sync=True):
         """Step root computed on the GPU (verde_root_plan): C2 gather of the shard digest
-        regions (N > 1), node digests, RFC 6962 root; only 32 bytes come back."""
-        gather_shard_digests(self.digests, self.rep_slots, self.shard_slots, self.s0, self.S_loc, self.world, self.pg)
-        self.root_plan.run()
-        self.root_host.copy_(self.root_plan.root, non_blocking=True)
+        regions (N > 1), node digests, RFC 6962 root; only 32 bytes come back.  After
+        run(join=False) this is enqueued on the side stream behind the tail commits;
+        with sync=False call root_bytes() later."""
+        s = torch.cuda.current_stream() if self._joined else self.side
+        with torch.cuda.stream(s):
+            gather_shard_digests(self.digests, self.rep_slots, self.shard_slots, self.s0, self.S_loc, self.world,
+                                 self.pg)
+            self.root_plan.run(stream=s)
+            self.root_host.copy_(self.root_plan.root, non_blocking=True)
+            self._ev_root.record(s)
         if sync:
-            torch.cuda.current_stream().synchronize()
+            return self.root_bytes()
+        return None
+
+    def root_bytes(self):
+        """The last device_root() result (waits for it)."""
+        self._ev_root.synchronize()
         return bytes(self.root_host.numpy())
 
     def step_root(self, table=None):

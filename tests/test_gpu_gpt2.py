@@ -119,3 +119,27 @@ def test_tiny_step_replay_is_bit_identical(tiny_run):
 def test_tiny_loss_is_near_log_vocab(tiny_run):
     cfg, st, *_ = tiny_run
     assert abs(st.loss() - np.log(cfg.vocab)) < 0.5
+
+
+def test_unjoined_steps_give_the_joined_roots():
+    """run(join=False) lets step n's tail commits and root overlap step n+1; the
+    roots must equal those of fully joined steps."""
+    from paper_2502_19405_b200.gpt2 import GPT2Config, GPT2Step
+    cfg = GPT2Config.tiny()
+    a = GPT2Step(cfg)
+    ref = []
+    for k in range(3):
+        a.set_tokens(k)
+        a.run()
+        ref.append(a.device_root())
+    b = GPT2Step(cfg)
+    got = []
+    for k in range(3):
+        b.set_tokens(k)
+        b.run(join=False)
+        b.device_root(sync=False)
+        with torch.cuda.stream(b.side):
+            got.append(b.root_plan.root.clone())  # ordered after this step's root plan
+    b.join()
+    torch.cuda.synchronize()
+    assert [bytes(g.cpu().numpy()) for g in got] == ref
