@@ -258,6 +258,36 @@ int verde_commit_tensor(const void *data, int64_t nbytes, int dtype, int rank, c
  * root32 (host).  n == 0 -> REPOPS_EINVAL. */
 int verde_merkle_root(const uint8_t *leaves, int64_t n, uint8_t *root32);
 
+/* RFC 6962 MTH over n leaf HASHES (MTH of one leaf = the leaf hash itself), e.g.
+ * the chunk leaves of verde_chunk_leaves: equals the data_root of R11.  Host. */
+int verde_merkle_root_hashed(const uint8_t *leaf_hashes, int64_t n, uint8_t *root32);
+
+/* Merkle membership proofs (Fig. 2 caption; Case 2(a)):
+ * RFC 6962 §2.1.1 audit path PATH(m, D[n]) of item m, sibling roots leaf level first.
+ * items: n x 32 host bytes, entries (hashed = 0: leaf = SHA-256(0x00 || entry)) or
+ * leaf hashes (hashed = 1).  path: host, room for 64 x 32 bytes; *len = path length. */
+int verde_merkle_audit_path(const uint8_t *items, int64_t n, int64_t m, int hashed, uint8_t *path, int32_t *len);
+/* RFC 9162 §2.1.3.2 check that leaf_hash is item m of an n-leaf tree with root32;
+ * *ok = 1 if it is, 0 otherwise (a failed proof is not an error).  All host. */
+int verde_merkle_verify_path(const uint8_t *leaf_hash, int64_t m, int64_t n, const uint8_t *path, int32_t len,
+                             const uint8_t *root32, int *ok);
+
+/* R-TCOMMIT header over a given data root: SHA-256(0x54 || dtype || rank || dims ||
+ * nbytes || 4096 || data_root) (data_root ignored, SHA-256 of nothing used, when
+ * nbytes == 0).  Lets the referee check claimed chunk leaves against a tensor
+ * digest.  Host. */
+int verde_tensor_digest_from_root(const uint8_t *data_root, int dtype, int rank, const int64_t *dims,
+                                  int64_t nbytes, uint8_t *out32);
+
+/* R11 leaf hashes SHA-256(0x00 || chunk) of every 4096-byte chunk of a device
+ * buffer (last chunk ragged) into leaves (device, ceil(nbytes/4096) x 32 bytes):
+ * what a trainer serves for intra-tensor bisection. */
+int verde_chunk_leaves(const void *data, int64_t nbytes, uint8_t *leaves, void *stream);
+
+/* As verde_first_divergence, over leaf HASHES (the trees of verde_merkle_root_hashed). */
+int verde_first_divergence_hashed(const uint8_t *seq0, const uint8_t *seq1, int64_t n, int64_t *d_out,
+                                  int64_t *rounds_out);
+
 /* SHA-256 of a host buffer (host). */
 int verde_sha256(const uint8_t *data, int64_t n, uint8_t *out32);
 

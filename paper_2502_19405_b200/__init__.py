@@ -572,12 +572,63 @@ def verde_node_digest(index, op, shard, attrs, inputs, dsts, in_digests, out_dig
     return out.raw
 
 
-def verde_first_divergence(seq0: bytes, seq1: bytes) -> tuple[int, int]:
-    """(first differing index or -1, number of subtree comparisons)."""
+def verde_first_divergence(seq0: bytes, seq1: bytes, hashed=False) -> tuple[int, int]:
+    """(first differing index or -1, number of subtree comparisons); hashed: the
+    items are leaf hashes (verde_first_divergence_hashed)."""
     n = len(seq0) // 32
     a = C.create_string_buffer(bytes(seq0), max(len(seq0), 1))
     b = C.create_string_buffer(bytes(seq1), max(len(seq1), 1))
     d = C.c_int64()
     r = C.c_int64()
-    check(lib().verde_first_divergence(a, b, n, C.byref(d), C.byref(r)), "verde_first_divergence")
+    fn = lib().verde_first_divergence_hashed if hashed else lib().verde_first_divergence
+    check(fn(a, b, n, C.byref(d), C.byref(r)), "verde_first_divergence")
     return d.value, r.value
+
+
+def verde_merkle_root_hashed(leaf_hashes: bytes) -> bytes:
+    """RFC 6962 MTH over leaf hashes (= the R11 data root of a tensor's chunk leaves)."""
+    blob = bytes(leaf_hashes)
+    buf = C.create_string_buffer(blob, max(len(blob), 1))
+    out = C.create_string_buffer(32)
+    check(lib().verde_merkle_root_hashed(buf, len(blob) // 32, out), "verde_merkle_root_hashed")
+    return out.raw
+
+
+def verde_merkle_audit_path(items: bytes, m: int, hashed=False) -> list[bytes]:
+    """RFC 6962 audit path of item m (membership proof)."""
+    blob = bytes(items)
+    buf = C.create_string_buffer(blob, max(len(blob), 1))
+    path = C.create_string_buffer(64 * 32)
+    ln = C.c_int32()
+    check(lib().verde_merkle_audit_path(buf, len(blob) // 32, int(m), int(bool(hashed)), path, C.byref(ln)),
+          "verde_merkle_audit_path")
+    return [path.raw[32 * i:32 * i + 32] for i in range(ln.value)]
+
+
+def verde_merkle_verify_path(leaf_hash: bytes, m: int, n: int, path: list[bytes], root: bytes) -> bool:
+    """RFC 9162 inclusion check of leaf_hash at index m of an n-leaf tree with `root`."""
+    p = b"".join(path)
+    pb = C.create_string_buffer(p, max(len(p), 1))
+    ok = C.c_int()
+    check(lib().verde_merkle_verify_path(bytes(leaf_hash), int(m), int(n), pb, len(path), bytes(root), C.byref(ok)),
+          "verde_merkle_verify_path")
+    return bool(ok.value)
+
+
+def verde_tensor_digest_from_root(data_root: bytes, dtype: int, dims, nbytes: int) -> bytes:
+    dims = list(dims)
+    arr = (C.c_int64 * max(len(dims), 1))(*dims)
+    out = C.create_string_buffer(32)
+    check(lib().verde_tensor_digest_from_root(bytes(data_root), int(dtype), len(dims), arr, int(nbytes), out),
+          "verde_tensor_digest_from_root")
+    return out.raw
+
+
+def verde_chunk_leaves(t, stream=None):
+    """uint8 [ceil(nbytes/4096), 32] device tensor of the R11 chunk leaf hashes of t."""
+    if not t.is_contiguous():
+        raise RepopsError("verde_chunk_leaves: tensor must be contiguous")
+    nbytes = t.numel() * t.element_size()
+    out = torch.empty(((nbytes + 4095) // 4096, 32), dtype=torch.uint8, device=t.device)
+    check(lib().verde_chunk_leaves(_p(t), nbytes, _p(out), _stream(stream)), "verde_chunk_leaves")
+    return out

@@ -80,6 +80,12 @@ SIGNATURES = {
     "verde_node_digest": (i32, [vp, vp]),
     "verde_node_digests": (i32, [i64, vp, vp, vp, vp, vp, i64, vp, vp]),
     "verde_first_divergence": (i32, [vp, vp, i64, vp, vp]),
+    "verde_first_divergence_hashed": (i32, [vp, vp, i64, vp, vp]),
+    "verde_merkle_root_hashed": (i32, [vp, i64, vp]),
+    "verde_merkle_audit_path": (i32, [vp, i64, i64, i32, vp, vp]),
+    "verde_merkle_verify_path": (i32, [vp, i64, i64, vp, i32, vp, vp]),
+    "verde_tensor_digest_from_root": (i32, [vp, i32, i32, vp, i64, vp]),
+    "verde_chunk_leaves": (i32, [vp, i64, vp, vp]),
     "verde_root_plan_workspace_bytes": (i64, [i64]),
     "verde_root_plan_create": (i32, [i64, vp, vp, vp, vp, vp, vp, vp, vp, i64, vp]),
     "verde_root_plan_run": (i32, [vp, vp]),

@@ -140,19 +140,36 @@ class Sha256 {
 
 struct Node32 { uint8_t b[32]; };
 
-// RFC 6962 MTH of entries[lo, lo+n)  (entries are 32-byte digests)
-Node32 mth(const uint8_t *e, int64_t lo, int64_t n) {
+// RFC 6962 MTH of entries[lo, lo+n)  (entries are 32-byte digests).  hashed:
+// the items already are leaf hashes (e.g. SHA-256(0x00 || chunk) from the GPU),
+// so MTH of a single item is the item itself.
+Node32 mth(const uint8_t *e, int64_t lo, int64_t n, bool hashed = false) {
     Node32 out;
     Sha256 h;
     if (n == 1) {
-        h.u8(0x00).put(e + 32 * lo, 32).done(out.b);
+        if (hashed) memcpy(out.b, e + 32 * lo, 32);
+        else h.u8(0x00).put(e + 32 * lo, 32).done(out.b);
         return out;
     }
     int64_t k = 1;
     while (2 * k < n) k *= 2;
-    Node32 l = mth(e, lo, k), r = mth(e, lo + k, n - k);
+    Node32 l = mth(e, lo, k, hashed), r = mth(e, lo + k, n - k, hashed);
     h.u8(0x01).put(l.b, 32).put(r.b, 32).done(out.b);
     return out;
+}
+
+// RFC 6962 §2.1.1 PATH(m, D[lo, lo+n)): sibling subtree roots, leaf level first
+void audit_path(const uint8_t *e, int64_t lo, int64_t n, int64_t m, bool hashed, std::vector<Node32> &out) {
+    if (n <= 1) return;
+    int64_t k = 1;
+    while (2 * k < n) k *= 2;
+    if (m < k) {
+        audit_path(e, lo, k, m, hashed, out);
+        out.push_back(mth(e, lo + k, n - k, hashed));
+    } else {
+        audit_path(e, lo + k, n - k, m - k, hashed, out);
+        out.push_back(mth(e, lo, k, hashed));
+    }
 }
 
 }  // namespace
@@ -568,6 +585,98 @@ int verde_merkle_root(const uint8_t *leaves, int64_t n, uint8_t *root32) {
     REQ(leaves && root32, "merkle_root: null pointer");
     Node32 r = mth(leaves, 0, n);
     memcpy(root32, r.b, 32);
+    return REPOPS_OK;
+}
+
+int verde_merkle_root_hashed(const uint8_t *leaf_hashes, int64_t n, uint8_t *root32) {
+    if (n <= 0) return fail(REPOPS_EINVAL, "merkle_root_hashed: empty leaf list");
+    REQ(leaf_hashes && root32, "merkle_root_hashed: null pointer");
+    Node32 r = mth(leaf_hashes, 0, n, true);
+    memcpy(root32, r.b, 32);
+    return REPOPS_OK;
+}
+
+int verde_merkle_audit_path(const uint8_t *items, int64_t n, int64_t m, int hashed, uint8_t *path, int32_t *len) {
+    REQ(items && path && len && n >= 1 && m >= 0 && m < n, "merkle_audit_path: bad argument");
+    std::vector<Node32> p;
+    audit_path(items, 0, n, m, hashed != 0, p);
+    for (size_t i = 0; i < p.size(); ++i) memcpy(path + 32 * i, p[i].b, 32);
+    *len = (int32_t)p.size();
+    return REPOPS_OK;
+}
+
+int verde_merkle_verify_path(const uint8_t *leaf_hash, int64_t m, int64_t n, const uint8_t *path, int32_t len,
+                             const uint8_t *root32, int *ok) {
+    REQ(leaf_hash && root32 && ok && (len == 0 || path) && n >= 1 && m >= 0 && m < n && len >= 0,
+        "merkle_verify_path: bad argument");
+    // RFC 9162 §2.1.3.2 inclusion-proof verification
+    int64_t fn = m, sn = n - 1;
+    Node32 r;
+    memcpy(r.b, leaf_hash, 32);
+    *ok = 0;
+    for (int32_t i = 0; i < len; ++i) {
+        if (sn == 0) return REPOPS_OK;
+        const uint8_t *p = path + 32 * i;
+        Sha256 h;
+        if ((fn & 1) || fn == sn) {
+            h.u8(0x01).put(p, 32).put(r.b, 32).done(r.b);
+            if (!(fn & 1))
+                while (!(fn & 1) && fn != 0) { fn >>= 1; sn >>= 1; }
+        } else {
+            h.u8(0x01).put(r.b, 32).put(p, 32).done(r.b);
+        }
+        fn >>= 1;
+        sn >>= 1;
+    }
+    *ok = (sn == 0 && memcmp(r.b, root32, 32) == 0) ? 1 : 0;
+    return REPOPS_OK;
+}
+
+int verde_tensor_digest_from_root(const uint8_t *data_root, int dtype, int rank, const int64_t *dims,
+                                  int64_t nbytes, uint8_t *out32) {
+    REQ(out32 && rank >= 0 && rank <= 8 && (rank == 0 || dims) && nbytes >= 0, "tensor_digest_from_root: bad argument");
+    uint8_t empty[32];
+    if (nbytes == 0) {
+        Sha256 e;
+        e.done(empty);
+        data_root = empty;
+    }
+    REQ(data_root, "tensor_digest_from_root: null root");
+    Sha256 h;
+    h.u8(0x54).u8((uint8_t)dtype).u64((uint64_t)rank);
+    for (int i = 0; i < rank; ++i) h.u64((uint64_t)dims[i]);
+    h.u64((uint64_t)nbytes).u32(4096).put(data_root, 32).done(out32);
+    return REPOPS_OK;
+}
+
+int verde_chunk_leaves(const void *data, int64_t nbytes, uint8_t *leaves, void *stream) {
+    REQ(nbytes >= 0, "chunk_leaves: negative size");
+    if (nbytes == 0) return REPOPS_OK;
+    REQ(data && leaves, "chunk_leaves: null pointer");
+    return cuda_status(chunk_leaves_launch(static_cast<const uint8_t *>(data), nbytes, leaves, S(stream)),
+                       "chunk_leaves");
+}
+
+int verde_first_divergence_hashed(const uint8_t *seq0, const uint8_t *seq1, int64_t n, int64_t *d_out,
+                                  int64_t *rounds_out) {
+    REQ(n >= 1 && seq0 && seq1 && d_out, "first_divergence_hashed: bad argument");
+    int64_t lo = 0, len = n, rounds = 1;
+    Node32 a = mth(seq0, 0, n, true), b = mth(seq1, 0, n, true);
+    if (memcmp(a.b, b.b, 32) == 0) {
+        *d_out = -1;
+        if (rounds_out) *rounds_out = rounds;
+        return REPOPS_OK;
+    }
+    while (len > 1) {
+        int64_t k = 1;
+        while (2 * k < len) k *= 2;
+        Node32 l0 = mth(seq0, lo, k, true), l1 = mth(seq1, lo, k, true);
+        ++rounds;
+        if (memcmp(l0.b, l1.b, 32) != 0) len = k;
+        else { lo += k; len -= k; }
+    }
+    *d_out = lo;
+    if (rounds_out) *rounds_out = rounds;
     return REPOPS_OK;
 }
 

@@ -202,6 +202,22 @@ __global__ void leaf_kernel(const DevTensor *__restrict__ ts, int n, const int64
     }
 }
 
+// leaf hashes of one buffer: thread g hashes chunk g (verde_chunk_leaves)
+__global__ void chunk_leaf_kernel(const uint8_t *__restrict__ data, int64_t nbytes, int64_t nchunks,
+                                  uint8_t *__restrict__ out) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= nchunks) return;
+    const int64_t off = g * 4096;
+    uint32_t st[8];
+    hash_leaf(data + off, nbytes - off < 4096 ? nbytes - off : 4096, st);
+    uint8_t *o = out + 32 * g;  // big-endian digest bytes
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        o[4 * i] = (uint8_t)(st[i] >> 24); o[4 * i + 1] = (uint8_t)(st[i] >> 16);
+        o[4 * i + 2] = (uint8_t)(st[i] >> 8); o[4 * i + 3] = (uint8_t)st[i];
+    }
+}
+
 // one CTA (128 threads) per group of <= 256 nodes of one tensor
 __global__ void reduce_kernel(const int64_t *__restrict__ block_prefix, const int64_t *__restrict__ cur_off,
                               const int64_t *__restrict__ cur_cnt, const int64_t *__restrict__ nxt_off, int n,
@@ -610,3 +626,9 @@ cudaError_t root_plan_run(const void *plan, cudaStream_t s, int *nkernels) {
 }
 
 void root_plan_destroy(void *plan) { delete reinterpret_cast<RootPlanImpl *>(plan); }
+
+cudaError_t chunk_leaves_launch(const uint8_t *data, int64_t nbytes, uint8_t *leaves, cudaStream_t s) {
+    const int64_t n = (nbytes + 4095) / 4096;
+    chunk_leaf_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(data, nbytes, n, leaves);
+    return cudaGetLastError();
+}

@@ -21,5 +21,7 @@ cudaError_t root_plan_create(int64_t n, const uint8_t *blob, const int64_t *offs
 cudaError_t root_plan_run(const void *plan, cudaStream_t s, int *nkernels);
 void root_plan_destroy(void *plan);
 void commit_plan_destroy(void *plan);
+// R11 leaf hashes of every 4096-byte chunk of one buffer (device -> device)
+cudaError_t chunk_leaves_launch(const uint8_t *data, int64_t nbytes, uint8_t *leaves, cudaStream_t s);
 // tuning hook: resident leaf-kernel CTAs per SM (co-residency with GEMMs; bits-neutral)
 extern std::atomic<int> g_leaf_ctas_per_sm;

@@ -128,6 +128,8 @@ class GPT2Step:
         self.dev = torch.device("meta" if structure_only else device)
         self.s0, self.S_loc = shard_block(rank, world, cfg.shards)
         self._fault = None
+        self.keep_committed = False  # stash tensors an in-place writer overwrites (for disputes)
+        self.stash = {}
         self.step_no = 0
         c = cfg
         self.M = self.S_loc * c.seq
@@ -245,12 +247,14 @@ class GPT2Step:
                     repops_transpose(self.pview(self.params, name), out=t)
             self.launch(transposes)
         self.param_in = {}
+        self.param_in_node, self.adamw_node = {}, {}
         for name, shape, kind in self.specs:
             ids = [T_(f"param/{name}", self.pview(self.params, name), REPLICATED),
                    T_(f"m/{name}", self.pview(self.m, name), REPLICATED),
                    T_(f"v/{name}", self.pview(self.v, name), REPLICATED)]
             self.node(OP["PARAM_IN"], REPLICATED, {}, [], ids, f"in/{name}")
             self.param_in[name] = ids
+            self.param_in_node[name] = len(self.nodes) - 1
         # ---- per shard (global ids); only local shards get launches, but every
         # shard's structure is recorded so the node list is the global one
         self.shard_nodes = {}
@@ -672,6 +676,7 @@ class GPT2Step:
                      AK["adam_eps"]: f32bits(c.adam_eps), AK["wd"]: f32bits(c.wd),
                      AK["decay"]: int(len(shape) == 2)}
             self.node(OP["ADAMW"], REPLICATED, attrs, [p_, self.grad_out[name], m_, v_], outs, f"adamw/{name}")
+            self.adamw_node[name] = len(self.nodes) - 1
             self.adam_out[name] = outs
 
     # ------------------------------------------------------------------ finalisation
@@ -743,6 +748,18 @@ class GPT2Step:
             self._ev_act = torch.cuda.Event()
             self._ev_root = torch.cuda.Event()
         self._build_node_blob()
+        # committed tensors that a later node rewrites in place (same storage): the
+        # tied lm-head gradient (EMBED_BWD accumulates into it).  PARAM_IN outputs are
+        # excluded: a trainer serves those from its saved starting checkpoint.
+        self._overwritten = []
+        if not self.structure_only:
+            groups = {}
+            for tid, t in enumerate(self.tensors):
+                groups.setdefault((t.view.data_ptr(), t.view.numel()), []).append(tid)
+            for tids in groups.values():
+                for tid in tids[:-1]:
+                    if self.nodes[self.tensors[tid].producer].op != OP["PARAM_IN"]:
+                        self._overwritten.append(tid)
         if not self.structure_only:
             from . import RootPlan
             self.root_plan = RootPlan(self.node_blob, self.node_offs, self.node_slots, self.node_soffs,
@@ -776,6 +793,14 @@ class GPT2Step:
         self.node_soffs = np.asarray(soffs, np.int64)
 
     # ------------------------------------------------------------------ running
+    def batch_tokens(self, shard: int, step_index: int):
+        """The dataset's batch for `shard` at training step `step_index` (1-based; step t
+        consumes synthetic batch t-1), as the committed int32 [T+1] tensor -- what the
+        referee checks a disputed TOKENS_IN node against."""
+        c = self.cfg
+        h = synth.gpt2_tokens(c.vocab, c.seq, shard, step_index - 1, c.seed)
+        return torch.from_numpy(np.ascontiguousarray(h, dtype=np.int32))
+
     def set_tokens(self, step: int | None = None, host_tokens=None):
         """Load this rank's shards' tokens (synthetic recipe, or given host int32 [S_loc, T+1])."""
         c = self.cfg
@@ -814,11 +839,16 @@ class GPT2Step:
         runs on the side stream and join() waits for everything."""
         main = torch.cuda.current_stream()
         side = self.side if self.overlap_commits else main
+        self.stash = {}
         if side is not main:
             side.wait_stream(main)  # the step's inputs (tokens, checkpoint) are ready
         for i, (name, fns, _) in enumerate(self.phases):
             if commit and side is not main and i in self._wait_side_before:
                 main.wait_stream(side)  # in-place writers wait until their inputs are hashed
+            if self.keep_committed and i in self._wait_side_before:
+                for tid in self._overwritten:  # first in-place writer of the step comes next
+                    if tid not in self.stash:
+                        self.stash[tid] = self.tensors[tid].view.clone()
             for fn in fns:
                 fn()
             if inject is not None and inject[0] == name:

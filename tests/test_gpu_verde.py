@@ -99,3 +99,82 @@ def test_dispute_full_gpt2_mid_network():
     v = verde.dispute(cfg, node, elem=123457, bit=0)
     assert v.d == node and v.case == 3 and v.dishonest == 1
     assert v.rounds <= 14  # log2(3596) ~ 11.8 levels + root comparison
+
+
+# ---------------------------------------------------------------------- Phase 1 + Case 2(a) + chunk-level Case 3
+def _node_named(prog, name):
+    return next(nd.index for nd in prog.nodes if nd.name == name)
+
+
+def test_phase1_multilevel_then_phase2_chunk_decision(tiny_program):
+    """12-step run, a 1-bit fault in step 7: Phase 1 narrows 12 -> 3 -> 2 -> 1 steps with
+    re-execution of the diverging segments only; Phase 2 finds the node; the referee
+    recomputes just the 4 KiB chunk holding the flipped element."""
+    from paper_2502_19405_b200 import verde
+    cfg, prog = tiny_program
+    node = _node_named(prog, "s3/h1/fc")
+    numel = int(np.prod(prog.tensors[prog.nodes[node].outputs[0]].view.shape))
+    elem = numel - 5
+    for dishonest in (0, 1):
+        runs = [verde.TrainingRun(cfg), verde.TrainingRun(cfg, fault=(7, node, elem, 0, 0))]
+        if dishonest == 0:
+            runs.reverse()
+        for r in runs:
+            r.train(12, 4)
+        p1, v = verde.resolve(runs[0], runs[1], 12, counts=(4, 2))
+        assert p1.step == 7
+        assert [lv[:2] for lv in p1.levels] == [(0, 12), (6, 9), (6, 8)]
+        assert all(r.reexecuted == 3 + 2 + 1 for r in runs)  # levels 1, 2 + the Phase 2 step
+        assert v.d == node and v.case == 3 and v.dishonest == dishonest
+        assert v.chunk == elem // 1024
+        out = prog.tensors[prog.nodes[node].outputs[0]].view
+        assert v.recomputed <= out.shape[1] * (1024 // out.shape[1] + 2) < out.numel()
+
+
+@pytest.mark.parametrize("tamper_step", [1, 4])
+def test_case2a_checkpoint_membership_proof(tiny_program, tamper_step):
+    """A trainer silently alters one weight between checkpoints: the first diverging
+    node is that parameter's PARAM_IN; only the honest trainer can prove membership of
+    its digest in h_start (C0 tree for step 1, the previous step's AdamW node later)."""
+    from paper_2502_19405_b200 import verde
+    cfg, prog = tiny_program
+    runs = [verde.TrainingRun(cfg), verde.TrainingRun(cfg, tamper=(tamper_step, "h0.attn.w", 17, 3))]
+    for r in runs:
+        r.train(6, 3)
+    p1, v = verde.resolve(runs[0], runs[1], 6, counts=(3, 2))
+    assert p1.step == tamper_step
+    assert v.case == 2 and v.dishonest == 1 and "membership" in v.detail
+    assert v.d == prog.param_in_node["h0.attn.w"]
+
+
+def test_case2_training_data_checked_against_dataset(tiny_program):
+    from paper_2502_19405_b200 import verde
+    cfg, prog = tiny_program
+    runs = [verde.TrainingRun(cfg, tamper=(3, "__tokens__", 40, 0)), verde.TrainingRun(cfg)]
+    for r in runs:
+        r.train(4, 4)
+    p1, v = verde.resolve(runs[0], runs[1], 4, counts=(4,))
+    assert p1.step == 3 and v.case == 2 and v.dishonest == 0 and "dataset" in v.detail
+    assert prog.nodes[v.d].op == 2  # TOKENS_IN
+
+
+def test_chunk_recompute_equals_full_replay(tiny_program):
+    """The referee's partial recompute gives exactly the bytes of the full operator."""
+    from paper_2502_19405_b200 import verde
+    from paper_2502_19405_b200.gpt2 import GPT2Step
+    cfg, prog = tiny_program
+    st = GPT2Step(cfg)
+    st.set_tokens(0)
+    ck = (st.params.clone(), st.m.clone(), st.v.clone())
+    st.run()
+    tr = verde.Trainer(st, ck)
+    for name in ("s2/h0/qkv", "s5/head/lm_head", "s1/h1/fc2_dgrad", "s0/h1/fc_wgrad", "s6/h0/gelu", "s4/h1/res2",
+                 "s3/h0/softmax"):
+        d = _node_named(prog, name)
+        o = tr.open(d)
+        ins = tr.input_tensors(d)
+        full = verde.referee_recompute(prog, d, ins, o.in_digests, 1)[0].reshape(-1).cpu().numpy().tobytes()
+        n_chunks = (len(full) + 4095) // 4096
+        for c in sorted({0, n_chunks // 2, n_chunks - 1}):
+            got, count = verde.referee_recompute_chunk(prog, d, ins, o.in_digests, 0, c, 1)
+            assert got == full[4096 * c:4096 * (c + 1)], (name, c)
