@@ -65,6 +65,9 @@ def lib():
                 "orc_add": (None, [vp, vp, i64, vp]),
                 "orc_gelu": (None, [vp, i64, vp]),
                 "orc_relu": (None, [vp, i64, vp]),
+                "orc_sin_vec": (None, [vp, i64, vp]),
+                "orc_cos_vec": (None, [vp, i64, vp]),
+                "orc_rope_tables": (None, [vp, i64, i64, vp, vp]),
                 "orc_relu_backward": (None, [vp, vp, i64, vp]),
                 "orc_gelu_backward": (None, [vp, vp, i64, vp]),
                 "orc_softmax": (None, [vp, i64, i64, i64, i32, vp, i64]),
@@ -214,6 +217,26 @@ def gelu_backward(x, dy):
     dx = np.empty_like(x)
     lib().orc_gelu_backward(_p(x), _p(dy), x.size, _p(dx))
     return dx
+
+
+def sin(x):
+    """orc_sin (Cephes sinf chain, reading R26)."""
+    return _vec("orc_sin_vec", x)
+
+
+def cos(x):
+    """orc_cos (Cephes cosf chain, reading R26)."""
+    return _vec("orc_cos_vec", x)
+
+
+def rope_tables_from_inv_freq(inv_freq, T):
+    """orc_rope_tables: (cos, sin) [T, h] of angle fmul(t, inv_freq[i]) (reading R26)."""
+    f = _f32(inv_freq)
+    h = f.size
+    c = np.empty((T, h), np.float32)
+    s = np.empty((T, h), np.float32)
+    lib().orc_rope_tables(_p(f), T, h, _p(c), _p(s))
+    return c, s
 
 
 def relu(x):

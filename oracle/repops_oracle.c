@@ -240,6 +240,79 @@ float orc_tanh(float u) {
     return copysignf(t, u);
 }
 
+/* sin / cos ("exp, sin, cos, tanh"; reading R26): Cephes sinf/cosf --
+ * octant j = trunc(|x| * 4/pi) rounded up to even, Cody-Waite reduction
+ * r = ((|x| - y DP1) - y DP2) - y DP3 (separate mul / sub; |x| > 8192: |x| - y pi/4),
+ * then on [-pi/4, pi/4] the sine polynomial r + r z P(z) (one fmaf) or the cosine
+ * polynomial 1 - z/2 + z^2 Q(z), selected and signed by the octant.
+ * |x| > 16777215 returns +0 (Cephes TLOSS); +-inf and NaN return NaN. */
+static const float SC_FOPI = 1.27323954473516f, SC_PIO4 = 0.7853981633974483096f;
+static const float SC_DP1 = 0.78515625f, SC_DP2 = 2.4187564849853515625e-4f, SC_DP3 = 3.77489497744594108e-8f;
+
+static float sc_reduce(float a, int *oct) {
+    float t = a * SC_FOPI;
+    uint32_t j = (uint32_t)t;                 /* truncation; 0 <= t < 2^24 */
+    float y = (float)j;
+    if (j & 1u) { j += 1u; y = y + 1.0f; }
+    *oct = (int)(j & 7u);
+    if (a > 8192.0f) return a - y * SC_PIO4;
+    return ((a - y * SC_DP1) - y * SC_DP2) - y * SC_DP3;
+}
+
+static float sc_sinpoly(float r, float z) {
+    float p = fmaf(-1.9515295891E-4f, z, 8.3321608736E-3f);
+    p = fmaf(p, z, -1.6666654611E-1f);
+    return fmaf(p * z, r, r);
+}
+
+static float sc_cospoly(float z) {
+    float p = fmaf(2.443315711809948E-5f, z, -1.388731625493765E-3f);
+    p = fmaf(p, z, 4.166664568298827E-2f);
+    float v = p * (z * z);
+    v = v - 0.5f * z;
+    return v + 1.0f;
+}
+
+float orc_sin(float x) {
+    if (x != x || x == bits2f(0x7F800000u) || x == bits2f(0xFF800000u)) return bits2f(0x7FC00000u);
+    int neg = x < 0.0f;
+    float a = neg ? -x : x;
+    if (a > 16777215.0f) return 0.0f;
+    int j;
+    float r = sc_reduce(a, &j);
+    if (j > 3) { neg = !neg; j -= 4; }
+    float z = r * r;
+    float v = (j == 1 || j == 2) ? sc_cospoly(z) : sc_sinpoly(r, z);
+    return neg ? -v : v;
+}
+
+float orc_cos(float x) {
+    if (x != x || x == bits2f(0x7F800000u) || x == bits2f(0xFF800000u)) return bits2f(0x7FC00000u);
+    float a = x < 0.0f ? -x : x;
+    if (a > 16777215.0f) return 0.0f;
+    int j, neg = 0;
+    float r = sc_reduce(a, &j);
+    if (j > 3) { neg = !neg; j -= 4; }
+    if (j > 1) neg = !neg;
+    float z = r * r;
+    float v = (j == 1 || j == 2) ? sc_sinpoly(r, z) : sc_cospoly(z);
+    return neg ? -v : v;
+}
+
+void orc_sin_vec(const float *x, i64 n, float *y) { for (i64 i = 0; i < n; ++i) y[i] = orc_sin(x[i]); }
+void orc_cos_vec(const float *x, i64 n, float *y) { for (i64 i = 0; i < n; ++i) y[i] = orc_cos(x[i]); }
+
+/* RoPE tables from the inverse frequencies (reading R26): angle = fmul(float(t), inv_freq[i]),
+ * cos[t][i] = R-COS(angle), sin[t][i] = R-SIN(angle), t < T, i < h. */
+void orc_rope_tables(const float *inv_freq, i64 T, i64 h, float *cosv, float *sinv) {
+    for (i64 t = 0; t < T; ++t)
+        for (i64 i = 0; i < h; ++i) {
+            float ang = (float)t * inv_freq[i];
+            cosv[t * h + i] = orc_cos(ang);
+            sinv[t * h + i] = orc_sin(ang);
+        }
+}
+
 /* Reading R6: rsqrt = IEEE fdiv(1, IEEE fsqrt(x)), both correctly rounded. */
 float orc_rsqrt(float x) { return canon(1.0f / sqrtf(x)); }
 

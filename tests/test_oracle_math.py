@@ -8,6 +8,7 @@ import numpy as np
 import pytest
 
 import oracle
+import synth
 
 
 def u2f(u):
@@ -125,3 +126,47 @@ def test_gelu_pins():
     # dy scaling is one IEEE multiply
     dy2 = np.full_like(x, 0.375)
     assert np.array_equal(oracle.gelu_backward(x, dy2), (oracle.gelu_backward(x, dy) * np.float32(0.375)))
+
+
+# ---------------------------------------------------------------------- sin / cos (reading R26)
+def _bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+def test_sin_cos_accuracy_sweep():
+    """Cephes sinf/cosf accuracy: |error| <= 2^-23 over [-3000, 3000] against float64,
+    relative error <= 1e-7 on the reduced interval [-pi/4, pi/4] (Cephes: 7.8e-8)."""
+    x = np.linspace(-3000, 3000, 600001).astype(np.float32)
+    x64 = x.astype(np.float64)
+    assert np.max(np.abs(oracle.sin(x) - np.sin(x64))) <= 2.0 ** -23
+    assert np.max(np.abs(oracle.cos(x) - np.cos(x64))) <= 2.0 ** -23
+    y = np.linspace(-0.785, 0.785, 100001).astype(np.float32)
+    y64 = y.astype(np.float64)
+    nz = np.abs(y64) > 1e-30
+    assert np.max(np.abs(oracle.sin(y)[nz] - np.sin(y64[nz])) / np.abs(np.sin(y64[nz]))) <= 1e-7
+    assert np.max(np.abs(oracle.cos(y) - np.cos(y64)) / np.cos(y64)) <= 1e-7
+
+
+def test_sin_cos_exact_identities_and_special_values():
+    x = synth.uniform(3, 100001, 2000.0)
+    assert np.array_equal(_bits(oracle.sin(-x)), _bits(-oracle.sin(x)))   # odd, bit for bit
+    assert np.array_equal(_bits(oracle.cos(-x)), _bits(oracle.cos(x)))    # even, bit for bit
+    z = np.float32([0.0, -0.0])
+    # the chain's zero: fmaf(p z, r, r) = (-0)(-0) + (-0) = +0, so sin(-0) = +0 (R26)
+    assert _bits(oracle.sin(z)).tolist() == [0, 0]
+    assert oracle.cos(z).tolist() == [1.0, 1.0]
+    bad = np.float32([np.inf, -np.inf, np.nan])
+    assert np.all(_bits(oracle.sin(bad)) == 0x7FC00000) and np.all(_bits(oracle.cos(bad)) == 0x7FC00000)
+    assert oracle.sin(np.float32([3e7]))[0] == 0.0 and oracle.cos(np.float32([-3e7]))[0] == 0.0  # Cephes TLOSS
+    s, c = oracle.sin(x).astype(np.float64), oracle.cos(x).astype(np.float64)
+    assert np.max(np.abs(s * s + c * c - 1.0)) < 4e-7
+
+
+def test_rope_tables_from_inv_freq():
+    hd, T = 128, 2048
+    inv = (500000.0 ** (-np.arange(0, hd, 2, dtype=np.float64) / hd)).astype(np.float32)
+    c, s = oracle.rope_tables_from_inv_freq(inv, T)
+    assert np.all(c[0] == 1.0) and np.all(_bits(s[0]) == 0)                # t = 0: angle +0
+    ang = (np.arange(T, dtype=np.float32)[:, None] * inv[None, :]).astype(np.float32)  # the rounded fmul
+    assert np.max(np.abs(c - np.cos(ang.astype(np.float64)))) <= 2.0 ** -23
+    assert np.max(np.abs(s - np.sin(ang.astype(np.float64)))) <= 2.0 ** -23
