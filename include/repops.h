@@ -156,6 +156,13 @@ int repops_add(const float *a, const float *b, int64_t n, float *y, void *stream
  * give +0); dx = x > 0 ? g : +0 (subgradient 0 at x = 0); a NaN x gives the canonical NaN.
  * x, g, y, dx: device float[n], contiguous; y / dx may alias x / g. */
 int repops_relu(const float *x, int64_t n, float *y, void *stream);
+/* sin / cos (P:572 lists them among the re-implemented functions; reading R26): the
+ * Cephes sinf / cosf chains; |x| > 16777215 -> +0, +-inf / NaN -> NaN. */
+int repops_sin(const float *x, int64_t n, float *y, void *stream);
+int repops_cos(const float *x, int64_t n, float *y, void *stream);
+/* RoPE tables (R26): cos[t][i] = R-COS(a), sin[t][i] = R-SIN(a), a = fmul(float(t), inv_freq[i]),
+ * t < T (< 2^24), i < h.  inv_freq: device float[h]; cos, sin: device float[T * h] (row-major). */
+int repops_rope_tables(const float *inv_freq, int64_t T, int64_t h, float *cosv, float *sinv, void *stream);
 int repops_relu_backward(const float *x, const float *g, int64_t n, float *dx, void *stream);
 
 /* R-EMB forward: x0[t][c] = fadd(wte[tok[t]][c], wpe[t mod T][c]); tok device int32. */

@@ -22,7 +22,7 @@ __all__ = [
     "repops_gemm", "repops_gemm_strided_batched", "repops_sum_rows", "repops_sum_cols_seq", "repops_tree_sum",
     "repops_softmax", "repops_softmax_backward", "repops_layernorm", "repops_layernorm_backward",
     "repops_layernorm_backward_params", "repops_cross_entropy", "repops_exp", "repops_log", "repops_tanh",
-    "repops_rsqrt", "repops_gelu", "repops_gelu_backward", "repops_relu", "repops_relu_backward", "repops_add", "repops_embedding",
+    "repops_rsqrt", "repops_gelu", "repops_gelu_backward", "repops_relu", "repops_relu_backward", "repops_sin", "repops_cos", "repops_rope_tables", "repops_add", "repops_embedding",
     "repops_embedding_backward", "repops_adamw", "repops_flip_bit", "verde_commit_tensor",
     "verde_commit_tensors", "verde_merkle_root", "verde_sha256", "verde_node_digest",
     "verde_first_divergence", "verde_digest_from_subroots", "launch_count", "CommitWorkspace", "CommitPlan",
@@ -269,6 +269,26 @@ def repops_rsqrt(x, out=None, stream=None):
 
 def repops_gelu(x, out=None, stream=None):
     return _unary("repops_gelu", x, out, stream)
+
+
+def repops_sin(x, out=None, stream=None):
+    """R26 (Cephes sinf chain)."""
+    return _unary("repops_sin", x, out, stream)
+
+
+def repops_cos(x, out=None, stream=None):
+    """R26 (Cephes cosf chain)."""
+    return _unary("repops_cos", x, out, stream)
+
+
+def repops_rope_tables(inv_freq, T, cos=None, sin=None, stream=None):
+    """R26: (cos, sin) [T, h] with angle fmul(t, inv_freq[i])."""
+    _contig(inv_freq, "inv_freq")
+    h = inv_freq.numel()
+    cos = torch.empty((T, h), dtype=torch.float32, device=inv_freq.device) if cos is None else cos
+    sin = torch.empty((T, h), dtype=torch.float32, device=inv_freq.device) if sin is None else sin
+    check(lib().repops_rope_tables(_p(inv_freq), int(T), h, _p(cos), _p(sin), _stream(stream)), "repops_rope_tables")
+    return cos, sin
 
 
 def repops_relu(x, out=None, stream=None):

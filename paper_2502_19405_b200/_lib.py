@@ -54,6 +54,9 @@ SIGNATURES = {
     "repops_rsqrt": (i32, [vp, i64, vp, vp]),
     "repops_gelu": (i32, [vp, i64, vp, vp]),
     "repops_relu": (i32, [vp, i64, vp, vp]),
+    "repops_sin": (i32, [vp, i64, vp, vp]),
+    "repops_cos": (i32, [vp, i64, vp, vp]),
+    "repops_rope_tables": (i32, [vp, i64, i64, vp, vp, vp]),
     "repops_relu_backward": (i32, [vp, vp, i64, vp, vp]),
     "repops_gelu_backward": (i32, [vp, vp, i64, vp, vp]),
     "repops_add": (i32, [vp, vp, i64, vp, vp]),

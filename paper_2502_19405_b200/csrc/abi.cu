@@ -377,6 +377,15 @@ UNARY(repops_tanh, launch_tanh)
 UNARY(repops_rsqrt, launch_rsqrt)
 UNARY(repops_gelu, launch_gelu)
 UNARY(repops_relu, launch_relu)
+UNARY(repops_sin, launch_sin)
+UNARY(repops_cos, launch_cos)
+
+int repops_rope_tables(const float *inv_freq, int64_t T, int64_t h, float *cosv, float *sinv, void *stream) {
+    REQ(T >= 0 && h >= 0 && T < (1 << 24), "rope_tables: bad T / h");
+    if (T * h == 0) return REPOPS_OK;
+    REQ(inv_freq && cosv && sinv, "rope_tables: null pointer");
+    return cuda_status(launch_rope_tables(inv_freq, T, h, cosv, sinv, S(stream)), "rope_tables");
+}
 
 int repops_relu_backward(const float *x, const float *g, int64_t n, float *dx, void *stream) {
     REQ(n >= 0, "relu_backward: negative n");

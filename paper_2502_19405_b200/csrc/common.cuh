@@ -148,6 +148,53 @@ RO_DEV float tanh_rn(float u) {
 
 RO_DEV float rsqrt_rn(float x) { return __fdiv_rn(1.0f, __fsqrt_rn(x)); }
 
+// sin / cos (R26): Cephes sinf/cosf.  Octant from trunc(|x| * 4/pi) rounded up to
+// even; three-constant Cody-Waite reduction (|x| > 8192: one pi/4 product); sine
+// polynomial fma(r z P(z)... , r, r) or cosine 1 - z/2 + z^2 Q(z) by octant; sign by
+// octant (and, for sin, by x).  |x| > 16777215 -> +0; inf / NaN -> canonical NaN.
+RO_DEV float sc_reduce_rn(float a, int &oct) {
+    const float t = __fmul_rn(a, 1.27323954473516f);
+    uint32_t j = __float2uint_rz(t);
+    float y = __uint2float_rn(j);
+    if (j & 1u) {
+        j += 1u;
+        y = __fadd_rn(y, 1.0f);
+    }
+    oct = (int)(j & 7u);
+    if (a > 8192.0f) return __fsub_rn(a, __fmul_rn(y, 0.7853981633974483096f));
+    float r = __fsub_rn(a, __fmul_rn(y, 0.78515625f));
+    r = __fsub_rn(r, __fmul_rn(y, 2.4187564849853515625e-4f));
+    return __fsub_rn(r, __fmul_rn(y, 3.77489497744594108e-8f));
+}
+RO_DEV float sc_sin_poly(float r, float z) {
+    float p = __fmaf_rn(-1.9515295891E-4f, z, 8.3321608736E-3f);
+    p = __fmaf_rn(p, z, -1.6666654611E-1f);
+    return __fmaf_rn(__fmul_rn(p, z), r, r);
+}
+RO_DEV float sc_cos_poly(float z) {
+    float p = __fmaf_rn(2.443315711809948E-5f, z, -1.388731625493765E-3f);
+    p = __fmaf_rn(p, z, 4.166664568298827E-2f);
+    const float v = __fsub_rn(__fmul_rn(p, __fmul_rn(z, z)), __fmul_rn(0.5f, z));
+    return __fadd_rn(v, 1.0f);
+}
+RO_DEV float sincos_rn(float x, bool want_cos) {
+    const float a = fabsf(x);
+    if (!(a <= 3.4028235e38f)) return __uint_as_float(0x7FC00000u);  // NaN, +-inf
+    if (a > 16777215.0f) return 0.0f;
+    int j;
+    const float r = sc_reduce_rn(a, j);
+    bool neg = want_cos ? false : (x < 0.0f);
+    if (j > 3) {
+        neg = !neg;
+        j -= 4;
+    }
+    if (want_cos && j > 1) neg = !neg;
+    const float z = __fmul_rn(r, r);
+    const bool sin_branch = (j == 1 || j == 2) == want_cos;
+    const float v = sin_branch ? sc_sin_poly(r, z) : sc_cos_poly(z);
+    return neg ? -v : v;
+}
+
 // GELU (tanh form, R13): u = c*(x + 0.044715 x^3), y = 0.5x(1 + tanh u)
 RO_DEV float gelu_rn(float v) {
     float x2 = __fmul_rn(v, v);

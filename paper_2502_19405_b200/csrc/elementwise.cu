@@ -41,6 +41,19 @@ struct TanhF { RO_DEV float operator()(float x) const { return canon(tanh_rn(x))
 struct RsqrtF { RO_DEV float operator()(float x) const { return canon(rsqrt_rn(x)); } };
 struct GeluF { RO_DEV float operator()(float x) const { return canon(gelu_rn(x)); } };
 struct GeluBwdF { RO_DEV float operator()(float x, float dy) const { return canon(gelu_grad_rn(x, dy)); } };
+struct SinF { RO_DEV float operator()(float x) const { return ro::sincos_rn(x, false); } };
+struct CosF { RO_DEV float operator()(float x) const { return ro::sincos_rn(x, true); } };
+// R26 RoPE tables: angle = fmul(float(t), inv_freq[i]); one thread per (t, i)
+__global__ void rope_tables_kernel(const float *__restrict__ inv_freq, int64_t T, int64_t h, float *__restrict__ cosv,
+                                   float *__restrict__ sinv) {
+    const int64_t n = T * h;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = q / h, i = q % h;
+        const float ang = __fmul_rn((float)t, __ldg(inv_freq + i));  // t < 2^24: exact conversion
+        cosv[q] = ro::sincos_rn(ang, true);
+        sinv[q] = ro::sincos_rn(ang, false);
+    }
+}
 // R24 (config-1 MLP): relu(x) = x > 0 ? x : +0; relu'(x) g = x > 0 ? g : +0; NaN x -> NaN
 struct ReluF {
     RO_DEV float operator()(float x) const { return x != x ? canon(x) : (x > 0.f ? x : 0.f); }
@@ -202,6 +215,13 @@ cudaError_t launch_rsqrt(const float *x, int64_t n, float *y, cudaStream_t s) { 
 cudaError_t launch_gelu(const float *x, int64_t n, float *y, cudaStream_t s) { return run_unary(x, n, y, s, GeluF{}); }
 
 cudaError_t launch_relu(const float *x, int64_t n, float *y, cudaStream_t s) { return run_unary(x, n, y, s, ReluF{}); }
+cudaError_t launch_sin(const float *x, int64_t n, float *y, cudaStream_t s) { return run_unary(x, n, y, s, SinF{}); }
+cudaError_t launch_cos(const float *x, int64_t n, float *y, cudaStream_t s) { return run_unary(x, n, y, s, CosF{}); }
+cudaError_t launch_rope_tables(const float *inv_freq, int64_t T, int64_t h, float *cosv, float *sinv, cudaStream_t s) {
+    if (T * h == 0) return cudaSuccess;
+    rope_tables_kernel<<<ew_grid(T * h), 256, 0, s>>>(inv_freq, T, h, cosv, sinv);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_relu_backward(const float *x, const float *g, int64_t n, float *dx, cudaStream_t s) {
     if (n == 0) return cudaSuccess;

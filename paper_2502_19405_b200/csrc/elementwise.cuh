@@ -8,6 +8,9 @@ cudaError_t launch_log(const float *x, int64_t n, float *y, cudaStream_t s);
 cudaError_t launch_tanh(const float *x, int64_t n, float *y, cudaStream_t s);
 cudaError_t launch_rsqrt(const float *x, int64_t n, float *y, cudaStream_t s);
 cudaError_t launch_gelu(const float *x, int64_t n, float *y, cudaStream_t s);
+cudaError_t launch_sin(const float *x, int64_t n, float *y, cudaStream_t s);
+cudaError_t launch_cos(const float *x, int64_t n, float *y, cudaStream_t s);
+cudaError_t launch_rope_tables(const float *inv_freq, int64_t T, int64_t h, float *cosv, float *sinv, cudaStream_t s);
 cudaError_t launch_relu(const float *x, int64_t n, float *y, cudaStream_t s);
 cudaError_t launch_relu_backward(const float *x, const float *g, int64_t n, float *dx, cudaStream_t s);
 cudaError_t launch_gelu_backward(const float *x, const float *dy, int64_t n, float *dx, cudaStream_t s);

@@ -305,6 +305,19 @@ def test_adamw_parity():
         assert_bits(host(tv), rv, "adam v")
 
 
+def test_sin_cos_and_rope_tables_exact():
+    x = np.concatenate([synth.uniform(51, 200003, 3000.0), synth.uniform(52, 1001, 1e7),
+                        np.float32([0.0, -0.0, np.inf, -np.inf, np.nan, 8192.0, 8192.5, 16777215.0, 3e7,
+                                    np.pi / 4, -np.pi / 4, 1e-40])])
+    assert_bits(host(R.repops_sin(dev(x))), oracle.sin(x), "sin")
+    assert_bits(host(R.repops_cos(dev(x))), oracle.cos(x), "cos")
+    inv = (500000.0 ** (-np.arange(0, 128, 2, dtype=np.float64) / 128)).astype(np.float32)
+    c, s_ = R.repops_rope_tables(dev(inv), 2048)
+    rc, rs = oracle.rope_tables_from_inv_freq(inv, 2048)
+    assert_bits(host(c), rc, "rope cos")
+    assert_bits(host(s_), rs, "rope sin")
+
+
 def test_relu_and_backward_exact():
     x = np.concatenate([synth.uniform(41, 100003, 3.0),
                         np.float32([0.0, -0.0, np.inf, -np.inf, np.nan, 1e-45, -1e-45])])
