@@ -14,7 +14,7 @@ import numpy as np
 
 import synth
 
-from . import add, gemm, rmsnorm, rope, softmax, swiglu
+from . import add, gemm, rmsnorm, rope, rope_tables_from_inv_freq, softmax, swiglu
 
 
 def _c(a):
@@ -28,9 +28,10 @@ def run_prefill(cfg, tokens=None):
     specs = synth.llama_param_specs(L, d, H, KV, hd, F, V)
     W = {n: synth.llama_param(n, s, k, cfg.seed) for n, s, k in specs}
     tok = synth.llama_tokens(V, T, cfg.seed) if tokens is None else tokens
-    cos, sin = synth.rope_tables(T, hd, cfg.theta)
+    inv = synth.rope_inv_freq(hd, cfg.theta)
+    cos, sin = rope_tables_from_inv_freq(inv, T)   # R26
     scale = float(np.float32(1.0 / np.sqrt(hd)))
-    out = {"tokens": tok.astype(np.int32), "rope/cos": cos, "rope/sin": sin}
+    out = {"tokens": tok.astype(np.int32), "rope/inv_freq": inv, "rope/cos": cos, "rope/sin": sin}
     x = _c(W["tok_emb"][tok])  # exact gather
     out["x0"] = x
     for l in range(L):

@@ -32,12 +32,12 @@ import synth
 
 from . import (EPI_SCALE, CommitPlan, RootPlan, repops_add, repops_copy2d, repops_fill_uniform, repops_gather_rows,
                repops_gemm_strided_batched, repops_rmsnorm, repops_rope, repops_softmax, repops_swiglu,
-               repops_transpose, verde_commit_tensors)
+               repops_rope_tables, repops_transpose, verde_commit_tensors)
 from ._lib import check, lib
 from .dist import all_gather_rows, gather_shard_digests, shard_block
 
 OP = dict(PARAM_IN=1, TOKENS_IN=2, TABLES_IN=3, EMBED=4, RMSNORM=5, QKV=6, ROPE=7, SCORES=8, SOFTMAX=9, PV=10,
-          OPROJ=11, RESIDUAL=12, GATE=13, UP=14, SWIGLU=15, DOWN=16, LMHEAD=17)
+          OPROJ=11, RESIDUAL=12, GATE=13, UP=14, SWIGLU=15, DOWN=16, LMHEAD=17, ROPE_TABLES=18)
 REPLICATED = 0xFFFFFFFF
 
 
@@ -110,9 +110,9 @@ class LlamaPrefill:
         E = lambda *s: torch.empty(*s, dtype=torch.float32, device=dev)  # noqa: E731
         L, d, hd, qh = c.n_layer, c.d, c.hd, c.qh
         self.tok = torch.empty(T, dtype=torch.int32, device=dev)
-        cos, sin = synth.rope_tables(T, hd, c.theta)
-        self.cos = torch.from_numpy(cos).to(dev) if not self.structure_only else E(T, hd // 2)
-        self.sin = torch.from_numpy(sin).to(dev) if not self.structure_only else E(T, hd // 2)
+        inv = synth.rope_inv_freq(hd, c.theta)
+        self.inv_freq = torch.from_numpy(inv).to(dev) if not self.structure_only else E(hd // 2)
+        self.cos, self.sin = E(T, hd // 2), E(T, hd // 2)  # R26 tables, computed by the pass
         # local weights in block layout
         self.w = []
         for _ in range(L):
@@ -228,9 +228,12 @@ class LlamaPrefill:
             N_(OP["PARAM_IN"], REPLICATED, {}, [], [pin[name]], "in/" + name)
         t_tok = T_("tokens", self.tok, REPLICATED)
         N_(OP["TOKENS_IN"], REPLICATED, {}, [], [t_tok], "tokens")
-        t_cos, t_sin = T_("rope/cos", self.cos, REPLICATED), T_("rope/sin", self.sin, REPLICATED)
+        t_inv = T_("rope/inv_freq", self.inv_freq, REPLICATED)
         N_(OP["TABLES_IN"], REPLICATED, {1: struct.unpack("<Q", struct.pack("<d", c.theta))[0]}, [],
-           [t_cos, t_sin], "rope_tables")
+           [t_inv], "rope_inv_freq")
+        self._launch(lambda: repops_rope_tables(self.inv_freq, T, cos=self.cos, sin=self.sin))
+        t_cos, t_sin = T_("rope/cos", self.cos, REPLICATED), T_("rope/sin", self.sin, REPLICATED)
+        N_(OP["ROPE_TABLES"], REPLICATED, {}, [t_inv], [t_cos, t_sin], "rope_tables")
         self._launch(lambda: repops_gather_rows(self.tok_emb, self.tok, out=self.x[0]))
         t_x = T_("x0", self.x[0], REPLICATED)
         N_(OP["EMBED"], REPLICATED, {}, [t_tok, pin["tok_emb"]], [t_x], "embed")

@@ -147,6 +147,12 @@ def llama_tokens(vocab, seq, seed=0):
     return integers(seed_for("llama-tokens", seed), seq, vocab)
 
 
+def rope_inv_freq(hd, theta=500000.0):
+    """RoPE inverse frequencies theta^(-2i/hd), i < hd/2 (float64, rounded once): input data
+    of config 4; the cos/sin tables are computed from them by R26."""
+    return (theta ** (-np.arange(0, hd, 2, dtype=np.float64) / hd)).astype(np.float32)
+
+
 def rope_tables(seq, hd, theta=500000.0):
     """cos/sin tables [seq, hd/2] (float64 angles rounded once to binary32): input data."""
     inv = theta ** (-np.arange(0, hd, 2, dtype=np.float64) / hd)
