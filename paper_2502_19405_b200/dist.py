@@ -53,6 +53,35 @@ def dp_tree_combine(local_parts, world: int, tree, pg=None, out=None):
     return tree([allp[r] for r in range(world)], out)  # top levels, identical on every rank
 
 
+def dp_tree_combine_sliced(local_parts, world: int, tree, pg=None, out=None):
+    """Bandwidth-optimal R-TREE_S: the same bits as dp_tree_combine with
+    2(G-1)/G x P instead of (G-1) x P bytes received per rank.  Each rank reduces its
+    aligned local subtree, an all-to-all hands rank r slice r of every rank's partial,
+    rank r applies the top levels to its slice (elementwise, so slicing cannot change
+    a bit), and an all-gather of the summed slices rebuilds the full gradient."""
+    if world == 1:
+        return tree(local_parts, out)
+    import torch.distributed as dist
+    partial = tree(local_parts, None).reshape(-1)
+    n = partial.numel()
+    per = -(-n // world)
+    send = torch.zeros(world * per, dtype=partial.dtype, device=partial.device)
+    send[:n] = partial
+    recv = torch.empty_like(send)
+    if send.is_cuda and dist.get_backend(pg) != "nccl":  # gloo test transport: stage through the host
+        rh = torch.empty(recv.shape, dtype=recv.dtype)
+        dist.all_to_all_single(rh, send.cpu(), group=pg)
+        recv.copy_(rh)
+    else:
+        dist.all_to_all_single(recv, send, group=pg)    # recv[j] = slice r of rank j's partial
+    mine = tree([recv[j * per:(j + 1) * per] for j in range(world)], None)
+    full = all_gather_rows(mine, world, pg).reshape(-1)[:n]
+    if out is None:
+        return full.reshape(local_parts[0].shape)
+    out.copy_(full.reshape(out.shape))
+    return out
+
+
 def gather_shard_digests(table: torch.Tensor, rep_slots: int, shard_slots: int, s0: int, s_loc: int, world: int,
                          pg=None) -> torch.Tensor:
     """C2: fill every shard region of the digest table from the rank that owns it.

@@ -42,7 +42,7 @@ from . import (EPI_BIAS, EPI_SCALE, CommitPlan, repops_add, repops_cross_entropy
                repops_layernorm_backward_params, repops_softmax, repops_softmax_backward, repops_sum_cols_seq,
                repops_adamw, repops_tree_sum)
 from ._lib import check, lib
-from .dist import all_gather_rows, dp_tree_combine, gather_shard_digests, shard_block
+from .dist import all_gather_rows, dp_tree_combine, dp_tree_combine_sliced, gather_shard_digests, shard_block
 
 # node operator codes (u16)
 OP = dict(PARAM_IN=1, TOKENS_IN=2, EMBED=3, LAYERNORM=4, LINEAR=5, ATTN_SCORES=6, SOFTMAX=7, ATTN_PV=8,
@@ -129,6 +129,7 @@ class GPT2Step:
         self.s0, self.S_loc = shard_block(rank, world, cfg.shards)
         self._fault = None
         self.keep_committed = False  # stash tensors an in-place writer overwrites (for disputes)
+        self.sliced_combine = True   # R-TREE_S via all-to-all + all-gather (same bits, fewer bytes)
         self.stash = {}
         self.step_no = 0
         c = cfg
@@ -648,7 +649,8 @@ class GPT2Step:
 
         def tree():
             parts = [self.glocal[q] for q in range(self.S_loc)]
-            dp_tree_combine(parts, self.world, lambda ps, out: repops_tree_sum(ps, out=out), self.pg, out=self.grad)
+            combine = dp_tree_combine_sliced if self.sliced_combine else dp_tree_combine
+            combine(parts, self.world, lambda ps, out: repops_tree_sum(ps, out=out), self.pg, out=self.grad)
         self.launch(tree)
         T_ = self._T
         self.grad_out = {}

@@ -110,6 +110,8 @@ def _worker(rank, world, port, q):
         parts[0][:3] = torch.tensor([2.0 ** 24, 1.0, 1.0])
         parts[4][:3] = torch.tensor([1.0, 1.0, 2.0 ** 24])
         got = D.dp_tree_combine(parts[s0:s0 + per], world, _oracle_tree)
+        got2 = D.dp_tree_combine_sliced(parts[s0:s0 + per], world, _oracle_tree)
+        assert got2.numpy().tobytes() == got.numpy().tobytes()
         # digest table: replicated region + shard regions; each rank fills its own
         rep, ss = 3, 5
         table = torch.zeros((rep + S * ss, 32), dtype=torch.uint8)
@@ -122,7 +124,7 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
+@pytest.mark.parametrize("world", [2, 4])
 def test_gloo_dp_combine_and_digest_gather(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
