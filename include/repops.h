@@ -180,6 +180,13 @@ int repops_embedding_backward(const int32_t *tok, int64_t ntok, int64_t T, const
  * bc2 = 1 - b2^step with b^step by iterated binary32 multiplication (host side). */
 int repops_adamw(float *p, const float *g, float *m, float *v, int64_t n, int64_t step,
                  float lr, float b1, float b2, float eps, float wd, int decay, void *stream);
+/* R-ADAMW over nseg (<= 256) parameter tensors stored back to back in p, g, m, v
+ * (one launch per optimizer step): tensor k = elements [seg_start[k], seg_start[k+1]),
+ * seg_start[0] == 0, with weight decay iff decay[k] != 0.  Bit-identical to nseg
+ * repops_adamw calls.  seg_start (nseg + 1) and decay (nseg) are host arrays. */
+int repops_adamw_segments(float *p, const float *g, float *m, float *v, int nseg, const int64_t *seg_start,
+                          const uint8_t *decay, int64_t step, float lr, float b1, float b2, float eps, float wd,
+                          void *stream);
 
 /* ------------------------------------------------------------------ Llama operators (config 4)
  * R-RMSNORM (R20): ms = CDOT(x,x)/n; rstd = fdiv(1, fsqrt(ms + eps)); y = fmul(fmul(x, rstd), w).

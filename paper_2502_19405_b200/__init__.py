@@ -339,6 +339,19 @@ def repops_embedding_backward(tok, dx0, T, dwte, dwpe=None, stream=None):
     return dwte, dwpe
 
 
+def repops_adamw_segments(p, g, m, v, seg_start, decay, step, lr, b1, b2, eps, wd, stream=None):
+    """AdamW over back-to-back parameter tensors in one launch; seg_start: nseg+1 element
+    offsets (first 0), decay: nseg flags.  In place on p, m, v."""
+    for t, nm in ((p, "p"), (g, "g"), (m, "m"), (v, "v")):
+        _contig(t, nm)
+    nseg = len(decay)
+    st = (C.c_int64 * (nseg + 1))(*[int(x) for x in seg_start])
+    dc = (C.c_uint8 * nseg)(*[1 if d else 0 for d in decay])
+    check(lib().repops_adamw_segments(_p(p), _p(g), _p(m), _p(v), nseg, st, dc, int(step), float(lr), float(b1),
+                                      float(b2), float(eps), float(wd), _stream(stream)), "repops_adamw_segments")
+    return p, m, v
+
+
 def repops_adamw(p, g, m, v, step, lr, b1, b2, eps, wd, decay, stream=None):
     """In place on p, m, v."""
     for t, nm in ((p, "p"), (g, "g"), (m, "m"), (v, "v")):

@@ -54,6 +54,7 @@ SIGNATURES = {
     "repops_rsqrt": (i32, [vp, i64, vp, vp]),
     "repops_gelu": (i32, [vp, i64, vp, vp]),
     "repops_relu": (i32, [vp, i64, vp, vp]),
+    "repops_adamw_segments": (i32, [vp, vp, vp, vp, i32, vp, vp, i64, f32, f32, f32, f32, f32, vp]),
     "repops_sin": (i32, [vp, i64, vp, vp]),
     "repops_cos": (i32, [vp, i64, vp, vp]),
     "repops_rope_tables": (i32, [vp, i64, i64, vp, vp, vp]),

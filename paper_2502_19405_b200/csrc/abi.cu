@@ -425,6 +425,25 @@ int repops_embedding_backward(const int32_t *tok, int64_t ntok, int64_t T, const
     return cuda_status(launch_embedding_backward(tok, ntok, T, dx0, C, dwte, dwpe, S(stream)), "embedding_backward");
 }
 
+int repops_adamw_segments(float *p, const float *g, float *m, float *v, int nseg, const int64_t *seg_start,
+                          const uint8_t *decay, int64_t step, float lr, float b1, float b2, float eps, float wd,
+                          void *stream) {
+    REQ(nseg >= 1 && nseg <= ADAM_MAX_SEGS && seg_start && decay && step >= 1, "adamw_segments: bad segments");
+    REQ(seg_start[0] == 0, "adamw_segments: seg_start[0] must be 0");
+    for (int k = 0; k < nseg; ++k) REQ(seg_start[k + 1] >= seg_start[k], "adamw_segments: starts must not decrease");
+    if (seg_start[nseg] == 0) return REPOPS_OK;
+    REQ(p && g && m && v, "adamw_segments: null pointer");
+    volatile float pw1 = b1, pw2 = b2;  // R15, as repops_adamw
+    for (int64_t i = 1; i < step; ++i) {
+        pw1 = pw1 * b1;
+        pw2 = pw2 * b2;
+    }
+    volatile float bc1 = 1.0f - pw1, bc2 = 1.0f - pw2, omb1 = 1.0f - b1, omb2 = 1.0f - b2;
+    return cuda_status(launch_adamw_segments(p, g, m, v, nseg, seg_start, decay, lr, b1, b2, eps, wd, bc1, bc2, omb1,
+                                             omb2, S(stream)),
+                       "adamw_segments");
+}
+
 int repops_adamw(float *p, const float *g, float *m, float *v, int64_t n, int64_t step, float lr, float b1, float b2,
                  float eps, float wd, int decay, void *stream) {
     REQ(n >= 0 && step >= 1, "adamw: bad n/step");

@@ -144,6 +144,66 @@ __global__ void adamw_kernel(float *__restrict__ p, const float *__restrict__ g,
     }
 }
 
+// AdamW over many parameter tensors stored back to back (one launch per step):
+// element i belongs to segment k with start[k] <= i < start[k+1], whose decay flag
+// selects the weight-decay term; the element chain is adam_elem (same bits as the
+// per-tensor launch).
+struct AdamSegs {
+    int64_t start[ADAM_MAX_SEGS + 1];
+    uint8_t decay[ADAM_MAX_SEGS];
+    int n;
+};
+
+RO_DEV int adam_seg_of(const AdamSegs &s, int64_t i) {
+    int lo = 0, hi = s.n;  // start[lo] <= i < start[hi]
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (s.start[mid] <= i) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void adamw_seg_kernel(float *__restrict__ p, const float *__restrict__ g, float *__restrict__ m,
+                                 float *__restrict__ v, int64_t n, AdamHyper h, AdamSegs segs) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const bool al = aligned16(p) && aligned16(g) && aligned16(m) && aligned16(v);
+    const int64_t n4 = al ? n / 4 : 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+        float4 pp = reinterpret_cast<float4 *>(p)[i];
+        float4 gg = __ldg(reinterpret_cast<const float4 *>(g) + i);
+        float4 mm = reinterpret_cast<float4 *>(m)[i];
+        float4 vv = reinterpret_cast<float4 *>(v)[i];
+        const int k = adam_seg_of(segs, 4 * i);
+        AdamHyper hk = h;
+        hk.decay = segs.decay[k];
+        if (4 * i + 3 < segs.start[k + 1]) {  // the usual case: all four in one tensor
+            adam_elem(pp.x, gg.x, mm.x, vv.x, hk);
+            adam_elem(pp.y, gg.y, mm.y, vv.y, hk);
+            adam_elem(pp.z, gg.z, mm.z, vv.z, hk);
+            adam_elem(pp.w, gg.w, mm.w, vv.w, hk);
+        } else {
+            float *pe = &pp.x, *me = &mm.x, *ve = &vv.x;
+            const float *ge = &gg.x;
+            for (int e = 0; e < 4; ++e) {
+                hk.decay = segs.decay[adam_seg_of(segs, 4 * i + e)];
+                adam_elem(pe[e], ge[e], me[e], ve[e], hk);
+            }
+        }
+        reinterpret_cast<float4 *>(p)[i] = pp;
+        reinterpret_cast<float4 *>(m)[i] = mm;
+        reinterpret_cast<float4 *>(v)[i] = vv;
+    }
+    for (int64_t i = n4 * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        float pp = p[i], mm = m[i], vv = v[i];
+        AdamHyper hk = h;
+        hk.decay = segs.decay[adam_seg_of(segs, i)];
+        adam_elem(pp, g[i], mm, vv, hk);
+        p[i] = pp;
+        m[i] = mm;
+        v[i] = vv;
+    }
+}
+
 // R-EMB forward: x0[t][c] = wte[tok[t]][c] + wpe[t mod T][c]; one CTA-row per token
 __global__ void embedding_kernel(const int32_t *__restrict__ tok, int64_t ntok, int64_t T,
                                  const float *__restrict__ wte, const float *__restrict__ wpe, int64_t C,
@@ -263,6 +323,20 @@ cudaError_t launch_adamw(float *p, const float *g, float *m, float *v, int64_t n
     if (n == 0) return cudaSuccess;
     AdamHyper h{lr, b1, b2, eps, wd, bc1, bc2, omb1, omb2, decay};
     adamw_kernel<<<ew_grid(n), 256, 0, s>>>(p, g, m, v, n, h);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_adamw_segments(float *p, const float *g, float *m, float *v, int nseg, const int64_t *start,
+                                  const uint8_t *decay, float lr, float b1, float b2, float eps, float wd, float bc1,
+                                  float bc2, float omb1, float omb2, cudaStream_t s) {
+    const int64_t n = start[nseg];
+    if (n == 0) return cudaSuccess;
+    AdamHyper h{lr, b1, b2, eps, wd, bc1, bc2, omb1, omb2, 0};
+    AdamSegs segs{};
+    for (int k = 0; k <= nseg; ++k) segs.start[k] = start[k];
+    for (int k = 0; k < nseg; ++k) segs.decay[k] = decay[k] ? 1 : 0;
+    segs.n = nseg;
+    adamw_seg_kernel<<<ew_grid(n), 256, 0, s>>>(p, g, m, v, n, h, segs);
     return cudaGetLastError();
 }
 

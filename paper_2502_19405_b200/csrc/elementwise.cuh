@@ -8,6 +8,10 @@ cudaError_t launch_log(const float *x, int64_t n, float *y, cudaStream_t s);
 cudaError_t launch_tanh(const float *x, int64_t n, float *y, cudaStream_t s);
 cudaError_t launch_rsqrt(const float *x, int64_t n, float *y, cudaStream_t s);
 cudaError_t launch_gelu(const float *x, int64_t n, float *y, cudaStream_t s);
+constexpr int ADAM_MAX_SEGS = 256;
+cudaError_t launch_adamw_segments(float *p, const float *g, float *m, float *v, int nseg, const int64_t *start,
+                                  const uint8_t *decay, float lr, float b1, float b2, float eps, float wd, float bc1,
+                                  float bc2, float omb1, float omb2, cudaStream_t s);
 cudaError_t launch_sin(const float *x, int64_t n, float *y, cudaStream_t s);
 cudaError_t launch_cos(const float *x, int64_t n, float *y, cudaStream_t s);
 cudaError_t launch_rope_tables(const float *inv_freq, int64_t T, int64_t h, float *cosv, float *sinv, cudaStream_t s);

@@ -40,7 +40,7 @@ from . import (EPI_BIAS, EPI_SCALE, CommitPlan, repops_add, repops_cross_entropy
                repops_embedding_backward, repops_gelu, repops_gelu_backward, repops_gemm,
                repops_gemm_strided_batched, repops_layernorm, repops_layernorm_backward,
                repops_layernorm_backward_params, repops_softmax, repops_softmax_backward, repops_sum_cols_seq,
-               repops_adamw, repops_tree_sum)
+               repops_adamw, repops_adamw_segments, repops_tree_sum)
 from ._lib import check, lib
 from .dist import all_gather_rows, dp_tree_combine, dp_tree_combine_sliced, gather_shard_digests, shard_block
 
@@ -661,12 +661,14 @@ class GPT2Step:
             self.grad_out[name] = t
         self.phase("adamw")
 
+        # one launch for all parameter tensors (they are stored back to back in
+        # spec order); per-tensor decay flags, same element chain as repops_adamw
+        seg_start = [self.off[name][0] for name, _, _ in self.specs] + [self.P]
+        seg_decay = [len(shape) == 2 for _, shape, _ in self.specs]
+
         def adam():
-            for name, shape, kind in self.specs:
-                decay = len(shape) == 2
-                repops_adamw(self.pview(self.params, name), self.pview(self.grad, name), self.pview(self.m, name),
-                             self.pview(self.v, name), self.step_no + 1, c.lr, c.beta1, c.beta2, c.adam_eps, c.wd,
-                             decay)
+            repops_adamw_segments(self.params, self.grad, self.m, self.v, seg_start, seg_decay, self.step_no + 1,
+                                  c.lr, c.beta1, c.beta2, c.adam_eps, c.wd)
         self.launch(adam)
         self.adam_out = {}
         for name, shape, kind in self.specs:

@@ -318,6 +318,24 @@ def test_sin_cos_and_rope_tables_exact():
     assert_bits(host(s_), rs, "rope sin")
 
 
+def test_adamw_segments_equals_per_tensor_launches():
+    sizes = [5, 768, 3, 4097, 64, 1, 1000]
+    start = np.concatenate([[0], np.cumsum(sizes)])
+    decay = [1, 0, 1, 1, 0, 0, 1]
+    n = int(start[-1])
+    p, g = synth.uniform(61, n, 0.05), synth.uniform(62, n, 0.01)
+    m, v = synth.uniform(63, n, 0.001), np.abs(synth.uniform(64, n, 1e-4))
+    for step in (1, 7):
+        a = [dev(t) for t in (p, g, m, v)]
+        R.repops_adamw_segments(a[0], a[1], a[2], a[3], start, decay, step, 6e-4, 0.9, 0.95, 1e-8, 0.1)
+        b = [dev(t) for t in (p, g, m, v)]
+        for k in range(len(sizes)):
+            sl = slice(int(start[k]), int(start[k + 1]))
+            R.repops_adamw(b[0][sl], b[1][sl], b[2][sl], b[3][sl], step, 6e-4, 0.9, 0.95, 1e-8, 0.1, decay[k])
+        for x, y in zip(a, b):
+            assert np.array_equal(host(x).view(np.uint32), host(y).view(np.uint32))
+
+
 def test_relu_and_backward_exact():
     x = np.concatenate([synth.uniform(41, 100003, 3.0),
                         np.float32([0.0, -0.0, np.inf, -np.inf, np.nan, 1e-45, -1e-45])])
