@@ -759,11 +759,24 @@ class GPT2Step:
         if not self.structure_only:
             groups = {}
             for tid, t in enumerate(self.tensors):
-                groups.setdefault((t.view.data_ptr(), t.view.numel()), []).append(tid)
+                if t.view.numel() and t.view.device.type != "meta":  # remote shards hold empty placeholders
+                    groups.setdefault((t.view.data_ptr(), t.view.numel()), []).append(tid)
             for tids in groups.values():
                 for tid in tids[:-1]:
                     if self.nodes[self.tensors[tid].producer].op != OP["PARAM_IN"]:
                         self._overwritten.append(tid)
+        # Targeted waits: an in-place writer waits only for the commit plan that
+        # hashed what it overwrites (not for the whole side-stream backlog):
+        #   embed_bwd -> the plan holding the tied lm-head gradients (_overwritten),
+        #   adamw     -> the plan holding the PARAM_IN tensors (p, m, v).
+        ph_of = lambda t: deferred_phase if self._tensor_phase.get(t) is None else self._tensor_phase[t]  # noqa: E731
+        adamw_phase = next(i for i, p in enumerate(self.phases) if p[0] == "adamw")
+        pin = [t for ids in self.param_in.values() for t in ids]
+        self._wait_on = {adamw_phase: max(ph_of(t) for t in pin)}
+        if self._overwritten:
+            self._wait_on[deferred_phase] = max(ph_of(t) for t in self._overwritten)
+        assert all(w in self.plan_after or self.structure_only for w in self._wait_on.values())
+        self._plan_ev = {} if self.structure_only else {ph: torch.cuda.Event() for ph in self.plan_after}
         if not self.structure_only:
             from . import RootPlan
             self.root_plan = RootPlan(self.node_blob, self.node_offs, self.node_slots, self.node_soffs,
@@ -847,8 +860,8 @@ class GPT2Step:
         if side is not main:
             side.wait_stream(main)  # the step's inputs (tokens, checkpoint) are ready
         for i, (name, fns, _) in enumerate(self.phases):
-            if commit and side is not main and i in self._wait_side_before:
-                main.wait_stream(side)  # in-place writers wait until their inputs are hashed
+            if commit and side is not main and i in self._wait_on:
+                main.wait_event(self._plan_ev[self._wait_on[i]])  # what it overwrites is hashed
             if self.keep_committed and i in self._wait_side_before:
                 for tid in self._overwritten:  # first in-place writer of the step comes next
                     if tid not in self.stash:
@@ -864,6 +877,7 @@ class GPT2Step:
                 else:
                     side.wait_stream(main)
                     plan.run(stream=side)
+                    self._plan_ev[i].record(side)
                     if i == self._last_act_plan:
                         self._ev_act.record(side)
         if side is not main:

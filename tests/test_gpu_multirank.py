@@ -38,6 +38,10 @@ def _worker(rank, world, port, tiny, q):
         # the updated parameters themselves must be identical on every rank
         pdig = st.digests_host.numpy()[st.tensors[st.adam_out["wte"][0]].slot].tobytes()
         q.put((rank, root.hex(), loss, pdig.hex()))
+    except Exception:  # report instead of leaving the parent waiting on the queue
+        import traceback
+        q.put((rank, "ERROR " + traceback.format_exc(), None, None))
+        raise
     finally:
         dist.destroy_process_group()
 
@@ -49,7 +53,11 @@ def _run(world, tiny):
     ps = [ctx.Process(target=_worker, args=(r, world, port, tiny, q)) for r in range(world)]
     for p in ps:
         p.start()
-    res = [q.get(timeout=900) for _ in ps]
+    res = []
+    for _ in ps:
+        r = q.get(timeout=900)
+        assert not str(r[1]).startswith("ERROR"), f"rank {r[0]} failed:\n{r[1]}"
+        res.append(r)
     for p in ps:
         p.join(timeout=120)
         assert p.exitcode == 0
