@@ -217,6 +217,22 @@ class GPT2Train:
         self.st.run(commit=self.commit, join=False)
         self.st.device_root(sync=False)       # C2 gather + node digests + step root on the GPU; 32 B D2H
 
+    @staticmethod
+    def isolated_gemm(wl, world, local, steps=2):
+        import torch
+        commit = wl.commit
+        wl.commit = False
+        try:
+            for _ in range(1):
+                wl.step()
+            torch.cuda.synchronize()
+            _, tot, _, _ = timed(wl, steps, world, local)
+        finally:
+            wl.commit = commit
+        g_ms, g_fl, _ = tot.get("gemm", (0.0, 0, 0))
+        g_ms = max_over_ranks(g_ms, world)
+        return g_fl / (g_ms * 1e-3) / 1e12 if g_ms else None
+
     def join(self):
         self.st.join()
         self.root = self.st.root_bytes()
@@ -488,6 +504,11 @@ def main():
         if wname == "gpt2":
             res["root"] = wl.root.hex()
             res["loss"] = wl.st.loss()
+            # diagnostic (not the headline): the same GEMM launches with the commit side
+            # stream idle, i.e. the GEMM kernels' own rate without the SHA-256 sharing the SMs
+            iso = GPT2Train.isolated_gemm(wl, world, local)
+            if iso:
+                res["gemm_isolated"] = iso
         elif wname == "llama":
             res["root"] = wl.root.hex()
         else:
@@ -526,6 +547,10 @@ def main():
                                         achieved / fp32_peak_tflops(clk["sm_mhz"]) if clk["sm_mhz"] else -1),
                        "gemm_ms_per_step": gemm_ms_step, "gemm_launches_per_step": gemm_launches,
                        "traffic": profiled_gemm_traffic(),
+                       "achieved_commit_idle": head.get("gemm_isolated"),
+                       "frac_commit_idle": (head["gemm_isolated"] / peak) if head.get("gemm_isolated") else None,
+                       "commit_idle_note": "diagnostic: the step's GEMMs timed live in 2 extra steps run with "
+                                           "commit=False (no SHA-256 on the side stream sharing the SMs)",
                        "traffic_note": "DRAM bytes (read + write) per R-GEMM launch, mean over one GPT-2 step's "
                                        "GEMM launches, from the committed ncu launch list "
                                        "profiles/r01_gpt2_step_launches.csv (cold-cache replay)"}
