@@ -66,6 +66,9 @@ def lib():
                 "orc_gelu": (None, [vp, i64, vp]),
                 "orc_relu": (None, [vp, i64, vp]),
                 "orc_sin_vec": (None, [vp, i64, vp]),
+                "orc_erf_vec": (None, [vp, i64, vp]),
+                "orc_gelu_erf": (None, [vp, i64, vp]),
+                "orc_gelu_erf_backward": (None, [vp, vp, i64, vp]),
                 "orc_cos_vec": (None, [vp, i64, vp]),
                 "orc_rope_tables": (None, [vp, i64, i64, vp, vp]),
                 "orc_relu_backward": (None, [vp, vp, i64, vp]),
@@ -216,6 +219,25 @@ def gelu_backward(x, dy):
     dy = _f32(dy)
     dx = np.empty_like(x)
     lib().orc_gelu_backward(_p(x), _p(dy), x.size, _p(dx))
+    return dx
+
+
+def erf(x):
+    """orc_erf (Cephes erff / erfcf chain, reading R27)."""
+    return _vec("orc_erf_vec", x)
+
+
+def gelu_erf(x):
+    """orc_gelu_erf: exact GELU 0.5 x (1 + erf(x / sqrt 2)) (reading R27)."""
+    return _vec("orc_gelu_erf", x)
+
+
+def gelu_erf_backward(x, dy):
+    """orc_gelu_erf_backward (reading R27)."""
+    x = _f32(x)
+    dy = _f32(dy)
+    dx = np.empty_like(x)
+    lib().orc_gelu_erf_backward(_p(x), _p(dy), x.size, _p(dx))
     return dx
 
 

@@ -313,6 +313,63 @@ void orc_rope_tables(const float *inv_freq, i64 T, i64 h, float *cosv, float *si
         }
 }
 
+/* erf (exact GELU of BERT-family models, "GeLU, and ERF"; reading R27):
+ * Cephes erff / erfcf.  |x| <= 1: x T(x^2) (Horner, fmaf); |x| > 1: 1 - erfc(|x|) with
+ * erfc(a) = exp(-a^2) (1/a) P(1/a^2) (P for a < 2, R for a >= 2), exp = R-EXP; the sign
+ * of x is applied last (erf is odd).  a^2 is one rounded product. */
+static float horner(const float *c, int n, float x) {
+    float p = c[0];
+    for (int i = 1; i <= n; ++i) p = fmaf(p, x, c[i]);
+    return p;
+}
+static const float ERF_T[7] = {7.853861353153693E-5f, -8.010193625184903E-4f, 5.188327685732524E-3f,
+                               -2.685381193529856E-2f, 1.128358514861418E-1f, -3.761262582423300E-1f,
+                               1.128379165726710E+0f};
+static const float ERFC_P[9] = {2.326819970068386E-2f, -1.387039388740657E-1f, 3.687424674597105E-1f,
+                                -5.824733027278666E-1f, 6.210004621745983E-1f, -4.944515323274145E-1f,
+                                3.404879937665872E-1f, -2.741127028184656E-1f, 5.638259427386472E-1f};
+static const float ERFC_R[8] = {-1.047766399936249E+1f, 1.297719955372516E+1f, -7.495518717768503E+0f,
+                                2.921019019210786E+0f, -1.015265279202700E+0f, 4.218463358204948E-1f,
+                                -2.820767439740514E-1f, 5.641895067754075E-1f};
+
+float orc_erf(float x) {
+    if (x != x) return bits2f(0x7FC00000u);
+    float a = fabsf(x);
+    float y;
+    if (a <= 1.0f) {
+        y = a * horner(ERF_T, 6, a * a);
+    } else if (a >= 10.0f) {
+        y = 1.0f;
+    } else {
+        float z = orc_exp(-(a * a));
+        float q = 1.0f / a;
+        float p = (a < 2.0f) ? horner(ERFC_P, 8, q * q) : horner(ERFC_R, 7, q * q);
+        y = 1.0f - (z * q) * p;
+    }
+    return x < 0.0f ? -y : y;
+}
+
+void orc_erf_vec(const float *x, i64 n, float *y) { for (i64 i = 0; i < n; ++i) y[i] = orc_erf(x[i]); }
+
+/* exact GELU (R27): y = (0.5 x) (1 + erf(x * 0.70710678118654752)) */
+void orc_gelu_erf(const float *x, i64 n, float *y) {
+    for (i64 i = 0; i < n; ++i) {
+        float v = x[i];
+        y[i] = canon((0.5f * v) * (1.0f + orc_erf(v * 0.70710678118654752f)));
+    }
+}
+
+/* exact GELU backward (R27): cdf = 0.5 (1 + erf(x / sqrt 2)), pdf = R-EXP(-(0.5 (x x))) / sqrt(2 pi),
+ * dx = dy (cdf + x pdf) */
+void orc_gelu_erf_backward(const float *x, const float *dy, i64 n, float *dx) {
+    for (i64 i = 0; i < n; ++i) {
+        float v = x[i];
+        float cdf = 0.5f * (1.0f + orc_erf(v * 0.70710678118654752f));
+        float pdf = orc_exp(-(0.5f * (v * v))) * 0.39894228040143268f;
+        dx[i] = canon(dy[i] * (cdf + v * pdf));
+    }
+}
+
 /* Reading R6: rsqrt = IEEE fdiv(1, IEEE fsqrt(x)), both correctly rounded. */
 float orc_rsqrt(float x) { return canon(1.0f / sqrtf(x)); }
 

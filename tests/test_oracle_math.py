@@ -170,3 +170,35 @@ def test_rope_tables_from_inv_freq():
     ang = (np.arange(T, dtype=np.float32)[:, None] * inv[None, :]).astype(np.float32)  # the rounded fmul
     assert np.max(np.abs(c - np.cos(ang.astype(np.float64)))) <= 2.0 ** -23
     assert np.max(np.abs(s - np.sin(ang.astype(np.float64)))) <= 2.0 ** -23
+
+
+# ---------------------------------------------------------------------- erf / exact GELU (reading R27)
+def test_erf_accuracy_and_exact_properties():
+    x = np.linspace(-6, 6, 240001).astype(np.float32)
+    ref = np.array([math.erf(float(v)) for v in x])
+    e = oracle.erf(x)
+    assert np.max(np.abs(e - ref)) <= 1.5e-7                      # Cephes erff / erfcf accuracy
+    small = (np.abs(x) <= 1) & (x != 0)
+    assert np.max(np.abs(e[small] - ref[small]) / np.abs(ref[small])) <= 2e-7
+    assert np.all(np.diff(e.astype(np.float64)) >= 0)            # monotone on the sweep
+    y = synth.uniform(8, 50001, 8.0)
+    assert np.array_equal(_bits(oracle.erf(-y)), _bits(-oracle.erf(y)))  # odd, bit for bit
+    sp = oracle.erf(np.float32([0.0, 10.0, -10.0, 1e30, np.inf, -np.inf, np.nan]))
+    assert sp[:6].tolist() == [0.0, 1.0, -1.0, 1.0, 1.0, -1.0] and _bits(sp)[6] == 0x7FC00000
+
+
+def test_gelu_erf_against_float64_and_its_derivative():
+    x = synth.uniform(9, 100001, 8.0)
+    x64 = x.astype(np.float64)
+    ref = 0.5 * x64 * (1 + np.array([math.erf(v / math.sqrt(2)) for v in x64]))
+    g = oracle.gelu_erf(x)
+    assert np.all(np.abs(g - ref) <= 4e-7 * np.abs(x64) + 1e-7)
+    assert oracle.gelu_erf(np.float32([20.0]))[0] == 20.0 and oracle.gelu_erf(np.float32([0.0]))[0] == 0.0
+    # backward = d/dx of the float64 GELU (central differences away from nothing special)
+    xs = synth.uniform(10, 200, 4.0).astype(np.float64)
+    h = 1e-4
+    f = lambda v: 0.5 * v * (1 + np.array([math.erf(t / math.sqrt(2)) for t in v]))  # noqa: E731
+    fd = (f(xs + h) - f(xs - h)) / (2 * h)
+    dy = synth.uniform(11, 200, 2.0)
+    got = oracle.gelu_erf_backward(xs.astype(np.float32), dy)
+    assert np.allclose(got, fd * dy, rtol=1e-5, atol=1e-6)
