@@ -160,6 +160,16 @@ int repops_relu(const float *x, int64_t n, float *y, void *stream);
  * Cephes sinf / cosf chains; |x| > 16777215 -> +0, +-inf / NaN -> NaN. */
 int repops_sin(const float *x, int64_t n, float *y, void *stream);
 int repops_cos(const float *x, int64_t n, float *y, void *stream);
+/* erf and exact GELU (BERT-family models; "LayerNorm, GeLU, and ERF"; reading R27):
+ * erf = the Cephes erff / erfcf chain (DESIGN.md §3 R27, exp = R-EXP); NaN -> canonical NaN.
+ * gelu_erf: y = fmul(fmul(0.5, x), fadd(1, erf(fmul(x, 1/sqrt 2)))).
+ * gelu_erf_backward: dx = dy * (cdf + x * pdf), cdf = 0.5 (1 + erf(x / sqrt 2)),
+ * pdf = R-EXP(-(0.5 x^2)) * 1/sqrt(2 pi), each product / sum one rounded op in that order.
+ * x, dy, y, dx: device float[n], contiguous (any alignment); y / dx may alias x / dy.
+ * Errors: REPOPS_EINVAL for n < 0 or a null pointer with n > 0. */
+int repops_erf(const float *x, int64_t n, float *y, void *stream);
+int repops_gelu_erf(const float *x, int64_t n, float *y, void *stream);
+int repops_gelu_erf_backward(const float *x, const float *dy, int64_t n, float *dx, void *stream);
 /* RoPE tables (R26): cos[t][i] = R-COS(a), sin[t][i] = R-SIN(a), a = fmul(float(t), inv_freq[i]),
  * t < T (< 2^24), i < h.  inv_freq: device float[h]; cos, sin: device float[T * h] (row-major). */
 int repops_rope_tables(const float *inv_freq, int64_t T, int64_t h, float *cosv, float *sinv, void *stream);

@@ -22,7 +22,8 @@ __all__ = [
     "repops_gemm", "repops_gemm_strided_batched", "repops_sum_rows", "repops_sum_cols_seq", "repops_tree_sum",
     "repops_softmax", "repops_softmax_backward", "repops_layernorm", "repops_layernorm_backward",
     "repops_layernorm_backward_params", "repops_cross_entropy", "repops_exp", "repops_log", "repops_tanh",
-    "repops_rsqrt", "repops_gelu", "repops_gelu_backward", "repops_relu", "repops_relu_backward", "repops_sin", "repops_cos", "repops_rope_tables", "repops_add", "repops_embedding",
+    "repops_rsqrt", "repops_gelu", "repops_gelu_backward", "repops_relu", "repops_relu_backward", "repops_sin", "repops_cos", "repops_erf", "repops_gelu_erf",
+    "repops_gelu_erf_backward", "repops_rope_tables", "repops_add", "repops_embedding",
     "repops_embedding_backward", "repops_adamw", "repops_flip_bit", "verde_commit_tensor",
     "verde_commit_tensors", "verde_merkle_root", "verde_sha256", "verde_node_digest",
     "verde_first_divergence", "verde_digest_from_subroots", "launch_count", "CommitWorkspace", "CommitPlan",
@@ -279,6 +280,26 @@ def repops_sin(x, out=None, stream=None):
 def repops_cos(x, out=None, stream=None):
     """R26 (Cephes cosf chain)."""
     return _unary("repops_cos", x, out, stream)
+
+
+def repops_erf(x, out=None, stream=None):
+    """R27 (Cephes erff / erfcf chain)."""
+    return _unary("repops_erf", x, out, stream)
+
+
+def repops_gelu_erf(x, out=None, stream=None):
+    """R27: exact GELU 0.5 x (1 + erf(x / sqrt 2))."""
+    return _unary("repops_gelu_erf", x, out, stream)
+
+
+def repops_gelu_erf_backward(x, dy, out=None, stream=None):
+    """R27: dx = dy (cdf + x pdf)."""
+    _contig(x, "x"), _contig(dy, "dy")
+    if out is None:
+        out = torch.empty_like(x)
+    check(lib().repops_gelu_erf_backward(_p(x), _p(dy), x.numel(), _p(out), _stream(stream)),
+          "repops_gelu_erf_backward")
+    return out
 
 
 def repops_rope_tables(inv_freq, T, cos=None, sin=None, stream=None):

@@ -57,6 +57,9 @@ SIGNATURES = {
     "repops_adamw_segments": (i32, [vp, vp, vp, vp, i32, vp, vp, i64, f32, f32, f32, f32, f32, vp]),
     "repops_sin": (i32, [vp, i64, vp, vp]),
     "repops_cos": (i32, [vp, i64, vp, vp]),
+    "repops_erf": (i32, [vp, i64, vp, vp]),
+    "repops_gelu_erf": (i32, [vp, i64, vp, vp]),
+    "repops_gelu_erf_backward": (i32, [vp, vp, i64, vp, vp]),
     "repops_rope_tables": (i32, [vp, i64, i64, vp, vp, vp]),
     "repops_relu_backward": (i32, [vp, vp, i64, vp, vp]),
     "repops_gelu_backward": (i32, [vp, vp, i64, vp, vp]),

@@ -379,6 +379,15 @@ UNARY(repops_gelu, launch_gelu)
 UNARY(repops_relu, launch_relu)
 UNARY(repops_sin, launch_sin)
 UNARY(repops_cos, launch_cos)
+UNARY(repops_erf, launch_erf)
+UNARY(repops_gelu_erf, launch_gelu_erf)
+
+int repops_gelu_erf_backward(const float *x, const float *dy, int64_t n, float *dx, void *stream) {
+    REQ(n >= 0, "gelu_erf_backward: negative n");
+    if (n == 0) return REPOPS_OK;
+    REQ(x && dy && dx, "gelu_erf_backward: null pointer");
+    return cuda_status(launch_gelu_erf_backward(x, dy, n, dx, S(stream)), "gelu_erf_backward");
+}
 
 int repops_rope_tables(const float *inv_freq, int64_t T, int64_t h, float *cosv, float *sinv, void *stream) {
     REQ(T >= 0 && h >= 0 && T < (1 << 24), "rope_tables: bad T / h");

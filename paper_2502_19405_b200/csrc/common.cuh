@@ -195,6 +195,65 @@ RO_DEV float sincos_rn(float x, bool want_cos) {
     return neg ? -v : v;
 }
 
+// erf (R27): Cephes erff / erfcf.  |x| <= 1: a * T(a^2); 1 < |x| < 10: 1 - (exp(-a^2) / a) * P(1/a^2)
+// (P on [1, 2), R on [2, 10)); |x| >= 10: 1; sign applied last.  Horner steps are fmaf.
+RO_DEV float erf_rn(float x) {
+    const float a = fabsf(x);
+    float y;
+    if (a <= 1.0f) {
+        const float z = __fmul_rn(a, a);
+        float p = 7.853861353153693E-5f;
+        p = __fmaf_rn(p, z, -8.010193625184903E-4f);
+        p = __fmaf_rn(p, z, 5.188327685732524E-3f);
+        p = __fmaf_rn(p, z, -2.685381193529856E-2f);
+        p = __fmaf_rn(p, z, 1.128358514861418E-1f);
+        p = __fmaf_rn(p, z, -3.761262582423300E-1f);
+        p = __fmaf_rn(p, z, 1.128379165726710E+0f);
+        y = __fmul_rn(a, p);
+    } else if (a >= 10.0f) {
+        y = 1.0f;
+    } else {
+        const float e = exp_rn(-__fmul_rn(a, a));
+        const float q = __fdiv_rn(1.0f, a);
+        const float w = __fmul_rn(q, q);
+        float p;
+        if (a < 2.0f) {
+            p = 2.326819970068386E-2f;
+            p = __fmaf_rn(p, w, -1.387039388740657E-1f);
+            p = __fmaf_rn(p, w, 3.687424674597105E-1f);
+            p = __fmaf_rn(p, w, -5.824733027278666E-1f);
+            p = __fmaf_rn(p, w, 6.210004621745983E-1f);
+            p = __fmaf_rn(p, w, -4.944515323274145E-1f);
+            p = __fmaf_rn(p, w, 3.404879937665872E-1f);
+            p = __fmaf_rn(p, w, -2.741127028184656E-1f);
+            p = __fmaf_rn(p, w, 5.638259427386472E-1f);
+        } else {
+            p = -1.047766399936249E+1f;
+            p = __fmaf_rn(p, w, 1.297719955372516E+1f);
+            p = __fmaf_rn(p, w, -7.495518717768503E+0f);
+            p = __fmaf_rn(p, w, 2.921019019210786E+0f);
+            p = __fmaf_rn(p, w, -1.015265279202700E+0f);
+            p = __fmaf_rn(p, w, 4.218463358204948E-1f);
+            p = __fmaf_rn(p, w, -2.820767439740514E-1f);
+            p = __fmaf_rn(p, w, 5.641895067754075E-1f);
+        }
+        y = __fsub_rn(1.0f, __fmul_rn(__fmul_rn(e, q), p));
+    }
+    y = (x < 0.0f) ? -y : y;
+    return (x != x) ? __uint_as_float(0x7FC00000u) : y;
+}
+
+// exact GELU (R27): y = (0.5 x)(1 + erf(x * 1/sqrt 2)); backward dx = dy (cdf + x pdf),
+// cdf = 0.5 (1 + erf(x / sqrt 2)), pdf = exp(-(0.5 x^2)) * 1/sqrt(2 pi)
+RO_DEV float gelu_erf_rn(float v) {
+    return __fmul_rn(__fmul_rn(0.5f, v), __fadd_rn(1.0f, erf_rn(__fmul_rn(v, 0.70710678118654752f))));
+}
+RO_DEV float gelu_erf_grad_rn(float v, float dy) {
+    const float cdf = __fmul_rn(0.5f, __fadd_rn(1.0f, erf_rn(__fmul_rn(v, 0.70710678118654752f))));
+    const float pdf = __fmul_rn(exp_rn(-__fmul_rn(0.5f, __fmul_rn(v, v))), 0.39894228040143268f);
+    return __fmul_rn(dy, __fadd_rn(cdf, __fmul_rn(v, pdf)));
+}
+
 // GELU (tanh form, R13): u = c*(x + 0.044715 x^3), y = 0.5x(1 + tanh u)
 RO_DEV float gelu_rn(float v) {
     float x2 = __fmul_rn(v, v);

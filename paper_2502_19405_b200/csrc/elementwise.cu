@@ -41,6 +41,9 @@ struct TanhF { RO_DEV float operator()(float x) const { return canon(tanh_rn(x))
 struct RsqrtF { RO_DEV float operator()(float x) const { return canon(rsqrt_rn(x)); } };
 struct GeluF { RO_DEV float operator()(float x) const { return canon(gelu_rn(x)); } };
 struct GeluBwdF { RO_DEV float operator()(float x, float dy) const { return canon(gelu_grad_rn(x, dy)); } };
+struct ErfF { RO_DEV float operator()(float x) const { return ro::erf_rn(x); } };
+struct GeluErfF { RO_DEV float operator()(float x) const { return canon(ro::gelu_erf_rn(x)); } };
+struct GeluErfBwdF { RO_DEV float operator()(float x, float dy) const { return canon(ro::gelu_erf_grad_rn(x, dy)); } };
 struct SinF { RO_DEV float operator()(float x) const { return ro::sincos_rn(x, false); } };
 struct CosF { RO_DEV float operator()(float x) const { return ro::sincos_rn(x, true); } };
 // R26 RoPE tables: angle = fmul(float(t), inv_freq[i]); one thread per (t, i)
@@ -277,6 +280,15 @@ cudaError_t launch_gelu(const float *x, int64_t n, float *y, cudaStream_t s) { r
 cudaError_t launch_relu(const float *x, int64_t n, float *y, cudaStream_t s) { return run_unary(x, n, y, s, ReluF{}); }
 cudaError_t launch_sin(const float *x, int64_t n, float *y, cudaStream_t s) { return run_unary(x, n, y, s, SinF{}); }
 cudaError_t launch_cos(const float *x, int64_t n, float *y, cudaStream_t s) { return run_unary(x, n, y, s, CosF{}); }
+cudaError_t launch_erf(const float *x, int64_t n, float *y, cudaStream_t s) { return run_unary(x, n, y, s, ErfF{}); }
+cudaError_t launch_gelu_erf(const float *x, int64_t n, float *y, cudaStream_t s) {
+    return run_unary(x, n, y, s, GeluErfF{});
+}
+cudaError_t launch_gelu_erf_backward(const float *x, const float *dy, int64_t n, float *dx, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    binary_kernel<<<ew_grid(n), 256, 0, s>>>(x, dy, n, dx, GeluErfBwdF{});
+    return cudaGetLastError();
+}
 cudaError_t launch_rope_tables(const float *inv_freq, int64_t T, int64_t h, float *cosv, float *sinv, cudaStream_t s) {
     if (T * h == 0) return cudaSuccess;
     rope_tables_kernel<<<ew_grid(T * h), 256, 0, s>>>(inv_freq, T, h, cosv, sinv);

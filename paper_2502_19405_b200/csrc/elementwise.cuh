@@ -14,6 +14,9 @@ cudaError_t launch_adamw_segments(float *p, const float *g, float *m, float *v, 
                                   float bc2, float omb1, float omb2, cudaStream_t s);
 cudaError_t launch_sin(const float *x, int64_t n, float *y, cudaStream_t s);
 cudaError_t launch_cos(const float *x, int64_t n, float *y, cudaStream_t s);
+cudaError_t launch_erf(const float *x, int64_t n, float *y, cudaStream_t s);
+cudaError_t launch_gelu_erf(const float *x, int64_t n, float *y, cudaStream_t s);
+cudaError_t launch_gelu_erf_backward(const float *x, const float *dy, int64_t n, float *dx, cudaStream_t s);
 cudaError_t launch_rope_tables(const float *inv_freq, int64_t T, int64_t h, float *cosv, float *sinv, cudaStream_t s);
 cudaError_t launch_relu(const float *x, int64_t n, float *y, cudaStream_t s);
 cudaError_t launch_relu_backward(const float *x, const float *g, int64_t n, float *dx, cudaStream_t s);

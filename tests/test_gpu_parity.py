@@ -267,6 +267,19 @@ def test_gelu_parity():
     assert_bits(host(R.repops_gelu_backward(dev(x), dev(dy))), oracle.gelu_backward(x, dy), "gelu bwd")
 
 
+def test_erf_and_exact_gelu_parity():
+    # R27: a stride-1009 sweep of all 2^32 patterns plus the branch boundaries (1, 2, 10)
+    x = np.concatenate([_sweep(1009), synth.uniform(3, 500003, 6.0),
+                        np.float32([0, -0.0, 1.0, -1.0, np.nextafter(np.float32(1), np.float32(2)), 2.0,
+                                    np.nextafter(np.float32(2), np.float32(0)), 10.0, -10.0, 9.999999,
+                                    np.nan, np.inf, -np.inf, 1e-40, -1e-40])])
+    assert_bits(host(R.repops_erf(dev(x))), oracle.erf(x), "erf")
+    g = np.concatenate([synth.uniform(4, 1000003, 8.0), np.float32([0, -0.0, 30, -30, np.nan, np.inf, -np.inf])])
+    assert_bits(host(R.repops_gelu_erf(dev(g))), oracle.gelu_erf(g), "gelu_erf")
+    dy = synth.uniform(5, g.size)
+    assert_bits(host(R.repops_gelu_erf_backward(dev(g), dev(dy))), oracle.gelu_erf_backward(g, dy), "gelu_erf bwd")
+
+
 def test_add_parity():
     a = synth.uniform(1, 100001)
     b = synth.uniform(2, 100001)
