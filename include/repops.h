@@ -370,6 +370,39 @@ void verde_root_plan_destroy(verde_root_plan *plan);
 int verde_first_divergence(const uint8_t *seq0, const uint8_t *seq1, int64_t n, int64_t *d_out,
                            int64_t *rounds_out);
 
+/* ------------------------------------------------------------------ peer memory (multi-GPU DP combine)
+ * R-TREE_S over G ranks as one kernel per rank over NVLink peer memory (reading R14;
+ * the combine order of the collective is future work in the paper, P:642-650;
+ * SURVEY §8(f) f1).  Memory exchanged between processes is allocated here and shared
+ * with CUDA IPC handles (64 opaque bytes, passed between ranks by the caller, e.g.
+ * over torch.distributed).  These are the only entry points that allocate.
+ *
+ * repops_ipc_alloc: cudaMalloc(nbytes) zero-filled; *ptr = device pointer owned by the
+ *   caller (release with repops_ipc_free), handle64 (host, 64 bytes) = its IPC handle.
+ * repops_ipc_open: map a peer's handle into this process (*ptr; unmap with
+ *   repops_ipc_close).  A handle cannot be opened in the process that created it.
+ * repops_p2p_tree_combine: for i in [lo, hi):
+ *     v = balanced tree over q of parts[q][i] (((p0+p1)+(p2+p3))+..., fadd, R-TREE_S top
+ *     levels), outs[q][i] = v for every q.
+ *   parts / outs: host arrays of G device pointers (local or peer-mapped), each a
+ *   float[>= hi] buffer; G in {1, 2, 4, 8}.  Bits equal repops_tree_sum(parts, G) on
+ *   [lo, hi) for any slicing.  Errors: REPOPS_EINVAL (bad G, slice, null pointer).
+ * repops_p2p_signal: after all prior work on `stream`, release-store (system scope)
+ *   `epoch` into peer_flags[q][slot] for every q < G (peer_flags: host array of G device
+ *   uint32 arrays of >= G entries, local or peer-mapped).
+ * repops_p2p_wait: stall `stream` until every flags[j], j < G, has reached `epoch`
+ *   (wrap-around compare), acquire (system scope).  Bounded: after timeout_ms the wait
+ *   gives up and, if status (device int32) is non-null, sets *status = 1. */
+int repops_ipc_alloc(int64_t nbytes, void **ptr, uint8_t *handle64);
+int repops_ipc_open(const uint8_t *handle64, void **ptr);
+int repops_ipc_close(void *ptr);
+int repops_ipc_free(void *ptr);
+int repops_p2p_tree_combine(const float *const *parts, int G, int64_t lo, int64_t hi, float *const *outs,
+                            void *stream);
+int repops_p2p_signal(uint32_t *const *peer_flags, int G, int slot, uint32_t epoch, void *stream);
+int repops_p2p_wait(const uint32_t *flags, int G, uint32_t epoch, int64_t timeout_ms, int32_t *status,
+                    void *stream);
+
 #ifdef __cplusplus
 }
 #endif

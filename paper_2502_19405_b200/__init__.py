@@ -23,7 +23,8 @@ __all__ = [
     "repops_softmax", "repops_softmax_backward", "repops_layernorm", "repops_layernorm_backward",
     "repops_layernorm_backward_params", "repops_cross_entropy", "repops_exp", "repops_log", "repops_tanh",
     "repops_rsqrt", "repops_gelu", "repops_gelu_backward", "repops_relu", "repops_relu_backward", "repops_sin", "repops_cos", "repops_erf", "repops_gelu_erf",
-    "repops_gelu_erf_backward", "repops_rope_tables", "repops_add", "repops_embedding",
+    "repops_gelu_erf_backward", "repops_rope_tables", "repops_ipc_alloc", "repops_ipc_open", "repops_ipc_close",
+    "repops_ipc_free", "repops_p2p_tree_combine", "repops_p2p_signal", "repops_p2p_wait", "repops_add", "repops_embedding",
     "repops_embedding_backward", "repops_adamw", "repops_flip_bit", "verde_commit_tensor",
     "verde_commit_tensors", "verde_merkle_root", "verde_sha256", "verde_node_digest",
     "verde_first_divergence", "verde_digest_from_subroots", "launch_count", "CommitWorkspace", "CommitPlan",
@@ -162,6 +163,64 @@ def repops_tree_sum(parts, out=None, stream=None):
     arr = (C.c_void_p * len(parts))(*[q.data_ptr() for q in parts])
     check(lib().repops_tree_sum(arr, len(parts), n, _p(out), _stream(stream)), "repops_tree_sum")
     return out
+
+
+# ------------------------------------------------------------------ peer memory (multi-GPU DP combine)
+class _DevArray:
+    """__cuda_array_interface__ view of a raw device allocation (no copy)."""
+
+    def __init__(self, ptr, n, typestr):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+_TYPESTR = {torch.float32: "<f4", torch.int32: "<i4", torch.uint8: "|u1"}
+
+
+def repops_ipc_alloc(n, dtype=torch.float32, device=None):
+    """(tensor, handle bytes): n zero-filled elements in an IPC-shareable cudaMalloc block.
+    The caller keeps the tensor alive and frees the block with repops_ipc_free(tensor)."""
+    esz = torch.empty(0, dtype=dtype).element_size()
+    ptr, h = C.c_void_p(), (C.c_uint8 * 64)()
+    check(lib().repops_ipc_alloc(int(n) * esz, C.byref(ptr), h), "repops_ipc_alloc")
+    t = torch.as_tensor(_DevArray(ptr.value, n, _TYPESTR[dtype]), device=device or torch.cuda.current_device())
+    return t, bytes(h)
+
+
+def repops_ipc_open(handle, n, dtype=torch.float32, device=None):
+    """tensor view of a peer's allocation (repops_ipc_close(tensor) unmaps it)."""
+    ptr = C.c_void_p()
+    check(lib().repops_ipc_open((C.c_uint8 * 64).from_buffer_copy(handle), C.byref(ptr)), "repops_ipc_open")
+    return torch.as_tensor(_DevArray(ptr.value, n, _TYPESTR[dtype]), device=device or torch.cuda.current_device())
+
+
+def repops_ipc_close(t):
+    check(lib().repops_ipc_close(t.data_ptr()), "repops_ipc_close")
+
+
+def repops_ipc_free(t):
+    check(lib().repops_ipc_free(t.data_ptr()), "repops_ipc_free")
+
+
+def repops_p2p_tree_combine(parts, lo, hi, outs, stream=None):
+    """out[q][i] = R-TREE_S over parts[*][i] for i in [lo, hi), stored into every outs[q]."""
+    G = len(parts)
+    if len(outs) != G:
+        raise RepopsError("repops_p2p_tree_combine: need one output per part")
+    pa = (C.c_void_p * G)(*[_p(q) for q in parts])
+    oa = (C.c_void_p * G)(*[_p(q) for q in outs])
+    check(lib().repops_p2p_tree_combine(pa, G, int(lo), int(hi), oa, _stream(stream)), "repops_p2p_tree_combine")
+
+
+def repops_p2p_signal(peer_flags, slot, epoch, stream=None):
+    fa = (C.c_void_p * len(peer_flags))(*[_p(q) for q in peer_flags])
+    check(lib().repops_p2p_signal(fa, len(peer_flags), int(slot), int(epoch) & 0xFFFFFFFF, _stream(stream)),
+          "repops_p2p_signal")
+
+
+def repops_p2p_wait(flags, G, epoch, timeout_ms=60000, status=None, stream=None):
+    check(lib().repops_p2p_wait(_p(flags), int(G), int(epoch) & 0xFFFFFFFF, int(timeout_ms), _p(status),
+                                _stream(stream)), "repops_p2p_wait")
 
 
 # ------------------------------------------------------------------ row operators

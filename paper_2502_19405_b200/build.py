@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import concurrent.futures as cf
 import os
+import re
 import subprocess
 import sys
 
@@ -20,8 +21,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librepops.so")
 OBJ = os.path.join(HERE, "build_obj")
-SOURCES = ["abi.cu", "gemm.cu", "rowops.cu", "elementwise.cu", "sha256.cu"]
-HEADERS = ["common.cuh", "gemm.cuh", "rowops.cuh", "elementwise.cuh", "sha256.cuh"]
+SOURCES = ["abi.cu", "gemm.cu", "rowops.cu", "elementwise.cu", "sha256.cu", "p2p.cu"]
+HEADERS = ["common.cuh", "gemm.cuh", "rowops.cuh", "elementwise.cuh", "sha256.cuh", "p2p.cuh"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -36,8 +37,30 @@ def _deps_mtime() -> float:
     return max(os.path.getmtime(f) for f in files)
 
 
-def _compile(src: str, verbose: bool) -> str:
+def _includes(path: str, seen: set) -> set:
+    """the file and every quoted #include it reaches (transitively)"""
+    if path in seen or not os.path.exists(path):
+        return seen
+    seen.add(path)
+    with open(path) as f:
+        for line in f:
+            m = re.match(r'\s*#include\s+"([^"]+)"', line)
+            if m:
+                _includes(os.path.normpath(os.path.join(os.path.dirname(path), m.group(1))), seen)
+    return seen
+
+
+def _src_deps_mtime(src: str) -> float:
+    """newest of the object's source, the headers it includes and this script"""
+    files = _includes(os.path.join(CSRC, src), set()) | {os.path.abspath(__file__)}
+    return max(os.path.getmtime(f) for f in files)
+
+
+def _compile(src: str, verbose: bool, force: bool = True) -> str:
     obj = os.path.join(OBJ, src.replace(".cu", ".o"))
+    if not force and not os.environ.get("RO_NVCC_DEFS") and os.path.exists(obj) \
+            and os.path.getmtime(obj) >= _src_deps_mtime(src):
+        return obj  # up to date
     extra = os.environ.get("RO_NVCC_DEFS", "").split()  # tuning variants only (tools/sha_tune.sh)
     cmd = [NVCC, *ARCH, *NUMERIC, *COMMON, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
     if verbose:
@@ -55,7 +78,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     os.makedirs(OBJ, exist_ok=True)
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
+        objs = list(ex.map(lambda s: _compile(s, verbose, force), SOURCES))
     tmp = LIB + f".tmp{os.getpid()}"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-Xcompiler", "-fPIC"]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -16,6 +16,7 @@
 #include "common.cuh"
 #include "elementwise.cuh"
 #include "gemm.cuh"
+#include "p2p.cuh"
 #include "rowops.cuh"
 #include "sha256.cuh"
 
@@ -821,6 +822,71 @@ int verde_first_divergence(const uint8_t *seq0, const uint8_t *seq1, int64_t n, 
     *d_out = lo;
     if (rounds_out) *rounds_out = rounds;
     return REPOPS_OK;
+}
+
+// ------------------------------------------------------------------ peer memory
+int repops_ipc_alloc(int64_t nbytes, void **ptr, uint8_t *handle64) {
+    REQ(nbytes > 0 && ptr && handle64, "ipc_alloc: bad argument");
+    void *p = nullptr;
+    cudaError_t e = cudaMalloc(&p, (size_t)nbytes);
+    if (e != cudaSuccess) return fail(REPOPS_ECUDA, "ipc_alloc: cudaMalloc(%lld): %s", (long long)nbytes,
+                                      cudaGetErrorString(e));
+    e = cudaMemset(p, 0, (size_t)nbytes);
+    cudaIpcMemHandle_t h;
+    if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, p);
+    if (e != cudaSuccess) {
+        cudaFree(p);
+        return fail(REPOPS_ECUDA, "ipc_alloc: %s", cudaGetErrorString(e));
+    }
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    memcpy(handle64, &h, 64);
+    *ptr = p;
+    return REPOPS_OK;
+}
+
+int repops_ipc_open(const uint8_t *handle64, void **ptr) {
+    REQ(handle64 && ptr, "ipc_open: bad argument");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle64, 64);
+    void *p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return fail(REPOPS_ECUDA, "ipc_open: %s", cudaGetErrorString(e));
+    *ptr = p;
+    return REPOPS_OK;
+}
+
+int repops_ipc_close(void *ptr) {
+    REQ(ptr, "ipc_close: null pointer");
+    cudaError_t e = cudaIpcCloseMemHandle(ptr);
+    return e == cudaSuccess ? REPOPS_OK : fail(REPOPS_ECUDA, "ipc_close: %s", cudaGetErrorString(e));
+}
+
+int repops_ipc_free(void *ptr) {
+    REQ(ptr, "ipc_free: null pointer");
+    cudaError_t e = cudaFree(ptr);
+    return e == cudaSuccess ? REPOPS_OK : fail(REPOPS_ECUDA, "ipc_free: %s", cudaGetErrorString(e));
+}
+
+int repops_p2p_tree_combine(const float *const *parts, int G, int64_t lo, int64_t hi, float *const *outs,
+                            void *stream) {
+    REQ(G == 1 || G == 2 || G == 4 || G == 8, "p2p_tree_combine: G = %d is not 1, 2, 4 or 8", G);
+    REQ(lo >= 0 && hi >= lo, "p2p_tree_combine: bad slice [%lld, %lld)", (long long)lo, (long long)hi);
+    if (hi == lo) return REPOPS_OK;
+    REQ(parts && outs, "p2p_tree_combine: null pointer array");
+    for (int q = 0; q < G; ++q) REQ(parts[q] && outs[q], "p2p_tree_combine: null peer pointer %d", q);
+    return cuda_status(launch_p2p_tree_combine(parts, G, lo, hi, outs, S(stream)), "p2p_tree_combine");
+}
+
+int repops_p2p_signal(uint32_t *const *peer_flags, int G, int slot, uint32_t epoch, void *stream) {
+    REQ(G >= 1 && G <= P2P_MAX_PEERS && slot >= 0 && slot < G && peer_flags, "p2p_signal: bad argument");
+    for (int q = 0; q < G; ++q) REQ(peer_flags[q], "p2p_signal: null peer flag array %d", q);
+    return cuda_status(launch_p2p_signal(peer_flags, G, slot, epoch, S(stream)), "p2p_signal");
+}
+
+int repops_p2p_wait(const uint32_t *flags, int G, uint32_t epoch, int64_t timeout_ms, int32_t *status,
+                    void *stream) {
+    REQ(G >= 1 && G <= P2P_MAX_PEERS && flags && timeout_ms > 0, "p2p_wait: bad argument");
+    return cuda_status(launch_p2p_wait(flags, G, epoch, timeout_ms * 1000000, status, S(stream)), "p2p_wait");
 }
 
 }  // extern "C"

@@ -82,6 +82,102 @@ def dp_tree_combine_sliced(local_parts, world: int, tree, pg=None, out=None):
     return out
 
 
+def p2p_slice(rank: int, world: int, n: int, align: int = 4) -> tuple[int, int]:
+    """[lo, hi) of the n-element gradient that `rank` combines in the peer-memory path:
+    equal slices rounded up to `align` elements (16-byte float4 boundaries), the last
+    one ragged; slices are disjoint and cover [0, n) for any n >= 0."""
+    per = -(-n // world)
+    per = -(-per // align) * align
+    lo = min(rank * per, n)
+    return lo, min(lo + per, n)
+
+
+class P2PTreeCombine:
+    """R-TREE_S across G ranks as ONE fused kernel per rank over NVLink peer memory
+    (the combine order is the paper's future work, fixed by
+    reading R14).  Same bits as dp_tree_combine / dp_tree_combine_sliced.
+
+    Setup (once): every rank allocates, with CUDA IPC, a partial buffer [P], a gradient
+    buffer [P] (what AdamW reads) and a flag array [2, G]; the 64-byte handles are
+    all-gathered over the process group and every peer buffer is mapped.
+    Per call (`epoch` = call count, all on the caller's stream, no host sync):
+      1. tree(local parts) -> my partial (the aligned local subtree);
+      2. signal "partial ready" into every peer's flags[0][me]; wait for all G;
+      3. repops_p2p_tree_combine on my slice p2p_slice(me): loads the slice of all G
+         partials (P2P), top log2(G) levels, stores the sum into all G gradient buffers;
+      4. signal "slice written" into flags[1][me] of every peer; wait for all G.
+    After 4 every rank's gradient buffer holds the full combined gradient, and no peer
+    will touch my partial again until I signal the next epoch (so buffers are reused).
+
+    sync="host" replaces the device flags by stream synchronisation + a process-group
+    barrier: the transport for tests where several processes share one GPU (their
+    contexts time-slice, so one rank's spinning wait kernel would stall the others)."""
+
+    def __init__(self, n: int, rank: int, world: int, pg=None, sync: str = "device", timeout_ms: int = 60000):
+        import torch.distributed as dist
+        from . import repops_ipc_alloc, repops_ipc_open
+        if world & (world - 1) or world > 8:
+            raise ValueError("P2PTreeCombine: world must be 1, 2, 4 or 8")
+        self.n, self.rank, self.world, self.pg, self.sync = n, rank, world, pg, sync
+        self.timeout_ms = timeout_ms
+        self.lo, self.hi = p2p_slice(rank, world, n)
+        self.partial, hp = repops_ipc_alloc(n)
+        self.grad, hg = repops_ipc_alloc(n)
+        self.flags, hf = repops_ipc_alloc(2 * world, torch.int32)
+        self.status = torch.zeros(1, dtype=torch.int32, device=self.grad.device)
+        handles = [None] * world
+        dist.all_gather_object(handles, (hp, hg, hf), group=pg)
+        self._opened = []
+
+        def peer(r, k, n_, dt):
+            if r == rank:
+                return (self.partial, self.grad, self.flags)[k]
+            t = repops_ipc_open(handles[r][k], n_, dt)
+            self._opened.append(t)
+            return t
+        self.peer_partial = [peer(r, 0, n, torch.float32) for r in range(world)]
+        self.peer_grad = [peer(r, 1, n, torch.float32) for r in range(world)]
+        peer_flags = [peer(r, 2, 2 * world, torch.int32) for r in range(world)]
+        self.peer_ready = [f[:world] for f in peer_flags]
+        self.peer_done = [f[world:] for f in peer_flags]
+        self.epoch = 0
+
+    def _barrier(self, phase: int, stream):
+        from . import repops_p2p_signal, repops_p2p_wait
+        if self.sync == "host":
+            import torch.distributed as dist
+            (stream or torch.cuda.current_stream()).synchronize()
+            dist.barrier(group=self.pg)
+            return
+        peers = self.peer_ready if phase == 0 else self.peer_done
+        repops_p2p_signal(peers, self.rank, self.epoch, stream)
+        repops_p2p_wait(peers[self.rank], self.world, self.epoch, self.timeout_ms, self.status, stream)
+
+    def __call__(self, local_parts, tree, stream=None):
+        """combine; returns self.grad (the IPC gradient buffer, identical on every rank)."""
+        from . import repops_p2p_tree_combine
+        self.epoch += 1
+        tree(local_parts, self.partial)
+        self._barrier(0, stream)
+        repops_p2p_tree_combine(self.peer_partial, self.lo, self.hi, self.peer_grad, stream)
+        self._barrier(1, stream)
+        return self.grad
+
+    def check(self):
+        """raise if a device wait timed out (call after synchronising)."""
+        if int(self.status.item()) != 0:
+            raise RuntimeError("P2PTreeCombine: a peer did not signal within the timeout")
+
+    def close(self):
+        from . import repops_ipc_close, repops_ipc_free
+        torch.cuda.synchronize()
+        for t in self._opened:
+            repops_ipc_close(t)
+        self._opened = []
+        for t in (self.partial, self.grad, self.flags):
+            repops_ipc_free(t)
+
+
 def gather_shard_digests(table: torch.Tensor, rep_slots: int, shard_slots: int, s0: int, s_loc: int, world: int,
                          pg=None) -> torch.Tensor:
     """C2: fill every shard region of the digest table from the rank that owns it.

@@ -42,7 +42,7 @@ from . import (EPI_BIAS, EPI_SCALE, CommitPlan, repops_add, repops_cross_entropy
                repops_layernorm_backward_params, repops_softmax, repops_softmax_backward, repops_sum_cols_seq,
                repops_adamw, repops_adamw_segments, repops_tree_sum)
 from ._lib import check, lib
-from .dist import all_gather_rows, dp_tree_combine, dp_tree_combine_sliced, gather_shard_digests, shard_block
+from .dist import P2PTreeCombine, all_gather_rows, dp_tree_combine, dp_tree_combine_sliced, gather_shard_digests, shard_block
 
 # node operator codes (u16)
 OP = dict(PARAM_IN=1, TOKENS_IN=2, EMBED=3, LAYERNORM=4, LINEAR=5, ATTN_SCORES=6, SOFTMAX=7, ATTN_PV=8,
@@ -119,7 +119,7 @@ class GPT2Step:
     """Static program of one training step for the shards owned by this rank."""
 
     def __init__(self, cfg: GPT2Config, rank: int = 0, world: int = 1, device="cuda", pg=None,
-                 structure_only=False):
+                 structure_only=False, combine: str = "sliced", p2p_sync: str = "device"):
         """structure_only: build the node graph / slot layout on the 'meta' device
         (no memory, no kernels) -- used by the CPU tests of the host logic."""
         assert cfg.shards % world == 0
@@ -129,7 +129,13 @@ class GPT2Step:
         self.s0, self.S_loc = shard_block(rank, world, cfg.shards)
         self._fault = None
         self.keep_committed = False  # stash tensors an in-place writer overwrites (for disputes)
-        self.sliced_combine = True   # R-TREE_S via all-to-all + all-gather (same bits, fewer bytes)
+        # R-TREE_S transport at G > 1 (same bits for all): "sliced" = NCCL all-to-all +
+        # all-gather; "gather" = all-gather of partials; "p2p" = one fused kernel per rank
+        # over NVLink peer memory (dist.P2PTreeCombine)
+        if combine not in ("sliced", "gather", "p2p"):
+            raise ValueError(f"unknown combine {combine!r}")
+        self.combine, self.p2p_sync, self.p2p = combine, p2p_sync, None
+        self.sliced_combine = combine == "sliced"
         self.stash = {}
         self.step_no = 0
         c = cfg
@@ -189,7 +195,11 @@ class GPT2Step:
                           dln1=E(M, d)))
         self.dx = [E(M, d) for _ in range(L + 1)]  # dx[l] = gradient w.r.t. x[l]
         self.glocal = torch.zeros(self.S_loc, self.P, device=dev)  # per-shard gradients (rows)
-        self.grad = E(self.P)
+        if self.combine == "p2p" and self.world > 1 and not self.structure_only:
+            self.p2p = P2PTreeCombine(self.P, self.rank, self.world, self.pg, sync=self.p2p_sync)
+            self.grad = self.p2p.grad   # IPC buffer every rank's combine kernel writes its slice into
+        else:
+            self.grad = E(self.P)
         self.shard_loss = E(self.S_loc)
         # transposed copies of the 2-D weights (refreshed every step, data movement
         # only): every dgrad GEMM and the LM head then read an n-contiguous B
@@ -649,6 +659,9 @@ class GPT2Step:
 
         def tree():
             parts = [self.glocal[q] for q in range(self.S_loc)]
+            if self.p2p is not None:
+                self.p2p(parts, lambda ps, out: repops_tree_sum(ps, out=out))
+                return
             combine = dp_tree_combine_sliced if self.sliced_combine else dp_tree_combine
             combine(parts, self.world, lambda ps, out: repops_tree_sum(ps, out=out), self.pg, out=self.grad)
         self.launch(tree)

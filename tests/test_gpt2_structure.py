@@ -148,3 +148,14 @@ def test_gloo_dp_combine_and_digest_gather(world):
     for rank, tree_bytes, table_bytes in res:
         assert tree_bytes == ref, f"rank {rank}: tree differs from the single-process R-TREE_S"
         assert table_bytes == expect.tobytes(), f"rank {rank}: digest table gather wrong"
+
+
+def test_p2p_slices_partition_and_align():
+    """the peer-memory combine's slices are disjoint, cover [0, n) and start on float4 boundaries"""
+    for world in (1, 2, 4, 8):
+        for n in (0, 1, 3, 4, 5, 31, 4096, 100003, 124439808):
+            sl = [D.p2p_slice(r, world, n) for r in range(world)]
+            assert sl[0][0] == 0 and sl[-1][1] == n
+            for (lo, hi), (lo2, _) in zip(sl, sl[1:]):
+                assert hi == lo2 and lo <= hi
+            assert all(lo % 4 == 0 or lo == n for lo, _ in sl)

@@ -21,7 +21,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, tiny, q):
+def _worker(rank, world, port, tiny, q, combine="sliced"):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -30,7 +30,7 @@ def _worker(rank, world, port, tiny, q):
         torch.cuda.set_device(0)
         from paper_2502_19405_b200.gpt2 import GPT2Config, GPT2Step
         cfg = GPT2Config.tiny() if tiny else GPT2Config()
-        st = GPT2Step(cfg, rank=rank, world=world)
+        st = GPT2Step(cfg, rank=rank, world=world, combine=combine, p2p_sync="host")
         st.set_tokens(0)
         st.run()
         root, _ = st.step_root()
@@ -46,11 +46,11 @@ def _worker(rank, world, port, tiny, q):
         dist.destroy_process_group()
 
 
-def _run(world, tiny):
+def _run(world, tiny, combine="sliced"):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, world, port, tiny, q)) for r in range(world)]
+    ps = [ctx.Process(target=_worker, args=(r, world, port, tiny, q, combine)) for r in range(world)]
     for p in ps:
         p.start()
     res = []
@@ -82,3 +82,12 @@ def test_full_gpt2_step_root_world2_equals_world1():
     for rank, root, loss, pdig in _run(2, False):
         assert root == one[1], f"rank {rank}: full GPT-2 step root differs between G=1 and G=2"
         assert pdig == one[3]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_tiny_step_root_p2p_combine(world, tiny_single):
+    """R-TREE_S through the fused peer-memory kernel (CUDA IPC between the rank
+    processes, P2P loads / stores) gives the single-process root."""
+    for rank, root, loss, pdig in _run(world, True, combine="p2p"):
+        assert root == tiny_single[1], f"p2p world {world} rank {rank}: step root differs"
+        assert pdig == tiny_single[3]

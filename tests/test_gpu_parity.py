@@ -397,3 +397,62 @@ def test_commit_large_tensor_multi_pass():
     b.view(np.uint32)[12345678] ^= 1
     got2 = host(R.verde_commit_tensor(t)).tobytes()
     assert got2 == oracle.commit_tensor(b) and got2 != got
+
+
+# ------------------------------------------------------------------ peer-memory combine (f1)
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+def test_p2p_tree_combine_equals_tree_sum(G):
+    """the fused combine over any slicing gives repops_tree_sum's bits (and the oracle's)
+    in every output buffer; unaligned slices take the scalar path"""
+    from paper_2502_19405_b200.dist import p2p_slice
+    n = 100003
+    parts_h = [synth.uniform(700 + q, n) for q in range(G)]
+    parts = [dev(p) for p in parts_h]
+    ref = oracle.tree_sum(parts_h)
+    assert_bits(host(R.repops_tree_sum(parts)), ref, "tree_sum")
+    outs = [torch.full((n,), float("nan"), device="cuda") for _ in range(G)]
+    for r in range(G):
+        lo, hi = p2p_slice(r, G, n)
+        R.repops_p2p_tree_combine(parts, lo, hi, outs)
+    for q in range(G):
+        assert_bits(host(outs[q]), ref, f"out {q}")
+    outs2 = [torch.zeros(n, device="cuda") for _ in range(G)]
+    for lo, hi in ((0, 7), (7, 1001), (1001, n)):   # unaligned slice starts
+        R.repops_p2p_tree_combine(parts, lo, hi, outs2)
+    for q in range(G):
+        assert_bits(host(outs2[q]), ref, f"unaligned out {q}")
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_p2p_flag_protocol_virtual_ranks(G):
+    """the device signal / wait protocol of P2PTreeCombine with G virtual ranks in one
+    process, each on its own stream (so their kernels run concurrently): 3 epochs,
+    every rank's gradient buffer equals the tree over all partials, no wait times out"""
+    from paper_2502_19405_b200.dist import p2p_slice
+    n = 65537
+    streams = [torch.cuda.Stream() for _ in range(G)]
+    partial = [torch.zeros(n, device="cuda") for _ in range(G)]
+    grad = [torch.zeros(n, device="cuda") for _ in range(G)]
+    flags = [torch.zeros(2 * G, dtype=torch.int32, device="cuda") for _ in range(G)]
+    ready = [f[:G] for f in flags]
+    done = [f[G:] for f in flags]
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    for epoch in (1, 2, 3):
+        src = [dev(synth.uniform(800 + 10 * epoch + r, n)) for r in range(G)]
+        torch.cuda.synchronize()
+        for r in range(G):
+            s = streams[r]
+            with torch.cuda.stream(s):
+                partial[r].copy_(src[r])
+                R.repops_p2p_signal(ready, r, epoch, stream=s)
+                R.repops_p2p_wait(ready[r], G, epoch, 10000, status, stream=s)
+                lo, hi = p2p_slice(r, G, n)
+                R.repops_p2p_tree_combine(partial, lo, hi, grad, stream=s)
+                R.repops_p2p_signal(done, r, epoch, stream=s)
+                R.repops_p2p_wait(done[r], G, epoch, 10000, status, stream=s)
+        torch.cuda.synchronize()
+        assert int(status.item()) == 0, "a wait timed out"
+        ref = oracle.tree_sum([host(t) for t in src])
+        for r in range(G):
+            assert_bits(host(grad[r]), ref, f"epoch {epoch} rank {r}")
