@@ -67,6 +67,10 @@ def lib():
                 "orc_relu": (None, [vp, i64, vp]),
                 "orc_sin_vec": (None, [vp, i64, vp]),
                 "orc_erf_vec": (None, [vp, i64, vp]),
+                "orc_philox4x32_10": (None, [vp, vp, vp]),
+                "orc_rand_uniform": (None, [C.c_uint64, C.c_uint64, i64, vp]),
+                "orc_dropout": (None, [vp, i64, f32, C.c_uint64, C.c_uint64, vp, vp]),
+                "orc_dropout_backward": (None, [vp, i64, f32, C.c_uint64, C.c_uint64, vp]),
                 "orc_gelu_erf": (None, [vp, i64, vp]),
                 "orc_gelu_erf_backward": (None, [vp, vp, i64, vp]),
                 "orc_cos_vec": (None, [vp, i64, vp]),
@@ -238,6 +242,39 @@ def gelu_erf_backward(x, dy):
     dy = _f32(dy)
     dx = np.empty_like(x)
     lib().orc_gelu_erf_backward(_p(x), _p(dy), x.size, _p(dx))
+    return dx
+
+
+def philox4x32_10(ctr, key):
+    """orc_philox4x32_10: one Philox4x32-10 block (reading R28)."""
+    c = np.ascontiguousarray(ctr, dtype=np.uint32)
+    k = np.ascontiguousarray(key, dtype=np.uint32)
+    out = np.empty(4, np.uint32)
+    lib().orc_philox4x32_10(_p(c), _p(k), _p(out))
+    return out
+
+
+def rand_uniform(seed, stream, n):
+    """orc_rand_uniform: u_i in [0, 1) on the 2^-24 grid (reading R28)."""
+    y = np.empty(n, np.float32)
+    lib().orc_rand_uniform(seed, stream, n, _p(y))
+    return y
+
+
+def dropout(x, p, seed, stream):
+    """orc_dropout -> (y, mask) (reading R28)."""
+    x = _f32(x)
+    y = np.empty_like(x)
+    m = np.empty(x.size, np.uint8)
+    lib().orc_dropout(_p(x), x.size, p, seed, stream, _p(y), _p(m))
+    return y, m
+
+
+def dropout_backward(dy, p, seed, stream):
+    """orc_dropout_backward (reading R28)."""
+    dy = _f32(dy)
+    dx = np.empty_like(dy)
+    lib().orc_dropout_backward(_p(dy), dy.size, p, seed, stream, _p(dx))
     return dx
 
 

@@ -370,6 +370,60 @@ void orc_gelu_erf_backward(const float *x, const float *dy, i64 n, float *dx) {
     }
 }
 
+/* Deterministic pseudorandomness ("built-in support for deterministic
+ * pseudorandomness generation in PyTorch and CUDA"; reading R28): Philox4x32-10, the
+ * counter-based generator behind curand's Philox4_32_10 and PyTorch's CUDA generator
+ * (Salmon et al., SC'11).  One round: (hi0, lo0) = M0 * c0, (hi1, lo1) = M1 * c2 (64-bit
+ * products), c' = (hi1 ^ c1 ^ k0, lo1, hi0 ^ c3 ^ k1, lo0); the key is bumped by
+ * (W0, W1) between rounds; 10 rounds. */
+void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+    uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3], k0 = key[0], k1 = key[1];
+    for (int r = 0; r < 10; ++r) {
+        if (r > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+        uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+        uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+        uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0;
+        uint32_t n1 = (uint32_t)p1;
+        uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
+        uint32_t n3 = (uint32_t)p0;
+        c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* R28 draw of element i: block b = i / 4 with counter (b lo, b hi, stream lo, stream hi) and
+ * key (seed lo, seed hi); word i % 4 of the block; u = (word >> 8) * 2^-24 in [0, 1)
+ * (exact in binary32). */
+static float rand_u(uint64_t seed, uint64_t stream, i64 i) {
+    uint64_t b = (uint64_t)i >> 2;
+    uint32_t ctr[4] = {(uint32_t)b, (uint32_t)(b >> 32), (uint32_t)stream, (uint32_t)(stream >> 32)};
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    uint32_t w[4];
+    orc_philox4x32_10(ctr, key, w);
+    return (float)(w[i & 3] >> 8) * 5.9604644775390625e-8f;
+}
+
+void orc_rand_uniform(uint64_t seed, uint64_t stream, i64 n, float *y) {
+    for (i64 i = 0; i < n; ++i) y[i] = rand_u(seed, stream, i);
+}
+
+/* R28 dropout: keep_i = (u_i >= p); scale = 1 / (1 - p) (binary32 ops);
+ * y_i = keep_i ? x_i * scale : +0; mask_i = keep_i (optional).  Backward regenerates the
+ * mask from (seed, stream, i): dx_i = keep_i ? dy_i * scale : +0. */
+void orc_dropout(const float *x, i64 n, float p, uint64_t seed, uint64_t stream, float *y, uint8_t *mask) {
+    float scale = 1.0f / (1.0f - p);
+    for (i64 i = 0; i < n; ++i) {
+        int keep = rand_u(seed, stream, i) >= p;
+        y[i] = keep ? canon(x[i] * scale) : 0.0f;
+        if (mask) mask[i] = (uint8_t)keep;
+    }
+}
+
+void orc_dropout_backward(const float *dy, i64 n, float p, uint64_t seed, uint64_t stream, float *dx) {
+    float scale = 1.0f / (1.0f - p);
+    for (i64 i = 0; i < n; ++i) dx[i] = (rand_u(seed, stream, i) >= p) ? canon(dy[i] * scale) : 0.0f;
+}
+
 /* Reading R6: rsqrt = IEEE fdiv(1, IEEE fsqrt(x)), both correctly rounded. */
 float orc_rsqrt(float x) { return canon(1.0f / sqrtf(x)); }
 
