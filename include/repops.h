@@ -170,6 +170,21 @@ int repops_cos(const float *x, int64_t n, float *y, void *stream);
 int repops_erf(const float *x, int64_t n, float *y, void *stream);
 int repops_gelu_erf(const float *x, int64_t n, float *y, void *stream);
 int repops_gelu_erf_backward(const float *x, const float *dy, int64_t n, float *dx, void *stream);
+/* Deterministic pseudorandomness (reading R28): Philox4x32-10 (curand's /
+ * PyTorch's CUDA counter-based generator).  Element i = word (i mod 4) of the Philox
+ * block with counter (floor(i/4) lo, hi, stream_id lo, hi) and key (seed lo, hi);
+ * u_i = (word >> 8) * 2^-24 in [0, 1).  Pure function of (seed, stream_id, i): any
+ * launch configuration, any device, any slicing of i gives the same draws.
+ * repops_rand_uniform: y[i] = u_i (device float[n]).
+ * repops_dropout: keep_i = u_i >= p, scale = fdiv(1, fsub(1, p)),
+ *   y[i] = keep_i ? fmul(x[i], scale) : +0; mask (device uint8[n], nullable) = keep_i.
+ * repops_dropout_backward: dx[i] = keep_i ? fmul(dy[i], scale) : +0 (mask regenerated).
+ * y / dx may alias x / dy.  Errors: REPOPS_EINVAL (n < 0, p outside [0, 1], null). */
+int repops_rand_uniform(uint64_t seed, uint64_t stream_id, int64_t n, float *y, void *stream);
+int repops_dropout(const float *x, int64_t n, float p, uint64_t seed, uint64_t stream_id, float *y, uint8_t *mask,
+                   void *stream);
+int repops_dropout_backward(const float *dy, int64_t n, float p, uint64_t seed, uint64_t stream_id, float *dx,
+                            void *stream);
 /* RoPE tables (R26): cos[t][i] = R-COS(a), sin[t][i] = R-SIN(a), a = fmul(float(t), inv_freq[i]),
  * t < T (< 2^24), i < h.  inv_freq: device float[h]; cos, sin: device float[T * h] (row-major). */
 int repops_rope_tables(const float *inv_freq, int64_t T, int64_t h, float *cosv, float *sinv, void *stream);

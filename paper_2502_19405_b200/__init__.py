@@ -22,7 +22,8 @@ __all__ = [
     "repops_gemm", "repops_gemm_strided_batched", "repops_sum_rows", "repops_sum_cols_seq", "repops_tree_sum",
     "repops_softmax", "repops_softmax_backward", "repops_layernorm", "repops_layernorm_backward",
     "repops_layernorm_backward_params", "repops_cross_entropy", "repops_exp", "repops_log", "repops_tanh",
-    "repops_rsqrt", "repops_gelu", "repops_gelu_backward", "repops_relu", "repops_relu_backward", "repops_sin", "repops_cos", "repops_erf", "repops_gelu_erf",
+    "repops_rsqrt", "repops_gelu", "repops_gelu_backward", "repops_relu", "repops_relu_backward", "repops_sin", "repops_cos", "repops_erf", "repops_gelu_erf", "repops_rand_uniform",
+    "repops_dropout", "repops_dropout_backward",
     "repops_gelu_erf_backward", "repops_rope_tables", "repops_ipc_alloc", "repops_ipc_open", "repops_ipc_close",
     "repops_ipc_free", "repops_p2p_tree_combine", "repops_p2p_signal", "repops_p2p_wait", "repops_add", "repops_embedding",
     "repops_embedding_backward", "repops_adamw", "repops_flip_bit", "verde_commit_tensor",
@@ -339,6 +340,35 @@ def repops_sin(x, out=None, stream=None):
 def repops_cos(x, out=None, stream=None):
     """R26 (Cephes cosf chain)."""
     return _unary("repops_cos", x, out, stream)
+
+
+def repops_rand_uniform(seed, stream_id, n, out=None, stream=None):
+    """R28: u_i in [0, 1) from Philox4x32-10 (seed, stream_id, i)."""
+    if out is None:
+        out = torch.empty(n, dtype=torch.float32, device="cuda")
+    check(lib().repops_rand_uniform(int(seed), int(stream_id), int(n), _p(out), _stream(stream)),
+          "repops_rand_uniform")
+    return out
+
+
+def repops_dropout(x, p, seed, stream_id, out=None, mask=None, stream=None):
+    """R28: y = keep ? x * (1 / (1 - p)) : +0, keep = u >= p; returns (y, mask or None)."""
+    _contig(x, "x")
+    if out is None:
+        out = torch.empty_like(x)
+    check(lib().repops_dropout(_p(x), x.numel(), float(p), int(seed), int(stream_id), _p(out), _p(mask),
+                               _stream(stream)), "repops_dropout")
+    return out, mask
+
+
+def repops_dropout_backward(dy, p, seed, stream_id, out=None, stream=None):
+    """R28: dx = keep ? dy * (1 / (1 - p)) : +0 (mask regenerated from the counter)."""
+    _contig(dy, "dy")
+    if out is None:
+        out = torch.empty_like(dy)
+    check(lib().repops_dropout_backward(_p(dy), dy.numel(), float(p), int(seed), int(stream_id), _p(out),
+                                        _stream(stream)), "repops_dropout_backward")
+    return out
 
 
 def repops_erf(x, out=None, stream=None):

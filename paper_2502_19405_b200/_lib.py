@@ -58,6 +58,9 @@ SIGNATURES = {
     "repops_sin": (i32, [vp, i64, vp, vp]),
     "repops_cos": (i32, [vp, i64, vp, vp]),
     "repops_erf": (i32, [vp, i64, vp, vp]),
+    "repops_rand_uniform": (i32, [C.c_uint64, C.c_uint64, i64, vp, vp]),
+    "repops_dropout": (i32, [vp, i64, f32, C.c_uint64, C.c_uint64, vp, vp, vp]),
+    "repops_dropout_backward": (i32, [vp, i64, f32, C.c_uint64, C.c_uint64, vp, vp]),
     "repops_ipc_alloc": (i32, [i64, vp, vp]),
     "repops_ipc_open": (i32, [vp, vp]),
     "repops_ipc_close": (i32, [vp]),

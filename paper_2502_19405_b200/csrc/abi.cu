@@ -383,6 +383,31 @@ UNARY(repops_cos, launch_cos)
 UNARY(repops_erf, launch_erf)
 UNARY(repops_gelu_erf, launch_gelu_erf)
 
+int repops_rand_uniform(uint64_t seed, uint64_t stream_id, int64_t n, float *y, void *stream) {
+    REQ(n >= 0, "rand_uniform: negative n");
+    if (n == 0) return REPOPS_OK;
+    REQ(y, "rand_uniform: null pointer");
+    return cuda_status(launch_rand_uniform(seed, stream_id, n, y, S(stream)), "rand_uniform");
+}
+
+int repops_dropout(const float *x, int64_t n, float p, uint64_t seed, uint64_t stream_id, float *y, uint8_t *mask,
+                   void *stream) {
+    REQ(n >= 0, "dropout: negative n");
+    REQ(p >= 0.0f && p <= 1.0f, "dropout: p = %g outside [0, 1]", (double)p);
+    if (n == 0) return REPOPS_OK;
+    REQ(x && y, "dropout: null pointer");
+    return cuda_status(launch_dropout(x, n, p, seed, stream_id, y, mask, S(stream)), "dropout");
+}
+
+int repops_dropout_backward(const float *dy, int64_t n, float p, uint64_t seed, uint64_t stream_id, float *dx,
+                            void *stream) {
+    REQ(n >= 0, "dropout_backward: negative n");
+    REQ(p >= 0.0f && p <= 1.0f, "dropout_backward: p = %g outside [0, 1]", (double)p);
+    if (n == 0) return REPOPS_OK;
+    REQ(dy && dx, "dropout_backward: null pointer");
+    return cuda_status(launch_dropout_backward(dy, n, p, seed, stream_id, dx, S(stream)), "dropout_backward");
+}
+
 int repops_gelu_erf_backward(const float *x, const float *dy, int64_t n, float *dx, void *stream) {
     REQ(n >= 0, "gelu_erf_backward: negative n");
     if (n == 0) return REPOPS_OK;

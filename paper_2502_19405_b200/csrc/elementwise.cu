@@ -57,6 +57,70 @@ __global__ void rope_tables_kernel(const float *__restrict__ inv_freq, int64_t T
         sinv[q] = ro::sincos_rn(ang, false);
     }
 }
+// R28 deterministic pseudorandomness: Philox4x32-10 (curand / PyTorch CUDA generator).
+// One thread per 4-element block b: counter (b lo, b hi, stream lo, stream hi), key =
+// seed; element 4b + j takes word j, u = (word >> 8) * 2^-24.
+RO_DEV uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+        const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+        c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+        k.x += 0x9E3779B9u;
+        k.y += 0xBB67AE85u;
+    }
+    return c;
+}
+RO_DEV float u24(uint32_t w) { return __uint2float_rn(w >> 8) * 5.9604644775390625e-8f; }  // exact
+
+// mode 0: uniform draws y = u; mode 1: dropout y = keep ? x * scale : +0 (+ mask);
+// mode 2: dropout backward (x = dy)
+template <int MODE>
+__global__ void philox_kernel(const float *__restrict__ x, int64_t n, float p, uint2 key, uint64_t stream,
+                              float *__restrict__ y, uint8_t *__restrict__ mask) {
+    const int64_t nb = (n + 3) / 4;
+    const float scale = __fdiv_rn(1.0f, __fsub_rn(1.0f, p));
+    const bool vec = aligned16(y) && (MODE == 0 || aligned16(x)) &&
+                     ((reinterpret_cast<uintptr_t>(mask) & 3u) == 0);
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+        const uint4 w = philox4x32_10(make_uint4((uint32_t)b, (uint32_t)((uint64_t)b >> 32), (uint32_t)stream,
+                                                 (uint32_t)(stream >> 32)), key);
+        const float u[4] = {u24(w.x), u24(w.y), u24(w.z), u24(w.w)};
+        const int64_t i0 = 4 * b;
+        float v[4] = {0.f, 0.f, 0.f, 0.f};
+        const bool full = i0 + 4 <= n;
+        if (MODE != 0) {
+            if (full && vec) {
+                const float4 t = __ldg(reinterpret_cast<const float4 *>(x) + b);
+                v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (i0 + j < n) v[j] = x[i0 + j];
+            }
+        }
+        float r[4];
+        uint8_t keep[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            keep[j] = u[j] >= p;
+            r[j] = MODE == 0 ? u[j] : (keep[j] ? canon(__fmul_rn(v[j], scale)) : 0.0f);
+        }
+        if (full && vec) {
+            reinterpret_cast<float4 *>(y)[b] = make_float4(r[0], r[1], r[2], r[3]);
+            if (MODE == 1 && mask)
+                reinterpret_cast<uchar4 *>(mask)[b] = make_uchar4(keep[0], keep[1], keep[2], keep[3]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (i0 + j < n) {
+                    y[i0 + j] = r[j];
+                    if (MODE == 1 && mask) mask[i0 + j] = keep[j];
+                }
+        }
+    }
+}
+
 // R24 (config-1 MLP): relu(x) = x > 0 ? x : +0; relu'(x) g = x > 0 ? g : +0; NaN x -> NaN
 struct ReluF {
     RO_DEV float operator()(float x) const { return x != x ? canon(x) : (x > 0.f ? x : 0.f); }
@@ -280,6 +344,27 @@ cudaError_t launch_gelu(const float *x, int64_t n, float *y, cudaStream_t s) { r
 cudaError_t launch_relu(const float *x, int64_t n, float *y, cudaStream_t s) { return run_unary(x, n, y, s, ReluF{}); }
 cudaError_t launch_sin(const float *x, int64_t n, float *y, cudaStream_t s) { return run_unary(x, n, y, s, SinF{}); }
 cudaError_t launch_cos(const float *x, int64_t n, float *y, cudaStream_t s) { return run_unary(x, n, y, s, CosF{}); }
+static cudaError_t run_philox(int mode, const float *x, int64_t n, float p, uint64_t seed, uint64_t stream,
+                              float *y, uint8_t *mask, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+    const int grid = ew_grid((n + 3) / 4 * 4);
+    if (mode == 0) philox_kernel<0><<<grid, 256, 0, s>>>(x, n, p, key, stream, y, mask);
+    else if (mode == 1) philox_kernel<1><<<grid, 256, 0, s>>>(x, n, p, key, stream, y, mask);
+    else philox_kernel<2><<<grid, 256, 0, s>>>(x, n, p, key, stream, y, mask);
+    return cudaGetLastError();
+}
+cudaError_t launch_rand_uniform(uint64_t seed, uint64_t stream, int64_t n, float *y, cudaStream_t s) {
+    return run_philox(0, nullptr, n, 0.0f, seed, stream, y, nullptr, s);
+}
+cudaError_t launch_dropout(const float *x, int64_t n, float p, uint64_t seed, uint64_t stream, float *y,
+                           uint8_t *mask, cudaStream_t s) {
+    return run_philox(1, x, n, p, seed, stream, y, mask, s);
+}
+cudaError_t launch_dropout_backward(const float *dy, int64_t n, float p, uint64_t seed, uint64_t stream, float *dx,
+                                    cudaStream_t s) {
+    return run_philox(2, dy, n, p, seed, stream, dx, nullptr, s);
+}
 cudaError_t launch_erf(const float *x, int64_t n, float *y, cudaStream_t s) { return run_unary(x, n, y, s, ErfF{}); }
 cudaError_t launch_gelu_erf(const float *x, int64_t n, float *y, cudaStream_t s) {
     return run_unary(x, n, y, s, GeluErfF{});

@@ -41,3 +41,8 @@ cudaError_t launch_gather_rows(const float *table, const int32_t *idx, int64_t n
 cudaError_t launch_fill_uniform(float *out, int64_t n, uint64_t seed, double scale, cudaStream_t s);
 cudaError_t launch_transpose(const float *x, int64_t rows, int64_t cols, int64_t ldx, float *y, int64_t ldy,
                              cudaStream_t s);
+cudaError_t launch_rand_uniform(uint64_t seed, uint64_t stream, int64_t n, float *y, cudaStream_t s);
+cudaError_t launch_dropout(const float *x, int64_t n, float p, uint64_t seed, uint64_t stream, float *y,
+                           uint8_t *mask, cudaStream_t s);
+cudaError_t launch_dropout_backward(const float *dy, int64_t n, float p, uint64_t seed, uint64_t stream, float *dx,
+                                    cudaStream_t s);

@@ -456,3 +456,28 @@ def test_p2p_flag_protocol_virtual_ranks(G):
         ref = oracle.tree_sum([host(t) for t in src])
         for r in range(G):
             assert_bits(host(grad[r]), ref, f"epoch {epoch} rank {r}")
+
+
+# ------------------------------------------------------------------ deterministic pseudorandomness (R28)
+@pytest.mark.parametrize("n", [1, 3, 4, 4097, 1_000_003])
+def test_rand_uniform_exact(n):
+    for seed, stream in ((0, 0), (0x0123456789ABCDEF, 0x0000000500000007), (2 ** 64 - 1, 2 ** 64 - 1)):
+        assert_bits(host(R.repops_rand_uniform(seed, stream, n)), oracle.rand_uniform(seed, stream, n),
+                    f"uniform n={n} seed={seed:x}")
+
+
+def test_dropout_exact_and_backward():
+    x = np.concatenate([synth.uniform(901, 1_000_001, 4.0), np.float32([np.nan, np.inf, -np.inf, -0.0, 3e38])])
+    dy = synth.uniform(902, x.size)
+    for p in (0.0, 0.1, 0.5, 0.9, 1.0):
+        ry, rm = oracle.dropout(x, p, 77, 5)
+        mask = torch.empty(x.size, dtype=torch.uint8, device="cuda")
+        y, _ = R.repops_dropout(dev(x), p, 77, 5, mask=mask)
+        assert_bits(host(y), ry, f"dropout p={p}")
+        assert np.array_equal(host(mask), rm), f"mask p={p}"
+        assert_bits(host(R.repops_dropout_backward(dev(dy), p, 77, 5)), oracle.dropout_backward(dy, p, 77, 5),
+                    f"dropout bwd p={p}")
+    # unaligned views take the scalar path with the same bits
+    xt = dev(x)
+    y, _ = R.repops_dropout(xt[1:], 0.3, 5, 6)
+    assert_bits(host(y), oracle.dropout(x[1:], 0.3, 5, 6)[0], "dropout unaligned")
