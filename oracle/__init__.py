@@ -68,6 +68,9 @@ def lib():
                 "orc_sin_vec": (None, [vp, i64, vp]),
                 "orc_erf_vec": (None, [vp, i64, vp]),
                 "orc_philox4x32_10": (None, [vp, vp, vp]),
+                "orc_convert": (None, [vp, i32, i64, i64, i64, vp, i32, i64]),
+                "orc_gemm_ex": (None, [i64, i64, i64, vp, i32, i64, i32, vp, i32, i64, i32, i32, vp, f32, vp, i32,
+                                       i64]),
                 "orc_rand_uniform": (None, [C.c_uint64, C.c_uint64, i64, vp]),
                 "orc_dropout": (None, [vp, i64, f32, C.c_uint64, C.c_uint64, vp, vp]),
                 "orc_dropout_backward": (None, [vp, i64, f32, C.c_uint64, C.c_uint64, vp]),
@@ -243,6 +246,34 @@ def gelu_erf_backward(x, dy):
     dx = np.empty_like(x)
     lib().orc_gelu_erf_backward(_p(x), _p(dy), x.size, _p(dx))
     return dx
+
+
+_DT_CODE = {"f32": 1, "bf16": 4, "f16": 5}
+
+
+def convert(x, src, dst):
+    """orc_convert (reading R30): x is a 2-D array of the storage type's bit patterns
+    (float32 for "f32", uint16 for "bf16" / "f16"); returns dst's bit patterns."""
+    x = np.ascontiguousarray(x, dtype=np.float32 if src == "f32" else np.uint16)
+    x2 = x.reshape(-1, x.shape[-1]) if x.ndim else x.reshape(1, 1)
+    out = np.empty(x2.shape, dtype=np.float32 if dst == "f32" else np.uint16)
+    lib().orc_convert(_p(x2), _DT_CODE[src], x2.shape[0], x2.shape[1], x2.shape[1], _p(out), _DT_CODE[dst],
+                      x2.shape[1])
+    return out.reshape(x.shape)
+
+
+def gemm_ex(A, adt, B, bdt, cdt, transA=False, transB=False, epi=0, bias=None, scale=1.0):
+    """orc_gemm_ex (reading R30): stored-precision operands, binary32 R-GEMM, narrowed C."""
+    A = np.ascontiguousarray(A, dtype=np.float32 if adt == "f32" else np.uint16)
+    B = np.ascontiguousarray(B, dtype=np.float32 if bdt == "f32" else np.uint16)
+    M = A.shape[1] if transA else A.shape[0]
+    K = A.shape[0] if transA else A.shape[1]
+    N = B.shape[0] if transB else B.shape[1]
+    Cm = np.empty((M, N), dtype=np.float32 if cdt == "f32" else np.uint16)
+    b = _f32(bias) if bias is not None else None
+    lib().orc_gemm_ex(M, N, K, _p(A), _DT_CODE[adt], A.shape[1], int(transA), _p(B), _DT_CODE[bdt], B.shape[1],
+                      int(transB), int(epi), _p(b) if b is not None else None, float(scale), _p(Cm), _DT_CODE[cdt], N)
+    return Cm
 
 
 def philox4x32_10(ctr, key):

@@ -424,6 +424,79 @@ void orc_dropout_backward(const float *dy, i64 n, float p, uint64_t seed, uint64
     for (i64 i = 0; i < n; ++i) dx[i] = (rand_u(seed, stream, i) >= p) ? canon(dy[i] * scale) : 0.0f;
 }
 
+/* Lower-precision storage ("RepOps works with any lower precision ...
+ * (particularly FP16)"; reading R30): tensors may be STORED as bfloat16 / binary16 while
+ * every operation computes in binary32.  Widening is exact; narrowing rounds to nearest
+ * even (IEEE 754 convertFormat), with gradual underflow, overflow to +-inf and the
+ * canonical NaNs 0x7FC0 (bf16) / 0x7E00 (f16). */
+uint16_t orc_f32_to_bf16(float x) {
+    uint32_t u = f2bits(x);
+    if (x != x) return 0x7FC0u;
+    u += 0x7FFFu + ((u >> 16) & 1u);      /* RN-even on the 16 dropped bits */
+    return (uint16_t)(u >> 16);
+}
+float orc_bf16_to_f32(uint16_t h) { return bits2f((uint32_t)h << 16); }
+
+/* binary16 by its definition: the representable value nearest |x| (ties to the even
+ * significand), computed exactly in double (power-of-two scalings and rint). */
+uint16_t orc_f32_to_f16(float x) {
+    if (x != x) return 0x7E00u;
+    uint16_t sign = (f2bits(x) >> 16) & 0x8000u;
+    double a = fabs((double)x);
+    if (a >= 65520.0) return sign | 0x7C00u;               /* halfway to 2^16 or above -> inf */
+    if (a < ldexp(1.0, -14)) {                             /* subnormal: multiples of 2^-24 */
+        double m = rint(a * ldexp(1.0, 24));               /* m <= 1024 (1024 = min normal) */
+        return sign | (uint16_t)m;
+    }
+    int e;
+    frexp(a, &e);                                          /* a in [2^(e-1), 2^e) */
+    e -= 1;                                                /* a in [2^e, 2^(e+1)), e in [-14, 15] */
+    double m = rint(a * ldexp(1.0, 10 - e));               /* significand in [1024, 2048] */
+    return sign | (uint16_t)((((uint32_t)(e + 15)) << 10) + (uint32_t)m - 1024u);
+}
+float orc_f16_to_f32(uint16_t h) {
+    int sign = h >> 15, e = (h >> 10) & 0x1F, m = h & 0x3FF;
+    double v;
+    if (e == 31) return m ? bits2f(0x7FC00000u) : (sign ? -INFINITY : INFINITY);
+    v = (e == 0) ? ldexp((double)m, -24) : ldexp((double)(m + 1024), e - 25);
+    return (float)(sign ? -v : v);                         /* exact */
+}
+
+/* dtype codes (repops.h verde_dtype): 1 = f32, 4 = bf16, 5 = f16 */
+static float ld_elem(const void *p, int dt, i64 i) {
+    if (dt == 4) return orc_bf16_to_f32(((const uint16_t *)p)[i]);
+    if (dt == 5) return orc_f16_to_f32(((const uint16_t *)p)[i]);
+    return ((const float *)p)[i];
+}
+static void st_elem(void *p, int dt, i64 i, float v) {
+    if (dt == 4) ((uint16_t *)p)[i] = orc_f32_to_bf16(v);
+    else if (dt == 5) ((uint16_t *)p)[i] = orc_f32_to_f16(v);
+    else ((float *)p)[i] = canon(v);
+}
+
+/* 2-D convert (rows x cols, leading dimensions in elements). */
+void orc_convert(const void *src, int sdt, i64 rows, i64 cols, i64 lds, void *dst, int ddt, i64 ldd) {
+    for (i64 r = 0; r < rows; ++r)
+        for (i64 c = 0; c < cols; ++c) st_elem(dst, ddt, r * ldd + c, ld_elem(src, sdt, r * lds + c));
+}
+
+/* R30 GEMM on stored operands: C = narrow_cdt(R-GEMM(widen(A), widen(B)) with epi);
+ * the K fold is R-GEMM's (binary32 fma, k ascending). */
+void orc_gemm(i64 M, i64 N, i64 K, const float *A, i64 lda, int transA, const float *B, i64 ldb, int transB,
+              int epi, const float *bias, float scale, float *Cm, i64 ldc);
+void orc_gemm_ex(i64 M, i64 N, i64 K, const void *A, int adt, i64 lda, int transA, const void *B, int bdt, i64 ldb,
+                 int transB, int epi, const float *bias, float scale, void *Cm, int cdt, i64 ldc) {
+    i64 ar = transA ? K : M, ac = transA ? M : K, br = transB ? N : K, bc = transB ? K : N;
+    float *a = (float *)malloc(sizeof(float) * (size_t)(ar * ac + 1));
+    float *b = (float *)malloc(sizeof(float) * (size_t)(br * bc + 1));
+    float *c = (float *)malloc(sizeof(float) * (size_t)(M * N + 1));
+    orc_convert(A, adt, ar, ac, lda, a, 1, ac);
+    orc_convert(B, bdt, br, bc, ldb, b, 1, bc);
+    orc_gemm(M, N, K, a, ac, transA, b, bc, transB, epi, bias, scale, c, N);
+    orc_convert(c, 1, M, N, N, Cm, cdt, ldc);
+    free(a); free(b); free(c);
+}
+
 /* Reading R6: rsqrt = IEEE fdiv(1, IEEE fsqrt(x)), both correctly rounded. */
 float orc_rsqrt(float x) { return canon(1.0f / sqrtf(x)); }
 
