@@ -50,7 +50,7 @@ enum repops_epilogue {
     REPOPS_EPI_SCALE = 2  /* C = fmul(acc, scale)         */
 };
 
-enum verde_dtype { VERDE_F32 = 1, VERDE_I32 = 2, VERDE_U8 = 3 };
+enum verde_dtype { VERDE_F32 = 1, VERDE_I32 = 2, VERDE_U8 = 3, VERDE_BF16 = 4, VERDE_F16 = 5 };
 
 int repops_abi_version(void);
 const char *repops_last_error(void);
@@ -84,6 +84,25 @@ int repops_gemm_strided_batched(int64_t M, int64_t N, int64_t K,
                                 int epi, const float *bias, float scale,
                                 float *C, int64_t ldc, int64_t sC0, int64_t sC1,
                                 int64_t batch0, int64_t batch1, void *stream);
+
+/* Lower-precision STORAGE, binary32 compute ("RepOps works with any lower
+ * precision ... (particularly FP16)"; reading R30).  dtypes: VERDE_F32, VERDE_BF16,
+ * VERDE_F16 (2-byte elements).  Widening is exact; narrowing is IEEE round to nearest
+ * even with gradual underflow and overflow to +-inf; NaN is written canonically
+ * (0x7FC00000 / 0x7FC0 / 0x7E00).
+ * repops_convert: dst[r][c] = convert(src[r][c]), rows x cols, leading dims lds / ldd in
+ *   elements of their own type.  Errors: REPOPS_EINVAL (dtype, ld < cols, null).
+ * repops_gemm_ex: C = narrow_c(R-GEMM(widen(op(A)), widen(op(B))) with epilogue `epi`);
+ *   A, B, C device buffers of their dtypes; bias is float (binary32).  Operands that are
+ *   not f32 are widened into the caller's workspace `ws` (device, >=
+ *   repops_gemm_ex_workspace_bytes(...) bytes; REPOPS_ENOSPACE if smaller); the K fold
+ *   is exactly R-GEMM's, so an all-f32 call equals repops_gemm bit for bit. */
+int repops_convert(const void *src, int src_dtype, int64_t rows, int64_t cols, int64_t lds, void *dst, int dst_dtype,
+                   int64_t ldd, void *stream);
+int64_t repops_gemm_ex_workspace_bytes(int64_t M, int64_t N, int64_t K, int a_dtype, int b_dtype, int c_dtype);
+int repops_gemm_ex(int64_t M, int64_t N, int64_t K, const void *A, int a_dtype, int64_t lda, int transA, const void *B,
+                   int b_dtype, int64_t ldb, int transB, int epi, const float *bias, float scale, void *C, int c_dtype,
+                   int64_t ldc, void *ws, int64_t ws_bytes, void *stream);
 
 /* ------------------------------------------------------------------ reductions
  * R-CSUM (R4): n <= 4096: 128 slots from +0, x[i] into slot i%128

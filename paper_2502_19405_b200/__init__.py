@@ -15,14 +15,14 @@ import torch
 from ._lib import Node, RepopsError, TensorDesc, check, header_symbols, lib
 
 EPI_NONE, EPI_BIAS, EPI_SCALE = 0, 1, 2
-F32, I32, U8 = 1, 2, 3
-_DT = {torch.float32: F32, torch.int32: I32, torch.uint8: U8}
+F32, I32, U8, BF16, F16 = 1, 2, 3, 4, 5
+_DT = {torch.float32: F32, torch.int32: I32, torch.uint8: U8, torch.bfloat16: BF16, torch.float16: F16}
 
 __all__ = [
     "repops_gemm", "repops_gemm_strided_batched", "repops_sum_rows", "repops_sum_cols_seq", "repops_tree_sum",
     "repops_softmax", "repops_softmax_backward", "repops_layernorm", "repops_layernorm_backward",
     "repops_layernorm_backward_params", "repops_cross_entropy", "repops_exp", "repops_log", "repops_tanh",
-    "repops_rsqrt", "repops_gelu", "repops_gelu_backward", "repops_relu", "repops_relu_backward", "repops_sin", "repops_cos", "repops_erf", "repops_gelu_erf", "repops_rand_uniform",
+    "repops_rsqrt", "repops_gelu", "repops_gelu_backward", "repops_relu", "repops_relu_backward", "repops_sin", "repops_cos", "repops_erf", "repops_gelu_erf", "repops_convert", "repops_gemm_ex", "repops_rand_uniform",
     "repops_dropout", "repops_dropout_backward",
     "repops_gelu_erf_backward", "repops_rope_tables", "repops_ipc_alloc", "repops_ipc_open", "repops_ipc_close",
     "repops_ipc_free", "repops_p2p_tree_combine", "repops_p2p_signal", "repops_p2p_wait", "repops_add", "repops_embedding",
@@ -131,6 +131,44 @@ def repops_gemm_strided_batched(A, B, C_out, M, N, K, lda, ldb, ldc, sA, sB, sC,
     if t0 is not None:
         _TIMER.end("gemm", t0, 2 * M * N * K * batch[0] * batch[1], stream)
     return C_out
+
+
+# ------------------------------------------------------------------ R30 stored precision
+_LP = {torch.float32: F32, torch.bfloat16: BF16, torch.float16: F16}
+
+
+def repops_convert(x, dtype, out=None, stream=None):
+    """R30: 2-D (or 1-D) x -> dtype (f32 / bf16 / f16): exact widening, RN-even narrowing."""
+    if x.dtype not in _LP or dtype not in _LP:
+        raise RepopsError("repops_convert: dtypes must be float32 / bfloat16 / float16")
+    x2 = x if x.dim() == 2 else x.reshape(1, -1)
+    if out is None:
+        out = torch.empty(x.shape, dtype=dtype, device=x.device)
+    o2 = out if out.dim() == 2 else out.reshape(1, -1)
+    check(lib().repops_convert(_p(x2), _LP[x.dtype], x2.shape[0], x2.shape[1], _ld(x2), _p(o2), _LP[dtype],
+                               _ld(o2), _stream(stream)), "repops_convert")
+    return out
+
+
+def repops_gemm_ex(A, B, transA=False, transB=False, epi=EPI_NONE, bias=None, scale=1.0, out=None, out_dtype=None,
+                   stream=None):
+    """R30: C = narrow(R-GEMM(widen(A), widen(B))); A / B / C stored as f32, bf16 or f16."""
+    M = A.shape[1] if transA else A.shape[0]
+    K = A.shape[0] if transA else A.shape[1]
+    N = B.shape[0] if transB else B.shape[1]
+    if (B.shape[1] if transB else B.shape[0]) != K:
+        raise RepopsError("repops_gemm_ex: inner dimensions differ")
+    if out is None:
+        out = torch.empty((M, N), dtype=out_dtype or A.dtype, device=A.device)
+    wsb = lib().repops_gemm_ex_workspace_bytes(M, N, K, _LP[A.dtype], _LP[B.dtype], _LP[out.dtype])
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=A.device)
+    t0 = _TIMER.begin(stream) if _TIMER else None
+    check(lib().repops_gemm_ex(M, N, K, _p(A), _LP[A.dtype], _ld(A), int(bool(transA)), _p(B), _LP[B.dtype], _ld(B),
+                               int(bool(transB)), int(epi), _p(bias), float(scale), _p(out), _LP[out.dtype], _ld(out),
+                               _p(ws), wsb, _stream(stream)), "repops_gemm_ex")
+    if t0 is not None:
+        _TIMER.end("gemm", t0, 2 * M * N * K, stream)
+    return out
 
 
 # ------------------------------------------------------------------ reductions

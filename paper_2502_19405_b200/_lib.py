@@ -58,6 +58,10 @@ SIGNATURES = {
     "repops_sin": (i32, [vp, i64, vp, vp]),
     "repops_cos": (i32, [vp, i64, vp, vp]),
     "repops_erf": (i32, [vp, i64, vp, vp]),
+    "repops_convert": (i32, [vp, i32, i64, i64, i64, vp, i32, i64, vp]),
+    "repops_gemm_ex_workspace_bytes": (i64, [i64, i64, i64, i32, i32, i32]),
+    "repops_gemm_ex": (i32, [i64, i64, i64, vp, i32, i64, i32, vp, i32, i64, i32, i32, vp, f32, vp, i32, i64, vp, i64,
+                             vp]),
     "repops_rand_uniform": (i32, [C.c_uint64, C.c_uint64, i64, vp, vp]),
     "repops_dropout": (i32, [vp, i64, f32, C.c_uint64, C.c_uint64, vp, vp, vp]),
     "repops_dropout_backward": (i32, [vp, i64, f32, C.c_uint64, C.c_uint64, vp, vp]),

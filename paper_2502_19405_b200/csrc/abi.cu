@@ -238,6 +238,68 @@ int repops_gemm_strided_batched(int64_t M, int64_t N, int64_t K, const float *A,
                        sC1, batch0, batch1, stream, -1);
 }
 
+// ------------------------------------------------------------------ R30 stored precision
+static bool lp_dtype(int dt) { return dt == VERDE_F32 || dt == VERDE_BF16 || dt == VERDE_F16; }
+static int64_t lp_size(int dt) { return dt == VERDE_F32 ? 4 : 2; }
+static int64_t align256(int64_t b) { return (b + 255) & ~int64_t(255); }
+
+int repops_convert(const void *src, int src_dtype, int64_t rows, int64_t cols, int64_t lds, void *dst, int dst_dtype,
+                   int64_t ldd, void *stream) {
+    REQ(lp_dtype(src_dtype) && lp_dtype(dst_dtype), "convert: dtypes %d -> %d not in {f32, bf16, f16}", src_dtype,
+        dst_dtype);
+    REQ(rows >= 0 && cols >= 0 && lds >= cols && ldd >= cols, "convert: bad extent / leading dimension");
+    if (rows * cols == 0) return REPOPS_OK;
+    REQ(src && dst, "convert: null pointer");
+    return cuda_status(launch_convert(src, src_dtype, rows, cols, lds, dst, dst_dtype, ldd, S(stream)), "convert");
+}
+
+int64_t repops_gemm_ex_workspace_bytes(int64_t M, int64_t N, int64_t K, int a_dtype, int b_dtype, int c_dtype) {
+    int64_t b = 0;
+    if (a_dtype != VERDE_F32) b += align256(M * K * 4);
+    if (b_dtype != VERDE_F32) b += align256(K * N * 4);
+    if (c_dtype != VERDE_F32) b += align256(M * N * 4);
+    return b;
+}
+
+int repops_gemm_ex(int64_t M, int64_t N, int64_t K, const void *A, int a_dtype, int64_t lda, int transA, const void *B,
+                   int b_dtype, int64_t ldb, int transB, int epi, const float *bias, float scale, void *C, int c_dtype,
+                   int64_t ldc, void *ws, int64_t ws_bytes, void *stream) {
+    REQ(lp_dtype(a_dtype) && lp_dtype(b_dtype) && lp_dtype(c_dtype), "gemm_ex: dtype not in {f32, bf16, f16}");
+    REQ(M >= 0 && N >= 0 && K >= 0, "gemm_ex: negative extent");
+    const int64_t need = repops_gemm_ex_workspace_bytes(M, N, K, a_dtype, b_dtype, c_dtype);
+    if (need > 0) REQ(ws != nullptr, "gemm_ex: workspace required");
+    if (ws_bytes < need) return fail(REPOPS_ENOSPACE, "gemm_ex: workspace %lld < %lld bytes", (long long)ws_bytes,
+                                     (long long)need);
+    char *w = static_cast<char *>(ws);
+    const float *a = static_cast<const float *>(A), *b = static_cast<const float *>(B);
+    int64_t la = lda, lb = ldb;
+    int st;
+    if (a_dtype != VERDE_F32 && M * K > 0) {   // widen A in its stored orientation, packed
+        const int64_t r = transA ? K : M, c = transA ? M : K;
+        REQ(A && lda >= c, "gemm_ex: A null or lda too small");
+        if ((st = repops_convert(A, a_dtype, r, c, lda, w, VERDE_F32, c, stream)) != REPOPS_OK) return st;
+        a = reinterpret_cast<const float *>(w);
+        la = c;
+        w += align256(M * K * 4);
+    }
+    if (b_dtype != VERDE_F32 && K * N > 0) {
+        const int64_t r = transB ? N : K, c = transB ? K : N;
+        REQ(B && ldb >= c, "gemm_ex: B null or ldb too small");
+        if ((st = repops_convert(B, b_dtype, r, c, ldb, w, VERDE_F32, c, stream)) != REPOPS_OK) return st;
+        b = reinterpret_cast<const float *>(w);
+        lb = c;
+        w += align256(K * N * 4);
+    }
+    if (c_dtype == VERDE_F32)
+        return repops_gemm(M, N, K, a, la, transA, b, lb, transB, epi, bias, scale, static_cast<float *>(C), ldc,
+                           stream);
+    REQ(C && ldc >= N, "gemm_ex: C null or ldc too small");
+    float *c32 = reinterpret_cast<float *>(w);
+    if ((st = repops_gemm(M, N, K, a, la, transA, b, lb, transB, epi, bias, scale, c32, N, stream)) != REPOPS_OK)
+        return st;
+    return repops_convert(c32, VERDE_F32, M, N, N, C, c_dtype, ldc, stream);
+}
+
 // Tuning hook (not in repops.h): process-wide override of the automatic tile
 // choice (-1 = automatic).  Bits never depend on it.
 int repops_gemm_force_cfg(int cfg) {

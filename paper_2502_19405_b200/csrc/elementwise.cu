@@ -4,6 +4,9 @@
 //
 // HBM-bound: grid-stride loops over float4 with a grid of a few waves of the
 // 148 SMs; each element's arithmetic is the fixed chain in common.cuh.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 #include "elementwise.cuh"
 
@@ -118,6 +121,34 @@ __global__ void philox_kernel(const float *__restrict__ x, int64_t n, float p, u
                     if (MODE == 1 && mask) mask[i0 + j] = keep[j];
                 }
         }
+    }
+}
+
+// R30 lower-precision storage: widen exactly, narrow RN-even (cvt.rn), canonical NaNs.
+// dtype codes: 1 = f32, 4 = bf16, 5 = f16.
+RO_DEV float ld_lp(const void *p, int dt, int64_t i) {
+    if (dt == 4) return __uint_as_float((uint32_t)reinterpret_cast<const uint16_t *>(p)[i] << 16);
+    if (dt == 5) return __half2float(reinterpret_cast<const __half *>(p)[i]);
+    return reinterpret_cast<const float *>(p)[i];
+}
+RO_DEV void st_lp(void *p, int dt, int64_t i, float v) {
+    if (dt == 4) {
+        const __nv_bfloat16 h = __float2bfloat16_rn(v);
+        reinterpret_cast<uint16_t *>(p)[i] = (v != v) ? (uint16_t)0x7FC0u : *reinterpret_cast<const uint16_t *>(&h);
+    } else if (dt == 5) {
+        const __half h = __float2half_rn(v);
+        reinterpret_cast<uint16_t *>(p)[i] = (v != v) ? (uint16_t)0x7E00u : __half_as_ushort(h);
+    } else {
+        reinterpret_cast<float *>(p)[i] = canon(v);
+    }
+}
+template <int SDT, int DDT>
+__global__ void convert_kernel(const void *__restrict__ src, int64_t rows, int64_t cols, int64_t lds,
+                               void *__restrict__ dst, int64_t ldd) {
+    const int64_t n = rows * cols;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = q / cols, c = q - r * cols;
+        st_lp(dst, DDT, r * ldd + c, ld_lp(src, SDT, r * lds + c));
     }
 }
 
@@ -344,6 +375,19 @@ cudaError_t launch_gelu(const float *x, int64_t n, float *y, cudaStream_t s) { r
 cudaError_t launch_relu(const float *x, int64_t n, float *y, cudaStream_t s) { return run_unary(x, n, y, s, ReluF{}); }
 cudaError_t launch_sin(const float *x, int64_t n, float *y, cudaStream_t s) { return run_unary(x, n, y, s, SinF{}); }
 cudaError_t launch_cos(const float *x, int64_t n, float *y, cudaStream_t s) { return run_unary(x, n, y, s, CosF{}); }
+cudaError_t launch_convert(const void *src, int sdt, int64_t rows, int64_t cols, int64_t lds, void *dst, int ddt,
+                           int64_t ldd, cudaStream_t s) {
+    const int64_t n = rows * cols;
+    if (n == 0) return cudaSuccess;
+    const int grid = ew_grid(n);
+#define RO_CONV(a, b) \
+    if (sdt == a && ddt == b) { convert_kernel<a, b><<<grid, 256, 0, s>>>(src, rows, cols, lds, dst, ldd); return cudaGetLastError(); }
+    RO_CONV(1, 1) RO_CONV(1, 4) RO_CONV(1, 5) RO_CONV(4, 1) RO_CONV(4, 4) RO_CONV(4, 5) RO_CONV(5, 1) RO_CONV(5, 4)
+    RO_CONV(5, 5)
+#undef RO_CONV
+    return cudaErrorInvalidValue;
+}
+
 static cudaError_t run_philox(int mode, const float *x, int64_t n, float p, uint64_t seed, uint64_t stream,
                               float *y, uint8_t *mask, cudaStream_t s) {
     if (n == 0) return cudaSuccess;

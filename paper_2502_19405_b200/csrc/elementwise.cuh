@@ -46,3 +46,5 @@ cudaError_t launch_dropout(const float *x, int64_t n, float p, uint64_t seed, ui
                            uint8_t *mask, cudaStream_t s);
 cudaError_t launch_dropout_backward(const float *dy, int64_t n, float p, uint64_t seed, uint64_t stream, float *dx,
                                     cudaStream_t s);
+cudaError_t launch_convert(const void *src, int sdt, int64_t rows, int64_t cols, int64_t lds, void *dst, int ddt,
+                           int64_t ldd, cudaStream_t s);

@@ -481,3 +481,54 @@ def test_dropout_exact_and_backward():
     xt = dev(x)
     y, _ = R.repops_dropout(xt[1:], 0.3, 5, 6)
     assert_bits(host(y), oracle.dropout(x[1:], 0.3, 5, 6)[0], "dropout unaligned")
+
+
+# ------------------------------------------------------------------ R30 stored precision
+def _u16(t):
+    return host(t.view(torch.int16)).view(np.uint16)
+
+
+@pytest.mark.parametrize("dt", ["bf16", "f16"])
+def test_convert_exact_all_patterns(dt):
+    tdt = {"bf16": torch.bfloat16, "f16": torch.float16}[dt]
+    x = np.concatenate([_sweep(1009), np.float32([0.0, -0.0, 65504, 65520, 65519.996, 2 ** -24, 2 ** -25,
+                                                  3 * 2 ** -25, 1 + 2 ** -11, 1 + 2 ** -8, 3.3895314e38, np.nan])])
+    n = _u16(R.repops_convert(dev(x), tdt))
+    assert np.array_equal(n, oracle.convert(x[None], "f32", dt).ravel()), f"narrow {dt}"
+    h = np.arange(2 ** 16, dtype=np.uint32).astype(np.uint16)
+    w = R.repops_convert(torch.from_numpy(h.view(np.int16)).cuda().view(tdt), torch.float32)
+    assert_bits(host(w), oracle.convert(h[None], dt, "f32").ravel(), f"widen {dt}")
+    # 2-D strided views (leading dimensions) and a cross-format conversion
+    X = dev(synth.uniform(41, 37 * 50, 100.0).reshape(37, 50))[:, 3:44]
+    Y = R.repops_convert(X, tdt)
+    assert np.array_equal(_u16(Y), oracle.convert(host(X).copy(), "f32", dt))
+    other, odt = ("f16", torch.float16) if dt == "bf16" else ("bf16", torch.bfloat16)
+    Z = R.repops_convert(Y, odt)
+    assert np.array_equal(_u16(Z), oracle.convert(_u16(Y), dt, other))
+
+
+@pytest.mark.parametrize("adt,bdt,cdt", [("bf16", "bf16", "bf16"), ("f16", "f16", "f32"), ("f32", "bf16", "f16"),
+                                         ("f32", "f32", "f32")])
+def test_gemm_ex_parity(adt, bdt, cdt):
+    tdt = {"f32": torch.float32, "bf16": torch.bfloat16, "f16": torch.float16}
+    M, N, K = 131, 257, 300
+    for tA, tB in ((False, False), (True, False), (False, True)):
+        A32 = synth.uniform(51, M * K).reshape((K, M) if tA else (M, K))
+        B32 = synth.uniform(52, K * N).reshape((N, K) if tB else (K, N))
+        A = A32 if adt == "f32" else oracle.convert(A32, "f32", adt)
+        B = B32 if bdt == "f32" else oracle.convert(B32, "f32", bdt)
+        bias = synth.uniform(53, N)
+        ref = oracle.gemm_ex(A, adt, B, bdt, cdt, transA=tA, transB=tB, epi=1, bias=bias)
+
+        def to_dev(a, dt):
+            return dev(a) if dt == "f32" else torch.from_numpy(a.view(np.int16)).cuda().view(tdt[dt])
+        C = R.repops_gemm_ex(to_dev(A, adt), to_dev(B, bdt), transA=tA, transB=tB, epi=R.EPI_BIAS, bias=dev(bias),
+                             out_dtype=tdt[cdt])
+        got = host(C) if cdt == "f32" else _u16(C)
+        if cdt == "f32":
+            assert_bits(got, ref, f"gemm_ex {adt}{bdt}{cdt} tA={tA} tB={tB}")
+        else:
+            assert np.array_equal(got, ref), f"gemm_ex {adt}{bdt}{cdt} tA={tA} tB={tB}"
+    if (adt, bdt, cdt) == ("f32", "f32", "f32"):   # all-f32 gemm_ex is repops_gemm bit for bit
+        A, B = dev(synth.uniform(54, M * K).reshape(M, K)), dev(synth.uniform(55, K * N).reshape(K, N))
+        assert_bits(host(R.repops_gemm_ex(A, B)), host(R.repops_gemm(A, B)), "gemm_ex == gemm")
