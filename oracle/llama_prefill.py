@@ -54,7 +54,8 @@ def run_prefill(cfg, tokens=None):
                 S[j * T:(j + 1) * T] = gemm(_c(qk[:, j * hd:(j + 1) * hd]), k, transB=True, epi=2, scale=scale)
                 P[j * T:(j + 1) * T] = softmax(S[j * T:(j + 1) * T], causal=True)
                 ob[:, j * hd:(j + 1) * hd] = gemm(_c(P[j * T:(j + 1) * T]), v)
-            out.update({q + "qkv": qkv, q + "qk_rope": qk, q + "scores": S, q + "probs": P, q + "attn_out": ob})
+            # R29: attention is one operator; S and P are internal (not committed tensors)
+            out.update({q + "qkv": qkv, q + "qk_rope": qk, q + "attn_out": ob})
             o_all[:, b * qh * hd:(b + 1) * qh * hd] = ob
         attn = np.empty((T, d), np.float32)
         for b in range(nb):

@@ -15,9 +15,15 @@ the K order.  Nodes are defined per column block (G-independent), so the
 pass's root is bit-identical for G in {1, 2, 4, 8}.
 
 Node order (R13 analogue): params | tokens, RoPE tables, embedding | per layer:
-attn RMSNorm, for each block (QKV, RoPE, scores, softmax, PV), for each block
+attn RMSNorm, for each block (QKV, RoPE, attention), for each block
 O-proj, residual, MLP RMSNorm, for each block (gate, up, SwiGLU), for each block
 down, residual | final RMSNorm, for each block LM head.
+
+Attention is ONE operator (reading R29, like PyTorch's scaled_dot_product_attention
+node): scores R-GEMM with the 1/sqrt(hd) epilogue, causal R-SOFTMAX, then the PV
+R-GEMM; its output (the per-block attention output) is committed, the scores and
+probabilities are scratch shared by all layers (a referee recomputes them from the
+committed Q/K/V, Verde Case 3).
 """
 from __future__ import annotations
 
@@ -36,8 +42,8 @@ from . import (EPI_SCALE, CommitPlan, RootPlan, repops_add, repops_copy2d, repop
 from ._lib import check, lib
 from .dist import all_gather_rows, gather_shard_digests, shard_block
 
-OP = dict(PARAM_IN=1, TOKENS_IN=2, TABLES_IN=3, EMBED=4, RMSNORM=5, QKV=6, ROPE=7, SCORES=8, SOFTMAX=9, PV=10,
-          OPROJ=11, RESIDUAL=12, GATE=13, UP=14, SWIGLU=15, DOWN=16, LMHEAD=17, ROPE_TABLES=18)
+OP = dict(PARAM_IN=1, TOKENS_IN=2, TABLES_IN=3, EMBED=4, RMSNORM=5, QKV=6, ROPE=7, OPROJ=11, RESIDUAL=12, GATE=13,
+          UP=14, SWIGLU=15, DOWN=16, LMHEAD=17, ROPE_TABLES=18, ATTENTION=19)
 REPLICATED = 0xFFFFFFFF
 
 
@@ -125,9 +131,11 @@ class LlamaPrefill:
         # activations
         self.x = [E(T, d) for _ in range(L + 1)]
         self.act = []
+        # R29: attention scores / probabilities are operator-internal scratch shared by all layers
+        self.S_scr, self.P_scr = E(nbl, qh * T, T), E(nbl, qh * T, T)
         for _ in range(L):
             self.act.append(dict(xn=E(T, d), rs1=E(T), qkv=E(nbl, T, self.Wb), qk=E(nbl, T, (qh + 1) * hd),
-                                 S=E(nbl, qh * T, T), P=E(nbl, qh * T, T), o=E(nbl, T, qh * hd),
+                                 S=self.S_scr, P=self.P_scr, o=E(nbl, T, qh * hd),
                                  o_all=E(T, c.n_head * hd), op=E(nbl, T, self.Db), attn=E(T, d), h=E(T, d),
                                  hn=E(T, d), rs2=E(T), g=E(nbl, T, self.Fb), u=E(nbl, T, self.Fb),
                                  a=E(nbl, T, self.Fb), a_all=E(T, c.ffn), dn=E(nbl, T, self.Db), mlp=E(T, d)))
@@ -253,12 +261,9 @@ class LlamaPrefill:
                 N_(OP["QKV"], b, {1: l}, [t_xn] + wins, [t_qkv], q + "qkv")
                 t_qk = T_(q + "qk_rope", bv(a["qk"], b), b)
                 N_(OP["ROPE"], b, {1: l}, [t_qkv, t_cos, t_sin], [t_qk], q + "rope")
-                t_S = T_(q + "scores", bv(a["S"], b), b)
-                N_(OP["SCORES"], b, {1: l, 3: int(np.float32(scale).view(np.uint32))}, [t_qk], [t_S], q + "scores")
-                t_P = T_(q + "probs", bv(a["P"], b), b)
-                N_(OP["SOFTMAX"], b, {1: l, 4: 1}, [t_S], [t_P], q + "softmax")
                 t_ob = T_(q + "attn_out", bv(a["o"], b), b)
-                N_(OP["PV"], b, {1: l}, [t_P, t_qkv], [t_ob], q + "pv")
+                N_(OP["ATTENTION"], b, {1: l, 3: int(np.float32(scale).view(np.uint32)), 4: 1}, [t_qk, t_qkv],
+                   [t_ob], q + "attention")
                 t_o.append(t_ob)
             t_op = []
             for b in range(nb):

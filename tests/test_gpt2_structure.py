@@ -66,7 +66,7 @@ def test_graph_is_topological_and_single_producer(ref_graph):
 def test_llama_tp_graph_identical_for_every_degree(world):
     from paper_2502_19405_b200.llama import LlamaConfig, LlamaPrefill
     ref = LlamaPrefill(LlamaConfig(), structure_only=True)
-    assert len(ref.nodes) == 2992  # + the R26 ROPE_TABLES node
+    assert len(ref.nodes) == 2480  # R26 ROPE_TABLES node; R29: one ATTENTION node per (layer, block)
     for rank in range(world):
         st = LlamaPrefill(LlamaConfig(), rank=rank, world=world, structure_only=True)
         assert np.array_equal(st.node_blob, ref.node_blob) and np.array_equal(st.node_slots, ref.node_slots)

@@ -159,13 +159,19 @@ def test_full_llama_prefill_sampled_referee():
     for i, j in zip(rng.integers(0, T, 12), rng.integers(0, qh * hd, 12)):
         r = oracle.gemm_element(xn, np.ascontiguousarray(wq[:, 3 * qh * hd:4 * qh * hd]), int(i), int(j))
         assert bits(qkv3[i, j]) == bits(r), (i, j)
-    # softmax rows of block 3, head 1 recomputed from the committed scores
-    S = a["S"][3].cpu().numpy()
-    P = a["P"][3].cpu().numpy()
-    for r in (T + 0, T + 5, 2 * T - 1):
-        L = r % T + 1
-        ref_row = oracle.softmax(S[r:r + 1, :L])[0]
-        assert np.array_equal(bits(P[r, :L]), bits(ref_row)) and np.all(bits(P[r, L:]) == 0)
+    # attention (R29: one operator) of block 3, head 1, recomputed for sampled query rows
+    # from the committed RoPE'd Q/K and V: scores, causal softmax, PV over all T keys
+    qk3 = a["qk"][3].cpu().numpy()
+    v3 = np.ascontiguousarray(qkv3[:, (qh + 1) * hd:])
+    k3 = np.ascontiguousarray(qk3[:, qh * hd:(qh + 1) * hd])
+    o3 = a["o"][3].cpu().numpy()
+    scale = float(np.float32(1.0 / np.sqrt(hd)))
+    for i in (0, 5, 1000, T - 1):
+        q_row = np.ascontiguousarray(qk3[i:i + 1, hd:2 * hd])
+        s_row = oracle.gemm(q_row, k3, transB=True, epi=2, scale=scale)
+        p_row = np.zeros((1, T), np.float32)
+        p_row[0, :i + 1] = oracle.softmax(np.ascontiguousarray(s_row[:, :i + 1]))[0]
+        assert np.array_equal(bits(o3[i, hd:2 * hd]), bits(oracle.gemm(p_row, v3)[0])), i
     # SwiGLU elements of the last layer, block 7
     al = st.act[cfg.n_layer - 1]
     g = al["g"][7].cpu().numpy()[:64]
