@@ -44,6 +44,18 @@ def fp32_peak_tflops(mhz: float, sms: int = 148) -> float:
     return sms * 128 * 2 * mhz * 1e6 / 1e12
 
 
+# SHA-256 leaf compression loop of sha256.o (cuobjdump -sass, tools/sass_mix.py): per
+# 64-byte block 673 SHF + 352 LOP3 + 244 IADD3 + 16 PRMT + 2 ISETP on the ALU pipe
+# (123 IMAD go to the FMA pipe).  The ALU pipe retires 16 lanes / clk / SMSP (rt = 2,
+# B300_MICROARCH "Pipe rates"), so the commit's roofline is ALU issue, not HBM.
+SHA_ALU_OPS_PER_64B = 1287
+
+
+def sha_alu_peak_gbs(mhz: float, sms: int = 148) -> float:
+    """bytes/s the ALU pipe allows for SHA-256 leaves: SMs x 64 lanes x clock / ALU ops per byte."""
+    return sms * 4 * 16 * mhz * 1e6 / (SHA_ALU_OPS_PER_64B / 64) / 1e9
+
+
 def profiled_gemm_traffic():
     """DRAM bytes per R-GEMM launch, averaged over one GPT-2 step's GEMM launches in
     the committed ncu launch list (profiles/, tools/profile_round.sh); None if absent."""
@@ -569,6 +581,11 @@ def main():
         cm = head["commit"]
         cm["hbm_frac"] = cm["gbs"] / hbm
         cm["hbm_peak_gbs"] = hbm
+        cm["bound"] = "alu"
+        cm["alu_peak_gbs"] = sha_alu_peak_gbs(clk["sm_max_mhz"] or 1965.0)
+        cm["alu_frac"] = cm["gbs"] / cm["alu_peak_gbs"]
+        cm["note"] = ("SHA-256 is integer-ALU bound (1287 ALU ops per 64 B block); gbs is the commit plans' "
+                      "device time on the side stream, sharing the SMs with the step's FFMA2 GEMMs")
         out["commit"] = cm
     out["clocks"] = clk
     out["gpu_launches"] = head["launches"]
