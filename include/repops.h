@@ -162,6 +162,25 @@ int repops_cross_entropy(const float *logits, int64_t rows, int64_t V, int64_t l
                          const int32_t *labels, float scale, float *loss, float *dlogits,
                          int64_t ldd, void *stream);
 
+/* Fused causal attention forward (P:571-574 operators, R-ATTN):
+ * per (b0 < batch0, b1 < batch1) with Q = Q + b0 s0 + b1 s1 (same for K, V), rows of
+ * stride ld, head dim hd:
+ *   S[i][j] = R-GEMM(Q, K^T) with the SCALE epilogue (every j < T),
+ *   P       = R-SOFTMAX(S) (causal: row i keeps keys j <= i, masked P = +0),
+ *   O[i][n] = R-GEMM(P, V) over all T keys.
+ * Bit-identical to repops_gemm_strided_batched(SCALE) -> repops_softmax -> repops_gemm:
+ * the same operation sequence per element, without the HBM round trips of S and P.
+ * S, P: [T][T] blocks at S + b0 sp0 + b1 sp1 (row stride T), optional (NULL = not
+ * stored).  O: rows of stride ldo at O + b0 so0 + b1 so1.  All rows 16-byte aligned.
+ * Supported: hd = 64, T % 128 == 0, T <= 512 (repops_attention_fwd_supported);
+ * otherwise REPOPS_ESHAPE (use the unfused composition).  REPOPS_EINVAL: null,
+ * misaligned, ld < hd. */
+int repops_attention_fwd_supported(int64_t T, int64_t hd);
+int repops_attention_fwd(int64_t T, int64_t hd, const float *Q, const float *K, const float *V, int64_t ld,
+                         int64_t s0, int64_t s1, float scale, int causal, float *S, float *P, int64_t sp0,
+                         int64_t sp1, float *O, int64_t ldo, int64_t so0, int64_t so1, int64_t batch0,
+                         int64_t batch1, void *stream);
+
 /* ------------------------------------------------------------------ elementwise
  * Software math (R5/R6): fixed IEEE-RN op chains. */
 int repops_exp(const float *x, int64_t n, float *y, void *stream);

@@ -22,7 +22,8 @@ __all__ = [
     "repops_gemm", "repops_gemm_strided_batched", "repops_sum_rows", "repops_sum_cols_seq", "repops_tree_sum",
     "repops_softmax", "repops_softmax_backward", "repops_layernorm", "repops_layernorm_backward",
     "repops_layernorm_backward_params", "repops_cross_entropy", "repops_exp", "repops_log", "repops_tanh",
-    "repops_rsqrt", "repops_gelu", "repops_gelu_backward", "repops_relu", "repops_relu_backward", "repops_sin", "repops_cos", "repops_erf", "repops_gelu_erf", "repops_convert", "repops_gemm_ex", "repops_rand_uniform",
+    "repops_rsqrt", "repops_gelu", "repops_gelu_backward", "repops_relu", "repops_relu_backward", "repops_sin", "repops_cos", "repops_erf", "repops_gelu_erf", "repops_convert", "repops_gemm_ex",
+    "repops_attention_fwd", "repops_attention_fwd_supported", "repops_rand_uniform",
     "repops_dropout", "repops_dropout_backward",
     "repops_gelu_erf_backward", "repops_rope_tables", "repops_ipc_alloc", "repops_ipc_open", "repops_ipc_close",
     "repops_ipc_free", "repops_p2p_tree_combine", "repops_p2p_signal", "repops_p2p_wait", "repops_add", "repops_embedding",
@@ -131,6 +132,28 @@ def repops_gemm_strided_batched(A, B, C_out, M, N, K, lda, ldb, ldc, sA, sB, sC,
     if t0 is not None:
         _TIMER.end("gemm", t0, 2 * M * N * K * batch[0] * batch[1], stream)
     return C_out
+
+
+# ------------------------------------------------------------------ fused attention (f4)
+def repops_attention_fwd_supported(T, hd):
+    return bool(lib().repops_attention_fwd_supported(int(T), int(hd)))
+
+
+def repops_attention_fwd(qkv, T, hd, ld, s, q_off, k_off, v_off, batch, O, ldo, so, S=None, P=None, sp=(0, 0),
+                         scale=1.0, causal=True, stream=None):
+    """Fused R-ATTN forward over a strided batch (element offsets / strides into the
+    storage of qkv, O, S, P): S = R-GEMM(Q K^T) * scale, P = causal R-SOFTMAX(S),
+    O = R-GEMM(P, V) -- bit-identical to the three unfused calls."""
+    _f32(qkv, "qkv"), _f32(O, "O")
+    base = qkv.data_ptr()
+    t0 = _TIMER.begin(stream) if _TIMER else None
+    check(lib().repops_attention_fwd(int(T), int(hd), base + 4 * q_off, base + 4 * k_off, base + 4 * v_off, int(ld),
+                                     int(s[0]), int(s[1]), float(scale), int(bool(causal)), _p(S), _p(P),
+                                     int(sp[0]), int(sp[1]), _p(O), int(ldo), int(so[0]), int(so[1]), int(batch[0]),
+                                     int(batch[1]), _stream(stream)), "repops_attention_fwd")
+    if t0 is not None:
+        _TIMER.end("gemm", t0, 4 * T * T * hd * batch[0] * batch[1], stream)
+    return O
 
 
 # ------------------------------------------------------------------ R30 stored precision

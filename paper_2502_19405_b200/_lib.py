@@ -58,6 +58,9 @@ SIGNATURES = {
     "repops_sin": (i32, [vp, i64, vp, vp]),
     "repops_cos": (i32, [vp, i64, vp, vp]),
     "repops_erf": (i32, [vp, i64, vp, vp]),
+    "repops_attention_fwd_supported": (i32, [i64, i64]),
+    "repops_attention_fwd": (i32, [i64, i64, vp, vp, vp, i64, i64, i64, f32, i32, vp, vp, i64, i64, vp, i64, i64, i64,
+                                   i64, i64, vp]),
     "repops_convert": (i32, [vp, i32, i64, i64, i64, vp, i32, i64, vp]),
     "repops_gemm_ex_workspace_bytes": (i64, [i64, i64, i64, i32, i32, i32]),
     "repops_gemm_ex": (i32, [i64, i64, i64, vp, i32, i64, i32, vp, i32, i64, i32, i32, vp, f32, vp, i32, i64, vp, i64,

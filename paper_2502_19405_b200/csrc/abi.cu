@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "../../include/repops.h"
+#include "attention.cuh"
 #include "common.cuh"
 #include "elementwise.cuh"
 #include "gemm.cuh"
@@ -236,6 +237,30 @@ int repops_gemm_strided_batched(int64_t M, int64_t N, int64_t K, const float *A,
                                 int64_t batch0, int64_t batch1, void *stream) {
     return gemm_common(M, N, K, A, lda, transA, sA0, sA1, B, ldb, transB, sB0, sB1, epi, bias, scale, C, ldc, sC0,
                        sC1, batch0, batch1, stream, -1);
+}
+
+// ------------------------------------------------------------------ fused attention (f4)
+int repops_attention_fwd_supported(int64_t T, int64_t hd) { return attention_fwd_supported(T, hd) ? 1 : 0; }
+
+int repops_attention_fwd(int64_t T, int64_t hd, const float *Q, const float *K, const float *V, int64_t ld,
+                         int64_t s0, int64_t s1, float scale, int causal, float *Sout, float *Pout, int64_t sp0,
+                         int64_t sp1, float *O, int64_t ldo, int64_t so0, int64_t so1, int64_t batch0,
+                         int64_t batch1, void *stream) {
+    REQ(T >= 0 && hd >= 0 && batch0 >= 0 && batch1 >= 0, "attention_fwd: negative extent");
+    if (T == 0 || batch0 * batch1 == 0) return REPOPS_OK;
+    if (!attention_fwd_supported(T, hd))
+        return fail(REPOPS_ESHAPE, "attention_fwd: T = %lld, hd = %lld unsupported (hd 64, T %% 128 == 0, T <= 512)",
+                    (long long)T, (long long)hd);
+    REQ(Q && K && V && O, "attention_fwd: null pointer");
+    REQ(ld >= hd && ldo >= hd, "attention_fwd: leading dimension < hd");
+    REQ(batch0 * batch1 <= 65535, "attention_fwd: too many (batch, head) pairs");
+    const bool al = a16(Q) && a16(K) && a16(V) && a16(O) && (!Sout || a16(Sout)) && (!Pout || a16(Pout)) && ld % 4 == 0 &&
+                    ldo % 4 == 0 && s0 % 4 == 0 && s1 % 4 == 0 && so0 % 4 == 0 && so1 % 4 == 0 && sp0 % 4 == 0 &&
+                    sp1 % 4 == 0;
+    REQ(al, "attention_fwd: rows must be 16-byte aligned");
+    return cuda_status(launch_attention_fwd(T, Q, K, V, ld, s0, s1, scale, causal, Sout, Pout, sp0, sp1, O, ldo, so0, so1,
+                                            batch0, batch1, S(stream)),
+                       "attention_fwd");
 }
 
 // ------------------------------------------------------------------ R30 stored precision

@@ -1,0 +1,265 @@
+// attention.cu -- fused non-online causal attention forward.
+//
+// One CTA owns BM = 64 query rows of one (batch, head) and keeps their FULL score
+// rows in shared memory (no online softmax, so no rescaling and no reordering):
+//   phase 1  S[i][j] = canon(fmul(fold_{k ascending} fma(Q[i,k], K[j,k], +0), scale))
+//            for every key j (R-GEMM with the SCALE epilogue), K streamed
+//            through shared memory in 128-key chunks (cp.async double buffer);
+//   phase 2  P = R-SOFTMAX causal of each row (reading R7): warp per row, max over
+//            the valid keys, exp_rn, the 128-slot CSUM + TREE128, y = e * fdiv(1, s);
+//   phase 3  O[i][n] = canon(fold_{j ascending over ALL T keys} fma(P[i][j], V[j][n], +0))
+//            (R-GEMM, masked P = +0 terms included exactly as the unfused GEMM does).
+// Every output element is produced by the same operation sequence as the unfused
+// composition repops_gemm(SCALE) -> repops_softmax(causal) -> repops_gemm, so S, P and O
+// are bit-identical to it (and to the oracle); what the fusion removes is the HBM
+// round trip of S and P between three launches.  S / P are written only if requested
+// (they are committed tensors of the GPT-2 step).
+//
+// Shapes: head dim 64, T a multiple of 128 and <= 512 (GPT-2); other shapes are
+// rejected by the ABI (the unfused path covers them).
+#include "attention.cuh"
+#include "common.cuh"
+
+namespace {
+
+using namespace ro;
+
+constexpr int HD = 64, BM = 64, KC = 128, THREADS = 256;
+constexpr int KLD = HD + 4;  // K chunk row stride (words): rows of one warp fall in distinct banks
+
+RO_DEV void cp16(float *dst, const float *src) {
+    unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
+}
+RO_DEV void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+RO_DEV void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+struct AttnArgs {
+    const float *Q, *K, *V;
+    int64_t ld, s0, s1;      // row stride of Q/K/V, batch strides (outer, inner)
+    float *S, *P;            // [T][T] per (batch, head), may be null
+    int64_t sp0, sp1;
+    float *O;
+    int64_t ldo, so0, so1;
+    int64_t batch1;
+    int T;
+    int causal;
+    float scale;
+};
+
+// rows [r0, r0 + KC) of a [.][HD] operand (row stride ld) -> dst rows of stride DLD
+template <int DLD>
+RO_DEV void load_chunk(float *dst, const float *src, int64_t ld, int tid) {
+#pragma unroll
+    for (int q = 0; q < KC * HD / 4 / THREADS; ++q) {
+        const int c = tid + q * THREADS;
+        const int r = c / (HD / 4), k4 = (c % (HD / 4)) * 4;
+        cp16(dst + r * DLD + k4, src + (int64_t)r * ld + k4);
+    }
+}
+
+__global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(AttnArgs a) {
+    extern __shared__ __align__(16) float sm[];
+    const int T = a.T, SLD = T + 4;
+    float *Qt = sm;                    // [HD][BM]  Q^T of this row block
+    float *Ss = Qt + HD * BM;          // [BM][T + 4] score rows, then probability rows
+    float *Kc = Ss + BM * SLD;         // [2][KC][KLD] K chunks, later [2][KC][HD] V chunks
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t bh = blockIdx.y, b0 = bh / a.batch1, b1 = bh % a.batch1;
+    const int q0 = blockIdx.x * BM;
+    const float *Q = a.Q + b0 * a.s0 + b1 * a.s1;
+    const float *K = a.K + b0 * a.s0 + b1 * a.s1;
+    const float *V = a.V + b0 * a.s0 + b1 * a.s1;
+    const int nchunks = T / KC;
+
+    // K chunk 0 in flight while Q^T is staged
+    load_chunk<KLD>(Kc, K, a.ld, tid);
+    cp_commit();
+#pragma unroll
+    for (int q = 0; q < BM * HD / 4 / THREADS; ++q) {
+        const int c = tid + q * THREADS;
+        const int r = c % BM, kq = (c / BM) * 4;  // a warp: 32 consecutive rows, one k quad
+        const float4 v = __ldg(reinterpret_cast<const float4 *>(Q + (int64_t)(q0 + r) * a.ld + kq));
+        Qt[(kq + 0) * BM + r] = v.x;
+        Qt[(kq + 1) * BM + r] = v.y;
+        Qt[(kq + 2) * BM + r] = v.z;
+        Qt[(kq + 3) * BM + r] = v.w;
+    }
+
+    // ---------------- phase 1: S^T chunk [KC keys x BM queries] per iteration
+    // thread: 8 keys (ty + 16 r) x 4 queries (tx * 4 + c); warps 8 (n) x 4 (m) lanes
+    {
+        const int tx = (warp & 1) * 8 + (lane & 7);
+        const int ty = (warp >> 1) * 4 + (lane >> 3);
+        for (int ch = 0; ch < nchunks; ++ch) {
+            if (ch + 1 < nchunks) load_chunk<KLD>(Kc + ((ch + 1) & 1) * KC * KLD, K + (int64_t)(ch + 1) * KC * a.ld,
+                                                  a.ld, tid);
+            cp_commit();
+            cp_wait<1>();
+            __syncthreads();
+            const float *Kb = Kc + (ch & 1) * KC * KLD;
+            float2 acc[8][2];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) acc[r][0] = acc[r][1] = make_float2(0.f, 0.f);  // +0 (R2)
+#pragma unroll
+            for (int kg = 0; kg < HD; kg += 4) {
+                float ak[8][4];
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    const float4 v = *reinterpret_cast<const float4 *>(Kb + (ty + 16 * r) * KLD + kg);
+                    ak[r][0] = v.x; ak[r][1] = v.y; ak[r][2] = v.z; ak[r][3] = v.w;
+                }
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    const float4 bq = *reinterpret_cast<const float4 *>(Qt + (kg + kk) * BM + tx * 4);
+                    const float2 b01 = make_float2(bq.x, bq.y), b23 = make_float2(bq.z, bq.w);
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) {
+                        const float2 av = make_float2(ak[r][kk], ak[r][kk]);
+                        acc[r][0] = __ffma2_rn(av, b01, acc[r][0]);  // fma(K[j,k], Q[i,k], acc): commutative
+                        acc[r][1] = __ffma2_rn(av, b23, acc[r][1]);
+                    }
+                }
+            }
+            // epilogue (R3, R10): S = canon(fmul(acc, scale)) into the query-major rows
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const int j = ch * KC + ty + 16 * r;
+                const float v[4] = {acc[r][0].x, acc[r][0].y, acc[r][1].x, acc[r][1].y};
+#pragma unroll
+                for (int c = 0; c < 4; ++c) Ss[(tx * 4 + c) * SLD + j] = canon(__fmul_rn(v[c], a.scale));
+            }
+            __syncthreads();  // chunk buffer free for the prefetch two iterations on
+        }
+    }
+
+    // V chunk 0 in flight during the softmax (the K buffers are free)
+    load_chunk<HD>(Kc, V, a.ld, tid);
+    cp_commit();
+
+    // write the score rows (coalesced float4)
+    if (a.S) {
+        float *Sg = a.S + b0 * a.sp0 + b1 * a.sp1 + (int64_t)q0 * T;
+        for (int c = tid; c < BM * T / 4; c += THREADS) {
+            const int r = c / (T / 4), j4 = (c % (T / 4)) * 4;
+            *reinterpret_cast<float4 *>(Sg + (int64_t)r * T + j4) = *reinterpret_cast<const float4 *>(Ss + r * SLD + j4);
+        }
+    }
+
+    __syncthreads();  // the score rows are read by the copy above before phase 2 overwrites them
+
+    // ---------------- phase 2: causal softmax, warp per row (softmax_warp's order)
+    for (int r = warp; r < BM; r += THREADS / 32) {
+        float *row = Ss + r * SLD;
+        const int L = a.causal ? q0 + r + 1 : T;
+        float m = __uint_as_float(0xFF800000u);
+        for (int b = 0; b < L; b += 128) {
+            const int i = b + 4 * lane;
+            const float4 v = *reinterpret_cast<const float4 *>(row + i);  // i + 3 < T always
+            if (i < L) m = fmaxf(m, v.x);
+            if (i + 1 < L) m = fmaxf(m, v.y);
+            if (i + 2 < L) m = fmaxf(m, v.z);
+            if (i + 3 < L) m = fmaxf(m, v.w);
+        }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) m = fmaxf(m, __shfl_xor_sync(FULL, m, off));
+        m = (m == 0.0f) ? 0.0f : m;
+        float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;
+        for (int b = 0; b < L; b += 128) {
+            const int i = b + 4 * lane;
+            const float4 v = *reinterpret_cast<const float4 *>(row + i);
+            if (i < L) p0 = __fadd_rn(p0, exp_rn(__fsub_rn(v.x, m)));
+            if (i + 1 < L) p1 = __fadd_rn(p1, exp_rn(__fsub_rn(v.y, m)));
+            if (i + 2 < L) p2 = __fadd_rn(p2, exp_rn(__fsub_rn(v.z, m)));
+            if (i + 3 < L) p3 = __fadd_rn(p3, exp_rn(__fsub_rn(v.w, m)));
+        }
+        const float rinv = __fdiv_rn(1.0f, tree128(p0, p1, p2, p3));
+        float *Pg = a.P ? a.P + b0 * a.sp0 + b1 * a.sp1 + (int64_t)(q0 + r) * T : nullptr;
+        for (int b = 0; b < T; b += 128) {
+            const int i = b + 4 * lane;
+            const float4 v = *reinterpret_cast<const float4 *>(row + i);
+            float o[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) o[c] = (i + c < L) ? canon(__fmul_rn(exp_rn(__fsub_rn(o[c], m)), rinv)) : 0.0f;
+            const float4 y = make_float4(o[0], o[1], o[2], o[3]);
+            *reinterpret_cast<float4 *>(row + i) = y;
+            if (Pg) *reinterpret_cast<float4 *>(Pg + i) = y;
+        }
+    }
+
+    // ---------------- phase 3: O = P V, keys ascending over all T (thread: 4 rows x 4 cols)
+    {
+        const int tx = (warp & 1) * 8 + (lane & 7);   // cols tx * 4 .. + 3
+        const int ty = (warp >> 1) * 4 + (lane >> 3); // rows ty + 16 r
+        float2 acc[4][2];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[r][0] = acc[r][1] = make_float2(0.f, 0.f);
+        for (int ch = 0; ch < nchunks; ++ch) {
+            if (ch + 1 < nchunks) load_chunk<HD>(Kc + ((ch + 1) & 1) * KC * KLD, V + (int64_t)(ch + 1) * KC * a.ld,
+                                                 a.ld, tid);
+            cp_commit();
+            cp_wait<1>();
+            __syncthreads();  // V chunk landed; (first iteration) every probability row written
+            const float *Vb = Kc + (ch & 1) * KC * KLD;
+            const float *Pr = Ss + ch * KC;
+#pragma unroll 4
+            for (int kg = 0; kg < KC; kg += 4) {
+                float ap[4][4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const float4 v = *reinterpret_cast<const float4 *>(Pr + (ty + 16 * r) * SLD + kg);
+                    ap[r][0] = v.x; ap[r][1] = v.y; ap[r][2] = v.z; ap[r][3] = v.w;
+                }
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    const float4 bv = *reinterpret_cast<const float4 *>(Vb + (kg + kk) * HD + tx * 4);
+                    const float2 b01 = make_float2(bv.x, bv.y), b23 = make_float2(bv.z, bv.w);
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const float2 av = make_float2(ap[r][kk], ap[r][kk]);
+                        acc[r][0] = __ffma2_rn(av, b01, acc[r][0]);
+                        acc[r][1] = __ffma2_rn(av, b23, acc[r][1]);
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        float *Og = a.O + b0 * a.so0 + b1 * a.so1;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int i = q0 + ty + 16 * r;
+            *reinterpret_cast<float4 *>(Og + (int64_t)i * a.ldo + tx * 4) =
+                make_float4(canon(acc[r][0].x), canon(acc[r][0].y), canon(acc[r][1].x), canon(acc[r][1].y));
+        }
+    }
+}
+
+}  // namespace
+
+size_t attention_fwd_smem_bytes(int64_t T) {
+    return (size_t)(HD * BM + BM * (T + 4) + 2 * KC * KLD) * sizeof(float);
+}
+
+bool attention_fwd_supported(int64_t T, int64_t hd) {
+    return hd == HD && T > 0 && T % KC == 0 && attention_fwd_smem_bytes(T) <= 227 * 1024;
+}
+
+cudaError_t launch_attention_fwd(int64_t T, const float *Q, const float *K, const float *V, int64_t ld, int64_t s0,
+                                 int64_t s1, float scale, int causal, float *S, float *P, int64_t sp0, int64_t sp1,
+                                 float *O, int64_t ldo, int64_t so0, int64_t so1, int64_t batch0, int64_t batch1,
+                                 cudaStream_t s) {
+    if (batch0 * batch1 == 0 || T == 0) return cudaSuccess;
+    const size_t smem = attention_fwd_smem_bytes(T);
+    static size_t attr = 0;
+    if (smem > attr) {
+        cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = smem;
+    }
+    AttnArgs a{Q, K, V, ld, s0, s1, S, P, sp0, sp1, O, ldo, so0, so1, batch1, (int)T, causal, scale};
+    dim3 grid((unsigned)(T / BM), (unsigned)(batch0 * batch1));
+    attn_fwd_kernel<<<grid, THREADS, smem, s>>>(a);
+    return cudaGetLastError();
+}

@@ -36,7 +36,7 @@ import torch
 
 import synth
 
-from . import (EPI_BIAS, EPI_SCALE, CommitPlan, repops_add, repops_cross_entropy, repops_embedding,
+from . import (EPI_BIAS, EPI_SCALE, CommitPlan, repops_add, repops_attention_fwd, repops_attention_fwd_supported, repops_cross_entropy, repops_embedding,
                repops_embedding_backward, repops_gelu, repops_gelu_backward, repops_gemm,
                repops_gemm_strided_batched, repops_layernorm, repops_layernorm_backward,
                repops_layernorm_backward_params, repops_softmax, repops_softmax_backward, repops_sum_cols_seq,
@@ -136,6 +136,8 @@ class GPT2Step:
             raise ValueError(f"unknown combine {combine!r}")
         self.combine, self.p2p_sync, self.p2p = combine, p2p_sync, None
         self.sliced_combine = combine == "sliced"
+        # f4: scores + causal softmax + PV as one kernel where the shape allows (same bits)
+        self.fused_attention = (not structure_only) and repops_attention_fwd_supported(cfg.seq, cfg.d // cfg.n_head)
         self.stash = {}
         self.step_no = 0
         c = cfg
@@ -360,18 +362,26 @@ class GPT2Step:
                     self._hook(f"h{l}/ln1")
                     self._gemm_tn(a["ln1"], W("attn.w"), epi=EPI_BIAS, bias=W("attn.b"), out=a["qkv"])
                     self._hook(f"h{l}/qkv")
-                    # scores S = (Q K^T) * 1/sqrt(hd), batched over (local shard, head)
-                    repops_gemm_strided_batched(a["qkv"], a["qkv"], a["S"], M=T, N=T, K=hd, lda=3 * d, ldb=3 * d,
-                                                ldc=T, sA=(T * 3 * d, hd), sB=(T * 3 * d, hd),
-                                                sC=(H * T * T, T * T), batch=(S_loc, H), transB=True,
-                                                epi=EPI_SCALE, scale=1.0 / np.sqrt(hd), offB=d)
-                    self._hook(f"h{l}/scores")
-                    repops_softmax(a["S"], causal=True, out=a["P"])
-                    self._hook(f"h{l}/softmax")
-                    repops_gemm_strided_batched(a["P"], a["qkv"], a["att"], M=T, N=hd, K=T, lda=T, ldb=3 * d,
-                                                ldc=d, sA=(H * T * T, T * T), sB=(T * 3 * d, hd), sC=(T * d, hd),
-                                                batch=(S_loc, H), offB=2 * d)
-                    self._hook(f"h{l}/pv")
+                    if self.fused_attention and self._fault is None:
+                        # one fused kernel writes the same S, P and att bits (f4; no HBM round
+                        # trip of S / P between launches); fault-injection runs keep the
+                        # per-op launches so a flipped S bit propagates as in the graph
+                        repops_attention_fwd(a["qkv"], T, hd, 3 * d, (T * 3 * d, hd), 0, d, 2 * d, (S_loc, H),
+                                             a["att"], d, (T * d, hd), S=a["S"], P=a["P"], sp=(H * T * T, T * T),
+                                             scale=1.0 / np.sqrt(hd), causal=True)
+                    else:
+                        # scores S = (Q K^T) * 1/sqrt(hd), batched over (local shard, head)
+                        repops_gemm_strided_batched(a["qkv"], a["qkv"], a["S"], M=T, N=T, K=hd, lda=3 * d,
+                                                    ldb=3 * d, ldc=T, sA=(T * 3 * d, hd), sB=(T * 3 * d, hd),
+                                                    sC=(H * T * T, T * T), batch=(S_loc, H), transB=True,
+                                                    epi=EPI_SCALE, scale=1.0 / np.sqrt(hd), offB=d)
+                        self._hook(f"h{l}/scores")
+                        repops_softmax(a["S"], causal=True, out=a["P"])
+                        self._hook(f"h{l}/softmax")
+                        repops_gemm_strided_batched(a["P"], a["qkv"], a["att"], M=T, N=hd, K=T, lda=T, ldb=3 * d,
+                                                    ldc=d, sA=(H * T * T, T * T), sB=(T * 3 * d, hd),
+                                                    sC=(T * d, hd), batch=(S_loc, H), offB=2 * d)
+                        self._hook(f"h{l}/pv")
                     self._gemm_tn(a["att"], W("proj.w"), epi=EPI_BIAS, bias=W("proj.b"), out=a["proj"])
                     self._hook(f"h{l}/proj")
                     repops_add(self.x[l], a["proj"], out=a["xmid"])

@@ -143,3 +143,25 @@ def test_unjoined_steps_give_the_joined_roots():
     b.join()
     torch.cuda.synchronize()
     assert [bytes(g.cpu().numpy()) for g in got] == ref
+
+
+def test_fused_attention_step_root_equals_unfused():
+    """a GPT-2 step whose attention shape takes the fused kernel (T = 512, hd = 64)
+    commits the same S, P, att bits as the three unfused launches: identical roots
+    over two steps (so the AdamW update and the second forward agree too)"""
+    from paper_2502_19405_b200.gpt2 import GPT2Config, GPT2Step
+    cfg = GPT2Config(n_layer=2, d=128, n_head=2, ffn=512, vocab=1000, n_pos=512, seq=512, shards=8)
+    roots = []
+    for fused in (True, False):
+        st = GPT2Step(cfg)
+        assert st.fused_attention  # the shape is supported
+        st.fused_attention = fused
+        r = []
+        for k in range(2):
+            st.set_tokens(k)
+            st.run()
+            r.append(st.device_root())
+        roots.append(r)
+        del st
+        torch.cuda.empty_cache()
+    assert roots[0] == roots[1]

@@ -532,3 +532,67 @@ def test_gemm_ex_parity(adt, bdt, cdt):
     if (adt, bdt, cdt) == ("f32", "f32", "f32"):   # all-f32 gemm_ex is repops_gemm bit for bit
         A, B = dev(synth.uniform(54, M * K).reshape(M, K)), dev(synth.uniform(55, K * N).reshape(K, N))
         assert_bits(host(R.repops_gemm_ex(A, B)), host(R.repops_gemm(A, B)), "gemm_ex == gemm")
+
+
+# ------------------------------------------------------------------ fused attention forward (f4)
+def _attn_inputs(S_, H, T, hd, seed):
+    d = H * hd
+    return synth.uniform(seed, (S_ * T, 3 * d), 2.0)
+
+
+@pytest.mark.parametrize("causal", [True, False])
+def test_attention_fwd_equals_unfused_and_oracle(causal):
+    """S, P and O of the fused kernel equal the three unfused calls bit for bit (every
+    head of a GPT-2-shaped layer) and the oracle composition (sampled heads)"""
+    S_, H, T, hd = 2, 12, 512, 64
+    d = H * hd
+    qkv_h = _attn_inputs(S_, H, T, hd, 31)
+    qkv = dev(qkv_h)
+    scale = 1.0 / np.sqrt(hd)
+    Sf = torch.empty(S_ * H * T, T, device="cuda")
+    Pf = torch.empty_like(Sf)
+    Of = torch.empty(S_ * T, d, device="cuda")
+    assert R.repops_attention_fwd_supported(T, hd)
+    R.repops_attention_fwd(qkv, T, hd, 3 * d, (T * 3 * d, hd), 0, d, 2 * d, (S_, H), Of, d, (T * d, hd), S=Sf, P=Pf,
+                           sp=(H * T * T, T * T), scale=scale, causal=causal)
+    Su = torch.empty_like(Sf)
+    Pu = torch.empty_like(Sf)
+    Ou = torch.empty_like(Of)
+    R.repops_gemm_strided_batched(qkv, qkv, Su, M=T, N=T, K=hd, lda=3 * d, ldb=3 * d, ldc=T, sA=(T * 3 * d, hd),
+                                  sB=(T * 3 * d, hd), sC=(H * T * T, T * T), batch=(S_, H), transB=True,
+                                  epi=R.EPI_SCALE, scale=scale, offB=d)
+    R.repops_softmax(Su, causal=causal, out=Pu)
+    R.repops_gemm_strided_batched(Pu, qkv, Ou, M=T, N=hd, K=T, lda=T, ldb=3 * d, ldc=d, sA=(H * T * T, T * T),
+                                  sB=(T * 3 * d, hd), sC=(T * d, hd), batch=(S_, H), offB=2 * d)
+    assert_bits(host(Sf), host(Su), "S fused vs unfused")
+    assert_bits(host(Pf), host(Pu), "P fused vs unfused")
+    assert_bits(host(Of), host(Ou), "O fused vs unfused")
+    Ph, Oh = host(Pf), host(Of)
+    for s_, h in ((0, 0), (1, 11)):
+        q = np.ascontiguousarray(qkv_h[s_ * T:(s_ + 1) * T, h * hd:(h + 1) * hd])
+        k = np.ascontiguousarray(qkv_h[s_ * T:(s_ + 1) * T, d + h * hd:d + (h + 1) * hd])
+        v = np.ascontiguousarray(qkv_h[s_ * T:(s_ + 1) * T, 2 * d + h * hd:2 * d + (h + 1) * hd])
+        s_ref = oracle.gemm(q, k, transB=True, epi=2, scale=scale)
+        p_ref = oracle.softmax(s_ref, causal=causal)
+        o_ref = oracle.gemm(p_ref, v)
+        r0 = (s_ * H + h) * T
+        assert_bits(Ph[r0:r0 + T], p_ref, f"P oracle s{s_} h{h}")
+        assert_bits(Oh[s_ * T:(s_ + 1) * T, h * hd:(h + 1) * hd], o_ref, f"O oracle s{s_} h{h}")
+
+
+def test_attention_fwd_optional_outputs_and_shapes():
+    S_, H, T, hd = 1, 2, 256, 64
+    d = H * hd
+    qkv = dev(_attn_inputs(S_, H, T, hd, 32))
+    O1 = torch.empty(T, d, device="cuda")
+    O2 = torch.empty(T, d, device="cuda")
+    P = torch.empty(H * T, T, device="cuda")
+    R.repops_attention_fwd(qkv, T, hd, 3 * d, (T * 3 * d, hd), 0, d, 2 * d, (S_, H), O1, d, (T * d, hd), P=P,
+                           sp=(H * T * T, T * T), scale=0.125)
+    R.repops_attention_fwd(qkv, T, hd, 3 * d, (T * 3 * d, hd), 0, d, 2 * d, (S_, H), O2, d, (T * d, hd),
+                           scale=0.125)   # neither S nor P stored: same O
+    assert_bits(host(O1), host(O2), "O with / without P")
+    assert not R.repops_attention_fwd_supported(512, 128)
+    assert not R.repops_attention_fwd_supported(100, 64)
+    with pytest.raises(R.RepopsError):
+        R.repops_attention_fwd(qkv, 100, hd, 3 * d, (T * 3 * d, hd), 0, d, 2 * d, (S_, H), O1, d, (T * d, hd))
