@@ -136,8 +136,12 @@ class GPT2Step:
             raise ValueError(f"unknown combine {combine!r}")
         self.combine, self.p2p_sync, self.p2p = combine, p2p_sync, None
         self.sliced_combine = combine == "sliced"
-        # f4: scores + causal softmax + PV as one kernel where the shape allows (same bits)
-        self.fused_attention = (not structure_only) and repops_attention_fwd_supported(cfg.seq, cfg.d // cfg.n_head)
+        # f4: scores + causal softmax + PV as one kernel (same bits).  Off by default: at the
+        # GPT-2 shape the fused kernel (1 CTA / SM, 213 KB of shared memory) measured 307 us
+        # per layer vs 253 us for the three tuned launches (tools/attn_fused_bench.py)
+        self.fused_attention = False
+        self.fused_attention_ok = (not structure_only) and repops_attention_fwd_supported(cfg.seq,
+                                                                                            cfg.d // cfg.n_head)
         self.stash = {}
         self.step_no = 0
         c = cfg
@@ -362,7 +366,7 @@ class GPT2Step:
                     self._hook(f"h{l}/ln1")
                     self._gemm_tn(a["ln1"], W("attn.w"), epi=EPI_BIAS, bias=W("attn.b"), out=a["qkv"])
                     self._hook(f"h{l}/qkv")
-                    if self.fused_attention and self._fault is None:
+                    if self.fused_attention and self.fused_attention_ok and self._fault is None:
                         # one fused kernel writes the same S, P and att bits (f4; no HBM round
                         # trip of S / P between launches); fault-injection runs keep the
                         # per-op launches so a flipped S bit propagates as in the graph

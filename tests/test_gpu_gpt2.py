@@ -154,7 +154,7 @@ def test_fused_attention_step_root_equals_unfused():
     roots = []
     for fused in (True, False):
         st = GPT2Step(cfg)
-        assert st.fused_attention  # the shape is supported
+        assert st.fused_attention_ok  # the shape is supported
         st.fused_attention = fused
         r = []
         for k in range(2):
