@@ -44,11 +44,13 @@ def fp32_peak_tflops(mhz: float, sms: int = 148) -> float:
     return sms * 128 * 2 * mhz * 1e6 / 1e12
 
 
-# SHA-256 leaf compression loop of sha256.o (cuobjdump -sass, tools/sass_mix.py): per
-# 64-byte block 673 SHF + 352 LOP3 + 244 IADD3 + 16 PRMT + 2 ISETP on the ALU pipe
-# (123 IMAD go to the FMA pipe).  The ALU pipe retires 16 lanes / clk / SMSP (rt = 2,
-# B300_MICROARCH "Pipe rates"), so the commit's roofline is ALU issue, not HBM.
-SHA_ALU_OPS_PER_64B = 1287
+# SHA-256 leaf compression (sha256.o, cuobjdump -sass): the all-ALU form is 673 SHF + 352
+# LOP3 + 244 IADD3 + 16 PRMT + 2 ISETP per 64-byte block; the default leaf kernel (mode 3)
+# moves the round / schedule adds and the schedule shifts to IMAD on the FMA pipe, leaving
+# 949 ALU ops per block (the function-wide ALU count drops by 338).  The ALU pipe retires
+# 16 lanes / clk / SMSP (rt = 2, B300_MICROARCH "Pipe rates"): the commit's roofline is
+# ALU issue, not HBM.
+SHA_ALU_OPS_PER_64B = 949
 
 
 def sha_alu_peak_gbs(mhz: float, sms: int = 148) -> float:
@@ -584,7 +586,7 @@ def main():
         cm["bound"] = "alu"
         cm["alu_peak_gbs"] = sha_alu_peak_gbs(clk["sm_max_mhz"] or 1965.0)
         cm["alu_frac"] = cm["gbs"] / cm["alu_peak_gbs"]
-        cm["note"] = ("SHA-256 is integer-ALU bound (1287 ALU ops per 64 B block); gbs is the commit plans' "
+        cm["note"] = ("SHA-256 is integer-ALU bound (949 ALU-pipe ops per 64 B block); gbs is the commit plans' "
                       "device time on the side stream, sharing the SMs with the step's FFMA2 GEMMs")
         out["commit"] = cm
     out["clocks"] = clk

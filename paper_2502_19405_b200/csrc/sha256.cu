@@ -19,12 +19,17 @@
 //                      || dims || nbytes || 4096 || data_root)
 // SHA-256 is integer-ALU bound on sm_100a (rotates = SHF, Ch/Maj/xor = LOP3,
 // adds = IADD3/IMAD), not HBM bound; see DESIGN.md §5.
+#include <cstdlib>
 #include <cstring>
 #include <utility>
 #include <vector>
 
 #include "common.cuh"
 #include "sha256.cuh"
+
+#ifndef RO_SHA_MODE_DEFAULT
+#define RO_SHA_MODE_DEFAULT 3
+#endif
 
 namespace {
 
@@ -47,8 +52,43 @@ RO_DEV void init_state(uint32_t s[8]) {
     s[4] = 0x510e527f; s[5] = 0x9b05688c; s[6] = 0x1f83d9ab; s[7] = 0x5be0cd19;
 }
 
-// FIPS 180-4 compression of one 512-bit block (w = big-endian message words)
-RO_DEV void compress(uint32_t s[8], uint32_t w[16]) {
+// runtime 1 (constant bank, unknown to ptxas): a * kOne + b is an IMAD on the FMA pipe,
+// so adds can be moved off the saturated ALU pipe (SHF / LOP3 / IADD3); bits unchanged
+__constant__ uint32_t kOne = 1u;
+
+RO_DEV uint32_t madd(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(kOne), "r"(b));
+    return r;
+}
+
+// powers of two in the constant bank (unknown to ptxas): x >> n = mul.hi(x, 2^(32-n)) and
+// rotr(x, n) = lo + hi of mul.wide(x, 2^(32-n)) (disjoint halves) run on the FMA pipe
+__constant__ uint32_t kP2[32] = {1u, 2u, 4u, 8u, 16u, 32u, 64u, 128u, 256u, 512u, 1024u, 2048u, 4096u, 8192u,
+                                 16384u, 32768u, 65536u, 131072u, 262144u, 524288u, 1048576u, 2097152u, 4194304u,
+                                 8388608u, 16777216u, 33554432u, 67108864u, 134217728u, 268435456u, 536870912u,
+                                 1073741824u, 2147483648u};
+RO_DEV uint32_t shr_fma(uint32_t x, int n) {
+    uint32_t r;
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(kP2[32 - n]));
+    return r;
+}
+RO_DEV uint32_t rotr_fma(uint32_t x, int n) {
+    uint64_t p;
+    asm("mul.wide.u32 %0, %1, %2;" : "=l"(p) : "r"(x), "r"(kP2[32 - n]));
+    return madd((uint32_t)p, (uint32_t)(p >> 32));
+}
+
+// FIPS 180-4 compression of one 512-bit block (w = big-endian message words).
+// MODE (bits-neutral pipe balance): 0 = all adds on the ALU pipe (IADD3); 1 = the round
+// adds (t1, e, a) as IMAD on the FMA pipe; 2 = also the message-schedule adds; 3 = also
+// the schedule's shifts (IMAD.HI); 4 = 3 + one rotate of Sigma0 / Sigma1 (IMAD.WIDE);
+// 5 = 3 + every remaining add.  Measured on B200 (tools/commit_one.py --time, 1 GiB):
+// 743 / 818 / 846 / 853 / 757 / 854 GB/s for modes 0..5 -> default 3 (ALU ops per 64-byte
+// block 1287 -> 949, the rest on the FMA pipe).  Occupancy is register-bound (56 regs,
+// 9 CTAs of 128 / SM; more CTAs spill).
+template <int MODE>
+RO_DEV void compress_m(uint32_t s[8], uint32_t w[16]) {
     uint32_t a = s[0], b = s[1], c = s[2], d = s[3], e = s[4], f = s[5], g = s[6], h = s[7];
 #pragma unroll
     for (int t = 0; t < 64; ++t) {
@@ -57,19 +97,35 @@ RO_DEV void compress(uint32_t s[8], uint32_t w[16]) {
             wt = w[t];
         } else {
             uint32_t w15 = w[(t - 15) & 15], w2 = w[(t - 2) & 15];
-            uint32_t s0 = rotr(w15, 7) ^ rotr(w15, 18) ^ (w15 >> 3);
-            uint32_t s1 = rotr(w2, 17) ^ rotr(w2, 19) ^ (w2 >> 10);
-            wt = w[t & 15] = w[t & 15] + s0 + w[(t - 7) & 15] + s1;
+            uint32_t s0 = rotr(w15, 7) ^ rotr(w15, 18) ^ (MODE >= 3 ? shr_fma(w15, 3) : (w15 >> 3));
+            uint32_t s1 = rotr(w2, 17) ^ rotr(w2, 19) ^ (MODE >= 3 ? shr_fma(w2, 10) : (w2 >> 10));
+            if (MODE >= 5)
+                wt = w[t & 15] = madd(madd(w[t & 15], s0), madd(w[(t - 7) & 15], s1));
+            else if (MODE >= 2)
+                wt = w[t & 15] = madd(w[t & 15], s0) + madd(w[(t - 7) & 15], s1);
+            else
+                wt = w[t & 15] = w[t & 15] + s0 + w[(t - 7) & 15] + s1;
         }
-        uint32_t S1 = rotr(e, 6) ^ rotr(e, 11) ^ rotr(e, 25);
+        uint32_t S1 = rotr(e, 6) ^ rotr(e, 11) ^ (MODE == 4 ? rotr_fma(e, 25) : rotr(e, 25));
         uint32_t ch = (e & f) ^ (~e & g);
-        uint32_t t1 = h + S1 + ch + kK[t] + wt;
-        uint32_t S0 = rotr(a, 2) ^ rotr(a, 13) ^ rotr(a, 22);
+        uint32_t S0 = rotr(a, 2) ^ rotr(a, 13) ^ (MODE == 4 ? rotr_fma(a, 22) : rotr(a, 22));
         uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
-        h = g; g = f; f = e; e = d + t1; d = c; c = b; b = a; a = t1 + S0 + mj;
+        uint32_t t1;
+        if (MODE >= 5) {
+            t1 = madd(madd(h, kK[t]), madd(S1, madd(ch, wt)));
+            h = g; g = f; f = e; e = madd(d, t1); d = c; c = b; b = a; a = madd(t1, madd(S0, mj));
+        } else if (MODE >= 1) {
+            t1 = madd(madd(h, kK[t]), madd(S1, ch + wt));
+            h = g; g = f; f = e; e = madd(d, t1); d = c; c = b; b = a; a = madd(t1, S0 + mj);
+        } else {
+            t1 = h + S1 + ch + kK[t] + wt;
+            h = g; g = f; f = e; e = d + t1; d = c; c = b; b = a; a = t1 + S0 + mj;
+        }
     }
     s[0] += a; s[1] += b; s[2] += c; s[3] += d; s[4] += e; s[5] += f; s[6] += g; s[7] += h;
 }
+
+RO_DEV void compress(uint32_t s[8], uint32_t w[16]) { compress_m<0>(s, w); }
 
 // SHA-256 of a short local byte message (<= 119 bytes -> at most 2 blocks)
 RO_DEV void sha_small(const uint8_t *msg, int len, uint32_t out[8]) {
@@ -111,6 +167,7 @@ RO_DEV uint32_t leaf_msg_byte(const uint8_t *data, int64_t len, int64_t m, int64
 }
 
 // SHA-256(0x00 || chunk), chunk = data[0..len), len <= 4096
+template <int MODE = 0>
 RO_DEV void hash_leaf(const uint8_t *__restrict__ data, int64_t len, uint32_t st[8]) {
     init_state(st);
     const int64_t nblk = (len + 1 + 9 + 63) / 64;
@@ -132,7 +189,7 @@ RO_DEV void hash_leaf(const uint8_t *__restrict__ data, int64_t len, uint32_t st
 #pragma unroll
             for (int i = 1; i < 16; ++i) w[i] = __byte_perm(D[i - 1], D[i], 0x3456);
             prev = D[15];
-            compress(st, w);
+            compress_m<MODE>(st, w);
         }
     }
     for (; blk < nblk; ++blk) {
@@ -184,6 +241,7 @@ RO_DEV int64_t find_seg(const int64_t *prefix, int n, int64_t g) {
     return lo;
 }
 
+template <int MODE>
 __global__ void leaf_kernel(const DevTensor *__restrict__ ts, int n, const int64_t *__restrict__ chunk_prefix,
                             int64_t total, Digest *__restrict__ out) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -194,7 +252,7 @@ __global__ void leaf_kernel(const DevTensor *__restrict__ ts, int n, const int64
         int64_t off = c * 4096;
         int64_t len = T.nbytes - off < 4096 ? T.nbytes - off : 4096;
         uint32_t st[8];
-        hash_leaf(T.data + off, len, st);
+        hash_leaf<MODE>(T.data + off, len, st);
         Digest d;
 #pragma unroll
         for (int i = 0; i < 8; ++i) d.h[i] = st[i];
@@ -423,7 +481,22 @@ static cudaError_t run_kernels(const Plan &p, const Layout &L, uint8_t *base, in
         int64_t blocks = (p.total_chunks + 127) / 128;
         int64_t cap = (int64_t)ro_host::num_sms() * g_leaf_ctas_per_sm.load(std::memory_order_relaxed);
         if (blocks > cap) blocks = cap;
-        leaf_kernel<<<(unsigned)blocks, 128, 0, s>>>(dts, n, tab + L.chunk_prefix_at, p.total_chunks, A);
+        static const int sha_mode = [] {  // tuning hook (bits-neutral): REPOPS_SHA_MODE=0/1/2
+            const char *e = getenv("REPOPS_SHA_MODE");
+            return e ? atoi(e) : RO_SHA_MODE_DEFAULT;
+        }();
+        if (sha_mode == 5)
+            leaf_kernel<5><<<(unsigned)blocks, 128, 0, s>>>(dts, n, tab + L.chunk_prefix_at, p.total_chunks, A);
+        else if (sha_mode == 4)
+            leaf_kernel<4><<<(unsigned)blocks, 128, 0, s>>>(dts, n, tab + L.chunk_prefix_at, p.total_chunks, A);
+        else if (sha_mode == 3)
+            leaf_kernel<3><<<(unsigned)blocks, 128, 0, s>>>(dts, n, tab + L.chunk_prefix_at, p.total_chunks, A);
+        else if (sha_mode == 2)
+            leaf_kernel<2><<<(unsigned)blocks, 128, 0, s>>>(dts, n, tab + L.chunk_prefix_at, p.total_chunks, A);
+        else if (sha_mode == 1)
+            leaf_kernel<1><<<(unsigned)blocks, 128, 0, s>>>(dts, n, tab + L.chunk_prefix_at, p.total_chunks, A);
+        else
+            leaf_kernel<0><<<(unsigned)blocks, 128, 0, s>>>(dts, n, tab + L.chunk_prefix_at, p.total_chunks, A);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     for (size_t q = 0; q < p.passes.size(); ++q) {

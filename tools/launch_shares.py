@@ -1,6 +1,8 @@
 """Kernel-time shares (and DRAM traffic) of one step from an ncu launch list
 (--metrics gpu__time_duration.sum[,dram__bytes_read.sum,dram__bytes_write.sum] --csv).
-Usage: launch_shares.py launches.csv launches_per_step"""
+Usage: launch_shares.py launches.csv launches_per_step [marker_kernel step_index]
+  (with a marker: the step = the launches from the step_index-th launch of marker_kernel
+   up to the next one)"""
 import collections, csv, re, sys
 
 rows = list(csv.reader(open(sys.argv[1])))
@@ -14,7 +16,14 @@ for r in rows[hi + 1:]:
     d = launch.setdefault(r[ii], {'name': r[ki]})
     d[r[mi]] = float(r[vi].replace(',', ''))
 per = int(sys.argv[2])
-step = list(launch.values())[-per:]
+allv = list(launch.values())
+if len(sys.argv) > 4:
+    marks = [i for i, d in enumerate(allv) if sys.argv[3] in d['name']]
+    k = int(sys.argv[4])
+    step = allv[marks[k]:marks[k + 1]]
+    assert len(step) == per, (len(step), per)
+else:
+    step = allv[-per:]
 
 
 def short(k):
