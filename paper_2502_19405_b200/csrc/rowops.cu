@@ -119,7 +119,7 @@ __global__ void sum_rows_cta(const float *__restrict__ x, int64_t rows, int64_t 
 // FR-row chunks of the [rows x 32] panel into shared memory with coalesced
 // 128-byte row reads (double buffered), and warp 0's 32 lanes run the 32 folds
 // out of shared memory (lane = column: conflict-free).
-constexpr int FC = 32, FR = 64;
+constexpr int FC = 32, FR = 64;  // panel columns, rows per double-buffered chunk
 
 __global__ void __launch_bounds__(256) sum_cols_seq_kernel(const float *__restrict__ x, int64_t rows, int64_t cols,
                                                            int64_t ld, int64_t nseg, float *__restrict__ out,
@@ -133,10 +133,14 @@ __global__ void __launch_bounds__(256) sum_cols_seq_kernel(const float *__restri
     const int64_t jl = j0 + lane;
     const int64_t nch = (per + FR - 1) / FR;
     auto load = [&](int buf, int64_t c) {
-        for (int r = w; r < FR; r += 8) {
-            const int64_t t = c * FR + r;
-            tile[buf][r][lane] = (t < per && jl < cols) ? __ldg(base + t * ld + jl) : 0.f;
+        float v[FR / 8];  // all loads of this warp in flight before the shared stores
+#pragma unroll
+        for (int q = 0; q < FR / 8; ++q) {
+            const int64_t t = c * FR + w + 8 * q;
+            v[q] = (t < per && jl < cols) ? __ldg(base + t * ld + jl) : 0.f;
         }
+#pragma unroll
+        for (int q = 0; q < FR / 8; ++q) tile[buf][w + 8 * q][lane] = v[q];
     };
     float acc = 0.f;
     if (nch > 0) load(0, 0);
@@ -146,6 +150,7 @@ __global__ void __launch_bounds__(256) sum_cols_seq_kernel(const float *__restri
         if (w == 0) {
             const int n = (int)min((int64_t)FR, per - c * FR);
             const float(*tb)[FC] = tile[c & 1];
+#pragma unroll 8
             for (int r = 0; r < n; ++r) acc = __fadd_rn(acc, tb[r][lane]);  // ascending rows
         }
         __syncthreads();
@@ -422,12 +427,23 @@ __global__ void layernorm_params_kernel(const float *__restrict__ dy, const floa
     const int64_t jl = j0 + lane;
     const int64_t nch = (per + FR - 1) / FR;
     auto load = [&](int buf, int64_t c) {
-        for (int r = w; r < FR; r += 8) {
+        float vd[FR / 8], vx[FR / 8], vm[FR / 8], vr[FR / 8];  // every load in flight first
+#pragma unroll
+        for (int q = 0; q < FR / 8; ++q) {
+            const int r = w + 8 * q;
             const int64_t t = s * per + c * FR + r;
             const bool ok = (c * FR + r < per) && jl < cols;
-            tdy[buf][r][lane] = ok ? __ldg(dy + t * cols + jl) : 0.f;
-            txh[buf][r][lane] =
-                ok ? __fmul_rn(__fsub_rn(__ldg(x + t * cols + jl), __ldg(mean + t)), __ldg(rstd + t)) : 0.f;
+            vd[q] = ok ? __ldg(dy + t * cols + jl) : 0.f;
+            vx[q] = ok ? __ldg(x + t * cols + jl) : 0.f;
+            vm[q] = ok ? __ldg(mean + t) : 0.f;
+            vr[q] = ok ? __ldg(rstd + t) : 0.f;
+        }
+#pragma unroll
+        for (int q = 0; q < FR / 8; ++q) {
+            const int r = w + 8 * q;
+            const bool ok = (c * FR + r < per) && jl < cols;
+            tdy[buf][r][lane] = vd[q];
+            txh[buf][r][lane] = ok ? __fmul_rn(__fsub_rn(vx[q], vm[q]), vr[q]) : 0.f;
         }
     };
     float ag = 0.f, ab = 0.f;
@@ -438,6 +454,7 @@ __global__ void layernorm_params_kernel(const float *__restrict__ dy, const floa
         if (w == 0) {
             const int n = (int)min((int64_t)FR, per - c * FR);
             const int b = (int)(c & 1);
+#pragma unroll 8
             for (int r = 0; r < n; ++r) {  // ascending rows of the segment
                 const float d = tdy[b][r][lane];
                 ag = __fmaf_rn(d, txh[b][r][lane], ag);

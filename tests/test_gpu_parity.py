@@ -386,6 +386,18 @@ def test_commit_parity_and_batching():
         assert host(R.verde_commit_tensor(t, ws=ws)).tobytes() == r
 
 
+def test_commit_reduce_group_boundaries():
+    """chunk counts around the reduce kernel's 8-node thread blocks and 1024-node CTA
+    groups (ragged last block, ragged last group, one node over) match the oracle's
+    RFC 6962 tree"""
+    counts = [2, 3, 7, 8, 9, 15, 17, 1023, 1024, 1025, 1031, 2047, 2049, 8 * 1024 + 3]
+    arrs = [synth.uniform(900 + c, c * 1024 - (c % 3) * 7) for c in counts]   # c chunks, last one short
+    ts = [dev(a) for a in arrs]
+    digs = host(R.verde_commit_tensors(ts, ws=R.CommitWorkspace()))
+    for i, a in enumerate(arrs):
+        assert digs[i].tobytes() == oracle.commit_tensor(a), counts[i]
+
+
 def test_commit_large_tensor_multi_pass():
     # > 256*256 leaves -> three reduce passes (logits-sized tensors)
     a = synth.uniform(77, 256 * 256 * 1024 + 12345)  # 268 MB

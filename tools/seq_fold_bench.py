@@ -1,0 +1,35 @@
+"""R-SEQ column folds at the GPT-2 step's shapes (bias / LayerNorm parameter gradients
+per shard): CUDA-event time per launch and effective GB/s."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2502_19405_b200 as R  # noqa: E402
+
+
+def t(fn, n=20):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(n):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / n
+
+
+for cols in (768, 2304, 3072):
+    x = torch.rand(4096, cols, device="cuda")
+    out = torch.empty(8, cols, device="cuda")
+    ms = t(lambda: R.repops_sum_cols_seq(x, nseg=8, out=out))
+    print(f"sum_cols_seq 4096x{cols}: {ms * 1e3:7.1f} us  {x.numel() * 4 / ms / 1e6:7.1f} GB/s")
+dy = torch.rand(4096, 768, device="cuda")
+x = torch.rand(4096, 768, device="cuda")
+mu, rs = torch.rand(4096, device="cuda"), torch.rand(4096, device="cuda")
+dg, db = torch.empty(8, 768, device="cuda"), torch.empty(8, 768, device="cuda")
+ms = t(lambda: R.repops_layernorm_backward_params(dy, x, mu, rs, nseg=8, dgamma=dg, dbeta=db))
+print(f"layernorm_params 4096x768: {ms * 1e3:7.1f} us  {2 * dy.numel() * 4 / ms / 1e6:7.1f} GB/s")
