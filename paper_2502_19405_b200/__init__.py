@@ -84,6 +84,21 @@ class KernelTimer:
         return {k: (sum(a.elapsed_time(b) for a, b, _ in v), sum(w for _, _, w in v), len(v))
                 for k, v in self.ev.items()}
 
+    def union_ms(self, kind, ref):
+        """Length of the union of `kind`'s launch intervals (ms), measured from the event
+        `ref` recorded before them: launches of one family that overlap each other on
+        different streams are counted once."""
+        iv = sorted((ref.elapsed_time(a), ref.elapsed_time(b)) for a, b, _ in self.ev.get(kind, []))
+        tot, cur_s, cur_e = 0.0, None, None
+        for s, e in iv:
+            if cur_e is None or s > cur_e:
+                if cur_e is not None:
+                    tot += cur_e - cur_s
+                cur_s, cur_e = s, e
+            else:
+                cur_e = max(cur_e, e)
+        return tot + ((cur_e - cur_s) if cur_e is not None else 0.0)
+
 
 _TIMER = None
 

@@ -140,6 +140,9 @@ class GPT2Step:
         # GPT-2 shape the fused kernel (1 CTA / SM, 213 KB of shared memory) measured 307 us
         # per layer vs 253 us for the three tuned launches (tools/attn_fused_bench.py)
         self.fused_attention = False
+        # backward: weight / bias / LN-parameter gradients on an aux stream beside the dgrads
+        self.aux_wgrad = not structure_only
+        self.aux = None if structure_only else torch.cuda.Stream(device=device)
         self.fused_attention_ok = (not structure_only) and repops_attention_fwd_supported(cfg.seq,
                                                                                             cfg.d // cfg.n_head)
         self.stash = {}
@@ -287,6 +290,24 @@ class GPT2Step:
 
     def launch(self, fn):
         self._cur[1].append(fn)
+
+    def _aux(self, fn):
+        """Run fn's launches on the aux stream, ordered after everything enqueued so far on
+        the current stream (its inputs); inline when disabled or under fault injection
+        (so an injected fault lands exactly where the per-op order puts it)."""
+        if not self.aux_wgrad or self._fault is not None:
+            fn()
+            return
+        main = torch.cuda.current_stream()
+        self.aux.wait_stream(main)
+        with torch.cuda.stream(self.aux):
+            fn()
+        self._aux_pending = True
+
+    def _aux_join(self):
+        if getattr(self, "_aux_pending", False):
+            torch.cuda.current_stream().wait_stream(self.aux)
+            self._aux_pending = False
 
     def _hook(self, label):
         """Fault-injection point after the launch of op `label` (config 5 dispute demo)."""
@@ -475,13 +496,16 @@ class GPT2Step:
         if first_local:
             def head_bwd():
                 wte = self.pview(self.params, "wte")
+                o = self.off["wte"][0]
+
+                def w_lm():  # aux stream, beside the LM dgrad (N = 768: wave-quantised)
+                    repops_gemm_strided_batched(self.dlogits, self.lnf, gl, M=c.vocab, N=d, K=T, lda=c.vocab_ld,
+                                                ldb=d, ldc=d, sA=(T * c.vocab_ld, 0), sB=(T * d, 0),
+                                                sC=(self.P, 0), batch=(S_loc, 1), transA=True, offC=o)
+                    self._hook("head/lm_wgrad")
+                self._aux(w_lm)
                 self._gemm_tn(self.dlogits[:, :c.vocab], wte, out=self.dlnf)
                 self._hook("head/lm_dgrad")
-                o = self.off["wte"][0]
-                repops_gemm_strided_batched(self.dlogits, self.lnf, gl, M=c.vocab, N=d, K=T, lda=c.vocab_ld, ldb=d,
-                                            ldc=d, sA=(T * c.vocab_ld, 0), sB=(T * d, 0), sC=(self.P, 0),
-                                            batch=(S_loc, 1), transA=True, offC=o)
-                self._hook("head/lm_wgrad")
                 repops_layernorm_backward(self.dlnf, self.x[L], self.pview(self.params, "lnf.g"), self.muf, self.rsf,
                                           out=self.dx[L])
                 self._hook("head/lnf_bwd")
@@ -489,6 +513,7 @@ class GPT2Step:
                                                  dgamma=gl[:, self.off["lnf.g"][0]:],
                                                  dbeta=gl[:, self.off["lnf.b"][0]:], ldo=self.P)
                 self._hook("head/lnf_params")
+                self._aux_join()
             self.launch(head_bwd)
         t_dlnf = T_(pre + "dlnf", V(self.dlnf, T), s)
         self.node(OP["LM_DGRAD"], s, {}, [t_dlog, P_["wte"][0]], [t_dlnf], pre + "lm_dgrad")
@@ -514,42 +539,73 @@ class GPT2Step:
                 def bwd(l=l, a=a, g=g, W=W, p=p):
                     dout = self.dx[l + 1]
                     o = lambda n: self.off[p + n][0]  # noqa: E731
+                    # weight / bias / LN-parameter gradients depend only on this layer's
+                    # activations and output gradients: they run on the aux stream beside
+                    # the dgrad chain (filling its wave-quantised GEMMs' idle SM slots)
+
+                    def w_fc2():
+                        repops_gemm_strided_batched(a["gelu"], dout, gl, M=c.ffn, N=d, K=T, lda=c.ffn, ldb=d,
+                                                    ldc=d, sA=(T * c.ffn, 0), sB=(T * d, 0), sC=(self.P, 0),
+                                                    batch=(S_loc, 1), transA=True, offC=o("fc2.w"))
+                        self._hook(f"h{l}/fc2_wgrad")
+                        repops_sum_cols_seq(dout, nseg=S_loc, out=gl[:, o("fc2.b"):], ldo=self.P)
+                        self._hook(f"h{l}/fc2_bgrad")
+
+                    def w_fc():
+                        repops_gemm_strided_batched(a["ln2"], g["dfc"], gl, M=d, N=c.ffn, K=T, lda=d, ldb=c.ffn,
+                                                    ldc=c.ffn, sA=(T * d, 0), sB=(T * c.ffn, 0), sC=(self.P, 0),
+                                                    batch=(S_loc, 1), transA=True, offC=o("fc.w"))
+                        self._hook(f"h{l}/fc_wgrad")
+                        repops_sum_cols_seq(g["dfc"], nseg=S_loc, out=gl[:, o("fc.b"):], ldo=self.P)
+                        self._hook(f"h{l}/fc_bgrad")
+
+                    def w_ln2():
+                        repops_layernorm_backward_params(g["dln2"], a["xmid"], a["mu2"], a["rs2"], nseg=S_loc,
+                                                         dgamma=gl[:, o("ln2.g"):], dbeta=gl[:, o("ln2.b"):],
+                                                         ldo=self.P)
+                        self._hook(f"h{l}/ln2_params")
+
+                    def w_proj():
+                        repops_gemm_strided_batched(a["att"], g["dxmid"], gl, M=d, N=d, K=T, lda=d, ldb=d, ldc=d,
+                                                    sA=(T * d, 0), sB=(T * d, 0), sC=(self.P, 0), batch=(S_loc, 1),
+                                                    transA=True, offC=o("proj.w"))
+                        self._hook(f"h{l}/proj_wgrad")
+                        repops_sum_cols_seq(g["dxmid"], nseg=S_loc, out=gl[:, o("proj.b"):], ldo=self.P)
+                        self._hook(f"h{l}/proj_bgrad")
+
+                    def w_qkv():
+                        repops_gemm_strided_batched(a["ln1"], g["dqkv"], gl, M=d, N=3 * d, K=T, lda=d, ldb=3 * d,
+                                                    ldc=3 * d, sA=(T * d, 0), sB=(T * 3 * d, 0), sC=(self.P, 0),
+                                                    batch=(S_loc, 1), transA=True, offC=o("attn.w"))
+                        self._hook(f"h{l}/qkv_wgrad")
+                        repops_sum_cols_seq(g["dqkv"], nseg=S_loc, out=gl[:, o("attn.b"):], ldo=self.P)
+                        self._hook(f"h{l}/qkv_bgrad")
+
+                    def w_ln1():
+                        repops_layernorm_backward_params(g["dln1"], self.x[l], a["mu1"], a["rs1"], nseg=S_loc,
+                                                         dgamma=gl[:, o("ln1.g"):], dbeta=gl[:, o("ln1.b"):],
+                                                         ldo=self.P)
+                        self._hook(f"h{l}/ln1_params")
+
                     # FC2
                     self._gemm_tn(dout, self.wT[p + "fc2.w"], out=g["dgelu"])
                     self._hook(f"h{l}/fc2_dgrad")
-                    repops_gemm_strided_batched(a["gelu"], dout, gl, M=c.ffn, N=d, K=T, lda=c.ffn, ldb=d, ldc=d,
-                                                sA=(T * c.ffn, 0), sB=(T * d, 0), sC=(self.P, 0), batch=(S_loc, 1),
-                                                transA=True, offC=o("fc2.w"))
-                    self._hook(f"h{l}/fc2_wgrad")
-                    repops_sum_cols_seq(dout, nseg=S_loc, out=gl[:, o("fc2.b"):], ldo=self.P)
-                    self._hook(f"h{l}/fc2_bgrad")
+                    self._aux(w_fc2)
                     repops_gelu_backward(a["fc"], g["dgelu"], out=g["dfc"])
                     self._hook(f"h{l}/gelu_bwd")
                     # FC
+                    self._aux(w_fc)
                     self._gemm_tn(g["dfc"], self.wT[p + "fc.w"], out=g["dln2"])
                     self._hook(f"h{l}/fc_dgrad")
-                    repops_gemm_strided_batched(a["ln2"], g["dfc"], gl, M=d, N=c.ffn, K=T, lda=d, ldb=c.ffn,
-                                                ldc=c.ffn, sA=(T * d, 0), sB=(T * c.ffn, 0), sC=(self.P, 0),
-                                                batch=(S_loc, 1), transA=True, offC=o("fc.w"))
-                    self._hook(f"h{l}/fc_wgrad")
-                    repops_sum_cols_seq(g["dfc"], nseg=S_loc, out=gl[:, o("fc.b"):], ldo=self.P)
-                    self._hook(f"h{l}/fc_bgrad")
                     # LN2 (+ residual gradient)
                     repops_layernorm_backward(g["dln2"], a["xmid"], W("ln2.g"), a["mu2"], a["rs2"], dres=dout,
                                               out=g["dxmid"])
                     self._hook(f"h{l}/ln2_bwd")
-                    repops_layernorm_backward_params(g["dln2"], a["xmid"], a["mu2"], a["rs2"], nseg=S_loc,
-                                                     dgamma=gl[:, o("ln2.g"):], dbeta=gl[:, o("ln2.b"):], ldo=self.P)
-                    self._hook(f"h{l}/ln2_params")
+                    self._aux(w_ln2)
                     # proj
+                    self._aux(w_proj)
                     self._gemm_tn(g["dxmid"], self.wT[p + "proj.w"], out=g["datt"])
                     self._hook(f"h{l}/proj_dgrad")
-                    repops_gemm_strided_batched(a["att"], g["dxmid"], gl, M=d, N=d, K=T, lda=d, ldb=d, ldc=d,
-                                                sA=(T * d, 0), sB=(T * d, 0), sC=(self.P, 0), batch=(S_loc, 1),
-                                                transA=True, offC=o("proj.w"))
-                    self._hook(f"h{l}/proj_wgrad")
-                    repops_sum_cols_seq(g["dxmid"], nseg=S_loc, out=gl[:, o("proj.b"):], ldo=self.P)
-                    self._hook(f"h{l}/proj_bgrad")
                     # attention
                     repops_gemm_strided_batched(g["datt"], a["qkv"], g["dP"], M=T, N=T, K=hd, lda=d, ldb=3 * d,
                                                 ldc=T, sA=(T * d, hd), sB=(T * 3 * d, hd), sC=(H * T * T, T * T),
@@ -569,20 +625,14 @@ class GPT2Step:
                                                 sC=(T * 3 * d, hd), batch=(S_loc, H), transA=True, offC=d)
                     self._hook(f"h{l}/attn_dqkv")
                     # QKV
+                    self._aux(w_qkv)
                     self._gemm_tn(g["dqkv"], self.wT[p + "attn.w"], out=g["dln1"])
                     self._hook(f"h{l}/qkv_dgrad")
-                    repops_gemm_strided_batched(a["ln1"], g["dqkv"], gl, M=d, N=3 * d, K=T, lda=d, ldb=3 * d,
-                                                ldc=3 * d, sA=(T * d, 0), sB=(T * 3 * d, 0), sC=(self.P, 0),
-                                                batch=(S_loc, 1), transA=True, offC=o("attn.w"))
-                    self._hook(f"h{l}/qkv_wgrad")
-                    repops_sum_cols_seq(g["dqkv"], nseg=S_loc, out=gl[:, o("attn.b"):], ldo=self.P)
-                    self._hook(f"h{l}/qkv_bgrad")
                     repops_layernorm_backward(g["dln1"], self.x[l], W("ln1.g"), a["mu1"], a["rs1"], dres=g["dxmid"],
                                               out=self.dx[l])
                     self._hook(f"h{l}/ln1_bwd")
-                    repops_layernorm_backward_params(g["dln1"], self.x[l], a["mu1"], a["rs1"], nseg=S_loc,
-                                                     dgamma=gl[:, o("ln1.g"):], dbeta=gl[:, o("ln1.b"):], ldo=self.P)
-                    self._hook(f"h{l}/ln1_params")
+                    self._aux(w_ln1)
+                    self._aux_join()  # the phase's commit plan hashes every output of the layer
                 self.launch(bwd)
             pre = f"s{s}/h{l}/"
             t_dout = t_dx
