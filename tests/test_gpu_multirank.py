@@ -77,11 +77,18 @@ def test_tiny_step_root_identical_across_world_sizes(world, tiny_single):
         assert pdig == tiny_single[3]
 
 
-def test_full_gpt2_step_root_world2_equals_world1():
-    one = _run(1, False)[0]
-    for rank, root, loss, pdig in _run(2, False):
-        assert root == one[1], f"rank {rank}: full GPT-2 step root differs between G=1 and G=2"
-        assert pdig == one[3]
+@pytest.fixture(scope="module")
+def full_single():
+    return _run(1, False)[0]
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_full_gpt2_step_root_equals_world1(world, full_single):
+    """the full GPT-2 124M step (every operator output committed) gives the G = 1 root
+    with its 8 shards spread over 2, 4 and 8 rank processes"""
+    for rank, root, loss, pdig in _run(world, False):
+        assert root == full_single[1], f"rank {rank}: full GPT-2 step root differs between G=1 and G={world}"
+        assert pdig == full_single[3]
 
 
 @pytest.mark.parametrize("world", [2, 4])
