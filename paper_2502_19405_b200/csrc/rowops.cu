@@ -189,6 +189,67 @@ __global__ void softmax_warp(const float *__restrict__ x, int64_t rows, int64_t 
     }
 }
 
+// warp per row, row length <= 128 * NQ, row held in registers: one global read, exp
+// computed once (the same e_i feed the slot sums and the outputs), one global write.
+// Lane l owns elements b + 4l .. b + 4l + 3 for b = 0, 128, ... exactly as
+// softmax_warp, so the max, the 128-slot CSUM order and every output bit are identical.
+template <int NQ>
+__global__ void softmax_warp_reg(const float *__restrict__ x, int64_t rows, int64_t cols, int64_t ldx, int causal,
+                                 float *__restrict__ y, int64_t ldy) {
+    const int lane = threadIdx.x & 31;
+    const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (r >= rows) return;
+    const float *xr = x + r * ldx;
+    float *yr = y + r * ldy;
+    const int64_t L = causal ? (r % cols) + 1 : cols;
+    const bool al = al16(xr);
+    float v[NQ][4];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        const int64_t i = 128 * q + 4 * lane;
+        if (128 * q < L) {  // warp-uniform: chunks past the valid length are never read
+            const float4 t = ld4(xr, i, L, al);
+            v[q][0] = t.x; v[q][1] = t.y; v[q][2] = t.z; v[q][3] = t.w;
+        } else {
+            v[q][0] = v[q][1] = v[q][2] = v[q][3] = 0.f;
+        }
+    }
+    float m = __uint_as_float(0xFF800000u);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            if (128 * q + 4 * lane + c < L) m = fmaxf(m, v[q][c]);
+    m = warp_max(m);
+    m = (m == 0.0f) ? 0.0f : m;
+    float p[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            if (128 * q + 4 * lane + c < L) {
+                v[q][c] = exp_rn(__fsub_rn(v[q][c], m));
+                p[c] = __fadd_rn(p[c], v[q][c]);
+            }
+    const float rinv = __fdiv_rn(1.0f, tree128(p[0], p[1], p[2], p[3]));
+    const bool aly = al16(yr);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        const int64_t i = 128 * q + 4 * lane;
+        if (128 * q >= cols) break;
+        float o[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) o[c] = (i + c < L) ? canon(__fmul_rn(v[q][c], rinv)) : 0.0f;
+        if (aly && i + 3 < cols) {
+            *reinterpret_cast<float4 *>(yr + i) = make_float4(o[0], o[1], o[2], o[3]);
+        } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                if (i + c < cols) yr[i + c] = o[c];
+        }
+    }
+}
+
 // CTA per row (cols > 4096): tiles of 4096 per warp, CSUM over tile sums
 __global__ void softmax_cta(const float *__restrict__ x, int64_t rows, int64_t cols, int64_t ldx, int causal,
                             float *__restrict__ y, int64_t ldy) {
@@ -540,7 +601,11 @@ cudaError_t launch_sum_cols_seq(const float *x, int64_t rows, int64_t cols, int6
 cudaError_t launch_softmax(const float *x, int64_t rows, int64_t cols, int64_t ldx, int causal, float *y,
                            int64_t ldy, cudaStream_t s) {
     if (rows == 0 || cols == 0) return cudaSuccess;
-    if (cols <= TILE_ELEMS) softmax_warp<<<rows_grid(rows, 8), 256, 0, s>>>(x, rows, cols, ldx, causal, y, ldy);
+    if (cols <= 512)
+        softmax_warp_reg<4><<<rows_grid(rows, 8), 256, 0, s>>>(x, rows, cols, ldx, causal, y, ldy);
+    else if (cols <= 1024)
+        softmax_warp_reg<8><<<rows_grid(rows, 8), 256, 0, s>>>(x, rows, cols, ldx, causal, y, ldy);
+    else if (cols <= TILE_ELEMS) softmax_warp<<<rows_grid(rows, 8), 256, 0, s>>>(x, rows, cols, ldx, causal, y, ldy);
     else {
         size_t nt = (size_t)((cols + TILE_ELEMS - 1) / TILE_ELEMS);
         softmax_cta<<<(unsigned)rows, 512, (((nt + 3) & ~3ull) + 32) * sizeof(float), s>>>(x, rows, cols, ldx,

@@ -33,3 +33,13 @@ mu, rs = torch.rand(4096, device="cuda"), torch.rand(4096, device="cuda")
 dg, db = torch.empty(8, 768, device="cuda"), torch.empty(8, 768, device="cuda")
 ms = t(lambda: R.repops_layernorm_backward_params(dy, x, mu, rs, nseg=8, dgamma=dg, dbeta=db))
 print(f"layernorm_params 4096x768: {ms * 1e3:7.1f} us  {2 * dy.numel() * 4 / ms / 1e6:7.1f} GB/s")
+
+# row operators of the GPT-2 step: causal softmax over the [8 x 12 x 512, 512] scores
+S = torch.rand(8 * 12 * 512, 512, device="cuda") * 8 - 4
+Pm = torch.empty_like(S)
+ms = t(lambda: R.repops_softmax(S, causal=True, out=Pm))
+print(f"softmax causal 49152x512: {ms * 1e3:7.1f} us  {2 * S.numel() * 4 / ms / 1e6:7.1f} GB/s (algorithmic)")
+X = torch.rand(4096, 768, device="cuda")
+g_, b_ = torch.rand(768, device="cuda"), torch.rand(768, device="cuda")
+ms = t(lambda: R.repops_layernorm(X, g_, b_))
+print(f"layernorm 4096x768: {ms * 1e3:7.1f} us  {2 * X.numel() * 4 / ms / 1e6:7.1f} GB/s (algorithmic)")
