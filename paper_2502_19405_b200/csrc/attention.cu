@@ -17,15 +17,23 @@
 //
 // Shapes: head dim 64, T a multiple of 128 and <= 512 (GPT-2); other shapes are
 // rejected by the ABI (the unfused path covers them).
+#include <cstdlib>
+
 #include "attention.cuh"
 #include "common.cuh"
+
+#ifndef RO_ATTN_VARIANT_DEFAULT
+#define RO_ATTN_VARIANT_DEFAULT 1
+#endif
 
 namespace {
 
 using namespace ro;
 
-constexpr int HD = 64, BM = 64, KC = 128, THREADS = 256;
+constexpr int HD = 64;
 constexpr int KLD = HD + 4;  // K chunk row stride (words): rows of one warp fall in distinct banks
+// variants: <BM query rows, KC keys per chunk, THREADS>.  (64, 128, 256): 213 KB, 1 CTA / SM;
+// (32, 64, 128): 109 KB, 2 CTAs / SM so one CTA's softmax overlaps the other's FFMA2 phases
 
 RO_DEV void cp16(float *dst, const float *src) {
     unsigned d = (unsigned)__cvta_generic_to_shared(dst);
@@ -49,7 +57,7 @@ struct AttnArgs {
 };
 
 // rows [r0, r0 + KC) of a [.][HD] operand (row stride ld) -> dst rows of stride DLD
-template <int DLD>
+template <int DLD, int KC, int THREADS>
 RO_DEV void load_chunk(float *dst, const float *src, int64_t ld, int tid) {
 #pragma unroll
     for (int q = 0; q < KC * HD / 4 / THREADS; ++q) {
@@ -59,7 +67,12 @@ RO_DEV void load_chunk(float *dst, const float *src, int64_t ld, int tid) {
     }
 }
 
+template <int BM, int KC, int THREADS>
 __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(AttnArgs a) {
+    // phase-1 thread tile: TM1 keys x TN1 queries; phase-3: TM3 rows x 4 columns
+    constexpr int TX = 16, TY = THREADS / TX, WX = TX / 8;
+    constexpr int TN1 = BM / TX, TM1 = KC / TY, TM3 = BM / TY;
+    static_assert(TN1 == 2 || TN1 == 4, "phase-1 query pairs");
     extern __shared__ __align__(16) float sm[];
     const int T = a.T, SLD = T + 4;
     float *Qt = sm;                    // [HD][BM]  Q^T of this row block
@@ -75,7 +88,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(AttnArgs a) {
     const int nchunks = T / KC;
 
     // K chunk 0 in flight while Q^T is staged
-    load_chunk<KLD>(Kc, K, a.ld, tid);
+    load_chunk<KLD, KC, THREADS>(Kc, K, a.ld, tid);
     cp_commit();
 #pragma unroll
     for (int q = 0; q < BM * HD / 4 / THREADS; ++q) {
@@ -89,54 +102,66 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(AttnArgs a) {
     }
 
     // ---------------- phase 1: S^T chunk [KC keys x BM queries] per iteration
-    // thread: 8 keys (ty + 16 r) x 4 queries (tx * 4 + c); warps 8 (n) x 4 (m) lanes
+    // thread: TM1 keys (ty + TY r) x TN1 queries (tx * TN1 + c); warps 8 (n) x 4 (m) lanes
     {
-        const int tx = (warp & 1) * 8 + (lane & 7);
-        const int ty = (warp >> 1) * 4 + (lane >> 3);
+        const int tx = (warp % WX) * 8 + (lane & 7);
+        const int ty = (warp / WX) * 4 + (lane >> 3);
         for (int ch = 0; ch < nchunks; ++ch) {
-            if (ch + 1 < nchunks) load_chunk<KLD>(Kc + ((ch + 1) & 1) * KC * KLD, K + (int64_t)(ch + 1) * KC * a.ld,
-                                                  a.ld, tid);
+            if (ch + 1 < nchunks)
+                load_chunk<KLD, KC, THREADS>(Kc + ((ch + 1) & 1) * KC * KLD, K + (int64_t)(ch + 1) * KC * a.ld, a.ld,
+                                             tid);
             cp_commit();
             cp_wait<1>();
             __syncthreads();
             const float *Kb = Kc + (ch & 1) * KC * KLD;
-            float2 acc[8][2];
+            float2 acc[TM1][TN1 / 2];
 #pragma unroll
-            for (int r = 0; r < 8; ++r) acc[r][0] = acc[r][1] = make_float2(0.f, 0.f);  // +0 (R2)
+            for (int r = 0; r < TM1; ++r)
+#pragma unroll
+                for (int h = 0; h < TN1 / 2; ++h) acc[r][h] = make_float2(0.f, 0.f);  // +0 (R2)
 #pragma unroll
             for (int kg = 0; kg < HD; kg += 4) {
-                float ak[8][4];
+                float ak[TM1][4];
 #pragma unroll
-                for (int r = 0; r < 8; ++r) {
-                    const float4 v = *reinterpret_cast<const float4 *>(Kb + (ty + 16 * r) * KLD + kg);
+                for (int r = 0; r < TM1; ++r) {
+                    const float4 v = *reinterpret_cast<const float4 *>(Kb + (ty + TY * r) * KLD + kg);
                     ak[r][0] = v.x; ak[r][1] = v.y; ak[r][2] = v.z; ak[r][3] = v.w;
                 }
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
-                    const float4 bq = *reinterpret_cast<const float4 *>(Qt + (kg + kk) * BM + tx * 4);
-                    const float2 b01 = make_float2(bq.x, bq.y), b23 = make_float2(bq.z, bq.w);
+                    float2 bq[TN1 / 2];
+                    if constexpr (TN1 == 4) {
+                        const float4 q4 = *reinterpret_cast<const float4 *>(Qt + (kg + kk) * BM + tx * 4);
+                        bq[0] = make_float2(q4.x, q4.y);
+                        bq[1] = make_float2(q4.z, q4.w);
+                    } else {
+                        bq[0] = *reinterpret_cast<const float2 *>(Qt + (kg + kk) * BM + tx * 2);
+                    }
 #pragma unroll
-                    for (int r = 0; r < 8; ++r) {
+                    for (int r = 0; r < TM1; ++r) {
                         const float2 av = make_float2(ak[r][kk], ak[r][kk]);
-                        acc[r][0] = __ffma2_rn(av, b01, acc[r][0]);  // fma(K[j,k], Q[i,k], acc): commutative
-                        acc[r][1] = __ffma2_rn(av, b23, acc[r][1]);
+#pragma unroll
+                        for (int h = 0; h < TN1 / 2; ++h)  // fma(K[j,k], Q[i,k], acc): commutative
+                            acc[r][h] = __ffma2_rn(av, bq[h], acc[r][h]);
                     }
                 }
             }
             // epilogue (R3, R10): S = canon(fmul(acc, scale)) into the query-major rows
 #pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                const int j = ch * KC + ty + 16 * r;
-                const float v[4] = {acc[r][0].x, acc[r][0].y, acc[r][1].x, acc[r][1].y};
+            for (int r = 0; r < TM1; ++r) {
+                const int j = ch * KC + ty + TY * r;
 #pragma unroll
-                for (int c = 0; c < 4; ++c) Ss[(tx * 4 + c) * SLD + j] = canon(__fmul_rn(v[c], a.scale));
+                for (int h = 0; h < TN1 / 2; ++h) {
+                    Ss[(tx * TN1 + 2 * h) * SLD + j] = canon(__fmul_rn(acc[r][h].x, a.scale));
+                    Ss[(tx * TN1 + 2 * h + 1) * SLD + j] = canon(__fmul_rn(acc[r][h].y, a.scale));
+                }
             }
             __syncthreads();  // chunk buffer free for the prefetch two iterations on
         }
     }
 
     // V chunk 0 in flight during the softmax (the K buffers are free)
-    load_chunk<HD>(Kc, V, a.ld, tid);
+    load_chunk<HD, KC, THREADS>(Kc, V, a.ld, tid);
     cp_commit();
 
     // write the score rows (coalesced float4)
@@ -189,16 +214,17 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(AttnArgs a) {
         }
     }
 
-    // ---------------- phase 3: O = P V, keys ascending over all T (thread: 4 rows x 4 cols)
+    // ---------------- phase 3: O = P V, keys ascending over all T (thread: TM3 rows x 4 cols)
     {
-        const int tx = (warp & 1) * 8 + (lane & 7);   // cols tx * 4 .. + 3
-        const int ty = (warp >> 1) * 4 + (lane >> 3); // rows ty + 16 r
-        float2 acc[4][2];
+        const int tx = (warp % WX) * 8 + (lane & 7);   // cols tx * 4 .. + 3
+        const int ty = (warp / WX) * 4 + (lane >> 3);  // rows ty + TY r
+        float2 acc[TM3][2];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) acc[r][0] = acc[r][1] = make_float2(0.f, 0.f);
+        for (int r = 0; r < TM3; ++r) acc[r][0] = acc[r][1] = make_float2(0.f, 0.f);
         for (int ch = 0; ch < nchunks; ++ch) {
-            if (ch + 1 < nchunks) load_chunk<HD>(Kc + ((ch + 1) & 1) * KC * KLD, V + (int64_t)(ch + 1) * KC * a.ld,
-                                                 a.ld, tid);
+            if (ch + 1 < nchunks)
+                load_chunk<HD, KC, THREADS>(Kc + ((ch + 1) & 1) * KC * KLD, V + (int64_t)(ch + 1) * KC * a.ld, a.ld,
+                                            tid);
             cp_commit();
             cp_wait<1>();
             __syncthreads();  // V chunk landed; (first iteration) every probability row written
@@ -206,10 +232,10 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(AttnArgs a) {
             const float *Pr = Ss + ch * KC;
 #pragma unroll 4
             for (int kg = 0; kg < KC; kg += 4) {
-                float ap[4][4];
+                float ap[TM3][4];
 #pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    const float4 v = *reinterpret_cast<const float4 *>(Pr + (ty + 16 * r) * SLD + kg);
+                for (int r = 0; r < TM3; ++r) {
+                    const float4 v = *reinterpret_cast<const float4 *>(Pr + (ty + TY * r) * SLD + kg);
                     ap[r][0] = v.x; ap[r][1] = v.y; ap[r][2] = v.z; ap[r][3] = v.w;
                 }
 #pragma unroll
@@ -217,7 +243,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(AttnArgs a) {
                     const float4 bv = *reinterpret_cast<const float4 *>(Vb + (kg + kk) * HD + tx * 4);
                     const float2 b01 = make_float2(bv.x, bv.y), b23 = make_float2(bv.z, bv.w);
 #pragma unroll
-                    for (int r = 0; r < 4; ++r) {
+                    for (int r = 0; r < TM3; ++r) {
                         const float2 av = make_float2(ap[r][kk], ap[r][kk]);
                         acc[r][0] = __ffma2_rn(av, b01, acc[r][0]);
                         acc[r][1] = __ffma2_rn(av, b23, acc[r][1]);
@@ -228,8 +254,8 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(AttnArgs a) {
         }
         float *Og = a.O + b0 * a.so0 + b1 * a.so1;
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            const int i = q0 + ty + 16 * r;
+        for (int r = 0; r < TM3; ++r) {
+            const int i = q0 + ty + TY * r;
             *reinterpret_cast<float4 *>(Og + (int64_t)i * a.ldo + tx * 4) =
                 make_float4(canon(acc[r][0].x), canon(acc[r][0].y), canon(acc[r][1].x), canon(acc[r][1].y));
         }
@@ -238,12 +264,38 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(AttnArgs a) {
 
 }  // namespace
 
-size_t attention_fwd_smem_bytes(int64_t T) {
+static int attn_variant() {  // 0 = (64, 128, 256), 1 = (32, 64, 128); REPOPS_ATTN_VARIANT overrides
+    static const int v = [] {
+        const char *e = getenv("REPOPS_ATTN_VARIANT");
+        return e ? atoi(e) : RO_ATTN_VARIANT_DEFAULT;
+    }();
+    return v;
+}
+
+template <int BM, int KC>
+static size_t smem_bytes(int64_t T) {
     return (size_t)(HD * BM + BM * (T + 4) + 2 * KC * KLD) * sizeof(float);
 }
 
+size_t attention_fwd_smem_bytes(int64_t T) { return attn_variant() ? smem_bytes<32, 64>(T) : smem_bytes<64, 128>(T); }
+
 bool attention_fwd_supported(int64_t T, int64_t hd) {
-    return hd == HD && T > 0 && T % KC == 0 && attention_fwd_smem_bytes(T) <= 227 * 1024;
+    return hd == HD && T > 0 && T % 128 == 0 && smem_bytes<64, 128>(T) <= 227 * 1024;
+}
+
+template <int BM, int KC, int THREADS>
+static cudaError_t launch_variant(const AttnArgs &a, int64_t batch, cudaStream_t s) {
+    const size_t smem = smem_bytes<BM, KC>(a.T);
+    static size_t attr = 0;
+    if (smem > attr) {
+        cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<BM, KC, THREADS>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = smem;
+    }
+    dim3 grid((unsigned)(a.T / BM), (unsigned)batch);
+    attn_fwd_kernel<BM, KC, THREADS><<<grid, THREADS, smem, s>>>(a);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_attention_fwd(int64_t T, const float *Q, const float *K, const float *V, int64_t ld, int64_t s0,
@@ -251,15 +303,7 @@ cudaError_t launch_attention_fwd(int64_t T, const float *Q, const float *K, cons
                                  float *O, int64_t ldo, int64_t so0, int64_t so1, int64_t batch0, int64_t batch1,
                                  cudaStream_t s) {
     if (batch0 * batch1 == 0 || T == 0) return cudaSuccess;
-    const size_t smem = attention_fwd_smem_bytes(T);
-    static size_t attr = 0;
-    if (smem > attr) {
-        cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        attr = smem;
-    }
     AttnArgs a{Q, K, V, ld, s0, s1, S, P, sp0, sp1, O, ldo, so0, so1, batch1, (int)T, causal, scale};
-    dim3 grid((unsigned)(T / BM), (unsigned)(batch0 * batch1));
-    attn_fwd_kernel<<<grid, THREADS, smem, s>>>(a);
-    return cudaGetLastError();
+    return attn_variant() ? launch_variant<32, 64, 128>(a, batch0 * batch1, s)
+                          : launch_variant<64, 128, 256>(a, batch0 * batch1, s);
 }
