@@ -573,6 +573,75 @@ __global__ void cross_entropy_cta(const float *logits, int64_t rows, int64_t V, 
     }
 }
 
+// Cross entropy with the whole row staged in shared memory (V <= CE_SMEM_MAX): one HBM
+// read of the logits (cp.async), exp computed once and kept in shared memory for the
+// gradient; the max, the per-tile 128-slot CSUMs, the CSUM over tile sums and every
+// output operation are those of cross_entropy_cta, so the bits are identical.
+constexpr int CE_THREADS = 1024;
+
+__global__ void __launch_bounds__(CE_THREADS, 1) cross_entropy_smem(
+    const float *logits, int64_t rows, int64_t V, int64_t ld, const int32_t *__restrict__ labels, float scale,
+    float *__restrict__ loss, float *dlogits, int64_t ldd) {
+    extern __shared__ __align__(16) float sm[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = CE_THREADS / 32;
+    const int64_t r = blockIdx.x;
+    const float *xr = logits + r * ld;
+    const int Vi = (int)V, V4 = Vi & ~3, Vp = (Vi + 3) & ~3;
+    const int nt = (Vi + TILE - 1) / TILE;
+    float *row = sm;
+    float *tsum = sm + Vp;
+    float *scratch = tsum + ((nt + 3) & ~3);
+    for (int i = 4 * threadIdx.x; i < V4; i += 4 * CE_THREADS) {
+        const unsigned d = (unsigned)__cvta_generic_to_shared(row + i);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(xr + i));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    for (int i = V4 + threadIdx.x; i < Vp; i += CE_THREADS) row[i] = (i < Vi) ? xr[i] : 0.f;
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncthreads();
+    // max over the row (order-free; NaN ignored, zero -> +0 as in cross_entropy_cta)
+    float m = __uint_as_float(0xFF800000u);
+    for (int i = threadIdx.x; i < Vi; i += CE_THREADS) m = fmaxf(m, row[i]);
+    m = warp_max(m);
+    if (lane == 0) scratch[w] = m;
+    __syncthreads();
+    m = (lane < nw) ? scratch[lane] : __uint_as_float(0xFF800000u);
+    m = warp_max(m);
+    m = (m == 0.0f) ? 0.0f : m;
+    // per-tile CSUM of e = exp(x - m) (warp_expsum_tile's slot order); e kept in place
+    for (int t = w; t < nt; t += nw) {
+        const int t0 = t * TILE, n = min(TILE, Vi - t0);
+        float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;
+        for (int b = 0; b < n; b += 128) {
+            const int i = b + 4 * lane;
+            if (i >= n) continue;  // (i < n implies i + 3 < Vp: the float4 stays in the row)
+            float4 v = *reinterpret_cast<const float4 *>(row + t0 + i);
+            { v.x = exp_rn(__fsub_rn(v.x, m)); p0 = __fadd_rn(p0, v.x); }
+            if (i + 1 < n) { v.y = exp_rn(__fsub_rn(v.y, m)); p1 = __fadd_rn(p1, v.y); }
+            if (i + 2 < n) { v.z = exp_rn(__fsub_rn(v.z, m)); p2 = __fadd_rn(p2, v.z); }
+            if (i + 3 < n) { v.w = exp_rn(__fsub_rn(v.w, m)); p3 = __fadd_rn(p3, v.w); }
+            *reinterpret_cast<float4 *>(row + t0 + i) = v;
+        }
+        const float ts = tree128(p0, p1, p2, p3);
+        if (lane == 0) tsum[t] = ts;
+    }
+    __syncthreads();
+    const float s = (nt == 1) ? tsum[0] : warp_csum_tile(tsum, nt, lane);
+    const int32_t lab = __ldg(labels + r);
+    const float xl = xr[lab];
+    if (loss && threadIdx.x == 0) loss[r] = canon(__fsub_rn(__fadd_rn(m, log_rn(s)), xl));
+    if (dlogits) {
+        __syncthreads();  // every read of the global row (xl) before an aliased write
+        const float rinv = __fdiv_rn(1.0f, s);
+        float *dr = dlogits + r * ldd;
+        for (int i = threadIdx.x; i < Vi; i += CE_THREADS) {
+            const float p = __fmul_rn(row[i], rinv);
+            const float d = __fsub_rn(p, (i == lab) ? 1.0f : 0.0f);
+            dr[i] = canon(__fmul_rn(d, scale));
+        }
+    }
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
@@ -662,6 +731,20 @@ cudaError_t launch_cross_entropy(const float *logits, int64_t rows, int64_t V, i
                                  float scale, float *loss, float *dlogits, int64_t ldd, cudaStream_t s) {
     if (rows == 0) return cudaSuccess;
     size_t nt = (size_t)((V + TILE_ELEMS - 1) / TILE_ELEMS);
+    const size_t smem = (size_t)(((V + 3) & ~3ll) + ((nt + 3) & ~3ull) + 32) * sizeof(float);
+    const bool al = ((reinterpret_cast<uintptr_t>(logits) & 15u) == 0) && (ld % 4 == 0);
+    if (al && smem <= 227 * 1024) {
+        static size_t attr = 0;
+        if (smem > attr) {
+            cudaError_t e = cudaFuncSetAttribute(cross_entropy_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem);
+            if (e != cudaSuccess) return e;
+            attr = smem;
+        }
+        cross_entropy_smem<<<(unsigned)rows, CE_THREADS, smem, s>>>(logits, rows, V, ld, labels, scale, loss, dlogits,
+                                                                     ldd);
+        return cudaGetLastError();
+    }
     cross_entropy_cta<<<(unsigned)rows, 512, (((nt + 3) & ~3ull) + 32) * sizeof(float), s>>>(
         logits, rows, V, ld, labels, scale, loss, dlogits, ldd);
     return cudaGetLastError();

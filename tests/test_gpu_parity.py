@@ -226,7 +226,7 @@ def test_layernorm_parity(rows, cols):
         assert_bits(host(gdb), dbt, "dbeta")
 
 
-@pytest.mark.parametrize("rows,V", [(8, 4), (16, 1000), (6, 50257)])
+@pytest.mark.parametrize("rows,V", [(8, 4), (16, 1000), (6, 50257), (3, 4097), (2, 55000)])
 def test_cross_entropy_parity(rows, V):
     x = synth.uniform(11, (rows, V), 8.0)
     lab = synth.integers(12, rows, V)
@@ -242,6 +242,19 @@ def test_cross_entropy_parity(rows, V):
     gl2, _ = R.repops_cross_entropy(t, dev(lab), scale=2.0 ** -12, dlogits=t, V=V)
     assert_bits(host(gl2), loss, "ce loss padded")
     assert_bits(host(t)[:, :V], d, "ce grad in place")
+    # 16-byte aligned padded rows (the GPT-2 logits layout, ld = V rounded up to 64):
+    # the shared-memory-row kernel, in place and out of place
+    ld = (V + 63) // 64 * 64
+    xp = np.zeros((rows, ld), np.float32)
+    xp[:, :V] = x
+    t = dev(xp)
+    out = torch.zeros_like(t)
+    gl3, _ = R.repops_cross_entropy(t, dev(lab), scale=2.0 ** -12, dlogits=out, V=V)
+    assert_bits(host(gl3), loss, "ce loss aligned")
+    assert_bits(host(out)[:, :V], d, "ce grad aligned")
+    gl4, _ = R.repops_cross_entropy(t, dev(lab), scale=2.0 ** -12, dlogits=t, V=V)
+    assert_bits(host(gl4), loss, "ce loss aligned in place")
+    assert_bits(host(t)[:, :V], d, "ce grad aligned in place")
 
 
 # ------------------------------------------------------------------ elementwise / math

@@ -43,3 +43,9 @@ X = torch.rand(4096, 768, device="cuda")
 g_, b_ = torch.rand(768, device="cuda"), torch.rand(768, device="cuda")
 ms = t(lambda: R.repops_layernorm(X, g_, b_))
 print(f"layernorm 4096x768: {ms * 1e3:7.1f} us  {2 * X.numel() * 4 / ms / 1e6:7.1f} GB/s (algorithmic)")
+logits = torch.rand(4096, 50304, device="cuda") * 8 - 4
+labels = torch.randint(0, 50257, (4096,), dtype=torch.int32, device="cuda")
+dl = torch.empty_like(logits)
+lo = torch.empty(4096, device="cuda")
+ms = t(lambda: R.repops_cross_entropy(logits, labels, scale=2.0 ** -12, loss=lo, dlogits=dl, V=50257), n=5)
+print(f"cross_entropy 4096x50257: {ms * 1e3:7.1f} us  {2 * 4096 * 50257 * 4 / ms / 1e6:7.1f} GB/s (algorithmic)")
