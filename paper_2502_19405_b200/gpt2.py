@@ -142,7 +142,9 @@ class GPT2Step:
         self.fused_attention = False
         # backward: weight / bias / LN-parameter gradients on an aux stream beside the dgrads
         self.aux_wgrad = not structure_only
-        self.aux = None if structure_only else torch.cuda.Stream(device=device)
+        # the aux stream carries critical-path work (joined every layer): high priority, so
+        # the block scheduler prefers it over the commit side stream's SHA-256 CTAs
+        self.aux = None if structure_only else torch.cuda.Stream(device=device, priority=-1)
         self.fused_attention_ok = (not structure_only) and repops_attention_fwd_supported(cfg.seq,
                                                                                             cfg.d // cfg.n_head)
         self.stash = {}
