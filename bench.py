@@ -299,8 +299,9 @@ class LlamaPrefillBench:
         self.root = None
 
     def step(self):
-        self.st.run()
-        self.root = self.st.device_root()
+        with GPT2Train.stream_ctx(self):   # high-priority pass stream, commits on the low-priority side
+            self.st.run()
+            self.root = self.st.device_root()   # waits for the pass (host)
 
     def e2e_step(self):
         self.st.set_tokens()
