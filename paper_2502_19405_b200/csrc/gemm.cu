@@ -402,7 +402,7 @@ cudaError_t launch_cfg(const GemmParams &p, cudaStream_t s) {
 //   5: 128 x 64, 6: 64 x 128 (8 x 8), 3 CTAs/SM  -- the usual winners
 //   2, 7, 8, 9: stage / fragment / occupancy variants kept for tools/gemm_tune.py
 //   10..14: 6, 5, 3, 1, 4 with XP (A stored M x K transposed in shared memory)
-int gemm_num_cfgs() { return 19; }
+int gemm_num_cfgs() { return 20; }
 std::atomic<int> g_gemm_smem_floor{0};
 
 cudaError_t gemm_launch(const GemmParams &p, cudaStream_t s, int force_cfg) {
@@ -429,6 +429,9 @@ cudaError_t gemm_launch(const GemmParams &p, cudaStream_t s, int force_cfg) {
         }
         // NN: same tiles with the A operand transposed in shared memory (+1..3%, tools/gemm_tune.py)
         if (!p.transA && !p.transB && cfg == 6) cfg = 10;
+        // far below one wave of the large tiles: the per-thread K chain (TM x TN FFMA per k)
+        // is the latency, so take the small-tile configuration
+        if (p.M * p.N * nb <= (int64_t)sms * 16 * 32 * 4) cfg = 19;
     }
     switch (cfg) {
         case 0: return launch_cfg<128, 128, 16, 8, 8, 3, 2, 4>(p, s);
@@ -450,6 +453,9 @@ cudaError_t gemm_launch(const GemmParams &p, cudaStream_t s, int force_cfg) {
         case 16: return launch_cfg<64, 128, 16, 8, 8, 5, 3, 4, true>(p, s);
         case 17: return launch_cfg<64, 128, 32, 8, 8, 3, 2, 4, true>(p, s);
         case 18: return launch_cfg<64, 128, 32, 8, 8, 2, 3, 4, true>(p, s);
+        // 16 x 32 tiles, one warp, 4 x 4 per thread: latency configuration for problems
+        // far below one wave (config 1's MLP, 128^3): 8 FFMA2 per k per thread instead of 32
+        case 19: return launch_cfg<16, 32, 16, 4, 4, 3, 16, 4, true>(p, s);
         default: return cudaErrorInvalidValue;
     }
 }

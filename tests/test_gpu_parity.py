@@ -51,7 +51,7 @@ def test_gemm_parity(M, N, K, tA, tB):
     Ain = np.ascontiguousarray(A.T) if tA else A
     Bin = np.ascontiguousarray(B.T) if tB else B
     ref = oracle.gemm(Ain, Bin, transA=bool(tA), transB=bool(tB))
-    for cfg in (None, 0, 1):
+    for cfg in (None, 0, 1, 19):
         got = R.repops_gemm(dev(Ain), dev(Bin), transA=bool(tA), transB=bool(tB), cfg=cfg)
         assert_bits(host(got), ref, f"gemm {M}x{N}x{K} tA{tA} tB{tB} cfg{cfg}")
 
@@ -66,7 +66,7 @@ def test_gemm_full_tiles_ragged_k_every_cfg(K, tA, tB):
     Ain = np.ascontiguousarray(A.T) if tA else A
     Bin = np.ascontiguousarray(B.T) if tB else B
     ref = oracle.gemm(Ain, Bin, transA=bool(tA), transB=bool(tB))
-    for cfg in range(10):
+    for cfg in list(range(10)) + [19]:
         got = R.repops_gemm(dev(Ain), dev(Bin), transA=bool(tA), transB=bool(tB), cfg=cfg)
         assert_bits(host(got), ref, f"gemm {M}x{N}x{K} tA{tA} tB{tB} cfg{cfg}")
 
