@@ -346,9 +346,20 @@ def mlp_extra(with_oracle=True, reps=200):
     root = st.root().hex()
     A, B = (torch.from_numpy(t).cuda() for t in synth.gemm_inputs(128, "bench"))
     C = torch.empty(128, 128, device="cuda")
-    g128 = us(lambda: R.repops_gemm(A, B, out=C), reps)
+    g128 = us(lambda: R.repops_gemm(A, B, out=C), reps)   # per Python-level call (host-bound)
+    # device time per launch: 50 back-to-back launches captured in one CUDA graph
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(side):
+        R.repops_gemm(A, B, out=C)
+        with torch.cuda.graph(g, stream=side):
+            for _ in range(50):
+                R.repops_gemm(A, B, out=C)
+    torch.cuda.synchronize()
+    g128_dev = us(g.replay, 20) / 50
     res = {"us_per_step_graph": graph, "us_per_step_eager": eager, "gpu_launches": launches,
-           "gemm128_us": g128, "root": root,
+           "gemm128_us": g128, "gemm128_device_us": g128_dev, "root": root,
            "config": "Linear-ReLU-Linear-CE, width 256, batch 32 = 8 shards x 4 rows, AdamW, every output "
                      "committed (BASELINE configs[0])"}
     if with_oracle:
