@@ -159,3 +159,17 @@ def test_p2p_slices_partition_and_align():
             for (lo, hi), (lo2, _) in zip(sl, sl[1:]):
                 assert hi == lo2 and lo <= hi
             assert all(lo % 4 == 0 or lo == n for lo, _ in sl)
+
+
+def test_combine_transport_validation():
+    """host-side validation of the gradient-combine transports (no GPU needed)"""
+    with pytest.raises(ValueError):
+        GPT2Step(GPT2Config.tiny(), structure_only=True, combine="allreduce")  # NCCL reductions are never used
+    with pytest.raises(ValueError):
+        D.P2PTreeCombine(1000, 0, 3)   # world must be a power of two <= 8 (aligned R-TREE_S subtrees)
+    with pytest.raises(ValueError):
+        D.P2PTreeCombine(1000, 0, 16)
+    # the structure (node graph, slots) does not depend on the transport
+    a = GPT2Step(GPT2Config.tiny(), structure_only=True, combine="sliced")
+    b = GPT2Step(GPT2Config.tiny(), structure_only=True, combine="p2p")
+    assert np.array_equal(a.node_blob, b.node_blob) and np.array_equal(a.node_slots, b.node_slots)
