@@ -49,3 +49,8 @@ dl = torch.empty_like(logits)
 lo = torch.empty(4096, device="cuda")
 ms = t(lambda: R.repops_cross_entropy(logits, labels, scale=2.0 ** -12, loss=lo, dlogits=dl, V=50257), n=5)
 print(f"cross_entropy 4096x50257: {ms * 1e3:7.1f} us  {2 * 4096 * 50257 * 4 / ms / 1e6:7.1f} GB/s (algorithmic)")
+for rows, cols in ((4096, 768), (4096, 3072), (4096, 2304)):
+    X = torch.rand(rows, cols, device="cuda")
+    Y = torch.empty(cols, rows, device="cuda")
+    ms = t(lambda: R.repops_transpose(X, out=Y))
+    print(f"transpose {rows}x{cols}: {ms * 1e3:7.1f} us  {2 * X.numel() * 4 / ms / 1e6:7.1f} GB/s")
