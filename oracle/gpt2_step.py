@@ -35,15 +35,92 @@ def _c(a):
     return np.ascontiguousarray(a, dtype=np.float32)
 
 
+def layer_forward(W, l, x, cfg):
+    """Forward of transformer block l for one shard: x [T, d] -> dict of every
+    tensor the block commits (names without the "s{s}/h{l}/" prefix) plus "x_next"."""
+    d, H, T = cfg.d, cfg.n_head, cfg.seq
+    hd = d // H
+    scale = float(np.float32(1.0 / np.sqrt(hd)))
+    p = f"h{l}."
+    ln1, mu1, rs1 = layernorm(x, W[p + "ln1.g"], W[p + "ln1.b"], cfg.ln_eps)
+    qkv = gemm(ln1, W[p + "attn.w"], epi=1, bias=W[p + "attn.b"])
+    Sc = np.empty((H * T, T), np.float32)
+    Pr = np.empty((H * T, T), np.float32)
+    att = np.empty((T, d), np.float32)
+    for h in range(H):
+        Q = _c(qkv[:, h * hd:(h + 1) * hd])
+        K = _c(qkv[:, d + h * hd:d + (h + 1) * hd])
+        Vh = _c(qkv[:, 2 * d + h * hd:2 * d + (h + 1) * hd])
+        Sc[h * T:(h + 1) * T] = gemm(Q, K, transB=True, epi=2, scale=scale)
+        Pr[h * T:(h + 1) * T] = softmax(Sc[h * T:(h + 1) * T], causal=True)
+        att[:, h * hd:(h + 1) * hd] = gemm(_c(Pr[h * T:(h + 1) * T]), Vh)
+    proj = gemm(att, W[p + "proj.w"], epi=1, bias=W[p + "proj.b"])
+    xmid = add(x, proj)
+    ln2, mu2, rs2 = layernorm(xmid, W[p + "ln2.g"], W[p + "ln2.b"], cfg.ln_eps)
+    fc = gemm(ln2, W[p + "fc.w"], epi=1, bias=W[p + "fc.b"])
+    g = gelu(fc)
+    fc2 = gemm(g, W[p + "fc2.w"], epi=1, bias=W[p + "fc2.b"])
+    xn = add(xmid, fc2)
+    return {"ln1": ln1, "mu1": mu1, "rs1": rs1, "qkv": qkv, "scores": Sc, "probs": Pr, "att": att, "proj": proj,
+            "xmid": xmid, "ln2": ln2, "mu2": mu2, "rs2": rs2, "fc": fc, "gelu": g, "fc2": fc2, "x_next": xn}
+
+
+def layer_backward(W, l, x, a, dout, cfg):
+    """Backward of block l for one shard from its input x, its saved forward tensors a
+    (layer_forward's dict) and the output gradient dout [T, d].  Returns (tensors,
+    grads): tensors by their committed names (without prefix) plus "dx" (gradient
+    w.r.t. x), grads = this shard's parameter gradients of the block."""
+    d, H, T = cfg.d, cfg.n_head, cfg.seq
+    hd = d // H
+    scale = float(np.float32(1.0 / np.sqrt(hd)))
+    p = f"h{l}."
+    gr = {}
+    dgelu = gemm(dout, W[p + "fc2.w"], transB=True)
+    gr[p + "fc2.w"] = gemm(a["gelu"], dout, transA=True)
+    gr[p + "fc2.b"] = sum_cols_seq(dout)[0]
+    dfc = gelu_backward(a["fc"], dgelu)
+    dln2 = gemm(dfc, W[p + "fc.w"], transB=True)
+    gr[p + "fc.w"] = gemm(a["ln2"], dfc, transA=True)
+    gr[p + "fc.b"] = sum_cols_seq(dfc)[0]
+    dxmid = layernorm_backward(dln2, a["xmid"], W[p + "ln2.g"], a["mu2"], a["rs2"], dres=dout)
+    dg, db = layernorm_backward_params(dln2, a["xmid"], a["mu2"], a["rs2"])
+    gr[p + "ln2.g"], gr[p + "ln2.b"] = dg[0], db[0]
+    datt = gemm(dxmid, W[p + "proj.w"], transB=True)
+    gr[p + "proj.w"] = gemm(a["att"], dxmid, transA=True)
+    gr[p + "proj.b"] = sum_cols_seq(dxmid)[0]
+    dP = np.empty((H * T, T), np.float32)
+    dS = np.empty((H * T, T), np.float32)
+    dqkv = np.empty((T, 3 * d), np.float32)
+    for h in range(H):
+        dO = _c(datt[:, h * hd:(h + 1) * hd])
+        Q = _c(a["qkv"][:, h * hd:(h + 1) * hd])
+        K = _c(a["qkv"][:, d + h * hd:d + (h + 1) * hd])
+        Vh = _c(a["qkv"][:, 2 * d + h * hd:2 * d + (h + 1) * hd])
+        Ph = _c(a["probs"][h * T:(h + 1) * T])
+        dP[h * T:(h + 1) * T] = gemm(dO, Vh, transB=True)
+        dS[h * T:(h + 1) * T] = softmax_backward(Ph, dP[h * T:(h + 1) * T], scale=scale)
+        dSh = _c(dS[h * T:(h + 1) * T])
+        dqkv[:, 2 * d + h * hd:2 * d + (h + 1) * hd] = gemm(Ph, dO, transA=True)
+        dqkv[:, h * hd:(h + 1) * hd] = gemm(dSh, K)
+        dqkv[:, d + h * hd:d + (h + 1) * hd] = gemm(dSh, Q, transA=True)
+    dln1 = gemm(dqkv, W[p + "attn.w"], transB=True)
+    gr[p + "attn.w"] = gemm(a["ln1"], dqkv, transA=True)
+    gr[p + "attn.b"] = sum_cols_seq(dqkv)[0]
+    dxn = layernorm_backward(dln1, x, W[p + "ln1.g"], a["mu1"], a["rs1"], dres=dxmid)
+    dg, db = layernorm_backward_params(dln1, x, a["mu1"], a["rs1"])
+    gr[p + "ln1.g"], gr[p + "ln1.b"] = dg[0], db[0]
+    t = {"dgelu": dgelu, "dfc": dfc, "dln2": dln2, "dxmid": dxmid, "datt": datt, "dP": dP, "dS": dS, "dqkv": dqkv,
+         "dln1": dln1, "dx": dxn}
+    return t, gr
+
+
 def run_step(cfg, tokens=None, step=1):
     """cfg: object with n_layer, d, n_head, ffn, vocab, n_pos, seq, shards, ln_eps, lr,
     beta1, beta2, adam_eps, wd, seed, vocab_ld.  Returns (tensors: dict name -> array,
     params: dict, new_params/m/v dicts)."""
-    L, d, H, F, V, T, S = cfg.n_layer, cfg.d, cfg.n_head, cfg.ffn, cfg.vocab, cfg.seq, cfg.shards
-    hd = d // H
-    scale = float(np.float32(1.0 / np.sqrt(hd)))
+    L, d, V, T, S = cfg.n_layer, cfg.d, cfg.vocab, cfg.seq, cfg.shards
     ce_scale = 1.0 / (S * T)
-    specs = synth.gpt2_param_specs(L, d, F, V, cfg.n_pos)
+    specs = synth.gpt2_param_specs(L, d, cfg.ffn, V, cfg.n_pos)
     W = {name: synth.gpt2_param(name, shape, kind, cfg.seed) for name, shape, kind in specs}
     out = {}
     grads = {name: [None] * S for name, _, _ in specs}
@@ -56,33 +133,12 @@ def run_step(cfg, tokens=None, step=1):
         out[pre + "x0"] = x
         saved = []
         for l in range(L):
-            p, q = f"h{l}.", f"s{s}/h{l}/"
-            ln1, mu1, rs1 = layernorm(x, W[p + "ln1.g"], W[p + "ln1.b"], cfg.ln_eps)
-            qkv = gemm(ln1, W[p + "attn.w"], epi=1, bias=W[p + "attn.b"])
-            Sc = np.empty((H * T, T), np.float32)
-            Pr = np.empty((H * T, T), np.float32)
-            att = np.empty((T, d), np.float32)
-            for h in range(H):
-                Q = _c(qkv[:, h * hd:(h + 1) * hd])
-                K = _c(qkv[:, d + h * hd:d + (h + 1) * hd])
-                Vh = _c(qkv[:, 2 * d + h * hd:2 * d + (h + 1) * hd])
-                Sc[h * T:(h + 1) * T] = gemm(Q, K, transB=True, epi=2, scale=scale)
-                Pr[h * T:(h + 1) * T] = softmax(Sc[h * T:(h + 1) * T], causal=True)
-                att[:, h * hd:(h + 1) * hd] = gemm(_c(Pr[h * T:(h + 1) * T]), Vh)
-            proj = gemm(att, W[p + "proj.w"], epi=1, bias=W[p + "proj.b"])
-            xmid = add(x, proj)
-            ln2, mu2, rs2 = layernorm(xmid, W[p + "ln2.g"], W[p + "ln2.b"], cfg.ln_eps)
-            fc = gemm(ln2, W[p + "fc.w"], epi=1, bias=W[p + "fc.b"])
-            g = gelu(fc)
-            fc2 = gemm(g, W[p + "fc2.w"], epi=1, bias=W[p + "fc2.b"])
-            xn = add(xmid, fc2)
-            out.update({q + "ln1": ln1, q + "mu1": mu1, q + "rs1": rs1, q + "qkv": qkv, q + "scores": Sc,
-                        q + "probs": Pr, q + "att": att, q + "proj": proj, q + "xmid": xmid, q + "ln2": ln2,
-                        q + "mu2": mu2, q + "rs2": rs2, q + "fc": fc, q + "gelu": g, q + "fc2": fc2,
-                        f"s{s}/x{l + 1}": xn})
-            saved.append(dict(x=x, ln1=ln1, mu1=mu1, rs1=rs1, qkv=qkv, P=Pr, att=att, xmid=xmid, ln2=ln2, mu2=mu2,
-                              rs2=rs2, fc=fc, gelu=g))
-            x = xn
+            q = f"s{s}/h{l}/"
+            a = layer_forward(W, l, x, cfg)
+            out.update({q + k: v for k, v in a.items() if k != "x_next"})
+            out[f"s{s}/x{l + 1}"] = a["x_next"]
+            saved.append((x, a))
+            x = a["x_next"]
         q = f"s{s}/head/"
         lnf, muf, rsf = layernorm(x, W["lnf.g"], W["lnf.b"], cfg.ln_eps)
         logits = gemm(lnf, W["wte"], transB=True)
@@ -99,46 +155,14 @@ def run_step(cfg, tokens=None, step=1):
         grads["lnf.g"][s], grads["lnf.b"][s] = dg[0], db[0]
         # ---- backward: layers
         for l in reversed(range(L)):
-            p, q = f"h{l}.", f"s{s}/h{l}/"
-            a = saved[l]
-            dout = dx
-            dgelu = gemm(dout, W[p + "fc2.w"], transB=True)
-            grads[p + "fc2.w"][s] = gemm(a["gelu"], dout, transA=True)
-            grads[p + "fc2.b"][s] = sum_cols_seq(dout)[0]
-            dfc = gelu_backward(a["fc"], dgelu)
-            dln2 = gemm(dfc, W[p + "fc.w"], transB=True)
-            grads[p + "fc.w"][s] = gemm(a["ln2"], dfc, transA=True)
-            grads[p + "fc.b"][s] = sum_cols_seq(dfc)[0]
-            dxmid = layernorm_backward(dln2, a["xmid"], W[p + "ln2.g"], a["mu2"], a["rs2"], dres=dout)
-            dg, db = layernorm_backward_params(dln2, a["xmid"], a["mu2"], a["rs2"])
-            grads[p + "ln2.g"][s], grads[p + "ln2.b"][s] = dg[0], db[0]
-            datt = gemm(dxmid, W[p + "proj.w"], transB=True)
-            grads[p + "proj.w"][s] = gemm(a["att"], dxmid, transA=True)
-            grads[p + "proj.b"][s] = sum_cols_seq(dxmid)[0]
-            dP = np.empty((H * T, T), np.float32)
-            dS = np.empty((H * T, T), np.float32)
-            dqkv = np.empty((T, 3 * d), np.float32)
-            for h in range(H):
-                dO = _c(datt[:, h * hd:(h + 1) * hd])
-                Q = _c(a["qkv"][:, h * hd:(h + 1) * hd])
-                K = _c(a["qkv"][:, d + h * hd:d + (h + 1) * hd])
-                Vh = _c(a["qkv"][:, 2 * d + h * hd:2 * d + (h + 1) * hd])
-                Ph = _c(a["P"][h * T:(h + 1) * T])
-                dP[h * T:(h + 1) * T] = gemm(dO, Vh, transB=True)
-                dS[h * T:(h + 1) * T] = softmax_backward(Ph, dP[h * T:(h + 1) * T], scale=scale)
-                dSh = _c(dS[h * T:(h + 1) * T])
-                dqkv[:, 2 * d + h * hd:2 * d + (h + 1) * hd] = gemm(Ph, dO, transA=True)
-                dqkv[:, h * hd:(h + 1) * hd] = gemm(dSh, K)
-                dqkv[:, d + h * hd:d + (h + 1) * hd] = gemm(dSh, Q, transA=True)
-            dln1 = gemm(dqkv, W[p + "attn.w"], transB=True)
-            grads[p + "attn.w"][s] = gemm(a["ln1"], dqkv, transA=True)
-            grads[p + "attn.b"][s] = sum_cols_seq(dqkv)[0]
-            dxn = layernorm_backward(dln1, a["x"], W[p + "ln1.g"], a["mu1"], a["rs1"], dres=dxmid)
-            dg, db = layernorm_backward_params(dln1, a["x"], a["mu1"], a["rs1"])
-            grads[p + "ln1.g"][s], grads[p + "ln1.b"][s] = dg[0], db[0]
-            out.update({q + "dgelu": dgelu, q + "dfc": dfc, q + "dln2": dln2, q + "dxmid": dxmid, q + "datt": datt,
-                        q + "dP": dP, q + "dS": dS, q + "dqkv": dqkv, q + "dln1": dln1, f"s{s}/dx{l}": dxn})
-            dx = dxn
+            q = f"s{s}/h{l}/"
+            xl, a = saved[l]
+            t, gr = layer_backward(W, l, xl, a, dx, cfg)
+            for name, g in gr.items():
+                grads[name][s] = g
+            out.update({q + k: v for k, v in t.items() if k != "dx"})
+            out[f"s{s}/dx{l}"] = t["dx"]
+            dx = t["dx"]
         gwte, gwpe = embedding_backward(tin, dx, T, gwte_lm, np.zeros((cfg.n_pos, d), np.float32))
         grads["wte"][s], grads["wpe"][s] = gwte, gwpe
         for name, _, _ in specs:

@@ -119,8 +119,21 @@ def repops_gemm(A, B, transA=False, transB=False, epi=EPI_NONE, bias=None, scale
     Kb = B.shape[1] if transB else B.shape[0]
     if Kb != K:
         raise RepopsError(f"repops_gemm: inner dimensions differ ({K} vs {Kb})")
+    if B.device != A.device:
+        raise RepopsError(f"repops_gemm: A on {A.device}, B on {B.device}")
     if out is None:
         out = torch.empty((M, N), dtype=torch.float32, device=A.device)
+    else:
+        _f32(out, "out")
+        if tuple(out.shape) != (M, N) or out.device != A.device:
+            raise RepopsError(f"repops_gemm: out must be ({M}, {N}) on {A.device}, got {tuple(out.shape)} "
+                              f"on {out.device}")
+    if epi == EPI_BIAS:
+        if bias is None:
+            raise RepopsError("repops_gemm: EPI_BIAS needs a bias")
+        _f32(bias, "bias")
+        if bias.device != A.device or bias.numel() < N or (bias.dim() == 1 and bias.stride(0) != 1):
+            raise RepopsError(f"repops_gemm: bias must hold >= {N} contiguous floats on {A.device}")
     args = (M, N, K, _p(A), _ld(A), int(bool(transA)), _p(B), _ld(B), int(bool(transB)), int(epi), _p(bias),
             float(scale), _p(out), _ld(out), _stream(stream))
     t0 = _TIMER.begin(stream) if _TIMER else None
@@ -745,6 +758,11 @@ def verde_digest_from_subroots(subroots: bytes, dtype: int, shape, nbytes: int) 
     check(lib().verde_digest_from_subroots(buf, k, int(dtype), len(shape), dims, int(nbytes), out),
           "verde_digest_from_subroots")
     return out.raw
+
+
+def gemm_num_cfgs() -> int:
+    """Number of R-GEMM tile configurations (test hook: every one gives the same bits)."""
+    return lib().repops_gemm_num_cfgs()
 
 
 def launch_count() -> int:

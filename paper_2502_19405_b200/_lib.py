@@ -158,6 +158,8 @@ def check(status: int, what: str) -> None:
 # tuning / test hooks exported by the library but not part of include/repops.h
 def _hooks(L):
     L.repops_gemm_force_cfg.restype = i32
+    L.repops_gemm_num_cfgs.restype = i32
+    L.repops_gemm_num_cfgs.argtypes = []
     L.repops_gemm_force_cfg.argtypes = [i32]
     L.repops_gemm_smem_floor.restype = i32
     L.repops_gemm_smem_floor.argtypes = [i32]

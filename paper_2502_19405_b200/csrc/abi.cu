@@ -348,6 +348,9 @@ int repops_commit_ctas_per_sm(int n) {
     return REPOPS_OK;
 }
 
+// Test hook (not in repops.h): number of tile configurations repops_gemm_cfg accepts.
+int repops_gemm_num_cfgs() { return gemm_num_cfgs(); }
+
 // Test hook (not in repops.h): force a tile configuration to prove bits-neutrality.
 int repops_gemm_cfg(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, int transA, const float *B,
                     int64_t ldb, int transB, int epi, const float *bias, float scale, float *C, int64_t ldc,

@@ -89,3 +89,35 @@ def test_first_divergence(n, d):
     assert rounds <= 2 + (n - 1).bit_length()
     same, _ = R.verde_first_divergence(b"".join(a), b"".join(a))
     assert same == -1
+
+
+@pytest.mark.parametrize("n,k", [(1024, 1), (1024, 2), (1024, 4), (1024, 8), (2048, 8), (64, 2)])
+def test_digest_from_subroots_equals_oracle_whole_tensor_commit(n, k):
+    """Config-2 M-split: rank r commits only the data root of
+    its (n/k) x n slab; verde_digest_from_subroots joins the k slab roots into the digest
+    of the whole n x n output.  It must equal the oracle's R-TCOMMIT of the full tensor
+    (the slabs are aligned power-of-two chunk groups, so the RFC 6962 tree splits there)."""
+    import numpy as np
+
+    import oracle
+    import synth
+    C_ = synth.uniform(synth.seed_for("msplit", n, k), (n, n))
+    rows = n // k
+    sub = b"".join(oracle.data_root(C_[r * rows:(r + 1) * rows]) for r in range(k))
+    got = R.verde_digest_from_subroots(sub, R.F32, (n, n), n * n * 4)
+    assert got == oracle.commit_tensor(C_)
+    # a slab root out of order, or a flipped bit in one slab, changes the digest
+    if k > 1:
+        swapped = sub[32:64] + sub[:32] + sub[64:]
+        assert R.verde_digest_from_subroots(swapped, R.F32, (n, n), n * n * 4) != got
+    D = C_.copy()
+    D.reshape(-1).view(np.uint32)[n * n - 1] ^= 1
+    sub2 = b"".join(oracle.data_root(D[r * rows:(r + 1) * rows]) for r in range(k))
+    assert R.verde_digest_from_subroots(sub2, R.F32, (n, n), n * n * 4) != got
+
+
+def test_digest_from_subroots_rejects_unaligned_slabs():
+    with pytest.raises(RuntimeError):
+        R.verde_digest_from_subroots(b"\0" * 96, R.F32, (96, 1024), 96 * 1024 * 4)   # k = 3
+    with pytest.raises(RuntimeError):
+        R.verde_digest_from_subroots(b"\0" * 64, R.F32, (3, 1024), 3 * 1024 * 4)     # 1.5 chunks per slab

@@ -1,0 +1,206 @@
+"""Full-size GPT-2 124M training step (BASELINE configs[2], 8 x 512 tokens) checked
+against the CPU ORACLE by per-node referee recomputes -- Verde's Case 3 (PAPER.md
+P:516-524: the referee re-executes the disputed node from its agreed inputs and
+compares the outputs), with the oracle as the referee (SURVEY.md §8(c) "Whole
+steps: per-node referee recompute ... from the GPU's committed inputs").
+
+One GPT2Config() step runs through the product path (aux-stream weight gradients,
+side-stream commits, scratch transposes, every GEMM tile configuration the cost
+model picks at full size, the shared-memory cross entropy at ld 50,304, multi-pass
+commit reduces).  Then, from the tensors the GPU committed (inputs re-verified
+against their digests), the oracle recomputes bit for bit:
+  * every node of one transformer block, forward and backward, of one shard
+    (LN, QKV, scores, softmax, PV, proj, residuals, LN2, FC, GELU, FC2 and their
+    dgrads / wgrads / bias folds / LN-parameter folds / softmax backward / dQKV);
+  * every other node type at least once: embedding forward, final LN forward and
+    backward (+ its parameter folds), LM-head rows, cross-entropy rows, LM dgrad
+    rows, LM wgrad vocabulary rows, the embedding backward, R-TREE_S and AdamW on
+    whole parameter tensors;
+and the digests the GPU committed for those outputs equal the oracle's R-TCOMMIT
+of its own recomputed tensors.  0 ULP everywhere (raw uint32 comparison)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from oracle import gpt2_step as ostep
+
+pytestmark = pytest.mark.gpu
+
+SHARD = 3   # the shard whose block is recomputed in full
+LAYER = 5   # the block recomputed in full (forward + backward)
+
+
+@pytest.fixture(scope="module")
+def full():
+    from paper_2502_19405_b200.gpt2 import GPT2Config, GPT2Step
+    torch.cuda.set_device(0)
+    cfg = GPT2Config()
+    st = GPT2Step(cfg)
+    st.keep_committed = True  # serve the tied LM-head gradient as committed (before EMBED_BWD)
+    st.set_tokens(0)
+    st.run()
+    torch.cuda.synchronize()
+    table = st.gather_digests().copy()
+    by_name = {t.name: (i, t) for i, t in enumerate(st.tensors)}
+
+    def get(name):
+        tid, t = by_name[name]
+        v = st.stash.get(tid, t.view)
+        return v.detach().cpu().numpy().copy()
+
+    def digest(name):
+        return table[by_name[name][1].slot].tobytes()
+
+    specs = synth.gpt2_param_specs(cfg.n_layer, cfg.d, cfg.ffn, cfg.vocab, cfg.n_pos)
+    W = {name: synth.gpt2_param(name, shape, kind, cfg.seed) for name, shape, kind in specs}
+    return cfg, st, get, digest, W, specs
+
+
+def same_bits(got, ref, what):
+    g = np.ascontiguousarray(got, dtype=np.float32).view(np.uint32).ravel()
+    r = np.ascontiguousarray(ref, dtype=np.float32).view(np.uint32).ravel()
+    assert g.size == r.size, (what, g.size, r.size)
+    bad = np.flatnonzero(g != r)
+    assert bad.size == 0, f"{what}: {bad.size}/{g.size} elements differ from the oracle, first {bad[:5]}"
+
+
+def check_inputs(digest, W, names):
+    """the parameters the referee uses are the ones the GPU committed (PARAM_IN digests)"""
+    for n in names:
+        assert digest(f"param/{n}") == oracle.commit_tensor(W[n]), f"committed param/{n} differs from the recipe"
+
+
+def block_param_names(l):
+    p = f"h{l}."
+    return [p + n for n in ("ln1.g", "ln1.b", "attn.w", "attn.b", "proj.w", "proj.b", "ln2.g", "ln2.b", "fc.w",
+                            "fc.b", "fc2.w", "fc2.b")]
+
+
+def test_block_forward_every_node(full):
+    cfg, st, get, digest, W, _ = full
+    s, l = SHARD, LAYER
+    check_inputs(digest, W, block_param_names(l))
+    x = get(f"s{s}/x{l}")
+    assert digest(f"s{s}/x{l}") == oracle.commit_tensor(x)  # the agreed input
+    ref = ostep.layer_forward(W, l, x, cfg)
+    for k, v in ref.items():
+        name = f"s{s}/x{l + 1}" if k == "x_next" else f"s{s}/h{l}/{k}"
+        got = get(name)
+        same_bits(got, v, name)
+        assert digest(name) == oracle.commit_tensor(np.ascontiguousarray(v).reshape(got.shape)), f"digest {name}"
+
+
+def test_block_backward_every_node(full):
+    cfg, st, get, digest, W, _ = full
+    s, l = SHARD, LAYER
+    pre = f"s{s}/h{l}/"
+    x = get(f"s{s}/x{l}")
+    saved = {k: get(pre + k) for k in ("ln1", "mu1", "rs1", "qkv", "probs", "att", "xmid", "ln2", "mu2", "rs2",
+                                       "fc", "gelu")}
+    dout = get(f"s{s}/dx{l + 1}")
+    t, gr = ostep.layer_backward(W, l, x, saved, dout, cfg)
+    for k, v in t.items():
+        name = f"s{s}/dx{l}" if k == "dx" else pre + k
+        got = get(name)
+        same_bits(got, v, name)
+        assert digest(name) == oracle.commit_tensor(np.ascontiguousarray(v).reshape(got.shape)), f"digest {name}"
+    for pname, v in gr.items():
+        name = f"s{s}/grad/{pname}"
+        got = get(name)
+        same_bits(got, v, name)
+        assert digest(name) == oracle.commit_tensor(np.ascontiguousarray(v).reshape(got.shape)), f"digest {name}"
+
+
+def test_embedding_and_final_layernorm(full):
+    cfg, st, get, digest, W, _ = full
+    s, L, T = SHARD, cfg.n_layer, cfg.seq
+    check_inputs(digest, W, ["wte", "wpe", "lnf.g", "lnf.b"])
+    tok = get(f"s{s}/tokens")
+    assert np.array_equal(tok, synth.gpt2_tokens(cfg.vocab, T, s, 0, cfg.seed).astype(np.int32))
+    x0 = oracle.embedding(tok[:T], W["wte"], W["wpe"], T)
+    same_bits(get(f"s{s}/x0"), x0, "x0")
+    xL = get(f"s{s}/x{L}")
+    lnf, muf, rsf = oracle.layernorm(xL, W["lnf.g"], W["lnf.b"], cfg.ln_eps)
+    for k, v in (("lnf", lnf), ("muf", muf), ("rsf", rsf)):
+        same_bits(get(f"s{s}/head/{k}"), v, k)
+    dlnf = get(f"s{s}/head/dlnf")
+    dx = oracle.layernorm_backward(dlnf, xL, W["lnf.g"], muf, rsf)
+    same_bits(get(f"s{s}/dx{L}"), dx, f"dx{L}")
+    dg, db = oracle.layernorm_backward_params(dlnf, xL, muf, rsf)
+    same_bits(get(f"s{s}/grad/lnf.g"), dg[0], "grad lnf.g")
+    same_bits(get(f"s{s}/grad/lnf.b"), db[0], "grad lnf.b")
+
+
+def _rows(T, seed):
+    rng = np.random.default_rng(seed)
+    return sorted({0, 1, T - 1, *rng.integers(0, T, 6).tolist()})
+
+
+def test_lm_head_cross_entropy_and_dgrad_rows(full):
+    cfg, st, get, digest, W, _ = full
+    s, V, T = SHARD, cfg.vocab, cfg.seq
+    rows = _rows(T, 11)
+    lnf = get(f"s{s}/head/lnf")
+    logits = get(f"s{s}/head/logits")
+    assert logits.shape == (T, cfg.vocab_ld)
+    assert np.all(logits[:, V:].view(np.uint32) == 0), "padding columns of the logits must be +0"
+    ref = oracle.gemm(lnf[rows], W["wte"], transB=True)
+    same_bits(logits[rows, :V], ref, "logits rows")
+    tgt = get(f"s{s}/tokens")[1:]
+    loss, dlog = oracle.cross_entropy(np.ascontiguousarray(logits[rows, :V]), tgt[rows],
+                                      scale=1.0 / (cfg.shards * cfg.seq))
+    same_bits(get(f"s{s}/head/loss")[rows], loss, "CE loss rows")
+    dlogits = get(f"s{s}/head/dlogits")
+    same_bits(dlogits[rows, :V], dlog, "CE dlogits rows")
+    assert np.all(dlogits[:, V:].view(np.uint32) == 0)
+    dlnf = oracle.gemm(np.ascontiguousarray(dlogits[rows, :V]), W["wte"])
+    same_bits(get(f"s{s}/head/dlnf")[rows], dlnf, "LM dgrad rows")
+
+
+def test_lm_wgrad_rows_and_embedding_backward(full):
+    cfg, st, get, digest, W, _ = full
+    s, V, T = SHARD, cfg.vocab, cfg.seq
+    lnf = get(f"s{s}/head/lnf")
+    dlogits = get(f"s{s}/head/dlogits")
+    gwte_lm = get(f"s{s}/grad/wte_lm")  # as committed (stashed before EMBED_BWD accumulated into it)
+    assert digest(f"s{s}/grad/wte_lm") == oracle.commit_tensor(gwte_lm)
+    vs = sorted({0, 1, V - 1, *np.random.default_rng(5).integers(0, V, 13).tolist()})
+    ref = oracle.gemm(np.ascontiguousarray(dlogits[:, vs]), lnf, transA=True)  # rows v of dlogits^T lnf
+    same_bits(gwte_lm[vs], ref, "LM wgrad vocabulary rows")
+    tok = get(f"s{s}/tokens")
+    dx0 = get(f"s{s}/dx0")
+    dwte, dwpe = oracle.embedding_backward(tok[:T], dx0, T, gwte_lm, np.zeros((cfg.n_pos, cfg.d), np.float32))
+    same_bits(get(f"s{s}/grad/wte"), dwte, "EMBED_BWD wte")
+    same_bits(get(f"s{s}/grad/wpe"), dwpe, "EMBED_BWD wpe")
+
+
+@pytest.mark.parametrize("pname", ["h5.attn.w", "h11.fc2.b", "lnf.g", "wpe"])
+def test_tree_and_adamw_whole_tensors(full, pname):
+    cfg, st, get, digest, W, specs = full
+    shape = dict((n, sh) for n, sh, _ in specs)[pname]
+    parts = [get(f"s{q}/grad/{pname}") for q in range(cfg.shards)]
+    g = oracle.tree_sum(parts)
+    same_bits(get(f"grad/{pname}"), g, f"R-TREE_S {pname}")
+    assert digest(f"grad/{pname}") == oracle.commit_tensor(g.reshape(shape))
+    p, m, v = oracle.adamw(W[pname], g, np.zeros(shape, np.float32), np.zeros(shape, np.float32), 1, cfg.lr,
+                           cfg.beta1, cfg.beta2, cfg.adam_eps, cfg.wd, len(shape) == 2)
+    same_bits(get(f"param'/{pname}"), p, f"AdamW p' {pname}")
+    same_bits(get(f"m'/{pname}"), m, f"AdamW m' {pname}")
+    same_bits(get(f"v'/{pname}"), v, f"AdamW v' {pname}")
+    assert digest(f"param'/{pname}") == oracle.commit_tensor(p.reshape(shape))
+
+
+def test_wte_tree_and_adamw_slice(full):
+    """the tied embedding (largest tensor, 38.6 M elements): R-TREE_S and AdamW on a
+    slice of rows (both are elementwise, so a slice is a complete recompute of it)"""
+    cfg, st, get, digest, W, _ = full
+    r0, r1 = 1000, 1300
+    parts = [get(f"s{q}/grad/wte")[r0:r1] for q in range(cfg.shards)]
+    g = oracle.tree_sum(parts)
+    same_bits(get("grad/wte")[r0:r1], g, "R-TREE_S wte rows")
+    z = np.zeros_like(g)
+    p, m, v = oracle.adamw(W["wte"][r0:r1], g, z, z, 1, cfg.lr, cfg.beta1, cfg.beta2, cfg.adam_eps, cfg.wd, True)
+    same_bits(get("param'/wte")[r0:r1], p, "AdamW wte rows")
+    same_bits(get("v'/wte")[r0:r1], v, "AdamW v' wte rows")

@@ -66,9 +66,85 @@ def test_gemm_full_tiles_ragged_k_every_cfg(K, tA, tB):
     Ain = np.ascontiguousarray(A.T) if tA else A
     Bin = np.ascontiguousarray(B.T) if tB else B
     ref = oracle.gemm(Ain, Bin, transA=bool(tA), transB=bool(tB))
-    for cfg in list(range(10)) + [19]:
+    assert R.gemm_num_cfgs() == 20
+    for cfg in range(R.gemm_num_cfgs()):  # every tile configuration, XP and BK = 32 variants included
         got = R.repops_gemm(dev(Ain), dev(Bin), transA=bool(tA), transB=bool(tB), cfg=cfg)
         assert_bits(host(got), ref, f"gemm {M}x{N}x{K} tA{tA} tB{tB} cfg{cfg}")
+
+
+@pytest.mark.parametrize("tA,tB", [(0, 0), (0, 1), (1, 0), (1, 1)])
+def test_gemm_ragged_every_cfg(tA, tB):
+    # ragged M / N / K tails on every configuration (the bounded-load paths)
+    M, N, K = 197, 301, 77
+    A, B = synth.gemm_inputs((M, N, K), "gr")
+    Ain = np.ascontiguousarray(A.T) if tA else A
+    Bin = np.ascontiguousarray(B.T) if tB else B
+    ref = oracle.gemm(Ain, Bin, transA=bool(tA), transB=bool(tB))
+    for cfg in range(R.gemm_num_cfgs()):
+        got = R.repops_gemm(dev(Ain), dev(Bin), transA=bool(tA), transB=bool(tB), cfg=cfg)
+        assert_bits(host(got), ref, f"gemm {M}x{N}x{K} tA{tA} tB{tB} cfg{cfg}")
+
+
+def _subnormal_operands(M, N, K, tag):
+    """operands whose products and partial sums fall in the binary32 subnormal range
+    (|x| < 2^-126), so every fma in the K fold rounds with gradual underflow (R9)"""
+    A, B = synth.gemm_inputs((M, N, K), tag)
+    A = (A * np.float32(2.0 ** -66)).astype(np.float32)      # normal operands ...
+    B = (B * np.float32(2.0 ** -66)).astype(np.float32)      # ... subnormal products
+    A[::3] = (A[::3] * np.float32(2.0 ** -64)).astype(np.float32)  # subnormal operands in every third row
+    A[1, :] = np.float32(2.0 ** -149)                        # the smallest subnormal
+    B[:, 2] = -np.float32(2.0 ** -126)                       # the smallest normal
+    return A, B
+
+
+@pytest.mark.parametrize("tA,tB", [(0, 0), (0, 1), (1, 0), (1, 1)])
+def test_gemm_subnormal_operands_and_products(tA, tB):
+    M, N, K = 130, 257, 96
+    A, B = _subnormal_operands(M, N, K, "gsub")
+    assert np.count_nonzero((np.abs(A) < 2.0 ** -126) & (A != 0)) > 1000
+    ref = oracle.gemm(A, B)
+    tiny = np.abs(ref) < 2.0 ** -126
+    assert np.count_nonzero(tiny & (ref != 0)) > M * N // 4  # most results are themselves subnormal
+    Ain = np.ascontiguousarray(A.T) if tA else A
+    Bin = np.ascontiguousarray(B.T) if tB else B
+    ref = oracle.gemm(Ain, Bin, transA=bool(tA), transB=bool(tB))
+    for cfg in (None, 0, 3, 6, 10, 19):
+        got = R.repops_gemm(dev(Ain), dev(Bin), transA=bool(tA), transB=bool(tB), cfg=cfg)
+        assert_bits(host(got), ref, f"subnormal gemm tA{tA} tB{tB} cfg{cfg}")
+    # an FTZ implementation would flush these: the oracle result is not the flushed one
+    flushed = np.where(np.abs(A) < 2.0 ** -126, np.float32(0), A).astype(np.float32)
+    assert not np.array_equal(oracle.gemm(flushed, B).view(np.uint32), oracle.gemm(A, B).view(np.uint32))
+
+
+def _oracle_rows(args):
+    A, B, r0, r1 = args
+    return oracle.gemm(A[r0:r1], B)
+
+
+def oracle_gemm_parallel(A, B, blocks=None):
+    """the oracle's full R-GEMM split across host processes by output rows (rows are
+    independent, so the bits equal one oracle call)"""
+    import multiprocessing as mp
+    import os
+    n = A.shape[0]
+    procs = max(1, min(os.cpu_count() or 1, 64))
+    blocks = blocks or procs * 2
+    step = (n + blocks - 1) // blocks
+    jobs = [(A, B, r, min(n, r + step)) for r in range(0, n, step)]
+    with mp.get_context("fork").Pool(procs) as pool:
+        return np.concatenate(pool.map(_oracle_rows, jobs))
+
+
+@pytest.mark.slow
+def test_gemm_full_matrix_nn_4096_cfg10():
+    # config 2's 4096 point, NN, in the configuration the cost model picks for it (cfg 10,
+    # the XP shared-memory transpose): every one of the 16.8 M outputs against the oracle
+    n = 4096
+    A, B = synth.gemm_inputs(n, "bench")
+    got = host(R.repops_gemm(dev(A), dev(B), cfg=10))
+    ref = oracle_gemm_parallel(A, B)
+    assert_bits(got, ref, "4096 NN cfg10 full matrix")
+    assert_bits(host(R.repops_gemm(dev(A), dev(B))), ref, "4096 NN default cfg full matrix")
 
 
 def test_gemm_epilogues_and_edge_cases():
@@ -125,7 +201,7 @@ def test_gemm_strided_batched_attention_layout():
             assert_bits(got[(b * H + h) * T:(b * H + h + 1) * T], ref, f"batch {b},{h}")
 
 
-@pytest.mark.parametrize("n", [1024, 2048, 8192])
+@pytest.mark.parametrize("n", [1024, 2048, 4096, 8192])
 def test_gemm_full_size_sampled(n):
     # BASELINE config 2 sizes in the launch configuration bench.py times; the
     # oracle recomputes sampled elements one by one (full K fold each)
