@@ -439,7 +439,12 @@ int verde_first_divergence(const uint8_t *seq0, const uint8_t *seq1, int64_t n, 
  *     levels), outs[q][i] = v for every q.
  *   parts / outs: host arrays of G device pointers (local or peer-mapped), each a
  *   float[>= hi] buffer; G in {1, 2, 4, 8}.  Bits equal repops_tree_sum(parts, G) on
- *   [lo, hi) for any slicing.  Errors: REPOPS_EINVAL (bad G, slice, null pointer).
+ *   [lo, hi) for any slicing.  status: nullable device int32 written by a preceding
+ *   repops_p2p_wait on the same stream; when *status != 0 (a peer did not signal in
+ *   time) the kernel stores nothing, so no stale partial reaches any rank's gradient
+ *   buffer and no peer buffer is written while a late peer may still read it; the
+ *   caller must check the status before trusting the step (P2PTreeCombine.check).
+ *   Errors: REPOPS_EINVAL (bad G, slice, null pointer).
  * repops_p2p_signal: after all prior work on `stream`, release-store (system scope)
  *   `epoch` into peer_flags[q][slot] for every q < G (peer_flags: host array of G device
  *   uint32 arrays of >= G entries, local or peer-mapped).
@@ -451,7 +456,7 @@ int repops_ipc_open(const uint8_t *handle64, void **ptr);
 int repops_ipc_close(void *ptr);
 int repops_ipc_free(void *ptr);
 int repops_p2p_tree_combine(const float *const *parts, int G, int64_t lo, int64_t hi, float *const *outs,
-                            void *stream);
+                            const int32_t *status, void *stream);
 int repops_p2p_signal(uint32_t *const *peer_flags, int G, int slot, uint32_t epoch, void *stream);
 int repops_p2p_wait(const uint32_t *flags, int G, uint32_t epoch, int64_t timeout_ms, int32_t *status,
                     void *stream);

@@ -292,14 +292,16 @@ def repops_ipc_free(t):
     check(lib().repops_ipc_free(t.data_ptr()), "repops_ipc_free")
 
 
-def repops_p2p_tree_combine(parts, lo, hi, outs, stream=None):
-    """out[q][i] = R-TREE_S over parts[*][i] for i in [lo, hi), stored into every outs[q]."""
+def repops_p2p_tree_combine(parts, lo, hi, outs, stream=None, status=None):
+    """out[q][i] = R-TREE_S over parts[*][i] for i in [lo, hi), stored into every outs[q].
+    status: optional device int32 set by a timed-out repops_p2p_wait -- nothing is stored then."""
     G = len(parts)
     if len(outs) != G:
         raise RepopsError("repops_p2p_tree_combine: need one output per part")
     pa = (C.c_void_p * G)(*[_p(q) for q in parts])
     oa = (C.c_void_p * G)(*[_p(q) for q in outs])
-    check(lib().repops_p2p_tree_combine(pa, G, int(lo), int(hi), oa, _stream(stream)), "repops_p2p_tree_combine")
+    check(lib().repops_p2p_tree_combine(pa, G, int(lo), int(hi), oa, _p(status), _stream(stream)),
+          "repops_p2p_tree_combine")
 
 
 def repops_p2p_signal(peer_flags, slot, epoch, stream=None):

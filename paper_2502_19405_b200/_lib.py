@@ -72,7 +72,7 @@ SIGNATURES = {
     "repops_ipc_open": (i32, [vp, vp]),
     "repops_ipc_close": (i32, [vp]),
     "repops_ipc_free": (i32, [vp]),
-    "repops_p2p_tree_combine": (i32, [vp, i32, i64, i64, vp, vp]),
+    "repops_p2p_tree_combine": (i32, [vp, i32, i64, i64, vp, vp, vp]),
     "repops_p2p_signal": (i32, [vp, i32, i32, C.c_uint32, vp]),
     "repops_p2p_wait": (i32, [vp, i32, C.c_uint32, i64, vp, vp]),
     "repops_gelu_erf": (i32, [vp, i64, vp, vp]),

@@ -983,13 +983,13 @@ int repops_ipc_free(void *ptr) {
 }
 
 int repops_p2p_tree_combine(const float *const *parts, int G, int64_t lo, int64_t hi, float *const *outs,
-                            void *stream) {
+                            const int32_t *status, void *stream) {
     REQ(G == 1 || G == 2 || G == 4 || G == 8, "p2p_tree_combine: G = %d is not 1, 2, 4 or 8", G);
     REQ(lo >= 0 && hi >= lo, "p2p_tree_combine: bad slice [%lld, %lld)", (long long)lo, (long long)hi);
     if (hi == lo) return REPOPS_OK;
     REQ(parts && outs, "p2p_tree_combine: null pointer array");
     for (int q = 0; q < G; ++q) REQ(parts[q] && outs[q], "p2p_tree_combine: null peer pointer %d", q);
-    return cuda_status(launch_p2p_tree_combine(parts, G, lo, hi, outs, S(stream)), "p2p_tree_combine");
+    return cuda_status(launch_p2p_tree_combine(parts, G, lo, hi, outs, status, S(stream)), "p2p_tree_combine");
 }
 
 int repops_p2p_signal(uint32_t *const *peer_flags, int G, int slot, uint32_t epoch, void *stream) {

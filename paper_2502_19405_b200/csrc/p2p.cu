@@ -33,7 +33,11 @@ struct PeerOut { float *p[P2P_MAX_PEERS]; };
 struct PeerFlags { uint32_t *p[P2P_MAX_PEERS]; };
 
 template <int G>
-__global__ void __launch_bounds__(256) p2p_tree_kernel(PeerIn in, int64_t lo, int64_t hi, PeerOut out, bool vec) {
+__global__ void __launch_bounds__(256) p2p_tree_kernel(PeerIn in, int64_t lo, int64_t hi, PeerOut out, bool vec,
+                                                            const int32_t *status) {
+    // a timed-out wait before this launch: store nothing (no stale partial is combined,
+    // no peer buffer is written while a late peer may still be reading it)
+    if (status && *reinterpret_cast<const volatile int32_t *>(status) != 0) return;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t n = hi - lo;
@@ -99,7 +103,7 @@ __global__ void p2p_wait_kernel(const uint32_t *flags, int G, uint32_t epoch, in
 }  // namespace
 
 cudaError_t launch_p2p_tree_combine(const float *const *parts, int G, int64_t lo, int64_t hi, float *const *outs,
-                                    cudaStream_t s) {
+                                    const int32_t *status, cudaStream_t s) {
     if (hi <= lo) return cudaSuccess;
     PeerIn in{};
     PeerOut out{};
@@ -114,10 +118,10 @@ cudaError_t launch_p2p_tree_combine(const float *const *parts, int G, int64_t lo
     int64_t cap = (int64_t)ro_host::num_sms() * 8;
     const int grid = (int)(want < 1 ? 1 : (want > cap ? cap : want));
     switch (G) {
-        case 1: p2p_tree_kernel<1><<<grid, 256, 0, s>>>(in, lo, hi, out, vec); break;
-        case 2: p2p_tree_kernel<2><<<grid, 256, 0, s>>>(in, lo, hi, out, vec); break;
-        case 4: p2p_tree_kernel<4><<<grid, 256, 0, s>>>(in, lo, hi, out, vec); break;
-        case 8: p2p_tree_kernel<8><<<grid, 256, 0, s>>>(in, lo, hi, out, vec); break;
+        case 1: p2p_tree_kernel<1><<<grid, 256, 0, s>>>(in, lo, hi, out, vec, status); break;
+        case 2: p2p_tree_kernel<2><<<grid, 256, 0, s>>>(in, lo, hi, out, vec, status); break;
+        case 4: p2p_tree_kernel<4><<<grid, 256, 0, s>>>(in, lo, hi, out, vec, status); break;
+        case 8: p2p_tree_kernel<8><<<grid, 256, 0, s>>>(in, lo, hi, out, vec, status); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

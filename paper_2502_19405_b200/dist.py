@@ -159,7 +159,9 @@ class P2PTreeCombine:
         self.epoch += 1
         tree(local_parts, self.partial)
         self._barrier(0, stream)
-        repops_p2p_tree_combine(self.peer_partial, self.lo, self.hi, self.peer_grad, stream)
+        # a timed-out "ready" wait leaves self.status set: the kernel then stores nothing
+        repops_p2p_tree_combine(self.peer_partial, self.lo, self.hi, self.peer_grad, stream,
+                                status=None if self.sync == "host" else self.status)
         self._barrier(1, stream)
         return self.grad
 

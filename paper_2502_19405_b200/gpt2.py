@@ -997,13 +997,22 @@ class GPT2Step:
         return None
 
     def root_bytes(self):
-        """The last device_root() result (waits for it)."""
+        """The last device_root() result (waits for it).  Raises if the step's peer-memory
+        gradient exchange timed out (its gradients -- and so this root -- are not valid)."""
         self._ev_root.synchronize()
+        self._check_exchange()
         return bytes(self.root_host.numpy())
+
+    def _check_exchange(self):
+        if self.p2p is not None:
+            torch.cuda.current_stream().synchronize()
+            self.p2p.check()
 
     def step_root(self, table=None):
         """Node digests (R-NODE) and the step's Merkle root (R-MERKLE), host native code."""
-        table = self.gather_digests() if table is None else table
+        if table is None:
+            table = self.gather_digests()
+            self._check_exchange()
         n = len(self.nodes)
         out = np.empty((n, 32), np.uint8)
         root = np.empty(32, np.uint8)

@@ -128,22 +128,47 @@ class Trainer:
         return verde_chunk_leaves(v).cpu().numpy().tobytes()
 
 
-def verify_checkpoint_proof(proof, h_start: bytes) -> bool:
-    """Referee side of Case 2(a): does the proof place the claimed digest in h_start?"""
+def verify_checkpoint_proof(proof, h_start: bytes, program: GPT2Step, param: str, slot: int) -> bool:
+    """Referee side of Case 2(a): does the proof place the claimed digest of the DISPUTED
+    tensor (param, slot) in h_start?  Everything that selects the tree position comes
+    from the referee's own program, never from the prover: the C0 entry index
+    (parameter order x 3 + slot) and tree size, or the previous step's AdamW node of
+    `param` (its index, static structure and the node-tree size) and the output slot."""
     if proof["kind"] == "c0":
+        order = [n for n, _, _ in program.specs]
+        if param not in order or proof["index"] != order.index(param) * 3 + slot or proof["n"] != 3 * len(order):
+            return False
         leaf = verde_sha256(b"\x00" + proof["claimed"])
         return verde_merkle_verify_path(leaf, proof["index"], proof["n"], proof["path"], h_start)
-    if proof["outs"][proof["slot"]] != proof["claimed"]:
+    if proof["kind"] != "node":
+        return False
+    j = program.adamw_node.get(param)
+    blob = program.node_blob[program.node_offs[j]:program.node_offs[j + 1]].tobytes() if j is not None else None
+    if j is None or proof["index"] != j or proof["structure"] != blob or proof["slot"] != slot or \
+            proof["n"] != len(program.nodes) or not 0 <= slot < len(proof["outs"]):
+        return False
+    if proof["outs"][slot] != proof["claimed"]:
         return False
     node_digest = verde_sha256(proof["structure"] + b"".join(proof["ins"]) + b"".join(proof["outs"]))
     leaf = verde_sha256(b"\x00" + node_digest)
     return verde_merkle_verify_path(leaf, proof["index"], proof["n"], proof["path"], h_start)
 
 
+def opening_consistent(t: "Trainer", o: Opening) -> bool:
+    """Does the opening of node o.index hash to the node digest the trainer committed in
+    its sequence (R-NODE: SHA-256(structure || in-digests || out-digests))?"""
+    seq = t.seq()
+    if not 0 <= o.index < len(seq) // 32:
+        return False
+    dig = verde_sha256(o.structure + b"".join(o.in_digests) + b"".join(o.out_digests))
+    return dig == seq[32 * o.index:32 * o.index + 32]
+
+
 @dataclass
 class Verdict:
     d: int
-    case: int               # 1, 2 or 3
+    case: int               # 1, 2 or 3; 0 = protocol violation (an opening or served
+                            # tensor inconsistent with the trainer's own commitment)
     dishonest: int          # 0 or 1
     rounds: int             # subtree comparisons to find d
     detail: str
@@ -165,6 +190,15 @@ def phase2(t0: Trainer, t1: Trainer, h_end=None) -> tuple[int, int]:
 def decide(t0: Trainer, t1: Trainer, d: int, rounds: int, program: GPT2Step, h_start=None,
            chunks=True) -> Verdict:
     o0, o1 = t0.open(d), t1.open(d)
+    # every opening must match what the trainer committed (its node digest in the
+    # sequence whose root Phase 2 checked); one that does not convicts its trainer
+    # before any case logic can be steered by forged digests
+    ok = [opening_consistent(t0, o0), opening_consistent(t1, o1)]
+    if ok[0] != ok[1]:
+        return Verdict(d, 0, 0 if not ok[0] else 1, rounds, "opening of the disputed node does not match the "
+                       "trainer's committed node digest")
+    if not ok[0]:
+        raise RuntimeError("neither trainer's opening matches its committed node digest")
     nd = program.nodes[d]
     ref_struct = program.node_blob[program.node_offs[d]:program.node_offs[d + 1]].tobytes()
     # Case 1: graph structure (inputs, outputs, operator) -- the referee knows the program
@@ -175,7 +209,7 @@ def decide(t0: Trainer, t1: Trainer, d: int, rounds: int, program: GPT2Step, h_s
     if nd.op == OP["PARAM_IN"]:
         q = next(i for i, (a, b) in enumerate(zip(o0.out_digests, o1.out_digests)) if a != b)
         param = program.tensors[nd.outputs[q]].name.split("/", 1)[1]
-        ok = [verify_checkpoint_proof(t.prove_checkpoint(param, q), h_start) for t in (t0, t1)]
+        ok = [verify_checkpoint_proof(t.prove_checkpoint(param, q), h_start, program, param, q) for t in (t0, t1)]
         if ok[0] == ok[1]:
             raise RuntimeError("membership proofs verify for neither / both trainers")
         return Verdict(d, 2, 1 if ok[0] else 0, rounds, f"checkpoint tensor {param}[{q}]: membership proof")
@@ -191,14 +225,36 @@ def decide(t0: Trainer, t1: Trainer, d: int, rounds: int, program: GPT2Step, h_s
     for q, (a, b) in enumerate(zip(o0.in_digests, o1.in_digests)):
         if a != b:
             src = program.tensors[nd.inputs[q]]
-            # nodes before d agree, so the source node's output hash is common to both
-            agreed = t0.open(src.producer).out_digests[src.pslot]
+            # nodes before d have equal digests in both sequences; each trainer opens the
+            # source node, and an opening must hash to that common node digest
+            srcs = [t.open(src.producer) for t in (t0, t1)]
+            sok = [opening_consistent(t, o) for t, o in zip((t0, t1), srcs)]
+            if sok[0] != sok[1]:
+                return Verdict(d, 0, 0 if not sok[0] else 1, rounds,
+                               f"opening of source node {src.producer} does not match the committed digest")
+            if not sok[0]:
+                raise RuntimeError("neither trainer's opening of the source node matches its commitment")
+            agreed = srcs[0].out_digests[src.pslot]
             bad = 0 if a != agreed else 1
             return Verdict(d, 2, bad, rounds, f"input {q} hash differs from source node {src.producer}")
     # Case 3: output hashes differ -> recompute on the agreed inputs
     step = t0.step_index
+    # the agreed inputs: from t0, else from t1; a trainer that cannot serve tensors
+    # matching the agreed input digests is convicted
+    served = []
+    for t in (t0, t1):
+        try:
+            served.append(_check_inputs(t.input_tensors(d), o0.in_digests))
+        except ValueError:
+            served.append(None)
+    if (served[0] is None) != (served[1] is None):
+        return Verdict(d, 0, 0 if served[0] is None else 1, rounds,
+                       "served input tensors do not match the agreed input digests")
+    if served[0] is None:
+        raise RuntimeError("neither trainer served inputs matching the agreed input digests")
+    agreed_in = served[0]
     if not chunks:
-        outs = referee_recompute(program, d, t0.input_tensors(d), o0.in_digests, step)
+        outs = referee_recompute(program, d, agreed_in, o0.in_digests, step)
         mine = [bytes(x) for x in verde_commit_tensors(outs).cpu().numpy()]
         ok0, ok1 = mine == o0.out_digests, mine == o1.out_digests
         if ok0 == ok1:
@@ -221,7 +277,7 @@ def decide(t0: Trainer, t1: Trainer, d: int, rounds: int, program: GPT2Step, h_s
     if leaves[0] is None:
         raise RuntimeError("neither trainer served chunk leaves consistent with its digest")
     c, crounds = verde_first_divergence(leaves[0], leaves[1], hashed=True)
-    chunk, count = referee_recompute_chunk(program, d, t0.input_tensors(d), o0.in_digests, q, c, step)
+    chunk, count = referee_recompute_chunk(program, d, agreed_in, o0.in_digests, q, c, step)
     h = verde_sha256(b"\x00" + chunk)
     ok0, ok1 = h == leaves[0][32 * c:32 * c + 32], h == leaves[1][32 * c:32 * c + 32]
     if ok0 == ok1:

@@ -549,7 +549,7 @@ def test_p2p_flag_protocol_virtual_ranks(G):
                 R.repops_p2p_signal(ready, r, epoch, stream=s)
                 R.repops_p2p_wait(ready[r], G, epoch, 10000, status, stream=s)
                 lo, hi = p2p_slice(r, G, n)
-                R.repops_p2p_tree_combine(partial, lo, hi, grad, stream=s)
+                R.repops_p2p_tree_combine(partial, lo, hi, grad, stream=s, status=status)
                 R.repops_p2p_signal(done, r, epoch, stream=s)
                 R.repops_p2p_wait(done[r], G, epoch, 10000, status, stream=s)
         torch.cuda.synchronize()
@@ -557,6 +557,27 @@ def test_p2p_flag_protocol_virtual_ranks(G):
         ref = oracle.tree_sum([host(t) for t in src])
         for r in range(G):
             assert_bits(host(grad[r]), ref, f"epoch {epoch} rank {r}")
+
+
+def test_p2p_wait_timeout_blocks_the_combine():
+    """a peer that never signals: the bounded wait records the timeout in the status
+    word and the combine launched behind it stores nothing (ADVICE: no stale partials
+    reach any gradient buffer); P2P-style check() then raises"""
+    G, n = 2, 4099
+    flags = torch.zeros(G, dtype=torch.int32, device="cuda")
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    parts = [dev(synth.uniform(900 + q, n)) for q in range(G)]
+    grad = [torch.full((n,), 7.0, device="cuda") for _ in range(G)]
+    R.repops_p2p_signal([flags], 0, 1)                     # only slot 0 ever signals
+    R.repops_p2p_wait(flags, G, 1, 50, status)             # 50 ms, slot 1 never arrives
+    R.repops_p2p_tree_combine(parts, 0, n, grad, status=status)
+    torch.cuda.synchronize()
+    assert int(status.item()) == 1
+    for q in range(G):
+        assert torch.all(grad[q] == 7.0), "combine stored after a timed-out wait"
+    status.zero_()
+    R.repops_p2p_tree_combine(parts, 0, n, grad, status=status)   # status clear: it runs
+    assert_bits(host(grad[1]), oracle.tree_sum([host(p) for p in parts]), "after reset")
 
 
 # ------------------------------------------------------------------ deterministic pseudorandomness (R28)

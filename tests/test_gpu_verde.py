@@ -178,3 +178,126 @@ def test_chunk_recompute_equals_full_replay(tiny_program):
         for c in sorted({0, n_chunks // 2, n_chunks - 1}):
             got, count = verde.referee_recompute_chunk(prog, d, ins, o.in_digests, 0, c, 1)
             assert got == full[4096 * c:4096 * (c + 1)], (name, c)
+
+
+# ---------------------------------------------------------------- dishonest openings / proofs / inputs
+def _two_trainers(cfg, node):
+    """an honest trainer and one whose node `node` output has a flipped bit"""
+    from paper_2502_19405_b200 import verde
+    from paper_2502_19405_b200.gpt2 import GPT2Step
+    out = []
+    for fault in (False, True):
+        st = GPT2Step(cfg)
+        st.keep_committed = True
+        st.set_tokens(0)
+        ck = (st.params.clone(), st.m.clone(), st.v.clone())
+        if fault:
+            st.inject_fault(node, 0, 3, 0)
+        st.run()
+        out.append(verde.Trainer(st, ck))
+    return out
+
+
+def test_forged_opening_convicts_the_forger(tiny_program):
+    """A dishonest trainer opens the disputed node with the honest trainer's digests
+    (so the openings look equal): its opening does not hash to the node digest it
+    committed, and the referee convicts it before any case logic (ADVICE: an honest
+    trainer must never be convicted)."""
+    from paper_2502_19405_b200 import verde
+    cfg, prog = tiny_program
+    node = _node_named(prog, "s2/h1/fc")
+    honest, cheat = _two_trainers(cfg, node)
+
+    class Forger(verde.Trainer):
+        def open(self, d):
+            return honest.open(d)
+
+    forger = Forger.__new__(Forger)
+    forger.__dict__.update(cheat.__dict__)
+    for dishonest, (t0, t1) in ((1, (honest, forger)), (0, (forger, honest))):
+        d, rounds = verde.phase2(t0, t1)
+        assert d == node
+        v = verde.decide(t0, t1, d, rounds, prog)
+        assert v.case == 0 and v.dishonest == dishonest, v
+
+
+def test_forged_source_opening_in_case2b(tiny_program):
+    """Case 2(b): the dishonest trainer claims a different input digest for node d and
+    opens the source node with that same forged digest -- both openings are checked
+    against its commitments, so it is convicted (not the honest trainer)."""
+    from paper_2502_19405_b200 import verde
+    cfg, prog = tiny_program
+    node = _node_named(prog, "s2/h1/gelu")           # input: s2/h1/fc (source node)
+    src = prog.tensors[prog.nodes[node].inputs[0]].producer
+    honest, cheat = _two_trainers(cfg, _node_named(prog, "s2/h1/fc"))
+    forged = b"\xab" * 32
+
+    class Liar(verde.Trainer):
+        def open(self, d):
+            o = honest.open(d)
+            if d == node:
+                o.in_digests = [forged]
+            if d == src:
+                o.out_digests = [forged]
+            return o
+
+        def seq(self):
+            return honest.seq()   # claims the honest sequence, so node d is reached with equal digests
+
+    liar = Liar.__new__(Liar)
+    liar.__dict__.update(cheat.__dict__)
+    v = verde.decide(honest, liar, node, 0, prog)
+    assert v.case == 0 and v.dishonest == 1
+
+
+def test_checkpoint_proof_is_bound_to_the_disputed_tensor(tiny_program):
+    """Case 2(a) verifier: a valid proof for one (param, slot) does not verify for
+    another parameter, another slot, or with a prover-chosen node index (e.g. the
+    previous step's PARAM_IN node instead of its AdamW node)."""
+    from paper_2502_19405_b200 import verde
+    cfg, prog = tiny_program
+    run = verde.TrainingRun(cfg)
+    run.train(2, 2)
+    t2 = run.trainer_for_step(2)
+    h1 = run.log[1]["root"]
+    proof = t2.prove_checkpoint("h0.attn.w", 0)
+    assert verde.verify_checkpoint_proof(proof, h1, prog, "h0.attn.w", 0)
+    assert not verde.verify_checkpoint_proof(proof, h1, prog, "h0.fc.w", 0)
+    assert not verde.verify_checkpoint_proof(proof, h1, prog, "h0.attn.w", 1)
+    stale = dict(proof)
+    j = prog.param_in_node["h0.attn.w"]
+    stale["index"] = j
+    stale["structure"] = prog.node_blob[prog.node_offs[j]:prog.node_offs[j + 1]].tobytes()
+    assert not verde.verify_checkpoint_proof(stale, h1, prog, "h0.attn.w", 0)
+    # step-1 proofs from the C0 tree are bound to (param order, slot) the same way
+    t1 = run.trainer_for_step(1)
+    p0 = t1.prove_checkpoint("h1.fc.b", 2)
+    h0 = run.log[0]["root"]
+    assert verde.verify_checkpoint_proof(p0, h0, prog, "h1.fc.b", 2)
+    assert not verde.verify_checkpoint_proof(p0, h0, prog, "h1.fc.w", 2)
+    assert not verde.verify_checkpoint_proof(dict(p0, n=p0["n"] + 1), h0, prog, "h1.fc.b", 2)
+
+
+def test_case3_trainer_serving_wrong_inputs_is_convicted(tiny_program):
+    """Case 3 takes the agreed inputs from t0, else t1; a trainer whose served tensors
+    do not hash to the agreed input digests is convicted (the dispute still resolves)."""
+    from paper_2502_19405_b200 import verde
+    cfg, prog = tiny_program
+    node = _node_named(prog, "s1/h0/fc2")
+    honest, cheat = _two_trainers(cfg, node)
+
+    class BadServer(verde.Trainer):
+        def input_tensors(self, d):
+            xs = [x.clone() for x in super().input_tensors(d)]
+            xs[0].view(-1)[0] += 1.0
+            return xs
+
+    bad = BadServer.__new__(BadServer)
+    bad.__dict__.update(cheat.__dict__)
+    d, rounds = verde.phase2(bad, honest)
+    assert d == node
+    v = verde.decide(bad, honest, d, rounds, prog)
+    assert v.case == 0 and v.dishonest == 0
+    # served correctly by t0, the normal Case 3 decision follows
+    v = verde.decide(cheat, honest, d, rounds, prog)
+    assert v.case == 3 and v.dishonest == 0
