@@ -21,7 +21,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librepops.so")
 OBJ = os.path.join(HERE, "build_obj")
-SOURCES = ["abi.cu", "gemm.cu", "rowops.cu", "elementwise.cu", "sha256.cu", "p2p.cu", "attention.cu"]
+SOURCES = ["abi.cu", "gemm.cu", "gemm_tn.cu", "rowops.cu", "elementwise.cu", "sha256.cu", "p2p.cu", "attention.cu"]
 HEADERS = ["common.cuh", "gemm.cuh", "rowops.cuh", "elementwise.cuh", "sha256.cuh", "p2p.cuh", "attention.cuh"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

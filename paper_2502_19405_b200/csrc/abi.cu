@@ -6,6 +6,7 @@
 // search).  Every compute step on a tensor runs in the kernels of gemm.cu,
 // rowops.cu, elementwise.cu and sha256.cu.
 #include <atomic>
+#include <mutex>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -222,6 +223,40 @@ static int gemm_common(int64_t M, int64_t N, int64_t K, const float *A, int64_t 
     p.vecB = a16(B) && ldb % 4 == 0 && sB0 % 4 == 0 && sB1 % 4 == 0;
     p.vecC = a16(C) && ldc % 4 == 0 && sC0 % 4 == 0 && sC1 % 4 == 0;
     if (force_cfg < 0) force_cfg = g_force_cfg.load(std::memory_order_relaxed);
+    // Large single NN products run as (A^T)^T B: A is transposed (a bit-exact copy) into a
+    // stream-ordered temporary and the A^T-tile kernel runs -- the row-major A tile costs
+    // the shared->shared transpose of every K tile (~8 % at 8192^3), one transpose pass
+    // costs < 1 %.  The K order of every output is unchanged, so are its bits (R2).
+    if (!transA && force_cfg < 0 && b0 * b1 == 1 && K > 0 && p.vecA && (double)M * N * K >= 1073741824.0 &&
+        M % 4 == 0) {
+        void *tmp = nullptr;
+        cudaStream_t st = S(stream);
+        static std::once_flag pool_once;  // keep freed temporaries cached in the stream-ordered pool
+        std::call_once(pool_once, [] {
+            int dev = 0;
+            cudaMemPool_t pool;
+            if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t keep = 1ull << 30;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            }
+            cudaGetLastError();
+        });
+        if (cudaMallocAsync(&tmp, (size_t)(M * K) * sizeof(float), st) == cudaSuccess) {
+            cudaError_t e = launch_transpose(A, M, K, lda, reinterpret_cast<float *>(tmp), M, st);
+            if (e == cudaSuccess) {
+                GemmParams q = p;
+                q.A = reinterpret_cast<const float *>(tmp);
+                q.lda = M;
+                q.transA = 1;
+                q.vecA = true;
+                e = gemm_launch(q, st, force_cfg);
+            }
+            cudaError_t f = cudaFreeAsync(tmp, st);
+            if (e == cudaSuccess && f == cudaSuccess) g_launches.fetch_add(1, std::memory_order_relaxed);  // transpose
+            return cuda_status(e != cudaSuccess ? e : f, "gemm launch (transposed A)");
+        }
+        cudaGetLastError();  // no temporary: fall back to the direct kernel below
+    }
     return cuda_status(gemm_launch(p, S(stream), force_cfg), "gemm launch");
 }
 

@@ -83,20 +83,42 @@ RO_DEV void tile_async(float *dst, const float *__restrict__ src, int64_t ld, in
     }
 }
 
-// Interior fast path of tile_async: every chunk in range, 16-byte aligned rows,
-// 32-bit offset arithmetic (ld < 2^23), no predicates.
-template <int R, int L, int SLD, int THREADS>
-RO_DEV void tile_async_full(float *dst, const float *__restrict__ src, int ld, int tid) {
-    constexpr int CPR = L / 4;
-    constexpr int TOTAL = R * CPR;
-#pragma unroll
-    for (int q = 0; q < TOTAL / THREADS; ++q) {
-        const int c = tid + q * THREADS;
-        const int r = c / CPR;
-        const int l = (c % CPR) * 4;
-        cp_async16(dst + r * SLD + l, src + (r * ld + l), 16);
-    }
+RO_DEV void cp_async16_s(uint32_t dst, const float *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
 }
+
+// Interior fast path of tile_async (every chunk in range, 16-byte aligned rows, no
+// predicates) as a stateful per-thread loader: the thread's chunk c = tid + q*THREADS
+// sits at row r0 + q*RPQ, column l0 of the tile, so one global pointer (advanced by one
+// K tile per issue) plus a constant row step addresses all of its chunks -- 64-bit adds
+// on the ALU pipe instead of per-chunk IMAD address math on the FMA pipe the FFMA2s use.
+// Tiles must be issued in K order (the ring prefetches kt = 0, 1, 2, ... in sequence).
+template <int R, int L, int SLD, int THREADS>
+struct FullLoader {
+    static constexpr int CPR = L / 4;
+    static_assert(THREADS % CPR == 0 && (R * CPR) % THREADS == 0, "full-tile loader geometry");
+    static constexpr int RPQ = THREADS / CPR;  // tile rows between a thread's chunks
+    static constexpr int NQ = R * CPR / THREADS;
+    const float *src;
+    int64_t qstep, tstep;  // elements: RPQ rows; one K tile
+    uint32_t soff;         // bytes: the thread's first chunk within the tile
+    RO_DEV void init(const float *base, int64_t ld, int64_t tile_step, int tid) {
+        const int r = tid / CPR, l = (tid % CPR) * 4;
+        src = base + (int64_t)r * ld + l;
+        qstep = (int64_t)RPQ * ld;
+        tstep = tile_step;
+        soff = (uint32_t)((r * SLD + l) * 4);
+    }
+    RO_DEV void issue(uint32_t stile) {
+        const float *g = src;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            cp_async16_s(stile + soff + q * RPQ * SLD * 4, g);
+            g += qstep;
+        }
+        src += tstep;
+    }
+};
 
 // B^T stored N x K (k contiguous): each thread loads 4 consecutive k of rows
 // n = (tid % BN) (+ BN*... for more chunks) into registers ...
@@ -184,14 +206,22 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB) gemm_kernel(GemmP
 
     // LD == 2: the launcher proved every tile full and aligned -> predicate-free loads
     constexpr bool VEC = LD >= 1;
+    const uint32_t smem_s = (uint32_t)__cvta_generic_to_shared(smem);
+    FullLoader<TA ? BK : BM, TA ? BM : BK, TA ? BM : SKP, THREADS> lda_;
+    FullLoader<BK, BN, BN, THREADS> ldb_;
+    if constexpr (LD == 2) {
+        if (TA) lda_.init(A + m0, p.lda, (int64_t)BK * p.lda, tid);
+        else lda_.init(A + m0 * p.lda, p.lda, BK, tid);
+        if (!TB) ldb_.init(B + n0, p.ldb, (int64_t)BK * p.ldb, tid);
+    }
     auto load_a = [&](int slot, int64_t kt) {
         float *As = smem + slot * CF::STAGE_WORDS;
         const int64_t k0 = kt * BK;
         if constexpr (LD == 2) {
-            if (k0 + BK <= K) {  // every K tile but a ragged last one
-                if (TA) tile_async_full<BK, BM, BM, THREADS>(As, A + k0 * p.lda + m0, (int)p.lda, tid);
-                else tile_async_full<BM, BK, SKP, THREADS>(As, A + m0 * p.lda + k0, (int)p.lda, tid);
-                if (!TB) tile_async_full<BK, BN, BN, THREADS>(As + CF::A_WORDS, B + k0 * p.ldb + n0, (int)p.ldb, tid);
+            if (k0 + BK <= K) {  // every K tile but a ragged last one (always issued in K order)
+                const uint32_t st = smem_s + (uint32_t)(slot * CF::STAGE_WORDS * 4);
+                lda_.issue(st);
+                if (!TB) ldb_.issue(st + CF::A_WORDS * 4);
                 return;
             }
         }
@@ -379,7 +409,7 @@ template <int BM, int BN, int BK, int TM, int TN, int STAGES, int MINB, int KG =
 cudaError_t launch_cfg(const GemmParams &p, cudaStream_t s) {
     const bool vec = p.vecA && p.vecB;
     // full: every M/N tile complete (a ragged last K tile takes the bounded load)
-    const bool full = vec && p.M % BM == 0 && p.N % BN == 0 && p.lda < (1 << 23) && p.ldb < (1 << 23);
+    const bool full = vec && p.M % BM == 0 && p.N % BN == 0;
 #define RO_GEMM_CASE(TA_, TB_)                                                                   \
     if ((bool)p.transA == TA_ && (bool)p.transB == TB_)                                          \
         return full ? launch_one<BM, BN, BK, TM, TN, STAGES, MINB, KG, TA_, TB_, 2, XP>(p, s)        \
@@ -402,13 +432,31 @@ cudaError_t launch_cfg(const GemmParams &p, cudaStream_t s) {
 //   5: 128 x 64, 6: 64 x 128 (8 x 8), 3 CTAs/SM  -- the usual winners
 //   2, 7, 8, 9: stage / fragment / occupancy variants kept for tools/gemm_tune.py
 //   10..14: 6, 5, 3, 1, 4 with XP (A stored M x K transposed in shared memory)
-int gemm_num_cfgs() { return 20; }
+//   15..18: stage / BK variants of 10; 19: 16 x 32 latency tiles
+//   20, 21: gemm_tn.cu 128 x 128 full-tile A^T kernel (BK 32 / 16)
+int gemm_num_cfgs() { return 22; }
 std::atomic<int> g_gemm_smem_floor{0};
 
 cudaError_t gemm_launch(const GemmParams &p, cudaStream_t s, int force_cfg) {
     if (p.M == 0 || p.N == 0 || p.batch0 * p.batch1 == 0) return cudaSuccess;
     if (p.batch0 * p.batch1 > 65535) return cudaErrorInvalidValue;
     int cfg = force_cfg;
+    if (cfg < 0 && gemm_tn_eligible(p) && p.M * p.N * p.batch0 * p.batch1 > (int64_t)ro_host::num_sms() * 16 * 32 * 4) {
+        // A^T-stored full-tile problems: the 128 x 128 x 32 kernel of gemm_tn.cu against the
+        // 64 x 128 and 128 x 64 tiles here.  Cost = tiles on the busiest SM x tile work / rate
+        // (measured on B200: one or two CTAs of either kernel nearly saturate an SM, so the
+        // SM-count quantisation of the tile count is what decides; tools/gemm_tune.py)
+        struct C { int id, bm, bn; double rate; };
+        static const C cand[] = {{20, 128, 128, 66.9}, {6, 64, 128, 64.1}, {5, 128, 64, 60.0}};
+        const int64_t nb = p.batch0 * p.batch1;
+        const int64_t sms = ro_host::num_sms();
+        double best = 1e300;
+        for (const C &c : cand) {
+            const int64_t tiles = ((p.M + c.bm - 1) / c.bm) * ((p.N + c.bn - 1) / c.bn) * nb;
+            const double t = (double)((tiles + sms - 1) / sms) * c.bm * c.bn / c.rate;
+            if (t < best) { best = t; cfg = c.id; }
+        }
+    }
     if (cfg < 0) {
         // Wave-quantisation cost model (bits-neutral choice): time ~ waves x tile
         // area / sustained rate, rates measured on B200 with tools/gemm_tune.py and
@@ -456,6 +504,12 @@ cudaError_t gemm_launch(const GemmParams &p, cudaStream_t s, int force_cfg) {
         // 16 x 32 tiles, one warp, 4 x 4 per thread: latency configuration for problems
         // far below one wave (config 1's MLP, 128^3): 8 FFMA2 per k per thread instead of 32
         case 19: return launch_cfg<16, 32, 16, 4, 4, 3, 16, 4, true>(p, s);
+        // gemm_tn.cu: 128 x 128 tiles, pair-along-m FFMA2 (BK = 32 when K allows, else 16);
+        // shapes it does not take run the same 128 x 128 x 16 tiling in this kernel
+        case 20:
+        case 21:
+            if (gemm_tn_eligible(p)) return gemm_tn_launch(p, s, cfg == 20 ? 32 : 16);
+            return launch_cfg<128, 128, 16, 8, 16, 3, 2>(p, s);
         default: return cudaErrorInvalidValue;
     }
 }

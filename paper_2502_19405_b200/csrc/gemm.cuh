@@ -24,5 +24,8 @@ struct GemmParams {
 // force_cfg: -1 = automatic, else one of gemm_num_cfgs() tile configurations (bits-neutral)
 cudaError_t gemm_launch(const GemmParams &p, cudaStream_t s, int force_cfg);
 int gemm_num_cfgs();
+// gemm_tn.cu: 128 x 128 x 16 full-tile kernel for op(A) = A^T, op(B) = B (bits-neutral)
+bool gemm_tn_eligible(const GemmParams &p);
+cudaError_t gemm_tn_launch(const GemmParams &p, cudaStream_t s, int bk);
 // tuning hook: minimum dynamic shared memory per GEMM CTA (limits occupancy; bits-neutral)
 extern std::atomic<int> g_gemm_smem_floor;
