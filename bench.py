@@ -217,19 +217,35 @@ class GemmSweep:
 
 # ---------------------------------------------------------------------- GPT-2 workload
 class GPT2Train:
-    def __init__(self, rank, world, device, pg=None, commit=True, overlap=True, combine="p2p"):
+    """mode "every" (configs[2] + [4], the headline): every operator output committed,
+    node digests and the step root every step.  mode "checkpoint" (configs[2] alone, as
+    Verde's trainers run between disputes, "log checkpoints only at specified
+    steps"): no per-operator commitments; every CKPT_EVERY-th step commits the training
+    state (param, m, v of every parameter) and its RFC 6962 root."""
+
+    CKPT_EVERY = 10
+
+    def __init__(self, rank, world, device, pg=None, commit=True, overlap=True, combine="p2p", mode="every"):
         from paper_2502_19405_b200.gpt2 import GPT2Config, GPT2Step
         # G > 1: R-TREE_S as one fused peer-memory kernel per rank (CUDA IPC over NVLink)
         self.st = GPT2Step(GPT2Config(), rank=rank, world=world, device=device, pg=pg, combine=combine)
         self.st.overlap_commits = overlap
         self.commit = commit
+        self.mode = mode
+        self.n_steps = 0
         self.st.set_tokens(0)
         self.flops = self.st.flops_per_step()
         self.root = None
 
     def step(self):
-        # the tail commits + root of step n run beside step n+1's forward (no host sync)
         with self.stream_ctx():
+            if self.mode == "checkpoint":
+                self.st.run(commit=False)
+                self.n_steps += 1
+                if self.commit and self.n_steps % self.CKPT_EVERY == 0:
+                    self.st.checkpoint_commit()
+                return
+            # the tail commits + root of step n run beside step n+1's forward (no host sync)
             self.st.run(commit=self.commit, join=False)
             self.st.device_root(sync=False)   # C2 gather + node digests + step root on the GPU; 32 B D2H
 
@@ -269,10 +285,18 @@ class GPT2Train:
         if hasattr(self, "_hi"):
             import torch
             torch.cuda.current_stream().wait_stream(self._hi)  # the timing events see the step's work
-        self.root = self.st.root_bytes()
+        if self.mode == "every":
+            self.root = self.st.root_bytes()
 
     def e2e_step(self):
         self.st.set_tokens(self.st.step_no)    # H2D of this step's batch from pinned host memory
+        if self.mode == "checkpoint":
+            self.st.run(commit=False)
+            self.n_steps += 1
+            if self.commit and self.n_steps % self.CKPT_EVERY == 0:
+                self.st.checkpoint_commit()
+                self.root = self.st.checkpoint_root()   # 148 x 3 digests D2H, root on the host
+            return self.st.loss(), self.root
         self.st.run(commit=self.commit)
         self.root = self.st.device_root()      # 32 B D2H
         return self.st.loss(), self.root       # D2H of the loss
@@ -376,6 +400,116 @@ def mlp_extra(with_oracle=True, reps=200):
     return res
 
 
+# ---------------------------------------------------------------------- cuBLAS context
+# the distinct R-GEMM shapes of one GPT-2 step (tools/gpt2_gemm_shapes.py): layout, M, N, K, batch
+GPT2_GEMM_SHAPES = [("TN", 4096, 2304, 768, 1), ("TN", 4096, 768, 768, 1), ("TN", 4096, 3072, 768, 1),
+                    ("TN", 4096, 768, 3072, 1), ("TN", 4096, 50304, 768, 1), ("TN", 4096, 768, 2304, 1),
+                    ("TN", 4096, 768, 50257, 1), ("TN", 768, 2304, 512, 8), ("TN", 768, 768, 512, 8),
+                    ("TN", 768, 3072, 512, 8), ("TN", 3072, 768, 512, 8), ("TN", 50257, 768, 512, 8),
+                    ("NT", 512, 512, 64, 96), ("NN", 512, 64, 512, 96), ("TN", 512, 64, 512, 96)]
+
+
+def ulp_stats(got, ref):
+    """(elements differing, max ULP distance) of two float32 tensors (same-sign distance in
+    units of the last place; a sign mismatch counts as 2^31)."""
+    import torch
+    a = got.contiguous().view(torch.int32).to(torch.int64)
+    b = ref.contiguous().view(torch.int32).to(torch.int64)
+    a = torch.where(a < 0, -(a & 0x7FFFFFFF), a)   # sign-magnitude -> ordered integers
+    b = torch.where(b < 0, -(b & 0x7FFFFFFF), b)
+    d = (a - b).abs()
+    return int((d != 0).sum().item()), int(d.max().item()) if d.numel() else 0
+
+
+def cublas_context():
+    """Non-reproducible cuBLAS FP32 SGEMM (torch.mm / bmm, TF32 off) on the same shapes as
+    the R-GEMM -- the paper's own overhead comparison (RepOps vs torch::mm, P:684-771) --
+    with the ULP differences of its output from the R-GEMM's (which equals the oracle bit
+    for bit: tests/test_gpu_parity.py, tests/test_gpu_gpt2_referee.py)."""
+    import torch
+
+    import paper_2502_19405_b200 as R
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cuda.matmul.allow_fp16_reduced_precision_reduction = False
+
+    def ms(fn, iters=5):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(iters):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / iters
+
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    out = {}
+    shapes = [("NN", n, n, n, 1) for n in SIZES] + GPT2_GEMM_SHAPES
+    for lay, M, N, K, b in shapes:
+        ta, tb = lay[0] == "T", lay[1] == "T"
+        A = torch.rand((b, K, M) if ta else (b, M, K), device="cuda", generator=gen) * 2 - 1
+        B = torch.rand((b, N, K) if tb else (b, K, N), device="cuda", generator=gen) * 2 - 1
+        Cr = torch.empty((b, M, N), device="cuda")
+        opA = A.transpose(1, 2) if ta else A
+        opB = B.transpose(1, 2) if tb else B
+        if b == 1:
+            rep = lambda: R.repops_gemm(A[0], B[0], transA=ta, transB=tb, out=Cr[0])  # noqa: E731
+            lib = lambda: torch.mm(opA[0], opB[0])  # noqa: E731
+        else:
+            rep = lambda: R.repops_gemm_strided_batched(  # noqa: E731
+                A, B, Cr, M=M, N=N, K=K, lda=A.shape[2], ldb=B.shape[2], ldc=N, sA=(A.shape[1] * A.shape[2], 0),
+                sB=(B.shape[1] * B.shape[2], 0), sC=(M * N, 0), batch=(b, 1), transA=ta, transB=tb)
+            lib = lambda: torch.bmm(opA, opB)  # noqa: E731
+        t_rep, t_lib = ms(rep), ms(lib)
+        Cl = lib()
+        rep()
+        torch.cuda.synchronize()
+        nd, mx = ulp_stats(Cl, Cr)
+        fl = 2.0 * M * N * K * b
+        out[f"{lay} {M}x{N}x{K}" + (f" x{b}" if b > 1 else "")] = {
+            "repops_tflops": round(fl / t_rep / 1e9, 2), "cublas_tflops": round(fl / t_lib / 1e9, 2),
+            "time_ratio": round(t_rep / t_lib, 3), "cublas_ulp_diff_frac": round(nd / Cl.numel(), 4),
+            "cublas_max_ulp": mx}
+        del A, B, Cr, Cl
+    torch.cuda.empty_cache()
+    return out
+
+
+def cublas_vs_oracle_1024():
+    """cpu_baseline leg (rank 0, N = 1): the full oracle R-GEMM at n = 1024 beside cuBLAS
+    SGEMM and the R-GEMM on the same inputs -- ULP-diff counts against the oracle."""
+    import torch
+
+    import oracle
+    import paper_2502_19405_b200 as R
+    import synth
+    A, B = synth.gemm_inputs(1024, "bench")
+    t0 = time.perf_counter()
+    ref = torch.from_numpy(oracle.gemm(A, B)).cuda()
+    t_or = time.perf_counter() - t0
+    Ad, Bd = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    torch.backends.cuda.matmul.allow_tf32 = False
+    nd_c, mx_c = ulp_stats(torch.mm(Ad, Bd), ref)
+    nd_r, mx_r = ulp_stats(R.repops_gemm(Ad, Bd), ref)
+    return {"n": 1024, "elements": 1024 * 1024, "cublas_ulp_diff": nd_c, "cublas_max_ulp": mx_c,
+            "repops_ulp_diff": nd_r, "repops_max_ulp": mx_r, "oracle_s": round(t_or, 2)}
+
+
+def cpu_info():
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(),
+            "affinity": len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else None}
+
+
 # ---------------------------------------------------------------------- oracle legs
 def oracle_sample_gemm(seconds_target=10.0):
     """The oracle (as it stands) on a bounded sample of the GEMM sweep: the first r
@@ -450,7 +584,8 @@ def run_reference(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": cfg,
-        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": 1, "kind": "oracle", "sample": sample,
+                         **cpu_info()},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
@@ -516,7 +651,17 @@ def main():
                          "NCCL all-to-all + all-gather, or NCCL all-gather of partials")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # a bare `python bench.py --gpus N`: relaunch as N ranks (one process per GPU)
+        import subprocess
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={29500 + os.getpid() % 1000}", os.path.abspath(__file__),
+               *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
     rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}\n")
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -527,17 +672,20 @@ def main():
     hbm = measured_hbm_gbs()
     out = {"metric": METRIC}
     results = {}
-    order = [args.workload] + ([] if args.no_sweep else [w for w in ("gemm", "llama") if w != args.workload])
+    order = [args.workload] + ([] if args.no_sweep else
+                               [w for w in ("gpt2_ckpt", "gemm", "llama") if w != args.workload])
     for wname in order:
-        if wname == "gpt2":
+        if wname in ("gpt2", "gpt2_ckpt"):
             wl = GPT2Train(rank, world, device, commit=not args.no_commit, overlap=not args.no_overlap,
-                           combine=args.combine)
+                           combine=args.combine, mode="every" if wname == "gpt2" else "checkpoint")
         elif wname == "gemm":
             wl = GemmSweep(rank, world, device)
         else:
             wl = LlamaPrefillBench(rank, world, device)
         head_wl = wname == args.workload
-        steps = args.steps if head_wl else max(2, min(args.steps, 3))
+        # the config-3 step (checkpoint commits every CKPT_EVERY steps) is timed over a whole
+        # checkpoint interval so the amortised state commitment is inside the region
+        steps = args.steps if head_wl else (GPT2Train.CKPT_EVERY if wname == "gpt2_ckpt" else max(2, min(args.steps, 3)))
         for _ in range(args.warmup if head_wl else 1):
             wl.step()
         torch.cuda.synchronize()
@@ -568,6 +716,8 @@ def main():
                 res["gemm_isolated"] = iso
         elif wname == "llama":
             res["root"] = wl.root.hex()
+        elif wname == "gpt2_ckpt":
+            res["loss"] = wl.st.loss()
         else:
             res["digests"] = wl.digests()
         results[wname] = res
@@ -601,8 +751,16 @@ def main():
                          "sizes": list(SIZES), "sharding": f"M-split over {world} GPU(s), full K per rank",
                          "l2": "step working set 1.07 GB > 126 MB L2 (no explicit flush)"}
         out["digests"] = head["digests"]
+    # primary: the GEMM family's flops over the UNION of its launch intervals (the aux-stream
+    # weight-gradient GEMMs overlap the dgrads, so summed per-launch durations double-count)
+    per_launch = achieved
+    if head.get("gemm_union"):
+        achieved = head["gemm_union"]
     out["roofline"] = {"bound": "alu", "kernel": "repops_gemm (FP32 FFMA2 on CUDA cores, sequential K)",
                        "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else 0,
+                       "basis": "union of the R-GEMM launch intervals in the timed region" if head.get("gemm_union")
+                       else "sum of per-launch CUDA-event durations",
+                       "achieved_per_launch": per_launch, "frac_per_launch": per_launch / peak if peak else 0,
                        "peak_note": "148 SM x 128 FP32 lanes x 2 x sm_max_mhz (unit counts of the guides); frac at "
                                     "the median observed clock: %.3f" % (
                                         achieved / fp32_peak_tflops(clk["sm_mhz"]) if clk["sm_mhz"] else -1),
@@ -638,20 +796,34 @@ def main():
                           "the step, D2H of the committed result (max over ranks)"}
     for other, res in results.items():
         if other != args.workload:
-            key = {"gemm": "gemm_sweep", "llama": "llama_prefill", "gpt2": "gpt2_step"}[other]
+            key = {"gemm": "gemm_sweep", "llama": "llama_prefill", "gpt2": "gpt2_step",
+                   "gpt2_ckpt": "gpt2_train_step"}[other]
             out[key] = {"value": res["value"], "unit": "TFLOP/s", "ms_per_step": res["ms"],
                         "gemm_tflops": res["gemm"][0], "gemm_roofline_frac": res["gemm"][0] / res["gemm"][1],
                         "digests": res.get("digests"), "root": res.get("root"), "commit": res.get("commit"),
+                        "loss": res.get("loss"),
                         "config": {"gemm": "square n=1024..8192, M-split, each output committed",
+                                   "gpt2_ckpt": "configs[2]: GPT-2 124M train step B=8 T=512 without per-operator "
+                                                "commitments; the training state (param, m, v) committed + RFC 6962 "
+                                                f"root every {GPT2Train.CKPT_EVERY} steps (Verde Phase-1 checkpoint "
+                                                "logging, P:303-307), timed over one interval",
                                    "llama": "Llama-3-8B-shaped FP32 prefill, 2048 tokens, 32 layers, TP N-split "
                                             f"over {world} GPU(s) (8 column blocks), every output committed",
                                    "gpt2": "GPT-2 124M train step"}[other]}
     if rank == 0 and world == 1 and not args.no_sweep:
         out["mlp_step"] = mlp_extra(with_oracle=not args.no_cpu_baseline)
+    if rank == 0 and world == 1 and not args.no_sweep:
+        out["cublas"] = {"note": "non-reproducible cuBLAS FP32 SGEMM (torch.mm/bmm, TF32 off) on the same shapes, "
+                                 "as overhead context (the paper's RepOps-vs-torch::mm comparison, P:684-771); "
+                                 "time_ratio = R-GEMM time / cuBLAS time; ULP columns: cuBLAS output vs the "
+                                 "R-GEMM output (bit-identical to the oracle, tests/)",
+                         "shapes": cublas_context()}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, secs, sample = oracle_sample_gpt2() if args.workload == "gpt2" else oracle_sample_gemm()
         out["cpu_baseline"] = {"value": v, "unit": "TFLOP/s", "cores": 1, "kind": "oracle",
-                               "sample": f"{sample}; {secs:.1f} s on 1 host core"}
+                               "sample": f"{sample}; {secs:.1f} s on 1 host core", **cpu_info()}
+        if "cublas" in out:
+            out["cublas"]["vs_oracle_1024"] = cublas_vs_oracle_1024()
     if rank == 0:
         print(json.dumps(out))
     if world > 1:

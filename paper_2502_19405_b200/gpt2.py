@@ -1022,6 +1022,28 @@ class GPT2Step:
                                        P(root)), "verde_node_digests")
         return root.tobytes(), out
 
+    # ------------------------------------------------------------------ checkpoint commitments
+    def checkpoint_commit(self, stream=None):
+        """Enqueue the commitment of the training state (every parameter's param, m, v --
+        the starting checkpoint C_i of the next step): R-TCOMMIT digests into a
+        [3 x n_params, 32] device table, in checkpoint_entries order (verde.py).  This is
+        what a trainer logs at the checkpoint steps of Alg. 1 when it does not
+        commit every operator output (configs[2] without configs[4])."""
+        from . import CommitPlan
+        if getattr(self, "_ckpt_plan", None) is None:
+            views = []
+            for name, _, _ in self.specs:
+                views += [self.pview(self.params, name), self.pview(self.m, name), self.pview(self.v, name)]
+            self._ckpt_digests = torch.zeros((len(views), 32), dtype=torch.uint8, device=self.dev)
+            self._ckpt_plan = CommitPlan(views, self._ckpt_digests)
+        self._ckpt_plan.run(stream=stream)
+
+    def checkpoint_root(self) -> bytes:
+        """RFC 6962 root over the last checkpoint_commit()'s digests (waits for them)."""
+        from . import verde_merkle_root
+        d = self._ckpt_digests.cpu().numpy()
+        return verde_merkle_root([d[i].tobytes() for i in range(d.shape[0])])
+
     def loss(self):
         """Step loss (reported metric): R-SEQ per shard, R-TREE_S over shards, x 1/(S T)."""
         from . import repops_sum_cols_seq as seq
