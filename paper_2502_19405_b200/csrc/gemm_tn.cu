@@ -12,14 +12,14 @@
 //  * accumulator PAIRS run along m: FFMA2 acc{m,m+1}[n] += {a_m, a_m+1} * b_n, the A pair
 //    read straight from the [BK][BM] A^T tile (one LDS.128 = two pairs), the B value a
 //    broadcast scalar -- 64 FFMA2 per k for 6 LDS.128;
-//  * BK = 32 (16 when K % 32 != 0): one barrier per 2048 FFMA2; fragments are read per k
+//  * BK = 32: one barrier per 2048 FFMA2; fragments are read per k
 //    and ptxas schedules the LDS among the FFMA2s (explicit register double buffering of
 //    the fragments measured slower: 60.5 vs 65.9 TFLOP/s at 8192^3 -- 255 registers and
 //    renamed accumulators; a j-outer FFMA2 order measured 60.8);
 //  * global -> shared by cp.async with per-thread pointers advanced by one K tile (64-bit
 //    adds on the ALU pipe; no IMAD address math competing with the FFMA2s).
 // Preconditions (checked by the launcher): op(A) = A^T stored K x M, B stored K x N,
-// M % 128 == N % 128 == K % 16 == 0, 16-byte aligned rows.
+// 16-byte aligned rows; any M, N, K (edge tiles zero filled, ragged last K tile looped).
 // Measured (tools/gemm_auto.py, B200, 1965 MHz): 8192^3 67.0 TFLOP/s (cuBLAS SGEMM 68.5),
 // 4096^3 66.0 (59.5); NN through the transposed-A path of repops_gemm 66.6 (63.9).
 #include "common.cuh"
@@ -36,6 +36,10 @@ constexpr int GROUP_M = 16;                 // row tiles per rasterisation group
 RO_DEV void cp16(uint32_t dst, const float *src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
 }
+// bounded copy: the first `bytes` (0, 4, 8, 12 or 16) come from src, the rest is zero filled
+RO_DEV void cp16z(uint32_t dst, const float *src, int bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(bytes));
+}
 RO_DEV void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 RO_DEV void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
@@ -50,7 +54,7 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_tn_kernel(GemmParams p) {
     const int tx = lane & 7;                 // n: columns tx*4 + 32 h + {0..3}, h < 4
     const int ty = warp * 4 + (lane >> 3);   // m: rows ty*4 + 64 g + {0..3}, g < 2
 
-    const int64_t tiles_m = p.M / BM, tiles_n = p.N / BN;
+    const int64_t tiles_m = (p.M + BM - 1) / BM, tiles_n = (p.N + BN - 1) / BN;
     const int64_t t = blockIdx.x;
     const int64_t per_group = (int64_t)GROUP_M * tiles_n;
     const int64_t grp = t / per_group;
@@ -72,16 +76,34 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_tn_kernel(GemmParams p) {
     const int64_t ta = BK * p.lda, tb = BK * p.ldb;        // one K tile
     const uint32_t s_base = (uint32_t)__cvta_generic_to_shared(smem);
     const uint32_t s_off = (uint32_t)((r0 * BM + l0) * 4);
-    auto issue = [&](int slot) {
+    // edge tiles (ragged M / N) and a ragged last K tile take zero-filled bounded copies;
+    // the zeros are never used by the k loop (it stops at K) or stored (rows >= M, cols >= N)
+    const bool edge = m0 + BM > p.M || n0 + BN > p.N;
+    const int a_bytes = (int)max((int64_t)0, min((int64_t)16, (p.M - m0 - l0) * 4));
+    const int b_bytes = (int)max((int64_t)0, min((int64_t)16, (p.N - n0 - l0) * 4));
+    const int64_t kfull = p.K / BK;  // full K tiles (a ragged remainder follows them)
+    auto issue = [&](int slot, int64_t kt) {
         const uint32_t sa = s_base + (uint32_t)(slot * STAGE_WORDS * 4) + s_off;
         const uint32_t sb = sa + A_WORDS * 4;
         const float *a = ga, *b = gb;
+        if (!edge && kt < kfull) {
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-            cp16(sa + q * 4 * BM * 4, a);
-            cp16(sb + q * 4 * BN * 4, b);
-            a += qa;
-            b += qb;
+            for (int q = 0; q < NQ; ++q) {
+                cp16(sa + q * 4 * BM * 4, a);
+                cp16(sb + q * 4 * BN * 4, b);
+                a += qa;
+                b += qb;
+            }
+        } else {
+            const int64_t kvalid = p.K - kt * BK - r0;  // rows r0 + 4q < kvalid are in range
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const bool kin = 4 * q < kvalid;
+                cp16z(sa + q * 4 * BM * 4, kin && a_bytes ? a : A, kin ? a_bytes : 0);
+                cp16z(sb + q * 4 * BN * 4, kin && b_bytes ? b : B, kin ? b_bytes : 0);
+                a += qa;
+                b += qb;
+            }
         }
         ga += ta;
         gb += tb;
@@ -93,10 +115,10 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_tn_kernel(GemmParams p) {
 #pragma unroll
         for (int j = 0; j < TN; ++j) acc[i][j] = make_float2(0.f, 0.f);  // +0 (R2)
 
-    const int64_t ktiles = p.K / BK;
+    const int64_t ktiles = (p.K + BK - 1) / BK;
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) {
-        if (s < ktiles) issue(s);
+        if (s < ktiles) issue(s, s);
         cp_commit();
     }
 
@@ -126,7 +148,7 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_tn_kernel(GemmParams p) {
     cp_wait<STAGES - 1>();
     __syncthreads();
     int slot = 0;
-    for (int64_t kt = 0; kt < ktiles; ++kt) {
+    for (int64_t kt = 0; kt < kfull; ++kt) {
         const float *st = smem + slot * STAGE_WORDS;
 #pragma unroll
         for (int k = 0; k < BK; ++k) {
@@ -136,9 +158,18 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_tn_kernel(GemmParams p) {
         // the next tile must have landed; every thread is past its reads of this stage
         cp_wait<STAGES - 2>();
         __syncthreads();
-        if (kt + STAGES < ktiles) issue(slot);  // refill the stage just consumed
+        if (kt + STAGES < ktiles) issue(slot, kt + STAGES);  // refill the stage just consumed
         cp_commit();
         slot = (slot + 1 == STAGES) ? 0 : slot + 1;
+    }
+    if (kfull < ktiles) {  // ragged last K tile (landed at the last barrier): the real k only, ascending
+        const float *st = smem + slot * STAGE_WORDS;
+        const int kmax = (int)(p.K - kfull * BK);
+#pragma unroll 1
+        for (int k = 0; k < kmax; ++k) {
+            frag(0, st, k);
+            mma(0);
+        }
     }
     cp_wait<0>();
 
@@ -148,6 +179,7 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_tn_kernel(GemmParams p) {
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
             const int64_t m = m0 + (i >> 1) * 64 + ty * 4 + (i & 1) * 2 + half;
+            if (m >= p.M) continue;
             float *crow = Cp + m * p.ldc;
 #pragma unroll
             for (int h = 0; h < 4; ++h) {
@@ -156,15 +188,16 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_tn_kernel(GemmParams p) {
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     float x = half ? acc[i][4 * h + c].y : acc[i][4 * h + c].x;
-                    if (p.epi == 1) x = __fadd_rn(x, __ldg(p.bias + n + c));
+                    if (p.epi == 1) x = (n + c < p.N) ? __fadd_rn(x, __ldg(p.bias + n + c)) : x;
                     else if (p.epi == 2) x = __fmul_rn(x, p.scale);
                     v[c] = canon(x);
                 }
-                if (p.vecC) {
+                if (p.vecC && n + 4 <= p.N) {
                     *reinterpret_cast<float4 *>(crow + n) = make_float4(v[0], v[1], v[2], v[3]);
                 } else {
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) crow[n + c] = v[c];
+                    for (int c = 0; c < 4; ++c)
+                        if (n + c < p.N) crow[n + c] = v[c];
                 }
             }
         }
@@ -181,7 +214,7 @@ cudaError_t launch_tn(const GemmParams &p, cudaStream_t s) {
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    dim3 grid((unsigned)((p.M / BM) * (p.N / BN)), (unsigned)(p.batch0 * p.batch1));
+    dim3 grid((unsigned)(((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN)), (unsigned)(p.batch0 * p.batch1));
     kern<<<grid, THREADS, smem, s>>>(p);
     return cudaGetLastError();
 }
@@ -189,13 +222,14 @@ cudaError_t launch_tn(const GemmParams &p, cudaStream_t s) {
 }  // namespace
 
 bool gemm_tn_eligible(const GemmParams &p) {
-    return p.transA && !p.transB && p.vecA && p.vecB && p.M % BM == 0 && p.N % BN == 0 && p.K % 16 == 0 &&
-           p.K > 0;
+    // any M, N, K > 0 (ragged edges zero filled, a ragged last K tile runs a short loop);
+    // 16-byte aligned rows of A^T and B
+    return p.transA && !p.transB && p.vecA && p.vecB && p.K > 0;
 }
 
 cudaError_t gemm_tn_launch(const GemmParams &p, cudaStream_t s, int bk) {
     if (!gemm_tn_eligible(p)) return cudaErrorInvalidValue;
     // 3-stage ring: 3 x 32 KB (BK 32) or 3 x 16 KB (BK 16) of shared memory, 2 CTAs / SM
-    if (bk == 32 && p.K % 32 == 0) return launch_tn<3, 32>(p, s);
+    if (bk == 32) return launch_tn<3, 32>(p, s);
     return launch_tn<3, 16>(p, s);
 }

@@ -101,6 +101,25 @@ def test_gemm_tn_kernel_full_tiles(K, epi):
         assert_bits(host(got), ref, f"gemm_tn K{K} epi{epi} cfg{cfg}")
 
 
+@pytest.mark.parametrize("M,N,K", [(301, 200, 77), (50257 // 16, 768, 513), (129, 131, 32), (5, 7, 3),
+                                   (1000, 130, 1)])
+def test_gemm_tn_kernel_ragged_edges(M, N, K):
+    # ragged M / N edge tiles (zero-filled bounded copies, guarded epilogue) and a ragged
+    # last K tile (short loop, no padding) in gemm_tn.cu, e.g. the LM wgrad's M = vocab
+    # and the LM dgrad's K = vocab; 16-byte aligned padded rows (ld % 4 == 0)
+    A, B = synth.gemm_inputs((M, N, K), "gtr")
+    At = np.ascontiguousarray(A.T)
+    lda, ldb = (M + 3) // 4 * 4 + 4, (N + 3) // 4 * 4
+    Ab = np.full((K, lda), np.nan, np.float32)
+    Ab[:, :M] = At
+    Bb = np.full((K, ldb), np.nan, np.float32)
+    Bb[:, :N] = B
+    ref = oracle.gemm(At, B, transA=True)
+    for cfg in (None, 20, 21):
+        got = R.repops_gemm(dev(Ab)[:, :M], dev(Bb)[:, :N], transA=True, cfg=cfg)
+        assert_bits(host(got), ref, f"gemm_tn ragged {M}x{N}x{K} cfg{cfg}")
+
+
 def test_gemm_tn_kernel_batched_and_strided_output():
     # the GPT-2 per-shard weight-gradient layout: a batch of A^T B whose outputs sit at a
     # large stride inside one buffer with ldc > N (the step's [S, P] gradient rows)
