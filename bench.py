@@ -62,14 +62,14 @@ def profiled_gemm_traffic():
     """DRAM bytes per R-GEMM launch, averaged over one GPT-2 step's GEMM launches in
     the committed ncu launch list (profiles/, tools/profile_round.sh); None if absent."""
     import csv
-    path = os.path.join(ROOT, "profiles", "r01_gpt2_step_launches.csv")
+    path = os.path.join(ROOT, "profiles", "r02_gpt2_step_launches.csv")
     try:
         rows = list(csv.reader(open(path)))
         h = rows[0]
         ki, mi, vi = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value")
         byts, ids = 0.0, set()
         for r in rows[1:]:
-            if "gemm_kernel" in r[ki] and r[mi] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            if ("gemm_kernel" in r[ki] or "gemm_tn_kernel" in r[ki]) and r[mi] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
                 byts += float(r[vi].replace(",", ""))
                 ids.add(r[0])
         return byts / len(ids) if ids else None
@@ -777,7 +777,7 @@ def main():
                                            "commit=False (no SHA-256 on the side stream sharing the SMs)",
                        "traffic_note": "DRAM bytes (read + write) per R-GEMM launch, mean over one GPT-2 step's "
                                        "GEMM launches, from the committed ncu launch list "
-                                       "profiles/r01_gpt2_step_launches.csv (cold-cache replay)"}
+                                       "profiles/r02_gpt2_step_launches.csv (cold-cache replay)"}
     if "commit" in head:
         cm = head["commit"]
         cm["hbm_frac"] = cm["gbs"] / hbm

@@ -26,6 +26,14 @@ _SRC = os.path.join(_HERE, "repops_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fno-strict-aliasing",
           "-std=c11", "-fPIC", "-shared"]
+# REPOPS_ORACLE_SANITIZE=1: an AddressSanitizer + UndefinedBehaviorSanitizer build of the same
+# source (tests/test_oracle_sanitizers.py runs the oracle test suite against it; the process
+# needs libasan preloaded).  Same arithmetic flags, so the same bits.
+if os.environ.get("REPOPS_ORACLE_SANITIZE") == "1":
+    _LIB = os.path.join(_HERE, "liboracle_san.so")
+    CFLAGS = ["-O1", "-g", "-fno-omit-frame-pointer", "-fsanitize=address,undefined",
+              "-fno-sanitize-recover=all", "-ffp-contract=off", "-fno-fast-math", "-fno-strict-aliasing",
+              "-std=c11", "-fPIC", "-shared"]
 
 _lock = threading.Lock()
 _lib = None

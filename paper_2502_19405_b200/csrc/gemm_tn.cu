@@ -206,13 +206,15 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_tn_kernel(GemmParams p) {
 
 template <int STAGES, int BK>
 cudaError_t launch_tn(const GemmParams &p, cudaStream_t s) {
-    const size_t smem = (size_t)STAGES * BK * (BM + BN) * sizeof(float);
+    size_t smem = (size_t)STAGES * BK * (BM + BN) * sizeof(float);
+    const size_t floor_bytes = (size_t)g_gemm_smem_floor.load(std::memory_order_relaxed);
+    if (floor_bytes > smem) smem = floor_bytes;  // occupancy experiments only (tools/overlap_probe.py)
     auto kern = gemm_tn_kernel<STAGES, BK>;
-    static bool attr = false;
-    if (!attr) {
+    static size_t attr = 0;
+    if (smem > attr) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        attr = true;
+        attr = smem;
     }
     dim3 grid((unsigned)(((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN)), (unsigned)(p.batch0 * p.batch1));
     kern<<<grid, THREADS, smem, s>>>(p);

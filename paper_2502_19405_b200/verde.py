@@ -501,6 +501,7 @@ class TrainingRun:
     def _load(self, t):
         for dst, src in zip((self.st.params, self.st.m, self.st.v), self.log[t]["state"]):
             dst.copy_(src)
+        self.st.state_changed()
         self.st.step_no = t
 
     def _step(self, t):
@@ -515,6 +516,7 @@ class TrainingRun:
             st.set_tokens(t - 1)
         if tam is not None and tam[1] != "__tokens__":
             repops_flip_bit(st.pview(st.params, tam[1]).reshape(-1), tam[2], tam[3])
+            st.state_changed()
         if self.fault is not None and self.fault[0] == t:
             _, node, elem, bit, slot = self.fault
             st.inject_fault(node, slot, elem, bit)

@@ -165,3 +165,30 @@ def test_fused_attention_step_root_equals_unfused():
         del st
         torch.cuda.empty_cache()
     assert roots[0] == roots[1]
+
+
+def test_param_in_digest_reuse_matches_rehash():
+    """PARAM_IN digests copied from the previous step's AdamW outputs (no re-hash of the
+    unchanged training state) give exactly the step roots of re-hashing every step; an
+    outside write to the state (state_changed) forces the re-hash."""
+    from paper_2502_19405_b200.gpt2 import GPT2Config, GPT2Step
+    cfg = GPT2Config.tiny()
+    a, b = GPT2Step(cfg), GPT2Step(cfg)
+    b.reuse_state_digests = False
+    for t in range(3):
+        for st in (a, b):
+            st.set_tokens(t)
+            st.run()
+        ra, _ = a.step_root()
+        rb, _ = b.step_root()
+        assert ra == rb, f"step {t + 1}: reused PARAM_IN digests change the root"
+    assert a._state_digests_valid
+    # an outside write: without state_changed() the stale digests would be reused
+    import paper_2502_19405_b200 as R
+    for st in (a, b):
+        R.repops_flip_bit(st.pview(st.params, "h0.fc.w").reshape(-1), 5, 0)
+    a.state_changed()
+    for st in (a, b):
+        st.set_tokens(3)
+        st.run()
+    assert a.step_root()[0] == b.step_root()[0]

@@ -21,7 +21,7 @@ if len(sys.argv) > 4:
     marks = [i for i, d in enumerate(allv) if sys.argv[3] in d['name']]
     k = int(sys.argv[4])
     step = allv[marks[k]:marks[k + 1]]
-    assert len(step) == per, (len(step), per)
+    assert per == 0 or len(step) == per, (len(step), per)
 else:
     step = allv[-per:]
 
@@ -33,6 +33,8 @@ def short(k):
         t = lambda x: 'T' if x in ('true', '1') else 'N'  # noqa: E731
         return 'gemm_kernel %sx%s %s%s%s' % (m.group(1), m.group(2), t(m.group(3)), t(m.group(4)),
                                             ' XP' if t(m.group(6)) == 'T' and t(m.group(3)) == 'N' else '')
+    if 'gemm_tn_kernel' in k:
+        return 'gemm_tn_kernel 128x128 TN (gemm_tn.cu)'
     return re.sub(r'\(.*', '', k).replace('void ', '')
 
 

@@ -8,8 +8,11 @@ timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byt
     --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-sweep > gpurun_out/launches_bench.log 2>&1
 echo "launch list: $(wc -l < gpurun_out/launches.csv) lines"
+python tools/launch_shares.py gpurun_out/launches.csv 0 embedding_kernel 3 > gpurun_out/launch_shares.txt 2>&1
 bash tools/prof_gemm_remote.sh "4096x768x3072 1 0 -1 gemm_fc2_tn" "4096x3072x768 1 0 -1 gemm_fc_tn" \
-    "8192x8192x8192 1 0 -1 gemm_8192_tn" "8192x8192x8192 0 0 -1 gemm_8192_nn"
+    "8192x8192x8192 1 0 -1 gemm_8192_tn" "8192x8192x8192 0 0 -1 gemm_8192_nn" "4096x50304x768 1 0 -1 gemm_lmhead_tn" \
+    "512x512x64 0 1 -1 gemm_scores_nt"
+bash tools/prof_cublas_remote.sh 8192x8192x8192 1 0 cublas_8192_tn
 mkdir -p gpurun_out/prof_tmp
 timeout 300 ncu --set full --import-source on --clock-control none -k regex:leaf_kernel -s 1 -c 1 \
     -o gpurun_out/prof_tmp/leaf -f python tools/commit_one.py > /dev/null 2>&1
