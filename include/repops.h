@@ -85,6 +85,34 @@ int repops_gemm_strided_batched(int64_t M, int64_t N, int64_t K,
                                 float *C, int64_t ldc, int64_t sC0, int64_t sC1,
                                 int64_t batch0, int64_t batch1, void *stream);
 
+/* Causal structure of attention (R-ATTN, DESIGN R29 / R31), exact.
+ * repops_gemm_strided_batched_causal: repops_gemm_strided_batched plus `causal`:
+ *   0  none (identical to repops_gemm_strided_batched);
+ *   1  outputs with column > row are NOT computed or written (the caller guarantees they
+ *      are never read, e.g. operator-internal scores under R29 -- the causal softmax reads
+ *      columns <= row only); all other outputs are bit-identical to the full GEMM;
+ *   2  the caller guarantees op(A)[i][k] == +0 for k > i (causal softmax output).  Each
+ *      output tile folds k only up to its last row; the skipped terms fma(+0, B[k][j], acc)
+ *      are applied in closed form from kflags (below), so every output is bit-identical
+ *      to the full K fold for every input, including non-finite B and -0 accumulators.
+ *   kflags (causal 2, device, uint8): per problem [K + 1][ldf] from repops_causal_suffix_flags
+ *   of the same B (problem strides sF0, sF1; ldf >= N).  op(A) = A and op(B) = B only
+ *   (transA = transB = 0) for causal 2.  Errors: REPOPS_EINVAL.
+ * repops_causal_suffix_flags: F[b][k][n] for k = 0..K (rows of stride ldf): bit 0 = some
+ *   B[k'][n], k' >= k, is +-inf or NaN; bit 1 = every B[k'][n], k' >= k, has its sign bit
+ *   set; row K = 2 (empty suffix).  B: K x N, row stride ldb, problem strides sB0, sB1;
+ *   batch0 x batch1 problems.  Integer logic only. */
+int repops_gemm_strided_batched_causal(int64_t M, int64_t N, int64_t K,
+                                       const float *A, int64_t lda, int transA, int64_t sA0, int64_t sA1,
+                                       const float *B, int64_t ldb, int transB, int64_t sB0, int64_t sB1,
+                                       int epi, const float *bias, float scale,
+                                       float *C, int64_t ldc, int64_t sC0, int64_t sC1,
+                                       int64_t batch0, int64_t batch1, int causal, const uint8_t *kflags,
+                                       int64_t ldf, int64_t sF0, int64_t sF1, void *stream);
+int repops_causal_suffix_flags(const float *B, int64_t K, int64_t N, int64_t ldb, int64_t sB0, int64_t sB1,
+                               int64_t batch0, int64_t batch1, uint8_t *flags, int64_t ldf, int64_t sF0,
+                               int64_t sF1, void *stream);
+
 /* Lower-precision STORAGE, binary32 compute ("RepOps works with any lower
  * precision ... (particularly FP16)"; reading R30).  dtypes: VERDE_F32, VERDE_BF16,
  * VERDE_F16 (2-byte elements).  Widening is exact; narrowing is IEEE round to nearest

@@ -19,7 +19,7 @@ F32, I32, U8, BF16, F16 = 1, 2, 3, 4, 5
 _DT = {torch.float32: F32, torch.int32: I32, torch.uint8: U8, torch.bfloat16: BF16, torch.float16: F16}
 
 __all__ = [
-    "repops_gemm", "repops_gemm_strided_batched", "repops_sum_rows", "repops_sum_cols_seq", "repops_tree_sum",
+    "repops_gemm", "repops_gemm_strided_batched", "repops_causal_suffix_flags", "repops_sum_rows", "repops_sum_cols_seq", "repops_tree_sum",
     "repops_softmax", "repops_softmax_backward", "repops_layernorm", "repops_layernorm_backward",
     "repops_layernorm_backward_params", "repops_cross_entropy", "repops_exp", "repops_log", "repops_tanh",
     "repops_rsqrt", "repops_gelu", "repops_gelu_backward", "repops_relu", "repops_relu_backward", "repops_sin", "repops_cos", "repops_erf", "repops_gelu_erf", "repops_convert", "repops_gemm_ex",
@@ -148,18 +148,39 @@ def repops_gemm(A, B, transA=False, transB=False, epi=EPI_NONE, bias=None, scale
 
 def repops_gemm_strided_batched(A, B, C_out, M, N, K, lda, ldb, ldc, sA, sB, sC, batch, transA=False,
                                 transB=False, epi=EPI_NONE, bias=None, scale=1.0, offA=0, offB=0, offC=0,
-                                stream=None):
+                                stream=None, causal=0, kflags=None, ldf=0, sF=(0, 0)):
     """Two-level strided batch of R-GEMMs.  sA/sB/sC = (outer, inner) element strides,
-    batch = (outer, inner) counts; off* are element offsets into the storage of A/B/C."""
+    batch = (outer, inner) counts; off* are element offsets into the storage of A/B/C.
+    causal (repops_gemm_strided_batched_causal): 1 = outputs above the diagonal are not
+    computed (never-read scratch scores); 2 = op(A) is +0 above the diagonal (causal
+    probabilities) -- each tile's K fold stops at its last row, the skipped +0 terms applied
+    exactly from kflags (repops_causal_suffix_flags of B, [K + 1][ldf] per problem)."""
     _f32(A, "A"), _f32(B, "B"), _f32(C_out, "C")
     t0 = _TIMER.begin(stream) if _TIMER else None
-    check(lib().repops_gemm_strided_batched(
-        M, N, K, _p(A) + 4 * offA, lda, int(bool(transA)), sA[0], sA[1], _p(B) + 4 * offB, ldb,
-        int(bool(transB)), sB[0], sB[1], int(epi), _p(bias), float(scale), _p(C_out) + 4 * offC, ldc, sC[0],
-        sC[1], batch[0], batch[1], _stream(stream)), "repops_gemm_strided_batched")
+    args = (M, N, K, _p(A) + 4 * offA, lda, int(bool(transA)), sA[0], sA[1], _p(B) + 4 * offB, ldb,
+            int(bool(transB)), sB[0], sB[1], int(epi), _p(bias), float(scale), _p(C_out) + 4 * offC, ldc, sC[0],
+            sC[1], batch[0], batch[1])
+    if causal:
+        if causal == 2 and (kflags is None or kflags.dtype != torch.uint8):
+            raise RepopsError("repops_gemm_strided_batched: causal 2 needs uint8 kflags")
+        check(lib().repops_gemm_strided_batched_causal(*args, int(causal), _p(kflags), int(ldf), sF[0], sF[1],
+                                                       _stream(stream)), "repops_gemm_strided_batched_causal")
+    else:
+        check(lib().repops_gemm_strided_batched(*args, _stream(stream)), "repops_gemm_strided_batched")
     if t0 is not None:
         _TIMER.end("gemm", t0, 2 * M * N * K * batch[0] * batch[1], stream)
     return C_out
+
+
+def repops_causal_suffix_flags(B, K, N, ldb, sB, batch, out=None, ldf=None, sF=None, offB=0, stream=None):
+    """uint8 [batch0 * batch1, K + 1, ldf] suffix flags of B for causal mode 2 (see repops.h)."""
+    ldf = N if ldf is None else ldf
+    if out is None:
+        out = torch.empty((batch[0] * batch[1], K + 1, ldf), dtype=torch.uint8, device=B.device)
+        sF = ((K + 1) * ldf * batch[1], (K + 1) * ldf)
+    check(lib().repops_causal_suffix_flags(_p(B) + 4 * offB, K, N, ldb, sB[0], sB[1], batch[0], batch[1], _p(out),
+                                           ldf, sF[0], sF[1], _stream(stream)), "repops_causal_suffix_flags")
+    return out
 
 
 # ------------------------------------------------------------------ fused attention (f4)

@@ -36,6 +36,10 @@ SIGNATURES = {
     "repops_last_error": (C.c_char_p, []),
     "repops_launch_count": (i64, []),
     "repops_gemm": (i32, [i64, i64, i64, vp, i64, i32, vp, i64, i32, i32, vp, f32, vp, i64, vp]),
+    "repops_gemm_strided_batched_causal": (i32, [i64, i64, i64, vp, i64, i32, i64, i64, vp, i64, i32, i64, i64,
+                                                 i32, vp, f32, vp, i64, i64, i64, i64, i64, i32, vp, i64, i64, i64,
+                                                 vp]),
+    "repops_causal_suffix_flags": (i32, [vp, i64, i64, i64, i64, i64, i64, i64, vp, i64, i64, i64, vp]),
     "repops_gemm_strided_batched": (i32, [i64, i64, i64, vp, i64, i32, i64, i64, vp, i64, i32, i64, i64,
                                           i32, vp, f32, vp, i64, i64, i64, i64, i64, vp]),
     "repops_gemm_cfg": (i32, [i64, i64, i64, vp, i64, i32, vp, i64, i32, i32, vp, f32, vp, i64, vp, i32]),

@@ -199,8 +199,11 @@ const char *repops_last_error(void) { return g_err.c_str(); }
 static int gemm_common(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, int transA, int64_t sA0,
                        int64_t sA1, const float *B, int64_t ldb, int transB, int64_t sB0, int64_t sB1, int epi,
                        const float *bias, float scale, float *C, int64_t ldc, int64_t sC0, int64_t sC1, int64_t b0,
-                       int64_t b1, void *stream, int force_cfg) {
+                       int64_t b1, void *stream, int force_cfg, int causal = 0, const uint8_t *kflags = nullptr,
+                       int64_t ldf = 0, int64_t sF0 = 0, int64_t sF1 = 0) {
     REQ(M >= 0 && N >= 0 && K >= 0 && b0 >= 0 && b1 >= 0, "gemm: negative extent");
+    REQ(causal >= 0 && causal <= 2, "gemm: causal mode %d not in {0, 1, 2}", causal);
+    REQ(causal != 2 || (kflags && ldf >= N && !transA && !transB), "gemm: causal 2 needs kflags, ldf >= N, NN");
     REQ(epi >= REPOPS_EPI_NONE && epi <= REPOPS_EPI_SCALE, "gemm: unknown epilogue %d", epi);
     if (M == 0 || N == 0 || b0 == 0 || b1 == 0) return REPOPS_OK;
     REQ(C != nullptr, "gemm: C is null");
@@ -222,12 +225,15 @@ static int gemm_common(int64_t M, int64_t N, int64_t K, const float *A, int64_t 
     p.vecA = a16(A) && lda % 4 == 0 && sA0 % 4 == 0 && sA1 % 4 == 0;
     p.vecB = a16(B) && ldb % 4 == 0 && sB0 % 4 == 0 && sB1 % 4 == 0;
     p.vecC = a16(C) && ldc % 4 == 0 && sC0 % 4 == 0 && sC1 % 4 == 0;
+    p.causal = causal;
+    p.kflags = kflags;
+    p.ldf = ldf; p.sF0 = sF0; p.sF1 = sF1;
     if (force_cfg < 0) force_cfg = g_force_cfg.load(std::memory_order_relaxed);
     // Large single NN products run as (A^T)^T B: A is transposed (a bit-exact copy) into a
     // stream-ordered temporary and the A^T-tile kernel runs -- the row-major A tile costs
     // the shared->shared transpose of every K tile (~8 % at 8192^3), one transpose pass
     // costs < 1 %.  The K order of every output is unchanged, so are its bits (R2).
-    if (!transA && force_cfg < 0 && b0 * b1 == 1 && K > 0 && p.vecA && (double)M * N * K >= 1073741824.0 &&
+    if (!transA && causal == 0 && force_cfg < 0 && b0 * b1 == 1 && K > 0 && p.vecA && (double)M * N * K >= 1073741824.0 &&
         M % 4 == 0) {
         void *tmp = nullptr;
         cudaStream_t st = S(stream);
@@ -272,6 +278,25 @@ int repops_gemm_strided_batched(int64_t M, int64_t N, int64_t K, const float *A,
                                 int64_t batch0, int64_t batch1, void *stream) {
     return gemm_common(M, N, K, A, lda, transA, sA0, sA1, B, ldb, transB, sB0, sB1, epi, bias, scale, C, ldc, sC0,
                        sC1, batch0, batch1, stream, -1);
+}
+
+int repops_gemm_strided_batched_causal(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, int transA,
+                                       int64_t sA0, int64_t sA1, const float *B, int64_t ldb, int transB, int64_t sB0,
+                                       int64_t sB1, int epi, const float *bias, float scale, float *C, int64_t ldc,
+                                       int64_t sC0, int64_t sC1, int64_t batch0, int64_t batch1, int causal,
+                                       const uint8_t *kflags, int64_t ldf, int64_t sF0, int64_t sF1, void *stream) {
+    return gemm_common(M, N, K, A, lda, transA, sA0, sA1, B, ldb, transB, sB0, sB1, epi, bias, scale, C, ldc, sC0,
+                       sC1, batch0, batch1, stream, -1, causal, kflags, ldf, sF0, sF1);
+}
+
+int repops_causal_suffix_flags(const float *B, int64_t K, int64_t N, int64_t ldb, int64_t sB0, int64_t sB1,
+                               int64_t batch0, int64_t batch1, uint8_t *flags, int64_t ldf, int64_t sF0, int64_t sF1,
+                               void *stream) {
+    REQ(K >= 0 && N >= 0 && batch0 >= 0 && batch1 >= 0, "causal_suffix_flags: negative extent");
+    REQ(flags && ldf >= N && (K == 0 || (B && ldb >= N)), "causal_suffix_flags: bad pointer / leading dimension");
+    REQ(batch0 * batch1 <= 65535, "causal_suffix_flags: too many problems");
+    return cuda_status(launch_causal_flags(B, K, N, ldb, sB0, sB1, batch0, batch1, flags, ldf, sF0, sF1, S(stream)),
+                       "causal_suffix_flags");
 }
 
 // ------------------------------------------------------------------ fused attention (f4)

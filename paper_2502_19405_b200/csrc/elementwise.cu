@@ -654,6 +654,58 @@ cudaError_t launch_fill_uniform(float *out, int64_t n, uint64_t seed, double sca
     return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ causal suffix flags (f4)
+// flags[b][k][n], k = 0..K: bit 0 = some B[k'][n], k' >= k, is non-finite; bit 1 = every
+// B[k'][n], k' >= k, has its sign bit set (row K: the empty suffix, bits = 2).  One CTA of
+// 32 columns x 8 row segments: each thread folds its segment, the segment carries are
+// combined from the bottom, then each thread writes its rows.  Integer logic only.
+namespace {
+__global__ void __launch_bounds__(256) causal_flags_kernel(const float *__restrict__ B, int64_t K, int64_t N,
+                                                           int64_t ldb, int64_t sB0, int64_t sB1, int64_t b1n,
+                                                           uint8_t *__restrict__ F, int64_t ldf, int64_t sF0,
+                                                           int64_t sF1) {
+    __shared__ uint8_t carry[8][32];
+    const int cx = threadIdx.x & 31, sg = threadIdx.x >> 5;
+    const int64_t n = (int64_t)blockIdx.x * 32 + cx;
+    const int64_t bb0 = blockIdx.y / b1n, bb1 = blockIdx.y % b1n;
+    const float *Bb = B + bb0 * sB0 + bb1 * sB1;
+    uint8_t *Fb = F + bb0 * sF0 + bb1 * sF1;
+    const int64_t seg = (K + 7) / 8;
+    const int64_t k0 = min(K, sg * seg), k1 = min(K, k0 + seg);
+    auto bits = [&](int64_t k) -> uint32_t {  // flag bits of the single element B[k][n]
+        const uint32_t u = __float_as_uint(Bb[k * ldb + n]);
+        return (((u & 0x7F800000u) == 0x7F800000u) ? 1u : 0u) | ((u >> 31) << 1);
+    };
+    uint32_t f = 2u;  // empty segment: nothing non-finite, all negative (vacuously)
+    if (n < N)
+        for (int64_t k = k1 - 1; k >= k0; --k) {
+            const uint32_t e = bits(k);
+            f = (f & 1u) | (e & 1u) | (f & e & 2u);
+        }
+    carry[sg][cx] = (uint8_t)f;
+    __syncthreads();
+    uint32_t c = 2u;  // suffix of the segments below this one
+    for (int q = 7; q > sg; --q) c = (c & 1u) | (carry[q][cx] & 1u) | (c & carry[q][cx] & 2u);
+    if (n >= N) return;
+    if (sg == 7 || k1 == K) Fb[K * ldf + n] = 2u;
+    f = c;
+    for (int64_t k = k1 - 1; k >= k0; --k) {
+        const uint32_t e = bits(k);
+        f = (f & 1u) | (e & 1u) | (f & e & 2u);
+        Fb[k * ldf + n] = (uint8_t)f;
+    }
+}
+}  // namespace
+
+cudaError_t launch_causal_flags(const float *B, int64_t K, int64_t N, int64_t ldb, int64_t sB0, int64_t sB1,
+                                int64_t b0, int64_t b1, uint8_t *F, int64_t ldf, int64_t sF0, int64_t sF1,
+                                cudaStream_t s) {
+    if (N == 0 || b0 * b1 == 0) return cudaSuccess;
+    dim3 grid((unsigned)((N + 31) / 32), (unsigned)(b0 * b1));
+    causal_flags_kernel<<<grid, 256, 0, s>>>(B, K, N, ldb, sB0, sB1, b1, F, ldf, sF0, sF1);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_transpose(const float *x, int64_t rows, int64_t cols, int64_t ldx, float *y, int64_t ldy,
                              cudaStream_t s) {
     if (rows == 0 || cols == 0) return cudaSuccess;

@@ -39,6 +39,9 @@ cudaError_t launch_rope(const float *x, int64_t ntok, int64_t nhead, int64_t hd,
 cudaError_t launch_gather_rows(const float *table, const int32_t *idx, int64_t n, int64_t C, float *out,
                                cudaStream_t s);
 cudaError_t launch_fill_uniform(float *out, int64_t n, uint64_t seed, double scale, cudaStream_t s);
+cudaError_t launch_causal_flags(const float *B, int64_t K, int64_t N, int64_t ldb, int64_t sB0, int64_t sB1,
+                                int64_t b0, int64_t b1, uint8_t *F, int64_t ldf, int64_t sF0, int64_t sF1,
+                                cudaStream_t s);
 cudaError_t launch_transpose(const float *x, int64_t rows, int64_t cols, int64_t ldx, float *y, int64_t ldy,
                              cudaStream_t s);
 cudaError_t launch_rand_uniform(uint64_t seed, uint64_t stream, int64_t n, float *y, cudaStream_t s);

@@ -202,7 +202,10 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB) gemm_kernel(GemmP
     const float *__restrict__ A = p.A + b0 * p.sA0 + b1 * p.sA1;
     const float *__restrict__ B = p.B + b0 * p.sB0 + b1 * p.sB1;
     float *__restrict__ Cp = p.C + b0 * p.sC0 + b1 * p.sC1;
-    const int64_t M = p.M, N = p.N, K = p.K;
+    const int64_t M = p.M, N = p.N;
+    if (p.causal == 1 && n0 > m0 + BM - 1) return;  // every output of the tile is masked
+    // causal A: the tile's rows end at m0 + BM - 1, so op(A)[i][k] = +0 for k >= m0 + BM
+    const int64_t K = (p.causal == 2) ? min(p.K, m0 + BM) : p.K;
 
     // LD == 2: the launcher proved every tile full and aligned -> predicate-free loads
     constexpr bool VEC = LD >= 1;
@@ -357,6 +360,27 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB) gemm_kernel(GemmP
         if (TB && pref) store_bt(slot_pref);  // slot of tile kt-1: free since this iteration's barrier
     }
     cp_wait<0>();
+
+    if (p.causal == 2 && K < p.K) {
+        // the skipped terms fma(+0, B[k][j], acc), k = K .. p.K - 1, in closed form: a
+        // non-finite B gives NaN (0 * inf, NaN); otherwise only acc = -0 can change, to +0
+        // unless every skipped B[k][j] is negative (-0 + -0 = -0, -0 + +0 = +0 under RN)
+        const uint8_t *fl = p.kflags + b0 * p.sF0 + b1 * p.sF1 + K * p.ldf;
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < NP; ++j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int h = j / 2, c = (j % 2) * 2 + e;
+                    const int64_t n = n0 + h * (BN / (TN / 4)) + tx * 4 + c;
+                    if (n >= N) continue;
+                    const uint8_t f = fl[n];
+                    float &x = e ? acc[i][j].y : acc[i][j].x;
+                    if (f & 1) x = __uint_as_float(0x7FC00000u);
+                    else if (__float_as_uint(x) == 0x80000000u && !(f & 2)) x = 0.0f;
+                }
+    }
 
     // epilogue (R3): epi(acc) once, NaN canonicalised (R10)
 #pragma unroll

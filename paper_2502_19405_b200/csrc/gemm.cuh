@@ -19,6 +19,15 @@ struct GemmParams {
     const float *bias;
     float scale;
     bool vecA, vecB, vecC;  // 16-byte alignment of every row start (speed only)
+    // causal structure (f4, exact): 0 none; 1 = outputs with column > row are never read
+    // (scratch scores): CTA tiles entirely above the diagonal are skipped; 2 = op(A)[i][k]
+    // is +0 for k > i (causal probabilities): a CTA tile's K fold stops after its last
+    // row, and the skipped fma(+0, B[k][j], acc) terms are applied in closed form from
+    // kflags[k][j] (bit 0: some B[k'][j], k' >= k, is non-finite; bit 1: every such B
+    // has its sign bit set) -- bit-identical to the full fold for every input
+    int causal;
+    const uint8_t *kflags;
+    int64_t ldf, sF0, sF1;
 };
 
 // force_cfg: -1 = automatic, else one of gemm_num_cfgs() tile configurations (bits-neutral)

@@ -226,7 +226,7 @@ cudaError_t launch_tn(const GemmParams &p, cudaStream_t s) {
 bool gemm_tn_eligible(const GemmParams &p) {
     // any M, N, K > 0 (ragged edges zero filled, a ragged last K tile runs a short loop);
     // 16-byte aligned rows of A^T and B
-    return p.transA && !p.transB && p.vecA && p.vecB && p.K > 0;
+    return p.transA && !p.transB && p.vecA && p.vecB && p.K > 0 && p.causal == 0;
 }
 
 cudaError_t gemm_tn_launch(const GemmParams &p, cudaStream_t s, int bk) {

@@ -100,7 +100,7 @@ class P2PTreeCombine:
     Setup (once): every rank allocates, with CUDA IPC, a partial buffer [P], a gradient
     buffer [P] (what AdamW reads) and a flag array [2, G]; the 64-byte handles are
     all-gathered over the process group and every peer buffer is mapped.
-    Per call (`epoch` = call count, all on the caller's stream, no host sync):
+    Per bucket (`epoch` = bucket count, all on the caller's stream, no host sync):
       1. tree(local parts) -> my partial (the aligned local subtree);
       2. signal "partial ready" into every peer's flags[0][me]; wait for all G;
       3. repops_p2p_tree_combine on my slice p2p_slice(me): loads the slice of all G
@@ -153,17 +153,31 @@ class P2PTreeCombine:
         repops_p2p_signal(peers, self.rank, self.epoch, stream)
         repops_p2p_wait(peers[self.rank], self.world, self.epoch, self.timeout_ms, self.status, stream)
 
-    def __call__(self, local_parts, tree, stream=None):
-        """combine; returns self.grad (the IPC gradient buffer, identical on every rank)."""
+    def combine_range(self, local_parts, lo: int, hi: int, tree, stream=None):
+        """One bucket [lo, hi) of the gradient (a layer's parameters): local subtree ->
+        my partial[lo:hi]; "ready" signal / wait (next epoch); the fused kernel on my
+        sub-slice of the bucket.  Buckets of one step are disjoint and issued in the
+        same order on every rank; finish() closes the step."""
         from . import repops_p2p_tree_combine
         self.epoch += 1
-        tree(local_parts, self.partial)
+        tree([q[lo:hi] for q in local_parts], self.partial[lo:hi])
         self._barrier(0, stream)
+        slo, shi = p2p_slice(self.rank, self.world, hi - lo)
         # a timed-out "ready" wait leaves self.status set: the kernel then stores nothing
-        repops_p2p_tree_combine(self.peer_partial, self.lo, self.hi, self.peer_grad, stream,
+        repops_p2p_tree_combine(self.peer_partial, lo + slo, lo + shi, self.peer_grad, stream,
                                 status=None if self.sync == "host" else self.status)
+
+    def finish(self, stream=None):
+        """ "done" signal / wait: every rank's slices of every bucket are in every gradient
+        buffer, and no peer reads my partial again until the next step's first bucket."""
         self._barrier(1, stream)
         return self.grad
+
+    def __call__(self, local_parts, tree, stream=None):
+        """combine the whole gradient as one bucket; returns self.grad (the IPC gradient
+        buffer, identical on every rank)."""
+        self.combine_range(local_parts, 0, self.n, tree, stream)
+        return self.finish(stream)
 
     def check(self):
         """raise if a device wait timed out (call after synchronising)."""

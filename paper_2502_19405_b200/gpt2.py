@@ -135,6 +135,11 @@ class GPT2Step:
         if combine not in ("sliced", "gather", "p2p"):
             raise ValueError(f"unknown combine {combine!r}")
         self.combine, self.p2p_sync, self.p2p = combine, p2p_sync, None
+        # f1: with the peer-memory combine each layer's gradient bucket is combined on a
+        # comm stream right after that layer's backward (overlapping the next layers'
+        # backward); the embedding / final-LN buckets and the "done" barrier follow the
+        # embedding backward.  Same bits as one whole-gradient combine (elementwise).
+        self.bucketed = True
         self.sliced_combine = combine == "sliced"
         # f4: scores + causal softmax + PV as one kernel (same bits).  Off by default: at the
         # GPT-2 shape the fused kernel (1 CTA / SM, 213 KB of shared memory) measured 307 us
@@ -642,6 +647,9 @@ class GPT2Step:
                     self._hook(f"h{l}/ln1_bwd")
                     self._aux(w_ln1)
                     self._aux_join()  # the phase's commit plan hashes every output of the layer
+                    if self.p2p is not None and self.bucketed:
+                        lo, hi = self._layer_range(l)
+                        self._bucket(lo, hi)
                 self.launch(bwd)
             pre = f"s{s}/h{l}/"
             t_dout = t_dx
@@ -712,6 +720,26 @@ class GPT2Step:
         self.node(OP["EMBED_BWD"], s, {}, [t_tok, t_dx, t_gwte_lm], [fg["wte"], fg["wpe"]], f"s{s}/embed_bwd",
                   defer=True)
 
+    def _layer_range(self, l):
+        """[lo, hi) of block l's parameters in the flat parameter / gradient layout."""
+        c = self.cfg
+        lo = self.off[f"h{l}.ln1.g"][0]
+        hi = self.off[f"h{l + 1}.ln1.g"][0] if l + 1 < c.n_layer else self.off["lnf.g"][0]
+        return lo, hi
+
+    def _bucket(self, lo, hi):
+        """combine gradient bucket [lo, hi) on the comm stream, after what the current
+        stream has enqueued (the bucket's per-shard gradients)."""
+        if hi <= lo:
+            return
+        if getattr(self, "comm", None) is None:
+            self.comm = torch.cuda.Stream(device=self.dev, priority=-1)
+        main = torch.cuda.current_stream()
+        self.comm.wait_stream(main)
+        parts = [self.glocal[q] for q in range(self.S_loc)]
+        with torch.cuda.stream(self.comm):
+            self.p2p.combine_range(parts, lo, hi, lambda ps, out: repops_tree_sum(ps, out=out), stream=self.comm)
+
     def _gslice(self, s, name):
         if not self._is_local(s):
             return torch.empty(0, device=self.dev)
@@ -733,7 +761,16 @@ class GPT2Step:
         def tree():
             parts = [self.glocal[q] for q in range(self.S_loc)]
             if self.p2p is not None:
-                self.p2p(parts, lambda ps, out: repops_tree_sum(ps, out=out))
+                if not self.bucketed:
+                    self.p2p(parts, lambda ps, out: repops_tree_sum(ps, out=out))
+                    return
+                # the parameters outside the transformer blocks (wte, wpe before them, lnf
+                # after them), then the step's "done" barrier; AdamW waits for the comm stream
+                self._bucket(0, self._layer_range(0)[0])
+                self._bucket(self._layer_range(c.n_layer - 1)[1], self.P)
+                with torch.cuda.stream(self.comm):
+                    self.p2p.finish(stream=self.comm)
+                torch.cuda.current_stream().wait_stream(self.comm)
                 return
             combine = dp_tree_combine_sliced if self.sliced_combine else dp_tree_combine
             combine(parts, self.world, lambda ps, out: repops_tree_sum(ps, out=out), self.pg, out=self.grad)

@@ -36,7 +36,7 @@ import torch
 
 import synth
 
-from . import (EPI_SCALE, CommitPlan, RootPlan, repops_add, repops_copy2d, repops_fill_uniform, repops_gather_rows,
+from . import (repops_causal_suffix_flags, EPI_SCALE, CommitPlan, RootPlan, repops_add, repops_copy2d, repops_fill_uniform, repops_gather_rows,
                repops_gemm_strided_batched, repops_rmsnorm, repops_rope, repops_softmax, repops_swiglu,
                repops_rope_tables, repops_transpose, verde_commit_tensors)
 from ._lib import check, lib
@@ -133,6 +133,8 @@ class LlamaPrefill:
         self.act = []
         # R29: attention scores / probabilities are operator-internal scratch shared by all layers
         self.S_scr, self.P_scr = E(nbl, qh * T, T), E(nbl, qh * T, T)
+        self.causal_skip = True   # f4: exact causal tile skipping in the attention GEMMs
+        self.vflags = torch.empty((nbl, T + 1, hd), dtype=torch.uint8, device=self.dev)
         for _ in range(L):
             self.act.append(dict(xn=E(T, d), rs1=E(T), qkv=E(nbl, T, self.Wb), qk=E(nbl, T, (qh + 1) * hd),
                                  S=self.S_scr, P=self.P_scr, o=E(nbl, T, qh * hd),
@@ -332,13 +334,23 @@ class LlamaPrefill:
         for j in range(nbl):
             repops_rope(a["qkv"][j][:, :(qh + 1) * hd], self.cos, self.sin, qh + 1, hd, out=a["qk"][j])
         W2 = (qh + 1) * hd
+        # f4 (exact causal structure, R29 scratch): score tiles entirely above the diagonal
+        # are never read by the causal softmax, so they are not computed; the PV folds stop
+        # at each tile's last query row and the skipped +0-probability terms are applied in
+        # closed form from V's suffix flags -- the attention output bits are those of the
+        # full R-GEMM -> R-SOFTMAX -> R-GEMM composition for every input
         repops_gemm_strided_batched(a["qk"], a["qk"], a["S"], M=T, N=T, K=hd, lda=W2, ldb=W2, ldc=T,
                                     sA=(T * W2, hd), sB=(T * W2, 0), sC=(qh * T * T, T * T), batch=(nbl, qh),
-                                    transB=True, epi=EPI_SCALE, scale=scale, offB=qh * hd)
+                                    transB=True, epi=EPI_SCALE, scale=scale, offB=qh * hd,
+                                    causal=1 if self.causal_skip else 0)
         repops_softmax(a["S"].view(-1, T), causal=True, out=a["P"].view(-1, T))
+        if self.causal_skip:
+            repops_causal_suffix_flags(a["qkv"], T, hd, Wb, (T * Wb, 0), (nbl, 1), out=self.vflags,
+                                       ldf=hd, sF=((T + 1) * hd, 0), offB=(qh + 1) * hd)
         repops_gemm_strided_batched(a["P"], a["qkv"], a["o"], M=T, N=hd, K=T, lda=T, ldb=Wb, ldc=qh * hd,
                                     sA=(qh * T * T, T * T), sB=(T * Wb, 0), sC=(T * qh * hd, hd), batch=(nbl, qh),
-                                    offB=(qh + 1) * hd)
+                                    offB=(qh + 1) * hd, causal=2 if self.causal_skip else 0, kflags=self.vflags,
+                                    ldf=hd, sF=((T + 1) * hd, 0))
         self._gather_blocks(a["o"], a["o_all"], qh * hd)
         HD = c.n_head * hd
         repops_gemm_strided_batched(self._xT(a["o_all"]), w["wo"], a["op"], M=T, N=self.Db, K=HD, lda=T,

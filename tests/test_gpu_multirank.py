@@ -21,7 +21,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, tiny, q, combine="sliced"):
+def _worker(rank, world, port, tiny, q, combine="sliced", sync="host", bucketed=True):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -30,7 +30,8 @@ def _worker(rank, world, port, tiny, q, combine="sliced"):
         torch.cuda.set_device(0)
         from paper_2502_19405_b200.gpt2 import GPT2Config, GPT2Step
         cfg = GPT2Config.tiny() if tiny else GPT2Config()
-        st = GPT2Step(cfg, rank=rank, world=world, combine=combine, p2p_sync="host")
+        st = GPT2Step(cfg, rank=rank, world=world, combine=combine, p2p_sync=sync)
+        st.bucketed = bucketed
         st.set_tokens(0)
         st.run()
         root, _ = st.step_root()
@@ -46,11 +47,11 @@ def _worker(rank, world, port, tiny, q, combine="sliced"):
         dist.destroy_process_group()
 
 
-def _run(world, tiny, combine="sliced"):
+def _run(world, tiny, combine="sliced", sync="host", bucketed=True):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, world, port, tiny, q, combine)) for r in range(world)]
+    ps = [ctx.Process(target=_worker, args=(r, world, port, tiny, q, combine, sync, bucketed)) for r in range(world)]
     for p in ps:
         p.start()
     res = []
@@ -98,6 +99,32 @@ def test_tiny_step_root_p2p_combine(world, tiny_single):
     for rank, root, loss, pdig in _run(world, True, combine="p2p"):
         assert root == tiny_single[1], f"p2p world {world} rank {rank}: step root differs"
         assert pdig == tiny_single[3]
+
+
+def test_tiny_step_root_p2p_whole_gradient(tiny_single):
+    """the un-bucketed peer-memory combine (one bucket) gives the same root"""
+    for rank, root, loss, pdig in _run(2, True, combine="p2p", bucketed=False):
+        assert root == tiny_single[1]
+
+
+def test_tiny_step_root_p2p_device_flags_across_processes(tiny_single):
+    """the device-side signal / wait protocol (release / acquire on IPC-mapped flags,
+    system scope) between two rank PROCESSES -- the transport bench.py uses at N > 1.
+    On one GPU the two contexts time-slice, so every wait completes only after the
+    other process's context gets the GPU: slow, but it must complete without a
+    timeout and give the single-process root."""
+    for rank, root, loss, pdig in _run(2, True, combine="p2p", sync="device"):
+        assert root == tiny_single[1], f"device-flag p2p rank {rank}: step root differs"
+        assert pdig == tiny_single[3]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_full_gpt2_step_root_p2p_bucketed(world, full_single):
+    """full GPT-2 124M step with the per-layer bucketed peer-memory combine (13 buckets
+    overlapping the backward on a comm stream) at G = 2, 4: the G = 1 root"""
+    for rank, root, loss, pdig in _run(world, False, combine="p2p"):
+        assert root == full_single[1], f"bucketed p2p G={world} rank {rank}: full step root differs"
+        assert pdig == full_single[3]
 
 
 # ---------------------------------------------------------------- config 2: M-split GEMM

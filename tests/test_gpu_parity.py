@@ -137,6 +137,86 @@ def test_gemm_tn_kernel_batched_and_strided_output():
         assert np.all(blk[:, N:].view(np.uint32) == 0), "wrote outside the C tile"
 
 
+# ------------------------------------------------------------------ causal structure (f4)
+def test_gemm_causal_skip_scores():
+    # causal 1: tiles strictly above the diagonal are not written; every other output
+    # equals the full R-GEMM (scores with the 1/sqrt(hd) epilogue, batched heads)
+    T, hd, H = 384, 64, 3
+    q = synth.uniform(51, (H, T, hd))
+    k = synth.uniform(52, (H, T, hd))
+    S = torch.full((H, T, T), float("nan"), device="cuda")
+    R.repops_gemm_strided_batched(dev(q), dev(k), S, M=T, N=T, K=hd, lda=hd, ldb=hd, ldc=T, sA=(T * hd, 0),
+                                  sB=(T * hd, 0), sC=(T * T, 0), batch=(H, 1), transB=True, epi=R.EPI_SCALE,
+                                  scale=0.125, causal=1)
+    got = host(S)
+    for h in range(H):
+        ref = oracle.gemm(q[h], k[h], transB=True, epi=2, scale=0.125)
+        low = np.tril(np.ones((T, T), bool))
+        assert_bits(got[h][low], ref[low], f"causal scores head {h}")
+    # the causal softmax of the partially written scores equals the softmax of the full ones
+    P = host(R.repops_softmax(S.view(-1, T), causal=True)).reshape(H, T, T)
+    for h in range(H):
+        assert_bits(P[h], oracle.softmax(oracle.gemm(q[h], k[h], transB=True, epi=2, scale=0.125), causal=True),
+                    f"softmax after skipped tiles, head {h}")
+
+
+def _causal_pv_case(T, hd, H, seed, specials):
+    P = np.tril(synth.uniform(seed, (H, T, T)) * np.float32(0.5) + np.float32(0.5)).astype(np.float32)
+    P[:, np.triu_indices(T, 1)[0], np.triu_indices(T, 1)[1]] = 0.0  # exactly +0 above the diagonal
+    V = synth.uniform(seed + 1, (H, T, hd))
+    if specials:
+        # rows whose whole valid fold underflows to -0: p = 2^-149, v < 0 -> fma gives -0
+        for r in (0, 5, 64, 70):
+            P[0, r, :r + 1] = np.float32(2.0 ** -149)
+            V[0, :r + 1, :8] = -np.abs(V[0, :r + 1, :8])
+        # after the tile rows: negative-only columns keep -0, any +v / +0 turns -0 into +0
+        V[0, 128:, 0:4] = -np.abs(V[0, 128:, 0:4]) - np.float32(0.25)
+        V[0, 200, 4] = 0.0                      # a +0 in the skipped range
+        V[0, 300, 5] = -0.0                     # a -0 (sign bit set): keeps -0
+        V[1, 250, 6] = np.inf                   # non-finite in the skipped range -> NaN
+        V[1, 260, 7] = np.nan
+    return P, V
+
+
+@pytest.mark.parametrize("specials", [False, True])
+def test_gemm_causal_probabilities_exact(specials):
+    # causal 2: each tile's K fold stops at its last row; the skipped fma(+0, v, acc) terms
+    # are applied from the suffix flags -- bits equal the oracle's full K fold, including
+    # -0 accumulators and non-finite V in the skipped range
+    T, hd, H = 320, 64, 2
+    P, V = _causal_pv_case(T, hd, H, 61, specials)
+    Vd = dev(V)
+    fl = R.repops_causal_suffix_flags(Vd, T, hd, hd, (T * hd, 0), (H, 1))
+    for cfg in (None,):
+        O = torch.empty((H, T, hd), device="cuda")
+        R.repops_gemm_strided_batched(dev(P), Vd, O, M=T, N=hd, K=T, lda=T, ldb=hd, ldc=hd, sA=(T * T, 0),
+                                      sB=(T * hd, 0), sC=(T * hd, 0), batch=(H, 1), causal=2, kflags=fl, ldf=hd,
+                                      sF=((T + 1) * hd, 0))
+        got = host(O)
+        for h in range(H):
+            assert_bits(got[h], oracle.gemm(P[h], V[h]), f"causal PV head {h} specials={specials}")
+    if specials:
+        ref0 = oracle.gemm(P[0], V[0])
+        assert np.any(ref0.view(np.uint32) == 0x80000000)       # the -0 case is exercised
+        assert np.isnan(oracle.gemm(P[1], V[1])).any()          # and the non-finite case
+
+
+def test_causal_suffix_flags_definition():
+    K, N = 77, 9
+    B = synth.uniform(71, (K, N))
+    B[10, 0] = np.inf
+    B[:, 1] = -np.abs(B[:, 1]) - np.float32(0.5)
+    B[40, 2] = -0.0
+    B[:, 3] = 0.0
+    B[60, 4] = np.nan
+    got = host(R.repops_causal_suffix_flags(dev(B), K, N, N, (0, 0), (1, 1)))[0]
+    u = B.view(np.uint32)
+    for k in range(K + 1):
+        nf = ((u[k:] & 0x7F800000) == 0x7F800000).any(axis=0)
+        neg = (u[k:] >> 31).astype(bool).all(axis=0) if k < K else np.ones(N, bool)
+        assert np.array_equal(got[k], nf.astype(np.uint8) | (neg.astype(np.uint8) << 1)), k
+
+
 def _subnormal_operands(M, N, K, tag):
     """operands whose products and partial sums fall in the binary32 subnormal range
     (|x| < 2^-126), so every fma in the K fold rounds with gradual underflow (R9)"""
