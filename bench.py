@@ -449,8 +449,11 @@ def cublas_context():
     shapes = [("NN", n, n, n, 1) for n in SIZES] + GPT2_GEMM_SHAPES
     for lay, M, N, K, b in shapes:
         ta, tb = lay[0] == "T", lay[1] == "T"
-        A = torch.rand((b, K, M) if ta else (b, M, K), device="cuda", generator=gen) * 2 - 1
-        B = torch.rand((b, N, K) if tb else (b, K, N), device="cuda", generator=gen) * 2 - 1
+        # rows padded to a multiple of 4 floats, as the step's buffers are (e.g. the logits'
+        # ld 50304 for V = 50257): 16-byte aligned rows for both libraries
+        pad = lambda r, c: (torch.rand((b, r, (c + 3) // 4 * 4), device="cuda", generator=gen) * 2 - 1)[:, :, :c]  # noqa: E731
+        A = pad(K, M) if ta else pad(M, K)
+        B = pad(N, K) if tb else pad(K, N)
         Cr = torch.empty((b, M, N), device="cuda")
         opA = A.transpose(1, 2) if ta else A
         opB = B.transpose(1, 2) if tb else B
@@ -459,8 +462,8 @@ def cublas_context():
             lib = lambda: torch.mm(opA[0], opB[0])  # noqa: E731
         else:
             rep = lambda: R.repops_gemm_strided_batched(  # noqa: E731
-                A, B, Cr, M=M, N=N, K=K, lda=A.shape[2], ldb=B.shape[2], ldc=N, sA=(A.shape[1] * A.shape[2], 0),
-                sB=(B.shape[1] * B.shape[2], 0), sC=(M * N, 0), batch=(b, 1), transA=ta, transB=tb)
+                A, B, Cr, M=M, N=N, K=K, lda=A.stride(1), ldb=B.stride(1), ldc=N, sA=(A.stride(0), 0),
+                sB=(B.stride(0), 0), sC=(M * N, 0), batch=(b, 1), transA=ta, transB=tb)
             lib = lambda: torch.bmm(opA, opB)  # noqa: E731
         t_rep, t_lib = ms(rep), ms(lib)
         Cl = lib()

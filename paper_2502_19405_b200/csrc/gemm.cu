@@ -458,7 +458,7 @@ cudaError_t launch_cfg(const GemmParams &p, cudaStream_t s) {
 //   10..14: 6, 5, 3, 1, 4 with XP (A stored M x K transposed in shared memory)
 //   15..18: stage / BK variants of 10; 19: 16 x 32 latency tiles
 //   20, 21: gemm_tn.cu 128 x 128 full-tile A^T kernel (BK 32 / 16)
-int gemm_num_cfgs() { return 22; }
+int gemm_num_cfgs() { return 24; }
 std::atomic<int> g_gemm_smem_floor{0};
 
 cudaError_t gemm_launch(const GemmParams &p, cudaStream_t s, int force_cfg) {
@@ -466,12 +466,12 @@ cudaError_t gemm_launch(const GemmParams &p, cudaStream_t s, int force_cfg) {
     if (p.batch0 * p.batch1 > 65535) return cudaErrorInvalidValue;
     int cfg = force_cfg;
     if (cfg < 0 && gemm_tn_eligible(p) && p.M * p.N * p.batch0 * p.batch1 > (int64_t)ro_host::num_sms() * 16 * 32 * 4) {
-        // A^T-stored full-tile problems: the 128 x 128 x 32 kernel of gemm_tn.cu against the
-        // 64 x 128 and 128 x 64 tiles here.  Cost = tiles on the busiest SM x tile work / rate
+        // A^T-stored problems: gemm_tn.cu's 128 x 128 (cfg 20) and 64 x 128 (cfg 22) tiles and
+        // the 128 x 64 tiles here.  Cost = tiles on the busiest SM x tile work / rate
         // (measured on B200: one or two CTAs of either kernel nearly saturate an SM, so the
         // SM-count quantisation of the tile count is what decides; tools/gemm_tune.py)
         struct C { int id, bm, bn; double rate; };
-        static const C cand[] = {{20, 128, 128, 66.9}, {6, 64, 128, 64.1}, {5, 128, 64, 60.0}};
+        static const C cand[] = {{20, 128, 128, 66.9}, {22, 64, 128, 66.0}, {5, 128, 64, 60.0}};
         const int64_t nb = p.batch0 * p.batch1;
         const int64_t sms = ro_host::num_sms();
         double best = 1e300;
@@ -534,6 +534,11 @@ cudaError_t gemm_launch(const GemmParams &p, cudaStream_t s, int force_cfg) {
         case 21:
             if (gemm_tn_eligible(p)) return gemm_tn_launch(p, s, cfg == 20 ? 32 : 16);
             return launch_cfg<128, 128, 16, 8, 16, 3, 2>(p, s);
+        // gemm_tn.cu 64 x 128 tiles (8 x 8 per thread, pairs along m, 3 CTAs / SM), BK 32 / 16
+        case 22:
+        case 23:
+            if (gemm_tn_eligible(p)) return gemm_tn_launch(p, s, cfg == 22 ? 6432 : 6416);
+            return launch_cfg<64, 128, 16, 8, 8, 3, 3>(p, s);
         default: return cudaErrorInvalidValue;
     }
 }

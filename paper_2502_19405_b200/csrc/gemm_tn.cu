@@ -29,8 +29,7 @@ namespace {
 
 using ro::canon;
 
-constexpr int BM = 128, BN = 128, THREADS = 128;
-constexpr int TM = 8, TN = 16;              // outputs per thread
+constexpr int THREADS = 128;                // 4 warps, each 4 (m) x 8 (n) lanes
 constexpr int GROUP_M = 16;                 // row tiles per rasterisation group
 
 RO_DEV void cp16(uint32_t dst, const float *src) {
@@ -44,15 +43,23 @@ RO_DEV void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 RO_DEV void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-template <int STAGES, int BK>
-__global__ void __launch_bounds__(THREADS, 2) gemm_tn_kernel(GemmParams p) {
+// BM x BN CTA tile, warps WM (m) x WN (n) with WM * WN = 4: thread (ty, tx) owns rows
+// ty*4 + g*4*TYN + {0..3} (g < GM) and columns tx*4 + h*4*TXN + {0..3} (h < GN)
+template <int BM, int BN, int WM, int STAGES, int BK, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) gemm_tn_kernel(GemmParams p) {
+    constexpr int WN = 4 / WM, TYN = 4 * WM, TXN = 8 * WN;
+    constexpr int TM = BM / TYN, TN = BN / TXN, GM = TM / 4, GN = TN / 4;
+    static_assert(TM % 4 == 0 && TN % 4 == 0 && WM * WN == 4, "gemm_tn tile geometry");
     constexpr int A_WORDS = BK * BM, B_WORDS = BK * BN, STAGE_WORDS = A_WORDS + B_WORDS;
-    constexpr int NQ = BK / 4;  // 16-byte chunks per thread per operand and K tile
+    constexpr int CA = BM / 4, CB = BN / 4;                  // 16-byte chunks per tile row
+    constexpr int RA = THREADS / CA, RB = THREADS / CB;      // tile rows per chunk step
+    constexpr int NQA = BK * CA / THREADS, NQB = BK * CB / THREADS;
+    static_assert(THREADS % CA == 0 && THREADS % CB == 0 && NQA >= 1 && NQB >= 1, "gemm_tn load geometry");
     extern __shared__ __align__(16) float smem[];
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
-    const int tx = lane & 7;                 // n: columns tx*4 + 32 h + {0..3}, h < 4
-    const int ty = warp * 4 + (lane >> 3);   // m: rows ty*4 + 64 g + {0..3}, g < 2
+    const int tx = (warp % WN) * 8 + (lane & 7);
+    const int ty = (warp / WN) * 4 + (lane >> 3);
 
     const int64_t tiles_m = (p.M + BM - 1) / BM, tiles_n = (p.N + BN - 1) / BN;
     const int64_t t = blockIdx.x;
@@ -67,49 +74,48 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_tn_kernel(GemmParams p) {
     const float *__restrict__ B = p.B + b0 * p.sB0 + b1 * p.sB1;
     float *__restrict__ Cp = p.C + b0 * p.sC0 + b1 * p.sC1;
 
-    // cp.async geometry: a K tile of A^T is 16 rows x 128 floats = 512 16-byte chunks,
-    // of B also 512: 4 chunks per thread each, rows r0 + 4q, column l0 (both operands)
-    const int r0 = tid >> 5, l0 = (tid & 31) * 4;
-    const float *ga = A + (int64_t)r0 * p.lda + m0 + l0;
-    const float *gb = B + (int64_t)r0 * p.ldb + n0 + l0;
-    const int64_t qa = 4 * p.lda, qb = 4 * p.ldb;          // 4 rows
+    // cp.async geometry: thread tid copies the 16-byte chunks at tile rows ra0 + RA q of
+    // A^T (column la0) and rb0 + RB q of B (column lb0)
+    const int ra0 = tid / CA, la0 = (tid % CA) * 4, rb0 = tid / CB, lb0 = (tid % CB) * 4;
+    const float *ga = A + (int64_t)ra0 * p.lda + m0 + la0;
+    const float *gb = B + (int64_t)rb0 * p.ldb + n0 + lb0;
+    const int64_t qa = RA * p.lda, qb = RB * p.ldb;        // RA / RB rows
     const int64_t ta = BK * p.lda, tb = BK * p.ldb;        // one K tile
     const uint32_t s_base = (uint32_t)__cvta_generic_to_shared(smem);
-    const uint32_t s_off = (uint32_t)((r0 * BM + l0) * 4);
+    const uint32_t sa_off = (uint32_t)((ra0 * BM + la0) * 4), sb_off = (uint32_t)((rb0 * BN + lb0) * 4);
     // edge tiles (ragged M / N) and a ragged last K tile take zero-filled bounded copies;
     // the zeros are never used by the k loop (it stops at K) or stored (rows >= M, cols >= N)
     const bool edge = m0 + BM > p.M || n0 + BN > p.N;
-    const int a_bytes = (int)max((int64_t)0, min((int64_t)16, (p.M - m0 - l0) * 4));
-    const int b_bytes = (int)max((int64_t)0, min((int64_t)16, (p.N - n0 - l0) * 4));
+    const int a_bytes = (int)max((int64_t)0, min((int64_t)16, (p.M - m0 - la0) * 4));
+    const int b_bytes = (int)max((int64_t)0, min((int64_t)16, (p.N - n0 - lb0) * 4));
     const int64_t kfull = p.K / BK;  // full K tiles (a ragged remainder follows them)
     auto issue = [&](int slot, int64_t kt) {
-        const uint32_t sa = s_base + (uint32_t)(slot * STAGE_WORDS * 4) + s_off;
-        const uint32_t sb = sa + A_WORDS * 4;
+        const uint32_t st = s_base + (uint32_t)(slot * STAGE_WORDS * 4);
+        const uint32_t sa = st + sa_off, sb = st + A_WORDS * 4 + sb_off;
         const float *a = ga, *b = gb;
         if (!edge && kt < kfull) {
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-                cp16(sa + q * 4 * BM * 4, a);
-                cp16(sb + q * 4 * BN * 4, b);
-                a += qa;
-                b += qb;
-            }
-        } else {
-            const int64_t kvalid = p.K - kt * BK - r0;  // rows r0 + 4q < kvalid are in range
+            for (int q = 0; q < NQA; ++q, a += qa) cp16(sa + q * RA * BM * 4, a);
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-                const bool kin = 4 * q < kvalid;
-                cp16z(sa + q * 4 * BM * 4, kin && a_bytes ? a : A, kin ? a_bytes : 0);
-                cp16z(sb + q * 4 * BN * 4, kin && b_bytes ? b : B, kin ? b_bytes : 0);
-                a += qa;
-                b += qb;
+            for (int q = 0; q < NQB; ++q, b += qb) cp16(sb + q * RB * BN * 4, b);
+        } else {
+            const int64_t kva = p.K - kt * BK - ra0, kvb = p.K - kt * BK - rb0;  // rows still in range
+#pragma unroll
+            for (int q = 0; q < NQA; ++q, a += qa) {
+                const bool kin = RA * q < kva;
+                cp16z(sa + q * RA * BM * 4, kin && a_bytes ? a : A, kin ? a_bytes : 0);
+            }
+#pragma unroll
+            for (int q = 0; q < NQB; ++q, b += qb) {
+                const bool kin = RB * q < kvb;
+                cp16z(sb + q * RB * BN * 4, kin && b_bytes ? b : B, kin ? b_bytes : 0);
             }
         }
         ga += ta;
         gb += tb;
     };
 
-    float2 acc[TM / 2][TN];
+    float2 acc[TM / 2][TN];  // pairs of rows (m, m + 1) x columns
 #pragma unroll
     for (int i = 0; i < TM / 2; ++i)
 #pragma unroll
@@ -122,27 +128,33 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_tn_kernel(GemmParams p) {
         cp_commit();
     }
 
-    // fragment reads: A pairs at rows ty*4 + 64 g, B values at cols tx*4 + 32 h
-    float4 fa[1][2], fb[1][4];
+    // fragment reads: A pairs at rows ty*4 + 4 TYN g, B values at cols tx*4 + 4 TXN h
+    float4 fa[1][GM], fb[1][GN];
     auto frag = [&](int buf, const float *st, int k) {
         const float *As = st + k * BM + ty * 4;
         const float *Bs = st + A_WORDS + k * BN + tx * 4;
 #pragma unroll
-        for (int g = 0; g < 2; ++g) fa[buf][g] = *reinterpret_cast<const float4 *>(As + 64 * g);
+        for (int g = 0; g < GM; ++g) fa[buf][g] = *reinterpret_cast<const float4 *>(As + 4 * TYN * g);
 #pragma unroll
-        for (int h = 0; h < 4; ++h) fb[buf][h] = *reinterpret_cast<const float4 *>(Bs + 32 * h);
+        for (int h = 0; h < GN; ++h) fb[buf][h] = *reinterpret_cast<const float4 *>(Bs + 4 * TXN * h);
     };
     auto mma = [&](int buf) {
-        const float b[16] = {fb[buf][0].x, fb[buf][0].y, fb[buf][0].z, fb[buf][0].w,
-                             fb[buf][1].x, fb[buf][1].y, fb[buf][1].z, fb[buf][1].w,
-                             fb[buf][2].x, fb[buf][2].y, fb[buf][2].z, fb[buf][2].w,
-                             fb[buf][3].x, fb[buf][3].y, fb[buf][3].z, fb[buf][3].w};
-        const float2 a[4] = {make_float2(fa[buf][0].x, fa[buf][0].y), make_float2(fa[buf][0].z, fa[buf][0].w),
-                             make_float2(fa[buf][1].x, fa[buf][1].y), make_float2(fa[buf][1].z, fa[buf][1].w)};
+        float b[TN];
+        float2 a[TM / 2];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int h = 0; h < GN; ++h) {
+            b[4 * h] = fb[buf][h].x; b[4 * h + 1] = fb[buf][h].y;
+            b[4 * h + 2] = fb[buf][h].z; b[4 * h + 3] = fb[buf][h].w;
+        }
 #pragma unroll
-            for (int j = 0; j < 16; ++j) acc[i][j] = __ffma2_rn(a[i], make_float2(b[j], b[j]), acc[i][j]);
+        for (int g = 0; g < GM; ++g) {
+            a[2 * g] = make_float2(fa[buf][g].x, fa[buf][g].y);
+            a[2 * g + 1] = make_float2(fa[buf][g].z, fa[buf][g].w);
+        }
+#pragma unroll
+        for (int i = 0; i < TM / 2; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) acc[i][j] = __ffma2_rn(a[i], make_float2(b[j], b[j]), acc[i][j]);
     };
 
     cp_wait<STAGES - 1>();
@@ -173,17 +185,17 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_tn_kernel(GemmParams p) {
     }
     cp_wait<0>();
 
-    // epilogue (R3): epi(acc) once, NaN canonicalised (R10); rows ty*4 + 64 g + r
+    // epilogue (R3): epi(acc) once, NaN canonicalised (R10); rows ty*4 + 4 TYN g + r
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < TM / 2; ++i) {
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
-            const int64_t m = m0 + (i >> 1) * 64 + ty * 4 + (i & 1) * 2 + half;
+            const int64_t m = m0 + (i >> 1) * 4 * TYN + ty * 4 + (i & 1) * 2 + half;
             if (m >= p.M) continue;
             float *crow = Cp + m * p.ldc;
 #pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                const int64_t n = n0 + 32 * h + tx * 4;
+            for (int h = 0; h < GN; ++h) {
+                const int64_t n = n0 + 4 * TXN * h + tx * 4;
                 float v[4];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
@@ -204,12 +216,12 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_tn_kernel(GemmParams p) {
     }
 }
 
-template <int STAGES, int BK>
+template <int BM, int BN, int WM, int STAGES, int BK, int MINB>
 cudaError_t launch_tn(const GemmParams &p, cudaStream_t s) {
     size_t smem = (size_t)STAGES * BK * (BM + BN) * sizeof(float);
     const size_t floor_bytes = (size_t)g_gemm_smem_floor.load(std::memory_order_relaxed);
     if (floor_bytes > smem) smem = floor_bytes;  // occupancy experiments only (tools/overlap_probe.py)
-    auto kern = gemm_tn_kernel<STAGES, BK>;
+    auto kern = gemm_tn_kernel<BM, BN, WM, STAGES, BK, MINB>;
     static size_t attr = 0;
     if (smem > attr) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -229,9 +241,16 @@ bool gemm_tn_eligible(const GemmParams &p) {
     return p.transA && !p.transB && p.vecA && p.vecB && p.K > 0 && p.causal == 0;
 }
 
-cudaError_t gemm_tn_launch(const GemmParams &p, cudaStream_t s, int bk) {
+cudaError_t gemm_tn_launch(const GemmParams &p, cudaStream_t s, int variant) {
     if (!gemm_tn_eligible(p)) return cudaErrorInvalidValue;
-    // 3-stage ring: 3 x 32 KB (BK 32) or 3 x 16 KB (BK 16) of shared memory, 2 CTAs / SM
-    if (bk == 32) return launch_tn<3, 32>(p, s);
-    return launch_tn<3, 16>(p, s);
+    // 3-stage rings.  128 x 128 (warps 4 x 1, 8 x 16 per thread, 2 CTAs / SM):
+    // 3 x 32 KB (BK 32) / 3 x 16 KB (BK 16); 64 x 128 (warps 2 x 2, 8 x 8 per thread,
+    // 3 CTAs / SM): 3 x 24 KB / 3 x 12 KB
+    switch (variant) {
+        case 32: return launch_tn<128, 128, 4, 3, 32, 2>(p, s);
+        case 16: return launch_tn<128, 128, 4, 3, 16, 2>(p, s);
+        case 6432: return launch_tn<64, 128, 2, 3, 32, 3>(p, s);
+        case 6416: return launch_tn<64, 128, 2, 3, 16, 3>(p, s);
+        default: return cudaErrorInvalidValue;
+    }
 }

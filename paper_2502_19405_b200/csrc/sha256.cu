@@ -191,6 +191,17 @@ RO_DEV void hash_leaf(const uint8_t *__restrict__ data, int64_t len, uint32_t st
             prev = D[15];
             compress_m<MODE>(st, w);
         }
+        if (len == 4096) {
+            // a full chunk's final block: its last data byte, 0x80, zeros, and the message
+            // length 4097 * 8 bits -- the next "memory word" is the bytes 80 00 00 00
+            uint32_t w[16];
+            w[0] = __byte_perm(prev, 0x00000080u, 0x3456);
+#pragma unroll
+            for (int i = 1; i < 15; ++i) w[i] = 0;
+            w[15] = 4097u * 8u;
+            compress_m<MODE>(st, w);
+            return;
+        }
     }
     for (; blk < nblk; ++blk) {
         uint32_t w[16];

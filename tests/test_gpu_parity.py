@@ -95,7 +95,7 @@ def test_gemm_tn_kernel_full_tiles(K, epi):
     At = np.ascontiguousarray(A.T)
     bias = synth.uniform(31, N)
     ref = oracle.gemm(At, B, transA=True, epi=epi, bias=bias if epi == 1 else None, scale=0.375)
-    for cfg in (None, 20, 21):
+    for cfg in (None, 20, 21, 22, 23):
         got = R.repops_gemm(dev(At), dev(B), transA=True, epi=epi, bias=dev(bias) if epi == 1 else None,
                             scale=0.375, cfg=cfg)
         assert_bits(host(got), ref, f"gemm_tn K{K} epi{epi} cfg{cfg}")
@@ -115,7 +115,7 @@ def test_gemm_tn_kernel_ragged_edges(M, N, K):
     Bb = np.full((K, ldb), np.nan, np.float32)
     Bb[:, :N] = B
     ref = oracle.gemm(At, B, transA=True)
-    for cfg in (None, 20, 21):
+    for cfg in (None, 20, 21, 22, 23):
         got = R.repops_gemm(dev(Ab)[:, :M], dev(Bb)[:, :N], transA=True, cfg=cfg)
         assert_bits(host(got), ref, f"gemm_tn ragged {M}x{N}x{K} cfg{cfg}")
 
@@ -165,14 +165,13 @@ def _causal_pv_case(T, hd, H, seed, specials):
     P[:, np.triu_indices(T, 1)[0], np.triu_indices(T, 1)[1]] = 0.0  # exactly +0 above the diagonal
     V = synth.uniform(seed + 1, (H, T, hd))
     if specials:
-        # rows whose whole valid fold underflows to -0: p = 2^-149, v < 0 -> fma gives -0
+        # columns 0..7 of head 0: every V negative with |v| < 1/2, and rows whose probabilities
+        # are 2^-149: each fma(2^-149, v, -0) rounds to -0, so those accumulators are -0
+        V[0, :, :8] = (-np.abs(V[0, :, :8]) * np.float32(0.49)).astype(np.float32)
         for r in (0, 5, 64, 70):
             P[0, r, :r + 1] = np.float32(2.0 ** -149)
-            V[0, :r + 1, :8] = -np.abs(V[0, :r + 1, :8])
-        # after the tile rows: negative-only columns keep -0, any +v / +0 turns -0 into +0
-        V[0, 128:, 0:4] = -np.abs(V[0, 128:, 0:4]) - np.float32(0.25)
-        V[0, 200, 4] = 0.0                      # a +0 in the skipped range
-        V[0, 300, 5] = -0.0                     # a -0 (sign bit set): keeps -0
+        V[0, 200, 4] = 0.0                      # a +0 in the skipped range: -0 + +0 -> +0
+        V[0, 300, 5] = -0.0                     # a -0 (sign bit set): -0 survives
         V[1, 250, 6] = np.inf                   # non-finite in the skipped range -> NaN
         V[1, 260, 7] = np.nan
     return P, V
