@@ -458,7 +458,7 @@ cudaError_t launch_cfg(const GemmParams &p, cudaStream_t s) {
 //   10..14: 6, 5, 3, 1, 4 with XP (A stored M x K transposed in shared memory)
 //   15..18: stage / BK variants of 10; 19: 16 x 32 latency tiles
 //   20, 21: gemm_tn.cu 128 x 128 full-tile A^T kernel (BK 32 / 16)
-int gemm_num_cfgs() { return 24; }
+int gemm_num_cfgs() { return 25; }
 std::atomic<int> g_gemm_smem_floor{0};
 
 cudaError_t gemm_launch(const GemmParams &p, cudaStream_t s, int force_cfg) {
@@ -539,6 +539,10 @@ cudaError_t gemm_launch(const GemmParams &p, cudaStream_t s, int force_cfg) {
         case 23:
             if (gemm_tn_eligible(p)) return gemm_tn_launch(p, s, cfg == 22 ? 6432 : 6416);
             return launch_cfg<64, 128, 16, 8, 8, 3, 3>(p, s);
+        // gemm_tn.cu 64 x 64 tiles (8 x 4 per thread, 4 CTAs / SM): N = 64 problems (attention)
+        case 24:
+            if (gemm_tn_eligible(p)) return gemm_tn_launch(p, s, 646432);
+            return launch_cfg<64, 64, 16, 8, 4, 3, 2>(p, s);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -251,6 +251,7 @@ cudaError_t gemm_tn_launch(const GemmParams &p, cudaStream_t s, int variant) {
         case 16: return launch_tn<128, 128, 4, 3, 16, 2>(p, s);
         case 6432: return launch_tn<64, 128, 2, 3, 32, 3>(p, s);
         case 6416: return launch_tn<64, 128, 2, 3, 16, 3>(p, s);
+        case 646432: return launch_tn<64, 64, 2, 3, 32, 4>(p, s);
         default: return cudaErrorInvalidValue;
     }
 }
