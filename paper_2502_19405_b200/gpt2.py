@@ -49,7 +49,7 @@ OP = dict(PARAM_IN=1, TOKENS_IN=2, EMBED=3, LAYERNORM=4, LINEAR=5, ATTN_SCORES=6
           RESIDUAL=9, GELU=10, LM_HEAD=11, CROSS_ENTROPY=12,
           LM_DGRAD=20, LM_WGRAD=21, LN_BWD=22, LN_PARAM_GRAD=23, LINEAR_DGRAD=24, LINEAR_WGRAD=25,
           BIAS_GRAD=26, GELU_BWD=27, ATTN_DP=28, SOFTMAX_BWD=29, ATTN_DQKV=30, EMBED_BWD=31,
-          TREE_SUM=40, ADAMW=41)
+          TREE_SUM=40, ADAMW=41, ATTENTION=13, ATTENTION_BWD=32)
 # attribute keys
 AK = dict(layer=1, eps=2, scale=3, causal=4, lr=5, beta1=6, beta2=7, adam_eps=8, wd=9, step=10, decay=11,
           which=12)
@@ -119,11 +119,20 @@ class GPT2Step:
     """Static program of one training step for the shards owned by this rank."""
 
     def __init__(self, cfg: GPT2Config, rank: int = 0, world: int = 1, device="cuda", pg=None,
-                 structure_only=False, combine: str = "sliced", p2p_sync: str = "device"):
+                 structure_only=False, combine: str = "sliced", p2p_sync: str = "device", attn_nodes: str = "operator"):
         """structure_only: build the node graph / slot layout on the 'meta' device
         (no memory, no kernels) -- used by the CPU tests of the host logic."""
         assert cfg.shards % world == 0
         self.cfg, self.rank, self.world, self.pg = cfg, rank, world, pg
+        # graph granularity of attention (reading R29): "operator" = one ATTENTION node
+        # (qkv -> att) and one ATTENTION_BWD node (qkv, datt -> dqkv), as PyTorch's
+        # scaled_dot_product_attention and its backward are single graph nodes; the scores,
+        # probabilities and their gradients are operator-internal (recomputable from qkv)
+        # and not committed.  "primitive" = round 1's per-primitive nodes (scores, softmax,
+        # PV, dP, softmax backward, dQKV), each output committed.
+        if attn_nodes not in ("operator", "primitive"):
+            raise ValueError(f"unknown attn_nodes {attn_nodes!r}")
+        self.attn_op = attn_nodes == "operator"
         self.structure_only = structure_only
         self.dev = torch.device("meta" if structure_only else device)
         self.s0, self.S_loc = shard_block(rank, world, cfg.shards)
@@ -446,13 +455,19 @@ class GPT2Step:
             t_qkv = T_(pre + "qkv", V(a["qkv"], T), s)
             self.node(OP["LINEAR"], s, attrs(layer=l, which=1), [t_ln1, P_[p + "attn.w"][0], P_[p + "attn.b"][0]],
                       [t_qkv], pre + "qkv")
-            t_S = T_(pre + "scores", V(a["S"], H * T), s)
-            self.node(OP["ATTN_SCORES"], s, attrs(layer=l, scale=float(1.0 / np.sqrt(hd))), [t_qkv], [t_S],
-                      pre + "scores")
-            t_P = T_(pre + "probs", V(a["P"], H * T), s)
-            self.node(OP["SOFTMAX"], s, attrs(layer=l, causal=1), [t_S], [t_P], pre + "softmax")
-            t_att = T_(pre + "att", V(a["att"], T), s)
-            self.node(OP["ATTN_PV"], s, attrs(layer=l), [t_P, t_qkv], [t_att], pre + "pv")
+            if self.attn_op:
+                t_P = None
+                t_att = T_(pre + "att", V(a["att"], T), s)
+                self.node(OP["ATTENTION"], s, attrs(layer=l, scale=float(1.0 / np.sqrt(hd)), causal=1), [t_qkv],
+                          [t_att], pre + "attention", label=f"h{l}/pv")
+            else:
+                t_S = T_(pre + "scores", V(a["S"], H * T), s)
+                self.node(OP["ATTN_SCORES"], s, attrs(layer=l, scale=float(1.0 / np.sqrt(hd))), [t_qkv], [t_S],
+                          pre + "scores")
+                t_P = T_(pre + "probs", V(a["P"], H * T), s)
+                self.node(OP["SOFTMAX"], s, attrs(layer=l, causal=1), [t_S], [t_P], pre + "softmax")
+                t_att = T_(pre + "att", V(a["att"], T), s)
+                self.node(OP["ATTN_PV"], s, attrs(layer=l), [t_P, t_qkv], [t_att], pre + "pv")
             t_proj = T_(pre + "proj", V(a["proj"], T), s)
             self.node(OP["LINEAR"], s, attrs(layer=l, which=2), [t_att, P_[p + "proj.w"][0], P_[p + "proj.b"][0]],
                       [t_proj], pre + "proj")
@@ -687,14 +702,19 @@ class GPT2Step:
                       pre + "proj_wgrad")
             fg[p + "proj.b"] = T_(f"s{s}/grad/{p}proj.b", G_(p + "proj.b"), s)
             self.node(OP["BIAS_GRAD"], s, attrs(layer=l, which=2), [t_dxmid], [fg[p + "proj.b"]], pre + "proj_bgrad")
-            t_dP = T_(pre + "dP", V(g["dP"], H * T), s)
-            self.node(OP["ATTN_DP"], s, attrs(layer=l), [t_datt, ids["qkv"]], [t_dP], pre + "attn_dp")
-            t_dS = T_(pre + "dS", V(g["dS"], H * T), s)
-            self.node(OP["SOFTMAX_BWD"], s, attrs(layer=l, scale=float(1.0 / np.sqrt(hd))), [ids["P"], t_dP], [t_dS],
-                      pre + "softmax_bwd")
-            t_dqkv = T_(pre + "dqkv", V(g["dqkv"], T), s)
-            self.node(OP["ATTN_DQKV"], s, attrs(layer=l), [t_dS, ids["P"], t_datt, ids["qkv"]], [t_dqkv],
-                      pre + "attn_dqkv")
+            if self.attn_op:
+                t_dqkv = T_(pre + "dqkv", V(g["dqkv"], T), s)
+                self.node(OP["ATTENTION_BWD"], s, attrs(layer=l, scale=float(1.0 / np.sqrt(hd)), causal=1),
+                          [ids["qkv"], t_datt], [t_dqkv], pre + "attention_bwd", label=f"h{l}/attn_dqkv")
+            else:
+                t_dP = T_(pre + "dP", V(g["dP"], H * T), s)
+                self.node(OP["ATTN_DP"], s, attrs(layer=l), [t_datt, ids["qkv"]], [t_dP], pre + "attn_dp")
+                t_dS = T_(pre + "dS", V(g["dS"], H * T), s)
+                self.node(OP["SOFTMAX_BWD"], s, attrs(layer=l, scale=float(1.0 / np.sqrt(hd))), [ids["P"], t_dP],
+                          [t_dS], pre + "softmax_bwd")
+                t_dqkv = T_(pre + "dqkv", V(g["dqkv"], T), s)
+                self.node(OP["ATTN_DQKV"], s, attrs(layer=l), [t_dS, ids["P"], t_datt, ids["qkv"]], [t_dqkv],
+                          pre + "attn_dqkv")
             t_dln1 = T_(pre + "dln1", V(g["dln1"], T), s)
             self.node(OP["LINEAR_DGRAD"], s, attrs(layer=l, which=1), [t_dqkv, P_[p + "attn.w"][0]], [t_dln1],
                       pre + "qkv_dgrad")

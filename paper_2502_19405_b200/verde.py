@@ -373,6 +373,32 @@ def replay(st: GPT2Step, nd, x, step=None):
         repops_gemm_strided_batched(P, qkv, att, M=T, N=hd, K=T, lda=T, ldb=3 * d, ldc=d, sA=(0, T * T),
                                     sB=(0, hd), sC=(0, hd), batch=(1, H), offB=2 * d)
         return [att]
+    if op == OP["ATTENTION"]:      # R29: scores, causal softmax, PV as one operator
+        qkv = x[0]
+        S, P, att = E(H * T, T), E(H * T, T), E(T, d)
+        repops_gemm_strided_batched(qkv, qkv, S, M=T, N=T, K=hd, lda=3 * d, ldb=3 * d, ldc=T, sA=(0, hd),
+                                    sB=(0, hd), sC=(0, T * T), batch=(1, H), transB=True, epi=EPI_SCALE, scale=sc,
+                                    offB=d)
+        repops_softmax(S, causal=True, out=P)
+        repops_gemm_strided_batched(P, qkv, att, M=T, N=hd, K=T, lda=T, ldb=3 * d, ldc=d, sA=(0, T * T),
+                                    sB=(0, hd), sC=(0, hd), batch=(1, H), offB=2 * d)
+        return [att]
+    if op == OP["ATTENTION_BWD"]:  # recomputes the probabilities from qkv (operator-internal)
+        qkv, datt = x
+        S, P, dP = E(H * T, T), E(H * T, T), E(H * T, T)
+        repops_gemm_strided_batched(qkv, qkv, S, M=T, N=T, K=hd, lda=3 * d, ldb=3 * d, ldc=T, sA=(0, hd),
+                                    sB=(0, hd), sC=(0, T * T), batch=(1, H), transB=True, epi=EPI_SCALE, scale=sc,
+                                    offB=d)
+        repops_softmax(S, causal=True, out=P)
+        repops_gemm_strided_batched(datt, qkv, dP, M=T, N=T, K=hd, lda=d, ldb=3 * d, ldc=T, sA=(0, hd),
+                                    sB=(0, hd), sC=(0, T * T), batch=(1, H), transB=True, offB=2 * d)
+        dS = repops_softmax_backward(P, dP, scale=sc)
+        dq = E(T, 3 * d)
+        kw = dict(M=T, N=hd, K=T, lda=T, ldc=3 * d, sA=(0, T * T), sC=(0, hd), batch=(1, H))
+        repops_gemm_strided_batched(P, datt, dq, ldb=d, sB=(0, hd), transA=True, offC=2 * d, **kw)
+        repops_gemm_strided_batched(dS, qkv, dq, ldb=3 * d, sB=(0, hd), offB=d, **kw)
+        repops_gemm_strided_batched(dS, qkv, dq, ldb=3 * d, sB=(0, hd), transA=True, offC=d, **kw)
+        return [dq]
     if op == OP["RESIDUAL"]:
         return [repops_add(x[0], x[1])]
     if op == OP["GELU"]:

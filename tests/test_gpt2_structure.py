@@ -25,7 +25,8 @@ def ref_graph():
 def test_full_config_sizes(ref_graph):
     st = ref_graph
     assert st.P == 124_439_808  # GPT-2 small parameter count
-    assert len(st.nodes) == 3596
+    assert len(st.nodes) == 3212  # R29: one ATTENTION + one ATTENTION_BWD node per (shard, layer)
+    assert len(GPT2Step(GPT2Config(), structure_only=True, attn_nodes="primitive").nodes) == 3596
     assert st.n_slots == st.rep_slots + 8 * st.shard_slots
 
 

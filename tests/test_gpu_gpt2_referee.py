@@ -53,6 +53,8 @@ def full():
     def digest(name):
         return table[by_name[name][1].slot].tobytes()
 
+    get.names = by_name
+
     specs = synth.gpt2_param_specs(cfg.n_layer, cfg.d, cfg.ffn, cfg.vocab, cfg.n_pos)
     W = {name: synth.gpt2_param(name, shape, kind, cfg.seed) for name, shape, kind in specs}
     return cfg, st, get, digest, W, specs
@@ -85,11 +87,23 @@ def test_block_forward_every_node(full):
     x = get(f"s{s}/x{l}")
     assert digest(f"s{s}/x{l}") == oracle.commit_tensor(x)  # the agreed input
     ref = ostep.layer_forward(W, l, x, cfg)
+    checked = 0
     for k, v in ref.items():
         name = f"s{s}/x{l + 1}" if k == "x_next" else f"s{s}/h{l}/{k}"
+        if name not in get.names:  # scores / probabilities: operator-internal under R29 (below)
+            assert k in ("scores", "probs") and st.attn_op, name
+            continue
+        checked += 1
         got = get(name)
         same_bits(got, v, name)
         assert digest(name) == oracle.commit_tensor(np.ascontiguousarray(v).reshape(got.shape)), f"digest {name}"
+    assert checked >= 14
+    # the attention operator's internal scores / probabilities (scratch the backward reuses)
+    # are kernel outputs too: the shard's rows of the layer's S and P buffers
+    H, T = cfg.n_head, cfg.seq
+    sl = slice(s * H * T, (s + 1) * H * T)
+    same_bits(st.act[l]["S"][sl].cpu().numpy(), ref["scores"], "internal scores")
+    same_bits(st.act[l]["P"][sl].cpu().numpy(), ref["probs"], "internal probabilities")
 
 
 def test_block_backward_every_node(full):
@@ -97,12 +111,26 @@ def test_block_backward_every_node(full):
     s, l = SHARD, LAYER
     pre = f"s{s}/h{l}/"
     x = get(f"s{s}/x{l}")
-    saved = {k: get(pre + k) for k in ("ln1", "mu1", "rs1", "qkv", "probs", "att", "xmid", "ln2", "mu2", "rs2",
-                                       "fc", "gelu")}
+    saved = {k: get(pre + k) for k in ("ln1", "mu1", "rs1", "qkv", "att", "xmid", "ln2", "mu2", "rs2", "fc",
+                                       "gelu")}
+    # the probabilities: the operator recomputes them from qkv; the oracle does the same
+    H, T, hd, d = cfg.n_head, cfg.seq, cfg.hd, cfg.d
+    sc = float(np.float32(1.0 / np.sqrt(hd)))
+    q = saved["qkv"]
+    saved["probs"] = np.concatenate([
+        oracle.softmax(oracle.gemm(np.ascontiguousarray(q[:, h * hd:(h + 1) * hd]),
+                                   np.ascontiguousarray(q[:, d + h * hd:d + (h + 1) * hd]), transB=True, epi=2,
+                                   scale=sc), causal=True) for h in range(H)])
     dout = get(f"s{s}/dx{l + 1}")
     t, gr = ostep.layer_backward(W, l, x, saved, dout, cfg)
     for k, v in t.items():
         name = f"s{s}/dx{l}" if k == "dx" else pre + k
+        if name not in get.names:  # dP / dS: internal to the ATTENTION_BWD operator (R29)
+            assert k in ("dP", "dS") and st.attn_op, name
+            H, T = cfg.n_head, cfg.seq
+            buf = st.grad_act[l][k][s * H * T:(s + 1) * H * T].cpu().numpy()
+            same_bits(buf, v, f"internal {k}")
+            continue
         got = get(name)
         same_bits(got, v, name)
         assert digest(name) == oracle.commit_tensor(np.ascontiguousarray(v).reshape(got.shape)), f"digest {name}"

@@ -63,6 +63,26 @@ def _oracle_replay(cfg, op, xs):
     if op == OP["SOFTMAX"]:
         H, T = cfg.n_head, cfg.seq
         return [np.concatenate([oracle.softmax(xs[0][h * T:(h + 1) * T], causal=True) for h in range(H)])]
+    if op in (OP["ATTENTION"], OP["ATTENTION_BWD"]):
+        H, T, d = cfg.n_head, cfg.seq, cfg.d
+        hd = d // H
+        sc = float(np.float32(1.0 / np.sqrt(hd)))
+        qkv = xs[0]
+        c = lambda a: np.ascontiguousarray(a, dtype=np.float32)  # noqa: E731
+        att = np.empty((T, d), np.float32)
+        dq = np.empty((T, 3 * d), np.float32)
+        for h in range(H):
+            Q, K, Vh = (c(qkv[:, o + h * hd:o + (h + 1) * hd]) for o in (0, d, 2 * d))
+            P = oracle.softmax(oracle.gemm(Q, K, transB=True, epi=2, scale=sc), causal=True)
+            if op == OP["ATTENTION"]:
+                att[:, h * hd:(h + 1) * hd] = oracle.gemm(P, Vh)
+                continue
+            dO = c(xs[1][:, h * hd:(h + 1) * hd])
+            dS = oracle.softmax_backward(P, oracle.gemm(dO, Vh, transB=True), scale=sc)
+            dq[:, 2 * d + h * hd:2 * d + (h + 1) * hd] = oracle.gemm(P, dO, transA=True)
+            dq[:, h * hd:(h + 1) * hd] = oracle.gemm(dS, K)
+            dq[:, d + h * hd:d + (h + 1) * hd] = oracle.gemm(dS, Q, transA=True)
+        return [att if op == OP["ATTENTION"] else dq]
     return None
 
 
@@ -76,7 +96,7 @@ def test_referee_recompute_matches_oracle(tiny_program):
     st.run()
     tr = verde.Trainer(st, ck)
     wanted = [OP["LINEAR"], OP["LAYERNORM"], OP["GELU"], OP["RESIDUAL"], OP["LINEAR_DGRAD"], OP["LINEAR_WGRAD"],
-              OP["SOFTMAX"]]
+              OP["ATTENTION"], OP["ATTENTION_BWD"]]
     done = set()
     for nd in st.nodes:
         if nd.op in wanted and nd.op not in done and nd.shard == 3:
@@ -169,7 +189,7 @@ def test_chunk_recompute_equals_full_replay(tiny_program):
     st.run()
     tr = verde.Trainer(st, ck)
     for name in ("s2/h0/qkv", "s5/head/lm_head", "s1/h1/fc2_dgrad", "s0/h1/fc_wgrad", "s6/h0/gelu", "s4/h1/res2",
-                 "s3/h0/softmax"):
+                 "s3/h0/attention", "s2/h1/attention_bwd"):
         d = _node_named(prog, name)
         o = tr.open(d)
         ins = tr.input_tensors(d)
