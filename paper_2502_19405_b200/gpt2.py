@@ -119,7 +119,8 @@ class GPT2Step:
     """Static program of one training step for the shards owned by this rank."""
 
     def __init__(self, cfg: GPT2Config, rank: int = 0, world: int = 1, device="cuda", pg=None,
-                 structure_only=False, combine: str = "sliced", p2p_sync: str = "device", attn_nodes: str = "operator"):
+                 structure_only=False, combine: str = "sliced", p2p_sync: str = "device", attn_nodes: str = "operator",
+                 zero1: bool = False):
         """structure_only: build the node graph / slot layout on the 'meta' device
         (no memory, no kernels) -- used by the CPU tests of the host logic."""
         assert cfg.shards % world == 0
@@ -133,6 +134,12 @@ class GPT2Step:
         if attn_nodes not in ("operator", "primitive"):
             raise ValueError(f"unknown attn_nodes {attn_nodes!r}")
         self.attn_op = attn_nodes == "operator"
+        # ZeRO-1 (f1): the optimizer state is partitioned by whole parameter tensors -- rank
+        # owner(name) alone keeps m / v of `name`, runs its AdamW, commits its PARAM_IN /
+        # TREE_SUM / ADAMW outputs and broadcasts the updated parameter; the digests of the
+        # replicated nodes are exchanged by owner, so the step root equals the replicated
+        # run's.  Gradients stay fully combined on every rank (stage 1, not 2).
+        self.zero1 = zero1
         self.structure_only = structure_only
         self.dev = torch.device("meta" if structure_only else device)
         self.s0, self.S_loc = shard_block(rank, world, cfg.shards)
@@ -186,6 +193,21 @@ class GPT2Step:
             self.off[name] = (off, shape, kind)
             off += n
         self.P = off
+        # ZeRO-1 ownership: largest tensors first, each to the least-loaded rank (ties -> lower
+        # rank); deterministic, the same on every rank
+        self.owner = {name: 0 for name, _, _ in self.specs}
+        if self.zero1 and self.world > 1:
+            load = [0] * self.world
+            for name, shape, _ in sorted(self.specs, key=lambda t: (-int(np.prod(t[1])), t[0])):
+                r = min(range(self.world), key=lambda q: (load[q], q))
+                self.owner[name] = r
+                load[r] += int(np.prod(shape))
+        self.owned = [name for name, _, _ in self.specs if self.owner[name] == self.rank or not self.zero1]
+        self.moff, mo = {}, 0  # offsets of the owned tensors in the (compact) m / v buffers
+        for name in self.owned:
+            self.moff[name] = mo
+            mo += int(np.prod(self.off[name][1]))
+        self.P_own = mo
         if self.structure_only:
             self.params = torch.empty(self.P, device=self.dev)
             self.m = torch.empty(self.P, device=self.dev)
@@ -196,11 +218,21 @@ class GPT2Step:
             o, _, _ = self.off[name]
             host[o:o + int(np.prod(shape))] = synth.gpt2_param(name, shape, kind, c.seed).ravel()
         self.params = torch.from_numpy(host).to(self.dev)
-        self.m = torch.zeros(self.P, device=self.dev)
-        self.v = torch.zeros(self.P, device=self.dev)
+        self.m = torch.zeros(self.P_own if self.zero1 else self.P, device=self.dev)
+        self.v = torch.zeros(self.P_own if self.zero1 else self.P, device=self.dev)
 
     def pview(self, buf, name):
         o, shape, _ = self.off[name]
+        return buf[o:o + int(np.prod(shape))].view(*shape)
+
+    def mview(self, buf, name):
+        """view of `name` in the optimizer-state buffer m / v (ZeRO-1: compact, owned tensors
+        only; an empty placeholder for the others)"""
+        if not self.zero1:
+            return self.pview(buf, name)
+        if name not in self.moff:
+            return torch.empty(0, device=self.dev)
+        o, shape = self.moff[name], self.off[name][1]
         return buf[o:o + int(np.prod(shape))].view(*shape)
 
     # ------------------------------------------------------------------ buffers
@@ -293,8 +325,8 @@ class GPT2Step:
         self.param_in_node, self.adamw_node = {}, {}
         for name, shape, kind in self.specs:
             ids = [T_(f"param/{name}", self.pview(self.params, name), REPLICATED),
-                   T_(f"m/{name}", self.pview(self.m, name), REPLICATED),
-                   T_(f"v/{name}", self.pview(self.v, name), REPLICATED)]
+                   T_(f"m/{name}", self.mview(self.m, name), REPLICATED),
+                   T_(f"v/{name}", self.mview(self.v, name), REPLICATED)]
             self.node(OP["PARAM_IN"], REPLICATED, {}, [], ids, f"in/{name}")
             self.param_in[name] = ids
             self.param_in_node[name] = len(self.nodes) - 1
@@ -810,15 +842,28 @@ class GPT2Step:
         seg_decay = [len(shape) == 2 for _, shape, _ in self.specs]
 
         def adam():
-            repops_adamw_segments(self.params, self.grad, self.m, self.v, seg_start, seg_decay, self.step_no + 1,
-                                  c.lr, c.beta1, c.beta2, c.adam_eps, c.wd)
+            if not self.zero1:
+                repops_adamw_segments(self.params, self.grad, self.m, self.v, seg_start, seg_decay, self.step_no + 1,
+                                      c.lr, c.beta1, c.beta2, c.adam_eps, c.wd)
+                return
+            # ZeRO-1: the owned tensors' update (same element chain), then every parameter
+            # tensor broadcast from its owner (data movement only)
+            for name in self.owned:
+                shape = self.off[name][1]
+                repops_adamw(self.pview(self.params, name), self.pview(self.grad, name), self.mview(self.m, name),
+                             self.mview(self.v, name), self.step_no + 1, c.lr, c.beta1, c.beta2, c.adam_eps, c.wd,
+                             len(shape) == 2)
+            if self.world > 1:
+                import torch.distributed as dist
+                for name, _, _ in self.specs:
+                    dist.broadcast(self.pview(self.params, name), src=self.owner[name], group=self.pg)
         self.launch(adam)
         self.adam_out = {}
         for name, shape, kind in self.specs:
             p_, m_, v_ = self.param_in[name]
             outs = [T_(f"param'/{name}", self.pview(self.params, name), REPLICATED),
-                    T_(f"m'/{name}", self.pview(self.m, name), REPLICATED),
-                    T_(f"v'/{name}", self.pview(self.v, name), REPLICATED)]
+                    T_(f"m'/{name}", self.mview(self.m, name), REPLICATED),
+                    T_(f"v'/{name}", self.mview(self.v, name), REPLICATED)]
             attrs = {AK["lr"]: f32bits(c.lr), AK["beta1"]: f32bits(c.beta1), AK["beta2"]: f32bits(c.beta2),
                      AK["adam_eps"]: f32bits(c.adam_eps), AK["wd"]: f32bits(c.wd),
                      AK["decay"]: int(len(shape) == 2)}
@@ -874,7 +919,14 @@ class GPT2Step:
                 per_phase.setdefault(ph, []).append(t)
         self.plan_after = {}
         self.plans = []
+        # ZeRO-1: a rank commits only the replicated tensors of the parameters it owns; the
+        # other replicated digests come from their owners (_gather_rep_digests)
+        self._rep_owner = np.zeros(max(n_rep, 1), np.int64)
+        for i, t in enumerate(self._rep_ids):
+            self._rep_owner[i] = self.owner.get(self.tensors[t].name.split("/", 1)[1], 0)
+        not_mine = {t for i, t in enumerate(self._rep_ids) if self.zero1 and self._rep_owner[i] != self.rank}
         for ph, tids in sorted(per_phase.items()):
+            tids = [t for t in tids if t not in not_mine]
             if tids and not self.structure_only:
                 plan = CommitPlan([self.tensors[t].view for t in tids],
                                   [self.digests[self.tensors[t].slot] for t in tids])
@@ -1057,9 +1109,22 @@ class GPT2Step:
             torch.cuda.current_stream().wait_stream(self.side)
         self._joined = True
 
+    def _gather_rep_digests(self):
+        """ZeRO-1: every replicated slot takes its owner's digest (all-gather of the
+        replicated region, ≈ 7 x 32 B per parameter tensor per rank)."""
+        if not self.zero1 or self.world == 1:
+            return
+        from .dist import all_gather_rows
+        if not hasattr(self, "_rep_sel"):
+            self._rep_sel = (torch.from_numpy(self._rep_owner[:self.rep_slots]).to(self.dev),
+                             torch.arange(self.rep_slots, device=self.dev))
+        allr = all_gather_rows(self.digests[:self.rep_slots].contiguous(), self.world, self.pg)
+        self.digests[:self.rep_slots] = allr[self._rep_sel[0], self._rep_sel[1]]
+
     def gather_digests(self):
         """C2: all-gather the per-shard digest regions; copy the table to the host."""
         gather_shard_digests(self.digests, self.rep_slots, self.shard_slots, self.s0, self.S_loc, self.world, self.pg)
+        self._gather_rep_digests()
         self.digests_host.copy_(self.digests, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         return self.digests_host.numpy()
@@ -1073,6 +1138,7 @@ class GPT2Step:
         with torch.cuda.stream(s):
             gather_shard_digests(self.digests, self.rep_slots, self.shard_slots, self.s0, self.S_loc, self.world,
                                  self.pg)
+            self._gather_rep_digests()
             self.root_plan.run(stream=s)
             self.root_host.copy_(self.root_plan.root, non_blocking=True)
             self._ev_root.record(s)
@@ -1114,6 +1180,8 @@ class GPT2Step:
         what a trainer logs at the checkpoint steps of Alg. 1 when it does not
         commit every operator output (configs[2] without configs[4])."""
         from . import CommitPlan
+        if self.zero1 and self.world > 1:
+            raise NotImplementedError("checkpoint_commit with ZeRO-1: the state is partitioned across ranks")
         if getattr(self, "_ckpt_plan", None) is None:
             views = []
             for name, _, _ in self.specs:

@@ -174,3 +174,20 @@ def test_combine_transport_validation():
     a = GPT2Step(GPT2Config.tiny(), structure_only=True, combine="sliced")
     b = GPT2Step(GPT2Config.tiny(), structure_only=True, combine="p2p")
     assert np.array_equal(a.node_blob, b.node_blob) and np.array_equal(a.node_slots, b.node_slots)
+
+
+def test_zero1_ownership_partition():
+    """ZeRO-1 ownership: every parameter tensor has exactly one owner, the same on every
+    rank, and the compact optimizer-state buffers hold exactly the owned tensors"""
+    from paper_2502_19405_b200.gpt2 import GPT2Config, GPT2Step
+    for world in (2, 4, 8):
+        steps = [GPT2Step(GPT2Config(), rank=r, world=world, structure_only=True, zero1=True) for r in range(world)]
+        owners = [st.owner for st in steps]
+        assert all(o == owners[0] for o in owners)
+        owned = [set(st.owned) for st in steps]
+        assert set().union(*owned) == {n for n, _, _ in steps[0].specs}
+        assert sum(len(o) for o in owned) == len(steps[0].specs)
+        assert sum(st.P_own for st in steps) == steps[0].P
+        # greedy balance: no rank exceeds the largest tensor plus the ideal share
+        wte = 50257 * 768
+        assert max(st.P_own for st in steps) <= max(wte, steps[0].P // world + wte)

@@ -21,7 +21,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, tiny, q, combine="sliced", sync="host", bucketed=True):
+def _worker(rank, world, port, tiny, q, combine="sliced", sync="host", bucketed=True, zero1=False, steps=1):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -30,11 +30,12 @@ def _worker(rank, world, port, tiny, q, combine="sliced", sync="host", bucketed=
         torch.cuda.set_device(0)
         from paper_2502_19405_b200.gpt2 import GPT2Config, GPT2Step
         cfg = GPT2Config.tiny() if tiny else GPT2Config()
-        st = GPT2Step(cfg, rank=rank, world=world, combine=combine, p2p_sync=sync)
+        st = GPT2Step(cfg, rank=rank, world=world, combine=combine, p2p_sync=sync, zero1=zero1)
         st.bucketed = bucketed
-        st.set_tokens(0)
-        st.run()
-        root, _ = st.step_root()
+        for t in range(steps):   # several steps: the next step starts from the updated state
+            st.set_tokens(t)
+            st.run()
+            root, _ = st.step_root()
         loss = st.loss()
         # the updated parameters themselves must be identical on every rank
         pdig = st.digests_host.numpy()[st.tensors[st.adam_out["wte"][0]].slot].tobytes()
@@ -47,11 +48,12 @@ def _worker(rank, world, port, tiny, q, combine="sliced", sync="host", bucketed=
         dist.destroy_process_group()
 
 
-def _run(world, tiny, combine="sliced", sync="host", bucketed=True):
+def _run(world, tiny, combine="sliced", sync="host", bucketed=True, zero1=False, steps=1):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, world, port, tiny, q, combine, sync, bucketed)) for r in range(world)]
+    ps = [ctx.Process(target=_worker, args=(r, world, port, tiny, q, combine, sync, bucketed, zero1, steps))
+          for r in range(world)]
     for p in ps:
         p.start()
     res = []
@@ -125,6 +127,24 @@ def test_full_gpt2_step_root_p2p_bucketed(world, full_single):
     for rank, root, loss, pdig in _run(world, False, combine="p2p"):
         assert root == full_single[1], f"bucketed p2p G={world} rank {rank}: full step root differs"
         assert pdig == full_single[3]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_tiny_zero1_three_steps_root_equals_replicated(world):
+    """ZeRO-1 (optimizer state partitioned by parameter tensor, owner-only AdamW + commit,
+    parameters broadcast, replicated digests exchanged by owner) over 3 steps: every
+    step's root equals the single-process replicated run's"""
+    single = _run(1, True, steps=3)[0]
+    for rank, root, loss, pdig in _run(world, True, combine="p2p", zero1=True, steps=3):
+        assert root == single[1], f"ZeRO-1 G={world} rank {rank}: step-3 root differs"
+        assert loss == single[2]
+        assert pdig == single[3]
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_full_gpt2_zero1_root_equals_world1(world, full_single):
+    for rank, root, loss, pdig in _run(world, False, combine="p2p", zero1=True):
+        assert root == full_single[1], f"ZeRO-1 full G={world} rank {rank}: step root differs"
 
 
 # ---------------------------------------------------------------- config 2: M-split GEMM
