@@ -102,7 +102,11 @@ def test_block_forward_every_node(full):
     # are kernel outputs too: the shard's rows of the layer's S and P buffers
     H, T = cfg.n_head, cfg.seq
     sl = slice(s * H * T, (s + 1) * H * T)
-    same_bits(st.act[l]["S"][sl].cpu().numpy(), ref["scores"], "internal scores")
+    # scores: the entries the causal softmax reads (column <= row); tiles above the diagonal
+    # are not computed when the scores are operator-internal (R31)
+    S_gpu = st.act[l]["S"][sl].cpu().numpy().reshape(H, T, T)
+    low = np.tril(np.ones((T, T), bool))
+    same_bits(S_gpu[:, low], ref["scores"].reshape(H, T, T)[:, low], "internal scores (causal part)")
     same_bits(st.act[l]["P"][sl].cpu().numpy(), ref["probs"], "internal probabilities")
 
 
