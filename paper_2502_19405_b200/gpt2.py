@@ -36,7 +36,7 @@ import torch
 
 import synth
 
-from . import (EPI_BIAS, EPI_SCALE, repops_causal_suffix_flags, CommitPlan, repops_add, repops_attention_fwd, repops_attention_fwd_supported, repops_cross_entropy, repops_embedding,
+from . import (EPI_BIAS, EPI_SCALE, CommitPlan, repops_add, repops_attention_fwd, repops_attention_fwd_supported, repops_cross_entropy, repops_embedding,
                repops_embedding_backward, repops_gelu, repops_gelu_backward, repops_gemm,
                repops_gemm_strided_batched, repops_layernorm, repops_layernorm_backward,
                repops_layernorm_backward_params, repops_softmax, repops_softmax_backward, repops_sum_cols_seq,
@@ -259,8 +259,6 @@ class GPT2Step:
                           dP=E(self.S_loc * H * T, T), dS=E(self.S_loc * H * T, T), dqkv=E(M, 3 * d),
                           dln1=E(M, d)))
         self.dx = [E(M, d) for _ in range(L + 1)]  # dx[l] = gradient w.r.t. x[l]
-        # V suffix flags for the causal PV (R31), one [T + 1, hd] block per (local shard, head)
-        self.vflags = torch.empty((self.S_loc * H, T + 1, c.hd), dtype=torch.uint8, device=dev)
         self.glocal = torch.zeros(self.S_loc, self.P, device=dev)  # per-shard gradients (rows)
         if self.combine == "p2p" and self.world > 1 and not self.structure_only:
             self.p2p = P2PTreeCombine(self.P, self.rank, self.world, self.pg, sync=self.p2p_sync)
@@ -456,8 +454,7 @@ class GPT2Step:
                         # scores S = (Q K^T) * 1/sqrt(hd), batched over (local shard, head)
                         # with attention as one operator (R29) the scores are internal scratch: the
                         # tiles above the diagonal, which the causal softmax never reads, are not
-                        # computed, and the PV folds stop at each tile's last query row with the
-                        # skipped +0 terms applied exactly from V's suffix flags (R31)
+                        # computed (R31; tools/causal_bench.py: 106 -> 72 us per layer)
                         skip = self.attn_op and self.causal_skip
                         repops_gemm_strided_batched(a["qkv"], a["qkv"], a["S"], M=T, N=T, K=hd, lda=3 * d,
                                                     ldb=3 * d, ldc=T, sA=(T * 3 * d, hd), sB=(T * 3 * d, hd),
@@ -467,15 +464,12 @@ class GPT2Step:
                         self._hook(f"h{l}/scores")
                         repops_softmax(a["S"], causal=True, out=a["P"])
                         self._hook(f"h{l}/softmax")
-                        if skip:
-                            repops_causal_suffix_flags(a["qkv"], T, hd, 3 * d, (T * 3 * d, hd), (S_loc, H),
-                                                       out=self.vflags, ldf=hd, sF=(H * (T + 1) * hd, (T + 1) * hd),
-                                                       offB=2 * d)
+                        # the causal PV (mode 2) does not pay at T = 512: its 384 CTAs are one wave,
+                        # so the full-K row tiles set the time (tools/causal_bench.py: 83.5 vs 82.8
+                        # us, plus 13 us of suffix flags) -- the full PV runs here
                         repops_gemm_strided_batched(a["P"], a["qkv"], a["att"], M=T, N=hd, K=T, lda=T, ldb=3 * d,
                                                     ldc=d, sA=(H * T * T, T * T), sB=(T * 3 * d, hd),
-                                                    sC=(T * d, hd), batch=(S_loc, H), offB=2 * d,
-                                                    causal=2 if skip else 0, kflags=self.vflags, ldf=hd,
-                                                    sF=(H * (T + 1) * hd, (T + 1) * hd))
+                                                    sC=(T * d, hd), batch=(S_loc, H), offB=2 * d)
                         self._hook(f"h{l}/pv")
                     self._gemm_tn(a["att"], W("proj.w"), epi=EPI_BIAS, bias=W("proj.b"), out=a["proj"])
                     self._hook(f"h{l}/proj")
