@@ -14,6 +14,13 @@ bash tools/prof_gemm_remote.sh "4096x768x3072 1 0 -1 gemm_fc2_tn" "4096x3072x768
     "512x512x64 0 1 -1 gemm_scores_nt"
 bash tools/prof_cublas_remote.sh 8192x8192x8192 1 0 cublas_8192_tn
 mkdir -p gpurun_out/prof_tmp
+for k in 0 1 2; do
+  timeout 300 ncu --set full --import-source on --clock-control none -k regex:gemm -s $((3 + k)) -c 1 \
+      -o gpurun_out/prof_tmp/attn$k -f python tools/attn_one.py > /dev/null 2>&1
+  ncu -i gpurun_out/prof_tmp/attn$k.ncu-rep --page raw --csv > gpurun_out/prof_tmp/attn$k.csv 2>/dev/null
+  python tools/ncu_summary.py gpurun_out/prof_tmp/attn$k.csv > gpurun_out/ncu_gemm_attn$k.txt
+done
+mkdir -p gpurun_out/prof_tmp
 timeout 300 ncu --set full --import-source on --clock-control none -k regex:leaf_kernel -s 1 -c 1 \
     -o gpurun_out/prof_tmp/leaf -f python tools/commit_one.py > /dev/null 2>&1
 ncu -i gpurun_out/prof_tmp/leaf.ncu-rep --page raw --csv > gpurun_out/prof_tmp/leaf.csv 2>/dev/null
