@@ -570,10 +570,10 @@ def run_reference(args, rank, world):
     oracle.lib()
     if args.workload == "gemm":
         fn = lambda: oracle_sample_gemm(2.0)  # noqa: E731
-        cfg = {"workload": "gemm-sweep 1024-8192 (oracle sample)"}
+        cfg = gemm_config(world)
     else:
         fn = lambda: oracle_sample_gpt2(2)  # noqa: E731
-        cfg = {"workload": "gpt2-124m train step B=8 T=512 (oracle sample)"}
+        cfg = gpt2_config(world, args.combine)
     for _ in range(args.warmup):
         fn()
     vals, secs, sample = [], 0.0, ""
@@ -736,23 +736,12 @@ def main():
         "dtype": "f32", "data": "synthetic",
     })
     if args.workload == "gpt2":
-        out["config"] = {"workload": "gpt2-124m train step B=8 T=512 (S=8 DP shards) + Verde commit of every "
-                                     "operator output + node digests + step Merkle root",
-                         "global_batch": 8, "seq_len": 512, "parallelism": f"dp{world} (canonical R-TREE_S)",
-                         "combine": (f"{args.combine}: " + {"p2p": "one fused peer-memory kernel per rank (CUDA IPC)",
-                                                            "sliced": "NCCL all-to-all + all-gather",
-                                                            "gather": "NCCL all-gather of partials"}[args.combine])
-                         if world > 1 else "local tree (G=1)",
-                         "l2": "per-step working set ~17 GB >> 126 MB L2 (no explicit flush)",
-                         "inputs": "synthetic tokens + U(std 0.02) weights (synth.gpt2_*)",
-                         "flops_per_step": GPT2_FLOPS_NOTE}
+        out["config"] = gpt2_config(world, args.combine)
         out["gpt2_step_ms"] = head["ms"]
         out["loss"] = head["loss"]
         out["step_root"] = head["root"]
     else:
-        out["config"] = {"workload": "gemm-sweep: R-GEMM square n=1024..8192 + Verde commit of every output",
-                         "sizes": list(SIZES), "sharding": f"M-split over {world} GPU(s), full K per rank",
-                         "l2": "step working set 1.07 GB > 126 MB L2 (no explicit flush)"}
+        out["config"] = gemm_config(world)
         out["digests"] = head["digests"]
     # primary: the GEMM family's flops over the UNION of its launch intervals (the aux-stream
     # weight-gradient GEMMs overlap the dgrads, so summed per-launch durations double-count)
@@ -835,6 +824,26 @@ def main():
 
 
 GPT2_FLOPS_NOTE = "3 x (2 M N K over every fwd matmul: 12 x [QKV, proj, FC, FC2] + full (unmasked) QK^T, PV + LM head)"
+
+
+def gpt2_config(world, combine):
+    """the headline line's config (both arms print the same object)"""
+    return {"workload": "gpt2-124m train step B=8 T=512 (S=8 DP shards) + Verde commit of every operator output "
+                        "+ node digests + step Merkle root",
+            "global_batch": 8, "seq_len": 512, "parallelism": f"dp{world} (canonical R-TREE_S)",
+            "combine": (f"{combine}: " + {"p2p": "per-layer buckets, one fused peer-memory kernel per rank (CUDA IPC)",
+                                          "sliced": "NCCL all-to-all + all-gather",
+                                          "gather": "NCCL all-gather of partials"}[combine])
+            if world > 1 else "local tree (G=1)",
+            "l2": "per-step working set ~17 GB >> 126 MB L2 (no explicit flush)",
+            "inputs": "synthetic tokens + U(std 0.02) weights (synth.gpt2_*)",
+            "flops_per_step": GPT2_FLOPS_NOTE}
+
+
+def gemm_config(world):
+    return {"workload": "gemm-sweep: R-GEMM square n=1024..8192 + Verde commit of every output",
+            "sizes": list(SIZES), "sharding": f"M-split over {world} GPU(s), full K per rank",
+            "l2": "step working set 1.07 GB > 126 MB L2 (no explicit flush)"}
 
 if __name__ == "__main__":
     main()
