@@ -301,6 +301,10 @@ int repops_fill_uniform(float *out, int64_t n, uint64_t seed, double scale, void
 /* Strided 2-D copy (data movement only): dst[r*ldd + c] = src[r*lds + c], r < rows, c < cols.
  * Used to place all-gathered tensor-parallel column blocks into one activation. */
 int repops_copy2d(const float *src, int64_t rows, int64_t cols, int64_t lds, float *dst, int64_t ldd, void *stream);
+/* Batched form: for b < nb, dst + b*sd <- src + b*ss (rows x cols, row strides lds / ldd;
+ * element offsets).  One launch places all nb tensor-parallel blocks of an activation. */
+int repops_copy2d_batched(const float *src, int64_t rows, int64_t cols, int64_t lds, int64_t ss, float *dst,
+                          int64_t ldd, int64_t sd, int64_t nb, void *stream);
 
 /* Transpose (data movement only, bit-exact): y[j*ldy + i] = x[i*ldx + j] for a
  * rows x cols x.  Used to give backward GEMMs an n-contiguous weight operand. */

@@ -19,7 +19,7 @@ F32, I32, U8, BF16, F16 = 1, 2, 3, 4, 5
 _DT = {torch.float32: F32, torch.int32: I32, torch.uint8: U8, torch.bfloat16: BF16, torch.float16: F16}
 
 __all__ = [
-    "repops_gemm", "repops_gemm_strided_batched", "repops_causal_suffix_flags", "repops_sum_rows", "repops_sum_cols_seq", "repops_tree_sum",
+    "repops_gemm", "repops_gemm_strided_batched", "repops_causal_suffix_flags", "repops_copy2d_batched", "repops_sum_rows", "repops_sum_cols_seq", "repops_tree_sum",
     "repops_softmax", "repops_softmax_backward", "repops_layernorm", "repops_layernorm_backward",
     "repops_layernorm_backward_params", "repops_cross_entropy", "repops_exp", "repops_log", "repops_tanh",
     "repops_rsqrt", "repops_gelu", "repops_gelu_backward", "repops_relu", "repops_relu_backward", "repops_sin", "repops_cos", "repops_erf", "repops_gelu_erf", "repops_convert", "repops_gemm_ex",
@@ -635,6 +635,13 @@ def repops_copy2d(src, dst, stream=None):
     """dst[:, :] = src (both 2-D views with unit column stride; data movement only)."""
     rows, cols = src.shape
     check(lib().repops_copy2d(_p(src), rows, cols, _ld(src), _p(dst), _ld(dst), _stream(stream)), "repops_copy2d")
+    return dst
+
+
+def repops_copy2d_batched(src, dst, rows, cols, lds, ss, ldd, sd, nb, stream=None):
+    """for b < nb: dst[b*sd + r*ldd + c] = src[b*ss + r*lds + c] (element offsets; data movement)."""
+    check(lib().repops_copy2d_batched(_p(src), rows, cols, lds, ss, _p(dst), ldd, sd, nb, _stream(stream)),
+          "repops_copy2d_batched")
     return dst
 
 

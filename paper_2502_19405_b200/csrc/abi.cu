@@ -682,6 +682,14 @@ int repops_fill_uniform(float *out, int64_t n, uint64_t seed, double scale, void
     return cuda_status(launch_fill_uniform(out, n, seed, scale, S(stream)), "fill_uniform");
 }
 
+int repops_copy2d_batched(const float *src, int64_t rows, int64_t cols, int64_t lds, int64_t ss, float *dst,
+                          int64_t ldd, int64_t sd, int64_t nb, void *stream) {
+    REQ(rows >= 0 && cols >= 0 && nb >= 0, "copy2d_batched: negative extent");
+    if (rows == 0 || cols == 0 || nb == 0) return REPOPS_OK;
+    REQ(src && dst && lds >= cols && ldd >= cols && nb <= 65535, "copy2d_batched: bad pointer / ld / batch");
+    return cuda_status(launch_copy2d_batched(src, rows, cols, lds, ss, dst, ldd, sd, nb, S(stream)), "copy2d_batched");
+}
+
 int repops_copy2d(const float *src, int64_t rows, int64_t cols, int64_t lds, float *dst, int64_t ldd, void *stream) {
     REQ(rows >= 0 && cols >= 0, "copy2d: negative extent");
     if (rows == 0 || cols == 0) return REPOPS_OK;

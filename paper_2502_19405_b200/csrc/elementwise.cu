@@ -611,20 +611,42 @@ __global__ void fill_uniform_kernel(float *__restrict__ out, int64_t n, uint64_t
 }  // namespace
 
 namespace {
-__global__ void copy2d_kernel(const float *__restrict__ src, int64_t rows, int64_t cols, int64_t lds,
-                              float *__restrict__ dst, int64_t ldd) {
-    const int64_t r = blockIdx.y;
-    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += (int64_t)gridDim.x * blockDim.x)
-        dst[r * ldd + c] = src[r * lds + c];
+// batch b of rows x cols: dst + b*sd <- src + b*ss (row strides lds / ldd); float4 when
+// every row start is 16-byte aligned, else scalar.  Data movement only.
+template <bool V4>
+__global__ void copy2d_kernel(const float *__restrict__ src, int64_t rows, int64_t cols, int64_t lds, int64_t ss,
+                              float *__restrict__ dst, int64_t ldd, int64_t sd) {
+    const int64_t b = blockIdx.z;
+    src += b * ss;
+    dst += b * sd;
+    const int64_t w = V4 ? cols / 4 : cols;
+    const int64_t n = rows * w;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / w, c = i % w;
+        if (V4)
+            reinterpret_cast<float4 *>(dst + r * ldd)[c] = __ldg(reinterpret_cast<const float4 *>(src + r * lds) + c);
+        else
+            dst[r * ldd + c] = src[r * lds + c];
+    }
 }
 }  // namespace
 
+cudaError_t launch_copy2d_batched(const float *src, int64_t rows, int64_t cols, int64_t lds, int64_t ss, float *dst,
+                                  int64_t ldd, int64_t sd, int64_t nb, cudaStream_t s) {
+    if (rows == 0 || cols == 0 || nb == 0) return cudaSuccess;
+    const bool v4 = ((uintptr_t)src % 16 == 0) && ((uintptr_t)dst % 16 == 0) && cols % 4 == 0 && lds % 4 == 0 &&
+                    ldd % 4 == 0 && ss % 4 == 0 && sd % 4 == 0;
+    const int64_t work = rows * (v4 ? cols / 4 : cols);
+    const int64_t per = max((int64_t)1, (int64_t)ro_host::num_sms() * 8 / nb);
+    dim3 grid((unsigned)max((int64_t)1, min((work + 255) / 256, per)), 1, (unsigned)nb);
+    if (v4) copy2d_kernel<true><<<grid, 256, 0, s>>>(src, rows, cols, lds, ss, dst, ldd, sd);
+    else copy2d_kernel<false><<<grid, 256, 0, s>>>(src, rows, cols, lds, ss, dst, ldd, sd);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_copy2d(const float *src, int64_t rows, int64_t cols, int64_t lds, float *dst, int64_t ldd,
                           cudaStream_t s) {
-    if (rows == 0 || cols == 0) return cudaSuccess;
-    dim3 grid((unsigned)min((cols + 255) / 256, (int64_t)64), (unsigned)rows);
-    copy2d_kernel<<<grid, 256, 0, s>>>(src, rows, cols, lds, dst, ldd);
-    return cudaGetLastError();
+    return launch_copy2d_batched(src, rows, cols, lds, 0, dst, ldd, 0, 1, s);
 }
 
 cudaError_t launch_swiglu(const float *g, const float *u, int64_t n, float *h, cudaStream_t s) {

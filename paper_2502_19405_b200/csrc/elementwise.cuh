@@ -31,6 +31,8 @@ cudaError_t launch_embedding(const int32_t *tok, int64_t ntok, int64_t T, const 
 cudaError_t launch_embedding_backward(const int32_t *tok, int64_t ntok, int64_t T, const float *dx0, int64_t C,
                                       float *dwte, float *dwpe, cudaStream_t s);
 cudaError_t launch_flip_bit(void *data, int64_t elem, int bit, cudaStream_t s);
+cudaError_t launch_copy2d_batched(const float *src, int64_t rows, int64_t cols, int64_t lds, int64_t ss, float *dst,
+                                  int64_t ldd, int64_t sd, int64_t nb, cudaStream_t s);
 cudaError_t launch_copy2d(const float *src, int64_t rows, int64_t cols, int64_t lds, float *dst, int64_t ldd,
                           cudaStream_t s);
 cudaError_t launch_swiglu(const float *g, const float *u, int64_t n, float *h, cudaStream_t s);

@@ -36,7 +36,7 @@ import torch
 
 import synth
 
-from . import (repops_causal_suffix_flags, EPI_SCALE, CommitPlan, RootPlan, repops_add, repops_copy2d, repops_fill_uniform, repops_gather_rows,
+from . import (repops_causal_suffix_flags, repops_copy2d_batched, EPI_SCALE, CommitPlan, RootPlan, repops_add, repops_copy2d, repops_fill_uniform, repops_gather_rows,
                repops_gemm_strided_batched, repops_rmsnorm, repops_rope, repops_softmax, repops_swiglu,
                repops_rope_tables, repops_transpose, verde_commit_tensors)
 from ._lib import check, lib
@@ -316,8 +316,9 @@ class LlamaPrefill:
     def _gather_blocks(self, local, full, width):
         """all-gather [nbl, T, width] block results and place block b at full[:, b*width:(b+1)*width]."""
         allb = all_gather_rows(local, self.world, self.pg).reshape(self.cfg.nb, self.cfg.seq, width)
-        for b in range(self.cfg.nb):
-            repops_copy2d(allb[b], full[:, b * width:(b + 1) * width])
+        # one launch for all nb blocks: block b -> columns [b*width, (b+1)*width)
+        repops_copy2d_batched(allb, full, self.cfg.seq, width, width, self.cfg.seq * width, full.stride(0), width,
+                              self.cfg.nb)
 
     def _xT(self, x):
         rows, cols = x.shape

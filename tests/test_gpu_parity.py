@@ -137,6 +137,18 @@ def test_gemm_tn_kernel_batched_and_strided_output():
         assert np.all(blk[:, N:].view(np.uint32) == 0), "wrote outside the C tile"
 
 
+def test_copy2d_batched_places_blocks_bit_exactly():
+    # tensor-parallel block placement (Llama gathers): nb blocks of rows x w into column
+    # ranges of one matrix, float4 and scalar paths, every bit pattern preserved (NaN payloads)
+    for nb, rows, w in ((8, 33, 12), (3, 17, 5)):
+        src = synth.uniform(81 + w, (nb, rows, w))
+        src.view(np.uint32)[0, 1, :2] = [0x7FA00001, 0xFFC00002]   # NaN payloads travel unchanged
+        full = torch.zeros((rows, nb * w), device="cuda")
+        R.repops_copy2d_batched(dev(src), full, rows, w, w, rows * w, nb * w, w, nb)
+        ref = np.concatenate([src[b] for b in range(nb)], axis=1)
+        assert np.array_equal(host(full).view(np.uint32), ref.view(np.uint32))
+
+
 # ------------------------------------------------------------------ causal structure (f4)
 def test_gemm_causal_skip_scores():
     # causal 1: tiles strictly above the diagonal are not written; every other output
