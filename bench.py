@@ -792,6 +792,8 @@ def main():
                    "gpt2_ckpt": "gpt2_train_step"}[other]
             out[key] = {"value": res["value"], "unit": "TFLOP/s", "ms_per_step": res["ms"],
                         "gemm_tflops": res["gemm"][0], "gemm_roofline_frac": res["gemm"][0] / res["gemm"][1],
+                        "gemm_union_tflops": res.get("gemm_union"),
+                        "gemm_union_frac": (res["gemm_union"] / res["gemm"][1]) if res.get("gemm_union") else None,
                         "digests": res.get("digests"), "root": res.get("root"), "commit": res.get("commit"),
                         "loss": res.get("loss"),
                         "config": {"gemm": "square n=1024..8192, M-split, each output committed",

@@ -321,19 +321,34 @@ __global__ void embedding_kernel(const int32_t *__restrict__ tok, int64_t ntok, 
 __global__ void embedding_bwd_kernel(const int32_t *__restrict__ tok, int64_t ntok, int64_t T,
                                      const float *__restrict__ dx0, int64_t C, float *__restrict__ dwte,
                                      float *__restrict__ dwpe) {
+    // stok[0..ntok): the shard's tokens; occ[0..nocc): the positions holding token v, ascending
     extern __shared__ int32_t stok[];
+    int32_t *occ = stok + ntok;
+    __shared__ int nocc;
     const int64_t u = blockIdx.x;
     for (int64_t i = threadIdx.x; i < ntok; i += blockDim.x) stok[i] = __ldg(tok + i);
     __syncthreads();
     const int32_t v = stok[u];
-    bool first = true;
-    for (int64_t i = 0; i < u; ++i)
-        if (stok[i] == v) { first = false; break; }
+    // position u owns vocabulary row v iff v does not occur before u (checked in parallel)
+    int earlier = 0;
+    for (int64_t i = threadIdx.x; i < u; i += blockDim.x) earlier |= (stok[i] == v);
+    const bool first = !__syncthreads_or(earlier);
     if (first) {
+        if (threadIdx.x < 32) {  // warp 0 lists the occurrences of v in ascending order
+            int n = 0;
+            for (int64_t b = u; b < ntok; b += 32) {
+                const int64_t t = b + threadIdx.x;
+                const unsigned m = __ballot_sync(0xffffffffu, t < ntok && stok[t] == v);
+                if (t < ntok && stok[t] == v) occ[n + __popc(m & ((1u << threadIdx.x) - 1u))] = (int32_t)t;
+                n += __popc(m);
+            }
+            if (threadIdx.x == 0) nocc = n;
+        }
+        __syncthreads();
+        const int n = nocc;
         for (int64_t c = threadIdx.x; c < C; c += blockDim.x) {
-            float acc = 0.f;
-            for (int64_t t = u; t < ntok; ++t)
-                if (stok[t] == v) acc = __fadd_rn(acc, __ldg(dx0 + t * C + c));
+            float acc = 0.f;  // R-SEQ over the shard's tokens equal to v, ascending
+            for (int q = 0; q < n; ++q) acc = __fadd_rn(acc, __ldg(dx0 + (int64_t)occ[q] * C + c));
             float *o = dwte + (int64_t)v * C + c;
             *o = canon(__fadd_rn(*o, acc));
         }
@@ -492,7 +507,7 @@ cudaError_t launch_embedding(const int32_t *tok, int64_t ntok, int64_t T, const 
 cudaError_t launch_embedding_backward(const int32_t *tok, int64_t ntok, int64_t T, const float *dx0, int64_t C,
                                       float *dwte, float *dwpe, cudaStream_t s) {
     if (ntok == 0) return cudaSuccess;
-    size_t smem = (size_t)ntok * sizeof(int32_t);
+    size_t smem = (size_t)2 * ntok * sizeof(int32_t);  // tokens + the occurrence list
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(embedding_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
