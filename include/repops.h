@@ -85,6 +85,18 @@ int repops_gemm_strided_batched(int64_t M, int64_t N, int64_t K,
                                 float *C, int64_t ldc, int64_t sC0, int64_t sC1,
                                 int64_t batch0, int64_t batch1, void *stream);
 
+/* R-GEMM with its elementwise consumer fused into the epilogue: C as
+ * repops_gemm, and C2[i][j] = R-GELU(C[i][j]) (post = REPOPS_POST_GELU) or
+ * R-GELU-backward at X[i][j] with dy = C[i][j] (REPOPS_POST_GELU_BACKWARD).  C2's bits
+ * equal repops_gelu / repops_gelu_backward applied to C (same device functions).
+ * Shapes the fused A^T kernel does not take run the GEMM and the separate launch (then
+ * C, C2, X must be contiguous: ld = N).  X, C2: device, caller-owned.  Errors: REPOPS_EINVAL. */
+#define REPOPS_POST_GELU 1
+#define REPOPS_POST_GELU_BACKWARD 2
+int repops_gemm_post(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, int transA, const float *B,
+                     int64_t ldb, int transB, int epi, const float *bias, float scale, float *C, int64_t ldc, int post,
+                     const float *X, int64_t ldx, float *C2, int64_t ldc2, void *stream);
+
 /* Causal structure of attention (R-ATTN, DESIGN R29 / R31), exact.
  * repops_gemm_strided_batched_causal: repops_gemm_strided_batched plus `causal`:
  *   0  none (identical to repops_gemm_strided_batched);

@@ -19,7 +19,7 @@ F32, I32, U8, BF16, F16 = 1, 2, 3, 4, 5
 _DT = {torch.float32: F32, torch.int32: I32, torch.uint8: U8, torch.bfloat16: BF16, torch.float16: F16}
 
 __all__ = [
-    "repops_gemm", "repops_gemm_strided_batched", "repops_causal_suffix_flags", "repops_copy2d_batched", "repops_sum_rows", "repops_sum_cols_seq", "repops_tree_sum",
+    "repops_gemm", "repops_gemm_post", "repops_gemm_strided_batched", "repops_causal_suffix_flags", "repops_copy2d_batched", "repops_sum_rows", "repops_sum_cols_seq", "repops_tree_sum",
     "repops_softmax", "repops_softmax_backward", "repops_layernorm", "repops_layernorm_backward",
     "repops_layernorm_backward_params", "repops_cross_entropy", "repops_exp", "repops_log", "repops_tanh",
     "repops_rsqrt", "repops_gelu", "repops_gelu_backward", "repops_relu", "repops_relu_backward", "repops_sin", "repops_cos", "repops_erf", "repops_gelu_erf", "repops_convert", "repops_gemm_ex",
@@ -144,6 +144,37 @@ def repops_gemm(A, B, transA=False, transB=False, epi=EPI_NONE, bias=None, scale
     if t0 is not None:
         _TIMER.end("gemm", t0, 2 * M * N * K, stream)
     return out
+
+
+POST_GELU, POST_GELU_BACKWARD = 1, 2
+
+
+def repops_gemm_post(A, B, post, out2, X=None, transA=False, transB=False, epi=EPI_NONE, bias=None, scale=1.0,
+                     out=None, stream=None):
+    """R-GEMM with a fused elementwise consumer (repops.h repops_gemm_post): returns (C, C2)
+    with C2 = R-GELU(C) (post = POST_GELU) or R-GELU-backward at X with dy = C."""
+    _f32(A, "A"), _f32(B, "B"), _f32(out2, "out2")
+    M = A.shape[1] if transA else A.shape[0]
+    K = A.shape[0] if transA else A.shape[1]
+    N = B.shape[0] if transB else B.shape[1]
+    if (B.shape[1] if transB else B.shape[0]) != K:
+        raise RepopsError(f"repops_gemm_post: inner dimensions differ ({K})")
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.float32, device=A.device)
+    for t, nm in ((out, "out"), (out2, "out2")) + (((X, "X"),) if post == POST_GELU_BACKWARD else ()):
+        _f32(t, nm)
+        if tuple(t.shape) != (M, N):
+            raise RepopsError(f"repops_gemm_post: {nm} must be ({M}, {N})")
+    if epi == EPI_BIAS and (bias is None or bias.numel() < N):
+        raise RepopsError(f"repops_gemm_post: EPI_BIAS needs >= {N} bias values")
+    t0 = _TIMER.begin(stream) if _TIMER else None
+    check(lib().repops_gemm_post(M, N, K, _p(A), _ld(A), int(bool(transA)), _p(B), _ld(B), int(bool(transB)),
+                                 int(epi), _p(bias), float(scale), _p(out), _ld(out), int(post), _p(X),
+                                 _ld(X) if X is not None else 0, _p(out2), _ld(out2), _stream(stream)),
+          "repops_gemm_post")
+    if t0 is not None:
+        _TIMER.end("gemm", t0, 2 * M * N * K, stream)
+    return out, out2
 
 
 def repops_gemm_strided_batched(A, B, C_out, M, N, K, lda, ldb, ldc, sA, sB, sC, batch, transA=False,

@@ -91,6 +91,8 @@ SIGNATURES = {
     "repops_flip_bit": (i32, [vp, i64, i32, vp]),
     "repops_transpose": (i32, [vp, i64, i64, i64, vp, i64, vp]),
     "repops_copy2d_batched": (i32, [vp, i64, i64, i64, i64, vp, i64, i64, i64, vp]),
+    "repops_gemm_post": (i32, [i64, i64, i64, vp, i64, i32, vp, i64, i32, i32, vp, f32, vp, i64, i32, vp, i64, vp,
+                               i64, vp]),
     "repops_rmsnorm": (i32, [vp, vp, i64, i64, f32, vp, vp, vp]),
     "repops_copy2d": (i32, [vp, i64, i64, i64, vp, i64, vp]),
     "repops_swiglu": (i32, [vp, vp, i64, vp, vp]),

@@ -200,7 +200,8 @@ static int gemm_common(int64_t M, int64_t N, int64_t K, const float *A, int64_t 
                        int64_t sA1, const float *B, int64_t ldb, int transB, int64_t sB0, int64_t sB1, int epi,
                        const float *bias, float scale, float *C, int64_t ldc, int64_t sC0, int64_t sC1, int64_t b0,
                        int64_t b1, void *stream, int force_cfg, int causal = 0, const uint8_t *kflags = nullptr,
-                       int64_t ldf = 0, int64_t sF0 = 0, int64_t sF1 = 0) {
+                       int64_t ldf = 0, int64_t sF0 = 0, int64_t sF1 = 0, int post = 0, const float *X = nullptr,
+                       int64_t ldx = 0, float *C2 = nullptr, int64_t ldc2 = 0) {
     REQ(M >= 0 && N >= 0 && K >= 0 && b0 >= 0 && b1 >= 0, "gemm: negative extent");
     REQ(causal >= 0 && causal <= 2, "gemm: causal mode %d not in {0, 1, 2}", causal);
     REQ(causal != 2 || (kflags && ldf >= N && !transA && !transB), "gemm: causal 2 needs kflags, ldf >= N, NN");
@@ -228,12 +229,13 @@ static int gemm_common(int64_t M, int64_t N, int64_t K, const float *A, int64_t 
     p.causal = causal;
     p.kflags = kflags;
     p.ldf = ldf; p.sF0 = sF0; p.sF1 = sF1;
+    p.post = post; p.X = X; p.ldx = ldx; p.C2 = C2; p.ldc2 = ldc2;
     if (force_cfg < 0) force_cfg = g_force_cfg.load(std::memory_order_relaxed);
     // Large single NN products run as (A^T)^T B: A is transposed (a bit-exact copy) into a
     // stream-ordered temporary and the A^T-tile kernel runs -- the row-major A tile costs
     // the shared->shared transpose of every K tile (~8 % at 8192^3), one transpose pass
     // costs < 1 %.  The K order of every output is unchanged, so are its bits (R2).
-    if (!transA && causal == 0 && force_cfg < 0 && b0 * b1 == 1 && K > 0 && p.vecA && (double)M * N * K >= 1073741824.0 &&
+    if (!transA && causal == 0 && post == 0 && force_cfg < 0 && b0 * b1 == 1 && K > 0 && p.vecA && (double)M * N * K >= 1073741824.0 &&
         M % 4 == 0) {
         void *tmp = nullptr;
         cudaStream_t st = S(stream);
@@ -270,6 +272,31 @@ int repops_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, in
                 int transB, int epi, const float *bias, float scale, float *C, int64_t ldc, void *stream) {
     return gemm_common(M, N, K, A, lda, transA, 0, 0, B, ldb, transB, 0, 0, epi, bias, scale, C, ldc, 0, 0, 1, 1,
                        stream, -1);
+}
+
+int repops_gemm_post(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, int transA, const float *B,
+                     int64_t ldb, int transB, int epi, const float *bias, float scale, float *C, int64_t ldc, int post,
+                     const float *X, int64_t ldx, float *C2, int64_t ldc2, void *stream) {
+    REQ(post == REPOPS_POST_GELU || post == REPOPS_POST_GELU_BACKWARD, "gemm_post: unknown post %d", post);
+    REQ(C2 && ldc2 >= N && (post != REPOPS_POST_GELU_BACKWARD || (X && ldx >= N)), "gemm_post: bad C2 / X");
+    if (M == 0 || N == 0) return REPOPS_OK;
+    GemmParams q{};
+    q.M = M; q.N = N; q.K = K; q.transA = transA ? 1 : 0; q.transB = transB ? 1 : 0;
+    q.vecA = a16(A) && lda % 4 == 0;
+    q.vecB = a16(B) && ldb % 4 == 0;
+    q.post = post;
+    if (gemm_tn_eligible(q) && g_force_cfg.load(std::memory_order_relaxed) < 0) {
+        int st = gemm_common(M, N, K, A, lda, transA, 0, 0, B, ldb, transB, 0, 0, epi, bias, scale, C, ldc, 0, 0, 1,
+                             1, stream, -1, 0, nullptr, 0, 0, 0, post, X, ldx, C2, ldc2);
+        return st;
+    }
+    // not the A^T kernel's shape: the GEMM, then the separate elementwise launch (same bits)
+    REQ(ldc == N && ldc2 == N && (post != REPOPS_POST_GELU_BACKWARD || ldx == N),
+        "gemm_post: the unfused fallback needs contiguous C, C2 and X");
+    int st = repops_gemm(M, N, K, A, lda, transA, B, ldb, transB, epi, bias, scale, C, ldc, stream);
+    if (st != REPOPS_OK) return st;
+    return post == REPOPS_POST_GELU ? repops_gelu(C, M * N, C2, stream)
+                                    : repops_gelu_backward(X, C, M * N, C2, stream);
 }
 
 int repops_gemm_strided_batched(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, int transA, int64_t sA0,

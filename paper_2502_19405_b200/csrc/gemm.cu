@@ -459,27 +459,38 @@ cudaError_t launch_cfg(const GemmParams &p, cudaStream_t s) {
 //   15..18: stage / BK variants of 10; 19: 16 x 32 latency tiles
 //   20, 21: gemm_tn.cu 128 x 128 full-tile A^T kernel (BK 32 / 16)
 int gemm_num_cfgs() { return 25; }
+
+int gemm_tn_choice(const GemmParams &p) {
+    if (!gemm_tn_eligible(p)) return p.post != 0 ? 22 : -1;
+    if (p.post == 0 && p.M * p.N * p.batch0 * p.batch1 <= (int64_t)ro_host::num_sms() * 16 * 32 * 4) return -1;
+    // A^T-stored problems: gemm_tn.cu's 128 x 128 (cfg 20) and 64 x 128 (cfg 22) tiles and
+    // the 128 x 64 tiles of gemm.cu.  Cost = tiles on the busiest SM x tile work / rate
+    // (measured on B200: one or two CTAs of either kernel nearly saturate an SM, so the
+    // SM-count quantisation of the tile count is what decides; tools/gemm_tune.py)
+    struct C { int id, bm, bn; double rate; };
+    static const C cand[] = {{20, 128, 128, 66.9}, {22, 64, 128, 66.0}, {5, 128, 64, 60.0}};
+    const int64_t nb = p.batch0 * p.batch1;
+    const int64_t sms = ro_host::num_sms();
+    double best = 1e300;
+    int cfg = -1;
+    for (const C &c : cand) {
+        if (p.post != 0 && c.id == 5) continue;
+        const int64_t tiles = ((p.M + c.bm - 1) / c.bm) * ((p.N + c.bn - 1) / c.bn) * nb;
+        const double t = (double)((tiles + sms - 1) / sms) * c.bm * c.bn / c.rate;
+        if (t < best) { best = t; cfg = c.id; }
+    }
+    return cfg;
+}
 std::atomic<int> g_gemm_smem_floor{0};
 
 cudaError_t gemm_launch(const GemmParams &p, cudaStream_t s, int force_cfg) {
     if (p.M == 0 || p.N == 0 || p.batch0 * p.batch1 == 0) return cudaSuccess;
     if (p.batch0 * p.batch1 > 65535) return cudaErrorInvalidValue;
     int cfg = force_cfg;
-    if (cfg < 0 && gemm_tn_eligible(p) && p.M * p.N * p.batch0 * p.batch1 > (int64_t)ro_host::num_sms() * 16 * 32 * 4) {
-        // A^T-stored problems: gemm_tn.cu's 128 x 128 (cfg 20) and 64 x 128 (cfg 22) tiles and
-        // the 128 x 64 tiles here.  Cost = tiles on the busiest SM x tile work / rate
-        // (measured on B200: one or two CTAs of either kernel nearly saturate an SM, so the
-        // SM-count quantisation of the tile count is what decides; tools/gemm_tune.py)
-        struct C { int id, bm, bn; double rate; };
-        static const C cand[] = {{20, 128, 128, 66.9}, {22, 64, 128, 66.0}, {5, 128, 64, 60.0}};
-        const int64_t nb = p.batch0 * p.batch1;
-        const int64_t sms = ro_host::num_sms();
-        double best = 1e300;
-        for (const C &c : cand) {
-            const int64_t tiles = ((p.M + c.bm - 1) / c.bm) * ((p.N + c.bn - 1) / c.bn) * nb;
-            const double t = (double)((tiles + sms - 1) / sms) * c.bm * c.bn / c.rate;
-            if (t < best) { best = t; cfg = c.id; }
-        }
+    if (cfg < 0) cfg = gemm_tn_choice(p);
+    if (p.post != 0) {  // fused elementwise epilogue: gemm_tn's 128 x 128 / 64 x 128 tiles only
+        if (!gemm_tn_eligible(p)) return cudaErrorInvalidValue;
+        return gemm_tn_launch(p, s, cfg == 20 ? 32 : 6432);
     }
     if (cfg < 0) {
         // Wave-quantisation cost model (bits-neutral choice): time ~ waves x tile

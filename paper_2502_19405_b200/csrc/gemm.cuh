@@ -28,6 +28,13 @@ struct GemmParams {
     int causal;
     const uint8_t *kflags;
     int64_t ldf, sF0, sF1;
+    // fused elementwise consumer of C (gemm_tn only; bits of C2 = the separate kernel's):
+    // 0 none; 1 = C2 = R-GELU(C); 2 = C2 = R-GELU backward at X with dy = C
+    int post;
+    const float *X;
+    int64_t ldx;
+    float *C2;
+    int64_t ldc2;
 };
 
 // force_cfg: -1 = automatic, else one of gemm_num_cfgs() tile configurations (bits-neutral)
@@ -36,5 +43,7 @@ int gemm_num_cfgs();
 // gemm_tn.cu: 128 x 128 x 16 full-tile kernel for op(A) = A^T, op(B) = B (bits-neutral)
 bool gemm_tn_eligible(const GemmParams &p);
 cudaError_t gemm_tn_launch(const GemmParams &p, cudaStream_t s, int bk);
+// cost-model choice between gemm_tn's tiles for an eligible problem (20 / 22) or -1
+int gemm_tn_choice(const GemmParams &p);
 // tuning hook: minimum dynamic shared memory per GEMM CTA (limits occupancy; bits-neutral)
 extern std::atomic<int> g_gemm_smem_floor;

@@ -45,7 +45,7 @@ RO_DEV void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 // BM x BN CTA tile, warps WM (m) x WN (n) with WM * WN = 4: thread (ty, tx) owns rows
 // ty*4 + g*4*TYN + {0..3} (g < GM) and columns tx*4 + h*4*TXN + {0..3} (h < GN)
-template <int BM, int BN, int WM, int STAGES, int BK, int MINB>
+template <int BM, int BN, int WM, int STAGES, int BK, int MINB, int POST>
 __global__ void __launch_bounds__(THREADS, MINB) gemm_tn_kernel(GemmParams p) {
     constexpr int WN = 4 / WM, TYN = 4 * WM, TXN = 8 * WN;
     constexpr int TM = BM / TYN, TN = BN / TXN, GM = TM / 4, GN = TN / 4;
@@ -211,17 +211,28 @@ __global__ void __launch_bounds__(THREADS, MINB) gemm_tn_kernel(GemmParams p) {
                     for (int c = 0; c < 4; ++c)
                         if (n + c < p.N) crow[n + c] = v[c];
                 }
+                if constexpr (POST != 0) {
+                    // the elementwise consumer of the stored C values, the same device
+                    // functions as repops_gelu / repops_gelu_backward (same bits)
+                    float *c2row = p.C2 + b0 * p.sC0 + b1 * p.sC1 + m * p.ldc2;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        if (n + c >= p.N) continue;
+                        c2row[n + c] = POST == 1 ? canon(ro::gelu_rn(v[c]))
+                                                 : canon(ro::gelu_grad_rn(__ldg(p.X + m * p.ldx + n + c), v[c]));
+                    }
+                }
             }
         }
     }
 }
 
-template <int BM, int BN, int WM, int STAGES, int BK, int MINB>
+template <int BM, int BN, int WM, int STAGES, int BK, int MINB, int POST>
 cudaError_t launch_tn(const GemmParams &p, cudaStream_t s) {
     size_t smem = (size_t)STAGES * BK * (BM + BN) * sizeof(float);
     const size_t floor_bytes = (size_t)g_gemm_smem_floor.load(std::memory_order_relaxed);
     if (floor_bytes > smem) smem = floor_bytes;  // occupancy experiments only (tools/overlap_probe.py)
-    auto kern = gemm_tn_kernel<BM, BN, WM, STAGES, BK, MINB>;
+    auto kern = gemm_tn_kernel<BM, BN, WM, STAGES, BK, MINB, POST>;
     static size_t attr = 0;
     if (smem > attr) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -245,13 +256,23 @@ cudaError_t gemm_tn_launch(const GemmParams &p, cudaStream_t s, int variant) {
     if (!gemm_tn_eligible(p)) return cudaErrorInvalidValue;
     // 3-stage rings.  128 x 128 (warps 4 x 1, 8 x 16 per thread, 2 CTAs / SM):
     // 3 x 32 KB (BK 32) / 3 x 16 KB (BK 16); 64 x 128 (warps 2 x 2, 8 x 8 per thread,
-    // 3 CTAs / SM): 3 x 24 KB / 3 x 12 KB
+    // 3 CTAs / SM): 3 x 24 KB / 3 x 12 KB; 64 x 64 (8 x 4 per thread, 4 CTAs / SM)
+    if (p.post == 1) {
+        if (variant == 32) return launch_tn<128, 128, 4, 3, 32, 2, 1>(p, s);
+        if (variant == 6432) return launch_tn<64, 128, 2, 3, 32, 3, 1>(p, s);
+        return cudaErrorInvalidValue;
+    }
+    if (p.post == 2) {
+        if (variant == 32) return launch_tn<128, 128, 4, 3, 32, 2, 2>(p, s);
+        if (variant == 6432) return launch_tn<64, 128, 2, 3, 32, 3, 2>(p, s);
+        return cudaErrorInvalidValue;
+    }
     switch (variant) {
-        case 32: return launch_tn<128, 128, 4, 3, 32, 2>(p, s);
-        case 16: return launch_tn<128, 128, 4, 3, 16, 2>(p, s);
-        case 6432: return launch_tn<64, 128, 2, 3, 32, 3>(p, s);
-        case 6416: return launch_tn<64, 128, 2, 3, 16, 3>(p, s);
-        case 646432: return launch_tn<64, 64, 2, 3, 32, 4>(p, s);
+        case 32: return launch_tn<128, 128, 4, 3, 32, 2, 0>(p, s);
+        case 16: return launch_tn<128, 128, 4, 3, 16, 2, 0>(p, s);
+        case 6432: return launch_tn<64, 128, 2, 3, 32, 3, 0>(p, s);
+        case 6416: return launch_tn<64, 128, 2, 3, 16, 3, 0>(p, s);
+        case 646432: return launch_tn<64, 64, 2, 3, 32, 4, 0>(p, s);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -36,7 +36,7 @@ import torch
 
 import synth
 
-from . import (EPI_BIAS, EPI_SCALE, CommitPlan, repops_add, repops_attention_fwd, repops_attention_fwd_supported, repops_cross_entropy, repops_embedding,
+from . import (EPI_BIAS, EPI_SCALE, POST_GELU, POST_GELU_BACKWARD, CommitPlan, repops_add, repops_attention_fwd, repops_attention_fwd_supported, repops_cross_entropy, repops_embedding,
                repops_embedding_backward, repops_gelu, repops_gelu_backward, repops_gemm,
                repops_gemm_strided_batched, repops_layernorm, repops_layernorm_backward,
                repops_layernorm_backward_params, repops_softmax, repops_softmax_backward, repops_sum_cols_seq,
@@ -162,6 +162,11 @@ class GPT2Step:
         # GPT-2 shape the fused kernel (1 CTA / SM, 213 KB of shared memory) measured 307 us
         # per layer vs 253 us for the three tuned launches (tools/attn_fused_bench.py)
         self.fused_attention = False
+        # GELU / GELU-backward fused into the FC / FC2-dgrad GEMM epilogues (repops_gemm_post):
+        # same bits, but measured slower in the step (80.05 -> 80.43 ms; the tanh chain in the
+        # epilogue of a 2-3 CTA/SM GEMM hides latency worse than the standalone HBM-bound
+        # kernels), so off by default
+        self.fuse_gelu = False
         # backward: weight / bias / LN-parameter gradients on an aux stream beside the dgrads
         self.aux_wgrad = not structure_only
         # the aux stream carries critical-path work (joined every layer): high priority, so
@@ -279,6 +284,15 @@ class GPT2Step:
         # the GEMM runs TN (A^T tiles are 10-40% faster than row-major A on sm_100a,
         # DESIGN.md §5); data movement only, consumed by the very next GEMM
         self.xT = E(max(c.vocab, c.ffn, 3 * d) * M)
+
+    def _gemm_tn_post(self, X, B, post, out2, Xpost=None, **kw):
+        """_gemm_tn with the elementwise consumer fused into the GEMM epilogue
+        (repops_gemm_post: C2 = GELU(C) or GELU-backward at Xpost with dy = C)."""
+        from . import repops_gemm_post, repops_transpose
+        rows, cols = X.shape
+        xt = self.xT[:rows * cols].view(cols, rows)
+        repops_transpose(X, out=xt)
+        return repops_gemm_post(xt, B, post, out2, X=Xpost, transA=True, **kw)
 
     def _gemm_tn(self, X, B, **kw):
         """repops_gemm(X, B, **kw) computed as (X^T)^T B: X^T is written to the
@@ -478,10 +492,14 @@ class GPT2Step:
                     repops_layernorm(a["xmid"], W("ln2.g"), W("ln2.b"), c.ln_eps, out=a["ln2"], mean=a["mu2"],
                                      rstd=a["rs2"])
                     self._hook(f"h{l}/ln2")
-                    self._gemm_tn(a["ln2"], W("fc.w"), epi=EPI_BIAS, bias=W("fc.b"), out=a["fc"])
-                    self._hook(f"h{l}/fc")
-                    repops_gelu(a["fc"], out=a["gelu"])
-                    self._hook(f"h{l}/gelu")
+                    if self._fault is None and self.fuse_gelu:  # GELU fused into the FC GEMM's epilogue
+                        self._gemm_tn_post(a["ln2"], W("fc.w"), POST_GELU, a["gelu"], epi=EPI_BIAS, bias=W("fc.b"),
+                                           out=a["fc"])
+                    else:                    # fault injection: per-op launches and hooks
+                        self._gemm_tn(a["ln2"], W("fc.w"), epi=EPI_BIAS, bias=W("fc.b"), out=a["fc"])
+                        self._hook(f"h{l}/fc")
+                        repops_gelu(a["fc"], out=a["gelu"])
+                        self._hook(f"h{l}/gelu")
                     self._gemm_tn(a["gelu"], W("fc2.w"), epi=EPI_BIAS, bias=W("fc2.b"), out=a["fc2"])
                     self._hook(f"h{l}/fc2")
                     repops_add(a["xmid"], a["fc2"], out=self.x[l + 1])
@@ -658,11 +676,16 @@ class GPT2Step:
                         self._hook(f"h{l}/ln1_params")
 
                     # FC2
-                    self._gemm_tn(dout, self.wT[p + "fc2.w"], out=g["dgelu"])
-                    self._hook(f"h{l}/fc2_dgrad")
-                    self._aux(w_fc2)
-                    repops_gelu_backward(a["fc"], g["dgelu"], out=g["dfc"])
-                    self._hook(f"h{l}/gelu_bwd")
+                    if self._fault is None and self.fuse_gelu:  # GELU backward fused into the FC2 dgrad
+                        self._gemm_tn_post(dout, self.wT[p + "fc2.w"], POST_GELU_BACKWARD, g["dfc"], Xpost=a["fc"],
+                                           out=g["dgelu"])
+                        self._aux(w_fc2)
+                    else:
+                        self._gemm_tn(dout, self.wT[p + "fc2.w"], out=g["dgelu"])
+                        self._hook(f"h{l}/fc2_dgrad")
+                        self._aux(w_fc2)
+                        repops_gelu_backward(a["fc"], g["dgelu"], out=g["dfc"])
+                        self._hook(f"h{l}/gelu_bwd")
                     # FC
                     self._aux(w_fc)
                     self._gemm_tn(g["dfc"], self.wT[p + "fc.w"], out=g["dln2"])

@@ -149,6 +149,28 @@ def test_copy2d_batched_places_blocks_bit_exactly():
         assert np.array_equal(host(full).view(np.uint32), ref.view(np.uint32))
 
 
+@pytest.mark.parametrize("M,N,K,tA", [(256, 384, 96, 1), (4096 // 8, 3072 // 4, 768 // 4, 1), (130, 200, 77, 1),
+                                      (64, 96, 40, 0)])
+@pytest.mark.parametrize("post", [1, 2])
+def test_gemm_post_fused_gelu(M, N, K, tA, post):
+    # R-GEMM with GELU (post 1) or GELU backward at X (post 2) fused into the epilogue:
+    # C and C2 equal the GEMM followed by the separate elementwise launch, and the oracle
+    # (A^T kernel shapes fused; the others -- ragged / NN -- take the unfused fallback)
+    A, B = synth.gemm_inputs((M, N, K), "gpost")
+    A = (A * np.float32(2.0)).astype(np.float32)
+    X = synth.uniform(91, (M, N), 4.0)
+    bias = synth.uniform(92, N)
+    Ain = np.ascontiguousarray(A.T) if tA else A
+    epi = 1 if post == 1 else 0
+    C, C2 = R.repops_gemm_post(dev(Ain), dev(B), post, torch.empty((M, N), device="cuda"),
+                               X=dev(X) if post == 2 else None, transA=bool(tA), epi=epi,
+                               bias=dev(bias) if epi else None)
+    refC = oracle.gemm(Ain, B, transA=bool(tA), epi=epi, bias=bias if epi else None)
+    assert_bits(host(C), refC, "fused GEMM C")
+    ref2 = oracle.gelu(refC) if post == 1 else oracle.gelu_backward(X, refC)
+    assert_bits(host(C2), ref2, f"fused GEMM C2 post {post}")
+
+
 # ------------------------------------------------------------------ causal structure (f4)
 def test_gemm_causal_skip_scores():
     # causal 1: tiles strictly above the diagonal are not written; every other output
