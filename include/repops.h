@@ -221,6 +221,21 @@ int repops_attention_fwd(int64_t T, int64_t hd, const float *Q, const float *K, 
                          int64_t sp1, float *O, int64_t ldo, int64_t so0, int64_t so1, int64_t batch0,
                          int64_t batch1, void *stream);
 
+/* Attention scores + softmax fused, the probabilities only (f4, R7, R29, R31):
+ * per (b0, b1) as above, P = R-SOFTMAX(R-GEMM(Q, K^T) with the SCALE epilogue) (causal:
+ * row i keeps keys j <= i, masked P = +0, every element of the [T][T] block written).
+ * The scores stay in shared memory (operator scratch, R29); with causal set only the key
+ * blocks a CTA's rows read are computed (R31).  Bit-identical to
+ * repops_gemm_strided_batched(SCALE) -> repops_softmax.  Q, K: rows of stride ld, head
+ * dim hd, 16-byte aligned; P: [T][T] blocks at P + b0 sp0 + b1 sp1 (row stride T),
+ * device, caller-owned.  Supported: hd = 64, T % 32 == 0, T <= 1024
+ * (repops_attention_probs_supported), else REPOPS_ESHAPE; REPOPS_EINVAL: null,
+ * misaligned, ld < hd. */
+int repops_attention_probs_supported(int64_t T, int64_t hd);
+int repops_attention_probs(int64_t T, int64_t hd, const float *Q, const float *K, int64_t ld, int64_t s0,
+                           int64_t s1, float scale, int causal, float *P, int64_t sp0, int64_t sp1,
+                           int64_t batch0, int64_t batch1, void *stream);
+
 /* ------------------------------------------------------------------ elementwise
  * Software math (R5/R6): fixed IEEE-RN op chains. */
 int repops_exp(const float *x, int64_t n, float *y, void *stream);

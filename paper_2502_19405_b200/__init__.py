@@ -23,7 +23,8 @@ __all__ = [
     "repops_softmax", "repops_softmax_backward", "repops_layernorm", "repops_layernorm_backward",
     "repops_layernorm_backward_params", "repops_cross_entropy", "repops_exp", "repops_log", "repops_tanh",
     "repops_rsqrt", "repops_gelu", "repops_gelu_backward", "repops_relu", "repops_relu_backward", "repops_sin", "repops_cos", "repops_erf", "repops_gelu_erf", "repops_convert", "repops_gemm_ex",
-    "repops_attention_fwd", "repops_attention_fwd_supported", "repops_rand_uniform",
+    "repops_attention_fwd", "repops_attention_fwd_supported", "repops_attention_probs",
+    "repops_attention_probs_supported", "repops_rand_uniform",
     "repops_dropout", "repops_dropout_backward",
     "repops_gelu_erf_backward", "repops_rope_tables", "repops_ipc_alloc", "repops_ipc_open", "repops_ipc_close",
     "repops_ipc_free", "repops_p2p_tree_combine", "repops_p2p_signal", "repops_p2p_wait", "repops_add", "repops_embedding",
@@ -215,6 +216,33 @@ def repops_causal_suffix_flags(B, K, N, ldb, sB, batch, out=None, ldf=None, sF=N
 
 
 # ------------------------------------------------------------------ fused attention (f4)
+def repops_attention_probs_supported(T, hd):
+    return bool(lib().repops_attention_probs_supported(int(T), int(hd)))
+
+
+def repops_attention_probs(qkv, T, hd, ld, s, q_off, k_off, batch, P, sp, scale=1.0, causal=True, stream=None):
+    """Scores + softmax fused over a strided batch (element offsets / strides into the
+    storage of qkv and P): P = causal R-SOFTMAX(R-GEMM(Q K^T) * scale), the scores never
+    leaving shared memory -- bit-identical to repops_gemm_strided_batched(SCALE) ->
+    repops_softmax."""
+    _f32(qkv, "qkv"), _f32(P, "P")
+    if P.device != qkv.device:
+        raise ValueError("P must be on the device of qkv")
+    nb = int(batch[0]) * int(batch[1])
+    if nb and P.storage_offset() + (int(batch[0]) - 1) * int(sp[0]) + (int(batch[1]) - 1) * int(sp[1]) + T * T > \
+            P.untyped_storage().nbytes() // 4:
+        raise ValueError("P too small for the batch")
+    base = qkv.data_ptr()
+    t0 = _TIMER.begin(stream) if _TIMER else None
+    check(lib().repops_attention_probs(int(T), int(hd), base + 4 * q_off, base + 4 * k_off, int(ld), int(s[0]),
+                                       int(s[1]), float(scale), int(bool(causal)), P.data_ptr(), int(sp[0]),
+                                       int(sp[1]), int(batch[0]), int(batch[1]), _stream(stream)),
+          "repops_attention_probs")
+    if t0 is not None:
+        _TIMER.end("gemm", t0, 2 * T * T * hd * nb, stream)
+    return P
+
+
 def repops_attention_fwd_supported(T, hd):
     return bool(lib().repops_attention_fwd_supported(int(T), int(hd)))
 

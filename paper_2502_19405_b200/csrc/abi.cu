@@ -329,6 +329,26 @@ int repops_causal_suffix_flags(const float *B, int64_t K, int64_t N, int64_t ldb
 // ------------------------------------------------------------------ fused attention (f4)
 int repops_attention_fwd_supported(int64_t T, int64_t hd) { return attention_fwd_supported(T, hd) ? 1 : 0; }
 
+int repops_attention_probs_supported(int64_t T, int64_t hd) { return attention_probs_supported(T, hd) ? 1 : 0; }
+
+int repops_attention_probs(int64_t T, int64_t hd, const float *Q, const float *K, int64_t ld, int64_t s0,
+                           int64_t s1, float scale, int causal, float *P, int64_t sp0, int64_t sp1,
+                           int64_t batch0, int64_t batch1, void *stream) {
+    REQ(T >= 0 && hd >= 0 && batch0 >= 0 && batch1 >= 0, "attention_probs: negative extent");
+    if (T == 0 || batch0 * batch1 == 0) return REPOPS_OK;
+    if (!attention_probs_supported(T, hd))
+        return fail(REPOPS_ESHAPE, "attention_probs: T = %lld, hd = %lld unsupported (hd 64, T %% 32 == 0, T <= 1024)",
+                    (long long)T, (long long)hd);
+    REQ(Q && K && P, "attention_probs: null pointer");
+    REQ(ld >= hd, "attention_probs: leading dimension < hd");
+    const bool al = a16(Q) && a16(K) && a16(P) && ld % 4 == 0 && s0 % 4 == 0 && s1 % 4 == 0 && sp0 % 4 == 0 &&
+                    sp1 % 4 == 0;
+    REQ(al, "attention_probs: rows must be 16-byte aligned");
+    return cuda_status(launch_attention_probs(T, Q, K, ld, s0, s1, scale, causal, P, sp0, sp1, batch0, batch1,
+                                              S(stream)),
+                       "attention_probs");
+}
+
 int repops_attention_fwd(int64_t T, int64_t hd, const float *Q, const float *K, const float *V, int64_t ld,
                          int64_t s0, int64_t s1, float scale, int causal, float *Sout, float *Pout, int64_t sp0,
                          int64_t sp1, float *O, int64_t ldo, int64_t so0, int64_t so1, int64_t batch0,

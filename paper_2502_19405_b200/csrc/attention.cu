@@ -50,9 +50,9 @@ struct AttnArgs {
     int64_t sp0, sp1;
     float *O;
     int64_t ldo, so0, so1;
-    int64_t batch1;
+    int64_t batch1, nbatch;
     int T;
-    int causal;
+    int causal, skip;
     float scale;
 };
 
@@ -79,13 +79,43 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(AttnArgs a) {
     float *Ss = Qt + HD * BM;          // [BM][T + 4] score rows, then probability rows
     float *Kc = Ss + BM * SLD;         // [2][KC][KLD] K chunks, later [2][KC][HD] V chunks
 
+    __shared__ unsigned long long vflags[2];  // V suffix (keys >= kend): [0] any non-finite, [1] all sign bits
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t bh = blockIdx.y, b0 = bh / a.batch1, b1 = bh % a.batch1;
-    const int q0 = blockIdx.x * BM;
+    // heaviest row blocks first (causal: block qb folds qb + 1 chunks), (batch, head) fastest
+    const int nqb = T / BM;
+    const int64_t bh = blockIdx.x % a.nbatch, b0 = bh / a.batch1, b1 = bh % a.batch1;
+    const int q0 = (nqb - 1 - (int)(blockIdx.x / a.nbatch)) * BM;
     const float *Q = a.Q + b0 * a.s0 + b1 * a.s1;
     const float *K = a.K + b0 * a.s0 + b1 * a.s1;
     const float *V = a.V + b0 * a.s0 + b1 * a.s1;
     const int nchunks = T / KC;
+    // R31: with the scores scratch (S not stored) and a causal mask, the rows of this block
+    // read keys < q0 + BM only: phase 1 computes the chunks that hold them, phase 3 folds
+    // them and applies the remaining fma(+0, V[j][n], acc) terms in closed form
+    const int nch = a.skip ? min(nchunks, (q0 + BM + KC - 1) / KC) : nchunks;
+    const int kend = nch * KC;
+    if (tid == 0) {
+        vflags[0] = 0ull;
+        vflags[1] = ~0ull;
+    }
+    __syncthreads();
+    if (kend < T) {
+        // per column n: bit n of [0] = some V[j][n], j >= kend, non-finite; of [1] = every
+        // such V[j][n] has its sign bit set (integer logic, loads independent of the rest)
+        const int cq = tid % (HD / 4);
+        unsigned nf = 0u, neg = 0xFu;
+        for (int j = kend + tid / (HD / 4); j < T; j += THREADS / (HD / 4)) {
+            const uint4 u = __ldg(reinterpret_cast<const uint4 *>(V + (int64_t)j * a.ld + cq * 4));
+            const unsigned w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                nf |= (((w[c] & 0x7F800000u) == 0x7F800000u) ? 1u : 0u) << c;
+                neg &= ((w[c] >> 31) << c) | ~(1u << c);
+            }
+        }
+        atomicOr(&vflags[0], (unsigned long long)nf << (4 * cq));
+        atomicAnd(&vflags[1], ~(((unsigned long long)(~neg & 0xFu)) << (4 * cq)));
+    }
 
     // K chunk 0 in flight while Q^T is staged
     load_chunk<KLD, KC, THREADS>(Kc, K, a.ld, tid);
@@ -106,8 +136,8 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(AttnArgs a) {
     {
         const int tx = (warp % WX) * 8 + (lane & 7);
         const int ty = (warp / WX) * 4 + (lane >> 3);
-        for (int ch = 0; ch < nchunks; ++ch) {
-            if (ch + 1 < nchunks)
+        for (int ch = 0; ch < nch; ++ch) {
+            if (ch + 1 < nch)
                 load_chunk<KLD, KC, THREADS>(Kc + ((ch + 1) & 1) * KC * KLD, K + (int64_t)(ch + 1) * KC * a.ld, a.ld,
                                              tid);
             cp_commit();
@@ -202,7 +232,9 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(AttnArgs a) {
         }
         const float rinv = __fdiv_rn(1.0f, tree128(p0, p1, p2, p3));
         float *Pg = a.P ? a.P + b0 * a.sp0 + b1 * a.sp1 + (int64_t)(q0 + r) * T : nullptr;
-        for (int b = 0; b < T; b += 128) {
+        if (Pg)
+            for (int i = kend + 4 * lane; i < T; i += 128) *reinterpret_cast<float4 *>(Pg + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int b = 0; b < kend; b += 128) {
             const int i = b + 4 * lane;
             const float4 v = *reinterpret_cast<const float4 *>(row + i);
             float o[4] = {v.x, v.y, v.z, v.w};
@@ -221,8 +253,8 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(AttnArgs a) {
         float2 acc[TM3][2];
 #pragma unroll
         for (int r = 0; r < TM3; ++r) acc[r][0] = acc[r][1] = make_float2(0.f, 0.f);
-        for (int ch = 0; ch < nchunks; ++ch) {
-            if (ch + 1 < nchunks)
+        for (int ch = 0; ch < nch; ++ch) {
+            if (ch + 1 < nch)
                 load_chunk<HD, KC, THREADS>(Kc + ((ch + 1) & 1) * KC * KLD, V + (int64_t)(ch + 1) * KC * a.ld, a.ld,
                                             tid);
             cp_commit();
@@ -252,6 +284,20 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(AttnArgs a) {
             }
             __syncthreads();
         }
+        if (kend < T) {
+            // the skipped terms fma(+0, V[j][n], acc), j >= kend (R31): a non-finite V gives
+            // NaN; otherwise only acc = -0 can change, to +0 unless every V[j][n] is negative
+            const unsigned long long nfm = vflags[0], negm = vflags[1];
+#pragma unroll
+            for (int r = 0; r < TM3; ++r)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int n = tx * 4 + c;
+                    float &x = (c & 1) ? acc[r][c >> 1].y : acc[r][c >> 1].x;
+                    if ((nfm >> n) & 1ull) x = __uint_as_float(0x7FC00000u);
+                    else if (__float_as_uint(x) == 0x80000000u && !((negm >> n) & 1ull)) x = 0.0f;
+                }
+        }
         float *Og = a.O + b0 * a.so0 + b1 * a.so1;
 #pragma unroll
         for (int r = 0; r < TM3; ++r) {
@@ -262,14 +308,167 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(AttnArgs a) {
     }
 }
 
+// ---------------------------------------------------------------- scores + softmax (P only)
+// The attention operator's first half for the GPT-2 training step (R29: S is operator
+// scratch, P is kept for the PV R-GEMM and the backward): one CTA of PS_THREADS threads owns
+// PS_BM query rows of one (batch, head); S is computed straight into shared memory with a
+// GEMM-sized register tile (4 queries x 8 keys per thread, d ascending from +0, then
+// canon(fmul(acc, scale))), then each warp runs softmax_warp's sequence on its rows and
+// writes P.  S never reaches HBM; bits equal repops_gemm(SCALE) -> repops_softmax.
+constexpr int PS_BM = 32, PS_THREADS = 256, PS_KB = 256, PS_DS = 8, PS_KLD = PS_DS + 4, PS_NST = 3;
+
+struct ProbArgs {
+    const float *Q, *K;
+    int64_t ld, s0, s1;
+    float *P;
+    int64_t sp0, sp1;
+    int64_t batch1, nbatch;
+    int T, causal;
+    float scale;
+};
+
+__global__ void __launch_bounds__(PS_THREADS, 2) attn_probs_kernel(ProbArgs a) {
+    extern __shared__ __align__(16) float sm[];
+    const int T = a.T, SLD = T + 4;
+    float *Qt = sm;                       // [HD][PS_BM]
+    float *Ss = Qt + HD * PS_BM;          // [PS_BM][T + 4]
+    float *Ks = Ss + PS_BM * SLD;         // [PS_NST][PS_KB][PS_KLD] ring of d-slices of a key block
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nqb = T / PS_BM;
+    const int64_t bh = blockIdx.x % a.nbatch, b0 = bh / a.batch1, b1 = bh % a.batch1;
+    const int q0 = (nqb - 1 - (int)(blockIdx.x / a.nbatch)) * PS_BM;
+    const float *Q = a.Q + b0 * a.s0 + b1 * a.s1;
+    const float *K = a.K + b0 * a.s0 + b1 * a.s1;
+    // causal: the rows read keys < q0 + PS_BM only (R31: the other scores are never read)
+    const int kneed = a.causal ? min(T, q0 + PS_BM) : T;
+
+#pragma unroll
+    for (int q = 0; q < PS_BM * HD / 4 / PS_THREADS; ++q) {
+        const int c = tid + q * PS_THREADS;
+        const int r = c % PS_BM, kq = (c / PS_BM) * 4;
+        const float4 v = __ldg(reinterpret_cast<const float4 *>(Q + (int64_t)(q0 + r) * a.ld + kq));
+        Qt[(kq + 0) * PS_BM + r] = v.x;
+        Qt[(kq + 1) * PS_BM + r] = v.y;
+        Qt[(kq + 2) * PS_BM + r] = v.z;
+        Qt[(kq + 3) * PS_BM + r] = v.w;
+    }
+
+    // thread tile: queries 4 qg .. 4 qg + 3, keys kb + 32 warp + kg + 4 j (j < 8)
+    const int qg = lane & 7, kg = lane >> 3;
+    for (int kb = 0; kb < kneed; kb += PS_KB) {
+        const int nk = min(PS_KB, kneed - kb);           // keys of this block that are read
+        const int nrows = (nk + 31) & ~31;               // staged rows (whole warps)
+        const bool active = 32 * warp < nk;              // warp-uniform
+        auto stage = [&](int buf, int ds) {              // K[kb .. kb + nrows)[ds .. ds + 8)
+            float *dst = Ks + buf * PS_KB * PS_KLD;
+            for (int c = tid; c < nrows * (PS_DS / 4); c += PS_THREADS) {
+                const int r = c / (PS_DS / 4), k4 = (c % (PS_DS / 4)) * 4;
+                cp16(dst + r * PS_KLD + k4, K + (int64_t)(kb + r) * a.ld + ds + k4);
+            }
+        };
+        float2 acc[8][2];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = make_float2(0.f, 0.f);  // +0 (R2)
+#pragma unroll
+        for (int s = 0; s < PS_NST - 1; ++s) {
+            stage(s, s * PS_DS);
+            cp_commit();
+        }
+        for (int s = 0; s < HD / PS_DS; ++s) {
+            if (s + PS_NST - 1 < HD / PS_DS) stage((s + PS_NST - 1) % PS_NST, (s + PS_NST - 1) * PS_DS);
+            cp_commit();
+            cp_wait<PS_NST - 1>();
+            __syncthreads();
+            if (active) {
+                const float *Kb = Ks + (s % PS_NST) * PS_KB * PS_KLD + (32 * warp + kg) * PS_KLD;
+#pragma unroll
+                for (int d4 = 0; d4 < PS_DS; d4 += 4) {
+                    float kv[8][4];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const float4 v = *reinterpret_cast<const float4 *>(Kb + 4 * j * PS_KLD + d4);
+                        kv[j][0] = v.x; kv[j][1] = v.y; kv[j][2] = v.z; kv[j][3] = v.w;
+                    }
+#pragma unroll
+                    for (int dd = 0; dd < 4; ++dd) {
+                        const float4 q4 = *reinterpret_cast<const float4 *>(Qt + (s * PS_DS + d4 + dd) * PS_BM + 4 * qg);
+                        const float2 qa = make_float2(q4.x, q4.y), qb = make_float2(q4.z, q4.w);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {  // fma(K[j,d], Q[i,d], acc): commutative
+                            const float2 kk = make_float2(kv[j][dd], kv[j][dd]);
+                            acc[j][0] = __ffma2_rn(kk, qa, acc[j][0]);
+                            acc[j][1] = __ffma2_rn(kk, qb, acc[j][1]);
+                        }
+                    }
+                }
+            }
+            __syncthreads();  // slice buffer free for the stage PS_NST slices on
+        }
+        if (active) {  // epilogue (R3, R10): S = canon(fmul(acc, scale))
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int key = kb + 32 * warp + kg + 4 * j;
+                float *srow = Ss + 4 * qg * SLD + key;
+                srow[0] = canon(__fmul_rn(acc[j][0].x, a.scale));
+                srow[SLD] = canon(__fmul_rn(acc[j][0].y, a.scale));
+                srow[2 * SLD] = canon(__fmul_rn(acc[j][1].x, a.scale));
+                srow[3 * SLD] = canon(__fmul_rn(acc[j][1].y, a.scale));
+            }
+        }
+    }
+    __syncthreads();
+
+    // softmax, warp per row (softmax_warp's order: R7), P rows written in full (+0 masked)
+    for (int r = warp; r < PS_BM; r += PS_THREADS / 32) {
+        float *row = Ss + r * SLD;
+        const int L = a.causal ? q0 + r + 1 : T;
+        float m = __uint_as_float(0xFF800000u);
+        for (int b = 0; b < L; b += 128) {
+            const int i = b + 4 * lane;
+            const float4 v = *reinterpret_cast<const float4 *>(row + i);
+            if (i < L) m = fmaxf(m, v.x);
+            if (i + 1 < L) m = fmaxf(m, v.y);
+            if (i + 2 < L) m = fmaxf(m, v.z);
+            if (i + 3 < L) m = fmaxf(m, v.w);
+        }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) m = fmaxf(m, __shfl_xor_sync(FULL, m, off));
+        m = (m == 0.0f) ? 0.0f : m;
+        float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;
+        for (int b = 0; b < L; b += 128) {  // e = exp(x - m) replaces x in place (computed once)
+            const int i = b + 4 * lane;
+            float4 v = *reinterpret_cast<const float4 *>(row + i);
+            if (i < L) p0 = __fadd_rn(p0, v.x = exp_rn(__fsub_rn(v.x, m)));
+            if (i + 1 < L) p1 = __fadd_rn(p1, v.y = exp_rn(__fsub_rn(v.y, m)));
+            if (i + 2 < L) p2 = __fadd_rn(p2, v.z = exp_rn(__fsub_rn(v.z, m)));
+            if (i + 3 < L) p3 = __fadd_rn(p3, v.w = exp_rn(__fsub_rn(v.w, m)));
+            if (i < L) *reinterpret_cast<float4 *>(row + i) = v;
+        }
+        const float rinv = __fdiv_rn(1.0f, tree128(p0, p1, p2, p3));
+        float *Pg = a.P + b0 * a.sp0 + b1 * a.sp1 + (int64_t)(q0 + r) * T;
+        for (int b = 0; b < T; b += 128) {
+            const int i = b + 4 * lane;
+            if (i >= T) break;  // T % 4 == 0: i < T covers the whole float4
+            float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (i < L) {
+                const float4 v = *reinterpret_cast<const float4 *>(row + i);
+                float o[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int c = 0; c < 4; ++c) o[c] = (i + c < L) ? canon(__fmul_rn(o[c], rinv)) : 0.0f;
+                y = make_float4(o[0], o[1], o[2], o[3]);
+            }
+            *reinterpret_cast<float4 *>(Pg + i) = y;  // kept in L2 for the PV R-GEMM
+        }
+    }
+}
+
 }  // namespace
 
-static int attn_variant() {  // 0 = (64, 128, 256), 1 = (32, 64, 128); REPOPS_ATTN_VARIANT overrides
-    static const int v = [] {
-        const char *e = getenv("REPOPS_ATTN_VARIANT");
-        return e ? atoi(e) : RO_ATTN_VARIANT_DEFAULT;
-    }();
-    return v;
+// (BM, KC, THREADS): 0 = (64, 128, 256), 1 = (32, 64, 128), 2 = (64, 64, 256), 3 = (32, 64, 256);
+// REPOPS_ATTN_VARIANT overrides
+static int attn_variant() {
+    const char *e = getenv("REPOPS_ATTN_VARIANT");  // read per launch: tests switch it in-process
+    return e ? atoi(e) : RO_ATTN_VARIANT_DEFAULT;
 }
 
 template <int BM, int KC>
@@ -277,7 +476,13 @@ static size_t smem_bytes(int64_t T) {
     return (size_t)(HD * BM + BM * (T + 4) + 2 * KC * KLD) * sizeof(float);
 }
 
-size_t attention_fwd_smem_bytes(int64_t T) { return attn_variant() ? smem_bytes<32, 64>(T) : smem_bytes<64, 128>(T); }
+size_t attention_fwd_smem_bytes(int64_t T) {
+    switch (attn_variant()) {
+        case 0: return smem_bytes<64, 128>(T);
+        case 2: return smem_bytes<64, 64>(T);
+        default: return smem_bytes<32, 64>(T);
+    }
+}
 
 bool attention_fwd_supported(int64_t T, int64_t hd) {
     return hd == HD && T > 0 && T % 128 == 0 && smem_bytes<64, 128>(T) <= 227 * 1024;
@@ -293,8 +498,9 @@ static cudaError_t launch_variant(const AttnArgs &a, int64_t batch, cudaStream_t
         if (e != cudaSuccess) return e;
         attr = smem;
     }
-    dim3 grid((unsigned)(a.T / BM), (unsigned)batch);
-    attn_fwd_kernel<BM, KC, THREADS><<<grid, THREADS, smem, s>>>(a);
+    AttnArgs b = a;
+    b.nbatch = batch;
+    attn_fwd_kernel<BM, KC, THREADS><<<(unsigned)(a.T / BM * batch), THREADS, smem, s>>>(b);
     return cudaGetLastError();
 }
 
@@ -303,7 +509,38 @@ cudaError_t launch_attention_fwd(int64_t T, const float *Q, const float *K, cons
                                  float *O, int64_t ldo, int64_t so0, int64_t so1, int64_t batch0, int64_t batch1,
                                  cudaStream_t s) {
     if (batch0 * batch1 == 0 || T == 0) return cudaSuccess;
-    AttnArgs a{Q, K, V, ld, s0, s1, S, P, sp0, sp1, O, ldo, so0, so1, batch1, (int)T, causal, scale};
-    return attn_variant() ? launch_variant<32, 64, 128>(a, batch0 * batch1, s)
-                          : launch_variant<64, 128, 256>(a, batch0 * batch1, s);
+    // the skip needs the scores to be scratch: a caller that stores S gets every column
+    AttnArgs a{Q, K, V, ld, s0, s1, S, P, sp0, sp1, O, ldo, so0, so1, batch1, 0, (int)T, causal, (causal && !S) ? 1 : 0,
+               scale};
+    switch (attn_variant()) {
+        case 0: return launch_variant<64, 128, 256>(a, batch0 * batch1, s);
+        case 2: return launch_variant<64, 64, 256>(a, batch0 * batch1, s);
+        case 3: return launch_variant<32, 64, 256>(a, batch0 * batch1, s);
+        default: return launch_variant<32, 64, 128>(a, batch0 * batch1, s);
+    }
+}
+
+
+static size_t probs_smem_bytes(int64_t T) {
+    return (size_t)(HD * PS_BM + PS_BM * (T + 4) + PS_NST * PS_KB * PS_KLD) * sizeof(float);
+}
+
+bool attention_probs_supported(int64_t T, int64_t hd) {
+    return hd == HD && T > 0 && T % PS_BM == 0 && T % 4 == 0 && probs_smem_bytes(T) <= 227 * 1024;
+}
+
+cudaError_t launch_attention_probs(int64_t T, const float *Q, const float *K, int64_t ld, int64_t s0, int64_t s1,
+                                   float scale, int causal, float *P, int64_t sp0, int64_t sp1, int64_t batch0,
+                                   int64_t batch1, cudaStream_t s) {
+    if (batch0 * batch1 == 0 || T == 0) return cudaSuccess;
+    const size_t smem = probs_smem_bytes(T);
+    static size_t attr = 0;
+    if (smem > attr) {
+        cudaError_t e = cudaFuncSetAttribute(attn_probs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = smem;
+    }
+    ProbArgs a{Q, K, ld, s0, s1, P, sp0, sp1, batch1, batch0 * batch1, (int)T, causal, scale};
+    attn_probs_kernel<<<(unsigned)(T / PS_BM * batch0 * batch1), PS_THREADS, smem, s>>>(a);
+    return cudaGetLastError();
 }

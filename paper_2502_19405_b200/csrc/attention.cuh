@@ -10,3 +10,7 @@ cudaError_t launch_attention_fwd(int64_t T, const float *Q, const float *K, cons
                                  int64_t s1, float scale, int causal, float *S, float *P, int64_t sp0, int64_t sp1,
                                  float *O, int64_t ldo, int64_t so0, int64_t so1, int64_t batch0, int64_t batch1,
                                  cudaStream_t s);
+bool attention_probs_supported(int64_t T, int64_t hd);
+cudaError_t launch_attention_probs(int64_t T, const float *Q, const float *K, int64_t ld, int64_t s0, int64_t s1,
+                                   float scale, int causal, float *P, int64_t sp0, int64_t sp1, int64_t batch0,
+                                   int64_t batch1, cudaStream_t s);

@@ -36,7 +36,9 @@ import torch
 
 import synth
 
-from . import (EPI_BIAS, EPI_SCALE, POST_GELU, POST_GELU_BACKWARD, CommitPlan, repops_add, repops_attention_fwd, repops_attention_fwd_supported, repops_cross_entropy, repops_embedding,
+from . import (EPI_BIAS, EPI_SCALE, POST_GELU, POST_GELU_BACKWARD, CommitPlan, repops_add, repops_attention_fwd,
+               repops_attention_fwd_supported, repops_attention_probs, repops_attention_probs_supported,
+               repops_cross_entropy, repops_embedding,
                repops_embedding_backward, repops_gelu, repops_gelu_backward, repops_gemm,
                repops_gemm_strided_batched, repops_layernorm, repops_layernorm_backward,
                repops_layernorm_backward_params, repops_softmax, repops_softmax_backward, repops_sum_cols_seq,
@@ -162,6 +164,11 @@ class GPT2Step:
         # GPT-2 shape the fused kernel (1 CTA / SM, 213 KB of shared memory) measured 307 us
         # per layer vs 253 us for the three tuned launches (tools/attn_fused_bench.py)
         self.fused_attention = False
+        # f4 (round 2): scores + causal softmax as one kernel (repops_attention_probs: the scores
+        # never leave shared memory, P is written for the PV R-GEMM and the backward), then the
+        # PV R-GEMM; same bits as the three launches.  Needs the scores to be operator scratch
+        # (R29); fault-injection runs keep the per-op launches
+        self.attn_probs = True
         # GELU / GELU-backward fused into the FC / FC2-dgrad GEMM epilogues (repops_gemm_post):
         # same bits, but measured slower in the step (80.05 -> 80.43 ms; the tanh chain in the
         # epilogue of a 2-3 CTA/SM GEMM hides latency worse than the standalone HBM-bound
@@ -172,6 +179,7 @@ class GPT2Step:
         # the aux stream carries critical-path work (joined every layer): high priority, so
         # the block scheduler prefers it over the commit side stream's SHA-256 CTAs
         self.aux = None if structure_only else torch.cuda.Stream(device=device, priority=-1)
+        self.attn_probs_ok = (not structure_only) and repops_attention_probs_supported(cfg.seq, cfg.hd)
         self.fused_attention_ok = (not structure_only) and repops_attention_fwd_supported(cfg.seq,
                                                                                             cfg.d // cfg.n_head)
         self.stash = {}
@@ -461,9 +469,19 @@ class GPT2Step:
                         # one fused kernel writes the same S, P and att bits (f4; no HBM round
                         # trip of S / P between launches); fault-injection runs keep the
                         # per-op launches so a flipped S bit propagates as in the graph
+                        # with attention as one operator (R29) the scores are scratch and never
+                        # leave shared memory: the kernel computes the key chunks its rows read
+                        # and closes the PV fold from V's suffix flags (R31); P stays for the backward
                         repops_attention_fwd(a["qkv"], T, hd, 3 * d, (T * 3 * d, hd), 0, d, 2 * d, (S_loc, H),
-                                             a["att"], d, (T * d, hd), S=a["S"], P=a["P"], sp=(H * T * T, T * T),
+                                             a["att"], d, (T * d, hd), S=None if self.attn_op else a["S"],
+                                             P=a["P"], sp=(H * T * T, T * T),
                                              scale=1.0 / np.sqrt(hd), causal=True)
+                    elif self.attn_op and self.attn_probs and self.attn_probs_ok and self._fault is None:
+                        repops_attention_probs(a["qkv"], T, hd, 3 * d, (T * 3 * d, hd), 0, d, (S_loc, H), a["P"],
+                                               (H * T * T, T * T), scale=1.0 / np.sqrt(hd), causal=True)
+                        repops_gemm_strided_batched(a["P"], a["qkv"], a["att"], M=T, N=hd, K=T, lda=T, ldb=3 * d,
+                                                    ldc=d, sA=(H * T * T, T * T), sB=(T * 3 * d, hd),
+                                                    sC=(T * d, hd), batch=(S_loc, H), offB=2 * d)
                     else:
                         # scores S = (Q K^T) * 1/sqrt(hd), batched over (local shard, head)
                         # with attention as one operator (R29) the scores are internal scratch: the

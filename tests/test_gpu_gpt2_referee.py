@@ -104,9 +104,11 @@ def test_block_forward_every_node(full):
     sl = slice(s * H * T, (s + 1) * H * T)
     # scores: the entries the causal softmax reads (column <= row); tiles above the diagonal
     # are not computed when the scores are operator-internal (R31)
-    S_gpu = st.act[l]["S"][sl].cpu().numpy().reshape(H, T, T)
-    low = np.tril(np.ones((T, T), bool))
-    same_bits(S_gpu[:, low], ref["scores"].reshape(H, T, T)[:, low], "internal scores (causal part)")
+    # (with the fused attention kernel the scores never leave shared memory; P checks them)
+    if not ((st.fused_attention and st.fused_attention_ok) or (st.attn_probs and st.attn_probs_ok)):
+        S_gpu = st.act[l]["S"][sl].cpu().numpy().reshape(H, T, T)
+        low = np.tril(np.ones((T, T), bool))
+        same_bits(S_gpu[:, low], ref["scores"].reshape(H, T, T)[:, low], "internal scores (causal part)")
     same_bits(st.act[l]["P"][sl].cpu().numpy(), ref["probs"], "internal probabilities")
 
 

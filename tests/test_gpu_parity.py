@@ -883,3 +883,98 @@ def test_attention_fwd_optional_outputs_and_shapes():
     assert not R.repops_attention_fwd_supported(100, 64)
     with pytest.raises(R.RepopsError):
         R.repops_attention_fwd(qkv, 100, hd, 3 * d, (T * 3 * d, hd), 0, d, 2 * d, (S_, H), O1, d, (T * d, hd))
+
+
+def _unfused_attention(qkv, S_, H, T, hd, scale, causal=True):
+    d = H * hd
+    Su = torch.empty(S_ * H * T, T, device="cuda")
+    Pu = torch.empty_like(Su)
+    Ou = torch.empty(S_ * T, d, device="cuda")
+    R.repops_gemm_strided_batched(qkv, qkv, Su, M=T, N=T, K=hd, lda=3 * d, ldb=3 * d, ldc=T, sA=(T * 3 * d, hd),
+                                  sB=(T * 3 * d, hd), sC=(H * T * T, T * T), batch=(S_, H), transB=True,
+                                  epi=R.EPI_SCALE, scale=scale, offB=d)
+    R.repops_softmax(Su, causal=causal, out=Pu)
+    R.repops_gemm_strided_batched(Pu, qkv, Ou, M=T, N=hd, K=T, lda=T, ldb=3 * d, ldc=d, sA=(H * T * T, T * T),
+                                  sB=(T * 3 * d, hd), sC=(T * d, hd), batch=(S_, H), offB=2 * d)
+    return Pu, Ou
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+@pytest.mark.parametrize("T", [512, 256, 128])
+def test_attention_fwd_causal_skip_equals_full(variant, T, monkeypatch):
+    """S not stored + causal (R29 scratch scores): the fused kernel computes only the key
+    chunks its rows read and applies the skipped fma(+0, V, acc) terms of the PV fold in
+    closed form (R31) -- P and O bit-identical to the full unfused composition, including
+    non-finite V entries in every row block's skipped suffix (each must turn that column
+    of every earlier row into NaN, as the full fold does) and signed zeros there"""
+    monkeypatch.setenv("REPOPS_ATTN_VARIANT", str(variant))
+    S_, H, hd = 2, 12, 64
+    d = H * hd
+    qkv_h = _attn_inputs(S_, H, T, hd, 33 + T)
+    # V of (shard 0, head 1): +inf in the last row, column 5; NaN at row T-65, column 17;
+    # a column of -0 / +0 suffixes (column 30) and all-negative suffixes (column 31)
+    v0 = 2 * d + 1 * hd
+    qkv_h[T - 1, v0 + 5] = np.inf
+    qkv_h[T - 65, v0 + 17] = np.nan
+    qkv_h[T // 2:T, v0 + 30] = -0.0
+    qkv_h[T // 2:T, v0 + 31] = -np.abs(qkv_h[T // 2:T, v0 + 31])
+    # (shard 1, head 11): -inf at row 64 (inside the second chunk), column 63
+    qkv_h[T + 64, 2 * d + 11 * hd + 63] = -np.inf
+    qkv = dev(qkv_h)
+    scale = 1.0 / np.sqrt(hd)
+    Pf = torch.full((S_ * H * T, T), 7.0, device="cuda")   # the kernel writes every element
+    Of = torch.empty(S_ * T, d, device="cuda")
+    R.repops_attention_fwd(qkv, T, hd, 3 * d, (T * 3 * d, hd), 0, d, 2 * d, (S_, H), Of, d, (T * d, hd), P=Pf,
+                           sp=(H * T * T, T * T), scale=scale, causal=True)
+    Pu, Ou = _unfused_attention(qkv, S_, H, T, hd, scale)
+    assert_bits(host(Pf), host(Pu), "P skip vs full")
+    Oh = host(Of)
+    assert_bits(Oh, host(Ou), "O skip vs full")
+    assert np.isnan(Oh[:T - 1, hd + 5]).all() and np.isnan(Oh[:T - 64, hd + 17]).all()
+    O2 = torch.empty_like(Of)   # neither S nor P stored
+    R.repops_attention_fwd(qkv, T, hd, 3 * d, (T * 3 * d, hd), 0, d, 2 * d, (S_, H), O2, d, (T * d, hd),
+                           scale=scale, causal=True)
+    assert_bits(host(O2), Oh, "O without P")
+
+
+@pytest.mark.parametrize("causal", [True, False])
+@pytest.mark.parametrize("T", [512, 1024, 256, 96, 32])
+def test_attention_probs_equals_unfused_and_oracle(T, causal):
+    """scores + softmax fused (the scores never leave shared memory; causal: only the key
+    blocks a row block reads): P bit-identical to R-GEMM(SCALE) -> R-SOFTMAX for every
+    (shard, head) -- T = 96 / 32 are ragged against the 256-key blocks -- and to the oracle
+    on sampled heads; every element of P is written (masked +0)"""
+    S_, H, hd = 2, 12 if T <= 512 else 3, 64
+    d = H * hd
+    qkv_h = _attn_inputs(S_, H, T, hd, 40 + T + causal)
+    # large scores (exp underflow to +0 for most of a row), a -inf and a NaN score source
+    qkv_h[5, 0:hd] *= 64.0
+    qkv_h[T + 7, d + 3 * hd + 1] = -np.inf
+    qkv_h[2, 5 * hd + 9] = np.nan
+    qkv = dev(qkv_h)
+    scale = 1.0 / np.sqrt(hd)
+    Pf = torch.full((S_ * H * T, T), 7.0, device="cuda")
+    assert R.repops_attention_probs_supported(T, hd)
+    R.repops_attention_probs(qkv, T, hd, 3 * d, (T * 3 * d, hd), 0, d, (S_, H), Pf, (H * T * T, T * T),
+                             scale=scale, causal=causal)
+    Pu, _ = _unfused_attention(qkv, S_, H, T, hd, scale, causal=causal)
+    Ph = host(Pf)
+    assert_bits(Ph, host(Pu), "P fused vs unfused")
+    for s_, h in ((0, 0), (1, H - 1)):
+        q = np.ascontiguousarray(qkv_h[s_ * T:(s_ + 1) * T, h * hd:(h + 1) * hd])
+        k = np.ascontiguousarray(qkv_h[s_ * T:(s_ + 1) * T, d + h * hd:d + (h + 1) * hd])
+        p_ref = oracle.softmax(oracle.gemm(q, k, transB=True, epi=2, scale=scale), causal=causal)
+        r0 = (s_ * H + h) * T
+        assert_bits(Ph[r0:r0 + T], p_ref, f"P oracle s{s_} h{h}")
+
+
+def test_attention_probs_rejects():
+    qkv = torch.zeros(64, 3 * 64, device="cuda")
+    P = torch.zeros(64, 64, device="cuda")
+    assert not R.repops_attention_probs_supported(64, 128)
+    assert not R.repops_attention_probs_supported(100, 64)
+    assert not R.repops_attention_probs_supported(4096, 64)
+    with pytest.raises(R.RepopsError):
+        R.repops_attention_probs(qkv, 64, 128, 3 * 64, (0, 0), 0, 64, (1, 1), P, (0, 0))
+    with pytest.raises(ValueError):
+        R.repops_attention_probs(qkv, 128, 64, 3 * 64, (0, 0), 0, 64, (1, 1), P, (0, 0))  # P too small
