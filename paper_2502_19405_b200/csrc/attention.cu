@@ -23,7 +23,7 @@
 #include "common.cuh"
 
 #ifndef RO_ATTN_VARIANT_DEFAULT
-#define RO_ATTN_VARIANT_DEFAULT 1
+#define RO_ATTN_VARIANT_DEFAULT 3
 #endif
 
 namespace {

@@ -28,6 +28,7 @@ Python here only sequences C-ABI calls and owns buffers (torch memory).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import struct
 from dataclasses import dataclass, field
 
@@ -168,7 +169,7 @@ class GPT2Step:
         # never leave shared memory, P is written for the PV R-GEMM and the backward), then the
         # PV R-GEMM; same bits as the three launches.  Needs the scores to be operator scratch
         # (R29); fault-injection runs keep the per-op launches
-        self.attn_probs = True
+        self.attn_probs = os.environ.get("REPOPS_ATTN_PROBS", "1") == "1"   # (A/B switch for tools)
         # GELU / GELU-backward fused into the FC / FC2-dgrad GEMM epilogues (repops_gemm_post):
         # same bits, but measured slower in the step (80.05 -> 80.43 ms; the tanh chain in the
         # epilogue of a 2-3 CTA/SM GEMM hides latency worse than the standalone HBM-bound

@@ -33,8 +33,9 @@ def short(k):
         t = lambda x: 'T' if x in ('true', '1') else 'N'  # noqa: E731
         return 'gemm_kernel %sx%s %s%s%s' % (m.group(1), m.group(2), t(m.group(3)), t(m.group(4)),
                                             ' XP' if t(m.group(6)) == 'T' and t(m.group(3)) == 'N' else '')
-    if 'gemm_tn_kernel' in k:
-        return 'gemm_tn_kernel 128x128 TN (gemm_tn.cu)'
+    m = re.search(r'gemm_tn_kernel<(\d+), (\d+)', k)
+    if m:
+        return 'gemm_tn_kernel %sx%s TN (gemm_tn.cu)' % (m.group(1), m.group(2))
     return re.sub(r'\(.*', '', k).replace('void ', '')
 
 

@@ -21,6 +21,12 @@ for k in 0 1 2; do
   python tools/ncu_summary.py gpurun_out/prof_tmp/attn$k.csv > gpurun_out/ncu_gemm_attn$k.txt
 done
 mkdir -p gpurun_out/prof_tmp
+timeout 300 ncu --set full --import-source on --clock-control none -k regex:attn_probs -s 2 -c 1 \
+    -o gpurun_out/prof_tmp/probs -f python tools/attn_probs_one.py > /dev/null 2>&1
+ncu -i gpurun_out/prof_tmp/probs.ncu-rep --page raw --csv > gpurun_out/prof_tmp/probs.csv 2>/dev/null
+python tools/ncu_summary.py gpurun_out/prof_tmp/probs.csv > gpurun_out/ncu_attn_probs.txt
+ncu -i gpurun_out/prof_tmp/probs.ncu-rep --page source --csv --print-source sass > gpurun_out/prof_tmp/probs_src.csv 2>/dev/null
+python tools/sass_stalls.py gpurun_out/prof_tmp/probs_src.csv >> gpurun_out/ncu_attn_probs.txt
 timeout 300 ncu --set full --import-source on --clock-control none -k regex:leaf_kernel -s 1 -c 1 \
     -o gpurun_out/prof_tmp/leaf -f python tools/commit_one.py > /dev/null 2>&1
 ncu -i gpurun_out/prof_tmp/leaf.ncu-rep --page raw --csv > gpurun_out/prof_tmp/leaf.csv 2>/dev/null
