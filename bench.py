@@ -689,7 +689,7 @@ def main():
         # the config-3 step (checkpoint commits every CKPT_EVERY steps) is timed over a whole
         # checkpoint interval so the amortised state commitment is inside the region
         steps = args.steps if head_wl else (GPT2Train.CKPT_EVERY if wname == "gpt2_ckpt" else max(2, min(args.steps, 3)))
-        for _ in range(args.warmup if head_wl else 1):
+        for _ in range(args.warmup):   # W >= 3 for every workload of the line, not only the headline
             wl.step()
         torch.cuda.synchronize()
         ms, tot, launches, clk = timed(wl, steps, world, local)
