@@ -28,6 +28,7 @@ committed Q/K/V, Verde Case 3).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import struct
 from dataclasses import dataclass, field
 
@@ -432,6 +433,7 @@ class LlamaPrefill:
         self.root_plan = RootPlan(self.node_blob, self.node_offs, self.node_slots, self.node_soffs, self.digests)
         self.root_host = torch.zeros(32, dtype=torch.uint8).pin_memory()
         self.side = torch.cuda.Stream(device=self.dev)
+        self.commit_mode = os.environ.get("REPOPS_LLAMA_COMMIT", "side")
         self.commit_bytes = sum(p.nbytes for p in self.plans if p is not None)
 
     def set_tokens(self, host_tokens=None):
@@ -440,8 +442,11 @@ class LlamaPrefill:
             host_tokens = synth.llama_tokens(c.vocab, c.seq, c.seed)
         self.tok.copy_(torch.as_tensor(np.ascontiguousarray(host_tokens, dtype=np.int32)))
 
-    def run(self, commit=True):
-        """One prefill pass; commits of each phase run on a side stream (overlap)."""
+    def run(self, commit=True, commit_mode=None):
+        """One prefill pass.  commit_mode "side": each phase's commit plan runs on a side
+        stream beside the next phases; "inline": on the pass stream right after its phase;
+        "end": every plan after the last phase (same digests in every mode)."""
+        commit_mode = commit_mode or self.commit_mode
         main = torch.cuda.current_stream()
         side = self.side   # parameter digests were written into the table at load time
         side.wait_stream(main)
@@ -449,8 +454,15 @@ class LlamaPrefill:
             for fn in fns:
                 fn()
             if commit and plan is not None:
-                side.wait_stream(main)
-                plan.run(stream=side)
+                if commit_mode == "side":
+                    side.wait_stream(main)
+                    plan.run(stream=side)
+                elif commit_mode == "inline":
+                    plan.run(stream=main)
+        if commit and commit_mode == "end":
+            for plan in self.plans:
+                if plan is not None:
+                    plan.run(stream=main)
         main.wait_stream(side)
 
     def device_root(self):
