@@ -236,6 +236,19 @@ int repops_attention_probs(int64_t T, int64_t hd, const float *Q, const float *K
                            int64_t s1, float scale, int causal, float *P, int64_t sp0, int64_t sp1,
                            int64_t batch0, int64_t batch1, void *stream);
 
+/* The backward twin (f4; R7's backward, R29): per (b0, b1), dP = R-GEMM(dO, V^T) (no
+ * epilogue) over every key, kept in shared memory, then the softmax backward of each row:
+ * c = CDOT(P row, dP row), dS = canon(fmul(fmul(P, fsub(dP, c)), scale)).  Bit-identical to
+ * repops_gemm_strided_batched(dO, V^T) -> repops_softmax_backward(P, dP, scale).  dO rows:
+ * stride ldo at dO + b0 so0 + b1 so1; V rows: stride ldv at V + b0 sv0 + b1 sv1 (head dim
+ * hd); P, dS: [T][T] blocks (row stride T) at P + b0 sp0 + b1 sp1, dS + b0 sd0 + b1 sd1;
+ * device, caller-owned, 16-byte aligned rows.  Same support as repops_attention_probs
+ * (REPOPS_ESHAPE otherwise); REPOPS_EINVAL: null, misaligned, ldo / ldv < hd. */
+int repops_attention_dscores(int64_t T, int64_t hd, const float *dO, int64_t ldo, int64_t so0, int64_t so1,
+                             const float *V, int64_t ldv, int64_t sv0, int64_t sv1, const float *P, int64_t sp0,
+                             int64_t sp1, float scale, float *dS, int64_t sd0, int64_t sd1, int64_t batch0,
+                             int64_t batch1, void *stream);
+
 /* ------------------------------------------------------------------ elementwise
  * Software math (R5/R6): fixed IEEE-RN op chains. */
 int repops_exp(const float *x, int64_t n, float *y, void *stream);

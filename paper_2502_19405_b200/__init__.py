@@ -24,7 +24,7 @@ __all__ = [
     "repops_layernorm_backward_params", "repops_cross_entropy", "repops_exp", "repops_log", "repops_tanh",
     "repops_rsqrt", "repops_gelu", "repops_gelu_backward", "repops_relu", "repops_relu_backward", "repops_sin", "repops_cos", "repops_erf", "repops_gelu_erf", "repops_convert", "repops_gemm_ex",
     "repops_attention_fwd", "repops_attention_fwd_supported", "repops_attention_probs",
-    "repops_attention_probs_supported", "repops_rand_uniform",
+    "repops_attention_probs_supported", "repops_attention_dscores", "repops_rand_uniform",
     "repops_dropout", "repops_dropout_backward",
     "repops_gelu_erf_backward", "repops_rope_tables", "repops_ipc_alloc", "repops_ipc_open", "repops_ipc_close",
     "repops_ipc_free", "repops_p2p_tree_combine", "repops_p2p_signal", "repops_p2p_wait", "repops_add", "repops_embedding",
@@ -241,6 +241,38 @@ def repops_attention_probs(qkv, T, hd, ld, s, q_off, k_off, batch, P, sp, scale=
     if t0 is not None:
         _TIMER.end("gemm", t0, 2 * T * T * hd * nb, stream)
     return P
+
+
+def _fits(t, off, strides, batch, rows, cols, ld):
+    """the last (b0, b1) block of a strided batch lies inside t's storage"""
+    last = off + (int(batch[0]) - 1) * int(strides[0]) + (int(batch[1]) - 1) * int(strides[1]) + \
+        (rows - 1) * ld + cols
+    return t.storage_offset() + last <= t.untyped_storage().nbytes() // 4
+
+
+def repops_attention_dscores(dO, V, T, hd, ldo, so, o_off, ldv, sv, v_off, P, sp, dS, sd, batch, scale=1.0,
+                             stream=None):
+    """Attention backward, scores part, fused: dS = R-SOFTMAX-BWD(P, R-GEMM(dO, V^T)) * scale
+    over a strided batch (element offsets / strides into the storage of dO, V, P, dS), the
+    dP matrix never leaving shared memory -- bit-identical to repops_gemm_strided_batched ->
+    repops_softmax_backward."""
+    for t, n in ((dO, "dO"), (V, "V"), (P, "P"), (dS, "dS")):
+        _f32(t, n)
+        if t.device != dO.device:
+            raise ValueError(f"{n} must be on the device of dO")
+    nb = int(batch[0]) * int(batch[1])
+    if nb and not (_fits(dO, o_off, so, batch, T, hd, ldo) and _fits(V, v_off, sv, batch, T, hd, ldv)
+                   and _fits(P, 0, sp, batch, T, T, T) and _fits(dS, 0, sd, batch, T, T, T)):
+        raise ValueError("attention_dscores: an operand is too small for the batch")
+    t0 = _TIMER.begin(stream) if _TIMER else None
+    check(lib().repops_attention_dscores(int(T), int(hd), dO.data_ptr() + 4 * o_off, int(ldo), int(so[0]),
+                                         int(so[1]), V.data_ptr() + 4 * v_off, int(ldv), int(sv[0]), int(sv[1]),
+                                         P.data_ptr(), int(sp[0]), int(sp[1]), float(scale), dS.data_ptr(),
+                                         int(sd[0]), int(sd[1]), int(batch[0]), int(batch[1]), _stream(stream)),
+          "repops_attention_dscores")
+    if t0 is not None:
+        _TIMER.end("gemm", t0, 2 * T * T * hd * nb, stream)
+    return dS
 
 
 def repops_attention_fwd_supported(T, hd):

@@ -349,6 +349,26 @@ int repops_attention_probs(int64_t T, int64_t hd, const float *Q, const float *K
                        "attention_probs");
 }
 
+int repops_attention_dscores(int64_t T, int64_t hd, const float *dO, int64_t ldo, int64_t so0, int64_t so1,
+                             const float *V, int64_t ldv, int64_t sv0, int64_t sv1, const float *P, int64_t sp0,
+                             int64_t sp1, float scale, float *dS, int64_t sd0, int64_t sd1, int64_t batch0,
+                             int64_t batch1, void *stream) {
+    REQ(T >= 0 && hd >= 0 && batch0 >= 0 && batch1 >= 0, "attention_dscores: negative extent");
+    if (T == 0 || batch0 * batch1 == 0) return REPOPS_OK;
+    if (!attention_probs_supported(T, hd))
+        return fail(REPOPS_ESHAPE, "attention_dscores: T = %lld, hd = %lld unsupported (hd 64, T %% 32 == 0, T <= 1024)",
+                    (long long)T, (long long)hd);
+    REQ(dO && V && P && dS, "attention_dscores: null pointer");
+    REQ(ldo >= hd && ldv >= hd, "attention_dscores: leading dimension < hd");
+    const bool al = a16(dO) && a16(V) && a16(P) && a16(dS) && ldo % 4 == 0 && ldv % 4 == 0 && so0 % 4 == 0 &&
+                    so1 % 4 == 0 && sv0 % 4 == 0 && sv1 % 4 == 0 && sp0 % 4 == 0 && sp1 % 4 == 0 && sd0 % 4 == 0 &&
+                    sd1 % 4 == 0;
+    REQ(al, "attention_dscores: rows must be 16-byte aligned");
+    return cuda_status(launch_attention_dscores(T, dO, ldo, so0, so1, V, ldv, sv0, sv1, P, sp0, sp1, scale, dS, sd0,
+                                                sd1, batch0, batch1, S(stream)),
+                       "attention_dscores");
+}
+
 int repops_attention_fwd(int64_t T, int64_t hd, const float *Q, const float *K, const float *V, int64_t ld,
                          int64_t s0, int64_t s1, float scale, int causal, float *Sout, float *Pout, int64_t sp0,
                          int64_t sp1, float *O, int64_t ldo, int64_t so0, int64_t so1, int64_t batch0,

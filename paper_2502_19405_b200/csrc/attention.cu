@@ -315,18 +315,27 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(AttnArgs a) {
 // GEMM-sized register tile (4 queries x 8 keys per thread, d ascending from +0, then
 // canon(fmul(acc, scale))), then each warp runs softmax_warp's sequence on its rows and
 // writes P.  S never reaches HBM; bits equal repops_gemm(SCALE) -> repops_softmax.
+//
+// MODE 1 (the backward twin, repops_attention_dscores): the same phase 1 computes
+// dP = canon(fold_d fma(dO[i,d], V[j,d], +0)) for every key j (no epilogue; the softmax
+// backward's row fold reads every column), and phase 2 is softmax_bwd_warp's sequence:
+// c = CDOT(P row, dP row) (128 slots of fma from +0, then TREE128), dS = canon(fmul(fmul(P,
+// fsub(dP, c)), scale)).  dP never reaches HBM; bits equal repops_gemm -> repops_softmax_backward.
 constexpr int PS_BM = 32, PS_THREADS = 256, PS_KB = 256, PS_DS = 8, PS_KLD = PS_DS + 4, PS_NST = 3;
 
 struct ProbArgs {
-    const float *Q, *K;
-    int64_t ld, s0, s1;
-    float *P;
-    int64_t sp0, sp1;
+    const float *A, *B;          // rows of A (Q or dO) and B (K or V), head dim HD
+    int64_t lda, sa0, sa1, ldb, sb0, sb1;
+    const float *Pin;            // MODE 1: P blocks (row stride T)
+    int64_t spi0, spi1;
+    float *out;                  // MODE 0: P, MODE 1: dS (row stride T)
+    int64_t so0, so1;
     int64_t batch1, nbatch;
     int T, causal;
     float scale;
 };
 
+template <int MODE>
 __global__ void __launch_bounds__(PS_THREADS, 2) attn_probs_kernel(ProbArgs a) {
     extern __shared__ __align__(16) float sm[];
     const int T = a.T, SLD = T + 4;
@@ -337,16 +346,16 @@ __global__ void __launch_bounds__(PS_THREADS, 2) attn_probs_kernel(ProbArgs a) {
     const int nqb = T / PS_BM;
     const int64_t bh = blockIdx.x % a.nbatch, b0 = bh / a.batch1, b1 = bh % a.batch1;
     const int q0 = (nqb - 1 - (int)(blockIdx.x / a.nbatch)) * PS_BM;
-    const float *Q = a.Q + b0 * a.s0 + b1 * a.s1;
-    const float *K = a.K + b0 * a.s0 + b1 * a.s1;
+    const float *Q = a.A + b0 * a.sa0 + b1 * a.sa1;
+    const float *K = a.B + b0 * a.sb0 + b1 * a.sb1;
     // causal: the rows read keys < q0 + PS_BM only (R31: the other scores are never read)
-    const int kneed = a.causal ? min(T, q0 + PS_BM) : T;
+    const int kneed = (MODE == 0 && a.causal) ? min(T, q0 + PS_BM) : T;
 
 #pragma unroll
     for (int q = 0; q < PS_BM * HD / 4 / PS_THREADS; ++q) {
         const int c = tid + q * PS_THREADS;
         const int r = c % PS_BM, kq = (c / PS_BM) * 4;
-        const float4 v = __ldg(reinterpret_cast<const float4 *>(Q + (int64_t)(q0 + r) * a.ld + kq));
+        const float4 v = __ldg(reinterpret_cast<const float4 *>(Q + (int64_t)(q0 + r) * a.lda + kq));
         Qt[(kq + 0) * PS_BM + r] = v.x;
         Qt[(kq + 1) * PS_BM + r] = v.y;
         Qt[(kq + 2) * PS_BM + r] = v.z;
@@ -363,7 +372,7 @@ __global__ void __launch_bounds__(PS_THREADS, 2) attn_probs_kernel(ProbArgs a) {
             float *dst = Ks + buf * PS_KB * PS_KLD;
             for (int c = tid; c < nrows * (PS_DS / 4); c += PS_THREADS) {
                 const int r = c / (PS_DS / 4), k4 = (c % (PS_DS / 4)) * 4;
-                cp16(dst + r * PS_KLD + k4, K + (int64_t)(kb + r) * a.ld + ds + k4);
+                cp16(dst + r * PS_KLD + k4, K + (int64_t)(kb + r) * a.ldb + ds + k4);
             }
         };
         float2 acc[8][2];
@@ -404,19 +413,55 @@ __global__ void __launch_bounds__(PS_THREADS, 2) attn_probs_kernel(ProbArgs a) {
             }
             __syncthreads();  // slice buffer free for the stage PS_NST slices on
         }
-        if (active) {  // epilogue (R3, R10): S = canon(fmul(acc, scale))
+        if (active) {  // epilogue (R3, R10): MODE 0 S = canon(fmul(acc, scale)), MODE 1 dP = canon(acc)
+            auto epi = [&](float x) { return MODE == 0 ? canon(__fmul_rn(x, a.scale)) : canon(x); };
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 const int key = kb + 32 * warp + kg + 4 * j;
                 float *srow = Ss + 4 * qg * SLD + key;
-                srow[0] = canon(__fmul_rn(acc[j][0].x, a.scale));
-                srow[SLD] = canon(__fmul_rn(acc[j][0].y, a.scale));
-                srow[2 * SLD] = canon(__fmul_rn(acc[j][1].x, a.scale));
-                srow[3 * SLD] = canon(__fmul_rn(acc[j][1].y, a.scale));
+                srow[0] = epi(acc[j][0].x);
+                srow[SLD] = epi(acc[j][0].y);
+                srow[2 * SLD] = epi(acc[j][1].x);
+                srow[3 * SLD] = epi(acc[j][1].y);
             }
         }
     }
     __syncthreads();
+
+    if constexpr (MODE == 1) {
+        // softmax backward, warp per row (softmax_bwd_warp's order): c = CDOT(P, dP) over all T
+        // columns, dS = canon(fmul(fmul(P, fsub(dP, c)), scale)); T <= 1024 is one CSUM tile
+        for (int r = warp; r < PS_BM; r += PS_THREADS / 32) {
+            const float *dp = Ss + r * SLD;
+            const float *pr = a.Pin + b0 * a.spi0 + b1 * a.spi1 + (int64_t)(q0 + r) * T;
+            float *dr = a.out + b0 * a.so0 + b1 * a.so1 + (int64_t)(q0 + r) * T;
+            float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;
+            for (int b = 0; b < T; b += 128) {
+                const int i = b + 4 * lane;
+                if (i >= T) break;  // T % 4 == 0
+                const float4 y = __ldg(reinterpret_cast<const float4 *>(pr + i));
+                const float4 g = *reinterpret_cast<const float4 *>(dp + i);
+                p0 = __fmaf_rn(y.x, g.x, p0);
+                p1 = __fmaf_rn(y.y, g.y, p1);
+                p2 = __fmaf_rn(y.z, g.z, p2);
+                p3 = __fmaf_rn(y.w, g.w, p3);
+            }
+            const float c = tree128(p0, p1, p2, p3);
+            for (int b = 0; b < T; b += 128) {
+                const int i = b + 4 * lane;
+                if (i >= T) break;
+                const float4 y = __ldg(reinterpret_cast<const float4 *>(pr + i));
+                const float4 g = *reinterpret_cast<const float4 *>(dp + i);
+                float4 o;
+                o.x = canon(__fmul_rn(__fmul_rn(y.x, __fsub_rn(g.x, c)), a.scale));
+                o.y = canon(__fmul_rn(__fmul_rn(y.y, __fsub_rn(g.y, c)), a.scale));
+                o.z = canon(__fmul_rn(__fmul_rn(y.z, __fsub_rn(g.z, c)), a.scale));
+                o.w = canon(__fmul_rn(__fmul_rn(y.w, __fsub_rn(g.w, c)), a.scale));
+                *reinterpret_cast<float4 *>(dr + i) = o;
+            }
+        }
+        return;
+    }
 
     // softmax, warp per row (softmax_warp's order: R7), P rows written in full (+0 masked)
     for (int r = warp; r < PS_BM; r += PS_THREADS / 32) {
@@ -445,7 +490,7 @@ __global__ void __launch_bounds__(PS_THREADS, 2) attn_probs_kernel(ProbArgs a) {
             if (i < L) *reinterpret_cast<float4 *>(row + i) = v;
         }
         const float rinv = __fdiv_rn(1.0f, tree128(p0, p1, p2, p3));
-        float *Pg = a.P + b0 * a.sp0 + b1 * a.sp1 + (int64_t)(q0 + r) * T;
+        float *Pg = a.out + b0 * a.so0 + b1 * a.so1 + (int64_t)(q0 + r) * T;
         for (int b = 0; b < T; b += 128) {
             const int i = b + 4 * lane;
             if (i >= T) break;  // T % 4 == 0: i < T covers the whole float4
@@ -529,18 +574,34 @@ bool attention_probs_supported(int64_t T, int64_t hd) {
     return hd == HD && T > 0 && T % PS_BM == 0 && T % 4 == 0 && probs_smem_bytes(T) <= 227 * 1024;
 }
 
+template <int MODE>
+static cudaError_t launch_probs_mode(const ProbArgs &a, int64_t nb, cudaStream_t s) {
+    const size_t smem = probs_smem_bytes(a.T);
+    static size_t attr = 0;
+    if (smem > attr) {
+        cudaError_t e = cudaFuncSetAttribute(attn_probs_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = smem;
+    }
+    attn_probs_kernel<MODE><<<(unsigned)(a.T / PS_BM * nb), PS_THREADS, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_attention_probs(int64_t T, const float *Q, const float *K, int64_t ld, int64_t s0, int64_t s1,
                                    float scale, int causal, float *P, int64_t sp0, int64_t sp1, int64_t batch0,
                                    int64_t batch1, cudaStream_t s) {
     if (batch0 * batch1 == 0 || T == 0) return cudaSuccess;
-    const size_t smem = probs_smem_bytes(T);
-    static size_t attr = 0;
-    if (smem > attr) {
-        cudaError_t e = cudaFuncSetAttribute(attn_probs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        attr = smem;
-    }
-    ProbArgs a{Q, K, ld, s0, s1, P, sp0, sp1, batch1, batch0 * batch1, (int)T, causal, scale};
-    attn_probs_kernel<<<(unsigned)(T / PS_BM * batch0 * batch1), PS_THREADS, smem, s>>>(a);
-    return cudaGetLastError();
+    ProbArgs a{Q, K, ld, s0, s1, ld, s0, s1, nullptr, 0, 0, P, sp0, sp1, batch1, batch0 * batch1, (int)T, causal, scale};
+    return launch_probs_mode<0>(a, batch0 * batch1, s);
+}
+
+cudaError_t launch_attention_dscores(int64_t T, const float *dO, int64_t ldo, int64_t so0, int64_t so1,
+                                     const float *V, int64_t ldv, int64_t sv0, int64_t sv1, const float *P,
+                                     int64_t sp0, int64_t sp1, float scale, float *dS, int64_t sd0, int64_t sd1,
+                                     int64_t batch0, int64_t batch1, cudaStream_t s) {
+    if (batch0 * batch1 == 0 || T == 0) return cudaSuccess;
+    ProbArgs a{dO, V, ldo, so0, so1, ldv, sv0, sv1, P, sp0, sp1, dS, sd0, sd1, batch1, batch0 * batch1, (int)T, 0,
+               scale};
+    return launch_probs_mode<1>(a, batch0 * batch1, s);
 }

@@ -38,7 +38,8 @@ import torch
 import synth
 
 from . import (EPI_BIAS, EPI_SCALE, POST_GELU, POST_GELU_BACKWARD, CommitPlan, repops_add, repops_attention_fwd,
-               repops_attention_fwd_supported, repops_attention_probs, repops_attention_probs_supported,
+               repops_attention_fwd_supported, repops_attention_dscores, repops_attention_probs,
+               repops_attention_probs_supported,
                repops_cross_entropy, repops_embedding,
                repops_embedding_backward, repops_gelu, repops_gelu_backward, repops_gemm,
                repops_gemm_strided_batched, repops_layernorm, repops_layernorm_backward,
@@ -170,6 +171,10 @@ class GPT2Step:
         # PV R-GEMM; same bits as the three launches.  Needs the scores to be operator scratch
         # (R29); fault-injection runs keep the per-op launches
         self.attn_probs = os.environ.get("REPOPS_ATTN_PROBS", "1") == "1"   # (A/B switch for tools)
+        # its backward twin (repops_attention_dscores: dP in shared memory + softmax backward,
+        # same dS bits) measured slower than the dP R-GEMM + softmax_bwd launches (181 vs
+        # 161 us per layer, tools/attn_fused_bench.py): off by default
+        self.attn_dscores = os.environ.get("REPOPS_ATTN_DSCORES", "0") == "1"
         # GELU / GELU-backward fused into the FC / FC2-dgrad GEMM epilogues (repops_gemm_post):
         # same bits, but measured slower in the step (80.05 -> 80.43 ms; the tanh chain in the
         # epilogue of a 2-3 CTA/SM GEMM hides latency worse than the standalone HBM-bound
@@ -719,12 +724,19 @@ class GPT2Step:
                     self._gemm_tn(g["dxmid"], self.wT[p + "proj.w"], out=g["datt"])
                     self._hook(f"h{l}/proj_dgrad")
                     # attention
-                    repops_gemm_strided_batched(g["datt"], a["qkv"], g["dP"], M=T, N=T, K=hd, lda=d, ldb=3 * d,
-                                                ldc=T, sA=(T * d, hd), sB=(T * 3 * d, hd), sC=(H * T * T, T * T),
-                                                batch=(S_loc, H), transB=True, offB=2 * d)
-                    self._hook(f"h{l}/attn_dp")
-                    repops_softmax_backward(a["P"], g["dP"], scale=1.0 / np.sqrt(hd), out=g["dS"])
-                    self._hook(f"h{l}/softmax_bwd")
+                    if self.attn_op and self.attn_dscores and self.attn_probs_ok and self._fault is None:
+                        # f4: dP = dO V^T kept in shared memory, softmax backward in the same kernel
+                        # (dP is operator-internal under R29); same dS bits as the two launches
+                        repops_attention_dscores(g["datt"], a["qkv"], T, hd, d, (T * d, hd), 0, 3 * d,
+                                                 (T * 3 * d, hd), 2 * d, a["P"], (H * T * T, T * T), g["dS"],
+                                                 (H * T * T, T * T), (S_loc, H), scale=1.0 / np.sqrt(hd))
+                    else:
+                        repops_gemm_strided_batched(g["datt"], a["qkv"], g["dP"], M=T, N=T, K=hd, lda=d,
+                                                    ldb=3 * d, ldc=T, sA=(T * d, hd), sB=(T * 3 * d, hd),
+                                                    sC=(H * T * T, T * T), batch=(S_loc, H), transB=True, offB=2 * d)
+                        self._hook(f"h{l}/attn_dp")
+                        repops_softmax_backward(a["P"], g["dP"], scale=1.0 / np.sqrt(hd), out=g["dS"])
+                        self._hook(f"h{l}/softmax_bwd")
                     # dV = P^T dO ; dQ = dS K ; dK = dS^T Q   (into the packed dqkv)
                     repops_gemm_strided_batched(a["P"], g["datt"], g["dqkv"], M=T, N=hd, K=T, lda=T, ldb=d,
                                                 ldc=3 * d, sA=(H * T * T, T * T), sB=(T * d, hd),

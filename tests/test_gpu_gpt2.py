@@ -152,11 +152,12 @@ def test_fused_attention_step_root_equals_unfused():
     from paper_2502_19405_b200.gpt2 import GPT2Config, GPT2Step
     cfg = GPT2Config(n_layer=2, d=128, n_head=2, ffn=512, vocab=1000, n_pos=512, seq=512, shards=8)
     roots = []
-    # (all-in-one fused kernel, scores+softmax kernel + PV R-GEMM, three per-op launches)
+    # (all-in-one fused kernel, scores+softmax kernel + PV R-GEMM with the fused backward
+    # dscores kernel, three per-op launches forward and backward)
     for fused, probs in ((True, False), (False, True), (False, False)):
         st = GPT2Step(cfg)
         assert st.fused_attention_ok and st.attn_probs_ok  # the shape is supported
-        st.fused_attention, st.attn_probs = fused, probs
+        st.fused_attention, st.attn_probs, st.attn_dscores = fused, probs, probs
         r = []
         for k in range(2):
             st.set_tokens(k)

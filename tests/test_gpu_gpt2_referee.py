@@ -133,6 +133,8 @@ def test_block_backward_every_node(full):
         name = f"s{s}/dx{l}" if k == "dx" else pre + k
         if name not in get.names:  # dP / dS: internal to the ATTENTION_BWD operator (R29)
             assert k in ("dP", "dS") and st.attn_op, name
+            if k == "dP" and st.attn_dscores and st.attn_probs_ok:
+                continue   # the fused backward kernel keeps dP in shared memory; dS checks it
             H, T = cfg.n_head, cfg.seq
             buf = st.grad_act[l][k][s * H * T:(s + 1) * H * T].cpu().numpy()
             same_bits(buf, v, f"internal {k}")

@@ -978,3 +978,51 @@ def test_attention_probs_rejects():
         R.repops_attention_probs(qkv, 64, 128, 3 * 64, (0, 0), 0, 64, (1, 1), P, (0, 0))
     with pytest.raises(ValueError):
         R.repops_attention_probs(qkv, 128, 64, 3 * 64, (0, 0), 0, 64, (1, 1), P, (0, 0))  # P too small
+
+
+@pytest.mark.parametrize("T", [512, 1024, 256, 96, 32])
+def test_attention_dscores_equals_unfused_and_oracle(T):
+    """backward scores part fused (dP kept in shared memory): dS bit-identical to
+    R-GEMM(dO, V^T) -> R-SOFTMAX-BWD(P, dP, scale) for every (shard, head), with the causal
+    P of the forward (+0 above the diagonal), non-finite dO / V entries (their dP columns /
+    rows are inf / NaN, and the masked +0 * inf terms of the row fold give NaN), and the
+    oracle on sampled heads"""
+    S_, H, hd = 2, 12 if T <= 512 else 3, 64
+    d = H * hd
+    scale = 1.0 / np.sqrt(hd)
+    qkv_h = _attn_inputs(S_, H, T, hd, 60 + T)
+    h2, h4, h5 = 2 % H, 4 % H, 5 % H
+    qkv_h[T - 3, 2 * d + h2 * hd + 7] = np.inf          # V of (0, h2): key T-3 -> dP column T-3 inf
+    qkv_h[T + 1, 2 * d + h4 * hd + 11] = np.nan         # V of (1, h4): key 1 -> dP column 1 NaN
+    dO_h = synth.uniform(61 + T, (S_ * T, d), 1.0)
+    dO_h[7, h5 * hd + 3] = -np.inf                       # dO of (0, h5): row 7 -> dP row 7 inf / NaN
+    qkv, dO = dev(qkv_h), dev(dO_h)
+    Pu, _ = _unfused_attention(qkv, S_, H, T, hd, scale, causal=True)
+    sp = (H * T * T, T * T)
+    dSf = torch.full_like(Pu, 7.0)
+    R.repops_attention_dscores(dO, qkv, T, hd, d, (T * d, hd), 0, 3 * d, (T * 3 * d, hd), 2 * d, Pu, sp, dSf, sp,
+                               (S_, H), scale=scale)
+    dPu = torch.empty_like(Pu)
+    R.repops_gemm_strided_batched(dO, qkv, dPu, M=T, N=T, K=hd, lda=d, ldb=3 * d, ldc=T, sA=(T * d, hd),
+                                  sB=(T * 3 * d, hd), sC=sp, batch=(S_, H), transB=True, offB=2 * d)
+    dSu = torch.empty_like(Pu)
+    R.repops_softmax_backward(Pu, dPu, scale=scale, out=dSu)
+    dSh = host(dSf)
+    assert_bits(dSh, host(dSu), "dS fused vs unfused")
+    assert np.isnan(dSh[(0 * H + h5) * T + 7]).all()     # the row with -inf in dO
+    Ph = host(Pu)
+    for s_, h in ((0, h2), (1, h4), (1, H - 1)):
+        v = np.ascontiguousarray(qkv_h[s_ * T:(s_ + 1) * T, 2 * d + h * hd:2 * d + (h + 1) * hd])
+        g = np.ascontiguousarray(dO_h[s_ * T:(s_ + 1) * T, h * hd:(h + 1) * hd])
+        r0 = (s_ * H + h) * T
+        ref = oracle.softmax_backward(Ph[r0:r0 + T], oracle.gemm(g, v, transB=True), scale=scale)
+        assert_bits(dSh[r0:r0 + T], ref, f"dS oracle s{s_} h{h}")
+
+
+def test_attention_dscores_rejects():
+    x = torch.zeros(64, 3 * 64, device="cuda")
+    P = torch.zeros(64, 64, device="cuda")
+    with pytest.raises(R.RepopsError):
+        R.repops_attention_dscores(x, x, 64, 128, 3 * 64, (0, 0), 0, 3 * 64, (0, 0), 0, P, (0, 0), P, (0, 0), (1, 1))
+    with pytest.raises(ValueError):   # dS too small for T = 128
+        R.repops_attention_dscores(x, x, 128, 64, 3 * 64, (0, 0), 0, 3 * 64, (0, 0), 0, P, (0, 0), P, (0, 0), (1, 1))

@@ -44,6 +44,23 @@ def probs_only():
     R.repops_attention_probs(qkv, T, hd, 3 * d, (T * 3 * d, hd), 0, d, (S_, H), Pf, (H * T * T, T * T), scale=0.125)
 
 
+dO = torch.rand(S_ * T, d, device="cuda") - 0.5
+dPb = torch.empty_like(Sb)
+dSb = torch.empty_like(Sb)
+dSf = torch.empty_like(Sb)
+
+
+def bwd_unfused():
+    R.repops_gemm_strided_batched(dO, qkv, dPb, M=T, N=T, K=hd, lda=d, ldb=3 * d, ldc=T, sA=(T * d, hd),
+                                  sB=(T * 3 * d, hd), sC=(H * T * T, T * T), batch=(S_, H), transB=True, offB=2 * d)
+    R.repops_softmax_backward(Pb, dPb, scale=0.125, out=dSb)
+
+
+def bwd_fused():
+    R.repops_attention_dscores(dO, qkv, T, hd, d, (T * d, hd), 0, 3 * d, (T * 3 * d, hd), 2 * d, Pb,
+                               (H * T * T, T * T), dSf, (H * T * T, T * T), (S_, H), scale=0.125)
+
+
 def t(fn, n=50):
     for _ in range(5):
         fn()
@@ -71,3 +88,8 @@ for v in (sys.argv[1:] or ["0", "1", "2", "3"]):
     same = torch.equal(O.view(torch.int32), Ou.view(torch.int32)) and torch.equal(Pf.view(torch.int32),
                                                                                   Pb.view(torch.int32))
     print(f"fused v{v}     {ms * 1e3:8.1f} us  {fl / ms / 1e9:6.1f} TFLOP/s  bits {'same' if same else 'DIFFER'}")
+ms = t(bwd_unfused)
+print(f"bwd dP GEMM + softmax_bwd  {ms * 1e3:8.1f} us")
+ms = t(bwd_fused)
+same = torch.equal(dSf.view(torch.int32), dSb.view(torch.int32))
+print(f"bwd dscores fused          {ms * 1e3:8.1f} us  bits {'same' if same else 'DIFFER'}")
