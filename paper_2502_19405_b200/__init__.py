@@ -216,6 +216,13 @@ def repops_causal_suffix_flags(B, K, N, ldb, sB, batch, out=None, ldf=None, sF=N
 
 
 # ------------------------------------------------------------------ fused attention (f4)
+def _fits(t, off, strides, batch, rows, cols, ld):
+    """the last (b0, b1) block of a strided batch lies inside t's storage"""
+    last = off + (int(batch[0]) - 1) * int(strides[0]) + (int(batch[1]) - 1) * int(strides[1]) + \
+        (rows - 1) * ld + cols
+    return t.storage_offset() + last <= t.untyped_storage().nbytes() // 4
+
+
 def repops_attention_probs_supported(T, hd):
     return bool(lib().repops_attention_probs_supported(int(T), int(hd)))
 
@@ -229,9 +236,9 @@ def repops_attention_probs(qkv, T, hd, ld, s, q_off, k_off, batch, P, sp, scale=
     if P.device != qkv.device:
         raise ValueError("P must be on the device of qkv")
     nb = int(batch[0]) * int(batch[1])
-    if nb and P.storage_offset() + (int(batch[0]) - 1) * int(sp[0]) + (int(batch[1]) - 1) * int(sp[1]) + T * T > \
-            P.untyped_storage().nbytes() // 4:
-        raise ValueError("P too small for the batch")
+    if nb and not (_fits(qkv, q_off, s, batch, T, hd, ld) and _fits(qkv, k_off, s, batch, T, hd, ld)
+                   and _fits(P, 0, sp, batch, T, T, T)):
+        raise ValueError("attention_probs: qkv or P too small for the batch")
     base = qkv.data_ptr()
     t0 = _TIMER.begin(stream) if _TIMER else None
     check(lib().repops_attention_probs(int(T), int(hd), base + 4 * q_off, base + 4 * k_off, int(ld), int(s[0]),
@@ -241,13 +248,6 @@ def repops_attention_probs(qkv, T, hd, ld, s, q_off, k_off, batch, P, sp, scale=
     if t0 is not None:
         _TIMER.end("gemm", t0, 2 * T * T * hd * nb, stream)
     return P
-
-
-def _fits(t, off, strides, batch, rows, cols, ld):
-    """the last (b0, b1) block of a strided batch lies inside t's storage"""
-    last = off + (int(batch[0]) - 1) * int(strides[0]) + (int(batch[1]) - 1) * int(strides[1]) + \
-        (rows - 1) * ld + cols
-    return t.storage_offset() + last <= t.untyped_storage().nbytes() // 4
 
 
 def repops_attention_dscores(dO, V, T, hd, ldo, so, o_off, ldv, sv, v_off, P, sp, dS, sd, batch, scale=1.0,
