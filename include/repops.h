@@ -369,6 +369,20 @@ typedef struct {
     uint8_t *digest;    /* device, 32 bytes */
     int32_t mode;       /* 0 = tensor digest; 1 = data_root only (MTH over chunks, no header) */
     int32_t reserved;
+    /* Incremental commitment of a tensor rewritten in place in a few chunks (all optional,
+     * NULL = unused; the digest is the same R-TCOMMIT digest either way):
+     * leaves_out  device [nchunks x 32 B]: the chunk leaf hashes are also stored here (an
+     *             opaque per-chunk leaf record, only meant to be passed as base_leaves);
+     * base_leaves device [nchunks x 32 B] from an earlier leaves_out of a tensor of the same
+     *             nbytes, with dirty: device uint8 [nchunks]: chunk c is hashed iff dirty[c]
+     *             != 0, otherwise its leaf is taken from base_leaves[c].  The CALLER
+     *             guarantees that every clean chunk holds exactly the bytes base_leaves[c]
+     *             was hashed from (e.g. EMBED_BWD, which adds into the rows of the shard's
+     *             tokens only); chunks are then not re-read, so a violated guarantee gives a
+     *             digest of the wrong bytes. */
+    uint8_t *leaves_out;
+    const uint8_t *base_leaves;
+    const uint8_t *dirty;
 } verde_tensor_desc;
 
 /* Digest of a tensor whose byte image was committed as k equal, contiguous
@@ -379,6 +393,14 @@ typedef struct {
  * subroots, dims, out32: host.  EINVAL if the slab geometry is not aligned. */
 int verde_digest_from_subroots(const uint8_t *subroots, int64_t k, int dtype, int rank, const int64_t *dims,
                                int64_t nbytes, uint8_t *out32);
+
+/* Dirty-chunk flags for an incremental commitment (verde_tensor_desc.dirty) of a row-major
+ * tensor whose rows `rows[0..n)` (int32, device; duplicates allowed) were rewritten:
+ * flags[c] = 1 iff bytes [4096 c, 4096 c + 4096) of the tensor meet one of those rows
+ * (row r = bytes [r row_bytes, (r + 1) row_bytes)), else 0; all = 1 sets every flag (full
+ * re-hash).  flags: device uint8 [nchunks], nchunks = ceil(nbytes / 4096).  One launch. */
+int verde_dirty_chunks(const int32_t *rows, int64_t n, int64_t row_bytes, int64_t nbytes, int all,
+                       uint8_t *flags, void *stream);
 
 /* Workspace (device bytes) needed to commit the given tensors in one call. */
 int64_t verde_commit_workspace_bytes(const verde_tensor_desc *descs /* host */, int n);

@@ -24,7 +24,7 @@ __all__ = [
     "repops_layernorm_backward_params", "repops_cross_entropy", "repops_exp", "repops_log", "repops_tanh",
     "repops_rsqrt", "repops_gelu", "repops_gelu_backward", "repops_relu", "repops_relu_backward", "repops_sin", "repops_cos", "repops_erf", "repops_gelu_erf", "repops_convert", "repops_gemm_ex",
     "repops_attention_fwd", "repops_attention_fwd_supported", "repops_attention_probs",
-    "repops_attention_probs_supported", "repops_attention_dscores", "repops_rand_uniform",
+    "repops_attention_probs_supported", "repops_attention_dscores", "verde_dirty_chunks", "repops_rand_uniform",
     "repops_dropout", "repops_dropout_backward",
     "repops_gelu_erf_backward", "repops_rope_tables", "repops_ipc_alloc", "repops_ipc_open", "repops_ipc_close",
     "repops_ipc_free", "repops_p2p_tree_combine", "repops_p2p_signal", "repops_p2p_wait", "repops_add", "repops_embedding",
@@ -765,10 +765,20 @@ class CommitWorkspace:
         return self.buf
 
 
-def _desc(t, digest, mode=0) -> TensorDesc:
+def _desc(t, digest, mode=0, leaves_out=None, base_leaves=None, dirty=None) -> TensorDesc:
     if not t.is_contiguous():
         raise RepopsError("committed tensors must be contiguous")
+    nch = (t.numel() * t.element_size() + 4095) // 4096
+    for buf, nb, what in ((leaves_out, 32 * nch, "leaves_out"), (base_leaves, 32 * nch, "base_leaves"),
+                          (dirty, nch, "dirty")):
+        if buf is not None and (buf.dtype != torch.uint8 or buf.numel() < nb or buf.device != t.device):
+            raise ValueError(f"{what}: need a uint8 device buffer of >= {nb} bytes")
+    if (base_leaves is None) != (dirty is None):
+        raise ValueError("base_leaves and dirty go together")
     d = TensorDesc()
+    d.leaves_out = leaves_out.data_ptr() if leaves_out is not None else None
+    d.base_leaves = base_leaves.data_ptr() if base_leaves is not None else None
+    d.dirty = dirty.data_ptr() if dirty is not None else None
     d.data = t.data_ptr() if t.numel() else None
     d.nbytes = t.numel() * t.element_size()
     d.dtype = _DT[t.dtype]
@@ -778,6 +788,20 @@ def _desc(t, digest, mode=0) -> TensorDesc:
     d.digest = digest.data_ptr()
     d.mode = mode
     return d
+
+
+def verde_dirty_chunks(rows, row_bytes, nbytes, out, all_chunks=False, stream=None):
+    """uint8 flags per 4096-byte chunk of a row-major tensor: 1 where one of `rows` (int32
+    device tensor) meets the chunk (verde_tensor_desc.dirty of an incremental commit)."""
+    nch = (int(nbytes) + 4095) // 4096
+    if out.dtype != torch.uint8 or out.numel() < nch:
+        raise ValueError(f"out: need >= {nch} uint8 flags")
+    if rows is not None and rows.dtype != torch.int32:
+        raise ValueError("rows must be int32")
+    n = 0 if rows is None else rows.numel()
+    check(lib().verde_dirty_chunks(rows.data_ptr() if n else None, n, int(row_bytes), int(nbytes),
+                                   int(bool(all_chunks)), out.data_ptr(), _stream(stream)), "verde_dirty_chunks")
+    return out
 
 
 def verde_commit_tensors(tensors, digests=None, ws: CommitWorkspace | None = None, stream=None, mode=0):
@@ -800,12 +824,15 @@ class CommitPlan:
     """verde_commit_plan_*: a prepared commit of a fixed list of tensors into
     fixed digest slots; run() only enqueues kernels."""
 
-    def __init__(self, tensors, digests, modes=None, device=None):
+    def __init__(self, tensors, digests, modes=None, device=None, incremental=None):
+        """incremental: {index: dict(leaves_out=..., base_leaves=..., dirty=...)} per tensor
+        (verde_tensor_desc's incremental-commit fields; same digests)."""
         n = len(tensors)
         self.n = n
         modes = modes or [0] * n
-        self._keep = (list(tensors), digests)
-        arr = (TensorDesc * n)(*[_desc(t, digests[i], modes[i]) for i, t in enumerate(tensors)])
+        inc = incremental or {}
+        self._keep = (list(tensors), digests, inc)
+        arr = (TensorDesc * n)(*[_desc(t, digests[i], modes[i], **inc.get(i, {})) for i, t in enumerate(tensors)])
         need = lib().verde_commit_workspace_bytes(arr, n)
         dev = device or tensors[0].device
         self.ws = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)

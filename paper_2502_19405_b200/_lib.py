@@ -19,7 +19,8 @@ i64, i32, f32, vp, u8p = C.c_int64, C.c_int, C.c_float, C.c_void_p, C.c_void_p
 class TensorDesc(C.Structure):
     """verde_tensor_desc (repops.h)"""
     _fields_ = [("data", C.c_void_p), ("nbytes", C.c_int64), ("dtype", C.c_int32), ("rank", C.c_int32),
-                ("dims", C.c_int64 * 8), ("digest", C.c_void_p), ("mode", C.c_int32), ("reserved", C.c_int32)]
+                ("dims", C.c_int64 * 8), ("digest", C.c_void_p), ("mode", C.c_int32), ("reserved", C.c_int32),
+                ("leaves_out", C.c_void_p), ("base_leaves", C.c_void_p), ("dirty", C.c_void_p)]
 
 
 class Node(C.Structure):
@@ -104,6 +105,7 @@ SIGNATURES = {
     "repops_gather_rows": (i32, [vp, vp, i64, i64, vp, vp]),
     "repops_fill_uniform": (i32, [vp, i64, C.c_uint64, C.c_double, vp]),
     "verde_commit_workspace_bytes": (i64, [vp, i32]),
+    "verde_dirty_chunks": (i32, [vp, i64, i64, i64, i32, vp, vp]),
     "verde_commit_tensors": (i32, [vp, i32, vp, i64, vp]),
     "verde_commit_tensor": (i32, [vp, i64, i32, i32, vp, vp, vp, i64, vp]),
     "verde_commit_plan_create": (i32, [vp, i32, vp, i64, vp]),

@@ -777,6 +777,14 @@ int repops_flip_bit(void *data, int64_t elem, int bit, void *stream) {
 }
 
 // ------------------------------------------------------------------ Verde
+int verde_dirty_chunks(const int32_t *rows, int64_t n, int64_t row_bytes, int64_t nbytes, int all, uint8_t *flags,
+                       void *stream) {
+    REQ(n >= 0 && row_bytes > 0 && nbytes >= 0, "dirty_chunks: negative extent");
+    REQ(flags && (all || n == 0 || rows), "dirty_chunks: null pointer");
+    REQ(n <= 12288, "dirty_chunks: at most 12288 rows per call");
+    return cuda_status(launch_dirty_chunks(rows, n, row_bytes, nbytes, all, flags, S(stream)), "dirty_chunks");
+}
+
 int64_t verde_commit_workspace_bytes(const verde_tensor_desc *descs, int n) {
     if (!descs || n <= 0) return 0;
     return commit_workspace_bytes(descs, n);
@@ -790,6 +798,7 @@ int verde_commit_tensors(const verde_tensor_desc *descs, int n, void *ws, int64_
         REQ(descs[t].nbytes >= 0 && (descs[t].nbytes == 0 || descs[t].data), "commit: tensor %d has no data", t);
         REQ(descs[t].rank >= 0 && descs[t].rank <= 8, "commit: tensor %d rank %d", t, descs[t].rank);
         REQ(descs[t].digest != nullptr, "commit: tensor %d has no digest buffer", t);
+        REQ(!descs[t].base_leaves || descs[t].dirty, "commit: tensor %d has base_leaves without dirty flags", t);
     }
     REQ(ws != nullptr, "commit: null workspace");
     int64_t need = 0;
@@ -808,6 +817,7 @@ int verde_commit_plan_create(const verde_tensor_desc *descs, int n, void *ws, in
         REQ(descs[t].nbytes >= 0 && (descs[t].nbytes == 0 || descs[t].data), "commit_plan: tensor %d has no data", t);
         REQ(descs[t].rank >= 0 && descs[t].rank <= 8, "commit_plan: tensor %d rank %d", t, descs[t].rank);
         REQ(descs[t].digest != nullptr, "commit_plan: tensor %d has no digest buffer", t);
+        REQ(!descs[t].base_leaves || descs[t].dirty, "commit_plan: tensor %d has base_leaves without dirty flags", t);
     }
     int64_t need = 0;
     void *out = nullptr;

@@ -240,6 +240,9 @@ struct DevTensor {
     int64_t dims[8];
     uint8_t *digest;
     int32_t dtype, rank, mode;
+    Digest *leaves_out;          // optional copy of the leaf hashes
+    const Digest *base_leaves;   // optional: clean chunks take their leaf from here
+    const uint8_t *dirty;        //           (chunk c hashed iff dirty[c])
 };
 
 RO_DEV int64_t find_seg(const int64_t *prefix, int n, int64_t g) {
@@ -260,13 +263,18 @@ __global__ void leaf_kernel(const DevTensor *__restrict__ ts, int n, const int64
         int t = (int)find_seg(chunk_prefix, n, g);
         int64_t c = g - chunk_prefix[t];
         const DevTensor &T = ts[t];
-        int64_t off = c * 4096;
-        int64_t len = T.nbytes - off < 4096 ? T.nbytes - off : 4096;
-        uint32_t st[8];
-        hash_leaf<MODE>(T.data + off, len, st);
         Digest d;
+        if (T.base_leaves && !T.dirty[c]) {
+            d = T.base_leaves[c];  // incremental commit: the chunk's bytes are unchanged
+        } else {
+            int64_t off = c * 4096;
+            int64_t len = T.nbytes - off < 4096 ? T.nbytes - off : 4096;
+            uint32_t st[8];
+            hash_leaf<MODE>(T.data + off, len, st);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) d.h[i] = st[i];
+            for (int i = 0; i < 8; ++i) d.h[i] = st[i];
+        }
+        if (T.leaves_out) T.leaves_out[c] = d;
         out[g] = d;
     }
 }
@@ -474,6 +482,9 @@ static std::vector<uint8_t> stage_tables(const verde_tensor_desc *d, int n, cons
         dt[t].dtype = d[t].dtype;
         dt[t].rank = d[t].rank;
         dt[t].mode = d[t].mode;
+        dt[t].leaves_out = reinterpret_cast<Digest *>(d[t].leaves_out);
+        dt[t].base_leaves = reinterpret_cast<const Digest *>(d[t].base_leaves);
+        dt[t].dirty = d[t].base_leaves ? d[t].dirty : nullptr;
     }
     memcpy(host.data(), dt.data(), sizeof(DevTensor) * n);
     memcpy(host.data() + L.tables, L.blob.data(), L.blob.size() * 8);
@@ -714,5 +725,38 @@ void root_plan_destroy(void *plan) { delete reinterpret_cast<RootPlanImpl *>(pla
 cudaError_t chunk_leaves_launch(const uint8_t *data, int64_t nbytes, uint8_t *leaves, cudaStream_t s) {
     const int64_t n = (nbytes + 4095) / 4096;
     chunk_leaf_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(data, nbytes, n, leaves);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ incremental commit flags
+namespace {
+__global__ void dirty_chunks_kernel(const int32_t *__restrict__ rows, int64_t n, int64_t row_bytes, int64_t nchunks,
+                                    int all, uint8_t *__restrict__ flags) {
+    extern __shared__ int32_t srow[];
+    if (!all)
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) srow[i] = rows[i];
+    __syncthreads();
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nchunks) return;
+    uint8_t f = all ? 1 : 0;
+    if (!all) {
+        const int64_t r0 = c * 4096 / row_bytes, r1 = (c * 4096 + 4095) / row_bytes;  // rows the chunk meets
+        for (int64_t i = 0; i < n && !f; ++i) f = (srow[i] >= r0 && srow[i] <= r1) ? 1 : 0;
+    }
+    flags[c] = f;
+}
+}  // namespace
+
+cudaError_t launch_dirty_chunks(const int32_t *rows, int64_t n, int64_t row_bytes, int64_t nbytes, int all,
+                                uint8_t *flags, cudaStream_t s) {
+    const int64_t nchunks = (nbytes + 4095) / 4096;
+    if (nchunks == 0) return cudaSuccess;
+    const size_t smem = all ? 0 : (size_t)n * sizeof(int32_t);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(dirty_chunks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    dirty_chunks_kernel<<<(unsigned)((nchunks + 255) / 256), 256, smem, s>>>(rows, n, row_bytes, nchunks, all, flags);
     return cudaGetLastError();
 }

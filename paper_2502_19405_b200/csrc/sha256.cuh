@@ -25,3 +25,5 @@ void commit_plan_destroy(void *plan);
 cudaError_t chunk_leaves_launch(const uint8_t *data, int64_t nbytes, uint8_t *leaves, cudaStream_t s);
 // tuning hook: resident leaf-kernel CTAs per SM (co-residency with GEMMs; bits-neutral)
 extern std::atomic<int> g_leaf_ctas_per_sm;
+cudaError_t launch_dirty_chunks(const int32_t *rows, int64_t n, int64_t row_bytes, int64_t nbytes, int all,
+                                uint8_t *flags, cudaStream_t s);

@@ -44,7 +44,7 @@ from . import (EPI_BIAS, EPI_SCALE, POST_GELU, POST_GELU_BACKWARD, CommitPlan, r
                repops_embedding_backward, repops_gelu, repops_gelu_backward, repops_gemm,
                repops_gemm_strided_batched, repops_layernorm, repops_layernorm_backward,
                repops_layernorm_backward_params, repops_softmax, repops_softmax_backward, repops_sum_cols_seq,
-               repops_adamw, repops_adamw_segments, repops_tree_sum)
+               repops_adamw, repops_adamw_segments, repops_tree_sum, verde_dirty_chunks)
 from ._lib import check, lib
 from .dist import P2PTreeCombine, all_gather_rows, dp_tree_combine, dp_tree_combine_sliced, gather_shard_digests, shard_block
 
@@ -171,6 +171,9 @@ class GPT2Step:
         # PV R-GEMM; same bits as the three launches.  Needs the scores to be operator scratch
         # (R29); fault-injection runs keep the per-op launches
         self.attn_probs = os.environ.get("REPOPS_ATTN_PROBS", "1") == "1"   # (A/B switch for tools)
+        # incremental commit of the tied embedding gradient (see the plan construction)
+        self.delta_commit = os.environ.get("REPOPS_DELTA_COMMIT", "1") == "1"
+        self._inject_active = False
         # its backward twin (repops_attention_dscores: dP in shared memory + softmax backward,
         # same dS bits) measured slower than the dP R-GEMM + softmax_bwd launches (181 vs
         # 161 us per layer, tools/attn_fused_bench.py): off by default
@@ -869,6 +872,9 @@ class GPT2Step:
             for q in range(self.S_loc):
                 repops_embedding_backward(self.tok_in[q], self.dx[0][q * c.seq:(q + 1) * c.seq], c.seq,
                                           self._gslice(self.s0 + q, "wte"), self._gslice(self.s0 + q, "wpe"))
+            for q, v, dirty in self._wte_inc:   # chunks of grad/wte the embedding backward rewrote
+                verde_dirty_chunks(self.tok_in[q], v.shape[-1] * 4, v.numel() * 4, dirty,
+                                   all_chunks=self._fault is not None or self._inject_active)
         self.launch(emb_bwd)
         self._cur[2].extend(self._deferred)
         self.phase("tree")
@@ -988,11 +994,33 @@ class GPT2Step:
         for i, t in enumerate(self._rep_ids):
             self._rep_owner[i] = self.owner.get(self.tensors[t].name.split("/", 1)[1], 0)
         not_mine = {t for i, t in enumerate(self._rep_ids) if self.zero1 and self._rep_owner[i] != self.rank}
+        # Incremental commitment of the tied embedding gradient (R-TCOMMIT digest unchanged):
+        # EMBED_BWD adds into the rows of the shard's tokens of the buffer that already holds
+        # LM_WGRAD's output (committed as s/grad/wte_lm), so grad/wte differs from it in at most
+        # ntok rows; its commit re-hashes only the 4 KiB chunks those rows meet and takes every
+        # other chunk leaf from the wte_lm commit (1.2 GB less SHA-256 per GPT-2 step).  Fault
+        # injection (config 5) re-hashes every chunk (an injected flip may sit anywhere).
+        inc = {}
+        self._wte_inc = []
+        if self.delta_commit and not self.structure_only:
+            for q in range(self.S_loc):
+                s_ = self.s0 + q
+                t_lm = next(t for t, tr in enumerate(self.tensors) if tr.name == f"s{s_}/grad/wte_lm")
+                t_w = next(t for t, tr in enumerate(self.tensors) if tr.name == f"s{s_}/grad/wte")
+                v = self.tensors[t_w].view
+                assert v.data_ptr() == self.tensors[t_lm].view.data_ptr() and v.numel() == self.tensors[t_lm].view.numel()
+                nch = (v.numel() * 4 + 4095) // 4096
+                leaves = torch.empty(nch * 32, dtype=torch.uint8, device=self.dev)
+                dirty = torch.ones(nch, dtype=torch.uint8, device=self.dev)
+                inc[t_lm] = dict(leaves_out=leaves)
+                inc[t_w] = dict(base_leaves=leaves, dirty=dirty)
+                self._wte_inc.append((q, v, dirty))
         for ph, tids in sorted(per_phase.items()):
             tids = [t for t in tids if t not in not_mine]
             if tids and not self.structure_only:
                 plan = CommitPlan([self.tensors[t].view for t in tids],
-                                  [self.digests[self.tensors[t].slot] for t in tids])
+                                  [self.digests[self.tensors[t].slot] for t in tids],
+                                  incremental={i: inc[t] for i, t in enumerate(tids) if t in inc})
                 self.plans.append(plan)
                 self.plan_after[ph] = plan
         self.commit_bytes = sum(p.nbytes for p in self.plans)
@@ -1131,6 +1159,7 @@ class GPT2Step:
         runs on the side stream and join() waits for everything."""
         main = torch.cuda.current_stream()
         side = self.side if self.overlap_commits else main
+        self._inject_active = inject is not None   # a coarse fault may land anywhere: full re-hash
         self.stash = {}
         if side is not main:
             side.wait_stream(main)  # the step's inputs (tokens, checkpoint) are ready

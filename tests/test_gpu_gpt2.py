@@ -169,6 +169,27 @@ def test_fused_attention_step_root_equals_unfused():
     assert roots[0] == roots[1] == roots[2]
 
 
+def test_incremental_wte_commit_roots_equal_full_rehash(monkeypatch):
+    """the tied embedding gradient committed incrementally (only the chunks the shard's
+    tokens touch re-hashed, the rest taken from the LM_WGRAD commit's leaves) gives the step
+    roots of re-hashing it in full, over steps with different token batches"""
+    from paper_2502_19405_b200.gpt2 import GPT2Config, GPT2Step
+    cfg = GPT2Config.tiny()
+    roots = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("REPOPS_DELTA_COMMIT", flag)
+        st = GPT2Step(cfg)
+        assert bool(st._wte_inc) == (flag == "1")
+        r = []
+        for k in range(3):
+            st.set_tokens(k)
+            st.run()
+            r.append(st.device_root())
+        roots.append(r)
+        del st
+    assert roots[0] == roots[1]
+
+
 def test_param_in_digest_reuse_matches_rehash():
     """PARAM_IN digests copied from the previous step's AdamW outputs (no re-hash of the
     unchanged training state) give exactly the step roots of re-hashing every step; an

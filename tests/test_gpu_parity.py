@@ -665,6 +665,65 @@ def test_commit_large_tensor_multi_pass():
     assert got2 == oracle.commit_tensor(b) and got2 != got
 
 
+def _dirty_ref(rows, row_bytes, nbytes):
+    nch = (nbytes + 4095) // 4096
+    f = np.zeros(nch, np.uint8)
+    for r in rows:
+        for c in range(r * row_bytes // 4096, ((r + 1) * row_bytes - 1) // 4096 + 1):
+            if c < nch:
+                f[c] = 1
+    return f
+
+
+@pytest.mark.parametrize("shape", [(50257, 768), (1000, 100), (37, 1024), (5, 3)])
+def test_incremental_commit_equals_full(shape):
+    """verde_dirty_chunks flags exactly the 4 KiB chunks the given rows meet (rows straddling
+    chunk edges, duplicates, first / last row); an incremental commit (clean chunk leaves taken
+    from an earlier commit's leaves_out) of the tensor with those rows rewritten has the full
+    commit's digest, which is the oracle's; with no rows it is the base digest"""
+    R_, Cc = shape
+    a = synth.uniform(synth.seed_for("inc", shape), shape)
+    t = dev(a)
+    nb = a.nbytes
+    nch = (nb + 4095) // 4096
+    leaves = torch.empty(nch * 32, dtype=torch.uint8, device="cuda")
+    dig = torch.zeros((2, 32), dtype=torch.uint8, device="cuda")
+    R.CommitPlan([t], [dig[0]], incremental={0: dict(leaves_out=leaves)}).run()
+    assert host(dig[0]).tobytes() == oracle.commit_tensor(a)
+    rng = np.random.default_rng(R_)
+    rows = sorted(set([0, R_ - 1, R_ // 2, R_ // 2] + rng.integers(0, R_, min(40, R_)).tolist()))
+    rows_l = rows + rows[:3]                                   # duplicates
+    b = a.copy()
+    b[rows] += np.float32(1.0)
+    t.copy_(torch.from_numpy(b))
+    dirty = torch.full((nch,), 7, dtype=torch.uint8, device="cuda")
+    rr = torch.tensor(rows_l, dtype=torch.int32, device="cuda")
+    R.verde_dirty_chunks(rr, Cc * 4, nb, dirty)
+    assert np.array_equal(host(dirty), _dirty_ref(rows_l, Cc * 4, nb))
+    plan = R.CommitPlan([t], [dig[1]], incremental={0: dict(base_leaves=leaves, dirty=dirty)})
+    plan.run()
+    assert host(dig[1]).tobytes() == oracle.commit_tensor(b) == host(R.verde_commit_tensor(t)).tobytes()
+    R.verde_dirty_chunks(None, Cc * 4, nb, dirty, all_chunks=True)   # full re-hash mode
+    assert int(host(dirty).min()) == 1
+    plan.run()
+    assert host(dig[1]).tobytes() == oracle.commit_tensor(b)
+    R.verde_dirty_chunks(rr[:0], Cc * 4, nb, dirty)                 # no rows: every leaf reused
+    assert int(host(dirty).max()) == 0
+    t.copy_(torch.from_numpy(a))
+    plan.run()
+    assert host(dig[1]).tobytes() == oracle.commit_tensor(a)
+
+
+def test_incremental_commit_rejects():
+    t = torch.zeros(2048, device="cuda")
+    d = torch.zeros(32, dtype=torch.uint8, device="cuda")
+    with pytest.raises(ValueError):
+        R.CommitPlan([t], [d], incremental={0: dict(base_leaves=torch.zeros(64, dtype=torch.uint8,
+                                                                              device="cuda"))})
+    with pytest.raises(ValueError):   # leaves_out too small for 2 chunks
+        R.CommitPlan([t], [d], incremental={0: dict(leaves_out=torch.zeros(32, dtype=torch.uint8, device="cuda"))})
+
+
 # ------------------------------------------------------------------ peer-memory combine (f1)
 @pytest.mark.parametrize("G", [1, 2, 4, 8])
 def test_p2p_tree_combine_equals_tree_sum(G):
