@@ -1033,7 +1033,7 @@ class GPT2Step:
         self._last_act_plan = max(i for i in self.plan_after if i < self._tail_from) if self.plan_after else -1
         self._joined = True
         if not self.structure_only:
-            self.side = torch.cuda.Stream(device=self.dev)
+            self.side = torch.cuda.Stream(device=self.dev, priority=int(os.environ.get("REPOPS_SIDE_PRIO", "0")))
             self.overlap_commits = True
             self._ev_act = torch.cuda.Event()
             self._ev_root = torch.cuda.Event()
