@@ -222,19 +222,21 @@ int repops_attention_fwd(int64_t T, int64_t hd, const float *Q, const float *K, 
                          int64_t batch1, void *stream);
 
 /* Attention scores + softmax fused, the probabilities only (f4, R7, R29, R31):
- * per (b0, b1) as above, P = R-SOFTMAX(R-GEMM(Q, K^T) with the SCALE epilogue) (causal:
- * row i keeps keys j <= i, masked P = +0, every element of the [T][T] block written).
- * The scores stay in shared memory (operator scratch, R29); with causal set only the key
- * blocks a CTA's rows read are computed (R31).  Bit-identical to
- * repops_gemm_strided_batched(SCALE) -> repops_softmax.  Q, K: rows of stride ld, head
- * dim hd, 16-byte aligned; P: [T][T] blocks at P + b0 sp0 + b1 sp1 (row stride T),
- * device, caller-owned.  Supported: hd = 64, T % 32 == 0, T <= 1024
- * (repops_attention_probs_supported), else REPOPS_ESHAPE; REPOPS_EINVAL: null,
- * misaligned, ld < hd. */
+ * per (b0 < batch0, b1 < batch1), with Q rows of stride ldq at Q + b0 sq0 + b1 sq1 and K
+ * rows of stride ldk at K + b0 sk0 + b1 sk1 (head dim hd; sk1 = 0 shares one K among the
+ * inner batch, e.g. grouped-query attention), P = R-SOFTMAX(R-GEMM(Q, K^T) with the SCALE
+ * epilogue) (causal: row i keeps keys j <= i, masked P = +0, every element of the [T][T]
+ * block written).  The scores stay in shared memory (operator scratch, R29); with causal set
+ * only the key blocks a CTA's rows read are computed (R31).  Bit-identical to
+ * repops_gemm_strided_batched(SCALE) -> repops_softmax.  P: [T][T] blocks at
+ * P + b0 sp0 + b1 sp1 (row stride T); device, caller-owned, 16-byte aligned rows.
+ * Supported (repops_attention_probs_supported): hd = 64 with T % 32 == 0, T <= 1024 (GPT-2),
+ * hd = 128 with T % 16 == 0, T <= 2048 (Llama), else REPOPS_ESHAPE; REPOPS_EINVAL: null,
+ * misaligned, ldq / ldk < hd. */
 int repops_attention_probs_supported(int64_t T, int64_t hd);
-int repops_attention_probs(int64_t T, int64_t hd, const float *Q, const float *K, int64_t ld, int64_t s0,
-                           int64_t s1, float scale, int causal, float *P, int64_t sp0, int64_t sp1,
-                           int64_t batch0, int64_t batch1, void *stream);
+int repops_attention_probs(int64_t T, int64_t hd, const float *Q, int64_t ldq, int64_t sq0, int64_t sq1,
+                           const float *K, int64_t ldk, int64_t sk0, int64_t sk1, float scale, int causal,
+                           float *P, int64_t sp0, int64_t sp1, int64_t batch0, int64_t batch1, void *stream);
 
 /* The backward twin (f4; R7's backward, R29): per (b0, b1), dP = R-GEMM(dO, V^T) (no
  * epilogue) over every key, kept in shared memory, then the softmax backward of each row:
@@ -242,7 +244,7 @@ int repops_attention_probs(int64_t T, int64_t hd, const float *Q, const float *K
  * repops_gemm_strided_batched(dO, V^T) -> repops_softmax_backward(P, dP, scale).  dO rows:
  * stride ldo at dO + b0 so0 + b1 so1; V rows: stride ldv at V + b0 sv0 + b1 sv1 (head dim
  * hd); P, dS: [T][T] blocks (row stride T) at P + b0 sp0 + b1 sp1, dS + b0 sd0 + b1 sd1;
- * device, caller-owned, 16-byte aligned rows.  Same support as repops_attention_probs
+ * device, caller-owned, 16-byte aligned rows.  Supported: hd = 64, T % 32 == 0, T <= 1024
  * (REPOPS_ESHAPE otherwise); REPOPS_EINVAL: null, misaligned, ldo / ldv < hd. */
 int repops_attention_dscores(int64_t T, int64_t hd, const float *dO, int64_t ldo, int64_t so0, int64_t so1,
                              const float *V, int64_t ldv, int64_t sv0, int64_t sv1, const float *P, int64_t sp0,

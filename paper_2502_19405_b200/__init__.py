@@ -227,23 +227,28 @@ def repops_attention_probs_supported(T, hd):
     return bool(lib().repops_attention_probs_supported(int(T), int(hd)))
 
 
-def repops_attention_probs(qkv, T, hd, ld, s, q_off, k_off, batch, P, sp, scale=1.0, causal=True, stream=None):
+def repops_attention_probs(qkv, T, hd, ld, s, q_off, k_off, batch, P, sp, scale=1.0, causal=True, stream=None,
+                           kv=None, ldk=None, sk=None):
     """Scores + softmax fused over a strided batch (element offsets / strides into the
     storage of qkv and P): P = causal R-SOFTMAX(R-GEMM(Q K^T) * scale), the scores never
     leaving shared memory -- bit-identical to repops_gemm_strided_batched(SCALE) ->
-    repops_softmax."""
-    _f32(qkv, "qkv"), _f32(P, "P")
-    if P.device != qkv.device:
-        raise ValueError("P must be on the device of qkv")
+    repops_softmax.  K comes from kv (default qkv) with row stride ldk and batch strides sk
+    (default ld, s; sk[1] = 0 shares one K among the inner batch, grouped-query attention)."""
+    kv = qkv if kv is None else kv
+    ldk = ld if ldk is None else ldk
+    sk = s if sk is None else sk
+    _f32(qkv, "qkv"), _f32(kv, "kv"), _f32(P, "P")
+    if P.device != qkv.device or kv.device != qkv.device:
+        raise ValueError("qkv, kv and P must be on one device")
     nb = int(batch[0]) * int(batch[1])
-    if nb and not (_fits(qkv, q_off, s, batch, T, hd, ld) and _fits(qkv, k_off, s, batch, T, hd, ld)
+    if nb and not (_fits(qkv, q_off, s, batch, T, hd, ld) and _fits(kv, k_off, sk, batch, T, hd, ldk)
                    and _fits(P, 0, sp, batch, T, T, T)):
-        raise ValueError("attention_probs: qkv or P too small for the batch")
-    base = qkv.data_ptr()
+        raise ValueError("attention_probs: qkv, kv or P too small for the batch")
     t0 = _TIMER.begin(stream) if _TIMER else None
-    check(lib().repops_attention_probs(int(T), int(hd), base + 4 * q_off, base + 4 * k_off, int(ld), int(s[0]),
-                                       int(s[1]), float(scale), int(bool(causal)), P.data_ptr(), int(sp[0]),
-                                       int(sp[1]), int(batch[0]), int(batch[1]), _stream(stream)),
+    check(lib().repops_attention_probs(int(T), int(hd), qkv.data_ptr() + 4 * q_off, int(ld), int(s[0]), int(s[1]),
+                                       kv.data_ptr() + 4 * k_off, int(ldk), int(sk[0]), int(sk[1]), float(scale),
+                                       int(bool(causal)), P.data_ptr(), int(sp[0]), int(sp[1]), int(batch[0]),
+                                       int(batch[1]), _stream(stream)),
           "repops_attention_probs")
     if t0 is not None:
         _TIMER.end("gemm", t0, 2 * T * T * hd * nb, stream)

@@ -65,7 +65,8 @@ SIGNATURES = {
     "repops_erf": (i32, [vp, i64, vp, vp]),
     "repops_attention_fwd_supported": (i32, [i64, i64]),
     "repops_attention_probs_supported": (i32, [i64, i64]),
-    "repops_attention_probs": (i32, [i64, i64, vp, vp, i64, i64, i64, f32, i32, vp, i64, i64, i64, i64, vp]),
+    "repops_attention_probs": (i32, [i64, i64, vp, i64, i64, i64, vp, i64, i64, i64, f32, i32, vp, i64, i64, i64,
+                                     i64, vp]),
     "repops_attention_dscores": (i32, [i64, i64, vp, i64, i64, i64, vp, i64, i64, i64, vp, i64, i64, f32, vp, i64,
                                        i64, i64, i64, vp]),
     "repops_attention_fwd": (i32, [i64, i64, vp, vp, vp, i64, i64, i64, f32, i32, vp, vp, i64, i64, vp, i64, i64, i64,

@@ -331,21 +331,22 @@ int repops_attention_fwd_supported(int64_t T, int64_t hd) { return attention_fwd
 
 int repops_attention_probs_supported(int64_t T, int64_t hd) { return attention_probs_supported(T, hd) ? 1 : 0; }
 
-int repops_attention_probs(int64_t T, int64_t hd, const float *Q, const float *K, int64_t ld, int64_t s0,
-                           int64_t s1, float scale, int causal, float *P, int64_t sp0, int64_t sp1,
-                           int64_t batch0, int64_t batch1, void *stream) {
+int repops_attention_probs(int64_t T, int64_t hd, const float *Q, int64_t ldq, int64_t sq0, int64_t sq1,
+                           const float *K, int64_t ldk, int64_t sk0, int64_t sk1, float scale, int causal,
+                           float *P, int64_t sp0, int64_t sp1, int64_t batch0, int64_t batch1, void *stream) {
     REQ(T >= 0 && hd >= 0 && batch0 >= 0 && batch1 >= 0, "attention_probs: negative extent");
     if (T == 0 || batch0 * batch1 == 0) return REPOPS_OK;
     if (!attention_probs_supported(T, hd))
-        return fail(REPOPS_ESHAPE, "attention_probs: T = %lld, hd = %lld unsupported (hd 64, T %% 32 == 0, T <= 1024)",
-                    (long long)T, (long long)hd);
+        return fail(REPOPS_ESHAPE,
+                    "attention_probs: T = %lld, hd = %lld unsupported (hd 64: T %% 32 == 0, T <= 1024; "
+                    "hd 128: T %% 16 == 0, T <= 2048)", (long long)T, (long long)hd);
     REQ(Q && K && P, "attention_probs: null pointer");
-    REQ(ld >= hd, "attention_probs: leading dimension < hd");
-    const bool al = a16(Q) && a16(K) && a16(P) && ld % 4 == 0 && s0 % 4 == 0 && s1 % 4 == 0 && sp0 % 4 == 0 &&
-                    sp1 % 4 == 0;
+    REQ(ldq >= hd && ldk >= hd, "attention_probs: leading dimension < hd");
+    const bool al = a16(Q) && a16(K) && a16(P) && ldq % 4 == 0 && ldk % 4 == 0 && sq0 % 4 == 0 && sq1 % 4 == 0 &&
+                    sk0 % 4 == 0 && sk1 % 4 == 0 && sp0 % 4 == 0 && sp1 % 4 == 0;
     REQ(al, "attention_probs: rows must be 16-byte aligned");
-    return cuda_status(launch_attention_probs(T, Q, K, ld, s0, s1, scale, causal, P, sp0, sp1, batch0, batch1,
-                                              S(stream)),
+    return cuda_status(launch_attention_probs(T, hd, Q, K, ldq, sq0, sq1, ldk, sk0, sk1, scale, causal, P, sp0, sp1,
+                                              batch0, batch1, S(stream)),
                        "attention_probs");
 }
 
@@ -355,7 +356,7 @@ int repops_attention_dscores(int64_t T, int64_t hd, const float *dO, int64_t ldo
                              int64_t batch1, void *stream) {
     REQ(T >= 0 && hd >= 0 && batch0 >= 0 && batch1 >= 0, "attention_dscores: negative extent");
     if (T == 0 || batch0 * batch1 == 0) return REPOPS_OK;
-    if (!attention_probs_supported(T, hd))
+    if (!attention_dscores_supported(T, hd))
         return fail(REPOPS_ESHAPE, "attention_dscores: T = %lld, hd = %lld unsupported (hd 64, T %% 32 == 0, T <= 1024)",
                     (long long)T, (long long)hd);
     REQ(dO && V && P && dS, "attention_dscores: null pointer");

@@ -321,10 +321,20 @@ __global__ void __launch_bounds__(THREADS, 1) attn_fwd_kernel(AttnArgs a) {
 // backward's row fold reads every column), and phase 2 is softmax_bwd_warp's sequence:
 // c = CDOT(P row, dP row) (128 slots of fma from +0, then TREE128), dS = canon(fmul(fmul(P,
 // fsub(dP, c)), scale)).  dP never reaches HBM; bits equal repops_gemm -> repops_softmax_backward.
-constexpr int PS_BM = 32, PS_THREADS = 256, PS_KB = 256, PS_DS = 8, PS_KLD = PS_DS + 4, PS_NST = 3;
+constexpr int PS_THREADS = 256, PS_DS = 8, PS_KLD = PS_DS + 4, PS_NST = 3;
+// Row block per head dim: 64 -> 32 query rows (8 q-groups x 4 key groups of lanes per warp,
+// 256-key blocks); 128 (Llama) -> 16 rows (4 x 8 lanes per warp, 512-key blocks) so the score
+// rows of T = 2048 fit beside the K ring (16 x 2052 x 4 B + 3 x 512 x 12 x 4 B + Q^T = 211 KB).
+template <int PHD> struct ProbGeom {
+    static constexpr int BM = PHD == 64 ? 32 : 16;
+    static constexpr int NQG = BM / 4;                 // query groups (lanes along q)
+    static constexpr int NKG = 32 / NQG;               // key groups (lanes along keys)
+    static constexpr int KW = NKG * 8;                 // keys per warp
+    static constexpr int KB = KW * (PS_THREADS / 32);  // keys per block
+};
 
 struct ProbArgs {
-    const float *A, *B;          // rows of A (Q or dO) and B (K or V), head dim HD
+    const float *A, *B;          // rows of A (Q or dO) and B (K or V), head dim PHD
     int64_t lda, sa0, sa1, ldb, sb0, sb1;
     const float *Pin;            // MODE 1: P blocks (row stride T)
     int64_t spi0, spi1;
@@ -335,12 +345,14 @@ struct ProbArgs {
     float scale;
 };
 
-template <int MODE>
-__global__ void __launch_bounds__(PS_THREADS, 2) attn_probs_kernel(ProbArgs a) {
+template <int MODE, int PHD>
+__global__ void __launch_bounds__(PS_THREADS, PHD == 64 ? 2 : 1) attn_probs_kernel(ProbArgs a) {
+    using G = ProbGeom<PHD>;
+    constexpr int PS_BM = G::BM, PS_KB = G::KB, NQG = G::NQG, NKG = G::NKG, KW = G::KW;
     extern __shared__ __align__(16) float sm[];
     const int T = a.T, SLD = T + 4;
-    float *Qt = sm;                       // [HD][PS_BM]
-    float *Ss = Qt + HD * PS_BM;          // [PS_BM][T + 4]
+    float *Qt = sm;                       // [PHD][PS_BM]
+    float *Ss = Qt + PHD * PS_BM;         // [PS_BM][T + 4]
     float *Ks = Ss + PS_BM * SLD;         // [PS_NST][PS_KB][PS_KLD] ring of d-slices of a key block
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nqb = T / PS_BM;
@@ -352,7 +364,7 @@ __global__ void __launch_bounds__(PS_THREADS, 2) attn_probs_kernel(ProbArgs a) {
     const int kneed = (MODE == 0 && a.causal) ? min(T, q0 + PS_BM) : T;
 
 #pragma unroll
-    for (int q = 0; q < PS_BM * HD / 4 / PS_THREADS; ++q) {
+    for (int q = 0; q < PS_BM * PHD / 4 / PS_THREADS; ++q) {
         const int c = tid + q * PS_THREADS;
         const int r = c % PS_BM, kq = (c / PS_BM) * 4;
         const float4 v = __ldg(reinterpret_cast<const float4 *>(Q + (int64_t)(q0 + r) * a.lda + kq));
@@ -362,12 +374,14 @@ __global__ void __launch_bounds__(PS_THREADS, 2) attn_probs_kernel(ProbArgs a) {
         Qt[(kq + 3) * PS_BM + r] = v.w;
     }
 
-    // thread tile: queries 4 qg .. 4 qg + 3, keys kb + 32 warp + kg + 4 j (j < 8)
-    const int qg = lane & 7, kg = lane >> 3;
+    // thread tile: queries 4 qg .. 4 qg + 3, keys kb + KW warp + kg + NKG j (j < 8)
+    const int qg = lane % NQG, kg = lane / NQG;
     for (int kb = 0; kb < kneed; kb += PS_KB) {
         const int nk = min(PS_KB, kneed - kb);           // keys of this block that are read
-        const int nrows = (nk + 31) & ~31;               // staged rows (whole warps)
-        const bool active = 32 * warp < nk;              // warp-uniform
+        // staged rows: whole warps' key ranges, never past the T keys of the head (a warp's
+        // keys >= T compute on stale shared memory and are not stored)
+        const int nrows = min((nk + KW - 1) / KW * KW, T - kb);
+        const bool active = KW * warp < nk;              // warp-uniform
         auto stage = [&](int buf, int ds) {              // K[kb .. kb + nrows)[ds .. ds + 8)
             float *dst = Ks + buf * PS_KB * PS_KLD;
             for (int c = tid; c < nrows * (PS_DS / 4); c += PS_THREADS) {
@@ -383,19 +397,19 @@ __global__ void __launch_bounds__(PS_THREADS, 2) attn_probs_kernel(ProbArgs a) {
             stage(s, s * PS_DS);
             cp_commit();
         }
-        for (int s = 0; s < HD / PS_DS; ++s) {
-            if (s + PS_NST - 1 < HD / PS_DS) stage((s + PS_NST - 1) % PS_NST, (s + PS_NST - 1) * PS_DS);
+        for (int s = 0; s < PHD / PS_DS; ++s) {
+            if (s + PS_NST - 1 < PHD / PS_DS) stage((s + PS_NST - 1) % PS_NST, (s + PS_NST - 1) * PS_DS);
             cp_commit();
             cp_wait<PS_NST - 1>();
             __syncthreads();
             if (active) {
-                const float *Kb = Ks + (s % PS_NST) * PS_KB * PS_KLD + (32 * warp + kg) * PS_KLD;
+                const float *Kb = Ks + (s % PS_NST) * PS_KB * PS_KLD + (KW * warp + kg) * PS_KLD;
 #pragma unroll
                 for (int d4 = 0; d4 < PS_DS; d4 += 4) {
                     float kv[8][4];
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
-                        const float4 v = *reinterpret_cast<const float4 *>(Kb + 4 * j * PS_KLD + d4);
+                        const float4 v = *reinterpret_cast<const float4 *>(Kb + NKG * j * PS_KLD + d4);
                         kv[j][0] = v.x; kv[j][1] = v.y; kv[j][2] = v.z; kv[j][3] = v.w;
                     }
 #pragma unroll
@@ -417,7 +431,8 @@ __global__ void __launch_bounds__(PS_THREADS, 2) attn_probs_kernel(ProbArgs a) {
             auto epi = [&](float x) { return MODE == 0 ? canon(__fmul_rn(x, a.scale)) : canon(x); };
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                const int key = kb + 32 * warp + kg + 4 * j;
+                const int key = kb + KW * warp + kg + NKG * j;
+                if (key >= T) continue;   // (T % KW != 0 with hd 128) -- a row holds T + 4 columns
                 float *srow = Ss + 4 * qg * SLD + key;
                 srow[0] = epi(acc[j][0].x);
                 srow[SLD] = epi(acc[j][0].y);
@@ -566,34 +581,46 @@ cudaError_t launch_attention_fwd(int64_t T, const float *Q, const float *K, cons
 }
 
 
-static size_t probs_smem_bytes(int64_t T) {
-    return (size_t)(HD * PS_BM + PS_BM * (T + 4) + PS_NST * PS_KB * PS_KLD) * sizeof(float);
+template <int PHD>
+static size_t probs_smem_bytes_t(int64_t T) {
+    using G = ProbGeom<PHD>;
+    return (size_t)(PHD * G::BM + G::BM * (T + 4) + PS_NST * G::KB * PS_KLD) * sizeof(float);
+}
+
+static size_t probs_smem_bytes(int64_t T, int64_t hd) {
+    return hd == 64 ? probs_smem_bytes_t<64>(T) : probs_smem_bytes_t<128>(T);
 }
 
 bool attention_probs_supported(int64_t T, int64_t hd) {
-    return hd == HD && T > 0 && T % PS_BM == 0 && T % 4 == 0 && probs_smem_bytes(T) <= 227 * 1024;
+    if (hd != 64 && hd != 128) return false;
+    const int bm = hd == 64 ? ProbGeom<64>::BM : ProbGeom<128>::BM;
+    return T > 0 && T % bm == 0 && T % 4 == 0 && probs_smem_bytes(T, hd) <= 227 * 1024;
 }
 
-template <int MODE>
+bool attention_dscores_supported(int64_t T, int64_t hd) { return hd == 64 && attention_probs_supported(T, hd); }
+
+template <int MODE, int PHD>
 static cudaError_t launch_probs_mode(const ProbArgs &a, int64_t nb, cudaStream_t s) {
-    const size_t smem = probs_smem_bytes(a.T);
+    const size_t smem = probs_smem_bytes_t<PHD>(a.T);
     static size_t attr = 0;
     if (smem > attr) {
-        cudaError_t e = cudaFuncSetAttribute(attn_probs_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(attn_probs_kernel<MODE, PHD>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         attr = smem;
     }
-    attn_probs_kernel<MODE><<<(unsigned)(a.T / PS_BM * nb), PS_THREADS, smem, s>>>(a);
+    attn_probs_kernel<MODE, PHD><<<(unsigned)(a.T / ProbGeom<PHD>::BM * nb), PS_THREADS, smem, s>>>(a);
     return cudaGetLastError();
 }
 
-cudaError_t launch_attention_probs(int64_t T, const float *Q, const float *K, int64_t ld, int64_t s0, int64_t s1,
-                                   float scale, int causal, float *P, int64_t sp0, int64_t sp1, int64_t batch0,
-                                   int64_t batch1, cudaStream_t s) {
+cudaError_t launch_attention_probs(int64_t T, int64_t hd, const float *Q, const float *K, int64_t ld, int64_t s0,
+                                   int64_t s1, int64_t ldk, int64_t sk0, int64_t sk1, float scale, int causal,
+                                   float *P, int64_t sp0, int64_t sp1, int64_t batch0, int64_t batch1,
+                                   cudaStream_t s) {
     if (batch0 * batch1 == 0 || T == 0) return cudaSuccess;
-    ProbArgs a{Q, K, ld, s0, s1, ld, s0, s1, nullptr, 0, 0, P, sp0, sp1, batch1, batch0 * batch1, (int)T, causal, scale};
-    return launch_probs_mode<0>(a, batch0 * batch1, s);
+    ProbArgs a{Q, K, ld, s0, s1, ldk, sk0, sk1, nullptr, 0, 0, P, sp0, sp1, batch1, batch0 * batch1, (int)T, causal,
+               scale};
+    return hd == 64 ? launch_probs_mode<0, 64>(a, batch0 * batch1, s) : launch_probs_mode<0, 128>(a, batch0 * batch1, s);
 }
 
 cudaError_t launch_attention_dscores(int64_t T, const float *dO, int64_t ldo, int64_t so0, int64_t so1,
@@ -603,5 +630,5 @@ cudaError_t launch_attention_dscores(int64_t T, const float *dO, int64_t ldo, in
     if (batch0 * batch1 == 0 || T == 0) return cudaSuccess;
     ProbArgs a{dO, V, ldo, so0, so1, ldv, sv0, sv1, P, sp0, sp1, dS, sd0, sd1, batch1, batch0 * batch1, (int)T, 0,
                scale};
-    return launch_probs_mode<1>(a, batch0 * batch1, s);
+    return launch_probs_mode<1, 64>(a, batch0 * batch1, s);
 }

@@ -38,6 +38,7 @@ import torch
 import synth
 
 from . import (repops_causal_suffix_flags, repops_copy2d_batched, EPI_SCALE, CommitPlan, RootPlan, repops_add, repops_copy2d, repops_fill_uniform, repops_gather_rows,
+               repops_attention_probs, repops_attention_probs_supported,
                repops_gemm_strided_batched, repops_rmsnorm, repops_rope, repops_softmax, repops_swiglu,
                repops_rope_tables, repops_transpose, verde_commit_tensors)
 from ._lib import check, lib
@@ -135,6 +136,12 @@ class LlamaPrefill:
         # R29: attention scores / probabilities are operator-internal scratch shared by all layers
         self.S_scr, self.P_scr = E(nbl, qh * T, T), E(nbl, qh * T, T)
         self.causal_skip = True   # f4: exact causal tile skipping in the attention GEMMs
+        # f4: the fused scores + softmax kernel (hd 64 / 128), same P bits.  Off by default: at
+        # the Llama shape its 16-row blocks (the widest whose 2048-column score rows fit in
+        # shared memory) re-stream K per block at one CTA per SM -- 1165 us vs 767 us for the
+        # causal-skip scores R-GEMM + softmax per layer (tools/llama_attn_tune.py)
+        self.attn_probs = (os.environ.get("REPOPS_ATTN_PROBS_LLAMA", "0") == "1"
+                           and repops_attention_probs_supported(self.cfg.seq, self.cfg.hd))
         self.vflags = torch.empty((nbl, T + 1, hd), dtype=torch.uint8, device=self.dev)
         for _ in range(L):
             self.act.append(dict(xn=E(T, d), rs1=E(T), qkv=E(nbl, T, self.Wb), qk=E(nbl, T, (qh + 1) * hd),
@@ -341,11 +348,17 @@ class LlamaPrefill:
         # at each tile's last query row and the skipped +0-probability terms are applied in
         # closed form from V's suffix flags -- the attention output bits are those of the
         # full R-GEMM -> R-SOFTMAX -> R-GEMM composition for every input
-        repops_gemm_strided_batched(a["qk"], a["qk"], a["S"], M=T, N=T, K=hd, lda=W2, ldb=W2, ldc=T,
-                                    sA=(T * W2, hd), sB=(T * W2, 0), sC=(qh * T * T, T * T), batch=(nbl, qh),
-                                    transB=True, epi=EPI_SCALE, scale=scale, offB=qh * hd,
-                                    causal=1 if self.causal_skip else 0)
-        repops_softmax(a["S"].view(-1, T), causal=True, out=a["P"].view(-1, T))
+        if self.attn_probs and self.causal_skip:
+            # scores + causal softmax in one kernel: the scores never leave shared memory (R29),
+            # key blocks above a row block are not computed (R31); same P bits
+            repops_attention_probs(a["qk"], T, hd, W2, (T * W2, hd), 0, qh * hd, (nbl, qh), a["P"],
+                                   (qh * T * T, T * T), scale=scale, causal=True, sk=(T * W2, 0))
+        else:
+            repops_gemm_strided_batched(a["qk"], a["qk"], a["S"], M=T, N=T, K=hd, lda=W2, ldb=W2, ldc=T,
+                                        sA=(T * W2, hd), sB=(T * W2, 0), sC=(qh * T * T, T * T), batch=(nbl, qh),
+                                        transB=True, epi=EPI_SCALE, scale=scale, offB=qh * hd,
+                                        causal=1 if self.causal_skip else 0)
+            repops_softmax(a["S"].view(-1, T), causal=True, out=a["P"].view(-1, T))
         if self.causal_skip:
             repops_causal_suffix_flags(a["qkv"], T, hd, Wb, (T * Wb, 0), (nbl, 1), out=self.vflags,
                                        ldf=hd, sF=((T + 1) * hd, 0), offB=(qh + 1) * hd)

@@ -177,3 +177,23 @@ def test_full_llama_prefill_sampled_referee():
     g = al["g"][7].cpu().numpy()[:64]
     u = al["u"][7].cpu().numpy()[:64]
     assert np.array_equal(bits(al["a"][7].cpu().numpy()[:64]), bits(oracle.swiglu(g, u)))
+
+
+def test_llama_fused_probs_root_equals_unfused(monkeypatch):
+    """a Llama-shaped prefill with hd = 128 (the full model's head dim) through the fused
+    scores + softmax kernel commits the same attention outputs as the causal-skip scores
+    R-GEMM + R-SOFTMAX path: identical pass roots"""
+    from paper_2502_19405_b200.llama import LlamaConfig, LlamaPrefill
+    cfg = LlamaConfig(n_layer=2, d=2048, n_head=16, n_kv=8, hd=128, ffn=256, vocab=512, seq=256)
+    roots = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("REPOPS_ATTN_PROBS_LLAMA", flag)
+        st = LlamaPrefill(cfg)
+        assert st.attn_probs == (flag == "1")
+        st.load_weights()
+        st.set_tokens()
+        st.run()
+        roots.append(st.device_root())
+        del st
+        torch.cuda.empty_cache()
+    assert roots[0] == roots[1]

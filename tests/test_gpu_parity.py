@@ -1030,11 +1030,12 @@ def test_attention_probs_equals_unfused_and_oracle(T, causal):
 def test_attention_probs_rejects():
     qkv = torch.zeros(64, 3 * 64, device="cuda")
     P = torch.zeros(64, 64, device="cuda")
-    assert not R.repops_attention_probs_supported(64, 128)
+    assert not R.repops_attention_probs_supported(64, 96)
     assert not R.repops_attention_probs_supported(100, 64)
     assert not R.repops_attention_probs_supported(4096, 64)
+    assert not R.repops_attention_probs_supported(4096, 128) and not R.repops_attention_probs_supported(40, 128)
     with pytest.raises(R.RepopsError):
-        R.repops_attention_probs(qkv, 64, 128, 3 * 64, (0, 0), 0, 64, (1, 1), P, (0, 0))
+        R.repops_attention_probs(qkv, 64, 96, 3 * 64, (0, 0), 0, 64, (1, 1), P, (0, 0))
     with pytest.raises(ValueError):
         R.repops_attention_probs(qkv, 128, 64, 3 * 64, (0, 0), 0, 64, (1, 1), P, (0, 0))  # P too small
 
@@ -1085,3 +1086,37 @@ def test_attention_dscores_rejects():
         R.repops_attention_dscores(x, x, 64, 128, 3 * 64, (0, 0), 0, 3 * 64, (0, 0), 0, P, (0, 0), P, (0, 0), (1, 1))
     with pytest.raises(ValueError):   # dS too small for T = 128
         R.repops_attention_dscores(x, x, 128, 64, 3 * 64, (0, 0), 0, 3 * 64, (0, 0), 0, P, (0, 0), P, (0, 0), (1, 1))
+
+
+@pytest.mark.parametrize("T,causal", [(2048, True), (256, True), (48, True), (96, False)])
+def test_attention_probs_hd128_grouped_query(T, causal):
+    """hd = 128 (Llama): 16-row blocks, 512-key blocks; the Llama prefill's layout -- per
+    column block j a [T][(qh + 1) hd] buffer of qh query heads and one shared key head
+    (K batch stride 0 across the query heads) -- P bit-identical to the causal-skip scores
+    R-GEMM + R-SOFTMAX of the prefill and to the oracle on sampled heads; T = 48 is ragged
+    against the 512-key blocks"""
+    nbl, qh, hd = 2 if T == 2048 else 3, 4, 128
+    W2 = (qh + 1) * hd
+    qk_h = synth.uniform(90 + T, (nbl * T, W2), 1.0)
+    qk_h[3, 0:hd] *= 40.0                            # a row whose exps mostly underflow
+    qk_h[T + 5, qh * hd + 7] = np.inf                # key 5 of block 1: +-inf / NaN scores
+    qk = dev(qk_h)
+    scale = float(np.float32(1.0 / np.sqrt(hd)))
+    sp = (qh * T * T, T * T)
+    Pf = torch.full((nbl * qh * T, T), 7.0, device="cuda")
+    assert R.repops_attention_probs_supported(T, hd)
+    R.repops_attention_probs(qk, T, hd, W2, (T * W2, hd), 0, qh * hd, (nbl, qh), Pf, sp, scale=scale, causal=causal,
+                             sk=(T * W2, 0))
+    Su = torch.full_like(Pf, 5.0)
+    R.repops_gemm_strided_batched(qk, qk, Su, M=T, N=T, K=hd, lda=W2, ldb=W2, ldc=T, sA=(T * W2, hd),
+                                  sB=(T * W2, 0), sC=sp, batch=(nbl, qh), transB=True, epi=R.EPI_SCALE, scale=scale,
+                                  offB=qh * hd, causal=1 if causal else 0)
+    Pu = R.repops_softmax(Su, causal=causal)
+    Ph = host(Pf)
+    assert_bits(Ph, host(Pu), "P fused vs unfused (hd 128)")
+    for j, h in ((0, 0), (nbl - 1, qh - 1), (1, 2)):
+        q = np.ascontiguousarray(qk_h[j * T:(j + 1) * T, h * hd:(h + 1) * hd])
+        k = np.ascontiguousarray(qk_h[j * T:(j + 1) * T, qh * hd:(qh + 1) * hd])
+        ref = oracle.softmax(oracle.gemm(q, k, transB=True, epi=2, scale=scale), causal=causal)
+        r0 = (j * qh + h) * T
+        assert_bits(Ph[r0:r0 + T], ref, f"P oracle block {j} head {h}")

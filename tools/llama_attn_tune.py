@@ -68,3 +68,23 @@ run("PV NN causal2", lambda: R.repops_gemm_strided_batched(
     P, qkv, o, M=T, N=hd, K=T, lda=T, ldb=Wb, ldc=qh * hd, sA=(qh * T * T, T * T), sB=(T * Wb, 0),
     sC=(T * qh * hd, hd), batch=(nbl, qh), offB=(qh + 1) * hd, causal=2, kflags=fl, ldf=hd,
     sF=((T + 1) * hd, 0)), o, half, [-1, 0, 1, 3, 5, 6, 10, 11, 13, 2])
+
+# the fused scores + softmax kernel against the two launches it replaces
+P2 = torch.empty_like(P)
+
+
+def unfused():
+    R.repops_gemm_strided_batched(qk, qk, S, M=T, N=T, K=hd, lda=W2, ldb=W2, ldc=T, sA=(T * W2, hd),
+                                  sB=(T * W2, 0), sC=(qh * T * T, T * T), batch=(nbl, qh), transB=True,
+                                  epi=R.EPI_SCALE, scale=0.088, offB=qh * hd, causal=1)
+    R.repops_softmax(S.view(-1, T), causal=True, out=P.view(-1, T))
+
+
+def fused():
+    R.repops_attention_probs(qk, T, hd, W2, (T * W2, hd), 0, qh * hd, (nbl, qh), P2, (qh * T * T, T * T),
+                             scale=0.088, causal=True, sk=(T * W2, 0))
+
+
+mu, mf = t_ms(unfused), t_ms(fused)
+same = torch.equal(P.view(torch.int32), P2.view(torch.int32))
+print(f"scores+softmax unfused {mu * 1e3:6.0f} us | fused probs {mf * 1e3:6.0f} us | bits {'same' if same else 'DIFFER'}")
