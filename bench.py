@@ -336,6 +336,77 @@ class LlamaPrefillBench:
     d2h_bytes = 32
 
 
+def verde_dispute_bench(trials=10, with_oracle=True):
+    """BASELINE config 5, the dispute half: an honest and a dishonest trainer of the full
+    GPT-2 124M step (the dishonest one flips bit 0 of one element of one operator output,
+    node and element drawn from the seeded generator) -- Verde Phase 2 (Alg. 2: line-7
+    consistency, Merkle descent to the first diverging node) and the decision (Case 3 at
+    4 KiB-chunk granularity, the referee recomputing only the rows of the disputed chunk).
+    Per trial: found == injected node, case, convicted party, descent rounds, wall time of
+    phase 2 + decision (the two trainers' steps are outside it).  Beside it: the oracle's
+    SHA-256 commitment rate on one host core."""
+    import torch
+
+    import synth
+    from paper_2502_19405_b200 import verde
+    from paper_2502_19405_b200.gpt2 import OP, GPT2Config, GPT2Step
+    cfg = GPT2Config()
+    honest = GPT2Step(cfg)
+    honest.keep_committed = True
+    honest.set_tokens(0)
+    ck = (honest.params.clone(), honest.m.clone(), honest.v.clone())
+    honest.run()
+    th = verde.Trainer(honest, ck)
+    cheat = GPT2Step(cfg)
+    cheat.keep_committed = True
+    skip = {OP["TOKENS_IN"], OP["EMBED"], OP["EMBED_BWD"], OP["PARAM_IN"], OP["TREE_SUM"], OP["ADAMW"]}
+    cands = [nd.index for nd in cheat.nodes if nd.op not in skip and nd.label is not None]
+    picks = synth.integers(5150, trials, len(cands))
+    rows, times = [], []
+    for q in range(trials):
+        cheat.params.copy_(ck[0])
+        cheat.m.copy_(ck[1])
+        cheat.v.copy_(ck[2])
+        cheat.step_no = 0
+        cheat.state_changed()
+        cheat.set_tokens(0)
+        node = cands[int(picks[q])]
+        nd = cheat.nodes[node]
+        numel = cheat.tensors[nd.outputs[0]].view.numel()
+        elem = int(synth.integers(5151 + q, 1, numel)[0])
+        cheat.inject_fault(node, 0, elem, 0)
+        cheat.run()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        tc = verde.Trainer(cheat, ck)
+        d, rnd = verde.phase2(th, tc)
+        v = verde.decide(th, tc, d, rnd, honest)
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+        rows.append(dict(node=nd.name, found=v.d == node, case=v.case, convicted=v.dishonest, rounds=v.rounds,
+                         chunk_rounds=v.chunk_rounds, recomputed=v.recomputed))
+    cheat._fault = None
+    out = {"trials": trials, "nodes": len(cheat.nodes),
+           "found": sum(r["found"] for r in rows), "case3": sum(r["case"] == 3 for r in rows),
+           "dishonest_convicted": sum(r["convicted"] == 1 for r in rows),
+           "rounds_max": max(r["rounds"] for r in rows), "chunk_rounds_max": max(r["chunk_rounds"] for r in rows),
+           "resolve_s_median": sorted(times)[len(times) // 2], "resolve_s_max": max(times),
+           "trials_detail": rows,
+           "config": "GPT-2 124M step (configs[2]) honest vs one-bit-faulted trainer, Phase 2 + Case-3 decision "
+                     "(configs[4]); fault node / element from synth.integers(5150 / 5151+q)"}
+    del honest, cheat, th
+    torch.cuda.empty_cache()
+    if with_oracle:
+        import oracle
+        a = synth.uniform(5152, 8 * 2 ** 20)          # 32 MiB
+        t0 = time.perf_counter()
+        oracle.commit_tensor(a)
+        dt = time.perf_counter() - t0
+        out["oracle_sha256_gbs"] = a.nbytes / dt / 1e9
+        out["oracle_note"] = "oracle R-TCOMMIT (SHA-256 leaves + RFC 6962 tree + header) of 32 MiB, 1 host core"
+    return out
+
+
 def mlp_extra(with_oracle=True, reps=200):
     """BASELINE config 1 (configs[0]): the 2-layer MLP DP step (fwd, bwd, R-TREE_S,
     AdamW, commit of all 104 outputs) -- launch-latency bound, so reported in us per
@@ -859,6 +930,9 @@ def main():
 
     if rank == 0 and world == 1 and not args.no_sweep:
         out["mlp_step"] = guarded("mlp_step", lambda: mlp_extra(with_oracle=not args.no_cpu_baseline))
+    if rank == 0 and world == 1 and not args.no_sweep and args.workload == "gpt2":
+        out["verde_dispute"] = guarded("verde_dispute",
+                                       lambda: verde_dispute_bench(with_oracle=not args.no_cpu_baseline))
     if rank == 0 and world == 1 and not args.no_sweep:
         out["cublas"] = {"note": "non-reproducible cuBLAS FP32 SGEMM (torch.mm/bmm, TF32 off) on the same shapes, "
                                  "as overhead context (the paper's RepOps-vs-torch::mm comparison, P:684-771); "
