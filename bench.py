@@ -893,6 +893,15 @@ def main():
         cm["alu_frac"] = cm["gbs"] / cm["alu_peak_gbs"]
         cm["note"] = ("SHA-256 is integer-ALU bound (949 ALU-pipe ops per 64 B block); gbs is the commit plans' "
                       "device time on the side stream, sharing the SMs with the step's FFMA2 GEMMs")
+        try:
+            import paper_2502_19405_b200 as R
+            cm["register_probe_gbs"] = R.verde_sha256_probe_gbs()
+            cm["register_probe_note"] = ("measured live: the leaf kernel's compression sequence on register-resident "
+                                         "blocks over the whole GPU (verde_sha256_probe) -- the practical ceiling "
+                                         "of the commitment kernels, no loads / byte shifts / tree")
+        except Exception as e:  # noqa: BLE001 -- diagnostic only
+            cm["register_probe_gbs"] = None
+            cm["register_probe_note"] = f"{type(e).__name__}: {e}"[:200]
         out["commit"] = cm
     out["clocks"] = clk
     out["step_stats"] = head.get("stats")

@@ -404,6 +404,13 @@ int verde_digest_from_subroots(const uint8_t *subroots, int64_t k, int dtype, in
 int verde_dirty_chunks(const int32_t *rows, int64_t n, int64_t row_bytes, int64_t nbytes, int all,
                        uint8_t *flags, void *stream);
 
+/* Diagnostic (measurement aid, not part of the method): the commitment's practical ALU
+ * ceiling.  ctas x 128 threads each run `iters` SHA-256 compressions (the leaf kernel's
+ * instruction sequence) on a register-resident block -- no memory traffic; 64 bytes per
+ * compression.  out: device uint32 [ctas * 128] (a fold of each thread's final state, so
+ * nothing is optimised away).  Time it with events on `stream`. */
+int verde_sha256_probe(int64_t ctas, int64_t iters, uint32_t *out, void *stream);
+
 /* Workspace (device bytes) needed to commit the given tensors in one call. */
 int64_t verde_commit_workspace_bytes(const verde_tensor_desc *descs /* host */, int n);
 /* Commit n tensors in one batched launch sequence; digests are written to

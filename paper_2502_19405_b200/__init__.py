@@ -795,6 +795,23 @@ def _desc(t, digest, mode=0, leaves_out=None, base_leaves=None, dirty=None) -> T
     return d
 
 
+def verde_sha256_probe_gbs(ctas_per_sm=9, iters=2000):
+    """Diagnostic: the SHA-256 compression rate with register-resident blocks (no memory
+    traffic) over the whole GPU -- the commitment kernels' practical ALU ceiling, GB/s."""
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    ctas = sms * int(ctas_per_sm)
+    out = torch.empty(ctas * 128, dtype=torch.int32, device="cuda")
+    run = lambda: check(lib().verde_sha256_probe(ctas, int(iters), out.data_ptr(), _stream(None)),  # noqa: E731
+                        "verde_sha256_probe")
+    run()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    run()
+    b.record()
+    b.synchronize()
+    return ctas * 128 * int(iters) * 64 / (a.elapsed_time(b) * 1e-3) / 1e9
+
+
 def verde_dirty_chunks(rows, row_bytes, nbytes, out, all_chunks=False, stream=None):
     """uint8 flags per 4096-byte chunk of a row-major tensor: 1 where one of `rows` (int32
     device tensor) meets the chunk (verde_tensor_desc.dirty of an incremental commit)."""

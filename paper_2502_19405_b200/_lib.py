@@ -107,6 +107,7 @@ SIGNATURES = {
     "repops_fill_uniform": (i32, [vp, i64, C.c_uint64, C.c_double, vp]),
     "verde_commit_workspace_bytes": (i64, [vp, i32]),
     "verde_dirty_chunks": (i32, [vp, i64, i64, i64, i32, vp, vp]),
+    "verde_sha256_probe": (i32, [i64, i64, vp, vp]),
     "verde_commit_tensors": (i32, [vp, i32, vp, i64, vp]),
     "verde_commit_tensor": (i32, [vp, i64, i32, i32, vp, vp, vp, i64, vp]),
     "verde_commit_plan_create": (i32, [vp, i32, vp, i64, vp]),

@@ -778,6 +778,12 @@ int repops_flip_bit(void *data, int64_t elem, int bit, void *stream) {
 }
 
 // ------------------------------------------------------------------ Verde
+int verde_sha256_probe(int64_t ctas, int64_t iters, uint32_t *out, void *stream) {
+    REQ(ctas >= 0 && ctas <= 65535 * 64 && iters >= 0, "sha256_probe: bad extent");
+    REQ(out || ctas == 0, "sha256_probe: null output");
+    return cuda_status(launch_sha_probe(ctas, iters, out, S(stream)), "sha256_probe");
+}
+
 int verde_dirty_chunks(const int32_t *rows, int64_t n, int64_t row_bytes, int64_t nbytes, int all, uint8_t *flags,
                        void *stream) {
     REQ(n >= 0 && row_bytes > 0 && nbytes >= 0, "dirty_chunks: negative extent");

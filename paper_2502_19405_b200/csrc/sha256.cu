@@ -760,3 +760,32 @@ cudaError_t launch_dirty_chunks(const int32_t *rows, int64_t n, int64_t row_byte
     dirty_chunks_kernel<<<(unsigned)((nchunks + 255) / 256), 256, smem, s>>>(rows, n, row_bytes, nchunks, all, flags);
     return cudaGetLastError();
 }
+
+// ------------------------------------------------------------------ diagnostic: compression ceiling
+// The commit kernels' practical ALU ceiling: every thread runs `iters` SHA-256 compressions
+// (the leaf kernel's compress_m<RO_SHA_MODE_DEFAULT>) on a register-resident message block,
+// each block's words perturbed by the previous state so nothing folds away -- no loads, no
+// byte shifting, no tree.  Bytes "hashed" = 64 per compression.
+namespace {
+__global__ void __launch_bounds__(128) sha_probe_kernel(int64_t iters, uint32_t *out) {
+    uint32_t st[8], w[16];
+    init_state(st);
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) w[i] = g * 0x9E3779B9u + (uint32_t)i;
+    for (int64_t it = 0; it < iters; ++it) {
+        compress_m<RO_SHA_MODE_DEFAULT>(st, w);
+        w[it & 15] ^= st[0];
+    }
+    uint32_t x = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x ^= st[i];
+    out[g] = x;
+}
+}  // namespace
+
+cudaError_t launch_sha_probe(int64_t ctas, int64_t iters, uint32_t *out, cudaStream_t s) {
+    if (ctas <= 0 || iters <= 0) return cudaSuccess;
+    sha_probe_kernel<<<(unsigned)ctas, 128, 0, s>>>(iters, out);
+    return cudaGetLastError();
+}

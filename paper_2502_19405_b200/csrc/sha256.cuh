@@ -27,3 +27,4 @@ cudaError_t chunk_leaves_launch(const uint8_t *data, int64_t nbytes, uint8_t *le
 extern std::atomic<int> g_leaf_ctas_per_sm;
 cudaError_t launch_dirty_chunks(const int32_t *rows, int64_t n, int64_t row_bytes, int64_t nbytes, int all,
                                 uint8_t *flags, cudaStream_t s);
+cudaError_t launch_sha_probe(int64_t ctas, int64_t iters, uint32_t *out, cudaStream_t s);
