@@ -1120,3 +1120,13 @@ def test_attention_probs_hd128_grouped_query(T, causal):
         ref = oracle.softmax(oracle.gemm(q, k, transB=True, epi=2, scale=scale), causal=causal)
         r0 = (j * qh + h) * T
         assert_bits(Ph[r0:r0 + T], ref, f"P oracle block {j} head {h}")
+
+
+def test_sha256_probe_deterministic():
+    """the commitment-ceiling diagnostic runs, is deterministic, and reports a rate"""
+    from paper_2502_19405_b200._lib import check, lib
+    out = [torch.zeros(4 * 128, dtype=torch.int32, device="cuda") for _ in range(2)]
+    for o in out:
+        check(lib().verde_sha256_probe(4, 10, o.data_ptr(), None), "probe")
+    assert torch.equal(out[0], out[1]) and int(out[0].abs().sum()) > 0
+    assert R.verde_sha256_probe_gbs(ctas_per_sm=1, iters=20) > 0
