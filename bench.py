@@ -336,6 +336,14 @@ class LlamaPrefillBench:
     d2h_bytes = 32
 
 
+def ffma2_probe():
+    try:
+        import paper_2502_19405_b200 as R
+        return R.repops_ffma2_probe_tflops()
+    except Exception:  # noqa: BLE001 -- diagnostic only
+        return None
+
+
 def verde_dispute_bench(trials=10, with_oracle=True):
     """BASELINE config 5, the dispute half: an honest and a dishonest trainer of the full
     GPT-2 124M step (the dishonest one flips bit 0 of one element of one operator output,
@@ -872,6 +880,10 @@ def main():
                                         achieved / fp32_peak_tflops(clk["sm_mhz"]) if clk["sm_mhz"] else -1),
                        "gemm_ms_per_step": gemm_ms_step, "gemm_launches_per_step": gemm_launches,
                        "traffic": profiled_gemm_traffic(),
+                       "register_probe_tflops": ffma2_probe(),
+                       "register_probe_note": "measured live: register-resident FFMA2 chains over the whole GPU "
+                                              "(repops_ffma2_probe) -- the practical FP32 ceiling under the "
+                                              "run's clock; peak stays the unit-count figure",
                        "achieved_union": head.get("gemm_union"),
                        "frac_union": (head["gemm_union"] / peak) if head.get("gemm_union") else None,
                        "union_note": "R-GEMM flops / length of the union of the GEMM launch intervals: the "
@@ -884,6 +896,8 @@ def main():
                        "traffic_note": "DRAM bytes (read + write) per R-GEMM launch, mean over one GPT-2 step's "
                                        "GEMM launches, from the committed ncu launch list "
                                        "profiles/r02_gpt2_step_launches.csv (cold-cache replay)"}
+    rp = out["roofline"].get("register_probe_tflops")
+    out["roofline"]["frac_register_probe"] = (achieved / rp) if rp else None
     if "commit" in head:
         cm = head["commit"]
         cm["hbm_frac"] = cm["gbs"] / hbm
@@ -896,6 +910,7 @@ def main():
         try:
             import paper_2502_19405_b200 as R
             cm["register_probe_gbs"] = R.verde_sha256_probe_gbs()
+            cm["frac_register_probe"] = cm["gbs"] / cm["register_probe_gbs"]
             cm["register_probe_note"] = ("measured live: the leaf kernel's compression sequence on register-resident "
                                          "blocks over the whole GPU (verde_sha256_probe) -- the practical ceiling "
                                          "of the commitment kernels, no loads / byte shifts / tree")

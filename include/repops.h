@@ -404,6 +404,12 @@ int verde_digest_from_subroots(const uint8_t *subroots, int64_t k, int dtype, in
 int verde_dirty_chunks(const int32_t *rows, int64_t n, int64_t row_bytes, int64_t nbytes, int all,
                        uint8_t *flags, void *stream);
 
+/* Diagnostic (measurement aid, not part of the method): the R-GEMM's practical FP32 ceiling.
+ * ctas x 128 threads each run `iters` rounds of 32 independent FFMA2 (64 FMA = 128 flops)
+ * on register-resident operands -- no loads, no shared memory.  out: device float
+ * [ctas * 128] (a fold of each thread's accumulators).  Time it with events on `stream`. */
+int repops_ffma2_probe(int64_t ctas, int64_t iters, float *out, void *stream);
+
 /* Diagnostic (measurement aid, not part of the method): the commitment's practical ALU
  * ceiling.  ctas x 128 threads each run `iters` SHA-256 compressions (the leaf kernel's
  * instruction sequence) on a register-resident block -- no memory traffic; 64 bytes per

@@ -795,6 +795,23 @@ def _desc(t, digest, mode=0, leaves_out=None, base_leaves=None, dirty=None) -> T
     return d
 
 
+def repops_ffma2_probe_tflops(ctas_per_sm=4, iters=20000):
+    """Diagnostic: FP32 FMA rate of register-resident FFMA2 chains over the whole GPU --
+    the R-GEMM's practical ceiling, TFLOP/s."""
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    ctas = sms * int(ctas_per_sm)
+    out = torch.empty(ctas * 128, dtype=torch.float32, device="cuda")
+    run = lambda: check(lib().repops_ffma2_probe(ctas, int(iters), out.data_ptr(), _stream(None)),  # noqa: E731
+                        "repops_ffma2_probe")
+    run()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    run()
+    b.record()
+    b.synchronize()
+    return ctas * 128 * int(iters) * 128 / (a.elapsed_time(b) * 1e-3) / 1e12
+
+
 def verde_sha256_probe_gbs(ctas_per_sm=9, iters=2000):
     """Diagnostic: the SHA-256 compression rate with register-resident blocks (no memory
     traffic) over the whole GPU -- the commitment kernels' practical ALU ceiling, GB/s."""

@@ -108,6 +108,7 @@ SIGNATURES = {
     "verde_commit_workspace_bytes": (i64, [vp, i32]),
     "verde_dirty_chunks": (i32, [vp, i64, i64, i64, i32, vp, vp]),
     "verde_sha256_probe": (i32, [i64, i64, vp, vp]),
+    "repops_ffma2_probe": (i32, [i64, i64, vp, vp]),
     "verde_commit_tensors": (i32, [vp, i32, vp, i64, vp]),
     "verde_commit_tensor": (i32, [vp, i64, i32, i32, vp, vp, vp, i64, vp]),
     "verde_commit_plan_create": (i32, [vp, i32, vp, i64, vp]),

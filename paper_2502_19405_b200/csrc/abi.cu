@@ -778,6 +778,12 @@ int repops_flip_bit(void *data, int64_t elem, int bit, void *stream) {
 }
 
 // ------------------------------------------------------------------ Verde
+int repops_ffma2_probe(int64_t ctas, int64_t iters, float *out, void *stream) {
+    REQ(ctas >= 0 && ctas <= 65535 * 64 && iters >= 0, "ffma2_probe: bad extent");
+    REQ(out || ctas == 0, "ffma2_probe: null output");
+    return cuda_status(launch_ffma2_probe(ctas, iters, out, S(stream)), "ffma2_probe");
+}
+
 int verde_sha256_probe(int64_t ctas, int64_t iters, uint32_t *out, void *stream) {
     REQ(ctas >= 0 && ctas <= 65535 * 64 && iters >= 0, "sha256_probe: bad extent");
     REQ(out || ctas == 0, "sha256_probe: null output");

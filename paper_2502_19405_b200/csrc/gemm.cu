@@ -557,3 +557,31 @@ cudaError_t gemm_launch(const GemmParams &p, cudaStream_t s, int force_cfg) {
         default: return cudaErrorInvalidValue;
     }
 }
+
+// ------------------------------------------------------------------ diagnostic: FFMA2 ceiling
+// The R-GEMM's practical FP32 ceiling: every thread runs `iters` rounds of 32 independent
+// FFMA2 chains (64 FMA per round) on register-resident operands -- the FMA pipe with no
+// loads, no shared memory, no barriers.  2 flops per FMA.
+namespace {
+__global__ void __launch_bounds__(128) ffma2_probe_kernel(int64_t iters, float *out) {
+    const float g = (float)(blockIdx.x * blockDim.x + threadIdx.x);
+    float2 acc[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) acc[i] = make_float2(g + i, g - i);
+    const float2 a = make_float2(1.0000001f, 0.9999999f), b = make_float2(1e-7f, -1e-7f);
+    for (int64_t it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[i] = __ffma2_rn(acc[i], a, b);
+    }
+    float x = 0.f;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) x = __fadd_rn(x, __fadd_rn(acc[i].x, acc[i].y));
+    out[blockIdx.x * blockDim.x + threadIdx.x] = x;
+}
+}  // namespace
+
+cudaError_t launch_ffma2_probe(int64_t ctas, int64_t iters, float *out, cudaStream_t s) {
+    if (ctas <= 0 || iters <= 0) return cudaSuccess;
+    ffma2_probe_kernel<<<(unsigned)ctas, 128, 0, s>>>(iters, out);
+    return cudaGetLastError();
+}

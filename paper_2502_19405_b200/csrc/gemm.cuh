@@ -47,3 +47,5 @@ cudaError_t gemm_tn_launch(const GemmParams &p, cudaStream_t s, int bk);
 int gemm_tn_choice(const GemmParams &p);
 // tuning hook: minimum dynamic shared memory per GEMM CTA (limits occupancy; bits-neutral)
 extern std::atomic<int> g_gemm_smem_floor;
+// diagnostic: register-resident FFMA2 rate (the R-GEMM's practical ceiling)
+cudaError_t launch_ffma2_probe(int64_t ctas, int64_t iters, float *out, cudaStream_t s);

@@ -1130,3 +1130,13 @@ def test_sha256_probe_deterministic():
         check(lib().verde_sha256_probe(4, 10, o.data_ptr(), None), "probe")
     assert torch.equal(out[0], out[1]) and int(out[0].abs().sum()) > 0
     assert R.verde_sha256_probe_gbs(ctas_per_sm=1, iters=20) > 0
+
+
+def test_ffma2_probe_deterministic():
+    """the R-GEMM ceiling diagnostic runs, is deterministic, and reports a rate"""
+    from paper_2502_19405_b200._lib import check, lib
+    out = [torch.zeros(4 * 128, device="cuda") for _ in range(2)]
+    for o in out:
+        check(lib().repops_ffma2_probe(4, 10, o.data_ptr(), None), "probe")
+    assert torch.equal(out[0].view(torch.int32), out[1].view(torch.int32))
+    assert R.repops_ffma2_probe_tflops(ctas_per_sm=1, iters=100) > 0
