@@ -750,6 +750,9 @@ def main():
     ap.add_argument("--workload", default="gpt2", choices=["gpt2", "gemm"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--multi-extras", action="store_true",
+                    help="at N > 1 also run the secondary workloads (config 3, the M-split sweep, the TP Llama "
+                         "prefill); off by default so a scaling run times only the headline step")
     ap.add_argument("--no-commit", action="store_true", help="diagnostic: skip the Verde commitments")
     ap.add_argument("--no-overlap", action="store_true", help="diagnostic: commits on the main stream")
     ap.add_argument("--combine", default="p2p", choices=["p2p", "sliced", "gather"],
@@ -778,7 +781,10 @@ def main():
     hbm = measured_hbm_gbs()
     out = {"metric": METRIC}
     results = {}
-    order = [args.workload] + ([] if args.no_sweep else
+    # the secondary workloads' NCCL paths have only run as gloo processes sharing one GPU: at
+    # N > 1 they are opt-in, so an untested collective cannot stall the scaling run's headline
+    extras = not args.no_sweep and (world == 1 or args.multi_extras)
+    order = [args.workload] + ([] if not extras else
                                [w for w in ("gpt2_ckpt", "gemm", "llama") if w != args.workload])
 
     def run_workload(wname):
