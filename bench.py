@@ -819,6 +819,7 @@ def main():
             res["commit"] = dict(gbs=c_bytes / (c_ms * 1e-3) / 1e9, ms_per_step=c_ms / steps,
                                  gb_per_step=c_bytes / steps / 1e9, plans_per_step=c_n // steps)
         if wname == "gpt2":
+            res["combine"], res["combine_fallback"] = wl.st.combine, wl.st.combine_fallback
             if wl.st.p2p is not None:
                 wl.st.p2p.check()   # raises if a peer-memory wait timed out
             res["root"] = wl.root.hex()
@@ -864,7 +865,9 @@ def main():
         "dtype": "f32", "data": "synthetic",
     })
     if args.workload == "gpt2":
-        out["config"] = gpt2_config(world, args.combine)
+        out["config"] = gpt2_config(world, head.get("combine", args.combine))
+        if head.get("combine_fallback"):
+            out["config"]["combine_fallback"] = head["combine_fallback"]
         out["gpt2_step_ms"] = head["ms"]
         out["loss"] = head["loss"]
         out["step_root"] = head["root"]

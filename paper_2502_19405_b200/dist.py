@@ -92,6 +92,10 @@ def p2p_slice(rank: int, world: int, n: int, align: int = 4) -> tuple[int, int]:
     return lo, min(lo + per, n)
 
 
+class P2PUnavailable(RuntimeError):
+    """Peer-memory setup failed on some rank (raised on every rank, after agreeing)."""
+
+
 class P2PTreeCombine:
     """R-TREE_S across G ranks as ONE fused kernel per rank over NVLink peer memory
     (the combine order is the paper's future work, fixed by
@@ -135,9 +139,18 @@ class P2PTreeCombine:
             t = repops_ipc_open(handles[r][k], n_, dt)
             self._opened.append(t)
             return t
-        self.peer_partial = [peer(r, 0, n, torch.float32) for r in range(world)]
-        self.peer_grad = [peer(r, 1, n, torch.float32) for r in range(world)]
-        peer_flags = [peer(r, 2, 2 * world, torch.int32) for r in range(world)]
+        err = None
+        try:
+            self.peer_partial = [peer(r, 0, n, torch.float32) for r in range(world)]
+            self.peer_grad = [peer(r, 1, n, torch.float32) for r in range(world)]
+            peer_flags = [peer(r, 2, 2 * world, torch.int32) for r in range(world)]
+        except Exception as e:  # noqa: BLE001 -- agreed on below, then raised on every rank
+            err = f"rank {rank}: {type(e).__name__}: {e}"[:300]
+        errs = [None] * world
+        dist.all_gather_object(errs, err, group=pg)   # every rank reaches this: same decision everywhere
+        bad = [e for e in errs if e]
+        if bad:
+            raise P2PUnavailable(bad[0])
         self.peer_ready = [f[:world] for f in peer_flags]
         self.peer_done = [f[world:] for f in peer_flags]
         self.epoch = 0

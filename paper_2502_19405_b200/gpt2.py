@@ -46,7 +46,7 @@ from . import (EPI_BIAS, EPI_SCALE, POST_GELU, POST_GELU_BACKWARD, CommitPlan, r
                repops_layernorm_backward_params, repops_softmax, repops_softmax_backward, repops_sum_cols_seq,
                repops_adamw, repops_adamw_segments, repops_tree_sum, verde_dirty_chunks)
 from ._lib import check, lib
-from .dist import P2PTreeCombine, all_gather_rows, dp_tree_combine, dp_tree_combine_sliced, gather_shard_digests, shard_block
+from .dist import P2PTreeCombine, P2PUnavailable, all_gather_rows, dp_tree_combine, dp_tree_combine_sliced, gather_shard_digests, shard_block
 
 # node operator codes (u16)
 OP = dict(PARAM_IN=1, TOKENS_IN=2, EMBED=3, LAYERNORM=4, LINEAR=5, ATTN_SCORES=6, SOFTMAX=7, ATTN_PV=8,
@@ -282,8 +282,15 @@ class GPT2Step:
                           dln1=E(M, d)))
         self.dx = [E(M, d) for _ in range(L + 1)]  # dx[l] = gradient w.r.t. x[l]
         self.glocal = torch.zeros(self.S_loc, self.P, device=dev)  # per-shard gradients (rows)
+        self.combine_fallback = None
         if self.combine == "p2p" and self.world > 1 and not self.structure_only:
-            self.p2p = P2PTreeCombine(self.P, self.rank, self.world, self.pg, sync=self.p2p_sync)
+            try:
+                self.p2p = P2PTreeCombine(self.P, self.rank, self.world, self.pg, sync=self.p2p_sync)
+            except P2PUnavailable as e:
+                # CUDA IPC peer mapping failed on some rank (all ranks agreed): the NCCL
+                # transport of the same R-TREE_S (data movement only, same bits)
+                self.p2p, self.combine, self.sliced_combine, self.combine_fallback = None, "sliced", True, str(e)
+        if self.p2p is not None:
             self.grad = self.p2p.grad   # IPC buffer every rank's combine kernel writes its slice into
         else:
             self.grad = E(self.P)

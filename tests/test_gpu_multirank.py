@@ -21,7 +21,8 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, tiny, q, combine="sliced", sync="host", bucketed=True, zero1=False, steps=1):
+def _worker(rank, world, port, tiny, q, combine="sliced", sync="host", bucketed=True, zero1=False, steps=1,
+            fail_rank=None):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -29,8 +30,16 @@ def _worker(rank, world, port, tiny, q, combine="sliced", sync="host", bucketed=
     try:
         torch.cuda.set_device(0)
         from paper_2502_19405_b200.gpt2 import GPT2Config, GPT2Step
+        if rank == fail_rank:   # a rank whose peer-memory mapping fails
+            import paper_2502_19405_b200 as R
+
+            def _fail(*a, **k):
+                raise RuntimeError("injected IPC open failure")
+            R.repops_ipc_open = _fail
         cfg = GPT2Config.tiny() if tiny else GPT2Config()
         st = GPT2Step(cfg, rank=rank, world=world, combine=combine, p2p_sync=sync, zero1=zero1)
+        if fail_rank is not None:
+            assert st.combine == "sliced" and st.p2p is None and f"rank {fail_rank}" in st.combine_fallback
         st.bucketed = bucketed
         for t in range(steps):   # several steps: the next step starts from the updated state
             st.set_tokens(t)
@@ -48,11 +57,12 @@ def _worker(rank, world, port, tiny, q, combine="sliced", sync="host", bucketed=
         dist.destroy_process_group()
 
 
-def _run(world, tiny, combine="sliced", sync="host", bucketed=True, zero1=False, steps=1):
+def _run(world, tiny, combine="sliced", sync="host", bucketed=True, zero1=False, steps=1, fail_rank=None):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, world, port, tiny, q, combine, sync, bucketed, zero1, steps))
+    ps = [ctx.Process(target=_worker, args=(r, world, port, tiny, q, combine, sync, bucketed, zero1, steps,
+                                            fail_rank))
           for r in range(world)]
     for p in ps:
         p.start()
@@ -236,3 +246,11 @@ def test_msplit_gemm_digest_identical_across_world_sizes(world, msplit_single):
                 assert full == full1, f"G={world} rank {rank}: gathered slabs differ from G=1"
                 C = np.frombuffer(full, np.float32).reshape(n, n)
                 assert bytes.fromhex(dig) == oracle.commit_tensor(C)
+
+
+def test_p2p_setup_failure_falls_back_on_every_rank(tiny_single):
+    """one rank cannot map a peer's CUDA IPC buffer: every rank learns it (the setup agrees
+    over the process group), falls back to the NCCL-style sliced transport of the same
+    R-TREE_S, and the step root is the single-process one"""
+    for rank, root, loss, pdig in _run(2, True, combine="p2p", fail_rank=1):
+        assert root == tiny_single[1], f"rank {rank}: step root differs after the fallback"
